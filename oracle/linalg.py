@@ -1,0 +1,168 @@
+"""Oracle primitives — TEST INFRASTRUCTURE ONLY.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl
+reference leg may import this package. The product path (the CUDA library and
+its Python binding) never imports it.
+
+Plain, slow, obviously-correct numpy/scipy versions of the block operations of
+PAPER.md §2 and §4, in float64 / complex128. Every function names the passage
+it follows (P:n = /root/reference/PAPER.md line n).
+
+Conventions: <x, y> = y^H x and <X, Y> = tr(Y^H X).
+"""
+from __future__ import annotations
+
+import numpy as np
+import scipy.linalg as sla
+
+EPS_BRK = 1e-14   # reading G12: LU pivot |u_kk| <= EPS_BRK * max|G| is a singular Gram
+EPS_DEFL = 1e-12  # reading G11: thin-QR diagonal <= EPS_DEFL * ||Z||_F is rank deficiency
+
+
+class Breakdown(Exception):
+    """Numerical breakdown: data, not an error."""
+
+    def __init__(self, kind: str, col: int = -1):
+        super().__init__(kind)
+        self.kind = kind
+        self.col = col
+
+
+class Counter:
+    """Vector-operation counter with Proposition 1's convention: an
+    inner product or a SAXPY of length n is one vector operation."""
+
+    def __init__(self):
+        self.vector_ops = 0
+        self.matvec_cols_A = 0
+        self.matvec_cols_AH = 0
+
+
+def H(X):
+    return X.conj().T
+
+
+def _sum_rows(prod: np.ndarray, order: str) -> np.ndarray:
+    """Sum an (n, ...) array of elementwise products over its rows in a stated order.
+    'seq'  : plain left-to-right accumulation over chunks of 64 rows,
+    'rev'  : the same chunks accumulated right-to-left.
+    Two orders exist only to measure the method's own rounding spread."""
+    n = prod.shape[0]
+    chunks = [prod[i:i + 64].sum(axis=0) for i in range(0, n, 64)] or [np.zeros(prod.shape[1:], prod.dtype)]
+    if order == "rev":
+        chunks = chunks[::-1]
+    acc = np.zeros_like(chunks[0])
+    for c in chunks:
+        acc = acc + c
+    return acc
+
+
+def gram(Y: np.ndarray, X: np.ndarray, ctr: Counter | None = None, order: str = "blas") -> np.ndarray:
+    """Block inner product Y^H X (sy x sx) — Alg. 3 Grams, e.g. (R̂^(k))^H R^(k)."""
+    if ctr is not None:
+        ctr.vector_ops += Y.shape[1] * X.shape[1]
+    if order == "blas":
+        return H(Y) @ X
+    return _sum_rows(Y.conj()[:, :, None] * X[:, None, :], order)
+
+
+def col_inner(X: np.ndarray, Y: np.ndarray, ctr: Counter | None = None, order: str = "blas") -> np.ndarray:
+    """Per-column <x_i, y_i> = y_i^H x_i (Alg. 1)."""
+    if ctr is not None:
+        ctr.vector_ops += X.shape[1]
+    if order == "blas":
+        return np.einsum("ij,ij->j", Y.conj(), X)
+    return _sum_rows(Y.conj() * X, order)
+
+
+def trace_inner(X: np.ndarray, Y: np.ndarray, ctr: Counter | None = None, order: str = "blas"):
+    """<X, Y> = tr(Y^H X) (Alg. 2)."""
+    if ctr is not None:
+        ctr.vector_ops += X.shape[1]
+    if order == "blas":
+        return np.vdot(Y.ravel(), X.ravel())
+    return _sum_rows(Y.conj() * X, order).sum()
+
+
+def sum_inner(y: np.ndarray, X: np.ndarray, ctr: Counter | None = None, order: str = "blas"):
+    """sum(y^H X), the sum of the entries of the row vector y^H X (Alg. 4)."""
+    if ctr is not None:
+        ctr.vector_ops += X.shape[1]
+    if order == "blas":
+        return (y.conj() @ X).sum()
+    return _sum_rows(y.conj()[:, None] * X, order).sum()
+
+
+def fro2(X: np.ndarray, order: str = "blas") -> float:
+    """||X||_F^2 (stopping criterion)."""
+    if order == "blas":
+        return float(np.vdot(X.ravel(), X.ravel()).real)
+    return float(_sum_rows((X.conj() * X).real, order).sum())
+
+
+def saxpy_count(ctr: Counter | None, n_ops: int):
+    if ctr is not None:
+        ctr.vector_ops += n_ops
+
+
+def small_solve(G: np.ndarray, M: np.ndarray) -> np.ndarray:
+    """G^{-1} M by LU with partial pivoting (SPEC small_solve S:106-114; reading G29).
+    Singular Gram -> Breakdown('gram') (reading G12)."""
+    G = np.atleast_2d(G)
+    if not np.all(np.isfinite(G)) or not np.all(np.isfinite(M)):
+        raise Breakdown("nonfinite")
+    lu, piv = sla.lu_factor(G, check_finite=False)
+    gmax = np.abs(G).max()
+    if gmax == 0 or np.abs(np.diag(lu)).min() <= EPS_BRK * gmax:
+        raise Breakdown("gram")
+    return sla.lu_solve((lu, piv), M, check_finite=False)
+
+
+def small_solve_h(G: np.ndarray, M: np.ndarray) -> np.ndarray:
+    """G^{-H} M (adjoint reuse of Prop. 1's proof)."""
+    return small_solve(H(G), M)
+
+
+def thin_qr(Z: np.ndarray, ctr: Counter | None = None, order: str = "blas"):
+    """Thin QR Z = Q C by modified Gram-Schmidt with one full re-orthogonalisation
+    pass (Eq. (3); cost remark "3ns^2 ... modified Gram-Schmidt" P:598-603;
+    SPEC thin_qr S:97-105). C is upper triangular with real non-negative diagonal.
+    A diagonal <= EPS_DEFL*||Z||_F raises Breakdown('rank') (reading G11)."""
+    n, s = Z.shape
+    Q = np.array(Z, dtype=np.result_type(Z.dtype, np.float64), copy=True)
+    C = np.zeros((s, s), dtype=Q.dtype)
+    zn = np.sqrt(fro2(Z))
+    for j in range(s):
+        for _pass in range(2):
+            for i in range(j):
+                if order == "blas":
+                    r = np.vdot(Q[:, i], Q[:, j])
+                else:
+                    r = _sum_rows(Q[:, i].conj() * Q[:, j], order)
+                Q[:, j] -= r * Q[:, i]
+                C[i, j] += r
+        d = np.sqrt(fro2(Q[:, j:j + 1], order))
+        if not np.isfinite(d) or d <= EPS_DEFL * zn or zn == 0:
+            raise Breakdown("rank", j)
+        C[j, j] = d
+        Q[:, j] /= d
+    if ctr is not None:
+        ctr.vector_ops += 3 * s * s  # "at least a cost of 3ns^2", counted as vector ops
+    return Q, C
+
+
+def unitary_qr_stack(M: np.ndarray):
+    """Full QR of a (2s x s) stack, M = Omega [R; 0], Omega unitary 2s x 2s, R upper
+    triangular with real non-negative diagonal (Householder via LAPACK; block QMR
+    quasi-minimisation, SURVEY App. A.3 reading G19)."""
+    k = M.shape[1]
+    Om, R = np.linalg.qr(M, mode="complete")
+    d = np.diag(R[:k, :k])
+    ph = np.ones(k, dtype=np.result_type(M.dtype, np.float64))
+    nz = np.abs(d) > 0
+    ph[nz] = d[nz] / np.abs(d[nz])
+    Om = Om.astype(ph.dtype, copy=True)
+    R = R.astype(ph.dtype, copy=True)
+    Om[:, :k] = Om[:, :k] * ph[None, :]
+    R[:k, :] = R[:k, :] * ph.conj()[:, None]
+    return Om, R[:k, :]

@@ -1,0 +1,211 @@
+"""Seeded synthetic inputs shared by the oracle, the tests and bench.py.
+
+This module holds NO arithmetic of the solvers (no products, inner products,
+coefficients or factorisations of the method). It only builds the operators A
+(CSR arrays) and right-hand sides B of SURVEY.md §8(d).1, which stand in for
+the paper's examples (§5.1), whose matrices are not
+available (Ex. 4 gauge field and Ex. 5 graphene matrix are missing).
+
+Conventions:
+  * grid unknown index i + m*j (+ m^2*k), x fastest; h = 1/(m+1);
+  * operator h^2 * (-Laplace u + c . grad u), central differences: diagonal 2d,
+    neighbour at +e_d gets -1 + c_d*h/2, at -e_d gets -1 - c_d*h/2;
+    off-grid neighbours dropped (homogeneous Dirichlet); CSR columns ascending;
+  * RHS: numpy default_rng(seed); real B = standard_normal((n, s));
+    complex B = (standard_normal((n,s)) + 1j*standard_normal((n,s)))/sqrt(2).
+"""
+from __future__ import annotations
+
+import hashlib
+from dataclasses import dataclass, field
+
+import numpy as np
+
+
+@dataclass
+class CSR:
+    """Plain CSR arrays (0-based, sorted unique columns per row)."""
+    n: int
+    row_ptr: np.ndarray  # int64, n+1
+    col_idx: np.ndarray  # int32, nnz
+    values: np.ndarray   # float64 or complex128, nnz
+    meta: dict = field(default_factory=dict)
+
+    @property
+    def nnz(self) -> int:
+        return int(self.row_ptr[-1])
+
+    @property
+    def dtype(self):
+        return self.values.dtype
+
+    def to_scipy(self):
+        import scipy.sparse as sp
+        return sp.csr_matrix((self.values, self.col_idx, self.row_ptr), shape=(self.n, self.n))
+
+
+def _stencil_csr(dims: tuple, diag: complex, coup: list, dtype) -> CSR:
+    """Assemble a structured-grid CSR matrix.
+
+    dims: grid extents (x fastest). coup: list of (axis, direction, value) for
+    the neighbour couplings. Columns come out ascending because neighbours are
+    visited in order of their linear offset."""
+    dims = tuple(int(d) for d in dims)
+    n = int(np.prod(dims))
+    strides = [1]
+    for d in dims[:-1]:
+        strides.append(strides[-1] * d)
+    # entries: (offset, value, axis, direction); diagonal offset 0
+    ents = [(0, diag, None, 0)]
+    for axis, direction, val in coup:
+        ents.append((direction * strides[axis], val, axis, direction))
+    ents.sort(key=lambda e: e[0])
+    idx = np.arange(n, dtype=np.int64)
+    coords = []
+    rem = idx
+    for d in dims:
+        coords.append((rem % d).astype(np.int32))
+        rem = rem // d
+    k = len(ents)
+    valid = np.empty((n, k), dtype=bool)
+    cols = np.empty((n, k), dtype=np.int32)
+    vals = np.empty((n, k), dtype=dtype)
+    for j, (off, val, axis, direction) in enumerate(ents):
+        if axis is None:
+            valid[:, j] = True
+        elif direction > 0:
+            valid[:, j] = coords[axis] < dims[axis] - 1
+        else:
+            valid[:, j] = coords[axis] > 0
+        cols[:, j] = (idx + off).astype(np.int32)
+        vals[:, j] = val
+    counts = valid.sum(axis=1)
+    row_ptr = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(counts, out=row_ptr[1:])
+    m = valid.ravel()
+    col_idx = cols.ravel()[m]
+    values = vals.ravel()[m]
+    return CSR(n, row_ptr, np.ascontiguousarray(col_idx), np.ascontiguousarray(values))
+
+
+def conv_diff_2d(m: int, c=(20.0, 20.0), dtype=np.float64, shift=0.0) -> CSR:
+    """2D 5-point h^2-scaled -Laplace u + c.grad u (config 1; stands in for Ex. 1)."""
+    h = 1.0 / (m + 1)
+    coup = []
+    for axis in range(2):
+        coup.append((axis, +1, -1.0 + c[axis] * h / 2))
+        coup.append((axis, -1, -1.0 - c[axis] * h / 2))
+    A = _stencil_csr((m, m), 4.0 + shift, coup, dtype)
+    A.meta = dict(kind="conv_diff_2d", m=m, c=tuple(c), shift=shift)
+    return A
+
+
+def conv_diff_3d(m: int, c=(50.0, 30.0, 10.0), dtype=np.float64, shift=0.0) -> CSR:
+    """3D 7-point h^2-scaled -Laplace u + c.grad u (+ shift on the diagonal);
+    configs 2-3 (stand in for Ex. 2/3)."""
+    h = 1.0 / (m + 1)
+    coup = []
+    for axis in range(3):
+        coup.append((axis, +1, -1.0 + c[axis] * h / 2))
+        coup.append((axis, -1, -1.0 - c[axis] * h / 2))
+    A = _stencil_csr((m, m, m), 6.0 + shift, coup, dtype)
+    A.meta = dict(kind="conv_diff_3d", m=m, c=tuple(c), shift=shift)
+    return A
+
+
+def random_rhs(n: int, s: int, seed: int, complex_: bool = False) -> np.ndarray:
+    """Gaussian right-hand sides, row-major draw order."""
+    rng = np.random.default_rng(seed)
+    if not complex_:
+        return rng.standard_normal((n, s))
+    re = rng.standard_normal((n, s))
+    im = rng.standard_normal((n, s))
+    return (re + 1j * im) / np.sqrt(2.0)
+
+
+def random_sparse(n: int, nnz_per_row: int, seed: int, dtype=np.float64, dominance: float = 0.0) -> CSR:
+    """Small random nonsymmetric sparse test matrix (tests only): nnz_per_row
+    uniform random off-diagonal columns per row (duplicates merged) plus a
+    diagonal equal to `dominance` x off-diagonal absolute row sum (+1)."""
+    rng = np.random.default_rng(seed + 1000)
+    rows = np.repeat(np.arange(n), nnz_per_row)
+    cols = rng.integers(0, n, n * nnz_per_row)
+    v = rng.standard_normal(n * nnz_per_row)
+    if np.dtype(dtype).kind == "c":
+        v = v + 1j * rng.standard_normal(n * nnz_per_row)
+    import scipy.sparse as sp
+    M = sp.coo_matrix((v, (rows, cols)), shape=(n, n)).tocsr()
+    M.setdiag(0)
+    M.eliminate_zeros()
+    rs = np.asarray(abs(M).sum(axis=1)).ravel()
+    M = M + sp.diags(dominance * rs + 1.0)
+    M = M.tocsr()
+    M.sort_indices()
+    return CSR(n, M.indptr.astype(np.int64), M.indices.astype(np.int32),
+               M.data.astype(dtype), dict(kind="random_sparse", seed=seed))
+
+
+def power_law(n: int, seed: int, a: float = 1.19794, lmax: int = 512, lmin_scale: float = 4.0) -> CSR:
+    """Config 5 (reading G24): row lengths L_i (counting
+    the diagonal) = min(lmax, floor(4 U^(-1/a))), columns uniform over the other
+    rows, values N(0,1), duplicates summed, diagonal 1.1 x off-diagonal abs sum."""
+    rng = np.random.default_rng(seed + 1000)
+    U = 1.0 - rng.random(n)
+    L = np.minimum(lmax, np.floor(lmin_scale * U ** (-1.0 / a))).astype(np.int64)
+    noff = L - 1
+    tot = int(noff.sum())
+    c = rng.integers(0, n - 1, tot)
+    rows = np.repeat(np.arange(n, dtype=np.int64), noff)
+    c = c + (c >= rows)
+    v = rng.standard_normal(tot)
+    import scipy.sparse as sp
+    M = sp.coo_matrix((v, (rows, c)), shape=(n, n)).tocsr()  # duplicates summed
+    M.sum_duplicates()
+    rs = np.asarray(abs(M).sum(axis=1)).ravel()
+    M = (M + sp.diags(1.1 * rs)).tocsr()
+    M.sort_indices()
+    return CSR(n, M.indptr.astype(np.int64), M.indices.astype(np.int32), M.data.astype(np.float64),
+               dict(kind="power_law", seed=seed, a=a, lmax=lmax))
+
+
+def input_hash(A: CSR, B: np.ndarray) -> str:
+    h = hashlib.sha256()
+    for arr in (A.row_ptr, A.col_idx, A.values, B):
+        h.update(np.ascontiguousarray(arr).view(np.uint8).data)
+    return h.hexdigest()[:16]
+
+
+# ---------------------------------------------------------------------------
+# BASELINE.json configs (SURVEY §8 "Config geometry")
+# ---------------------------------------------------------------------------
+
+CONFIGS = {
+    1: dict(name="cfg1_conv_diff_2d_32", dims=2, m=32, c=(20.0, 20.0), dtype="f64", s=4, seed=0,
+            methods=("egl_bicg", "bl_bicgstab_rq")),
+    2: dict(name="cfg2_conv_diff_3d_128_c128", dims=3, m=128, c=(50.0, 30.0, 10.0), dtype="c128",
+            shift=-0.1j, s=8, seed=1, methods=("bl_bicg_rq", "bl_qmr", "bl_bicgstab_rq")),
+    3: dict(name="cfg3_conv_diff_3d_256", dims=3, m=256, c=(50.0, 30.0, 10.0), dtype="f64", s=16, seed=2,
+            methods=("egl_qmr", "gl_bicgstab")),
+    5: dict(name="cfg5_power_law_4M", n=1 << 22, dtype="f64", s=32, seed=4, methods=("egl_bicg",)),
+}
+
+
+def make_config(cfg: int, m: int | None = None, s: int | None = None, n: int | None = None):
+    """Build (A, B) for a BASELINE config; m / s / n override sizes for scaled-down tests."""
+    c = CONFIGS[cfg]
+    s = c["s"] if s is None else s
+    cplx = c["dtype"] == "c128"
+    dt = np.complex128 if cplx else np.float64
+    if cfg in (1, 2, 3):
+        mm = c["m"] if m is None else m
+        if c["dims"] == 2:
+            A = conv_diff_2d(mm, c["c"], dt, c.get("shift", 0.0))
+        else:
+            A = conv_diff_3d(mm, c["c"], dt, c.get("shift", 0.0))
+    elif cfg == 5:
+        nn = c["n"] if n is None else n
+        A = power_law(nn, c["seed"])
+    else:
+        raise ValueError(cfg)
+    B = random_rhs(A.n, s, c["seed"], cplx)
+    return A, B
