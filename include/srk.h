@@ -1,0 +1,192 @@
+/* srk.h — C-ABI of the B200-native hot path for simultaneous short-recurrence
+ * Krylov solvers, AX = B with s right-hand sides (Rashedi, Birk, Frommer,
+ * Ebadi, arXiv:1504.04395; PAPER.md = /root/reference/PAPER.md, cited P:line).
+ *
+ * Problem (Eq. (1)): A in C^{n x n} sparse, X, B in C^{n x s}.
+ *
+ * CONVENTIONS (all entry points)
+ *  - Block vectors (n x s; "block vector denoting a matrix of size n x s",
+ *    P:131-132) are ROW-MAJOR ("row-interleaved"): element (i, j) at i*s + j,
+ *    so one nonzero of A is applied to s contiguous values.
+ *    SRK_C128 values are interleaved (re, im) doubles. Base addresses must be
+ *    16-byte aligned (cudaMalloc / torch allocations are).
+ *  - s x s results are row-major; scalars are one value of the dtype.
+ *  - Inner products: <x, y> = y^H x and <X, Y> = tr(Y^H X).
+ *  - Pointers are DEVICE pointers unless a name ends in _host.
+ *  - Ownership: the caller owns every array it passes; srk_matrix_create copies
+ *    the CSR arrays (the caller may free them afterwards); the library owns the
+ *    workspace inside srk_ctx / srk_matrix / srk_solver.
+ *  - Errors: every function returns SRK_OK (0) or a negative code; the message
+ *    for the last error of the calling thread is srk_last_error(). Numerical
+ *    breakdown is NOT an error: it is reported in srk_report.outcome.
+ *  - Synchronisation: kernel-level calls (srk_spmm_block, srk_gram_block,
+ *    srk_block_update, srk_tsqr) are asynchronous on the context's stream;
+ *    srk_solve / srk_solver_* return after the device work they describe.
+ *  - Determinism: no floating-point atomics; for a fixed input and launch
+ *    configuration results are bitwise reproducible.
+ *  - There is no CPU fallback: without a CUDA device every compute call fails
+ *    with SRK_ECUDA.
+ */
+#ifndef SRK_H
+#define SRK_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum { SRK_F64 = 0, SRK_C128 = 1 } srk_dtype;
+
+/* The 13 simultaneous methods (§2, §4):
+ *  Li  = loop interchanged (Alg. 1), Gl = global (Alg. 2),
+ *  eGl = economic global (Alg. 4; eGl-QMR P:464-465),
+ *  Bl  = block (Alg. 3), rQ = QR of the block residual (Alg. 5,
+ *  P:565-583; Bl-BiCGStab-rQ P:625-631). */
+typedef enum {
+  SRK_LI_BICG = 0, SRK_GL_BICG = 1, SRK_EGL_BICG = 2, SRK_BL_BICG = 3, SRK_BL_BICG_RQ = 4,
+  SRK_LI_QMR = 5, SRK_GL_QMR = 6, SRK_EGL_QMR = 7, SRK_BL_QMR = 8,
+  SRK_LI_BICGSTAB = 9, SRK_GL_BICGSTAB = 10, SRK_BL_BICGSTAB = 11, SRK_BL_BICGSTAB_RQ = 12
+} srk_method;
+
+enum { SRK_OK = 0, SRK_EINVAL = -1, SRK_EDIM = -2, SRK_EUNSUPPORTED = -3, SRK_ECUDA = -4,
+       SRK_ENCCL = -5, SRK_ENOMEM = -6 };
+
+/* outcome of a solve ("div." = final true residual > 1) */
+typedef enum { SRK_CONVERGED = 0, SRK_MAXIT = 1, SRK_BREAKDOWN = 2, SRK_DIVERGED = 3 } srk_outcome;
+/* breakdown kinds: zero Lanczos denominator, singular s x s Gram
+ * (P:232-234), rank-deficient thin QR (reading G11), non-finite value */
+enum { SRK_BK_NONE = 0, SRK_BK_LANCZOS = 1, SRK_BK_GRAM = 2, SRK_BK_RANK = 3, SRK_BK_NONFINITE = 4,
+       SRK_BK_OMEGA = 5 };
+
+/* fused reductions */
+typedef enum {
+  SRK_GRAM_NONE = 0, SRK_GRAM_NORM2 = 1, SRK_GRAM_DIAG = 2, SRK_GRAM_TRACE = 3,
+  SRK_GRAM_SUMVEC = 4, SRK_GRAM_FULL = 5, SRK_GRAM_COLNORM2 = 6
+} srk_gram;
+typedef enum { SRK_COEF_SCALAR = 1, SRK_COEF_DIAG = 2, SRK_COEF_FULL = 3 } srk_coef;
+
+typedef struct srk_ctx srk_ctx;
+typedef struct srk_matrix srk_matrix;
+typedef struct srk_solver srk_solver;
+
+/* CSR operator (0-based, sorted unique column indices per row).
+ * row_ptr: n+1 int64 (values must fit int32: nnz < 2^31), col_idx: nnz int32,
+ * values: nnz of dtype. All DEVICE pointers. */
+typedef struct {
+  int64_t n;
+  int64_t nnz;
+  const int64_t* row_ptr;
+  const int32_t* col_idx;
+  const void* values;
+  int dtype; /* srk_dtype */
+} srk_csr;
+
+typedef struct {
+  int outcome;          /* srk_outcome */
+  int iterations;       /* completed iterations (a BiCGStab half-step counts as one) */
+  int half_step;        /* 1 if a BiCGStab variant stopped after its first half */
+  int breakdown_kind;   /* SRK_BK_* */
+  int breakdown_iter;   /* iteration (1-based) in which the breakdown occurred, else -1 */
+  int frozen_cols;      /* Li variants: number of columns frozen by breakdown (reading G13) */
+  int64_t matvec_cols_A;   /* columns multiplied by A (Prop. 1 counters) */
+  int64_t matvec_cols_AH;  /* columns multiplied by A^H */
+  double final_true_rel_residual;      /* ||B - A X||_F / ||R0||_F recomputed at exit */
+  double final_recursive_rel_residual; /* ||R||_F (or ||C||_F for rQ) / ||R0||_F */
+  double seconds;                      /* wall time of the iteration loop */
+  int64_t kernel_launches;             /* kernels launched by the loop */
+} srk_report;
+
+/* ------------------------------------------------------------------ context */
+/* Create a context on `device` using CUDA stream `cuda_stream` (NULL = default
+ * stream). Errors: SRK_ECUDA if no device. */
+int srk_create(srk_ctx** ctx, int device, void* cuda_stream);
+int srk_destroy(srk_ctx* ctx);
+const char* srk_last_error(void);
+int srk_version(void);
+
+/* --------------------------------------------------------- a0: the operator */
+/* Validate and copy a CSR operator to the device; if need_adjoint, also build
+ * A^H = conj(A)^T explicitly ("A^H P̂"). Errors: SRK_EINVAL for an
+ * invalid CSR (unsorted / out-of-range columns, bad row_ptr), SRK_ENOMEM. */
+int srk_matrix_create(srk_ctx* ctx, const srk_csr* A, int need_adjoint, srk_matrix** out);
+int srk_matrix_destroy(srk_matrix* A);
+/* copy A^H back (CSR arrays of size n+1 / nnz, device pointers) — for tests */
+int srk_matrix_adjoint(const srk_matrix* A, int64_t* row_ptr, int32_t* col_idx, void* values);
+
+/* ------------------------------------------------------ kernel-level calls */
+/* Q = op(A) P, op = A (adjoint = 0) or A^H (adjoint = 1, needs need_adjoint),
+ * P, Q: n x s row-major (a1/a2). If gram != SRK_GRAM_NONE the
+ * reduction of mode `gram` between X = Q and Y (n x s block; n-vector for SUMVEC)
+ * is fused into the epilogue and written to gram_out (device, dtype values):
+ *   NORM2: ||Q||_F^2 (1 double); COLNORM2: s doubles; DIAG: (y_c^H q_c)_c (s);
+ *   TRACE: tr(Y^H Q) (1); SUMVEC: sum(y^H Q) (1); FULL: Y^H Q (s x s).
+ * Errors: SRK_EDIM (s < 1 or s > 64), SRK_EUNSUPPORTED (FULL with s > 32 real /
+ * 16 complex, adjoint without A^H). */
+int srk_spmm_block(srk_ctx* ctx, const srk_matrix* A, int adjoint, const void* P, void* Q, int s,
+                   int gram, const void* Y, void* gram_out);
+
+/* out = reduction(X, Y) over n rows of two n x s blocks (mode as above; FULL gives
+ * Y^H X). a3. */
+int srk_gram_block(srk_ctx* ctx, const void* X, const void* Y, int64_t n, int s, int dtype, int gram,
+                   void* out);
+
+/* Yout = Yin + sign * X * coef (a5): coef is a scalar (Gl, Alg. 2), an s-vector
+ * applied per column (Li, Alg. 1: X diag(coef)) or an s x s matrix (Bl, Alg. 3,
+ * "BLAS3 GEMM" P:290-297); coef is a DEVICE pointer of dtype values. Yout may
+ * alias Yin. sign = +1 or -1. */
+int srk_block_update(srk_ctx* ctx, void* Yout, const void* Yin, const void* X, const void* coef, int coef_kind,
+                     int sign, int64_t n, int s, int dtype);
+
+/* Thin QR Z = Q C (a6; Eq. (3)) by CholQR2 on the device: C upper
+ * triangular with real positive diagonal (s x s, device). *rank_host = s on
+ * success; on rank deficiency (reading G11) returns SRK_OK with *rank_host < s
+ * and Q unspecified. Synchronous (reads the rank flag). */
+int srk_tsqr(srk_ctx* ctx, const void* Z, void* Q, void* C, int64_t n, int s, int dtype, int* rank_host);
+
+/* ------------------------------------------------------------------ solve */
+typedef struct {
+  double tol;          /* stop when ||R||_F (||C||_F for rQ) <= tol ||R0||_F */
+  int maxit;           /* iteration cap (reading G22: 2000) */
+  int poll_every;      /* host reads the device convergence flag every k iterations (default 8) */
+  int record_history;  /* keep ||R_k||_F/||R0||_F per iteration (srk_solver_history) */
+  int check_true_residual; /* confirm convergence with B - AX (reading G26; default 1) */
+} srk_opts;
+
+/* Full solve (a1-a7): B, X device n x s blocks; X holds X0 on entry and the
+ * iterate on exit. opts may be NULL (tol 1e-8, maxit 2000). */
+int srk_solve(srk_ctx* ctx, const srk_matrix* A, const void* B, void* X, int s, int method,
+              const srk_opts* opts, srk_report* rep);
+/* Same with HOST B and X (pinned or pageable): copies in, solves, copies out. */
+int srk_solve_host(srk_ctx* ctx, const srk_matrix* A, const void* B_host, void* X_host, int s, int method,
+                   const srk_opts* opts, srk_report* rep);
+
+/* Stepping interface (lock-step parity and benchmarking): create, start with
+ * (B, X0), run k iterations (stops early on convergence / breakdown), read the
+ * current X / residual block, finish with a report. */
+int srk_solver_create(srk_ctx* ctx, const srk_matrix* A, int s, int method, const srk_opts* opts,
+                      srk_solver** out);
+int srk_solver_destroy(srk_solver* sv);
+int srk_solver_start(srk_solver* sv, const void* B, const void* X0);
+/* run up to k more iterations; *state_host (optional) = 0 running, 1 converged,
+ * 2 breakdown, 3 maxit */
+int srk_solver_iterate(srk_solver* sv, int k, int* state_host);
+/* copy the current iterate X_k (n x s) to X_out (device) */
+int srk_solver_get_x(srk_solver* sv, void* X_out);
+/* copy the current residual block R_k (n x s) — or, for the rQ variants, C_k
+ * (s x s) — to out (device); *rows_host = n or s */
+int srk_solver_get_residual(srk_solver* sv, void* out, int64_t* rows_host);
+int srk_solver_report(srk_solver* sv, srk_report* rep);
+/* Per-launch CUDA-event timing of the solver's kernels (off by default). Tags:
+ * 0 SpMM with A, 1 SpMM with A^H, 2 block updates / Grams, 3 partial-sum
+ * finalisation, 4 s x s coefficient phases. profile_read synchronises, returns
+ * the summed milliseconds and launch counts per tag since the last read, and
+ * resets them. */
+int srk_solver_profile(srk_solver* sv, int enable);
+int srk_solver_profile_read(srk_solver* sv, double* ms_host, int64_t* count_host, int ntag);
+/* history (host array of length >= iterations): relative recursive residuals */
+int srk_solver_history(srk_solver* sv, double* hist_host, int cap);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SRK_H */

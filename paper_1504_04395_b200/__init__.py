@@ -1,0 +1,420 @@
+"""paper_1504_04395_b200 — B200-native simultaneous short-recurrence Krylov
+solvers for AX = B with s right-hand sides (arXiv:1504.04395).
+
+Thin Python binding over the C-ABI library libsrk.so (include/srk.h): argument
+marshalling only. Every step of the path runs in the library's CUDA kernels;
+PyTorch provides device memory and streams. There is no CPU fallback: if the
+library or a CUDA device is missing, every call raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIBPATH = os.path.join(_HERE, "libsrk.so")
+
+METHODS = ("li_bicg", "gl_bicg", "egl_bicg", "bl_bicg", "bl_bicg_rq",
+           "li_qmr", "gl_qmr", "egl_qmr", "bl_qmr",
+           "li_bicgstab", "gl_bicgstab", "bl_bicgstab", "bl_bicgstab_rq")
+METHOD_ID = {m: i for i, m in enumerate(METHODS)}
+NEEDS_ADJOINT = {m: ("bicgstab" not in m) for m in METHODS}
+GRAM = {"none": 0, "norm2": 1, "diag": 2, "trace": 3, "sumvec": 4, "full": 5, "colnorm2": 6}
+COEF = {"scalar": 1, "diag": 2, "full": 3}
+OUTCOME = {0: "converged", 1: "maxit", 2: "breakdown", 3: "diverged"}
+BREAKDOWN = {0: "", 1: "lanczos", 2: "gram", 3: "rank", 4: "nonfinite", 5: "omega"}
+SRK_F64, SRK_C128 = 0, 1
+
+EXPORTS = ("srk_create", "srk_destroy", "srk_last_error", "srk_version", "srk_matrix_create",
+           "srk_matrix_destroy", "srk_matrix_adjoint", "srk_spmm_block", "srk_gram_block",
+           "srk_block_update", "srk_tsqr", "srk_solve", "srk_solve_host", "srk_solver_create",
+           "srk_solver_destroy", "srk_solver_start", "srk_solver_iterate", "srk_solver_get_x",
+           "srk_solver_get_residual", "srk_solver_report", "srk_solver_history", "srk_solver_profile",
+           "srk_solver_profile_read")
+
+
+class SrkError(RuntimeError):
+    pass
+
+
+class _Csr(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int64), ("nnz", ctypes.c_int64), ("row_ptr", ctypes.c_void_p),
+                ("col_idx", ctypes.c_void_p), ("values", ctypes.c_void_p), ("dtype", ctypes.c_int)]
+
+
+class _Opts(ctypes.Structure):
+    _fields_ = [("tol", ctypes.c_double), ("maxit", ctypes.c_int), ("poll_every", ctypes.c_int),
+                ("record_history", ctypes.c_int), ("check_true_residual", ctypes.c_int)]
+
+
+class _Report(ctypes.Structure):
+    _fields_ = [("outcome", ctypes.c_int), ("iterations", ctypes.c_int), ("half_step", ctypes.c_int),
+                ("breakdown_kind", ctypes.c_int), ("breakdown_iter", ctypes.c_int), ("frozen_cols", ctypes.c_int),
+                ("matvec_cols_A", ctypes.c_int64), ("matvec_cols_AH", ctypes.c_int64),
+                ("final_true_rel_residual", ctypes.c_double), ("final_recursive_rel_residual", ctypes.c_double),
+                ("seconds", ctypes.c_double), ("kernel_launches", ctypes.c_int64)]
+
+
+_lib = None
+
+
+def load_library(path: str | None = None):
+    """Load libsrk.so (built in-tree by paper_1504_04395_b200.build). Raises if absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    p = path or _LIBPATH
+    if not os.path.exists(p):
+        raise SrkError(f"{p} not found: build it with `python -m paper_1504_04395_b200.build` "
+                       "(there is no CPU fallback)")
+    lib = ctypes.CDLL(p)
+    vp, i, i64, d = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_double
+    sig = {
+        "srk_create": ([ctypes.POINTER(vp), i, vp], i),
+        "srk_destroy": ([vp], i),
+        "srk_last_error": ([], ctypes.c_char_p),
+        "srk_version": ([], i),
+        "srk_matrix_create": ([vp, ctypes.POINTER(_Csr), i, ctypes.POINTER(vp)], i),
+        "srk_matrix_destroy": ([vp], i),
+        "srk_matrix_adjoint": ([vp, vp, vp, vp], i),
+        "srk_spmm_block": ([vp, vp, i, vp, vp, i, i, vp, vp], i),
+        "srk_gram_block": ([vp, vp, vp, i64, i, i, i, vp], i),
+        "srk_block_update": ([vp, vp, vp, vp, vp, i, i, i64, i, i], i),
+        "srk_tsqr": ([vp, vp, vp, vp, i64, i, i, ctypes.POINTER(i)], i),
+        "srk_solve": ([vp, vp, vp, vp, i, i, ctypes.POINTER(_Opts), ctypes.POINTER(_Report)], i),
+        "srk_solve_host": ([vp, vp, vp, vp, i, i, ctypes.POINTER(_Opts), ctypes.POINTER(_Report)], i),
+        "srk_solver_create": ([vp, vp, i, i, ctypes.POINTER(_Opts), ctypes.POINTER(vp)], i),
+        "srk_solver_destroy": ([vp], i),
+        "srk_solver_start": ([vp, vp, vp], i),
+        "srk_solver_iterate": ([vp, i, ctypes.POINTER(i)], i),
+        "srk_solver_get_x": ([vp, vp], i),
+        "srk_solver_get_residual": ([vp, vp, ctypes.POINTER(i64)], i),
+        "srk_solver_report": ([vp, ctypes.POINTER(_Report)], i),
+        "srk_solver_history": ([vp, ctypes.POINTER(d), i], i),
+        "srk_solver_profile": ([vp, i], i),
+        "srk_solver_profile_read": ([vp, ctypes.POINTER(d), ctypes.POINTER(i64), i], i),
+    }
+    for name, (args, res) in sig.items():
+        f = getattr(lib, name)
+        f.argtypes = args
+        f.restype = res
+    _lib = lib
+    return lib
+
+
+def _check(rc: int, what: str):
+    if rc != 0:
+        msg = _lib.srk_last_error().decode() if _lib else ""
+        raise SrkError(f"{what} failed ({rc}): {msg}")
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _dtype_code(t) -> int:
+    torch = _torch()
+    if t.dtype == torch.float64:
+        return SRK_F64
+    if t.dtype == torch.complex128:
+        return SRK_C128
+    raise SrkError(f"unsupported dtype {t.dtype}: float64 or complex128 required")
+
+
+def _dev(t, name):
+    if not t.is_cuda:
+        raise SrkError(f"{name} must be a CUDA tensor (no CPU fallback)")
+    if not t.is_contiguous():
+        raise SrkError(f"{name} must be contiguous (row-major n x s)")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+class Context:
+    """srk_ctx bound to the current CUDA device and torch's current stream."""
+
+    def __init__(self, device: int | None = None, stream=None):
+        torch = _torch()
+        lib = load_library()
+        if not torch.cuda.is_available():
+            raise SrkError("CUDA is not available: the srk path has no CPU fallback")
+        dev = torch.cuda.current_device() if device is None else device
+        st = stream if stream is not None else torch.cuda.current_stream(dev)
+        self.stream = st
+        self.device = dev
+        h = ctypes.c_void_p()
+        _check(lib.srk_create(ctypes.byref(h), dev, ctypes.c_void_p(st.cuda_stream)), "srk_create")
+        self.h = h
+
+    def close(self):
+        if self.h:
+            _lib.srk_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_default_ctx = None
+
+
+def default_context() -> Context:
+    global _default_ctx
+    if _default_ctx is None:
+        _default_ctx = Context()
+    return _default_ctx
+
+
+class Matrix:
+    """srk_matrix (a0): validated device CSR copy (+ explicit A^H when needed)."""
+
+    def __init__(self, row_ptr, col_idx, values, need_adjoint: bool = True, ctx: Context | None = None):
+        torch = _torch()
+        self.ctx = ctx or default_context()
+        dev = torch.device("cuda", self.ctx.device)
+        rp = torch.as_tensor(row_ptr).to(dev, torch.int64).contiguous()
+        ci = torch.as_tensor(col_idx).to(dev, torch.int32).contiguous()
+        va = torch.as_tensor(values).to(dev).contiguous()
+        if va.dtype not in (torch.float64, torch.complex128):
+            va = va.to(torch.float64)
+        self.n = rp.numel() - 1
+        self.nnz = ci.numel()
+        self.dtype = va.dtype
+        csr = _Csr(self.n, self.nnz, rp.data_ptr(), ci.data_ptr(), va.data_ptr(), _dtype_code(va))
+        h = ctypes.c_void_p()
+        _check(_lib.srk_matrix_create(self.ctx.h, ctypes.byref(csr), int(need_adjoint), ctypes.byref(h)),
+               "srk_matrix_create")
+        self.h = h
+        self.has_adjoint = need_adjoint
+
+    @classmethod
+    def from_csr(cls, A, need_adjoint=True, ctx=None):
+        """From a synth.CSR / scipy.sparse.csr_matrix / (row_ptr, col_idx, values) triple."""
+        if isinstance(A, tuple):
+            return cls(*A, need_adjoint=need_adjoint, ctx=ctx)
+        if hasattr(A, "indptr"):
+            return cls(A.indptr, A.indices, A.data, need_adjoint=need_adjoint, ctx=ctx)
+        return cls(A.row_ptr, A.col_idx, A.values, need_adjoint=need_adjoint, ctx=ctx)
+
+    def adjoint_csr(self):
+        torch = _torch()
+        dev = torch.device("cuda", self.ctx.device)
+        rp = torch.empty(self.n + 1, dtype=torch.int64, device=dev)
+        ci = torch.empty(self.nnz, dtype=torch.int32, device=dev)
+        va = torch.empty(self.nnz, dtype=self.dtype, device=dev)
+        _check(_lib.srk_matrix_adjoint(self.h, ctypes.c_void_p(rp.data_ptr()), ctypes.c_void_p(ci.data_ptr()),
+                                       ctypes.c_void_p(va.data_ptr())), "srk_matrix_adjoint")
+        return rp, ci, va
+
+    def close(self):
+        if getattr(self, "h", None):
+            _lib.srk_matrix_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _gram_shape(mode: str, s: int, cplx: bool):
+    torch = _torch()
+    dt = torch.complex128 if cplx else torch.float64
+    if mode == "norm2":
+        return (1,), torch.float64
+    if mode == "colnorm2":
+        return (s,), torch.float64
+    if mode == "diag":
+        return (s,), dt
+    if mode in ("trace", "sumvec"):
+        return (1,), dt
+    if mode == "full":
+        return (s, s), dt
+    raise SrkError(mode)
+
+
+def spmm_block(A: Matrix, P, adjoint: bool = False, gram: str = "none", Y=None, Q=None):
+    """Q = op(A) P (+ fused reduction between Q and Y). Returns Q or (Q, gram)."""
+    torch = _torch()
+    n, s = P.shape if P.dim() == 2 else (P.shape[0], 1)
+    if Q is None:
+        Q = torch.empty_like(P)
+    out = None
+    if gram != "none":
+        shp, dt = _gram_shape(gram, s, P.is_complex())
+        out = torch.empty(shp, dtype=dt, device=P.device)
+    _check(_lib.srk_spmm_block(A.ctx.h, A.h, int(adjoint), _dev(P, "P"), _dev(Q, "Q"), s, GRAM[gram],
+                               _dev(Y, "Y") if Y is not None else None,
+                               ctypes.c_void_p(out.data_ptr()) if out is not None else None), "srk_spmm_block")
+    return Q if out is None else (Q, out)
+
+
+def gram_block(X, Y=None, mode: str = "full", ctx: Context | None = None):
+    """Reduction between blocks X and Y (FULL: Y^H X)."""
+    torch = _torch()
+    ctx = ctx or default_context()
+    n = X.shape[0]
+    s = X.shape[1] if X.dim() == 2 else 1
+    shp, dt = _gram_shape(mode, s, X.is_complex())
+    out = torch.empty(shp, dtype=dt, device=X.device)
+    _check(_lib.srk_gram_block(ctx.h, _dev(X, "X"), _dev(Y, "Y") if Y is not None else None, n, s,
+                               _dtype_code(X), GRAM[mode], ctypes.c_void_p(out.data_ptr())), "srk_gram_block")
+    return out
+
+
+def block_update(Yin, X, coef, kind: str = "full", sign: int = 1, Yout=None, ctx: Context | None = None):
+    """Yout = Yin + sign * X * coef (coef scalar / s-vector / s x s, device tensor)."""
+    torch = _torch()
+    ctx = ctx or default_context()
+    if Yout is None:
+        Yout = torch.empty_like(Yin)
+    coef = torch.as_tensor(coef, device=Yin.device, dtype=Yin.dtype).contiguous()
+    n, s = Yin.shape
+    _check(_lib.srk_block_update(ctx.h, _dev(Yout, "Yout"), _dev(Yin, "Yin"), _dev(X, "X"), _dev(coef, "coef"),
+                                 COEF[kind], int(sign), n, s, _dtype_code(Yin)), "srk_block_update")
+    return Yout
+
+
+def tsqr(Z, ctx: Context | None = None):
+    """Thin QR Z = Q C (CholQR2). Returns (Q, C, rank)."""
+    torch = _torch()
+    ctx = ctx or default_context()
+    n, s = Z.shape
+    Q = torch.empty_like(Z)
+    C = torch.empty((s, s), dtype=Z.dtype, device=Z.device)
+    rank = ctypes.c_int(0)
+    _check(_lib.srk_tsqr(ctx.h, _dev(Z, "Z"), _dev(Q, "Q"), ctypes.c_void_p(C.data_ptr()), n, s, _dtype_code(Z),
+                         ctypes.byref(rank)), "srk_tsqr")
+    return Q, C, rank.value
+
+
+@dataclass
+class Report:
+    outcome: str
+    iterations: int
+    half_step: bool
+    breakdown_kind: str
+    breakdown_iter: int
+    frozen_cols: int
+    matvec_cols_A: int
+    matvec_cols_AH: int
+    final_true_rel_residual: float
+    final_recursive_rel_residual: float
+    seconds: float
+    kernel_launches: int
+
+
+def _report(r: _Report) -> Report:
+    return Report(OUTCOME.get(r.outcome, str(r.outcome)), r.iterations, bool(r.half_step),
+                  BREAKDOWN.get(r.breakdown_kind, str(r.breakdown_kind)), r.breakdown_iter, r.frozen_cols,
+                  r.matvec_cols_A, r.matvec_cols_AH, r.final_true_rel_residual, r.final_recursive_rel_residual,
+                  r.seconds, r.kernel_launches)
+
+
+def _opts(tol, maxit, poll_every=8, check_true_residual=True):
+    return _Opts(float(tol), int(maxit), int(poll_every), 1, int(check_true_residual))
+
+
+class Solver:
+    """Stepping interface (srk_solver_*): lock-step parity and benchmarking."""
+
+    def __init__(self, A: Matrix, s: int, method: str, tol: float = 1e-8, maxit: int = 2000, poll_every: int = 8,
+                 check_true_residual: bool = True):
+        if method not in METHOD_ID:
+            raise SrkError(f"unknown method {method}")
+        self.A, self.s, self.method = A, s, method
+        o = _opts(tol, maxit, poll_every, check_true_residual)
+        h = ctypes.c_void_p()
+        _check(_lib.srk_solver_create(A.ctx.h, A.h, s, METHOD_ID[method], ctypes.byref(o), ctypes.byref(h)),
+               "srk_solver_create")
+        self.h = h
+
+    def start(self, B, X0=None):
+        self._B = B
+        _check(_lib.srk_solver_start(self.h, _dev(B, "B"), _dev(X0, "X0") if X0 is not None else None),
+               "srk_solver_start")
+
+    def iterate(self, k: int) -> int:
+        st = ctypes.c_int(0)
+        _check(_lib.srk_solver_iterate(self.h, int(k), ctypes.byref(st)), "srk_solver_iterate")
+        return st.value
+
+    def x(self):
+        X = _torch().empty_like(self._B)
+        _check(_lib.srk_solver_get_x(self.h, _dev(X, "X")), "srk_solver_get_x")
+        return X
+
+    def residual(self):
+        torch = _torch()
+        n = self._B.shape[0]
+        buf = torch.empty((max(n, self.s), self.s), dtype=self._B.dtype, device=self._B.device)
+        rows = ctypes.c_int64(0)
+        _check(_lib.srk_solver_get_residual(self.h, _dev(buf, "out"), ctypes.byref(rows)), "srk_solver_get_residual")
+        return buf[: rows.value].clone()
+
+    def report(self) -> Report:
+        r = _Report()
+        _check(_lib.srk_solver_report(self.h, ctypes.byref(r)), "srk_solver_report")
+        return _report(r)
+
+    def history(self, k: int) -> np.ndarray:
+        buf = (ctypes.c_double * max(k, 1))()
+        _check(_lib.srk_solver_history(self.h, buf, k), "srk_solver_history")
+        return np.array(buf[:k])
+
+    PROFILE_TAGS = ("spmm", "spmm_adj", "update", "finalize", "coef")
+
+    def profile(self, enable: bool = True):
+        _check(_lib.srk_solver_profile(self.h, int(enable)), "srk_solver_profile")
+
+    def profile_read(self) -> dict:
+        n = len(self.PROFILE_TAGS)
+        ms = (ctypes.c_double * n)()
+        cnt = (ctypes.c_int64 * n)()
+        _check(_lib.srk_solver_profile_read(self.h, ms, cnt, n), "srk_solver_profile_read")
+        return {t: (ms[i], cnt[i]) for i, t in enumerate(self.PROFILE_TAGS)}
+
+    def close(self):
+        if getattr(self, "h", None):
+            _lib.srk_solver_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def solve(A: Matrix, B, method: str = "egl_bicg", tol: float = 1e-8, maxit: int = 2000, X0=None,
+          poll_every: int = 8):
+    """X, report = solve(A, B, method, tol, maxit) — srk_solve on device tensors
+    (B: contiguous (n, s) float64/complex128 CUDA tensor)."""
+    torch = _torch()
+    n, s = B.shape
+    X = torch.zeros_like(B) if X0 is None else X0.clone()
+    o = _opts(tol, maxit, poll_every)
+    r = _Report()
+    _check(_lib.srk_solve(A.ctx.h, A.h, _dev(B, "B"), _dev(X, "X"), s, METHOD_ID[method], ctypes.byref(o),
+                          ctypes.byref(r)), "srk_solve")
+    return X, _report(r)
+
+
+def solve_host(A: Matrix, B: np.ndarray, method: str = "egl_bicg", tol: float = 1e-8, maxit: int = 2000,
+               X0: np.ndarray | None = None, poll_every: int = 8):
+    """srk_solve_host: B, X in host memory (numpy, C-contiguous (n, s))."""
+    B = np.ascontiguousarray(B)
+    X = np.zeros_like(B) if X0 is None else np.ascontiguousarray(X0).copy()
+    n, s = B.shape
+    o = _opts(tol, maxit, poll_every)
+    r = _Report()
+    _check(_lib.srk_solve_host(A.ctx.h, A.h, B.ctypes.data_as(ctypes.c_void_p), X.ctypes.data_as(ctypes.c_void_p),
+                               s, METHOD_ID[method], ctypes.byref(o), ctypes.byref(r)), "srk_solve_host")
+    return X, _report(r)

@@ -1,0 +1,435 @@
+// api.cu — the C-ABI of include/srk.h. Argument checking and marshalling only;
+// all arithmetic happens in the kernels of block_kernels.cu / coef.cu.
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "solver.h"
+
+using namespace srk;
+
+struct srk_ctx {
+  Ctx c;
+};
+struct srk_matrix {
+  Mat m;
+};
+struct srk_solver {
+  Solver* sv;
+};
+
+static thread_local std::string g_err;
+
+static int fail(int code, const char* msg) {
+  g_err = msg;
+  return code;
+}
+static int cuda_fail(cudaError_t e, const char* where) {
+  g_err = std::string(where) + ": " + cudaGetErrorString(e);
+  return SRK_ECUDA;
+}
+static int check_cuda(int e, const char* where) {
+  if (e == 0) return SRK_OK;
+  return cuda_fail((cudaError_t)e, where);
+}
+
+extern "C" {
+
+const char* srk_last_error(void) { return g_err.c_str(); }
+int srk_version(void) { return 1; }
+
+int srk_create(srk_ctx** out, int device, void* stream) {
+  if (!out) return fail(SRK_EINVAL, "srk_create: null out");
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev == 0) return cuda_fail(e == cudaSuccess ? cudaErrorNoDevice : e, "srk_create");
+  if (device < 0 || device >= ndev) return fail(SRK_EINVAL, "srk_create: bad device");
+  if ((e = cudaSetDevice(device)) != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+  auto* ctx = new srk_ctx();
+  ctx->c.dev = device;
+  ctx->c.st = (cudaStream_t)stream;
+  cudaDeviceGetAttribute(&ctx->c.nsm, cudaDevAttrMultiProcessorCount, device);
+  *out = ctx;
+  return SRK_OK;
+}
+
+int srk_destroy(srk_ctx* ctx) {
+  if (!ctx) return SRK_OK;
+  if (ctx->c.partials) cudaFree(ctx->c.partials);
+  delete ctx;
+  return SRK_OK;
+}
+
+__global__ static void rp64to32(const int64_t* a, int* b, long long n, int* bad) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i <= n; i += (long long)gridDim.x * blockDim.x) {
+    const int64_t v = a[i];
+    if (v < 0 || v > 2147483647LL) atomicOr(bad, 8);
+    b[i] = (int)v;
+  }
+}
+
+int srk_matrix_create(srk_ctx* ctx, const srk_csr* A, int need_adjoint, srk_matrix** out) {
+  if (!ctx || !A || !out) return fail(SRK_EINVAL, "srk_matrix_create: null argument");
+  if (A->n <= 0 || A->nnz < 0 || !A->row_ptr || (A->nnz > 0 && (!A->col_idx || !A->values)))
+    return fail(SRK_EINVAL, "srk_matrix_create: invalid CSR header");
+  if (A->dtype != SRK_F64 && A->dtype != SRK_C128) return fail(SRK_EINVAL, "srk_matrix_create: bad dtype");
+  if (A->nnz >= 2147483647LL) return fail(SRK_EUNSUPPORTED, "srk_matrix_create: nnz >= 2^31");
+  cudaStream_t st = ctx->c.st;
+  auto* M = new srk_matrix();
+  Mat& m = M->m;
+  m.ctx = &ctx->c;
+  m.n = A->n;
+  m.nnz = A->nnz;
+  m.cplx = A->dtype == SRK_C128;
+  const size_t esz = m.cplx ? 16 : 8;
+  int* dbad = nullptr;
+  cudaError_t e;
+  if ((e = cudaMalloc(&m.rp, sizeof(int) * (m.n + 1))) != cudaSuccess ||
+      (e = cudaMalloc(&m.ci, sizeof(int) * (m.nnz + 1))) != cudaSuccess ||
+      (e = cudaMalloc(&m.val, esz * (m.nnz + 1))) != cudaSuccess || (e = cudaMalloc(&dbad, sizeof(int))) != cudaSuccess) {
+    srk_matrix_destroy(M);
+    if (dbad) cudaFree(dbad);
+    return fail(SRK_ENOMEM, "srk_matrix_create: out of device memory");
+  }
+  cudaMemsetAsync(dbad, 0, sizeof(int), st);
+  const int grid = (int)std::max<long long>(1, std::min<long long>((m.n + 256) / 256, 148 * 8));
+  rp64to32<<<grid, 256, 0, st>>>(A->row_ptr, m.rp, m.n, dbad);
+  if (m.nnz > 0) {
+    cudaMemcpyAsync(m.ci, A->col_idx, sizeof(int) * m.nnz, cudaMemcpyDeviceToDevice, st);
+    cudaMemcpyAsync(m.val, A->values, esz * m.nnz, cudaMemcpyDeviceToDevice, st);
+  }
+  launch_csr_check(m.n, m.nnz, m.rp, m.ci, dbad, st);
+  int bad = 0;
+  cudaMemcpyAsync(&bad, dbad, sizeof(int), cudaMemcpyDeviceToHost, st);
+  if ((e = cudaStreamSynchronize(st)) != cudaSuccess) {
+    cudaFree(dbad);
+    srk_matrix_destroy(M);
+    return cuda_fail(e, "srk_matrix_create");
+  }
+  if (bad) {
+    cudaFree(dbad);
+    srk_matrix_destroy(M);
+    char msg[128];
+    snprintf(msg, sizeof msg, "srk_matrix_create: invalid CSR (code %d: 1 row_ptr, 2 column range, 4 unsorted, 8 int32)", bad);
+    return fail(SRK_EINVAL, msg);
+  }
+  if (need_adjoint) {
+    int* work = nullptr;
+    if ((e = cudaMalloc(&m.rpH, sizeof(int) * (m.n + 1))) != cudaSuccess ||
+        (e = cudaMalloc(&m.ciH, sizeof(int) * (m.nnz + 1))) != cudaSuccess ||
+        (e = cudaMalloc(&m.valH, esz * (m.nnz + 1))) != cudaSuccess || (e = cudaMalloc(&work, sizeof(int) * (m.n + 1))) != cudaSuccess) {
+      cudaFree(dbad);
+      srk_matrix_destroy(M);
+      return fail(SRK_ENOMEM, "srk_matrix_create: out of device memory (adjoint)");
+    }
+    launch_csr_transpose(m.cplx, m.n, m.nnz, m.rp, m.ci, m.val, m.rpH, m.ciH, m.valH, work, st);
+    if ((e = cudaStreamSynchronize(st)) != cudaSuccess) {
+      cudaFree(work);
+      cudaFree(dbad);
+      srk_matrix_destroy(M);
+      return cuda_fail(e, "srk_matrix_create: adjoint");
+    }
+    cudaFree(work);
+    m.has_adj = true;
+    m.nnzH = m.nnz;
+  }
+  cudaFree(dbad);
+  *out = M;
+  return SRK_OK;
+}
+
+int srk_matrix_destroy(srk_matrix* M) {
+  if (!M) return SRK_OK;
+  Mat& m = M->m;
+  if (m.rp) cudaFree(m.rp);
+  if (m.ci) cudaFree(m.ci);
+  if (m.val) cudaFree(m.val);
+  if (m.rpH) cudaFree(m.rpH);
+  if (m.ciH) cudaFree(m.ciH);
+  if (m.valH) cudaFree(m.valH);
+  delete M;
+  return SRK_OK;
+}
+
+__global__ static void rp32to64(const int* a, int64_t* b, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i <= n; i += (long long)gridDim.x * blockDim.x) b[i] = a[i];
+}
+
+int srk_matrix_adjoint(const srk_matrix* M, int64_t* row_ptr, int32_t* col_idx, void* values) {
+  if (!M || !M->m.has_adj) return fail(SRK_EINVAL, "srk_matrix_adjoint: no adjoint");
+  const Mat& m = M->m;
+  cudaStream_t st = m.ctx->st;
+  rp32to64<<<64, 256, 0, st>>>(m.rpH, row_ptr, m.n);
+  cudaMemcpyAsync(col_idx, m.ciH, sizeof(int) * m.nnz, cudaMemcpyDeviceToDevice, st);
+  cudaMemcpyAsync(values, m.valH, (m.cplx ? 16 : 8) * m.nnz, cudaMemcpyDeviceToDevice, st);
+  cudaError_t e = cudaStreamSynchronize(st);
+  return e == cudaSuccess ? SRK_OK : cuda_fail(e, "srk_matrix_adjoint");
+}
+
+static bool gram_ok(int g) { return g >= SRK_GRAM_NONE && g <= SRK_GRAM_COLNORM2; }
+
+int srk_spmm_block(srk_ctx* ctx, const srk_matrix* A, int adjoint, const void* P, void* Q, int s, int gram,
+                   const void* Y, void* gram_out) {
+  if (!ctx || !A || !P || !Q) return fail(SRK_EINVAL, "srk_spmm_block: null argument");
+  if (s < 1 || s > 64) return fail(SRK_EDIM, "srk_spmm_block: s must be in [1, 64]");
+  if (!gram_ok(gram)) return fail(SRK_EINVAL, "srk_spmm_block: bad gram mode");
+  if (adjoint && !A->m.has_adj) return fail(SRK_EUNSUPPORTED, "srk_spmm_block: matrix created without adjoint");
+  if (gram != SRK_GRAM_NONE && (!gram_out || (gram != SRK_GRAM_NORM2 && gram != SRK_GRAM_COLNORM2 && !Y)))
+    return fail(SRK_EINVAL, "srk_spmm_block: gram needs Y and gram_out");
+  if (gram == SRK_GRAM_FULL && !full_supported(A->m.cplx, cap_for(s)))
+    return fail(SRK_EUNSUPPORTED, "srk_spmm_block: fused FULL Gram needs s <= 32 (real) / 16 (complex)");
+  Eng e;
+  e.c = &ctx->c;
+  e.A = &A->m;
+  e.cplx = A->m.cplx;
+  e.n = A->m.n;
+  e.ws = reinterpret_cast<double*>(gram_out);
+  std::vector<RQ> reds;
+  if (gram != SRK_GRAM_NONE) reds.push_back(RQ{gram, 0, -1, Y, 0});
+  int r = e.spmm(adjoint != 0, P, Q, s, reds);
+  return check_cuda(r, "srk_spmm_block");
+}
+
+int srk_gram_block(srk_ctx* ctx, const void* X, const void* Y, int64_t n, int s, int dtype, int gram, void* out) {
+  if (!ctx || !X || !out) return fail(SRK_EINVAL, "srk_gram_block: null argument");
+  if (s < 1 || s > 64 || n < 1) return fail(SRK_EDIM, "srk_gram_block: bad n or s");
+  if (!gram_ok(gram) || gram == SRK_GRAM_NONE) return fail(SRK_EINVAL, "srk_gram_block: bad gram mode");
+  if (gram != SRK_GRAM_NORM2 && gram != SRK_GRAM_COLNORM2 && !Y) return fail(SRK_EINVAL, "srk_gram_block: Y needed");
+  const bool cplx = dtype == SRK_C128;
+  if (gram == SRK_GRAM_FULL && !full_supported(cplx, cap_for(s)))
+    return fail(SRK_EUNSUPPORTED, "srk_gram_block: FULL Gram needs s <= 32 (real) / 16 (complex)");
+  Eng e;
+  e.c = &ctx->c;
+  e.cplx = cplx;
+  e.n = n;
+  e.ws = reinterpret_cast<double*>(out);
+  int r;
+  if (gram == SRK_GRAM_SUMVEC) r = e.upd(s, {X}, {}, {RQ{gram, 0, -1, Y, 0}});
+  else if (gram == SRK_GRAM_NORM2 || gram == SRK_GRAM_COLNORM2) r = e.upd(s, {X}, {}, {RQ{gram, 0, -1, nullptr, 0}});
+  else r = e.upd(s, {X, Y}, {}, {RQ{gram, 0, 1, nullptr, 0}});
+  return check_cuda(r, "srk_gram_block");
+}
+
+int srk_block_update(srk_ctx* ctx, void* Yout, const void* Yin, const void* X, const void* coef, int kind, int sign,
+                     int64_t n, int s, int dtype) {
+  if (!ctx || !Yout || !Yin || !X || !coef) return fail(SRK_EINVAL, "srk_block_update: null argument");
+  if (s < 1 || s > 64 || n < 1) return fail(SRK_EDIM, "srk_block_update: bad n or s");
+  if (kind != SRK_COEF_SCALAR && kind != SRK_COEF_DIAG && kind != SRK_COEF_FULL)
+    return fail(SRK_EINVAL, "srk_block_update: bad coefficient kind");
+  if (sign != 1 && sign != -1) return fail(SRK_EINVAL, "srk_block_update: sign must be +1 or -1");
+  Eng e;
+  e.c = &ctx->c;
+  e.cplx = dtype == SRK_C128;
+  e.n = n;
+  e.ws = reinterpret_cast<double*>(const_cast<void*>(coef));
+  Coef cf{kind, 0, sign < 0 ? 1 : 0, 0, 0};
+  int r = e.upd(s, {Yin, X}, {OutSpec{Yout, {{0, C1()}, {1, cf}}}}, {});
+  return check_cuda(r, "srk_block_update");
+}
+
+namespace {
+struct TsqrSolver : Solver {
+  int alloc() override { return 0; }
+  int init() override { return 0; }
+  void seg(int) override {}
+};
+}  // namespace
+
+static void fill_opts(srk_opts* o, const srk_opts* in) {
+  o->tol = 1e-8;
+  o->maxit = 2000;
+  o->poll_every = 8;
+  o->record_history = 1;
+  o->check_true_residual = 1;
+  if (in) {
+    if (in->tol > 0) o->tol = in->tol;
+    if (in->maxit > 0) o->maxit = in->maxit;
+    if (in->poll_every > 0) o->poll_every = in->poll_every;
+    o->record_history = in->record_history;
+    o->check_true_residual = in->check_true_residual;
+  }
+}
+
+int srk_tsqr(srk_ctx* ctx, const void* Z, void* Q, void* C, int64_t n, int s, int dtype, int* rank_host) {
+  if (!ctx || !Z || !Q || !C) return fail(SRK_EINVAL, "srk_tsqr: null argument");
+  if (s < 1 || s > 64 || n < s) return fail(SRK_EDIM, "srk_tsqr: need 1 <= s <= 64 and n >= s");
+  const bool cplx = dtype == SRK_C128;
+  if (!full_supported(cplx, cap_for(s))) return fail(SRK_EUNSUPPORTED, "srk_tsqr: s <= 32 (real) / 16 (complex)");
+  TsqrSolver T;
+  T.c = &ctx->c;
+  T.s = s;
+  T.n = n;
+  T.cplx = cplx;
+  T.method = M_BL_BICG_RQ;
+  fill_opts(&T.o, nullptr);
+  T.o.maxit = 1;
+  int r = T.setup();
+  if (r) return fail(r, "srk_tsqr: setup");
+  cudaMemsetAsync(T.ctl, 0, CTL_SIZE * sizeof(int), ctx->c.st);
+  Eng& e = T.e;
+  e.upd(s, {Z}, {OutSpec{nullptr, {{0, C1()}}}}, {RQ{RED_FULL, O0, O0, nullptr, T.off[SL_GZ]}});
+  T.coef(10);
+  e.upd(s, {Z}, {OutSpec{Q, {{0, FU(T.off[SL_R1I])}}}}, {RQ{RED_FULL, O0, O0, nullptr, T.off[SL_GZ]}});
+  T.coef(11);
+  e.upd(s, {Q}, {OutSpec{Q, {{0, FU(T.off[SL_R2I])}}}}, {});
+  cudaMemcpyAsync(C, T.ws + T.off[SL_C], (size_t)s * s * (cplx ? 16 : 8), cudaMemcpyDeviceToDevice, ctx->c.st);
+  if (T.read_ctl()) return cuda_fail((cudaError_t)T.e.err, "srk_tsqr");
+  if (rank_host) *rank_host = (T.ctl_host[CTL_FLAG] == FLAG_BRK) ? s - 1 : s;
+  return SRK_OK;
+}
+
+// ------------------------------------------------------------------ solver
+int srk_solver_create(srk_ctx* ctx, const srk_matrix* A, int s, int method, const srk_opts* opts, srk_solver** out) {
+  if (!ctx || !A || !out) return fail(SRK_EINVAL, "srk_solver_create: null argument");
+  if (s < 1 || s > 64) return fail(SRK_EDIM, "srk_solver_create: s must be in [1, 64]");
+  if (method < 0 || method > SRK_BL_BICGSTAB_RQ) return fail(SRK_EINVAL, "srk_solver_create: unknown method");
+  if (opts && (opts->tol < 0 || opts->maxit < 0)) return fail(SRK_EINVAL, "srk_solver_create: tol/maxit");
+  const bool needs_adj = !(method == SRK_LI_BICGSTAB || method == SRK_GL_BICGSTAB || method == SRK_BL_BICGSTAB ||
+                           method == SRK_BL_BICGSTAB_RQ);
+  if (needs_adj && !A->m.has_adj) return fail(SRK_EUNSUPPORTED, "srk_solver_create: method needs A^H (need_adjoint=1)");
+  const bool block = method == SRK_BL_BICG || method == SRK_BL_BICG_RQ || method == SRK_BL_QMR ||
+                     method == SRK_BL_BICGSTAB || method == SRK_BL_BICGSTAB_RQ;
+  if (block && !full_supported(A->m.cplx, cap_for(s)))
+    return fail(SRK_EUNSUPPORTED, "srk_solver_create: block methods need s <= 32 (real) / 16 (complex)");
+  Solver* sv = make_solver(method);
+  if (!sv) return fail(SRK_EINVAL, "srk_solver_create: unknown method");
+  sv->c = &ctx->c;
+  sv->A = &A->m;
+  sv->s = s;
+  sv->method = method;
+  sv->cplx = A->m.cplx;
+  sv->n = A->m.n;
+  fill_opts(&sv->o, opts);
+  int r = sv->setup();
+  if (r) {
+    delete sv;
+    return fail(r, "srk_solver_create: out of device memory");
+  }
+  auto* h = new srk_solver();
+  h->sv = sv;
+  *out = h;
+  return SRK_OK;
+}
+
+int srk_solver_destroy(srk_solver* h) {
+  if (!h) return SRK_OK;
+  delete h->sv;
+  delete h;
+  return SRK_OK;
+}
+
+int srk_solver_start(srk_solver* h, const void* B, const void* X0) {
+  if (!h || !B) return fail(SRK_EINVAL, "srk_solver_start: null argument");
+  int r = h->sv->start(B, X0);
+  if (r) return check_cuda(h->sv->e.err ? h->sv->e.err : (int)cudaErrorUnknown, "srk_solver_start");
+  return SRK_OK;
+}
+
+int srk_solver_iterate(srk_solver* h, int k, int* state) {
+  if (!h) return fail(SRK_EINVAL, "srk_solver_iterate: null solver");
+  if (k < 0) return fail(SRK_EINVAL, "srk_solver_iterate: k < 0");
+  int r = h->sv->iterate(k);
+  if (r) return check_cuda(h->sv->e.err ? h->sv->e.err : (int)cudaErrorUnknown, "srk_solver_iterate");
+  if (state) *state = h->sv->state;
+  return SRK_OK;
+}
+
+int srk_solver_get_x(srk_solver* h, void* X) {
+  if (!h || !X) return fail(SRK_EINVAL, "srk_solver_get_x: null argument");
+  Solver* sv = h->sv;
+  cudaMemcpyAsync(X, sv->X, (size_t)sv->n * sv->s * sv->esz(), cudaMemcpyDeviceToDevice, sv->c->st);
+  cudaError_t e = cudaStreamSynchronize(sv->c->st);
+  return e == cudaSuccess ? SRK_OK : cuda_fail(e, "srk_solver_get_x");
+}
+
+int srk_solver_get_residual(srk_solver* h, void* out, int64_t* rows) {
+  if (!h || !out) return fail(SRK_EINVAL, "srk_solver_get_residual: null argument");
+  int r = h->sv->residual(out, rows);
+  return r ? fail(r, "srk_solver_get_residual") : SRK_OK;
+}
+
+int srk_solver_report(srk_solver* h, srk_report* rep) {
+  if (!h || !rep) return fail(SRK_EINVAL, "srk_solver_report: null argument");
+  Solver* sv = h->sv;
+  memset(rep, 0, sizeof(*rep));
+  if (sv->read_ctl()) return cuda_fail((cudaError_t)sv->e.err, "srk_solver_report");
+  const int it = sv->ctl_host[CTL_ITER];
+  rep->iterations = it;
+  rep->half_step = sv->half;
+  rep->breakdown_kind = sv->state == 2 ? sv->brk_kind : 0;
+  rep->breakdown_iter = sv->state == 2 ? sv->brk_iter : -1;
+  rep->frozen_cols = sv->ctl_host[CTL_NFROZEN];
+  rep->matvec_cols_A = (int64_t)it * sv->cols_A - (sv->half ? sv->s : 0);
+  rep->matvec_cols_AH = (int64_t)it * sv->cols_AH;
+  rep->final_true_rel_residual = sv->true_rel(sv->X);
+  double last = 0.0;
+  if (it > 0 && it <= sv->hist_cap) cudaMemcpy(&last, sv->hist + (it - 1), sizeof(double), cudaMemcpyDeviceToHost);
+  rep->final_recursive_rel_residual = last;
+  rep->seconds = sv->seconds;
+  rep->kernel_launches = sv->launches;
+  if (sv->state == 1) rep->outcome = SRK_CONVERGED;
+  else if (sv->state == 2) rep->outcome = SRK_BREAKDOWN;
+  else rep->outcome = rep->final_true_rel_residual > 1.0 ? SRK_DIVERGED : SRK_MAXIT;
+  return SRK_OK;
+}
+
+int srk_solver_profile(srk_solver* h, int enable) {
+  if (!h) return fail(SRK_EINVAL, "srk_solver_profile: null solver");
+  h->sv->prof.on = enable != 0;
+  h->sv->prof.used = 0;
+  return SRK_OK;
+}
+
+int srk_solver_profile_read(srk_solver* h, double* ms_host, int64_t* count_host, int ntag) {
+  if (!h || !ms_host || !count_host) return fail(SRK_EINVAL, "srk_solver_profile_read: null argument");
+  std::vector<long long> cnt(ntag);
+  h->sv->prof.read(ms_host, cnt.data(), ntag);
+  for (int i = 0; i < ntag; ++i) count_host[i] = cnt[i];
+  return SRK_OK;
+}
+
+int srk_solver_history(srk_solver* h, double* hist_host, int cap) {
+  if (!h || !hist_host) return fail(SRK_EINVAL, "srk_solver_history: null argument");
+  Solver* sv = h->sv;
+  const int n = std::min(cap, sv->hist_cap);
+  cudaError_t e = cudaMemcpy(hist_host, sv->hist, sizeof(double) * n, cudaMemcpyDeviceToHost);
+  return e == cudaSuccess ? SRK_OK : cuda_fail(e, "srk_solver_history");
+}
+
+int srk_solve(srk_ctx* ctx, const srk_matrix* A, const void* B, void* X, int s, int method, const srk_opts* opts,
+              srk_report* rep) {
+  if (!B || !X) return fail(SRK_EINVAL, "srk_solve: null B or X");
+  srk_solver* h = nullptr;
+  int r = srk_solver_create(ctx, A, s, method, opts, &h);
+  if (r) return r;
+  r = srk_solver_start(h, B, X);
+  if (!r) r = srk_solver_iterate(h, h->sv->o.maxit, nullptr);
+  if (!r) r = srk_solver_get_x(h, X);
+  if (!r && rep) r = srk_solver_report(h, rep);
+  srk_solver_destroy(h);
+  return r;
+}
+
+int srk_solve_host(srk_ctx* ctx, const srk_matrix* A, const void* B_host, void* X_host, int s, int method,
+                   const srk_opts* opts, srk_report* rep) {
+  if (!ctx || !A || !B_host || !X_host) return fail(SRK_EINVAL, "srk_solve_host: null argument");
+  const size_t bytes = (size_t)A->m.n * s * (A->m.cplx ? 16 : 8);
+  void *Bd = nullptr, *Xd = nullptr;
+  if (cudaMalloc(&Bd, bytes) != cudaSuccess || cudaMalloc(&Xd, bytes) != cudaSuccess) {
+    if (Bd) cudaFree(Bd);
+    return fail(SRK_ENOMEM, "srk_solve_host: out of device memory");
+  }
+  cudaMemcpyAsync(Bd, B_host, bytes, cudaMemcpyHostToDevice, ctx->c.st);
+  cudaMemcpyAsync(Xd, X_host, bytes, cudaMemcpyHostToDevice, ctx->c.st);
+  int r = srk_solve(ctx, A, Bd, Xd, s, method, opts, rep);
+  if (!r) {
+    cudaMemcpyAsync(X_host, Xd, bytes, cudaMemcpyDeviceToHost, ctx->c.st);
+    cudaError_t e = cudaStreamSynchronize(ctx->c.st);
+    if (e != cudaSuccess) r = cuda_fail(e, "srk_solve_host");
+  }
+  cudaFree(Bd);
+  cudaFree(Xd);
+  return r;
+}
+
+}  // extern "C"

@@ -1,0 +1,617 @@
+// coef.cu — single-CTA coefficient phases for the 13 methods.
+// Each phase follows oracle/solvers.py's order of operations and breakdown
+// rules line by line (readings G11, G12, G13, G26 in DESIGN.md).
+#include "coef.cuh"
+
+namespace srk {
+
+template <typename T>
+__device__ __forceinline__ T* W(const CoefArgs& a, int slot) {
+  return reinterpret_cast<T*>(a.ws + a.off[slot]);
+}
+__device__ __forceinline__ double* D(const CoefArgs& a, int slot) { return a.ws + a.off[slot]; }
+
+#define T0 if (threadIdx.x == 0)
+#define SYNC __syncthreads()
+
+__device__ void set_brk(const CoefArgs& a, int kind) {
+  if (a.ctl[CTL_FLAG] == FLAG_RUN) {
+    a.ctl[CTL_FLAG] = FLAG_BRK;
+    a.ctl[CTL_BKIND] = kind;
+    a.ctl[CTL_BITER] = a.ctl[CTL_ITER] + 1;
+  }
+}
+
+// Stopping rule: relative recursive residual of iteration ctl[ITER]+1.
+__device__ void conv_check(const CoefArgs& a, double r2) {
+  T0 {
+    const double r0 = *D(a, SL_R0N);
+    const double rel = r0 > 0 ? sqrt(r2) / r0 : 0.0;
+    const int it = a.ctl[CTL_ITER];
+    if (it < a.hist_cap) a.hist[it] = rel;
+    if (!isfinite(rel)) set_brk(a, BK_NONFINITE);
+    else if (rel <= a.tol) a.ctl[CTL_CONVPEND] = 1;
+  }
+  SYNC;
+}
+
+// scalar q = num / den with breakdown on a zero / non-finite operand
+template <typename T>
+__device__ bool sdiv(const CoefArgs& a, T num, T den, T* out, int kind) {
+  if (is_zero(den) || !fin(num) || !fin(den)) { set_brk(a, kind); return false; }
+  T q = cdiv(num, den);
+  if (!fin(q)) { set_brk(a, kind); return false; }
+  *out = q;
+  return true;
+}
+
+// Li per-column division with the freeze policy (reading G13)
+template <typename T>
+__device__ T ldiv(const CoefArgs& a, int c, T num, T den) {
+  int* fr = a.ctl + CTL_FROZEN;
+  if (fr[c]) return Ar<T>::zero();
+  if (is_zero(den)) { fr[c] = 1; return Ar<T>::zero(); }
+  T q = cdiv(num, den);
+  if (!fin(q)) { fr[c] = 1; return Ar<T>::zero(); }
+  return q;
+}
+
+__device__ void li_all_frozen(const CoefArgs& a) {
+  int n = 0;
+  for (int c = 0; c < a.s; ++c) n += a.ctl[CTL_FROZEN + c] ? 1 : 0;
+  a.ctl[CTL_NFROZEN] = n;
+  if (n == a.s) set_brk(a, BK_LANCZOS);
+}
+
+__device__ void common_init(const CoefArgs& a) {
+  T0 {
+    const double r0 = sqrt(*D(a, SL_R0N2));
+    *D(a, SL_R0N) = r0;
+    for (int c = 0; c < 64; ++c) a.ctl[CTL_FROZEN + c] = 0;
+    a.ctl[CTL_NFROZEN] = 0;
+    if (r0 == 0.0) a.ctl[CTL_FLAG] = FLAG_CONV;  // B - A X0 = 0: nothing to do
+  }
+  SYNC;
+}
+
+// ---------------------------------------------------------------- BiCG family
+// Gl-BiCG (Alg. 2) and eGl-BiCG (Alg. 4): scalar alpha, beta.
+template <typename T>
+__device__ void gl_bicg(const CoefArgs& a) {
+  T0 {
+    if (a.phase == 1) {  // alpha = rho / den
+      T al;
+      if (sdiv<T>(a, *W<T>(a, SL_RHO), *W<T>(a, SL_DEN), &al, BK_LANCZOS)) *W<T>(a, SL_ALPHA) = al;
+    } else if (a.phase == 2) {  // beta = rho_new / rho ; rho = rho_new
+      T be;
+      if (sdiv<T>(a, *W<T>(a, SL_RHON), *W<T>(a, SL_RHO), &be, BK_LANCZOS)) {
+        *W<T>(a, SL_BETA) = be;
+        *W<T>(a, SL_RHO) = *W<T>(a, SL_RHON);
+      }
+    }
+  }
+  SYNC;
+  if (a.phase == 2) conv_check(a, *D(a, SL_R2));
+}
+
+// Li-BiCG (Alg. 1): per-column alpha_i, beta_i
+template <typename T>
+__device__ void li_bicg(const CoefArgs& a) {
+  T0 {
+    T* rho = W<T>(a, SL_RHO);
+    if (a.phase == 1) {
+      for (int c = 0; c < a.s; ++c) W<T>(a, SL_ALPHA)[c] = ldiv<T>(a, c, rho[c], W<T>(a, SL_DEN)[c]);
+    } else if (a.phase == 2) {
+      for (int c = 0; c < a.s; ++c) {
+        W<T>(a, SL_BETA)[c] = ldiv<T>(a, c, W<T>(a, SL_RHON)[c], rho[c]);
+        rho[c] = W<T>(a, SL_RHON)[c];
+      }
+      li_all_frozen(a);
+    }
+  }
+  SYNC;
+  if (a.phase == 2) conv_check(a, *D(a, SL_R2));
+}
+
+// Bl-BiCG (Alg. 3) with the adjoint reuse of Prop. 1's proof
+template <typename T>
+__device__ void bl_bicg(const CoefArgs& a, T* sh) {
+  const int s = a.s;
+  if (a.phase == 1) {  // alpha = G^-1 M, alpha_hat = G^-H M^H
+    if (sm_solve<T>(W<T>(a, SL_ALPHA), W<T>(a, SL_G), W<T>(a, SL_M), s, s, 0, sh)) { T0 set_brk(a, BK_GRAM); SYNC; return; }
+    sm_copy<T>(W<T>(a, SL_TMP0), W<T>(a, SL_M), s, s, 1);
+    if (sm_solve<T>(W<T>(a, SL_AH), W<T>(a, SL_G), W<T>(a, SL_TMP0), s, s, 1, sh)) { T0 set_brk(a, BK_GRAM); SYNC; return; }
+  } else if (a.phase == 2) {  // beta = M^-1 M+, beta_hat = M^-H M+^H, M = M+
+    if (sm_solve<T>(W<T>(a, SL_BETA), W<T>(a, SL_M), W<T>(a, SL_MN), s, s, 0, sh)) { T0 set_brk(a, BK_GRAM); SYNC; return; }
+    sm_copy<T>(W<T>(a, SL_TMP0), W<T>(a, SL_MN), s, s, 1);
+    if (sm_solve<T>(W<T>(a, SL_BH), W<T>(a, SL_M), W<T>(a, SL_TMP0), s, s, 1, sh)) { T0 set_brk(a, BK_GRAM); SYNC; return; }
+    sm_copy<T>(W<T>(a, SL_M), W<T>(a, SL_MN), s, s, 0);
+    conv_check(a, *D(a, SL_R2));
+  }
+}
+
+// CholQR2 helper phases (reading G10): pass 1 R1 = chol(G) (rank test), pass 2 R2.
+template <typename T>
+__device__ bool cholqr_pass(const CoefArgs& a, int gslot, int rslot, int rislot, int rank_check) {
+  if (sm_chol<T>(W<T>(a, rslot), W<T>(a, gslot), a.s, rank_check)) { T0 set_brk(a, BK_RANK); SYNC; return false; }
+  sm_trinv<T>(W<T>(a, rislot), W<T>(a, rslot), a.s);
+  return true;
+}
+
+// Sig = R2 R1 ; Cslot = Sig * Cslot (optional)
+template <typename T>
+__device__ void cholqr_sigma(const CoefArgs& a, int r2, int r1, int sig, int cslot) {
+  const int s = a.s;
+  sm_gemm<T>(W<T>(a, sig), W<T>(a, r2), W<T>(a, r1), s, s, s, 0, 0, one<T>());
+  if (cslot >= 0) {
+    sm_gemm<T>(W<T>(a, SL_TMP0), W<T>(a, sig), W<T>(a, cslot), s, s, s, 0, 0, one<T>());
+    sm_copy<T>(W<T>(a, cslot), W<T>(a, SL_TMP0), s, s, 0);
+  }
+}
+
+// Bl-BiCG-rQ (Alg. 5, Eqs. (4)-(7))
+template <typename T>
+__device__ void bl_bicg_rq(const CoefArgs& a, T* sh) {
+  const int s = a.s;
+  if (a.phase == 0) {  // after the initial QRs: ||C0||
+    double c2 = sm_fro2<T>(W<T>(a, SL_C), s * s, reinterpret_cast<double*>(sh));
+    T0 *D(a, SL_C0N) = sqrt(c2);
+    SYNC;
+  } else if (a.phase == 1) {  // alpha = G1^-1 G2, alpha_hat = G1^-H G2^H, AC = alpha C
+    if (sm_solve<T>(W<T>(a, SL_ALPHA), W<T>(a, SL_G1), W<T>(a, SL_G2), s, s, 0, sh)) { T0 set_brk(a, BK_GRAM); SYNC; return; }
+    sm_copy<T>(W<T>(a, SL_TMP0), W<T>(a, SL_G2), s, s, 1);
+    if (sm_solve<T>(W<T>(a, SL_AH), W<T>(a, SL_G1), W<T>(a, SL_TMP0), s, s, 1, sh)) { T0 set_brk(a, BK_GRAM); SYNC; return; }
+    sm_gemm<T>(W<T>(a, SL_AC), W<T>(a, SL_ALPHA), W<T>(a, SL_C), s, s, s, 0, 0, one<T>());
+  } else if (a.phase == 2) {  // CholQR pass 1 of Z and Z_hat
+    if (!cholqr_pass<T>(a, SL_GZ, SL_R1, SL_R1I, 1)) return;
+    if (!cholqr_pass<T>(a, SL_GZH, SL_R1H, SL_R1HI, 1)) return;
+  } else if (a.phase == 3) {  // pass 2, Sig = R2 R1, C = Sig C
+    if (!cholqr_pass<T>(a, SL_GZ, SL_R2F, SL_R2I, 0)) return;
+    if (!cholqr_pass<T>(a, SL_GZH, SL_R2H, SL_R2HI, 0)) return;
+    cholqr_sigma<T>(a, SL_R2F, SL_R1, SL_SIG, SL_C);
+    cholqr_sigma<T>(a, SL_R2H, SL_R1H, SL_SIGH, SL_CH);
+  } else if (a.phase == 4) {  // beta = G2^-1 Sig_h^H G2+, beta_hat = G2^-H Sig^H G2+^H (Eqs. 6-7)
+    sm_gemm<T>(W<T>(a, SL_TMP1), W<T>(a, SL_SIGH), W<T>(a, SL_G2N), s, s, s, 1, 0, one<T>());
+    if (sm_solve<T>(W<T>(a, SL_BETA), W<T>(a, SL_G2), W<T>(a, SL_TMP1), s, s, 0, sh)) { T0 set_brk(a, BK_GRAM); SYNC; return; }
+    sm_gemm<T>(W<T>(a, SL_TMP1), W<T>(a, SL_SIG), W<T>(a, SL_G2N), s, s, s, 1, 1, one<T>());
+    if (sm_solve<T>(W<T>(a, SL_BH), W<T>(a, SL_G2), W<T>(a, SL_TMP1), s, s, 1, sh)) { T0 set_brk(a, BK_GRAM); SYNC; return; }
+    sm_copy<T>(W<T>(a, SL_G2), W<T>(a, SL_G2N), s, s, 0);
+    double c2 = sm_fro2<T>(W<T>(a, SL_C), s * s, reinterpret_cast<double*>(sh));
+    conv_check(a, c2);
+  }
+}
+
+// ------------------------------------------------------------ BiCGStab family
+__device__ void half_check(const CoefArgs& a, double s2, double ref) {
+  T0 {
+    const double r = sqrt(fmax(s2, 0.0));
+    const double r0 = *D(a, SL_R0N);
+    if (ref > 0 && r <= a.tol * ref) {
+      const int it = a.ctl[CTL_ITER];
+      if (it < a.hist_cap) a.hist[it] = r0 > 0 ? r / r0 : 0.0;
+      a.ctl[CTL_FLAG] = FLAG_HALF;
+    }
+  }
+  SYNC;
+}
+
+// Gl-BiCGStab [Jbilou05]
+template <typename T>
+__device__ void gl_bicgstab(const CoefArgs& a) {
+  if (a.phase == 1) {
+    T0 {
+      T al;
+      if (sdiv<T>(a, *W<T>(a, SL_RHO), *W<T>(a, SL_DEN), &al, BK_LANCZOS)) *W<T>(a, SL_ALPHA) = al;
+    }
+    SYNC;
+  } else if (a.phase == 2) {
+    half_check(a, *D(a, SL_S2), *D(a, SL_R0N));
+  } else if (a.phase == 3) {  // omega = tr(T^H S) / tr(T^H T); SL_ST holds tr(S^H T)
+    T0 {
+      T om;
+      const T num = Ar<T>::conj(*W<T>(a, SL_ST));
+      const T den = mkT(*D(a, SL_TT), 0.0, T());
+      if (sdiv<T>(a, num, den, &om, BK_OMEGA)) *W<T>(a, SL_OMEGA) = om;
+    }
+    SYNC;
+  } else if (a.phase == 4) {  // beta = (rho+ alpha)/(rho omega); BW = beta omega
+    T0 {
+      T be;
+      const T num = Ar<T>::mul(*W<T>(a, SL_RHON), *W<T>(a, SL_ALPHA));
+      const T den = Ar<T>::mul(*W<T>(a, SL_RHO), *W<T>(a, SL_OMEGA));
+      if (sdiv<T>(a, num, den, &be, BK_LANCZOS)) {
+        *W<T>(a, SL_BETA) = be;
+        *W<T>(a, SL_BW) = Ar<T>::mul(be, *W<T>(a, SL_OMEGA));
+        *W<T>(a, SL_RHO) = *W<T>(a, SL_RHON);
+      }
+    }
+    SYNC;
+    conv_check(a, *D(a, SL_R2));
+  }
+}
+
+// Li-BiCGStab: per column
+template <typename T>
+__device__ void li_bicgstab(const CoefArgs& a) {
+  const int s = a.s;
+  if (a.phase == 2) { half_check(a, *D(a, SL_S2), *D(a, SL_R0N)); return; }
+  T0 {
+    if (a.phase == 1) {
+      for (int c = 0; c < s; ++c) W<T>(a, SL_ALPHA)[c] = ldiv<T>(a, c, W<T>(a, SL_RHO)[c], W<T>(a, SL_DEN)[c]);
+    } else if (a.phase == 3) {  // omega_i = (t_i^H s_i) / (t_i^H t_i); SL_ST holds s_i^H t_i
+      for (int c = 0; c < s; ++c)
+        W<T>(a, SL_OMEGA)[c] = ldiv<T>(a, c, Ar<T>::conj(W<T>(a, SL_ST)[c]), mkT(D(a, SL_TT)[c], 0.0, T()));
+    } else if (a.phase == 4) {
+      for (int c = 0; c < s; ++c) {
+        const T num = Ar<T>::mul(W<T>(a, SL_RHON)[c], W<T>(a, SL_ALPHA)[c]);
+        const T den = Ar<T>::mul(W<T>(a, SL_RHO)[c], W<T>(a, SL_OMEGA)[c]);
+        const T be = ldiv<T>(a, c, num, den);
+        W<T>(a, SL_BETA)[c] = be;
+        W<T>(a, SL_BW)[c] = Ar<T>::mul(be, W<T>(a, SL_OMEGA)[c]);
+        W<T>(a, SL_RHO)[c] = W<T>(a, SL_RHON)[c];
+      }
+      li_all_frozen(a);
+    }
+  }
+  SYNC;
+  if (a.phase == 4) conv_check(a, *D(a, SL_R2));
+}
+
+// Bl-BiCGStab [ELg03] (reading G14)
+template <typename T>
+__device__ void bl_bicgstab(const CoefArgs& a, T* sh) {
+  const int s = a.s;
+  if (a.phase == 1) {  // alpha = G^-1 (Rt^H R)
+    if (sm_solve<T>(W<T>(a, SL_ALPHA), W<T>(a, SL_G), W<T>(a, SL_M), s, s, 0, sh)) { T0 set_brk(a, BK_GRAM); SYNC; }
+  } else if (a.phase == 2) {
+    half_check(a, *D(a, SL_S2), *D(a, SL_R0N));
+  } else if (a.phase == 3) {
+    T0 {
+      T om;
+      if (sdiv<T>(a, Ar<T>::conj(*W<T>(a, SL_ST)), mkT(*D(a, SL_TT), 0.0, T()), &om, BK_OMEGA)) *W<T>(a, SL_OMEGA) = om;
+    }
+    SYNC;
+  } else if (a.phase == 4) {  // beta = -G^-1 (Rt^H T); BW = omega beta
+    if (sm_solve<T>(W<T>(a, SL_TMP1), W<T>(a, SL_G), W<T>(a, SL_MN), s, s, 0, sh)) { T0 set_brk(a, BK_GRAM); SYNC; return; }
+    sm_scale<T>(W<T>(a, SL_BETA), W<T>(a, SL_TMP1), s * s, mkT(-1.0, 0.0, T()));
+    sm_scale<T>(W<T>(a, SL_BW), W<T>(a, SL_BETA), s * s, *W<T>(a, SL_OMEGA));
+    conv_check(a, *D(a, SL_R2));
+  }
+}
+
+// Bl-BiCGStab-rQ (reading G16)
+template <typename T>
+__device__ void bl_bicgstab_rq(const CoefArgs& a, T* sh) {
+  const int s = a.s;
+  double* dsh = reinterpret_cast<double*>(sh);
+  if (a.phase == 0) {
+    double c2 = sm_fro2<T>(W<T>(a, SL_C), s * s, dsh);
+    T0 *D(a, SL_C0N) = sqrt(c2);
+    SYNC;
+  } else if (a.phase == 1) {  // alpha = G^-1 GQ ; AC = alpha C
+    if (sm_solve<T>(W<T>(a, SL_ALPHA), W<T>(a, SL_G), W<T>(a, SL_GQ), s, s, 0, sh)) { T0 set_brk(a, BK_GRAM); SYNC; return; }
+    sm_gemm<T>(W<T>(a, SL_AC), W<T>(a, SL_ALPHA), W<T>(a, SL_C), s, s, s, 0, 0, one<T>());
+  } else if (a.phase == 2) {  // ||S||^2 = tr(C^H (Z^H Z) C)
+    sm_gemm<T>(W<T>(a, SL_TMP0), W<T>(a, SL_ZZ), W<T>(a, SL_C), s, s, s, 0, 0, one<T>());
+    sm_gemm<T>(W<T>(a, SL_TMP1), W<T>(a, SL_C), W<T>(a, SL_TMP0), s, s, s, 1, 0, one<T>());
+    T0 {
+      double tr = 0.0;
+      for (int i = 0; i < s; ++i) tr += re(W<T>(a, SL_TMP1)[i * s + i]);
+      dsh[0] = tr;
+    }
+    SYNC;
+    half_check(a, dsh[0], *D(a, SL_C0N));
+  } else if (a.phase == 3) {  // M = C C^H ; omega = tr((Y^H Z) M) / tr((Y^H Y) M); WC = omega C
+    sm_gemm<T>(W<T>(a, SL_TMP0), W<T>(a, SL_C), W<T>(a, SL_C), s, s, s, 0, 1, one<T>());     // M
+    sm_copy<T>(W<T>(a, SL_TMP3), W<T>(a, SL_YZ), s, s, 1);                                    // Y^H Z = (Z^H Y)^H
+    sm_gemm<T>(W<T>(a, SL_TMP1), W<T>(a, SL_TMP3), W<T>(a, SL_TMP0), s, s, s, 0, 0, one<T>());
+    sm_gemm<T>(W<T>(a, SL_TMP2), W<T>(a, SL_YY), W<T>(a, SL_TMP0), s, s, s, 0, 0, one<T>());
+    T0 {
+      T num = Ar<T>::zero(), den = Ar<T>::zero();
+      for (int i = 0; i < s; ++i) {
+        num = Ar<T>::add(num, W<T>(a, SL_TMP1)[i * s + i]);
+        den = Ar<T>::add(den, W<T>(a, SL_TMP2)[i * s + i]);
+      }
+      T om;
+      if (sdiv<T>(a, num, den, &om, BK_OMEGA)) *W<T>(a, SL_OMEGA) = om;
+    }
+    SYNC;
+    if (a.ctl[CTL_FLAG] != FLAG_RUN) return;
+    sm_scale<T>(W<T>(a, SL_WC), W<T>(a, SL_C), s * s, *W<T>(a, SL_OMEGA));
+  } else if (a.phase == 4) {
+    cholqr_pass<T>(a, SL_GZ, SL_R1, SL_R1I, 1);
+  } else if (a.phase == 5) {
+    if (!cholqr_pass<T>(a, SL_GZ, SL_R2F, SL_R2I, 0)) return;
+    cholqr_sigma<T>(a, SL_R2F, SL_R1, SL_SIG, SL_C);
+  } else if (a.phase == 6) {  // beta = omega^-1 G^-1 GQ+ ; BW = omega beta ; GQ = GQ+
+    if (sm_solve<T>(W<T>(a, SL_TMP1), W<T>(a, SL_G), W<T>(a, SL_GQN), s, s, 0, sh)) { T0 set_brk(a, BK_GRAM); SYNC; return; }
+    const T om = *W<T>(a, SL_OMEGA);
+    for (int i = threadIdx.x; i < s * s; i += blockDim.x) {
+      const T b = cdiv(W<T>(a, SL_TMP1)[i], om);
+      W<T>(a, SL_BETA)[i] = b;
+      W<T>(a, SL_BW)[i] = Ar<T>::mul(om, b);
+    }
+    SYNC;
+    sm_copy<T>(W<T>(a, SL_GQ), W<T>(a, SL_GQN), s, s, 0);
+    double c2 = sm_fro2<T>(W<T>(a, SL_C), s * s, dsh);
+    conv_check(a, c2);
+  }
+}
+
+// ------------------------------------------------------------------ QMR family
+// Li / Gl / eGl-QMR (readings G17, G18). mode 0 = Li (per
+// column), 1 = Gl, 2 = eGl. rho, xi, gam, theta are real; eta complex.
+template <typename T>
+__device__ void qmr_scalar(const CoefArgs& a, int mode) {
+  const int s = a.s;
+  const int ncol = (mode == 0) ? s : 1;
+  T0 {
+    T* rho = W<T>(a, SL_QRHO);
+    T* xi = W<T>(a, SL_QXI);
+    if (a.phase == 0) {  // rho = ||Vt||, xi = ||Wt|| (eGl: sqrt(s) ||w||)
+      for (int c = 0; c < ncol; ++c) {
+        rho[c] = mkT(sqrt(D(a, SL_RHON2)[c]), 0.0, T());
+        const double x = sqrt(D(a, SL_XI2)[c]);
+        xi[c] = mkT(mode == 2 ? sqrt((double)s) * x : x, 0.0, T());
+        W<T>(a, SL_GAMP)[c] = one<T>();
+        W<T>(a, SL_ETA)[c] = mkT(-1.0, 0.0, T());
+        W<T>(a, SL_THETAP)[c] = Ar<T>::zero();
+      }
+    } else if (a.phase == 1) {  // 1/rho, 1/xi
+      for (int c = 0; c < ncol; ++c) {
+        if (mode == 0) {
+          W<T>(a, SL_INVRHO)[c] = ldiv<T>(a, c, one<T>(), rho[c]);
+          W<T>(a, SL_INVXI)[c] = ldiv<T>(a, c, one<T>(), xi[c]);
+        } else {
+          T q;
+          if (!sdiv<T>(a, one<T>(), rho[c], &q, BK_LANCZOS)) break;
+          W<T>(a, SL_INVRHO)[c] = q;
+          if (!sdiv<T>(a, one<T>(), xi[c], &q, BK_LANCZOS)) break;
+          W<T>(a, SL_INVXI)[c] = q;
+        }
+      }
+    } else if (a.phase == 2) {  // P = V - (xi delta/eps) P ; Q = W - conj(rho delta/eps) Q
+      for (int c = 0; c < ncol; ++c) {
+        if (a.k1) {
+          W<T>(a, SL_C1)[c] = Ar<T>::zero();
+          W<T>(a, SL_C2)[c] = Ar<T>::zero();
+          continue;
+        }
+        const T d = W<T>(a, SL_DELTA)[c], e = W<T>(a, SL_EPS)[c];
+        const T n1 = Ar<T>::mul(xi[c], d), n2 = Ar<T>::mul(rho[c], d);
+        if (mode == 0) {
+          W<T>(a, SL_C1)[c] = ldiv<T>(a, c, n1, e);
+          W<T>(a, SL_C2)[c] = Ar<T>::conj(ldiv<T>(a, c, n2, e));
+        } else {
+          T q1, q2;
+          if (!sdiv<T>(a, n1, e, &q1, BK_LANCZOS)) break;
+          if (!sdiv<T>(a, n2, e, &q2, BK_LANCZOS)) break;
+          W<T>(a, SL_C1)[c] = q1;
+          W<T>(a, SL_C2)[c] = Ar<T>::conj(q2);
+        }
+      }
+    } else if (a.phase == 3) {  // beta = eps / delta
+      for (int c = 0; c < ncol; ++c) {
+        if (mode == 0) {
+          W<T>(a, SL_BETA)[c] = ldiv<T>(a, c, W<T>(a, SL_EPS)[c], W<T>(a, SL_DELTA)[c]);
+        } else {
+          T q;
+          if (!sdiv<T>(a, W<T>(a, SL_EPS)[c], W<T>(a, SL_DELTA)[c], &q, BK_LANCZOS)) break;
+          W<T>(a, SL_BETA)[c] = q;
+        }
+      }
+    } else if (a.phase == 4) {  // theta, gamma, eta; f = (theta_prev gamma)^2
+      for (int c = 0; c < ncol; ++c) {
+        const double rn = sqrt(D(a, SL_RHON2)[c]);
+        const double xin = sqrt(D(a, SL_XI2)[c]);
+        const T be = W<T>(a, SL_BETA)[c];
+        const double gp = re(W<T>(a, SL_GAMP)[c]);
+        const double thp = re(W<T>(a, SL_THETAP)[c]);
+        double th = rn / (gp * cabs(be));
+        double ga = 1.0 / sqrt(1.0 + th * th);
+        // eta = -eta * rho * gam^2 / (beta * gam_prev^2)
+        T eta = W<T>(a, SL_ETA)[c];
+        T num = scal(eta, -re(rho[c]) * ga * ga);
+        T den = scal(be, gp * gp);
+        eta = cdiv(num, den);
+        if (mode == 0 && a.ctl[CTL_FROZEN + c]) { th = 0.0; ga = 1.0; eta = Ar<T>::zero(); }
+        if (mode != 0 && (ga == 0.0 || !fin(eta))) { set_brk(a, BK_LANCZOS); break; }
+        const double f = (thp * ga) * (thp * ga);
+        W<T>(a, SL_ETA)[c] = eta;
+        W<T>(a, SL_F)[c] = mkT(f, 0.0, T());
+        rho[c] = mkT(rn, 0.0, T());
+        xi[c] = mkT(mode == 2 ? sqrt((double)s) * xin : xin, 0.0, T());
+        W<T>(a, SL_GAMP)[c] = mkT(ga, 0.0, T());
+        W<T>(a, SL_THETAP)[c] = mkT(th, 0.0, T());
+      }
+    } else if (a.phase == 5) {
+      if (mode == 0) li_all_frozen(a);
+    }
+  }
+  SYNC;
+  if (a.phase == 5) conv_check(a, *D(a, SL_R2));
+}
+
+// Block QMR (reading G19)
+template <typename T>
+__device__ void bl_qmr(const CoefArgs& a, T* sh) {
+  const int s = a.s, s2 = 2 * s;
+  double* dsh = reinterpret_cast<double*>(sh);
+  (void)dsh;
+  if (a.phase == 0) {  // tau_t = rho ; Omega_prev = I (unused at k = 1)
+    sm_copy<T>(W<T>(a, SL_TAUT), W<T>(a, SL_RHOB), s, s, 0);
+  } else if (a.phase == 1) {  // c1 = eps^-1 xi^H delta ; c2 = eps^-H rho^H delta^H (k > 1)
+    if (a.k1) {
+      for (int i = threadIdx.x; i < s * s; i += blockDim.x) {
+        W<T>(a, SL_C1)[i] = Ar<T>::zero();
+        W<T>(a, SL_C2)[i] = Ar<T>::zero();
+      }
+      SYNC;
+      return;
+    }
+    sm_gemm<T>(W<T>(a, SL_TMP0), W<T>(a, SL_XIB), W<T>(a, SL_DELTA), s, s, s, 1, 0, one<T>());
+    if (sm_solve<T>(W<T>(a, SL_C1), W<T>(a, SL_EPS), W<T>(a, SL_TMP0), s, s, 0, sh)) { T0 set_brk(a, BK_GRAM); SYNC; return; }
+    sm_gemm<T>(W<T>(a, SL_TMP0), W<T>(a, SL_RHOB), W<T>(a, SL_DELTA), s, s, s, 1, 1, one<T>());
+    if (sm_solve<T>(W<T>(a, SL_C2), W<T>(a, SL_EPS), W<T>(a, SL_TMP0), s, s, 1, sh)) { T0 set_brk(a, BK_GRAM); SYNC; return; }
+  } else if (a.phase == 2) {  // beta = delta^-1 eps ; gamma_hat = delta^-H eps^H
+    if (sm_solve<T>(W<T>(a, SL_BETA), W<T>(a, SL_DELTA), W<T>(a, SL_EPS), s, s, 0, sh)) { T0 set_brk(a, BK_GRAM); SYNC; return; }
+    sm_copy<T>(W<T>(a, SL_TMP0), W<T>(a, SL_EPS), s, s, 1);
+    if (sm_solve<T>(W<T>(a, SL_GHAT), W<T>(a, SL_DELTA), W<T>(a, SL_TMP0), s, s, 1, sh)) { T0 set_brk(a, BK_GRAM); SYNC; return; }
+  } else if (a.phase == 3) {  // CholQR pass 1 of V~ and W~ (rank deficiency of V~ with V~ == 0 -> rho+ = 0, deferred)
+    T0 *D(a, SL_PEND) = 0.0;
+    SYNC;
+    if (sm_chol<T>(W<T>(a, SL_R1), W<T>(a, SL_GZ), s, 1)) {
+      double g2 = sm_fro2<T>(W<T>(a, SL_GZ), s * s, dsh);
+      if (g2 != 0.0) { T0 set_brk(a, BK_RANK); SYNC; return; }
+      T0 *D(a, SL_PEND) = 1.0;  // exactly zero block: rho+ = 0, breakdown deferred past the X update
+      SYNC;
+      for (int i = threadIdx.x; i < s * s; i += blockDim.x) { W<T>(a, SL_R1)[i] = Ar<T>::zero(); W<T>(a, SL_R1I)[i] = Ar<T>::zero(); }
+      SYNC;
+    } else {
+      sm_trinv<T>(W<T>(a, SL_R1I), W<T>(a, SL_R1), s);
+    }
+    if (sm_chol<T>(W<T>(a, SL_R1H), W<T>(a, SL_GZH), s, 1)) {
+      double g2 = sm_fro2<T>(W<T>(a, SL_GZH), s * s, dsh);
+      if (g2 != 0.0) { T0 set_brk(a, BK_RANK); SYNC; return; }
+      T0 *D(a, SL_PEND) = 1.0;
+      SYNC;
+      for (int i = threadIdx.x; i < s * s; i += blockDim.x) { W<T>(a, SL_R1H)[i] = Ar<T>::zero(); W<T>(a, SL_R1HI)[i] = Ar<T>::zero(); }
+      SYNC;
+    } else {
+      sm_trinv<T>(W<T>(a, SL_R1HI), W<T>(a, SL_R1H), s);
+    }
+  } else if (a.phase == 4) {  // pass 2 -> rho+ = R2 R1, xi+ ; quasi-minimisation update
+    const bool pend = *D(a, SL_PEND) != 0.0;
+    if (!pend) {
+      if (!cholqr_pass<T>(a, SL_GZ, SL_R2F, SL_R2I, 0)) return;
+      cholqr_sigma<T>(a, SL_R2F, SL_R1, SL_RHOBN, -1);
+      if (!cholqr_pass<T>(a, SL_GZH, SL_R2H, SL_R2HI, 0)) return;
+      cholqr_sigma<T>(a, SL_R2H, SL_R1H, SL_XIBN, -1);
+    } else {
+      for (int i = threadIdx.x; i < s * s; i += blockDim.x) {
+        W<T>(a, SL_RHOBN)[i] = Ar<T>::zero();
+        W<T>(a, SL_R2I)[i] = Ar<T>::zero();
+        W<T>(a, SL_R2HI)[i] = Ar<T>::zero();
+        W<T>(a, SL_XIBN)[i] = Ar<T>::zero();
+      }
+      SYNC;
+    }
+    // [top; c] = Omega_prev^H [0; beta]  (k = 1: top = 0, c = beta)
+    T* top = W<T>(a, SL_TOP);
+    T* stack = W<T>(a, SL_TMP1);  // 2s x s: [c; rho+]
+    if (a.k1) {
+      for (int i = threadIdx.x; i < s * s; i += blockDim.x) { top[i] = Ar<T>::zero(); stack[i] = W<T>(a, SL_BETA)[i]; }
+    } else {
+      const T* Om = W<T>(a, SL_OMP);
+      for (int idx = threadIdx.x; idx < s2 * s; idx += blockDim.x) {
+        const int i = idx / s, j = idx % s;
+        T acc = Ar<T>::zero();
+        for (int l = 0; l < s; ++l) acc = Ar<T>::cfma(Om[(s + l) * s2 + i], W<T>(a, SL_BETA)[l * s + j], acc);
+        if (i < s) top[i * s + j] = acc; else stack[(i - s) * s + j] = acc;
+      }
+    }
+    SYNC;
+    for (int i = threadIdx.x; i < s * s; i += blockDim.x) stack[s * s + i] = W<T>(a, SL_RHOBN)[i];
+    SYNC;
+    // [c; rho+] = Omega [Rii; 0]
+    sm_qr_stack<T>(W<T>(a, SL_OMP), W<T>(a, SL_RII), stack, s, W<T>(a, SL_TMP2));
+    // [tau; tau_t] = Omega^H [tau_t; 0]
+    {
+      const T* Om = W<T>(a, SL_OMP);
+      T* tnew = W<T>(a, SL_TMP3);
+      for (int idx = threadIdx.x; idx < s2 * s; idx += blockDim.x) {
+        const int i = idx / s, j = idx % s;
+        T acc = Ar<T>::zero();
+        for (int l = 0; l < s; ++l) acc = Ar<T>::cfma(Om[l * s2 + i], W<T>(a, SL_TAUT)[l * s + j], acc);
+        tnew[idx] = acc;
+      }
+      SYNC;
+      for (int i = threadIdx.x; i < s * s; i += blockDim.x) {
+        W<T>(a, SL_TAU)[i] = tnew[i];
+        W<T>(a, SL_TAUT)[i] = tnew[s * s + i];
+      }
+      SYNC;
+    }
+    // Rii^-1 (solve against I, as the oracle) and TR = top Rii^-1
+    for (int i = threadIdx.x; i < s * s; i += blockDim.x) W<T>(a, SL_TMP0)[i] = (i / s == i % s) ? one<T>() : Ar<T>::zero();
+    SYNC;
+    if (sm_solve<T>(W<T>(a, SL_RIII), W<T>(a, SL_RII), W<T>(a, SL_TMP0), s, s, 0, sh)) { T0 set_brk(a, BK_GRAM); SYNC; return; }
+    sm_gemm<T>(W<T>(a, SL_TR), top, W<T>(a, SL_RIII), s, s, s, 0, 0, one<T>());
+  } else if (a.phase == 5) {  // after X, R updates: rho, xi = rho+, xi+ ; convergence, deferred breakdown
+    sm_copy<T>(W<T>(a, SL_RHOB), W<T>(a, SL_RHOBN), s, s, 0);
+    sm_copy<T>(W<T>(a, SL_XIB), W<T>(a, SL_XIBN), s, s, 0);
+    conv_check(a, *D(a, SL_R2));
+    T0 {
+      if (*D(a, SL_PEND) != 0.0 && a.ctl[CTL_CONVPEND] == 0) set_brk(a, BK_RANK);
+    }
+    SYNC;
+  }
+}
+
+// ------------------------------------------------------------------ dispatch
+template <typename T>
+__global__ void __launch_bounds__(256) coef_kernel(CoefArgs a) {
+  if (a.ctl[CTL_FLAG] != FLAG_RUN) return;
+  extern __shared__ double smraw[];
+  T* sh = reinterpret_cast<T*>(smraw);
+  if (a.phase == 9) {  // common start: ||R0||
+    common_init(a);
+    return;
+  }
+  if (a.phase >= 10 && a.phase <= 13) {  // device thin QR (CholQR2) of an initial block
+    const bool hat = a.phase >= 12;
+    const int gz = hat ? SL_GZH : SL_GZ;
+    if ((a.phase & 1) == 0) {
+      cholqr_pass<T>(a, gz, hat ? SL_R1H : SL_R1, hat ? SL_R1HI : SL_R1I, 1);
+    } else {
+      if (!cholqr_pass<T>(a, gz, hat ? SL_R2H : SL_R2F, hat ? SL_R2HI : SL_R2I, 0)) return;
+      cholqr_sigma<T>(a, hat ? SL_R2H : SL_R2F, hat ? SL_R1H : SL_R1, hat ? SL_CH : SL_C, -1);
+    }
+    return;
+  }
+  switch (a.method) {
+    case M_GL_BICG:
+    case M_EGL_BICG: gl_bicg<T>(a); break;
+    case M_LI_BICG: li_bicg<T>(a); break;
+    case M_BL_BICG: bl_bicg<T>(a, sh); break;
+    case M_BL_BICG_RQ: bl_bicg_rq<T>(a, sh); break;
+    case M_GL_BICGSTAB: gl_bicgstab<T>(a); break;
+    case M_LI_BICGSTAB: li_bicgstab<T>(a); break;
+    case M_BL_BICGSTAB: bl_bicgstab<T>(a, sh); break;
+    case M_BL_BICGSTAB_RQ: bl_bicgstab_rq<T>(a, sh); break;
+    case M_LI_QMR: qmr_scalar<T>(a, 0); break;
+    case M_GL_QMR: qmr_scalar<T>(a, 1); break;
+    case M_EGL_QMR: qmr_scalar<T>(a, 2); break;
+    case M_BL_QMR: bl_qmr<T>(a, sh); break;
+    default: break;
+  }
+}
+
+// end of one iteration: count it and commit a pending convergence candidate
+__global__ void end_iter_kernel(int* ctl) {
+  if (ctl[CTL_FLAG] != FLAG_RUN) return;
+  ctl[CTL_ITER] += 1;
+  if (ctl[CTL_CONVPEND]) {
+    ctl[CTL_CONVPEND] = 0;
+    ctl[CTL_FLAG] = FLAG_CONV;
+  }
+}
+
+int launch_coef(bool cplx, const CoefArgs& a, size_t smem, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(coef_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(coef_kernel<double2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  if (cplx) coef_kernel<double2><<<1, 256, smem, st>>>(a);
+  else coef_kernel<double><<<1, 256, smem, st>>>(a);
+  return (int)cudaGetLastError();
+}
+
+int launch_end_iter(int* ctl, cudaStream_t st) {
+  end_iter_kernel<<<1, 1, 0, st>>>(ctl);
+  return (int)cudaGetLastError();
+}
+
+}  // namespace srk

@@ -1,0 +1,60 @@
+// coef.cuh — device-side s x s / scalar coefficient phases of every method
+// (SURVEY §8(a) a4), executed by one CTA between the block kernels. Each phase
+// mirrors the corresponding lines of oracle/solvers.py (same formulas, same
+// breakdown rules), but shares no code with it.
+#pragma once
+#include "small.cuh"
+
+namespace srk {
+
+// ---- control block (ints, device) ----
+enum Ctl : int {
+  CTL_FLAG = 0,      // 0 running, 1 converged candidate, 2 half-step candidate, 3 breakdown
+  CTL_ITER = 1,      // completed iterations
+  CTL_BKIND = 2,
+  CTL_BITER = 3,
+  CTL_CONVPEND = 4,  // set by the last coefficient phase, committed by end_iter
+  CTL_NFROZEN = 5,
+  CTL_FROZEN = 16,   // 64 per-column frozen flags (Li variants, reading G13)
+  CTL_SIZE = 96
+};
+enum Flag : int { FLAG_RUN = 0, FLAG_CONV = 1, FLAG_HALF = 2, FLAG_BRK = 3 };
+enum BK : int { BK_NONE = 0, BK_LANCZOS = 1, BK_GRAM = 2, BK_RANK = 3, BK_NONFINITE = 4, BK_OMEGA = 5 };
+
+// ---- coefficient workspace slots ----
+enum Slot : int {
+  SL_R0N2 = 0, SL_R0N, SL_TRUE, SL_C0N,
+  SL_RHO, SL_RHON, SL_DEN, SL_ALPHA, SL_BETA, SL_OMEGA, SL_BW, SL_R2, SL_S2, SL_ST, SL_TT,
+  SL_G, SL_M, SL_MN, SL_AH, SL_BH,
+  SL_C, SL_CH, SL_G1, SL_G2, SL_G2N, SL_GZ, SL_GZH, SL_R1, SL_R1I, SL_R1H, SL_R1HI,
+  SL_R2F, SL_R2I, SL_R2H, SL_R2HI, SL_SIG, SL_SIGH, SL_AC, SL_WC, SL_GQ, SL_GQN, SL_ZZ, SL_YZ, SL_YY,
+  // QMR
+  SL_QRHO, SL_QXI, SL_INVRHO, SL_INVXI, SL_DELTA, SL_EPS, SL_C1, SL_C2, SL_GAMP, SL_ETA, SL_THETAP, SL_F,
+  SL_RHON2, SL_XI2, SL_K1,
+  // Bl-QMR
+  SL_OMP, SL_TAUT, SL_TAU, SL_TOP, SL_RII, SL_RIII, SL_TR, SL_GHAT, SL_RHOB, SL_XIB, SL_RHOBN, SL_XIBN,
+  SL_PEND,
+  SL_TMP0, SL_TMP1, SL_TMP2, SL_TMP3, SL_TMP4,
+  NSLOT
+};
+
+enum MethodId : int {
+  M_LI_BICG = 0, M_GL_BICG, M_EGL_BICG, M_BL_BICG, M_BL_BICG_RQ,
+  M_LI_QMR, M_GL_QMR, M_EGL_QMR, M_BL_QMR,
+  M_LI_BICGSTAB, M_GL_BICGSTAB, M_BL_BICGSTAB, M_BL_BICGSTAB_RQ
+};
+
+struct CoefArgs {
+  int method;
+  int phase;
+  int s;
+  int k1;            // 1 on the first iteration (QMR)
+  double tol;
+  double* ws;
+  int* ctl;
+  double* hist;
+  int hist_cap;
+  int off[NSLOT];
+};
+
+}  // namespace srk

@@ -1,0 +1,331 @@
+// engine.cu — host helpers that marshal the generic block kernels, plus the
+// operator-preparation kernels (CSR validation and the
+// explicit A^H = conj(A)^T copy used by the BiCG/QMR families).
+#include <algorithm>
+#include <cstdio>
+
+#include "engine.h"
+
+namespace srk {
+
+int Ctx::ensure_partials(size_t n) {
+  if (n <= pcap) return 0;
+  if (partials) cudaFree(partials);
+  partials = nullptr;
+  pcap = 0;
+  cudaError_t e = cudaMalloc(&partials, n * sizeof(double));
+  if (e != cudaSuccess) return (int)e;
+  pcap = n;
+  return 0;
+}
+
+void Prof::begin(int t, cudaStream_t st) {
+  if (!on) return;
+  if (used * 2 + 2 > ev.size()) {
+    for (int i = 0; i < 2; ++i) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      ev.push_back(e);
+    }
+    tag.push_back(0);
+  }
+  tag[used] = t;
+  cudaEventRecord(ev[2 * used], st);
+}
+void Prof::end(cudaStream_t st) {
+  if (!on) return;
+  cudaEventRecord(ev[2 * used + 1], st);
+  used++;
+}
+int Prof::read(double* ms, long long* cnt, int ntag) {
+  for (int i = 0; i < ntag; ++i) { ms[i] = 0.0; cnt[i] = 0; }
+  for (size_t i = 0; i < used; ++i) {
+    cudaEventSynchronize(ev[2 * i + 1]);
+    float t = 0.f;
+    cudaEventElapsedTime(&t, ev[2 * i], ev[2 * i + 1]);
+    if (tag[i] < ntag) { ms[tag[i]] += t; cnt[tag[i]]++; }
+  }
+  used = 0;
+  return 0;
+}
+Prof::~Prof() {
+  for (auto e : ev) cudaEventDestroy(e);
+}
+
+int Eng::grid_for(int cap, bool full) const {
+  const long long rpc = rows_per_cta(cap, cplx);
+  long long need = (n + rpc - 1) / rpc;
+  // persistent-style grid: a multiple of the SM count (4 x 256-thread CTAs per SM,
+  // 2 when the s x s Gram accumulators are live)
+  const long long maxg = (long long)c->nsm * (full ? 2 : 4);
+  if (need < 1) need = 1;
+  return (int)std::min(need, maxg);
+}
+
+static void fill_red(Red& r, const RQ& q, int poff) {
+  r.mode = q.mode;
+  r.xsrc = q.x;
+  r.ysrc = q.y;
+  r.yext = q.yext;
+  r.poff = poff;
+}
+
+static int finish_reds(Eng& e, const std::vector<RQ>& reds, const std::vector<int>& poffs, int s, int grid,
+                       int pstride) {
+  if (reds.empty()) return 0;
+  FinArgs f{};
+  f.partials = e.c->partials;
+  f.nblk = grid;
+  f.pstride = pstride;
+  f.nseg = (int)reds.size();
+  for (size_t i = 0; i < reds.size(); ++i) {
+    f.seg[i].poff = poffs[i];
+    f.seg[i].len = red_len(reds[i].mode, s, e.cplx);
+    f.seg[i].woff = reds[i].woff;
+  }
+  f.ws = e.ws;
+  f.done = e.done;
+  e.nlaunch++;
+  if (e.prof) e.prof->begin(PT_FIN, e.c->st);
+  int r = launch_fin(f, e.c->st);
+  if (e.prof) e.prof->end(e.c->st);
+  return r;
+}
+
+int Eng::spmm(bool adj, const void* P, void* Q, int s, std::vector<RQ> reds) {
+  if (err) return err;
+  const int cap = cap_for(s);
+  bool full = false;
+  for (auto& r : reds) full |= (r.mode == RED_FULL);
+  if (full && !full_supported(cplx, cap)) return err = (int)cudaErrorNotSupported;
+  SpmmArgs a{};
+  a.row_ptr = adj ? A->rpH : A->rp;
+  a.col_idx = adj ? A->ciH : A->ci;
+  a.val = adj ? A->valH : A->val;
+  a.P = P;
+  a.Q = Q;
+  a.n = n;
+  a.s = s;
+  a.vec = cplx ? 1 : (s % 2 == 0);
+  a.nred = (int)reds.size();
+  std::vector<int> poffs;
+  int pstride = 0, maxlen = 0;
+  for (size_t i = 0; i < reds.size(); ++i) {
+    fill_red(a.red[i], reds[i], pstride);
+    poffs.push_back(pstride);
+    const int len = red_len(reds[i].mode, s, cplx);
+    pstride += len;
+    maxlen = std::max(maxlen, len);
+  }
+  a.pstride = std::max(pstride, 1);
+  const int grid = grid_for(cap, full);
+  if ((err = c->ensure_partials((size_t)grid * a.pstride))) return err;
+  a.partials = c->partials;
+  a.done = done;
+  const size_t smem = (size_t)8 * maxlen * sizeof(double);
+  nlaunch++;
+  if (prof) prof->begin(adj ? PT_SPMM_ADJ : PT_SPMM, c->st);
+  err = launch_spmm(cplx, cap, full, a, grid, 256, smem, c->st);
+  if (prof) prof->end(c->st);
+  if (err) return err;
+  return err = finish_reds(*this, reds, poffs, s, grid, a.pstride);
+}
+
+int Eng::upd(int s, std::vector<const void*> in, std::vector<OutSpec> outs, std::vector<RQ> reds) {
+  if (err) return err;
+  const int cap = cap_for(s);
+  bool full = false;
+  for (auto& r : reds) full |= (r.mode == RED_FULL);
+  if (full && !full_supported(cplx, cap)) return err = (int)cudaErrorNotSupported;
+  if (in.size() > MAX_IN || outs.size() > MAX_OUT || reds.size() > MAX_RED) return err = (int)cudaErrorInvalidValue;
+  UpdArgs a{};
+  a.nin = (int)in.size();
+  for (size_t i = 0; i < in.size(); ++i) a.in[i] = in[i];
+  a.nout = (int)outs.size();
+  int cslot = 0;
+  for (size_t o = 0; o < outs.size(); ++o) {
+    a.out[o].ptr = outs[o].ptr;
+    a.out[o].nterm = (int)outs[o].t.size();
+    if (outs[o].t.size() > 4) return err = (int)cudaErrorInvalidValue;
+    for (size_t t = 0; t < outs[o].t.size(); ++t) {
+      a.out[o].t[t].src = outs[o].t[t].src;
+      a.out[o].t[t].c = outs[o].t[t].c;
+      a.cslot[o][t] = cslot;
+      const int k = outs[o].t[t].c.kind;
+      const int pw = padded_width(cap, cplx);
+      cslot += (k == CK_FULL) ? cap * pw : (k == CK_DIAG ? pw : 1);
+      if (cslot & 1) cslot++;  // keep 16-byte alignment of the following slot
+    }
+  }
+  a.cslot_total = cslot;
+  a.nred = (int)reds.size();
+  std::vector<int> poffs;
+  int pstride = 0, maxlen = 0;
+  for (size_t i = 0; i < reds.size(); ++i) {
+    if (reds[i].mode == RED_FULL && i == 2) return err = (int)cudaErrorInvalidValue;  // slot 2 holds no s x s Gram
+    fill_red(a.red[i], reds[i], pstride);
+    poffs.push_back(pstride);
+    const int len = red_len(reds[i].mode, s, cplx);
+    pstride += len;
+    maxlen = std::max(maxlen, len);
+  }
+  a.pstride = std::max(pstride, 1);
+  a.ws = ws;
+  a.n = n;
+  a.s = s;
+  a.vec = cplx ? 1 : (s % 2 == 0);
+  a.done = done;
+  const int grid = grid_for(cap, full);
+  if ((err = c->ensure_partials((size_t)grid * a.pstride))) return err;
+  a.partials = c->partials;
+  const size_t esz = cplx ? 16 : 8;
+  const size_t smem = (size_t)cslot * esz + (size_t)8 * maxlen * sizeof(double);
+  nlaunch++;
+  if (prof) prof->begin(PT_UPD, c->st);
+  err = launch_upd(cplx, cap, full, a, grid, 256, smem, c->st);
+  if (prof) prof->end(c->st);
+  if (err) return err;
+  return err = finish_reds(*this, reds, poffs, s, grid, a.pstride);
+}
+
+// ---------------------------------------------------------------------------
+// small helper kernels
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void row_mean_kernel(const T* X, T* out, long long n, int s, const int* done) {
+  if (done && *done) return;
+  const double inv = 1.0 / s;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    T acc = Ar<T>::zero();
+    for (int c = 0; c < s; ++c) acc = Ar<T>::add(acc, X[i * s + c]);
+    if constexpr (Ar<T>::cplx) out[i] = mk(acc.x * inv, acc.y * inv);
+    else out[i] = acc * inv;
+  }
+}
+
+int launch_row_mean(bool cplx, const void* X, void* out, long long n, int s, const int* done, cudaStream_t st) {
+  const int grid = (int)std::min<long long>((n + 255) / 256, 148 * 8);
+  if (cplx)
+    row_mean_kernel<double2><<<std::max(grid, 1), 256, 0, st>>>((const double2*)X, (double2*)out, n, s, done);
+  else
+    row_mean_kernel<double><<<std::max(grid, 1), 256, 0, st>>>((const double*)X, (double*)out, n, s, done);
+  return (int)cudaGetLastError();
+}
+
+// CSR validation (SPEC SparseMatrix invariants S:36): row_ptr non-decreasing,
+// row_ptr[0] = 0, row_ptr[n] = nnz, columns in [0, n) strictly increasing per row.
+__global__ void csr_check_kernel(long long n, long long nnz, const int* rp, const int* ci, int* bad) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const int b = rp[i], e = rp[i + 1];
+    if (e < b || b < 0 || e > nnz) { atomicOr(bad, 1); continue; }
+    if (i == 0 && b != 0) atomicOr(bad, 1);
+    if (i == n - 1 && e != nnz) atomicOr(bad, 1);
+    for (int j = b; j < e; ++j) {
+      const int c = ci[j];
+      if (c < 0 || c >= n) atomicOr(bad, 2);
+      if (j > b && c <= ci[j - 1]) atomicOr(bad, 4);
+    }
+  }
+}
+
+int launch_csr_check(long long n, long long nnz, const int* rp, const int* ci, int* bad, cudaStream_t st) {
+  const int grid = (int)std::max<long long>(1, std::min<long long>((n + 255) / 256, 148 * 8));
+  csr_check_kernel<<<grid, 256, 0, st>>>(n, nnz, rp, ci, bad);
+  return (int)cudaGetLastError();
+}
+
+// A^H = conj(A)^T as CSR: (1) count entries per column, (2) exclusive scan,
+// (3) scatter with per-column cursors, (4) sort each row of A^H by column so
+// the result is deterministic (integer atomics only decide slot order, which the
+// sort removes).
+__global__ void colcount_kernel(long long nnz, const int* ci, int* cnt) {
+  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < nnz; j += (long long)gridDim.x * blockDim.x)
+    atomicAdd(cnt + ci[j], 1);
+}
+
+// single-CTA exclusive scan of n+1 ints (cnt -> rpT), chunked
+__global__ void scan_kernel(long long n, const int* cnt, int* rpT) {
+  __shared__ long long carry;
+  __shared__ long long part[1024];
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (long long base = 0; base < n; base += 1024 * 16) {
+    // each thread sums 16 consecutive entries
+    long long loc = 0;
+    const long long b0 = base + threadIdx.x * 16;
+    for (int k = 0; k < 16; ++k)
+      if (b0 + k < n) loc += cnt[b0 + k];
+    part[threadIdx.x] = loc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      long long acc = carry;
+      for (int t = 0; t < 1024; ++t) {
+        long long v = part[t];
+        part[t] = acc;
+        acc += v;
+      }
+      carry = acc;
+    }
+    __syncthreads();
+    long long acc = part[threadIdx.x];
+    for (int k = 0; k < 16; ++k)
+      if (b0 + k < n) {
+        rpT[b0 + k] = (int)acc;
+        acc += cnt[b0 + k];
+      }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) rpT[n] = (int)carry;
+}
+
+template <typename T>
+__global__ void scatter_kernel(long long n, const int* rp, const int* ci, const T* val, int* cursor, int* ciT,
+                               T* valT) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    for (int j = rp[i]; j < rp[i + 1]; ++j) {
+      const int c = ci[j];
+      const int pos = atomicAdd(cursor + c, 1);
+      ciT[pos] = (int)i;
+      valT[pos] = Ar<T>::conj(val[j]);
+    }
+  }
+}
+
+template <typename T>
+__global__ void rowsort_kernel(long long n, const int* rpT, int* ciT, T* valT) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const int b = rpT[i], e = rpT[i + 1];
+    for (int j = b + 1; j < e; ++j) {  // insertion sort (rows are short)
+      const int c = ciT[j];
+      const T v = valT[j];
+      int k = j - 1;
+      while (k >= b && ciT[k] > c) {
+        ciT[k + 1] = ciT[k];
+        valT[k + 1] = valT[k];
+        --k;
+      }
+      ciT[k + 1] = c;
+      valT[k + 1] = v;
+    }
+  }
+}
+
+int launch_csr_transpose(bool cplx, long long n, long long nnz, const int* rp, const int* ci, const void* val,
+                         int* rpT, int* ciT, void* valT, int* work, cudaStream_t st) {
+  const int gridn = (int)std::max<long long>(1, std::min<long long>((n + 255) / 256, 148 * 8));
+  const int gridz = (int)std::max<long long>(1, std::min<long long>((nnz + 255) / 256, 148 * 8));
+  cudaMemsetAsync(work, 0, sizeof(int) * n, st);
+  colcount_kernel<<<gridz, 256, 0, st>>>(nnz, ci, work);
+  scan_kernel<<<1, 1024, 0, st>>>(n, work, rpT);
+  cudaMemcpyAsync(work, rpT, sizeof(int) * n, cudaMemcpyDeviceToDevice, st);
+  if (cplx) {
+    scatter_kernel<double2><<<gridn, 256, 0, st>>>(n, rp, ci, (const double2*)val, work, ciT, (double2*)valT);
+    rowsort_kernel<double2><<<gridn, 256, 0, st>>>(n, rpT, ciT, (double2*)valT);
+  } else {
+    scatter_kernel<double><<<gridn, 256, 0, st>>>(n, rp, ci, (const double*)val, work, ciT, (double*)valT);
+    rowsort_kernel<double><<<gridn, 256, 0, st>>>(n, rpT, ciT, (double*)valT);
+  }
+  return (int)cudaGetLastError();
+}
+
+}  // namespace srk

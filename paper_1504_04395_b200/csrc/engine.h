@@ -1,0 +1,102 @@
+// engine.h — host-side engine: context, prepared operator, kernel-call helpers.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <string>
+#include <vector>
+
+#include "kernels.cuh"
+
+namespace srk {
+
+int cap_for(int s);
+int rows_per_cta(int cap, bool cplx);
+bool full_supported(bool cplx, int cap);
+int padded_width(int cap, bool cplx);
+int launch_spmm(bool cplx, int cap, bool full, const SpmmArgs& a, int grid, int block, size_t smem, cudaStream_t st);
+int launch_upd(bool cplx, int cap, bool full, const UpdArgs& a, int grid, int block, size_t smem, cudaStream_t st);
+int launch_fin(const FinArgs& a, cudaStream_t st);
+int launch_row_mean(bool cplx, const void* X, void* out, long long n, int s, const int* done, cudaStream_t st);
+int launch_csr_transpose(bool cplx, long long n, long long nnz, const int* rp, const int* ci, const void* val,
+                         int* rpT, int* ciT, void* valT, int* work, cudaStream_t st);
+int launch_csr_check(long long n, long long nnz, const int* rp, const int* ci, int* bad, cudaStream_t st);
+
+struct Comm;  // multi-GPU plumbing (comm.cpp)
+
+struct Ctx {
+  int dev = 0;
+  cudaStream_t st = nullptr;
+  int nsm = 148;
+  double* partials = nullptr;
+  size_t pcap = 0;  // doubles
+  Comm* comm = nullptr;
+  int ensure_partials(size_t n);
+};
+
+struct Mat {
+  Ctx* ctx = nullptr;
+  long long n = 0, nnz = 0, nnzH = 0;
+  bool cplx = false;
+  int* rp = nullptr;
+  int* ci = nullptr;
+  void* val = nullptr;
+  bool has_adj = false;
+  int* rpH = nullptr;
+  int* ciH = nullptr;
+  void* valH = nullptr;
+};
+
+// reduction request: X = source (or the SpMM output), Y = source or external
+struct RQ {
+  int mode;
+  int x;             // source index (SpMM: ignored, X = Q)
+  int y;             // source index, or -1 for yext
+  const void* yext;
+  int woff;          // destination offset (doubles) in the coefficient workspace
+};
+
+struct TermSpec {
+  int src;
+  Coef c;
+};
+struct OutSpec {
+  void* ptr;
+  std::vector<TermSpec> t;
+};
+
+inline Coef C1() { return Coef{CK_ONE, 0, 0, 0, 0}; }
+inline Coef SC(int off, int neg = 0, int conj = 0) { return Coef{CK_SCALAR, off, neg, conj, 0}; }
+inline Coef DG(int off, int neg = 0, int conj = 0) { return Coef{CK_DIAG, off, neg, conj, 0}; }
+inline Coef FU(int off, int neg = 0, int herm = 0) { return Coef{CK_FULL, off, neg, 0, herm}; }
+constexpr int O0 = SRC_OUT, O1 = SRC_OUT + 1, O2 = SRC_OUT + 2, O3 = SRC_OUT + 3;
+
+// Kernel-call helper bound to one (ctx, operator, dtype, n).
+// Per-launch CUDA-event timing (bench.py's live roofline): tags
+enum ProfTag : int { PT_SPMM = 0, PT_SPMM_ADJ = 1, PT_UPD = 2, PT_FIN = 3, PT_COEF = 4, PT_OTHER = 5, PT_N = 6 };
+struct Prof {
+  bool on = false;
+  std::vector<cudaEvent_t> ev;   // pairs (start, stop)
+  std::vector<int> tag;
+  size_t used = 0;               // pairs used since the last read
+  void begin(int t, cudaStream_t st);
+  void end(cudaStream_t st);
+  int read(double* ms, long long* cnt, int ntag);  // sums per tag, resets
+  ~Prof();
+};
+
+struct Eng {
+  Prof* prof = nullptr;
+  Ctx* c = nullptr;
+  const Mat* A = nullptr;
+  bool cplx = false;
+  long long n = 0;
+  double* ws = nullptr;   // coefficient workspace (device)
+  const int* done = nullptr;
+  int err = 0;            // first CUDA error
+  int nlaunch = 0;        // kernels launched (instrumentation)
+  int spmm(bool adj, const void* P, void* Q, int s, std::vector<RQ> reds);
+  int upd(int s, std::vector<const void*> in, std::vector<OutSpec> outs, std::vector<RQ> reds);
+  int grid_for(int cap, bool full) const;
+};
+
+}  // namespace srk

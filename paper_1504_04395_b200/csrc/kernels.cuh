@@ -1,0 +1,119 @@
+// kernels.cuh — argument structs shared by the host driver and the block kernels.
+#pragma once
+#include "common.cuh"
+
+namespace srk {
+
+// ----- reductions fused into the epilogue of a block kernel -----
+// Inner-product convention <x, y> = y^H x, <X, Y> = tr(Y^H X).
+enum RedMode : int {
+  RED_NONE = 0,
+  RED_NORM2 = 1,     // ||X||_F^2                            -> 1 double
+  RED_DIAG = 2,      // (y_c^H x_c)_c, per column (Alg. 1)    -> s values
+  RED_TRACE = 3,     // tr(Y^H X) (Alg. 2)                    -> 1 value
+  RED_SUMVEC = 4,    // sum(y^H X), y an n-vector (Alg. 4)    -> 1 value
+  RED_FULL = 5,      // Y^H X, s x s (Alg. 3/5 Grams)         -> s*s values (row-major: [a][c] = y_a^H x_c)
+  RED_COLNORM2 = 6,  // (||x_c||^2)_c                        -> s doubles
+};
+
+// number of doubles a reduction produces
+__host__ __device__ inline int red_len(int mode, int s, bool cplx) {
+  const int nd = cplx ? 2 : 1;
+  switch (mode) {
+    case RED_NORM2: return 1;
+    case RED_DIAG: return s * nd;
+    case RED_TRACE: return nd;
+    case RED_SUMVEC: return nd;
+    case RED_FULL: return s * s * nd;
+    case RED_COLNORM2: return s;
+    default: return 0;
+  }
+}
+
+// source encoding for terms / reductions: 0..7 = input block, 8..11 = output j (8 + j)
+constexpr int SRC_OUT = 8;
+
+struct Red {
+  int mode;
+  int xsrc;          // block whose rows are X
+  int ysrc;          // block whose rows are Y (-1: yext)
+  const void* yext;  // external Y (n x s block, or n-vector for RED_SUMVEC)
+  int poff;          // offset of this reduction inside a CTA partial (doubles)
+};
+
+enum CoefKind : int { CK_ONE = 0, CK_SCALAR = 1, CK_DIAG = 2, CK_FULL = 3 };
+
+struct Coef {
+  int kind;  // CoefKind
+  int off;   // offset into the coefficient workspace (doubles); value(s) in the block's dtype
+  int neg;   // multiply by -1
+  int conj;  // conjugate the coefficient values
+  int herm;  // CK_FULL only: use M^H instead of M
+};
+
+struct Term {
+  int src;
+  Coef c;
+};
+
+struct OutD {
+  void* ptr;  // n x s block to store (nullptr: kept in registers only, e.g. a Gram operand)
+  int nterm;
+  Term t[4];
+};
+
+constexpr int MAX_IN = 6;
+constexpr int MAX_OUT = 4;
+constexpr int MAX_RED = 3;
+
+// Generic fused block update / Gram kernel arguments:
+//   out_j = sum_t src_t * coef_t   (row by row; coef scalar, diag or s x s)
+// plus up to MAX_RED reductions over inputs/outputs, written as per-CTA partials.
+struct UpdArgs {
+  const void* in[MAX_IN];
+  OutD out[MAX_OUT];
+  Red red[MAX_RED];
+  int nin, nout, nred;
+  int cslot[MAX_OUT][4];  // offset (in values of T) of each term's staged coefficient in smem
+  int cslot_total;
+  const double* ws;    // coefficient workspace
+  double* partials;    // [gridDim.x][pstride]
+  int pstride;
+  long long n;
+  int s;
+  int vec;             // rows 16-byte aligned (real: s even)
+  const int* done;     // skip everything when *done != 0 (device convergence flag)
+};
+
+// SpMM Q = A P (CSR, row-interleaved blocks) with fused epilogue reductions over
+// (X = Q) and an optional on-the-fly axpy of the output: Q = A P (never in place).
+struct SpmmArgs {
+  const int* row_ptr;
+  const int* col_idx;
+  const void* val;
+  const void* P;
+  void* Q;
+  long long n;
+  int s;
+  int vec;
+  Red red[2];
+  int nred;
+  double* partials;
+  int pstride;
+  const int* done;
+};
+
+// Segments for the deterministic second-stage reduction of CTA partials.
+struct FinSeg {
+  int poff, len, woff;
+};
+struct FinArgs {
+  const double* partials;
+  int nblk, pstride;
+  FinSeg seg[4];
+  int nseg;
+  double* ws;
+  const int* done;
+};
+
+}  // namespace srk

@@ -1,0 +1,653 @@
+// solver.cu — host drivers of the 13 simultaneous methods. Each iteration is
+// enqueued as a fixed sequence of block kernels (SpMM with fused Grams, fused
+// block updates) and single-CTA coefficient phases, all on one stream with no
+// host synchronisation; the host polls a device flag every `poll_every`
+// iterations (kernels after a raised flag are no-ops). Step lists follow
+// PAPER.md Alg. 1-5 and SURVEY App. A (the same order as oracle/solvers.py,
+// with which this file shares no code).
+#include <chrono>
+#include <cstring>
+
+#include "solver.h"
+
+namespace srk {
+
+static size_t slot_doubles(int s) {
+  size_t v = (size_t)4 * s * s * 2;  // (2s x 2s) complex: the Bl-QMR unitary
+  if (v < 128) v = 128;
+  return v;
+}
+
+Solver::~Solver() {
+  for (void* p : owned) cudaFree(p);
+  if (ws) cudaFree(ws);
+  if (ctl) cudaFree(ctl);
+  if (hist) cudaFree(hist);
+  if (ctl_host) cudaFreeHost(ctl_host);
+}
+
+void* Solver::blk() {
+  void* p = nullptr;
+  if (cudaMalloc(&p, (size_t)n * s * esz()) != cudaSuccess) return nullptr;
+  owned.push_back(p);
+  return p;
+}
+void* Solver::vecn() {
+  void* p = nullptr;
+  if (cudaMalloc(&p, (size_t)n * esz()) != cudaSuccess) return nullptr;
+  owned.push_back(p);
+  return p;
+}
+
+int Solver::setup() {
+  const size_t sd = slot_doubles(s);
+  for (int i = 0; i < NSLOT; ++i) off[i] = (int)(i * sd);
+  if (cudaMalloc(&ws, sd * NSLOT * sizeof(double)) != cudaSuccess) return SRK_ENOMEM;
+  cudaMemset(ws, 0, sd * NSLOT * sizeof(double));
+  if (cudaMalloc(&ctl, CTL_SIZE * sizeof(int)) != cudaSuccess) return SRK_ENOMEM;
+  if (cudaMallocHost(&ctl_host, CTL_SIZE * sizeof(int)) != cudaSuccess) return SRK_ENOMEM;
+  hist_cap = o.maxit + 2;
+  if (cudaMalloc(&hist, sizeof(double) * hist_cap) != cudaSuccess) return SRK_ENOMEM;
+  e.c = c;
+  e.A = A;
+  e.cplx = cplx;
+  e.n = n;
+  e.ws = ws;
+  e.done = ctl + CTL_FLAG;
+  e.prof = &prof;
+  B = blk();
+  X = blk();
+  R = blk();
+  tmp = blk();
+  if (!B || !X || !R || !tmp) return SRK_ENOMEM;
+  return alloc();
+}
+
+int Solver::coef(int phase, int k1) {
+  if (e.err) return e.err;
+  CoefArgs a{};
+  a.method = method;
+  a.phase = phase;
+  a.s = s;
+  a.k1 = k1;
+  a.tol = o.tol;
+  a.ws = ws;
+  a.ctl = ctl;
+  a.hist = hist;
+  a.hist_cap = hist_cap;
+  for (int i = 0; i < NSLOT; ++i) a.off[i] = off[i];
+  const size_t sm = (size_t)(3 * s * s + 64) * esz() + 1024;
+  e.nlaunch++;
+  prof.begin(PT_COEF, c->st);
+  e.err = launch_coef(cplx, a, sm, c->st);
+  prof.end(c->st);
+  return e.err;
+}
+
+int Solver::read_ctl() {
+  cudaMemcpyAsync(ctl_host, ctl, CTL_SIZE * sizeof(int), cudaMemcpyDeviceToHost, c->st);
+  cudaError_t err = cudaStreamSynchronize(c->st);
+  if (err != cudaSuccess) return e.err = (int)err;
+  return e.err;
+}
+
+// ||B - A Xc||_F / ||R0||_F, computed with the same kernels (reading G26)
+double Solver::true_rel(const void* Xc) {
+  const int* saved = e.done;
+  e.done = nullptr;
+  e.spmm(false, Xc, tmp, s, {});
+  e.upd(s, {B, tmp}, {OutSpec{nullptr, {{0, C1()}, {1, Coef{CK_ONE, 0, 1, 0, 0}}}}},
+        {RQ{RED_NORM2, O0, -1, nullptr, off[SL_TRUE]}});
+  e.done = saved;
+  double v[2] = {0, 0};
+  cudaMemcpyAsync(v, ws + off[SL_TRUE], sizeof(double), cudaMemcpyDeviceToHost, c->st);
+  cudaMemcpyAsync(v + 1, ws + off[SL_R0N], sizeof(double), cudaMemcpyDeviceToHost, c->st);
+  if (cudaStreamSynchronize(c->st) != cudaSuccess) return -1.0;
+  if (v[1] == 0.0) return 0.0;
+  return sqrt(v[0]) / v[1];
+}
+
+int Solver::start(const void* Bd, const void* X0d) {
+  cudaStream_t st = c->st;
+  cudaMemcpyAsync(B, Bd, (size_t)n * s * esz(), cudaMemcpyDeviceToDevice, st);
+  cudaMemsetAsync(ctl, 0, CTL_SIZE * sizeof(int), st);
+  host_iter = 0;
+  state = 0;
+  half = 0;
+  brk_kind = 0;
+  brk_iter = -1;
+  frozen = 0;
+  final_true = final_rec = -1.0;
+  e.err = 0;
+  e.nlaunch = 0;
+  if (X0d) {
+    cudaMemcpyAsync(X, X0d, (size_t)n * s * esz(), cudaMemcpyDeviceToDevice, st);
+    e.spmm(false, X, tmp, s, {});
+    e.upd(s, {B, tmp}, {OutSpec{R, {{0, C1()}, {1, Coef{CK_ONE, 0, 1, 0, 0}}}}},
+          {RQ{RED_NORM2, O0, -1, nullptr, off[SL_R0N2]}});
+  } else {
+    cudaMemsetAsync(X, 0, (size_t)n * s * esz(), st);
+    e.upd(s, {B}, {OutSpec{R, {{0, C1()}}}}, {RQ{RED_NORM2, O0, -1, nullptr, off[SL_R0N2]}});
+  }
+  coef(9);  // ||R0|| (and the R0 = 0 shortcut)
+  int r = init();
+  if (r) return r;
+  started = true;
+  if (e.err) return SRK_ECUDA;
+  return SRK_OK;
+}
+
+int Solver::iterate(int k) {
+  if (!started) return SRK_EINVAL;
+  if (state != 0) return SRK_OK;
+  auto t0 = std::chrono::steady_clock::now();
+  const int poll = o.poll_every > 0 ? o.poll_every : 8;
+  // device iteration count = host_iter at every poll point
+  if (read_ctl()) return SRK_ECUDA;
+  int dev_iter = ctl_host[CTL_ITER];
+  const int target = std::min(dev_iter + k, o.maxit);
+  host_iter = dev_iter;
+  while (true) {
+    int flag = ctl_host[CTL_FLAG];
+    dev_iter = ctl_host[CTL_ITER];
+    if (flag == FLAG_RUN) {
+      if (dev_iter >= target) {
+        if (dev_iter >= o.maxit) state = 3;
+        break;
+      }
+      host_iter = dev_iter;
+      int launched = 0;
+      while (host_iter < target && launched < poll) {
+        for (int q = 0; q < nseg(); ++q) seg(q);
+        launch_end_iter(ctl, c->st);
+        e.nlaunch++;
+        host_iter++;
+        launched++;
+      }
+      if (e.err) return SRK_ECUDA;
+      if (read_ctl()) return SRK_ECUDA;
+      continue;
+    }
+    if (flag == FLAG_CONV) {
+      const double tr = o.check_true_residual ? true_rel(X) : 0.0;
+      if (tr <= o.tol) {
+        state = 1;
+        break;
+      }
+      // recursive residual met tol but the true residual does not: continue (G26)
+      cudaMemsetAsync(ctl + CTL_FLAG, 0, sizeof(int), c->st);
+      if (read_ctl()) return SRK_ECUDA;
+      continue;
+    }
+    if (flag == FLAG_HALF) {
+      // BiCGStab half step (S small): X_h = X + P alpha; accept if the true residual agrees
+      half_x(tmp2);
+      const double tr = o.check_true_residual ? true_rel(tmp2) : 0.0;
+      if (tr <= o.tol) {
+        cudaMemcpyAsync(X, tmp2, (size_t)n * s * esz(), cudaMemcpyDeviceToDevice, c->st);
+        cudaMemsetAsync(ctl + CTL_FLAG, 0, sizeof(int), c->st);
+        launch_end_iter(ctl, c->st);  // counts the half iteration
+        cudaMemsetAsync(ctl + CTL_FLAG, 0, sizeof(int), c->st);
+        half = 1;
+        state = 1;
+        if (read_ctl()) return SRK_ECUDA;
+        break;
+      }
+      cudaMemsetAsync(ctl + CTL_FLAG, 0, sizeof(int), c->st);
+      for (int q = 1; q < nseg(); ++q) seg(q);  // finish this iteration
+      launch_end_iter(ctl, c->st);
+      if (read_ctl()) return SRK_ECUDA;
+      continue;
+    }
+    if (flag == FLAG_BRK) {
+      brk_kind = ctl_host[CTL_BKIND];
+      brk_iter = ctl_host[CTL_BITER];
+      // a breakdown at an iterate that already satisfies the stopping rule is a lucky breakdown
+      const double tr = true_rel(X);
+      if (brk_iter > 0 && tr <= o.tol) {
+        state = 1;
+        cudaMemcpyAsync(ctl + CTL_ITER, &brk_iter, sizeof(int), cudaMemcpyHostToDevice, c->st);
+        if (read_ctl()) return SRK_ECUDA;
+      } else {
+        state = 2;
+      }
+      break;
+    }
+    break;
+  }
+  cudaStreamSynchronize(c->st);
+  auto t1 = std::chrono::steady_clock::now();
+  seconds += std::chrono::duration<double>(t1 - t0).count();
+  launches = e.nlaunch;
+  frozen = ctl_host[CTL_NFROZEN];
+  if (e.err) return SRK_ECUDA;
+  return SRK_OK;
+}
+
+int Solver::residual(void* out, int64_t* rows) {
+  cudaMemcpyAsync(out, R, (size_t)n * s * esz(), cudaMemcpyDeviceToDevice, c->st);
+  if (rows) *rows = n;
+  return cudaStreamSynchronize(c->st) == cudaSuccess ? SRK_OK : SRK_ECUDA;
+}
+
+// ---------------------------------------------------------------------------
+// device thin QR (CholQR2) used by the rQ variants' initialisation and srk_tsqr
+// Phases 10/11 (slots GZ -> R1, C) and 12/13 (GZH -> R1H, CH) of the coefficient kernel.
+// ---------------------------------------------------------------------------
+static void dev_tsqr(Solver& S, const void* Z, void* Q, bool hat) {
+  Eng& e = S.e;
+  const int gz = hat ? SL_GZH : SL_GZ;
+  e.upd(S.s, {Z}, {OutSpec{nullptr, {{0, C1()}}}}, {RQ{RED_FULL, O0, O0, nullptr, S.off[gz]}});
+  S.coef(hat ? 12 : 10);
+  e.upd(S.s, {Z}, {OutSpec{Q, {{0, FU(S.off[hat ? SL_R1HI : SL_R1I])}}}}, {RQ{RED_FULL, O0, O0, nullptr, S.off[gz]}});
+  S.coef(hat ? 13 : 11);
+  e.upd(S.s, {Q}, {OutSpec{Q, {{0, FU(S.off[hat ? SL_R2HI : SL_R2I])}}}}, {});
+}
+
+static inline Coef NEG1() { return Coef{CK_ONE, 0, 1, 0, 0}; }
+
+// =============================================================================
+// BiCG family
+// =============================================================================
+struct GlBiCG : Solver {  // Alg. 2 (Gl) and Alg. 1 (Li: diag coefficients)
+  bool li = false;
+  void *P, *Q, *Rh, *Ph, *Qh;
+  int alloc() override {
+    P = blk(); Q = blk(); Rh = blk(); Ph = blk(); Qh = blk();
+    cols_A = s; cols_AH = s;
+    return (P && Q && Rh && Ph && Qh) ? 0 : SRK_ENOMEM;
+  }
+  int rmode() const { return li ? RED_DIAG : RED_TRACE; }
+  Coef K(int slot, int neg = 0, int cj = 0) const { return li ? DG(off[slot], neg, cj) : SC(off[slot], neg, cj); }
+  int init() override {
+    const size_t b = (size_t)n * s * esz();
+    cudaMemcpyAsync(Rh, R, b, cudaMemcpyDeviceToDevice, c->st);  // shadow R̂0 = R0
+    cudaMemcpyAsync(P, R, b, cudaMemcpyDeviceToDevice, c->st);
+    cudaMemcpyAsync(Ph, R, b, cudaMemcpyDeviceToDevice, c->st);
+    e.upd(s, {R, Rh}, {}, {RQ{rmode(), 0, 1, nullptr, off[SL_RHO]}});
+    return coef(0);
+  }
+  void seg(int) override {
+    e.spmm(false, P, Q, s, {RQ{rmode(), 0, -1, Ph, off[SL_DEN]}});   // Q = A P ; <q, p̂>
+    e.spmm(true, Ph, Qh, s, {});                                     // A^H P̂
+    coef(1);
+    e.upd(s, {X, P, R, Q, Rh, Qh},
+          {OutSpec{X, {{0, C1()}, {1, K(SL_ALPHA)}}},
+           OutSpec{R, {{2, C1()}, {3, K(SL_ALPHA, 1)}}},
+           OutSpec{Rh, {{4, C1()}, {5, K(SL_ALPHA, 1, 1)}}}},
+          {RQ{rmode(), O1, O2, nullptr, off[SL_RHON]}, RQ{RED_NORM2, O1, -1, nullptr, off[SL_R2]}});
+    coef(2);
+    e.upd(s, {R, P, Rh, Ph},
+          {OutSpec{P, {{0, C1()}, {1, K(SL_BETA)}}}, OutSpec{Ph, {{2, C1()}, {3, K(SL_BETA, 0, 1)}}}}, {});
+  }
+};
+
+struct EglBiCG : Solver {  // Alg. 4
+  void *P, *Q, *rh, *ph, *qh;
+  int alloc() override {
+    P = blk(); Q = blk(); rh = vecn(); ph = vecn(); qh = vecn();
+    cols_A = s; cols_AH = 1;
+    return (P && Q && rh && ph && qh) ? 0 : SRK_ENOMEM;
+  }
+  int init() override {
+    cudaMemcpyAsync(P, R, (size_t)n * s * esz(), cudaMemcpyDeviceToDevice, c->st);
+    launch_row_mean(cplx, R, rh, n, s, nullptr, c->st);  // r̂0 = mean of the columns
+    cudaMemcpyAsync(ph, rh, (size_t)n * esz(), cudaMemcpyDeviceToDevice, c->st);
+    e.upd(s, {R}, {}, {RQ{RED_SUMVEC, 0, -1, rh, off[SL_RHO]}});
+    return coef(0);
+  }
+  void seg(int) override {
+    e.spmm(false, P, Q, s, {RQ{RED_SUMVEC, 0, -1, ph, off[SL_DEN]}});  // sum(p̂^H Q)
+    e.spmm(true, ph, qh, 1, {});                                        // A^H p̂ (one vector)
+    coef(1);
+    e.upd(1, {rh, qh}, {OutSpec{rh, {{0, C1()}, {1, SC(off[SL_ALPHA], 1, 1)}}}}, {});
+    e.upd(s, {X, P, R, Q},
+          {OutSpec{X, {{0, C1()}, {1, SC(off[SL_ALPHA])}}}, OutSpec{R, {{2, C1()}, {3, SC(off[SL_ALPHA], 1)}}}},
+          {RQ{RED_SUMVEC, O1, -1, rh, off[SL_RHON]}, RQ{RED_NORM2, O1, -1, nullptr, off[SL_R2]}});
+    coef(2);
+    e.upd(s, {R, P}, {OutSpec{P, {{0, C1()}, {1, SC(off[SL_BETA])}}}}, {});
+    e.upd(1, {rh, ph}, {OutSpec{ph, {{0, C1()}, {1, SC(off[SL_BETA], 0, 1)}}}}, {});
+  }
+};
+
+struct BlBiCG : Solver {  // Alg. 3
+  void *P, *Q, *Rh, *Ph, *Qh;
+  int alloc() override {
+    P = blk(); Q = blk(); Rh = blk(); Ph = blk(); Qh = blk();
+    cols_A = s; cols_AH = s;
+    return (P && Q && Rh && Ph && Qh) ? 0 : SRK_ENOMEM;
+  }
+  int init() override {
+    const size_t b = (size_t)n * s * esz();
+    cudaMemcpyAsync(Rh, R, b, cudaMemcpyDeviceToDevice, c->st);
+    cudaMemcpyAsync(P, R, b, cudaMemcpyDeviceToDevice, c->st);
+    cudaMemcpyAsync(Ph, R, b, cudaMemcpyDeviceToDevice, c->st);
+    e.upd(s, {R, Rh}, {}, {RQ{RED_FULL, 0, 1, nullptr, off[SL_M]}});  // M = R̂^H R
+    return coef(0);
+  }
+  void seg(int) override {
+    e.spmm(false, P, Q, s, {RQ{RED_FULL, 0, -1, Ph, off[SL_G]}});  // G = P̂^H Q
+    e.spmm(true, Ph, Qh, s, {});
+    coef(1);
+    e.upd(s, {X, P, R, Q, Rh, Qh},
+          {OutSpec{X, {{0, C1()}, {1, FU(off[SL_ALPHA])}}},
+           OutSpec{R, {{2, C1()}, {3, FU(off[SL_ALPHA], 1)}}},
+           OutSpec{Rh, {{4, C1()}, {5, FU(off[SL_AH], 1)}}}},
+          {RQ{RED_FULL, O1, O2, nullptr, off[SL_MN]}, RQ{RED_NORM2, O1, -1, nullptr, off[SL_R2]}});
+    coef(2);
+    e.upd(s, {R, P, Rh, Ph},
+          {OutSpec{P, {{0, C1()}, {1, FU(off[SL_BETA])}}}, OutSpec{Ph, {{2, C1()}, {3, FU(off[SL_BH])}}}}, {});
+  }
+};
+
+struct BlBiCGrQ : Solver {  // Alg. 5
+  void *Qr, *Qh, *V, *Vh, *W, *Wh, *Z, *Zh;
+  bool is_rq() const override { return true; }
+  int alloc() override {
+    Qr = blk(); Qh = blk(); V = blk(); Vh = blk(); W = blk(); Wh = blk(); Z = blk(); Zh = blk();
+    cols_A = s; cols_AH = s;
+    return (Qr && Qh && V && Vh && W && Wh && Z && Zh) ? 0 : SRK_ENOMEM;
+  }
+  int init() override {
+    const size_t b = (size_t)n * s * esz();
+    dev_tsqr(*this, R, Qr, false);  // Q(0) C(0) = R(0)
+    // shadow R̂0 = R0: Q̂(0) = Q(0), Ĉ(0) = C(0)
+    cudaMemcpyAsync(Qh, Qr, b, cudaMemcpyDeviceToDevice, c->st);
+    cudaMemcpyAsync(ws + off[SL_CH], ws + off[SL_C], s * s * esz(), cudaMemcpyDeviceToDevice, c->st);
+    cudaMemcpyAsync(V, Qr, b, cudaMemcpyDeviceToDevice, c->st);
+    cudaMemcpyAsync(Vh, Qh, b, cudaMemcpyDeviceToDevice, c->st);
+    e.upd(s, {Qr, Qh}, {}, {RQ{RED_FULL, 0, 1, nullptr, off[SL_G2]}});  // G2 = Q̂^H Q
+    return coef(0);
+  }
+  void seg(int) override {
+    e.spmm(false, V, W, s, {RQ{RED_FULL, 0, -1, Vh, off[SL_G1]}});  // G1 = V̂^H W
+    e.spmm(true, Vh, Wh, s, {});
+    coef(1);
+    e.upd(s, {X, V, Qr, W, Qh, Wh},
+          {OutSpec{X, {{0, C1()}, {1, FU(off[SL_AC])}}},
+           OutSpec{Z, {{2, C1()}, {3, FU(off[SL_ALPHA], 1)}}},
+           OutSpec{Zh, {{4, C1()}, {5, FU(off[SL_AH], 1)}}}},
+          {RQ{RED_FULL, O1, O1, nullptr, off[SL_GZ]}, RQ{RED_FULL, O2, O2, nullptr, off[SL_GZH]}});
+    coef(2);
+    e.upd(s, {Z, Zh}, {OutSpec{Z, {{0, FU(off[SL_R1I])}}}, OutSpec{Zh, {{1, FU(off[SL_R1HI])}}}},
+          {RQ{RED_FULL, O0, O0, nullptr, off[SL_GZ]}, RQ{RED_FULL, O1, O1, nullptr, off[SL_GZH]}});
+    coef(3);
+    e.upd(s, {Z, Zh}, {OutSpec{Qr, {{0, FU(off[SL_R2I])}}}, OutSpec{Qh, {{1, FU(off[SL_R2HI])}}}},
+          {RQ{RED_FULL, O0, O1, nullptr, off[SL_G2N]}});
+    coef(4);
+    e.upd(s, {Qr, V, Qh, Vh},
+          {OutSpec{V, {{0, C1()}, {1, FU(off[SL_BETA])}}}, OutSpec{Vh, {{2, C1()}, {3, FU(off[SL_BH])}}}}, {});
+  }
+  int residual(void* out, int64_t* rows) override {  // C(k): ||R|| = ||C||
+    cudaMemcpyAsync(out, ws + off[SL_C], (size_t)s * s * esz(), cudaMemcpyDeviceToDevice, c->st);
+    if (rows) *rows = s;
+    return cudaStreamSynchronize(c->st) == cudaSuccess ? SRK_OK : SRK_ECUDA;
+  }
+};
+
+// =============================================================================
+// BiCGStab family
+// =============================================================================
+struct GlBiCGStab : Solver {  // Gl (scalar) and Li (diag)
+  bool li = false;
+  void *P, *V, *S, *T, *Rt;
+  int nseg() const override { return 2; }
+  int alloc() override {
+    P = blk(); V = blk(); S = blk(); T = blk(); Rt = blk(); tmp2 = blk();
+    cols_A = 2 * s; cols_AH = 0;
+    return (P && V && S && T && Rt && tmp2) ? 0 : SRK_ENOMEM;
+  }
+  int rmode() const { return li ? RED_DIAG : RED_TRACE; }
+  Coef K(int slot, int neg = 0) const { return li ? DG(off[slot], neg) : SC(off[slot], neg); }
+  int init() override {
+    const size_t b = (size_t)n * s * esz();
+    cudaMemcpyAsync(Rt, R, b, cudaMemcpyDeviceToDevice, c->st);  // R̃ = R0
+    cudaMemcpyAsync(P, R, b, cudaMemcpyDeviceToDevice, c->st);
+    e.upd(s, {R, Rt}, {}, {RQ{rmode(), 0, 1, nullptr, off[SL_RHO]}});
+    return coef(0);
+  }
+  void seg(int q) override {
+    if (q == 0) {
+      e.spmm(false, P, V, s, {RQ{rmode(), 0, -1, Rt, off[SL_DEN]}});  // V = A P ; <v, r̃>
+      coef(1);
+      e.upd(s, {R, V}, {OutSpec{S, {{0, C1()}, {1, K(SL_ALPHA, 1)}}}}, {RQ{RED_NORM2, O0, -1, nullptr, off[SL_S2]}});
+      coef(2);  // half-step test on ||S||_F
+    } else {
+      e.spmm(false, S, T, s,
+             {RQ{rmode(), 0, -1, S, off[SL_ST]}, RQ{li ? RED_COLNORM2 : RED_NORM2, 0, -1, nullptr, off[SL_TT]}});
+      coef(3);
+      e.upd(s, {X, P, S, T, Rt},
+            {OutSpec{X, {{0, C1()}, {1, K(SL_ALPHA)}, {2, K(SL_OMEGA)}}},
+             OutSpec{R, {{2, C1()}, {3, K(SL_OMEGA, 1)}}}},
+            {RQ{rmode(), O1, 4, nullptr, off[SL_RHON]}, RQ{RED_NORM2, O1, -1, nullptr, off[SL_R2]}});
+      coef(4);
+      e.upd(s, {R, P, V}, {OutSpec{P, {{0, C1()}, {1, K(SL_BETA)}, {2, K(SL_BW, 1)}}}}, {});
+    }
+  }
+  void half_x(void* Xh) override {
+    const int* sv = e.done;
+    e.done = nullptr;
+    e.upd(s, {X, P}, {OutSpec{Xh, {{0, C1()}, {1, K(SL_ALPHA)}}}}, {});
+    e.done = sv;
+  }
+};
+
+struct BlBiCGStab : Solver {  // [ELg03], SURVEY App. A.4
+  void *P, *U, *S, *T, *Rt;
+  int nseg() const override { return 2; }
+  int alloc() override {
+    P = blk(); U = blk(); S = blk(); T = blk(); Rt = blk(); tmp2 = blk();
+    cols_A = 2 * s; cols_AH = 0;
+    return (P && U && S && T && Rt && tmp2) ? 0 : SRK_ENOMEM;
+  }
+  int init() override {
+    const size_t b = (size_t)n * s * esz();
+    cudaMemcpyAsync(Rt, R, b, cudaMemcpyDeviceToDevice, c->st);
+    cudaMemcpyAsync(P, R, b, cudaMemcpyDeviceToDevice, c->st);
+    e.upd(s, {R, Rt}, {}, {RQ{RED_FULL, 0, 1, nullptr, off[SL_M]}});  // R̃^H R
+    return coef(0);
+  }
+  void seg(int q) override {
+    if (q == 0) {
+      e.spmm(false, P, U, s, {RQ{RED_FULL, 0, -1, Rt, off[SL_G]}});  // G = R̃^H U
+      coef(1);
+      e.upd(s, {R, U}, {OutSpec{S, {{0, C1()}, {1, FU(off[SL_ALPHA], 1)}}}}, {RQ{RED_NORM2, O0, -1, nullptr, off[SL_S2]}});
+      coef(2);
+    } else {
+      e.spmm(false, S, T, s, {RQ{RED_TRACE, 0, -1, S, off[SL_ST]}, RQ{RED_NORM2, 0, -1, nullptr, off[SL_TT]}});
+      coef(3);
+      e.upd(s, {X, P, S, T, Rt},
+            {OutSpec{X, {{0, C1()}, {1, FU(off[SL_ALPHA])}, {2, SC(off[SL_OMEGA])}}},
+             OutSpec{R, {{2, C1()}, {3, SC(off[SL_OMEGA], 1)}}}},
+            {RQ{RED_FULL, 3, 4, nullptr, off[SL_MN]}, RQ{RED_FULL, O1, 4, nullptr, off[SL_M]},
+             RQ{RED_NORM2, O1, -1, nullptr, off[SL_R2]}});
+      coef(4);
+      e.upd(s, {R, P, U}, {OutSpec{P, {{0, C1()}, {1, FU(off[SL_BETA])}, {2, FU(off[SL_BW], 1)}}}}, {});
+    }
+  }
+  void half_x(void* Xh) override {
+    const int* sv = e.done;
+    e.done = nullptr;
+    e.upd(s, {X, P}, {OutSpec{Xh, {{0, C1()}, {1, FU(off[SL_ALPHA])}}}}, {});
+    e.done = sv;
+  }
+};
+
+struct BlBiCGStabrQ : Solver {
+  void *Qr, *Q0, *V, *W, *Z, *Y;
+  bool is_rq() const override { return true; }
+  int nseg() const override { return 2; }
+  int alloc() override {
+    Qr = blk(); Q0 = blk(); V = blk(); W = blk(); Z = blk(); Y = blk(); tmp2 = blk();
+    cols_A = 2 * s; cols_AH = 0;
+    return (Qr && Q0 && V && W && Z && Y && tmp2) ? 0 : SRK_ENOMEM;
+  }
+  int init() override {
+    const size_t b = (size_t)n * s * esz();
+    dev_tsqr(*this, R, Qr, false);
+    cudaMemcpyAsync(Q0, Qr, b, cudaMemcpyDeviceToDevice, c->st);  // Q̂0 = Qr when R̃ = R0
+    cudaMemcpyAsync(V, Qr, b, cudaMemcpyDeviceToDevice, c->st);
+    e.upd(s, {Qr, Q0}, {}, {RQ{RED_FULL, 0, 1, nullptr, off[SL_GQ]}});
+    return coef(0);
+  }
+  void seg(int q) override {
+    if (q == 0) {
+      e.spmm(false, V, W, s, {RQ{RED_FULL, 0, -1, Q0, off[SL_G]}});  // G = Q̂0^H W
+      coef(1);
+      e.upd(s, {Qr, W}, {OutSpec{Z, {{0, C1()}, {1, FU(off[SL_ALPHA], 1)}}}}, {RQ{RED_FULL, O0, O0, nullptr, off[SL_ZZ]}});
+      coef(2);
+    } else {
+      e.spmm(false, Z, Y, s, {RQ{RED_FULL, 0, -1, Z, off[SL_YZ]}, RQ{RED_FULL, 0, -1, Y, off[SL_YY]}});
+      coef(3);
+      e.upd(s, {X, V, Z, Y},
+            {OutSpec{X, {{0, C1()}, {1, FU(off[SL_AC])}, {2, FU(off[SL_WC])}}},
+             OutSpec{Z, {{2, C1()}, {3, SC(off[SL_OMEGA], 1)}}}},
+            {RQ{RED_FULL, O1, O1, nullptr, off[SL_GZ]}});
+      coef(4);
+      e.upd(s, {Z}, {OutSpec{Z, {{0, FU(off[SL_R1I])}}}}, {RQ{RED_FULL, O0, O0, nullptr, off[SL_GZ]}});
+      coef(5);
+      e.upd(s, {Z, Q0}, {OutSpec{Qr, {{0, FU(off[SL_R2I])}}}}, {RQ{RED_FULL, O0, 1, nullptr, off[SL_GQN]}});
+      coef(6);
+      e.upd(s, {Qr, V, W}, {OutSpec{V, {{0, C1()}, {1, FU(off[SL_BETA])}, {2, FU(off[SL_BW], 1)}}}}, {});
+    }
+  }
+  void half_x(void* Xh) override {
+    const int* sv = e.done;
+    e.done = nullptr;
+    e.upd(s, {X, V}, {OutSpec{Xh, {{0, C1()}, {1, FU(off[SL_AC])}}}}, {});
+    e.done = sv;
+  }
+  int residual(void* out, int64_t* rows) override {
+    cudaMemcpyAsync(out, ws + off[SL_C], (size_t)s * s * esz(), cudaMemcpyDeviceToDevice, c->st);
+    if (rows) *rows = s;
+    return cudaStreamSynchronize(c->st) == cudaSuccess ? SRK_OK : SRK_ECUDA;
+  }
+};
+
+// =============================================================================
+// QMR family
+// =============================================================================
+struct QMR : Solver {  // mode 0 Li, 1 Gl, 2 eGl
+  int mode = 1;
+  void *Vt, *V, *P, *Pt, *D, *S, *Wt, *Wv, *Qv, *AHQ;
+  int alloc() override {
+    Vt = blk(); V = blk(); P = blk(); Pt = blk(); D = blk(); S = blk();
+    if (mode == 2) { Wt = vecn(); Wv = vecn(); Qv = vecn(); AHQ = vecn(); }
+    else { Wt = blk(); Wv = blk(); Qv = blk(); AHQ = blk(); }
+    cols_A = s; cols_AH = (mode == 2) ? 1 : s;
+    return (Vt && V && P && Pt && D && S && Wt && Wv && Qv && AHQ) ? 0 : SRK_ENOMEM;
+  }
+  int ws_() const { return mode == 2 ? 1 : s; }  // width of the left Lanczos block
+  int nrm() const { return mode == 0 ? RED_COLNORM2 : RED_NORM2; }
+  Coef K(int slot, int neg = 0, int cj = 0) const { return mode == 0 ? DG(off[slot], neg, cj) : SC(off[slot], neg, cj); }
+  int init() override {
+    const size_t b = (size_t)n * s * esz();
+    cudaMemcpyAsync(Vt, R, b, cudaMemcpyDeviceToDevice, c->st);
+    if (mode == 2) launch_row_mean(cplx, R, Wt, n, s, nullptr, c->st);  // w̃0 = mean of the columns
+    else cudaMemcpyAsync(Wt, R, b, cudaMemcpyDeviceToDevice, c->st);     // W̃0 = R0
+    e.upd(s, {Vt}, {}, {RQ{nrm(), 0, -1, nullptr, off[SL_RHON2]}});
+    e.upd(ws_(), {Wt}, {}, {RQ{nrm(), 0, -1, nullptr, off[SL_XI2]}});
+    cudaMemsetAsync(P, 0, b, c->st);
+    cudaMemsetAsync(D, 0, b, c->st);
+    cudaMemsetAsync(S, 0, b, c->st);
+    cudaMemsetAsync(Qv, 0, (size_t)n * ws_() * esz(), c->st);
+    return coef(0);
+  }
+  void seg(int) override {
+    coef(1);  // 1/rho, 1/xi
+    const int dmode = mode == 0 ? RED_DIAG : (mode == 1 ? RED_TRACE : RED_SUMVEC);
+    if (mode == 2) {
+      e.upd(1, {Wt}, {OutSpec{Wv, {{0, SC(off[SL_INVXI])}}}}, {});
+      e.upd(s, {Vt}, {OutSpec{V, {{0, SC(off[SL_INVRHO])}}}}, {RQ{RED_SUMVEC, O0, -1, Wv, off[SL_DELTA]}});
+    } else {
+      e.upd(s, {Vt, Wt}, {OutSpec{V, {{0, K(SL_INVRHO)}}}, OutSpec{Wv, {{1, K(SL_INVXI)}}}},
+            {RQ{dmode, O0, O1, nullptr, off[SL_DELTA]}});
+    }
+    coef(2, host_iter == 0);
+    if (mode == 2) {
+      e.upd(s, {V, P}, {OutSpec{P, {{0, C1()}, {1, SC(off[SL_C1], 1)}}}}, {});
+      e.upd(1, {Wv, Qv}, {OutSpec{Qv, {{0, C1()}, {1, SC(off[SL_C2], 1)}}}}, {});
+    } else {
+      e.upd(s, {V, P, Wv, Qv},
+            {OutSpec{P, {{0, C1()}, {1, K(SL_C1, 1)}}}, OutSpec{Qv, {{2, C1()}, {3, K(SL_C2, 1)}}}}, {});
+    }
+    e.spmm(false, P, Pt, s, {RQ{dmode, 0, -1, Qv, off[SL_EPS]}});  // P~ = A P ; eps = <P~, Q>
+    e.spmm(true, Qv, AHQ, ws_(), {});
+    coef(3);  // beta
+    e.upd(s, {Pt, V}, {OutSpec{Vt, {{0, C1()}, {1, K(SL_BETA, 1)}}}}, {RQ{nrm(), O0, -1, nullptr, off[SL_RHON2]}});
+    e.upd(ws_(), {AHQ, Wv}, {OutSpec{Wt, {{0, C1()}, {1, K(SL_BETA, 1, 1)}}}}, {RQ{nrm(), O0, -1, nullptr, off[SL_XI2]}});
+    coef(4);  // theta, gamma, eta, f
+    e.upd(s, {P, D, Pt, S, X, R},
+          {OutSpec{D, {{0, K(SL_ETA)}, {1, K(SL_F)}}},
+           OutSpec{S, {{2, K(SL_ETA)}, {3, K(SL_F)}}},
+           OutSpec{X, {{4, C1()}, {O0, C1()}}},
+           OutSpec{R, {{5, C1()}, {O1, NEG1()}}}},
+          {RQ{RED_NORM2, O3, -1, nullptr, off[SL_R2]}});
+    coef(5);
+  }
+};
+
+struct BlQMR : Solver {
+  void *V, *Wb, *P, *Qb, *AP, *AHQ, *D, *F, *Zv, *Zw;
+  int alloc() override {
+    V = blk(); Wb = blk(); P = blk(); Qb = blk(); AP = blk(); AHQ = blk(); D = blk(); F = blk(); Zv = blk(); Zw = blk();
+    cols_A = s; cols_AH = s;
+    return (V && Wb && P && Qb && AP && AHQ && D && F && Zv && Zw) ? 0 : SRK_ENOMEM;
+  }
+  int init() override {
+    const size_t b = (size_t)n * s * esz();
+    dev_tsqr(*this, R, V, false);  // V rho = R0
+    cudaMemcpyAsync(ws + off[SL_RHOB], ws + off[SL_C], (size_t)s * s * esz(), cudaMemcpyDeviceToDevice, c->st);
+    cudaMemcpyAsync(Wb, V, b, cudaMemcpyDeviceToDevice, c->st);  // W xi = R̂0 = R0
+    cudaMemcpyAsync(ws + off[SL_XIB], ws + off[SL_C], (size_t)s * s * esz(), cudaMemcpyDeviceToDevice, c->st);
+    cudaMemsetAsync(P, 0, b, c->st);
+    cudaMemsetAsync(Qb, 0, b, c->st);
+    cudaMemsetAsync(D, 0, b, c->st);
+    cudaMemsetAsync(F, 0, b, c->st);
+    return coef(0);
+  }
+  void seg(int) override {
+    e.upd(s, {V, Wb}, {}, {RQ{RED_FULL, 0, 1, nullptr, off[SL_DELTA]}});  // delta = W^H V
+    coef(1, host_iter == 0);
+    e.upd(s, {V, P, Wb, Qb},
+          {OutSpec{P, {{0, C1()}, {1, FU(off[SL_C1], 1)}}}, OutSpec{Qb, {{2, C1()}, {3, FU(off[SL_C2], 1)}}}}, {});
+    e.spmm(false, P, AP, s, {RQ{RED_FULL, 0, -1, Qb, off[SL_EPS]}});  // eps = Q^H A P
+    e.spmm(true, Qb, AHQ, s, {});
+    coef(2);
+    e.upd(s, {AP, V, AHQ, Wb},
+          {OutSpec{Zv, {{0, C1()}, {1, FU(off[SL_BETA], 1)}}}, OutSpec{Zw, {{2, C1()}, {3, FU(off[SL_GHAT], 1)}}}},
+          {RQ{RED_FULL, O0, O0, nullptr, off[SL_GZ]}, RQ{RED_FULL, O1, O1, nullptr, off[SL_GZH]}});
+    coef(3);
+    e.upd(s, {Zv, Zw}, {OutSpec{Zv, {{0, FU(off[SL_R1I])}}}, OutSpec{Zw, {{1, FU(off[SL_R1HI])}}}},
+          {RQ{RED_FULL, O0, O0, nullptr, off[SL_GZ]}, RQ{RED_FULL, O1, O1, nullptr, off[SL_GZH]}});
+    coef(4, host_iter == 0);
+    e.upd(s, {Zv, Zw}, {OutSpec{V, {{0, FU(off[SL_R2I])}}}, OutSpec{Wb, {{1, FU(off[SL_R2HI])}}}}, {});
+    e.upd(s, {P, D, X},
+          {OutSpec{D, {{0, FU(off[SL_RIII])}, {1, FU(off[SL_TR], 1)}}}, OutSpec{X, {{2, C1()}, {O0, FU(off[SL_TAU])}}}}, {});
+    e.upd(s, {AP, F, R},
+          {OutSpec{F, {{0, FU(off[SL_RIII])}, {1, FU(off[SL_TR], 1)}}}, OutSpec{R, {{2, C1()}, {O0, FU(off[SL_TAU], 1)}}}},
+          {RQ{RED_NORM2, O1, -1, nullptr, off[SL_R2]}});
+    coef(5);
+  }
+};
+
+Solver* make_solver(int m) {
+  switch (m) {
+    case M_LI_BICG: { auto* p = new GlBiCG(); p->li = true; return p; }
+    case M_GL_BICG: return new GlBiCG();
+    case M_EGL_BICG: return new EglBiCG();
+    case M_BL_BICG: return new BlBiCG();
+    case M_BL_BICG_RQ: return new BlBiCGrQ();
+    case M_LI_QMR: { auto* p = new QMR(); p->mode = 0; return p; }
+    case M_GL_QMR: { auto* p = new QMR(); p->mode = 1; return p; }
+    case M_EGL_QMR: { auto* p = new QMR(); p->mode = 2; return p; }
+    case M_BL_QMR: return new BlQMR();
+    case M_LI_BICGSTAB: { auto* p = new GlBiCGStab(); p->li = true; return p; }
+    case M_GL_BICGSTAB: return new GlBiCGStab();
+    case M_BL_BICGSTAB: return new BlBiCGStab();
+    case M_BL_BICGSTAB_RQ: return new BlBiCGStabrQ();
+    default: return nullptr;
+  }
+}
+
+}  // namespace srk

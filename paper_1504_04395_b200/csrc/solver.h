@@ -1,0 +1,68 @@
+// solver.h — host drivers of the 13 methods.
+#pragma once
+#include <vector>
+
+#include "../../include/srk.h"
+#include "coef.cuh"
+#include "engine.h"
+
+namespace srk {
+
+int launch_coef(bool cplx, const CoefArgs& a, size_t smem, cudaStream_t st);
+int launch_end_iter(int* ctl, cudaStream_t st);
+
+struct Solver {
+  Ctx* c = nullptr;
+  const Mat* A = nullptr;
+  int s = 0, method = 0;
+  bool cplx = false;
+  long long n = 0;
+  srk_opts o{};
+  Eng e;
+  Prof prof;
+  double* ws = nullptr;
+  int* ctl = nullptr;
+  int* ctl_host = nullptr;  // pinned mirror
+  double* hist = nullptr;
+  int hist_cap = 0;
+  int off[NSLOT];
+  std::vector<void*> owned;
+  void* B = nullptr;  // internal copy of the right-hand sides
+  void* X = nullptr;  // iterate
+  void* R = nullptr;  // residual block
+  void* tmp = nullptr;
+  void* tmp2 = nullptr;
+  int host_iter = 0;
+  int state = 0;  // 0 running, 1 converged, 2 breakdown, 3 maxit
+  int half = 0;
+  int brk_kind = 0, brk_iter = -1, frozen = 0;
+  long long launches = 0;
+  double seconds = 0.0;
+  double final_true = -1.0, final_rec = -1.0;
+  int cols_A = 0, cols_AH = 0;  // per iteration (Prop. 1 counters)
+  long long matA = 0, matAH = 0;
+  bool started = false;
+
+  virtual ~Solver();
+  int setup();                 // allocate common state
+  void* blk();                 // allocate an n x s block
+  void* vecn();                // allocate an n-vector
+  int coef(int phase, int k1 = 0);
+  size_t esz() const { return cplx ? 16 : 8; }
+  int start(const void* Bd, const void* X0d);
+  int iterate(int k);
+  double true_rel(const void* Xc);  // sync
+  int read_ctl();
+
+  virtual int alloc() = 0;
+  virtual int init() = 0;          // R holds R0, ws[SL_R0N2] = ||R0||^2 after the common start
+  virtual void seg(int idx) = 0;   // enqueue segment idx of one iteration
+  virtual int nseg() const { return 1; }
+  virtual void half_x(void* Xh) { (void)Xh; }
+  virtual bool is_rq() const { return false; }
+  virtual int residual(void* out, int64_t* rows);
+};
+
+Solver* make_solver(int method);
+
+}  // namespace srk

@@ -1,0 +1,157 @@
+"""GPU parity of the kernel-level C-ABI calls (srk_spmm_block, srk_gram_block,
+srk_block_update, srk_tsqr, the A^H build) against the oracle (oracle/linalg.py
+and scipy products), element by element, on seeded inputs spanning several
+CTAs and a ragged tail, plus empty rows."""
+import numpy as np
+import pytest
+
+import oracle.linalg as OL
+import synth
+from tests.gpu_util import csr_with_empty_rows, rel, to_dev, to_np
+
+pytestmark = pytest.mark.gpu
+
+S_LIST = [1, 2, 3, 4, 8, 12, 16, 19, 32, 64]
+
+
+@pytest.fixture(scope="module")
+def srk():
+    import paper_1504_04395_b200 as srk
+    srk.load_library()
+    return srk
+
+
+def _rand(rng, n, s, cplx):
+    X = rng.standard_normal((n, s))
+    if cplx:
+        X = X + 1j * rng.standard_normal((n, s))
+    return X
+
+
+@pytest.mark.parametrize("cplx", [False, True])
+@pytest.mark.parametrize("s", S_LIST)
+def test_spmm_matches_scipy(srk, s, cplx):
+    A = csr_with_empty_rows(5003, seed=s, cplx=cplx)
+    M = srk.Matrix.from_csr(A)
+    rng = np.random.default_rng(s)
+    P = _rand(rng, A.shape[0], s, cplx)
+    Q = to_np(srk.spmm_block(M, to_dev(P)))
+    ref = A @ P
+    # summation order of one row differs at most by nnz_row * eps
+    assert np.max(np.abs(Q - ref)) <= 1e-13 * max(1.0, np.max(np.abs(ref)))
+    QH = to_np(srk.spmm_block(M, to_dev(P), adjoint=True))
+    refH = A.conj().T @ P
+    assert np.max(np.abs(QH - refH)) <= 1e-13 * max(1.0, np.max(np.abs(refH)))
+
+
+@pytest.mark.parametrize("cplx", [False, True])
+def test_adjoint_is_conj_transpose(srk, cplx):
+    A = csr_with_empty_rows(2001, seed=5, cplx=cplx)
+    M = srk.Matrix.from_csr(A)
+    rp, ci, va = (to_np(t) for t in M.adjoint_csr())
+    AH = A.conj().T.tocsr()
+    AH.sort_indices()
+    assert np.array_equal(rp, AH.indptr) and np.array_equal(ci, AH.indices)
+    assert np.array_equal(va, AH.data)  # a pure permutation + conjugation: bit-exact
+
+
+@pytest.mark.parametrize("cplx", [False, True])
+@pytest.mark.parametrize("s", [1, 3, 4, 8, 12, 16])
+@pytest.mark.parametrize("mode", ["norm2", "colnorm2", "diag", "trace", "sumvec", "full"])
+def test_spmm_fused_reductions(srk, s, cplx, mode):
+    A = synth.random_sparse(3001, 6, seed=2, dtype=np.complex128 if cplx else np.float64).to_scipy()
+    M = srk.Matrix.from_csr(A)
+    rng = np.random.default_rng(7)
+    P = _rand(rng, A.shape[0], s, cplx)
+    Y = _rand(rng, A.shape[0], s, cplx)
+    y = Y[:, 0].copy()
+    Yd = to_dev(y) if mode == "sumvec" else to_dev(Y)
+    Q, g = srk.spmm_block(M, to_dev(P), gram=mode, Y=Yd)
+    Q = to_np(Q)
+    g = to_np(g)
+    ref = {
+        "norm2": lambda: np.array([OL.fro2(Q)]),
+        "colnorm2": lambda: np.real(OL.col_inner(Q, Q)),
+        "diag": lambda: OL.col_inner(Q, Y),
+        "trace": lambda: np.array([OL.trace_inner(Q, Y)]),
+        "sumvec": lambda: np.array([OL.sum_inner(y, Q)]),
+        "full": lambda: OL.gram(Y, Q),
+    }[mode]()
+    assert rel(g.reshape(ref.shape), ref) < 1e-12
+
+
+@pytest.mark.parametrize("cplx", [False, True])
+@pytest.mark.parametrize("s", [1, 2, 5, 8, 16])
+def test_gram_block(srk, s, cplx):
+    rng = np.random.default_rng(11)
+    n = 10007
+    X, Y = _rand(rng, n, s, cplx), _rand(rng, n, s, cplx)
+    g = to_np(srk.gram_block(to_dev(X), to_dev(Y), "full"))
+    assert rel(g, OL.gram(Y, X)) < 1e-12
+    t = to_np(srk.gram_block(to_dev(X), to_dev(Y), "trace"))
+    assert abs(t[0] - OL.trace_inner(X, Y)) <= 1e-12 * abs(OL.trace_inner(X, Y))
+
+
+@pytest.mark.parametrize("cplx", [False, True])
+@pytest.mark.parametrize("s", [1, 4, 7, 12, 16])
+@pytest.mark.parametrize("kind", ["scalar", "diag", "full"])
+def test_block_update(srk, s, cplx, kind):
+    rng = np.random.default_rng(13)
+    n = 4099
+    Y, X = _rand(rng, n, s, cplx), _rand(rng, n, s, cplx)
+    coef = {"scalar": _rand(rng, 1, 1, cplx)[0], "diag": _rand(rng, 1, s, cplx)[0], "full": _rand(rng, s, s, cplx)}[kind]
+    out = to_np(srk.block_update(to_dev(Y), to_dev(X), to_dev(coef), kind, sign=-1))
+    ref = Y - (X @ coef if kind == "full" else X * coef)
+    assert np.max(np.abs(out - ref)) <= 1e-13 * np.max(np.abs(ref))
+
+
+@pytest.mark.parametrize("cplx", [False, True])
+@pytest.mark.parametrize("s", [1, 3, 8, 16])
+def test_tsqr_matches_oracle(srk, s, cplx):
+    rng = np.random.default_rng(17)
+    Z = _rand(rng, 20011, s, cplx)
+    Q, C, rank = srk.tsqr(to_dev(Z))
+    Q, C = to_np(Q), to_np(C)
+    Qo, Co = OL.thin_qr(Z)
+    assert rank == s
+    assert rel(C, Co) < 1e-12 and rel(Q, Qo) < 1e-12
+    assert np.linalg.norm(Q.conj().T @ Q - np.eye(s)) < 1e-12
+
+
+def test_tsqr_rank_deficient(srk):
+    rng = np.random.default_rng(19)
+    w = rng.standard_normal((3000, 1))
+    _, _, rank = srk.tsqr(to_dev(np.hstack([w, 2 * w, rng.standard_normal((3000, 1))])))
+    assert rank < 3
+
+
+def test_invalid_csr_rejected(srk):
+    import torch
+    rp = torch.tensor([0, 2, 3], dtype=torch.int64)
+    ci = torch.tensor([1, 0, 1], dtype=torch.int32)  # row 0 unsorted
+    va = torch.ones(3, dtype=torch.float64)
+    with pytest.raises(srk.SrkError):
+        srk.Matrix(rp, ci, va)
+    with pytest.raises(srk.SrkError):
+        srk.Matrix(rp, torch.tensor([0, 5, 1], dtype=torch.int32), va)  # column out of range
+
+
+def test_full_size_config3_spmm_sampled(srk):
+    """Config 3 at full size (n = 256^3, s = 16) in the bench launch configuration:
+    sampled rows of A P against the oracle, and the fused trace against numpy."""
+    import torch
+    A, B = synth.make_config(3)
+    M = srk.Matrix.from_csr(A, need_adjoint=False)
+    Bd = to_dev(B)
+    Rt = to_dev(synth.random_rhs(A.n, 16, 99))
+    Q, tr = srk.spmm_block(M, Bd, gram="trace", Y=Rt)
+    rows = np.random.default_rng(0).choice(A.n, 4096, replace=False)
+    rows.sort()
+    As = A.to_scipy()
+    ref = As[rows] @ B
+    Qs = to_np(Q[torch.from_numpy(rows).cuda()])
+    assert np.max(np.abs(Qs - ref)) <= 1e-13 * np.max(np.abs(ref))
+    Rtn = to_np(Rt)
+    full = As @ B
+    t_ref = np.vdot(Rtn.ravel(), full.ravel())
+    assert abs(to_np(tr)[0] - t_ref) <= 1e-11 * np.linalg.norm(full) * np.linalg.norm(Rtn)
