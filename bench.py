@@ -1,0 +1,325 @@
+#!/usr/bin/env python
+"""bench.py — RHS·iterations/s of the simultaneous-RHS Krylov hot path on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--method egl_qmr] [--config 3] [--m 256]
+
+A "step" is one full iteration of the method (every §8(a) row of SURVEY.md:
+SpMM A·P with the fused Gram epilogue, the A^H vector product, the fused block
+updates with their reductions, the s x s device coefficient phases and the
+convergence test) over config 3 of BASELINE.json (3D 7-point convection-
+diffusion 256^3, n = 16.8M, 117M nnz, FP64, s = 16 Gaussian RHS from seed 2),
+method eGl-QMR. Inputs are resident in HBM before the
+timed region; every block is 2.1 GB, far larger than the 126 MB L2, so no L2
+flush is needed between steps.
+
+One JSON line on rank 0 with: value (whole-job RHS·it/s), e2e (the same metric
+through srk_solve_host with host B/X, copies inside the timed region),
+roofline (the dominant kernel — the fused SpMM+Gram — timed live with CUDA
+events inside the timed region), cpu_baseline (the oracle on a bounded sample:
+one config-3 iteration on the host cores), clocks (nvidia-smi during the
+timed region), gpu_launches (kernels in the timed region).
+
+--impl reference times the oracle (oracle/, numpy/scipy on the host cores) on
+the same workload: each step is one oracle iteration, W+K of them.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "RHS·iterations/sec (SpMM+Gram achieved HBM GB/s in roofline)"
+UNIT = "RHS·it/s"
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region (B200_PROFILING.md)."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, uuid: str | None):
+        self.uuid = uuid
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        cmd = ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms", "200"]
+        if self.uuid:
+            cmd += ["-i", self.uuid]
+        try:
+            self.proc = subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 6:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def algorithmic_spmm_bytes(A, s, esz, operand_bytes):
+    """A's arrays once (int32 row_ptr / col, values), P read once,
+    Q written once, plus the Gram operand (here the eGl shadow vector q)."""
+    return (A.n + 1) * 4 + A.nnz * 4 + A.nnz * esz + 2 * A.n * s * esz + operand_bytes
+
+
+def iteration_bytes_egl_qmr(A, s, esz):
+    """Algorithmic bytes of one eGl-QMR iteration in this build's phase plan
+    (DESIGN.md §Kernels): blocks moved B = n*s*esz, vectors v = n*esz."""
+    B = A.n * s * esz
+    v = A.n * esz
+    a_bytes = (A.n + 1) * 4 + A.nnz * (4 + esz)
+    # V,W scale (Vt r, V w) 2B + 2v ; P,q update (V r, P rw) 3B + 3v ; SpMM (P r, Pt w, q r) 2B + v + A ;
+    # A^H q (q r, AHq w) 2v + A^H ; Vt (Pt r, V r, Vt w) 3B ; Wt (AHq, w r, wt w) 3v ;
+    # D,S,X,R (P,D,Pt,S,X,R r; D,S,X,R w) 10B
+    return 20 * B + 12 * v + 2 * a_bytes
+
+
+def oracle_iteration_rate(method, A, B, iters: int):
+    """Time the oracle (as it stands) per iteration via timestamps of its A-products."""
+    import scipy.sparse as sp
+
+    import oracle
+    stamps = []
+
+    class TimedCSR(sp.csr_matrix):
+        def __matmul__(self, other):
+            stamps.append(time.perf_counter())
+            return super().__matmul__(other)
+
+    As = TimedCSR((A.values, A.col_idx, A.row_ptr), shape=(A.n, A.n))
+    t0 = time.perf_counter()
+    oracle.solve(method, As, B, tol=1e-300, maxit=iters, record=0)
+    total = time.perf_counter() - t0
+    per_it_products = 2 if "bicgstab" in method else 1
+    # stamps: [R0, it1 (x per_it), it2, ..., final true residual]
+    it_starts = stamps[1:1 + iters * per_it_products:per_it_products] + [stamps[-1]]
+    durs = np.diff(it_starts)
+    return durs, total
+
+
+def cpu_info():
+    model = ""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    try:
+        from threadpoolctl import threadpool_info
+        th = max((d.get("num_threads", 1) for d in threadpool_info()), default=1)
+    except Exception:
+        th = os.cpu_count()
+    return model, th
+
+
+def run_reference(args, A, B, s, cfgd):
+    # one oracle iteration of config 3 takes ~10 s on the host: bound the sample
+    # to <= 3 timed iterations after 1 warm-up so the run ends within minutes
+    steps, warm = min(args.steps, 3), min(args.warmup, 1)
+    durs, total = oracle_iteration_rate(args.method, A, B, warm + steps)
+    timed = durs[warm:warm + steps] if len(durs) >= warm + steps else durs[-steps:]
+    T = float(np.sum(timed))
+    value = s * len(timed) / T
+    model, th = cpu_info()
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": len(timed), "warmup": warm, "ms_per_step": 1e3 * T / len(timed), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": cfgd,
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": th, "kind": "oracle",
+                         "sample": f"{len(timed)} oracle iterations of {args.method} on the full workload "
+                                   f"(numpy/scipy; scipy.sparse products single-threaded), CPU {model}"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--method", default="egl_qmr")
+    ap.add_argument("--config", type=int, default=3)
+    ap.add_argument("--m", type=int, default=None, help="override the grid size (tests)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    import synth
+    A, B = synth.make_config(args.config, m=args.m)
+    s = B.shape[1]
+    esz = 16 if np.iscomplexobj(B) else 8
+    c = synth.CONFIGS[args.config]
+    cfgd = {"workload": f"{c['name']} ({'m=%d' % (args.m or c.get('m', 0))}) {args.method}",
+            "method": args.method, "n": A.n, "nnz": A.nnz, "s": s, "dtype": c["dtype"],
+            "parallelism": "replicas" if world > 1 else "single",
+            "l2": "no flush: every n x s block (%.2f GB) exceeds the 126 MB L2" % (A.n * s * esz / 1e9),
+            "inputs_hash": synth.input_hash(A, B)}
+
+    if args.impl == "reference":
+        if rank == 0:
+            run_reference(args, A, B, s, cfgd)
+        return
+
+    import torch
+    import paper_1504_04395_b200 as srk
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    dev = torch.device("cuda", torch.cuda.current_device())
+    srk.load_library()
+    M = srk.Matrix.from_csr(A, need_adjoint=srk.NEEDS_ADJOINT[args.method])
+    Bd = torch.from_numpy(B).to(dev)
+    K, W = args.steps, args.warmup
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+            torch.cuda.synchronize()
+
+    # ---- device-resident timed region
+    sv = srk.Solver(M, s, args.method, tol=1e-300, maxit=W + K + 1, poll_every=W + K + 1,
+                    check_true_residual=False)
+    sv.start(Bd)
+    sv.iterate(W)
+    l0 = sv.report().kernel_launches
+    uuid = None
+    try:
+        uuid = str(torch.cuda.get_device_properties(dev).uuid)
+        uuid = uuid if uuid.startswith("GPU-") else "GPU-" + uuid
+    except Exception:
+        pass
+    clk = ClockSampler(uuid)
+    barrier()
+    clk.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sv.profile(True)
+    e0.record()
+    st = sv.iterate(K)
+    e1.record()
+    torch.cuda.synchronize()
+    clocks = clk.stop()
+    ms = e0.elapsed_time(e1)
+    prof = sv.profile_read()
+    rep = sv.report()
+    launches = rep.kernel_launches - l0
+    assert st == 0 and rep.iterations == W + K, (st, rep)
+    if world > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    value = world * s * K / (ms / 1e3)
+
+    # ---- roofline of the dominant kernel (SpMM A·P + fused Gram), timed live
+    spmm_ms, spmm_n = prof["spmm"]
+    operand = A.n * esz if args.method.startswith("egl") else A.n * s * esz
+    alg = algorithmic_spmm_bytes(A, s, esz, operand)
+    avg_s = spmm_ms / 1e3 / max(spmm_n, 1)
+    peak, peak_src = peaks()
+    achieved = alg / avg_s / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        traffic = json.load(open(tp)).get(f"cfg{args.config}_{args.method}_spmm")
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "traffic": traffic, "kernel": "spmm_kernel<double,16> (A·P + fused sum(q^H P~) partials)",
+            "algorithmic_bytes_per_launch": alg, "avg_launch_ms": avg_s * 1e3, "launches": spmm_n,
+            "share_of_step": spmm_ms / ms, "peak_source": peak_src}
+    it_bytes = iteration_bytes_egl_qmr(A, s, esz) if args.method == "egl_qmr" else None
+    breakdown = {k: {"ms_total": v[0], "launches": v[1]} for k, v in prof.items()}
+
+    # ---- end to end through the C-ABI with host buffers (pinned)
+    e2e = None
+    if not args.no_e2e:
+        Bh = torch.from_numpy(B).pin_memory()
+        Xh = torch.zeros_like(Bh).pin_memory()
+        barrier()
+        t0 = time.perf_counter()
+        X, r2 = srk.solve_host(M, Bh.numpy(), args.method, tol=1e-300, maxit=K, X0=Xh.numpy(), poll_every=K + 1)
+        T = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([T], device=dev, dtype=torch.float64)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            T = float(t.item())
+        nbytes = B.nbytes
+        e2e = {"value": world * s * r2.iterations / T, "unit": UNIT, "h2d_bytes_per_step": 2 * nbytes / K,
+               "d2h_bytes_per_step": nbytes / K,
+               "note": "srk_solve_host: H2D of B and X0, solver setup (R0 = B - A X0), K iterations, D2H of X"}
+
+    # ---- CPU baseline: the oracle on one config-3 iteration (rank 0, N = 1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        durs, total = oracle_iteration_rate(args.method, A, B, 2)
+        model, th = cpu_info()
+        cpu = {"value": s / float(durs[-1]), "unit": UNIT, "cores": th, "kind": "oracle",
+               "sample": f"iteration 2 of {args.method} on the full config-{args.config} workload "
+                         f"({durs[-1]:.1f} s; oracle call {total:.1f} s incl. setup), CPU {model}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
+            "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64" if esz == 8 else "c128", "data": "synthetic", "config": cfgd,
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks,
+            "iteration": {"algorithmic_bytes": it_bytes,
+                          "achieved_gbs": (it_bytes / (ms / K / 1e3) / 1e9) if it_bytes else None,
+                          "frac_of_peak": (it_bytes / (ms / K / 1e3) / 1e9 / peak) if it_bytes else None,
+                          "kernel_breakdown": breakdown},
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -401,12 +401,18 @@ __global__ void fin_kernel(FinArgs a) {
 // ============================================================================
 // Host-side launchers (explicit instantiation per capacity S)
 // ============================================================================
+// grid < 0: return the number of resident CTAs per SM instead of launching
 template <typename T, int S, bool FC>
 static int launch_spmm_t(const SpmmArgs& a, int grid, int block, size_t smem, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(spmm_kernel<T, S, FC>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
+  }
+  if (grid < 0) {
+    int nb = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, spmm_kernel<T, S, FC>, block, smem);
+    return nb;
   }
   spmm_kernel<T, S, FC><<<grid, block, smem, st>>>(a);
   return (int)cudaGetLastError();
@@ -417,6 +423,11 @@ static int launch_upd_t(const UpdArgs& a, int grid, int block, size_t smem, cuda
   if (!attr) {
     cudaFuncSetAttribute(upd_kernel<T, S, FC>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
+  }
+  if (grid < 0) {
+    int nb = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, upd_kernel<T, S, FC>, block, smem);
+    return nb;
   }
   upd_kernel<T, S, FC><<<grid, block, smem, st>>>(a);
   return (int)cudaGetLastError();

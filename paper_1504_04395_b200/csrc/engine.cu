@@ -52,12 +52,22 @@ Prof::~Prof() {
   for (auto e : ev) cudaEventDestroy(e);
 }
 
-int Eng::grid_for(int cap, bool full) const {
+// Persistent-style grid: exactly one wave, i.e. the SM count times the number of
+// CTAs the occupancy calculator says are resident for this kernel instance (so
+// no partial second wave), or fewer CTAs when n is small.
+int Eng::grid_for(int cap, bool full, bool is_spmm, size_t smem) const {
   const long long rpc = rows_per_cta(cap, cplx);
   long long need = (n + rpc - 1) / rpc;
-  // persistent-style grid: a multiple of the SM count (4 x 256-thread CTAs per SM,
-  // 2 when the s x s Gram accumulators are live)
-  const long long maxg = (long long)c->nsm * (full ? 2 : 4);
+  static int occ_cache[2][2][2][65] = {};
+  int& occ = occ_cache[is_spmm][cplx][full][cap];
+  if (occ == 0) {
+    SpmmArgs sa{};
+    UpdArgs ua{};
+    occ = is_spmm ? launch_spmm(cplx, cap, full, sa, -1, 256, smem, nullptr)
+                  : launch_upd(cplx, cap, full, ua, -1, 256, smem, nullptr);
+    if (occ < 1) occ = 1;
+  }
+  const long long maxg = (long long)c->nsm * occ;
   if (need < 1) need = 1;
   return (int)std::min(need, maxg);
 }
@@ -118,11 +128,11 @@ int Eng::spmm(bool adj, const void* P, void* Q, int s, std::vector<RQ> reds) {
     maxlen = std::max(maxlen, len);
   }
   a.pstride = std::max(pstride, 1);
-  const int grid = grid_for(cap, full);
+  const size_t smem = (size_t)8 * maxlen * sizeof(double);
+  const int grid = grid_for(cap, full, true, 8 * 2 * 8 * 16 * 16);  // occupancy at the largest epilogue smem
   if ((err = c->ensure_partials((size_t)grid * a.pstride))) return err;
   a.partials = c->partials;
   a.done = done;
-  const size_t smem = (size_t)8 * maxlen * sizeof(double);
   nlaunch++;
   if (prof) prof->begin(adj ? PT_SPMM_ADJ : PT_SPMM, c->st);
   err = launch_spmm(cplx, cap, full, a, grid, 256, smem, c->st);
@@ -175,11 +185,11 @@ int Eng::upd(int s, std::vector<const void*> in, std::vector<OutSpec> outs, std:
   a.s = s;
   a.vec = cplx ? 1 : (s % 2 == 0);
   a.done = done;
-  const int grid = grid_for(cap, full);
-  if ((err = c->ensure_partials((size_t)grid * a.pstride))) return err;
-  a.partials = c->partials;
   const size_t esz = cplx ? 16 : 8;
   const size_t smem = (size_t)cslot * esz + (size_t)8 * maxlen * sizeof(double);
+  const int grid = grid_for(cap, full, false, 48 * 1024);  // occupancy at a fixed smem budget (deterministic grid)
+  if ((err = c->ensure_partials((size_t)grid * a.pstride))) return err;
+  a.partials = c->partials;
   nlaunch++;
   if (prof) prof->begin(PT_UPD, c->st);
   err = launch_upd(cplx, cap, full, a, grid, 256, smem, c->st);

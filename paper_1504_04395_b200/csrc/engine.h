@@ -96,7 +96,7 @@ struct Eng {
   int nlaunch = 0;        // kernels launched (instrumentation)
   int spmm(bool adj, const void* P, void* Q, int s, std::vector<RQ> reds);
   int upd(int s, std::vector<const void*> in, std::vector<OutSpec> outs, std::vector<RQ> reds);
-  int grid_for(int cap, bool full) const;
+  int grid_for(int cap, bool full, bool is_spmm, size_t smem) const;
 };
 
 }  // namespace srk

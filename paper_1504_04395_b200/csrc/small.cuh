@@ -12,7 +12,11 @@
 namespace srk {
 
 constexpr double EPS_BRK = 1e-14;   // reading G12: LU pivot <= EPS_BRK * max|G| -> singular Gram
-constexpr double EPS_DEFL = 1e-12;  // reading G11: R_jj <= EPS_DEFL * ||Z||_F -> rank deficient
+constexpr double EPS_DEFL = 1e-12;  // reading G11: R_jj <= EPS_DEFL * ||Z||_F -> rank deficient (MGS2)
+// CholQR works on the Gram G = Z^H Z, whose pivots carry an absolute rounding error ~ eps * tr(G):
+// it flags rank deficiency when a pivot d_j <= EPS_CHOL * tr(G), i.e. a column norm below ~1e-7
+// relative — the resolution limit of CholQR (reading R5 in DESIGN.md).
+constexpr double EPS_CHOL = 1e-14;
 
 template <typename T> __device__ __forceinline__ T one();
 template <> __device__ __forceinline__ double one<double>() { return 1.0; }
@@ -182,8 +186,7 @@ __device__ int sm_solve(T* X, const T* G, const T* M, int n, int m, int herm, T*
 }
 
 // Upper Cholesky G = R^H R (n x n Hermitian positive definite). Rank test
-// (reading G11, same quantity as MGS2's diagonal): pivot d_j <= (EPS_DEFL*sqrt(tr G))^2
-// -> return 1. Single thread per column sweep (n <= 64).
+// (reading R5): pivot d_j <= EPS_CHOL * tr(G) -> return 1. Single thread (n <= 64).
 template <typename T>
 __device__ int sm_chol(T* R, const T* G, int n, int check_rank) {
   __shared__ int s_bad;
@@ -191,7 +194,7 @@ __device__ int sm_chol(T* R, const T* G, int n, int check_rank) {
     int bad = 0;
     double tr = 0.0;
     for (int i = 0; i < n; ++i) tr += re(G[i * n + i]);
-    const double thr = EPS_DEFL * EPS_DEFL * tr;
+    const double thr = EPS_CHOL * tr;
     for (int i = 0; i < n * n; ++i) R[i] = Ar<T>::zero();
     for (int j = 0; j < n && !bad; ++j) {
       // R_jj^2 = G_jj - sum_i |R_ij|^2
