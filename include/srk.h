@@ -113,6 +113,45 @@ int srk_matrix_destroy(srk_matrix* A);
 /* copy A^H back (CSR arrays of size n+1 / nnz, device pointers) — for tests */
 int srk_matrix_adjoint(const srk_matrix* A, int64_t* row_ptr, int32_t* col_idx, void* values);
 
+/* -------------------------------------------- a8: multi-GPU (one process per GPU) */
+/* Row partitioning and halo planning; HOST code, no GPU needed.
+ * srk_partition_rows: contiguous row ranges balanced by nnz, offsets[nranks+1].
+ * srk_plan_create: from the GLOBAL CSR (host arrays) the plan of `rank`: local CSR
+ * (rows offsets[rank]..offsets[rank+1]-1, owned columns renumbered to [0, n_local),
+ * ghost columns to n_local + position in the sorted ghost list, entries kept in the
+ * global order so values[row_ptr[off0] : row_ptr[off1]] apply unchanged), the ghost
+ * rows received per peer, and the owned rows sent to each peer. */
+typedef struct srk_plan srk_plan;
+int srk_partition_rows(int64_t n, const int64_t* row_ptr_host, int nranks, int64_t* offsets_host);
+int srk_plan_create(int64_t n, const int64_t* row_ptr_host, const int32_t* col_idx_host, int nranks,
+                    const int64_t* offsets_host, int rank, srk_plan** out);
+int srk_plan_sizes(const srk_plan* p, int64_t* n_local, int64_t* nnz_local, int64_t* n_ghost, int64_t* n_send);
+int srk_plan_arrays(const srk_plan* p, int64_t* row_ptr_local, int32_t* col_local, int64_t* ghost_global,
+                    int32_t* recv_counts, int32_t* send_counts, int32_t* send_local);
+int srk_plan_destroy(srk_plan* p);
+
+/* NCCL communicator of the context (NCCL resolved at run time): rank 0 calls
+ * srk_nccl_unique_id, broadcasts the 128 bytes (e.g. torch.distributed), every
+ * rank calls srk_comm_init. With a communicator every reduction of the solver is
+ * followed by an in-place FP64 ncclAllReduce and every SpMM by a halo exchange. */
+int srk_nccl_unique_id(void* id128_host);
+int srk_comm_init(srk_ctx* ctx, const void* id128_host, int nranks, int rank);
+
+/* halo of one local operator (host arrays): rows received from / sent to each peer */
+typedef struct {
+  const int32_t* recv_counts; /* nranks: ghost rows from each peer (sum = n_ghost) */
+  const int32_t* send_counts; /* nranks */
+  const int32_t* send_local;  /* n_send local row indices, grouped by peer */
+  int64_t n_send;
+} srk_halo;
+/* Distributed operator: local rows of A (columns < n_local + n_ghost, device CSR)
+ * and optionally of A^H with its own halo. Every n x s block passed to this
+ * operator's SpMM must hold n_local + n_ghost rows (the ghost tail is written by
+ * the halo exchange); the solver allocates its blocks that way. */
+int srk_matrix_create_dist(srk_ctx* ctx, const srk_csr* A_local, int64_t n_ghost, const srk_halo* halo,
+                           const srk_csr* AH_local, int64_t n_ghost_adj, const srk_halo* halo_adj,
+                           srk_matrix** out);
+
 /* ------------------------------------------------------ kernel-level calls */
 /* Q = op(A) P, op = A (adjoint = 0) or A^H (adjoint = 1, needs need_adjoint),
  * P, Q: n x s row-major (a1/a2). If gram != SRK_GRAM_NONE the
@@ -120,8 +159,8 @@ int srk_matrix_adjoint(const srk_matrix* A, int64_t* row_ptr, int32_t* col_idx, 
  * is fused into the epilogue and written to gram_out (device, dtype values):
  *   NORM2: ||Q||_F^2 (1 double); COLNORM2: s doubles; DIAG: (y_c^H q_c)_c (s);
  *   TRACE: tr(Y^H Q) (1); SUMVEC: sum(y^H Q) (1); FULL: Y^H Q (s x s).
- * Errors: SRK_EDIM (s < 1 or s > 64), SRK_EUNSUPPORTED (FULL with s > 32 real /
- * 16 complex, adjoint without A^H). */
+ * Errors: SRK_EDIM (s < 1 or s > 64), SRK_EUNSUPPORTED (FULL with s > 16,
+ * adjoint without A^H). */
 int srk_spmm_block(srk_ctx* ctx, const srk_matrix* A, int adjoint, const void* P, void* Q, int s,
                    int gram, const void* Y, void* gram_out);
 

@@ -33,7 +33,8 @@ EXPORTS = ("srk_create", "srk_destroy", "srk_last_error", "srk_version", "srk_ma
            "srk_block_update", "srk_tsqr", "srk_solve", "srk_solve_host", "srk_solver_create",
            "srk_solver_destroy", "srk_solver_start", "srk_solver_iterate", "srk_solver_get_x",
            "srk_solver_get_residual", "srk_solver_report", "srk_solver_history", "srk_solver_profile",
-           "srk_solver_profile_read")
+           "srk_solver_profile_read", "srk_partition_rows", "srk_plan_create", "srk_plan_sizes", "srk_plan_arrays",
+           "srk_plan_destroy", "srk_nccl_unique_id", "srk_comm_init", "srk_matrix_create_dist")
 
 
 class SrkError(RuntimeError):
@@ -48,6 +49,11 @@ class _Csr(ctypes.Structure):
 class _Opts(ctypes.Structure):
     _fields_ = [("tol", ctypes.c_double), ("maxit", ctypes.c_int), ("poll_every", ctypes.c_int),
                 ("record_history", ctypes.c_int), ("check_true_residual", ctypes.c_int)]
+
+
+class _Halo(ctypes.Structure):
+    _fields_ = [("recv_counts", ctypes.c_void_p), ("send_counts", ctypes.c_void_p), ("send_local", ctypes.c_void_p),
+                ("n_send", ctypes.c_int64)]
 
 
 class _Report(ctypes.Structure):
@@ -96,6 +102,15 @@ def load_library(path: str | None = None):
         "srk_solver_history": ([vp, ctypes.POINTER(d), i], i),
         "srk_solver_profile": ([vp, i], i),
         "srk_solver_profile_read": ([vp, ctypes.POINTER(d), ctypes.POINTER(i64), i], i),
+        "srk_partition_rows": ([i64, vp, i, vp], i),
+        "srk_plan_create": ([i64, vp, vp, i, vp, i, ctypes.POINTER(vp)], i),
+        "srk_plan_sizes": ([vp, ctypes.POINTER(i64), ctypes.POINTER(i64), ctypes.POINTER(i64), ctypes.POINTER(i64)], i),
+        "srk_plan_arrays": ([vp, vp, vp, vp, vp, vp, vp], i),
+        "srk_plan_destroy": ([vp], i),
+        "srk_nccl_unique_id": ([vp], i),
+        "srk_comm_init": ([vp, vp, i, i], i),
+        "srk_matrix_create_dist": ([vp, ctypes.POINTER(_Csr), i64, ctypes.POINTER(_Halo), ctypes.POINTER(_Csr), i64,
+                                    ctypes.POINTER(_Halo)], i),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -211,6 +226,145 @@ class Matrix:
         _check(_lib.srk_matrix_adjoint(self.h, ctypes.c_void_p(rp.data_ptr()), ctypes.c_void_p(ci.data_ptr()),
                                        ctypes.c_void_p(va.data_ptr())), "srk_matrix_adjoint")
         return rp, ci, va
+
+    def close(self):
+        if getattr(self, "h", None):
+            _lib.srk_matrix_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+# ------------------------------------------------------------------ multi-GPU
+def _np_ptr(a):
+    return ctypes.c_void_p(a.ctypes.data)
+
+
+def partition_rows(row_ptr, nranks: int) -> np.ndarray:
+    """Contiguous row ranges balanced by nnz (host; srk_partition_rows)."""
+    lib = load_library()
+    rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
+    off = np.zeros(nranks + 1, dtype=np.int64)
+    _check(lib.srk_partition_rows(rp.size - 1, _np_ptr(rp), nranks, _np_ptr(off)), "srk_partition_rows")
+    return off
+
+
+@dataclass
+class Plan:
+    """Halo plan of one rank (srk_plan_*): local CSR pattern, ghosts, send lists."""
+    n_local: int
+    row_ptr: np.ndarray
+    col: np.ndarray
+    ghosts: np.ndarray
+    recv_counts: np.ndarray
+    send_counts: np.ndarray
+    send_local: np.ndarray
+    off0: int
+    off1: int
+
+
+def make_plan(row_ptr, col_idx, offsets, rank: int) -> Plan:
+    lib = load_library()
+    rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
+    ci = np.ascontiguousarray(col_idx, dtype=np.int32)
+    off = np.ascontiguousarray(offsets, dtype=np.int64)
+    nr = off.size - 1
+    h = ctypes.c_void_p()
+    _check(lib.srk_plan_create(rp.size - 1, _np_ptr(rp), _np_ptr(ci), nr, _np_ptr(off), rank, ctypes.byref(h)),
+           "srk_plan_create")
+    try:
+        nl, nz, ng, ns = (ctypes.c_int64() for _ in range(4))
+        _check(lib.srk_plan_sizes(h, ctypes.byref(nl), ctypes.byref(nz), ctypes.byref(ng), ctypes.byref(ns)),
+               "srk_plan_sizes")
+        prl = np.zeros(nl.value + 1, np.int64)
+        col = np.zeros(max(nz.value, 1), np.int32)
+        gh = np.zeros(max(ng.value, 1), np.int64)
+        rc = np.zeros(nr, np.int32)
+        sc = np.zeros(nr, np.int32)
+        sl = np.zeros(max(ns.value, 1), np.int32)
+        _check(lib.srk_plan_arrays(h, _np_ptr(prl), _np_ptr(col), _np_ptr(gh), _np_ptr(rc), _np_ptr(sc), _np_ptr(sl)),
+               "srk_plan_arrays")
+    finally:
+        lib.srk_plan_destroy(h)
+    return Plan(nl.value, prl, col[:nz.value], gh[:ng.value], rc, sc, sl[:ns.value], int(off[rank]),
+                int(off[rank + 1]))
+
+
+def init_distributed(ctx: "Context | None" = None):
+    """Create the context's NCCL communicator over the torch.distributed world
+    (one process per GPU): rank 0 draws the unique id, broadcast as bytes."""
+    import torch.distributed as dist
+    ctx = ctx or default_context()
+    world, rank = dist.get_world_size(), dist.get_rank()
+    buf = (ctypes.c_char * 128)()
+    if rank == 0:
+        _check(_lib.srk_nccl_unique_id(buf), "srk_nccl_unique_id")
+    obj = [bytes(buf)]
+    dist.broadcast_object_list(obj, src=0)
+    ctypes.memmove(buf, obj[0], 128)
+    _check(_lib.srk_comm_init(ctx.h, buf, world, rank), "srk_comm_init")
+    return ctx
+
+
+class DistMatrix:
+    """srk_matrix_create_dist: this rank's rows of A (and of A^H) with halo plans."""
+
+    def __init__(self, A, offsets, rank: int, need_adjoint: bool = True, ctx: "Context | None" = None):
+        import scipy.sparse as sp
+        torch = _torch()
+        self.ctx = ctx or default_context()
+        dev = torch.device("cuda", self.ctx.device)
+        if hasattr(A, "indptr"):
+            rp, ci, va, n = A.indptr, A.indices, A.data, A.shape[0]
+        else:
+            rp, ci, va, n = A.row_ptr, A.col_idx, A.values, A.n
+        self.offsets = np.asarray(offsets, np.int64)
+        self.rank = rank
+        self.plan = make_plan(rp, ci, self.offsets, rank)
+        self.n_local = self.plan.n_local
+        self.n_ghost = self.plan.ghosts.size
+        self.dtype = torch.from_numpy(np.asarray(va[:1])).dtype
+        keep = []
+
+        def csr_struct(plan, vals):
+            t_rp = torch.from_numpy(plan.row_ptr).to(dev)
+            t_ci = torch.from_numpy(plan.col).to(dev)
+            t_va = torch.from_numpy(np.ascontiguousarray(vals)).to(dev)
+            keep.extend([t_rp, t_ci, t_va])
+            return _Csr(plan.n_local, plan.col.size, t_rp.data_ptr(), t_ci.data_ptr(), t_va.data_ptr(),
+                        _dtype_code(t_va))
+
+        def halo_struct(plan):
+            keep.extend([plan.recv_counts, plan.send_counts, plan.send_local])
+            return _Halo(plan.recv_counts.ctypes.data, plan.send_counts.ctypes.data,
+                         plan.send_local.ctypes.data if plan.send_local.size else None, plan.send_local.size)
+
+        lo, hi = int(rp[self.plan.off0]), int(rp[self.plan.off1])
+        csrA = csr_struct(self.plan, va[lo:hi])
+        haloA = halo_struct(self.plan)
+        csrH = haloH = None
+        ngH = 0
+        if need_adjoint:
+            AH = sp.csr_matrix((va, ci, rp), shape=(n, n)).conj().T.tocsr()
+            AH.sort_indices()
+            self.planH = make_plan(AH.indptr, AH.indices, self.offsets, rank)
+            lo, hi = int(AH.indptr[self.planH.off0]), int(AH.indptr[self.planH.off1])
+            csrH = csr_struct(self.planH, AH.data[lo:hi])
+            haloH = halo_struct(self.planH)
+            ngH = self.planH.ghosts.size
+        h = ctypes.c_void_p()
+        _check(_lib.srk_matrix_create_dist(self.ctx.h, ctypes.byref(csrA), self.n_ghost, ctypes.byref(haloA),
+                                           ctypes.byref(csrH) if csrH else None, ngH,
+                                           ctypes.byref(haloH) if haloH else None, ctypes.byref(h)),
+               "srk_matrix_create_dist")
+        torch.cuda.synchronize()
+        self.h = h
+        self.n = self.n_local
+        self.has_adjoint = need_adjoint
 
     def close(self):
         if getattr(self, "h", None):

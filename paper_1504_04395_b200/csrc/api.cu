@@ -56,6 +56,7 @@ int srk_create(srk_ctx** out, int device, void* stream) {
 int srk_destroy(srk_ctx* ctx) {
   if (!ctx) return SRK_OK;
   if (ctx->c.partials) cudaFree(ctx->c.partials);
+  if (ctx->c.comm) comm_destroy(ctx->c.comm);
   delete ctx;
   return SRK_OK;
 }
@@ -98,7 +99,7 @@ int srk_matrix_create(srk_ctx* ctx, const srk_csr* A, int need_adjoint, srk_matr
     cudaMemcpyAsync(m.ci, A->col_idx, sizeof(int) * m.nnz, cudaMemcpyDeviceToDevice, st);
     cudaMemcpyAsync(m.val, A->values, esz * m.nnz, cudaMemcpyDeviceToDevice, st);
   }
-  launch_csr_check(m.n, m.nnz, m.rp, m.ci, dbad, st);
+  launch_csr_check(m.n, m.n, m.nnz, m.rp, m.ci, 1, dbad, st);
   int bad = 0;
   cudaMemcpyAsync(&bad, dbad, sizeof(int), cudaMemcpyDeviceToHost, st);
   if ((e = cudaStreamSynchronize(st)) != cudaSuccess) {
@@ -138,6 +139,101 @@ int srk_matrix_create(srk_ctx* ctx, const srk_csr* A, int need_adjoint, srk_matr
   return SRK_OK;
 }
 
+// ---------------------------------------------------------------- multi-GPU
+int srk_nccl_unique_id(void* id128_host) {
+  if (!id128_host) return fail(SRK_EINVAL, "srk_nccl_unique_id: null buffer");
+  if (nccl_unique_id(id128_host)) return fail(SRK_ENCCL, "srk_nccl_unique_id: NCCL not available");
+  return SRK_OK;
+}
+
+int srk_comm_init(srk_ctx* ctx, const void* id128_host, int nranks, int rank) {
+  if (!ctx || !id128_host || nranks < 1 || rank < 0 || rank >= nranks) return fail(SRK_EINVAL, "srk_comm_init: bad argument");
+  if (ctx->c.comm) comm_destroy(ctx->c.comm);
+  ctx->c.comm = nullptr;
+  if (nranks == 1) return SRK_OK;
+  Comm* C = comm_create(id128_host, nranks, rank);
+  if (!C) return fail(SRK_ENCCL, "srk_comm_init: ncclCommInitRank failed (or NCCL not available)");
+  ctx->c.comm = C;
+  return SRK_OK;
+}
+
+static int upload_halo(Halo& H, const srk_halo* h, int nranks, long long n_ghost) {
+  H.nranks = nranks;
+  H.n_ghost = n_ghost;
+  H.n_send = h ? h->n_send : 0;
+  H.send_off = new int64_t[nranks + 1];
+  H.recv_off = new int64_t[nranks + 1];
+  H.send_off[0] = H.recv_off[0] = 0;
+  for (int p = 0; p < nranks; ++p) {
+    H.send_off[p + 1] = H.send_off[p] + (h ? h->send_counts[p] : 0);
+    H.recv_off[p + 1] = H.recv_off[p] + (h ? h->recv_counts[p] : 0);
+  }
+  if (H.send_off[nranks] != H.n_send || H.recv_off[nranks] != n_ghost) return SRK_EINVAL;
+  if (H.n_send > 0) {
+    if (cudaMalloc(&H.send_idx, sizeof(int) * H.n_send) != cudaSuccess) return SRK_ENOMEM;
+    if (cudaMemcpy(H.send_idx, h->send_local, sizeof(int) * H.n_send, cudaMemcpyHostToDevice) != cudaSuccess)
+      return SRK_ECUDA;
+  }
+  return SRK_OK;
+}
+
+static int upload_csr(Mat& m, const srk_csr* A, long long ncols, int** rp, int** ci, void** val, cudaStream_t st) {
+  const size_t esz = m.cplx ? 16 : 8;
+  int* dbad = nullptr;
+  if (cudaMalloc(rp, sizeof(int) * (A->n + 1)) != cudaSuccess || cudaMalloc(ci, sizeof(int) * (A->nnz + 1)) != cudaSuccess ||
+      cudaMalloc(val, esz * (A->nnz + 1)) != cudaSuccess || cudaMalloc(&dbad, sizeof(int)) != cudaSuccess) {
+    if (dbad) cudaFree(dbad);
+    return SRK_ENOMEM;
+  }
+  cudaMemsetAsync(dbad, 0, sizeof(int), st);
+  const int grid = (int)std::max<long long>(1, std::min<long long>((A->n + 256) / 256, 148 * 8));
+  rp64to32<<<grid, 256, 0, st>>>(A->row_ptr, *rp, A->n, dbad);
+  if (A->nnz > 0) {
+    cudaMemcpyAsync(*ci, A->col_idx, sizeof(int) * A->nnz, cudaMemcpyDeviceToDevice, st);
+    cudaMemcpyAsync(*val, A->values, esz * A->nnz, cudaMemcpyDeviceToDevice, st);
+  }
+  launch_csr_check(A->n, ncols, A->nnz, *rp, *ci, 0, dbad, st);
+  int bad = 0;
+  cudaMemcpyAsync(&bad, dbad, sizeof(int), cudaMemcpyDeviceToHost, st);
+  cudaError_t e = cudaStreamSynchronize(st);
+  cudaFree(dbad);
+  if (e != cudaSuccess) return SRK_ECUDA;
+  return bad ? SRK_EINVAL : SRK_OK;
+}
+
+int srk_matrix_create_dist(srk_ctx* ctx, const srk_csr* A, int64_t n_ghost, const srk_halo* halo, const srk_csr* AH,
+                           int64_t n_ghost_adj, const srk_halo* halo_adj, srk_matrix** out) {
+  if (!ctx || !A || !out || n_ghost < 0) return fail(SRK_EINVAL, "srk_matrix_create_dist: bad argument");
+  if (A->dtype != SRK_F64 && A->dtype != SRK_C128) return fail(SRK_EINVAL, "srk_matrix_create_dist: bad dtype");
+  const int nranks = ctx->c.comm ? ctx->c.comm->nranks : 1;
+  if ((n_ghost > 0 || (halo && halo->n_send > 0)) && nranks == 1)
+    return fail(SRK_EINVAL, "srk_matrix_create_dist: halo given but srk_comm_init was not called");
+  auto* M = new srk_matrix();
+  Mat& m = M->m;
+  m.ctx = &ctx->c;
+  m.n = A->n;
+  m.nnz = A->nnz;
+  m.cplx = A->dtype == SRK_C128;
+  m.dist = true;
+  int r = upload_csr(m, A, A->n + n_ghost, &m.rp, &m.ci, &m.val, ctx->c.st);
+  if (!r) r = upload_halo(m.halo, halo, nranks, n_ghost);
+  if (!r && AH) {
+    if (AH->n != A->n || AH->dtype != A->dtype) r = SRK_EDIM;
+    if (!r) r = upload_csr(m, AH, AH->n + n_ghost_adj, &m.rpH, &m.ciH, &m.valH, ctx->c.st);
+    if (!r) r = upload_halo(m.haloH, halo_adj, nranks, n_ghost_adj);
+    if (!r) {
+      m.has_adj = true;
+      m.nnzH = AH->nnz;
+    }
+  }
+  if (r) {
+    srk_matrix_destroy(M);
+    return fail(r, "srk_matrix_create_dist: invalid local CSR / halo (columns must be < n_local + n_ghost)");
+  }
+  *out = M;
+  return SRK_OK;
+}
+
 int srk_matrix_destroy(srk_matrix* M) {
   if (!M) return SRK_OK;
   Mat& m = M->m;
@@ -147,6 +243,12 @@ int srk_matrix_destroy(srk_matrix* M) {
   if (m.rpH) cudaFree(m.rpH);
   if (m.ciH) cudaFree(m.ciH);
   if (m.valH) cudaFree(m.valH);
+  for (Halo* H : {&m.halo, &m.haloH}) {
+    if (H->send_idx) cudaFree(H->send_idx);
+    delete[] H->send_off;
+    delete[] H->recv_off;
+  }
+  if (m.sendbuf) cudaFree(m.sendbuf);
   delete M;
   return SRK_OK;
 }
@@ -177,7 +279,7 @@ int srk_spmm_block(srk_ctx* ctx, const srk_matrix* A, int adjoint, const void* P
   if (gram != SRK_GRAM_NONE && (!gram_out || (gram != SRK_GRAM_NORM2 && gram != SRK_GRAM_COLNORM2 && !Y)))
     return fail(SRK_EINVAL, "srk_spmm_block: gram needs Y and gram_out");
   if (gram == SRK_GRAM_FULL && !full_supported(A->m.cplx, cap_for(s)))
-    return fail(SRK_EUNSUPPORTED, "srk_spmm_block: fused FULL Gram needs s <= 32 (real) / 16 (complex)");
+    return fail(SRK_EUNSUPPORTED, "srk_spmm_block: fused FULL Gram needs s <= 16");
   Eng e;
   e.c = &ctx->c;
   e.A = &A->m;
@@ -197,7 +299,7 @@ int srk_gram_block(srk_ctx* ctx, const void* X, const void* Y, int64_t n, int s,
   if (gram != SRK_GRAM_NORM2 && gram != SRK_GRAM_COLNORM2 && !Y) return fail(SRK_EINVAL, "srk_gram_block: Y needed");
   const bool cplx = dtype == SRK_C128;
   if (gram == SRK_GRAM_FULL && !full_supported(cplx, cap_for(s)))
-    return fail(SRK_EUNSUPPORTED, "srk_gram_block: FULL Gram needs s <= 32 (real) / 16 (complex)");
+    return fail(SRK_EUNSUPPORTED, "srk_gram_block: FULL Gram needs s <= 16");
   Eng e;
   e.c = &ctx->c;
   e.cplx = cplx;
@@ -254,7 +356,7 @@ int srk_tsqr(srk_ctx* ctx, const void* Z, void* Q, void* C, int64_t n, int s, in
   if (!ctx || !Z || !Q || !C) return fail(SRK_EINVAL, "srk_tsqr: null argument");
   if (s < 1 || s > 64 || n < s) return fail(SRK_EDIM, "srk_tsqr: need 1 <= s <= 64 and n >= s");
   const bool cplx = dtype == SRK_C128;
-  if (!full_supported(cplx, cap_for(s))) return fail(SRK_EUNSUPPORTED, "srk_tsqr: s <= 32 (real) / 16 (complex)");
+  if (!full_supported(cplx, cap_for(s))) return fail(SRK_EUNSUPPORTED, "srk_tsqr: s <= 16");
   TsqrSolver T;
   T.c = &ctx->c;
   T.s = s;
@@ -290,7 +392,7 @@ int srk_solver_create(srk_ctx* ctx, const srk_matrix* A, int s, int method, cons
   const bool block = method == SRK_BL_BICG || method == SRK_BL_BICG_RQ || method == SRK_BL_QMR ||
                      method == SRK_BL_BICGSTAB || method == SRK_BL_BICGSTAB_RQ;
   if (block && !full_supported(A->m.cplx, cap_for(s)))
-    return fail(SRK_EUNSUPPORTED, "srk_solver_create: block methods need s <= 32 (real) / 16 (complex)");
+    return fail(SRK_EUNSUPPORTED, "srk_solver_create: block methods need s <= 16");
   Solver* sv = make_solver(method);
   if (!sv) return fail(SRK_EINVAL, "srk_solver_create: unknown method");
   sv->c = &ctx->c;

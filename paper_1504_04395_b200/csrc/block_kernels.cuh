@@ -1,0 +1,571 @@
+// block_kernels.cuh — templates of the hot-path kernels over row-interleaved
+// n x s blocks (instantiated per dtype in blk_f64.cu / blk_c128.cu).
+//
+//  * spmm_kernel   Q = A P, CSR, one lane group per row, R rows per group in
+//                  flight: each nonzero a_ij is read once and applied to the s
+//                  contiguous values of P row j (PAPER.md P:66-74, P:128-132,
+//                  P:142-144), with the s x s / trace / sum /
+//                  diag Gram partials fused into the epilogue (
+//                  P:155-158, 178, 192-195, 243-249, 443-447).
+//  * upd_kernel    fused multi-output block updates out = sum_t src_t*coef_t with
+//                  scalar (Gl/eGl), diagonal (Li) or s x s (Bl, "BLAS3 GEMM"
+//                  P:290-297) coefficients read from device memory, plus fused
+//                  reductions. All NI inputs of R rows are
+//                  loaded before any arithmetic (memory-level parallelism).
+#pragma once
+#include "kernels.cuh"
+
+namespace srk {
+
+// Accumulators for one reduction held by one lane (capacity S).
+template <typename T, int S, bool FC>
+struct RedAcc {
+  using L = Lay<T, S>;
+  // FULL (FC) needs S x EPL values; the other modes use the first EPL.
+  static constexpr int N = FC ? S * L::EPL : L::EPL;
+  T v[N];
+  double r[L::EPL];  // NORM2 / COLNORM2
+};
+
+template <typename T, int S, bool FC>
+__device__ __forceinline__ void red_zero(RedAcc<T, S, FC>& a) {
+#pragma unroll
+  for (int i = 0; i < RedAcc<T, S, FC>::N; ++i) a.v[i] = Ar<T>::zero();
+#pragma unroll
+  for (int i = 0; i < Lay<T, S>::EPL; ++i) a.r[i] = 0.0;
+}
+
+// Accumulate one row's contribution. x: lane elements of the X row; y: lane
+// elements of the Y row (block modes) or yv the vector entry (SUMVEC).
+template <typename T, int S, int MODE, bool FC>
+__device__ __forceinline__ void red_row(RedAcc<T, S, FC>& a, const T (&x)[Lay<T, S>::EPL], const T (&y)[Lay<T, S>::EPL],
+                                        T yv, int base, int s, unsigned gmask) {
+  using L = Lay<T, S>;
+  if constexpr (MODE == RED_NORM2 || MODE == RED_COLNORM2) {
+#pragma unroll
+    for (int e = 0; e < L::EPL; ++e) a.r[e] += Ar<T>::abs2(x[e]);
+  } else if constexpr (MODE == RED_DIAG || MODE == RED_TRACE) {
+#pragma unroll
+    for (int e = 0; e < L::EPL; ++e) a.v[e] = Ar<T>::cfma(y[e], x[e], a.v[e]);
+  } else if constexpr (MODE == RED_SUMVEC) {
+#pragma unroll
+    for (int e = 0; e < L::EPL; ++e) a.v[e] = Ar<T>::cfma(yv, x[e], a.v[e]);
+  } else if constexpr (MODE == RED_FULL && FC) {
+#pragma unroll
+    for (int k = 0; k < S; ++k) {
+      if (k < s) {
+        const T yk = row_get<T, S>(y, base, k, gmask);
+#pragma unroll
+        for (int e = 0; e < L::EPL; ++e) a.v[k * L::EPL + e] = Ar<T>::cfma(yk, x[e], a.v[k * L::EPL + e]);
+      }
+    }
+  }
+}
+
+// CTA-level reduction of one RedAcc into partials[blockIdx.x*pstride + poff ...].
+// Order: xor-butterfly over lane groups, then warps summed in index order by
+// thread 0..len-1 — fixed for a given launch configuration.
+template <typename T, int S, int MODE, bool FC>
+__device__ void red_flush(RedAcc<T, S, FC>& a, double* __restrict__ partials, int pstride, int poff, int s,
+                          double* smem /* >= nwarps * len doubles */) {
+  using L = Lay<T, S>;
+  constexpr int ND = Ar<T>::ND;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const int g = lane % L::G;
+  // 1) sum over the lane groups of this warp (lanes with equal g hold the same entries)
+#pragma unroll
+  for (int m = L::G; m < 32; m <<= 1) {
+#pragma unroll
+    for (int i = 0; i < RedAcc<T, S, FC>::N; ++i) a.v[i] = Ar<T>::add(a.v[i], Ar<T>::shfl_xor(a.v[i], m));
+#pragma unroll
+    for (int i = 0; i < L::EPL; ++i) a.r[i] += __shfl_xor_sync(0xffffffffu, a.r[i], m);
+  }
+  const int len = red_len(MODE, s, Ar<T>::cplx);
+  // 2) lanes of group 0 scatter their entries into this warp's smem slice
+  double* w = smem + warp * len;
+  if constexpr (MODE == RED_NORM2 || MODE == RED_TRACE || MODE == RED_SUMVEC) {
+    // scalar result: reduce over the G lanes of group 0 first (fixed xor order)
+    double rs = 0.0;
+    T vs = Ar<T>::zero();
+#pragma unroll
+    for (int e = 0; e < L::EPL; ++e) {
+      rs += a.r[e];
+      vs = Ar<T>::add(vs, a.v[e]);
+    }
+#pragma unroll
+    for (int m = 1; m < L::G; m <<= 1) {
+      rs += __shfl_xor_sync(0xffffffffu, rs, m);
+      vs = Ar<T>::add(vs, Ar<T>::shfl_xor(vs, m));
+    }
+    if (lane == 0) {
+      if constexpr (MODE == RED_NORM2) w[0] = rs;
+      else Ar<T>::st(w, vs);
+    }
+  } else if constexpr (MODE == RED_DIAG || MODE == RED_COLNORM2) {
+    if (lane < L::G) {
+#pragma unroll
+      for (int e = 0; e < L::EPL; ++e) {
+        const int c = L::col(g, e);
+        if (c < s) {
+          if constexpr (MODE == RED_COLNORM2) w[c] = a.r[e];
+          else Ar<T>::st(w + c * ND, a.v[e]);
+        }
+      }
+    }
+  } else if constexpr (MODE == RED_FULL && FC) {
+    if (lane < L::G) {
+#pragma unroll
+      for (int k = 0; k < S; ++k) {
+        if (k < s) {
+#pragma unroll
+          for (int e = 0; e < L::EPL; ++e) {
+            const int c = L::col(g, e);
+            if (c < s) Ar<T>::st(w + (k * s + c) * ND, a.v[k * L::EPL + e]);
+          }
+        }
+      }
+    }
+  }
+  __syncthreads();
+  // 3) sum the warps' slices in warp order
+  for (int j = threadIdx.x; j < len; j += blockDim.x) {
+    double acc = 0.0;
+    for (int q = 0; q < nwarps; ++q) acc += smem[q * len + j];
+    partials[(size_t)blockIdx.x * pstride + poff + j] = acc;
+  }
+  __syncthreads();
+}
+
+template <typename T, int S, bool FC>
+__device__ __forceinline__ void red_dispatch_row(int mode, RedAcc<T, S, FC>& a, const T (&x)[Lay<T, S>::EPL],
+                                                 const T (&y)[Lay<T, S>::EPL], T yv, int base, int s,
+                                                 unsigned gmask) {
+  switch (mode) {
+    case RED_NORM2: red_row<T, S, RED_NORM2, FC>(a, x, y, yv, base, s, gmask); break;
+    case RED_COLNORM2: red_row<T, S, RED_COLNORM2, FC>(a, x, y, yv, base, s, gmask); break;
+    case RED_DIAG: red_row<T, S, RED_DIAG, FC>(a, x, y, yv, base, s, gmask); break;
+    case RED_TRACE: red_row<T, S, RED_TRACE, FC>(a, x, y, yv, base, s, gmask); break;
+    case RED_SUMVEC: red_row<T, S, RED_SUMVEC, FC>(a, x, y, yv, base, s, gmask); break;
+    case RED_FULL: red_row<T, S, RED_FULL, FC>(a, x, y, yv, base, s, gmask); break;
+    default: break;
+  }
+}
+
+template <typename T, int S, bool FC>
+__device__ void red_dispatch_flush(int mode, RedAcc<T, S, FC>& a, double* partials, int pstride, int poff, int s,
+                                   double* smem) {
+  switch (mode) {
+    case RED_NORM2: red_flush<T, S, RED_NORM2, FC>(a, partials, pstride, poff, s, smem); break;
+    case RED_COLNORM2: red_flush<T, S, RED_COLNORM2, FC>(a, partials, pstride, poff, s, smem); break;
+    case RED_DIAG: red_flush<T, S, RED_DIAG, FC>(a, partials, pstride, poff, s, smem); break;
+    case RED_TRACE: red_flush<T, S, RED_TRACE, FC>(a, partials, pstride, poff, s, smem); break;
+    case RED_SUMVEC: red_flush<T, S, RED_SUMVEC, FC>(a, partials, pstride, poff, s, smem); break;
+    case RED_FULL: red_flush<T, S, RED_FULL, FC>(a, partials, pstride, poff, s, smem); break;
+    default: break;
+  }
+}
+
+// ============================================================================
+// SpMM: Q = A P  (R rows per lane group in flight; EX = exact width s == S)
+// The nonzero loop is warp-uniform (trip count = the warp's longest row batch)
+// and every gather load is unconditional (absent entries use column 0 with a
+// zero value), so the CW*R loads of a step issue back to back.
+// ============================================================================
+template <typename T, int S, bool FC, int R, bool EX>
+__global__ void __launch_bounds__(256, FC ? 1 : 2) spmm_kernel(SpmmArgs a) {
+  if (a.done && *a.done) return;
+  using L = Lay<T, S>;
+  extern __shared__ double smem[];
+  const int lane = threadIdx.x & 31;
+  const int g = lane % L::G;
+  const int base = lane - g;
+  const unsigned gmask = (L::G == 32) ? 0xffffffffu : (((1u << L::G) - 1u) << base);
+  const long long groups_per_cta = (blockDim.x / 32) * L::RPW;
+  const long long wgrp0 = (long long)blockIdx.x * groups_per_cta + (threadIdx.x >> 5) * L::RPW;  // warp's first group
+  const int gin = lane / L::G;
+  const long long gstride = (long long)gridDim.x * groups_per_cta;
+  const T* __restrict__ P = reinterpret_cast<const T*>(a.P);
+  const T* __restrict__ val = reinterpret_cast<const T*>(a.val);
+  const int* __restrict__ rp = a.row_ptr;
+  const int* __restrict__ ci = a.col_idx;
+  T* __restrict__ Q = reinterpret_cast<T*>(a.Q);
+  const int s = a.s;
+  const long long n = a.n;
+  const int nred = a.nred;
+  const int mode0 = nred > 0 ? a.red[0].mode : RED_NONE;
+  const int mode1 = nred > 1 ? a.red[1].mode : RED_NONE;
+  const T* y0 = reinterpret_cast<const T*>(nred > 0 ? a.red[0].yext : nullptr);
+  const T* y1 = reinterpret_cast<const T*>(nred > 1 ? a.red[1].yext : nullptr);
+
+  RedAcc<T, S, FC> acc0, acc1;
+  red_zero(acc0);
+  red_zero(acc1);
+
+  for (long long wch = wgrp0; wch * R < n; wch += gstride) {  // warp-uniform loop
+    const long long r0 = (wch + gin) * R;
+    int beg[R], len[R];
+    int maxlen = 0;
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const long long r = r0 + i;
+      int b = 0, e = 0;
+      if (r < n) {
+        b = __ldg(rp + r);
+        e = __ldg(rp + r + 1);
+      }
+      beg[i] = b;
+      len[i] = e - b;
+      maxlen = max(maxlen, e - b);
+    }
+    maxlen = __reduce_max_sync(0xffffffffu, maxlen);
+    T q[R][L::EPL];
+#pragma unroll
+    for (int i = 0; i < R; ++i)
+#pragma unroll
+      for (int e = 0; e < L::EPL; ++e) q[i][e] = Ar<T>::zero();
+    // CW entries per step: G lanes hold CW/G (col, val) pairs each, fetched cooperatively
+    // and coalesced (streamed once with evict-first loads so L2 keeps P)
+    constexpr int CW = L::G >= 8 ? L::G : 8;
+    constexpr int EPN = CW / L::G;
+    for (int j0 = 0; j0 < maxlen; j0 += CW) {
+      int cj[R][EPN];
+      T vj[R][EPN];
+#pragma unroll
+      for (int i = 0; i < R; ++i)
+#pragma unroll
+        for (int u = 0; u < EPN; ++u) {
+          const int j = j0 + g + u * L::G;
+          const bool in = j < len[i];
+          cj[i][u] = in ? __ldcs(ci + beg[i] + j) : 0;
+          vj[i][u] = in ? __ldcs(val + beg[i] + j) : Ar<T>::zero();
+        }
+#pragma unroll
+      for (int t = 0; t < CW; ++t) {
+#pragma unroll
+        for (int i = 0; i < R; ++i) {
+          const int c = __shfl_sync(0xffffffffu, cj[i][t / L::G], base + t % L::G);
+          const T v = Ar<T>::shfl(vj[i][t / L::G], base + t % L::G, 0xffffffffu);
+          T p[L::EPL];
+          if constexpr (EX) {
+            row_load_ex<T, S>(P + (size_t)c * S, g, p);
+          } else {
+            row_load<T, S>(P + (size_t)c * s, g, s, a.vec, p);
+          }
+#pragma unroll
+          for (int e = 0; e < L::EPL; ++e) q[i][e] = Ar<T>::fma(v, p[e], q[i][e]);
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const long long row = r0 + i;
+      if (row < n) {
+        if constexpr (EX) row_store_ex<T, S>(Q + (size_t)row * S, g, q[i]);
+        else row_store<T, S>(Q + (size_t)row * s, g, s, a.vec, q[i]);
+        // fused epilogue: reductions with X = Q
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+          const int mode = r == 0 ? mode0 : mode1;
+          if (mode == RED_NONE) continue;
+          const T* yp = r == 0 ? y0 : y1;
+          T y[L::EPL];
+          T yv = Ar<T>::zero();
+#pragma unroll
+          for (int e = 0; e < L::EPL; ++e) y[e] = Ar<T>::zero();
+          if (mode == RED_SUMVEC) yv = yp[row];
+          else if (mode != RED_NORM2 && mode != RED_COLNORM2) {
+            if constexpr (EX) row_load_ex_rw<T, S>(yp + (size_t)row * S, g, y);
+            else row_load<T, S>(yp + (size_t)row * s, g, s, a.vec, y);
+          }
+          if (r == 0) red_dispatch_row<T, S, FC>(mode, acc0, q[i], y, yv, base, s, gmask);
+          else red_dispatch_row<T, S, FC>(mode, acc1, q[i], y, yv, base, s, gmask);
+        }
+      }
+    }
+  }
+  __syncwarp();
+  if (nred > 0) red_dispatch_flush<T, S, FC>(mode0, acc0, a.partials, a.pstride, a.red[0].poff, s, smem);
+  if (nred > 1) red_dispatch_flush<T, S, FC>(mode1, acc1, a.partials, a.pstride, a.red[1].poff, s, smem);
+}
+
+// ============================================================================
+// Fused block update / Gram (NI = compiled input count >= nin, R rows per group)
+// Every register array is indexed with compile-time indices only (sources are
+// visited by unrolled loops, absent terms skipped by a uniform branch), so the
+// rows stay in registers and all NI*R loads of a step are in flight together.
+// ============================================================================
+template <typename T, int S, bool FC, int NI, int R, bool EX>
+__global__ void __launch_bounds__(256, (NI >= 4 || FC) ? 1 : 2) upd_kernel(UpdArgs a) {
+  if (a.done && *a.done) return;
+  using L = Lay<T, S>;
+  constexpr int ND = Ar<T>::ND;
+  extern __shared__ double smem[];
+  __shared__ int s_kind[MAX_OUT][MAX_SRC];
+  __shared__ int s_cslot[MAX_OUT][MAX_SRC];
+  const int s = a.s;
+  const long long n = a.n;
+  if (threadIdx.x < MAX_OUT * MAX_SRC) {
+    const int o = threadIdx.x / MAX_SRC, b = threadIdx.x % MAX_SRC;
+    s_kind[o][b] = (o < a.nout) ? a.cf[o][b].kind : CK_NONE;
+    s_cslot[o][b] = a.cslot[o][b];
+  }
+  // ---- stage coefficients into shared memory (neg/conj/herm applied once),
+  // padded to the lane layout's row width PW
+  T* cs = reinterpret_cast<T*>(smem);
+  for (int o = 0; o < a.nout; ++o)
+    for (int b = 0; b < MAX_SRC; ++b) {
+      const Coef& cf = a.cf[o][b];
+      if (cf.kind == CK_NONE) continue;
+      T* dst = cs + a.cslot[o][b];
+      constexpr int PW = L::PW;
+      int cnt = cf.kind == CK_FULL ? S * PW : (cf.kind == CK_DIAG ? PW : 1);
+      for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+        T v = Ar<T>::zero();
+        if (cf.kind == CK_ONE) {
+          if constexpr (Ar<T>::cplx) v = mk(1.0, 0.0); else v = 1.0;
+        } else if (cf.kind == CK_SCALAR) {
+          v = Ar<T>::ld(a.ws + cf.off);
+        } else if (cf.kind == CK_DIAG) {
+          if (i < s) v = Ar<T>::ld(a.ws + cf.off + i * ND);
+        } else {
+          const int k = i / PW, c = i % PW;
+          if (k < s && c < s) v = cf.herm ? Ar<T>::conj(Ar<T>::ld(a.ws + cf.off + (c * s + k) * ND))
+                                          : Ar<T>::ld(a.ws + cf.off + (k * s + c) * ND);
+        }
+        if (cf.conj) v = Ar<T>::conj(v);
+        if (cf.neg) v = Ar<T>::sub(Ar<T>::zero(), v);
+        dst[i] = v;
+      }
+    }
+  double* rsm = reinterpret_cast<double*>(cs + a.cslot_total);
+  __syncthreads();
+
+  const int lane = threadIdx.x & 31;
+  const int g = lane % L::G;
+  const int base = lane - g;
+  const unsigned gmask = (L::G == 32) ? 0xffffffffu : (((1u << L::G) - 1u) << base);
+  const long long groups_per_cta = (blockDim.x / 32) * L::RPW;
+  const long long grp0 = (long long)blockIdx.x * groups_per_cta + (threadIdx.x >> 5) * L::RPW + lane / L::G;
+  const long long gstride = (long long)gridDim.x * groups_per_cta;
+  const int nin = a.nin, nout = a.nout, nred = a.nred;
+  int rmode[MAX_RED], rx[MAX_RED], ry[MAX_RED];
+#pragma unroll
+  for (int r = 0; r < MAX_RED; ++r) {
+    rmode[r] = r < nred ? a.red[r].mode : RED_NONE;
+    rx[r] = r < nred ? a.red[r].xsrc : -2;
+    ry[r] = r < nred ? a.red[r].ysrc : -2;
+  }
+
+  RedAcc<T, S, FC> acc0, acc1;
+  RedAcc<T, S, false> acc2;
+  red_zero(acc0);
+  red_zero(acc1);
+  red_zero(acc2);
+
+  // apply one term: o_row += x_row * coefficient (kind uniform over the CTA)
+  auto apply = [&](T (&o_row)[L::EPL], const T (&x)[L::EPL], int kind, const T* cf) {
+    if constexpr (FC) {  // s x s coefficients exist only in the block-method instances
+      if (kind == CK_FULL) {
+#pragma unroll
+        for (int k = 0; k < S; ++k) {
+          if (k < s) {
+            const T xk = row_get<T, S>(x, base, k, gmask);
+#pragma unroll
+            for (int e = 0; e < L::EPL; ++e) o_row[e] = Ar<T>::fma(xk, cf[k * L::PW + L::col(g, e)], o_row[e]);
+          }
+        }
+        return;
+      }
+    }
+    if (kind == CK_DIAG) {
+#pragma unroll
+      for (int e = 0; e < L::EPL; ++e) o_row[e] = Ar<T>::fma(x[e], cf[L::col(g, e)], o_row[e]);
+    } else {
+      const T c0 = cf[0];
+#pragma unroll
+      for (int e = 0; e < L::EPL; ++e) o_row[e] = Ar<T>::fma(x[e], c0, o_row[e]);
+    }
+  };
+
+  for (long long ch = grp0; ch * R < n; ch += gstride) {
+    const long long r0 = ch * R;
+    // ---- issue every load of the R rows first
+    T xin[NI][R][L::EPL];
+#pragma unroll
+    for (int b = 0; b < NI; ++b) {
+#pragma unroll
+      for (int i = 0; i < R; ++i) {
+#pragma unroll
+        for (int e = 0; e < L::EPL; ++e) xin[b][i][e] = Ar<T>::zero();
+        if (b < nin && r0 + i < n) {
+          if constexpr (EX) row_load_ex_rw<T, S>(reinterpret_cast<const T*>(a.in[b]) + (size_t)(r0 + i) * S, g, xin[b][i]);
+          else row_load<T, S>(reinterpret_cast<const T*>(a.in[b]) + (size_t)(r0 + i) * s, g, s, a.vec, xin[b][i]);
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const long long row = r0 + i;
+      if (row < n) {
+        T xo[MAX_OUT][L::EPL];
+#pragma unroll
+        for (int o = 0; o < MAX_OUT; ++o) {
+#pragma unroll
+          for (int e = 0; e < L::EPL; ++e) xo[o][e] = Ar<T>::zero();
+          if (o < nout) {
+#pragma unroll
+            for (int b = 0; b < NI; ++b) {
+              const int kind = s_kind[o][b];
+              if (kind != CK_NONE) apply(xo[o], xin[b][i], kind, cs + s_cslot[o][b]);
+            }
+#pragma unroll
+            for (int b = 0; b < o; ++b) {
+              const int kind = s_kind[o][MAX_IN + b];
+              if (kind != CK_NONE) apply(xo[o], xo[b], kind, cs + s_cslot[o][MAX_IN + b]);
+            }
+            if (a.out[o]) {
+              if constexpr (EX) row_store_ex<T, S>(reinterpret_cast<T*>(a.out[o]) + (size_t)row * S, g, xo[o]);
+              else row_store<T, S>(reinterpret_cast<T*>(a.out[o]) + (size_t)row * s, g, s, a.vec, xo[o]);
+            }
+          }
+        }
+        // ---- reductions: operands picked with compile-time indices
+#pragma unroll
+        for (int r = 0; r < MAX_RED; ++r) {
+          if (rmode[r] != RED_NONE) {
+            T x[L::EPL], y[L::EPL];
+            T yv = Ar<T>::zero();
+#pragma unroll
+            for (int e = 0; e < L::EPL; ++e) {
+              x[e] = Ar<T>::zero();
+              y[e] = Ar<T>::zero();
+            }
+#pragma unroll
+            for (int b = 0; b < NI; ++b) {
+#pragma unroll
+              for (int e = 0; e < L::EPL; ++e) {
+                x[e] = opaque_sel(rx[r] == b, xin[b][i][e], x[e]);
+                y[e] = opaque_sel(ry[r] == b, xin[b][i][e], y[e]);
+              }
+            }
+#pragma unroll
+            for (int b = 0; b < MAX_OUT; ++b) {
+#pragma unroll
+              for (int e = 0; e < L::EPL; ++e) {
+                x[e] = opaque_sel(rx[r] == SRC_OUT + b, xo[b][e], x[e]);
+                y[e] = opaque_sel(ry[r] == SRC_OUT + b, xo[b][e], y[e]);
+              }
+            }
+            if (ry[r] < 0 && a.red[r].yext) {
+              if (rmode[r] == RED_SUMVEC) yv = reinterpret_cast<const T*>(a.red[r].yext)[row];
+              else row_load<T, S>(reinterpret_cast<const T*>(a.red[r].yext) + (size_t)row * s, g, s, a.vec, y);
+            }
+            if (r == 0) red_dispatch_row<T, S, FC>(rmode[r], acc0, x, y, yv, base, s, gmask);
+            else if (r == 1) red_dispatch_row<T, S, FC>(rmode[r], acc1, x, y, yv, base, s, gmask);
+            else red_dispatch_row<T, S, false>(rmode[r], acc2, x, y, yv, base, s, gmask);
+          }
+        }
+      }  // row < n
+    }
+  }
+  __syncwarp();
+  if (nred > 0) red_dispatch_flush<T, S, FC>(rmode[0], acc0, a.partials, a.pstride, a.red[0].poff, s, rsm);
+  if (nred > 1) red_dispatch_flush<T, S, FC>(rmode[1], acc1, a.partials, a.pstride, a.red[1].poff, s, rsm);
+  if (nred > 2) red_dispatch_flush<T, S, false>(rmode[2], acc2, a.partials, a.pstride, a.red[2].poff, s, rsm);
+}
+
+// rows per group in flight
+template <typename T, int S> constexpr int spmm_rows() {
+  return (Lay<T, S>::G == 1 || S >= 64) ? 1 : (Lay<T, S>::G >= 16 ? 2 : 4);
+}
+template <int NI> constexpr int upd_rows() { return NI <= 1 ? 4 : (NI <= 2 ? 2 : 1); }
+template <typename T, int S> constexpr bool full_ok() { return S <= 16; }
+
+// grid < 0: return the number of resident CTAs per SM instead of launching
+template <typename T, int S, bool FC, bool EX>
+int launch_spmm_tx(const SpmmArgs& a, int grid, int block, size_t smem, cudaStream_t st) {
+  constexpr int R = spmm_rows<T, S>();
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(spmm_kernel<T, S, FC, R, EX>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  if (grid < 0) {
+    int nb = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, spmm_kernel<T, S, FC, R, EX>, block, smem);
+    return nb;
+  }
+  spmm_kernel<T, S, FC, R, EX><<<grid, block, smem, st>>>(a);
+  return (int)cudaGetLastError();
+}
+
+// grid < 0: return the number of resident CTAs per SM instead of launching
+template <typename T, int S, bool FC>
+int launch_spmm_t(const SpmmArgs& a, int grid, int block, size_t smem, cudaStream_t st) {
+  const bool ex = a.s == S && (sizeof(T) == 16 || S % 2 == 0);
+  if (grid < 0 || ex) return launch_spmm_tx<T, S, FC, true>(a, grid, block, smem, st);
+  return launch_spmm_tx<T, S, FC, false>(a, grid, block, smem, st);
+}
+
+template <typename T, int S, bool FC, int NI, bool EX>
+int launch_upd_nix(const UpdArgs& a, int grid, int block, size_t smem, cudaStream_t st) {
+  constexpr int R = upd_rows<NI>();
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(upd_kernel<T, S, FC, NI, R, EX>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  if (grid < 0) {
+    int nb = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, upd_kernel<T, S, FC, NI, R, EX>, block, smem);
+    return nb;
+  }
+  upd_kernel<T, S, FC, NI, R, EX><<<grid, block, smem, st>>>(a);
+  return (int)cudaGetLastError();
+}
+
+template <typename T, int S, bool FC, int NI>
+int launch_upd_ni(const UpdArgs& a, int grid, int block, size_t smem, cudaStream_t st) {
+  // exact-width variant only for the scalar/diagonal (non-block) instances
+  if constexpr (!FC) {
+    const bool ex = a.s == S && (sizeof(T) == 16 || S % 2 == 0);
+    if (grid < 0 || ex) return launch_upd_nix<T, S, FC, NI, true>(a, grid, block, smem, st);
+  }
+  return launch_upd_nix<T, S, FC, NI, false>(a, grid, block, smem, st);
+}
+
+template <typename T, int S, bool FC>
+int launch_upd_t(const UpdArgs& a, int grid, int block, size_t smem, cudaStream_t st) {
+  const int nin = a.nin;
+  if constexpr (FC) {  // block-method instances: two widths only (compile time)
+    if (nin <= 2) return launch_upd_ni<T, S, FC, 2>(a, grid, block, smem, st);
+    return launch_upd_ni<T, S, FC, MAX_IN>(a, grid, block, smem, st);
+  } else {
+    if (nin == 1) return launch_upd_ni<T, S, FC, 1>(a, grid, block, smem, st);
+    if (nin == 2) return launch_upd_ni<T, S, FC, 2>(a, grid, block, smem, st);
+    if (nin == 3 || nin == 4) return launch_upd_ni<T, S, FC, 4>(a, grid, block, smem, st);
+    return launch_upd_ni<T, S, FC, MAX_IN>(a, grid, block, smem, st);
+  }
+}
+
+template <typename T, int S>
+int pick_spmm(bool full, const SpmmArgs& a, int grid, int block, size_t smem, cudaStream_t st) {
+  if constexpr (full_ok<T, S>()) {
+    if (full) return launch_spmm_t<T, S, true>(a, grid, block, smem, st);
+  } else {
+    if (full) return (int)cudaErrorInvalidValue;
+  }
+  return launch_spmm_t<T, S, false>(a, grid, block, smem, st);
+}
+template <typename T, int S>
+int pick_upd(bool full, const UpdArgs& a, int grid, int block, size_t smem, cudaStream_t st) {
+  if constexpr (full_ok<T, S>()) {
+    if (full) return launch_upd_t<T, S, true>(a, grid, block, smem, st);
+  } else {
+    if (full) return (int)cudaErrorInvalidValue;
+  }
+  return launch_upd_t<T, S, false>(a, grid, block, smem, st);
+}
+
+
+}  // namespace srk

@@ -110,6 +110,62 @@ __device__ __forceinline__ void row_load(const T* __restrict__ p, int g, int s, 
   }
 }
 
+// Exact-width variants (s == S, rows 16-byte aligned): no data-dependent
+// branches, so a batch of loads can be issued back to back. Lanes beyond the
+// chunk count (G > NCH) are masked by a lane predicate only.
+template <typename T, int S>
+__device__ __forceinline__ void row_load_ex(const T* __restrict__ p, int g, T (&v)[Lay<T, S>::EPL]) {
+  using L = Lay<T, S>;
+#pragma unroll
+  for (int c = 0; c < L::CPL; ++c) {
+    const int ch = g + c * L::G;
+    const bool ok = (L::NCH % L::G == 0) || ch < L::NCH;
+    if constexpr (L::EPC == 2) {
+      double2 t = make_double2(0.0, 0.0);
+      if (ok) t = __ldg(reinterpret_cast<const double2*>(p) + ch);
+      v[c * 2] = t.x;
+      v[c * 2 + 1] = t.y;
+    } else {
+      T t = Ar<T>::zero();
+      if (ok) t = __ldg(p + ch);
+      v[c] = t;
+    }
+  }
+}
+template <typename T, int S>
+__device__ __forceinline__ void row_store_ex(T* __restrict__ p, int g, const T (&v)[Lay<T, S>::EPL]) {
+  using L = Lay<T, S>;
+#pragma unroll
+  for (int c = 0; c < L::CPL; ++c) {
+    const int ch = g + c * L::G;
+    const bool ok = (L::NCH % L::G == 0) || ch < L::NCH;
+    if (ok) {
+      if constexpr (L::EPC == 2) reinterpret_cast<double2*>(p)[ch] = make_double2(v[c * 2], v[c * 2 + 1]);
+      else p[ch] = v[c];
+    }
+  }
+}
+// row-local loads with a plain ld.global (data written earlier in the same kernel sequence)
+template <typename T, int S>
+__device__ __forceinline__ void row_load_ex_rw(const T* p, int g, T (&v)[Lay<T, S>::EPL]) {
+  using L = Lay<T, S>;
+#pragma unroll
+  for (int c = 0; c < L::CPL; ++c) {
+    const int ch = g + c * L::G;
+    const bool ok = (L::NCH % L::G == 0) || ch < L::NCH;
+    if constexpr (L::EPC == 2) {
+      double2 t = make_double2(0.0, 0.0);
+      if (ok) t = reinterpret_cast<const double2*>(p)[ch];
+      v[c * 2] = t.x;
+      v[c * 2 + 1] = t.y;
+    } else {
+      T t = Ar<T>::zero();
+      if (ok) t = p[ch];
+      v[c] = t;
+    }
+  }
+}
+
 template <typename T, int S>
 __device__ __forceinline__ void row_store(T* __restrict__ p, int g, int s, bool vec, const T (&v)[Lay<T, S>::EPL]) {
   using L = Lay<T, S>;
@@ -127,6 +183,17 @@ __device__ __forceinline__ void row_store(T* __restrict__ p, int g, int s, bool 
       if (c0 < s) p[c0] = v[c];
     }
   }
+}
+
+// Opaque select (inline PTX selp): keeps "pick one of several register rows by a
+// runtime index" from being turned into an indexed local-memory array.
+__device__ __forceinline__ double opaque_sel(int p, double a, double b) {
+  double r;
+  asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %3, 0;\n\tselp.f64 %0, %1, %2, q;\n\t}" : "=d"(r) : "d"(a), "d"(b), "r"(p));
+  return r;
+}
+__device__ __forceinline__ double2 opaque_sel(int p, double2 a, double2 b) {
+  return make_double2(opaque_sel(p, a.x, b.x), opaque_sel(p, a.y, b.y));
 }
 
 // Fetch element k (row-local column) of the row held by the lane group whose

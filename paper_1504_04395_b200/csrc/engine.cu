@@ -55,14 +55,15 @@ Prof::~Prof() {
 // Persistent-style grid: exactly one wave, i.e. the SM count times the number of
 // CTAs the occupancy calculator says are resident for this kernel instance (so
 // no partial second wave), or fewer CTAs when n is small.
-int Eng::grid_for(int cap, bool full, bool is_spmm, size_t smem) const {
+int Eng::grid_for(int cap, bool full, bool is_spmm, size_t smem, int nin) const {
   const long long rpc = rows_per_cta(cap, cplx);
   long long need = (n + rpc - 1) / rpc;
-  static int occ_cache[2][2][2][65] = {};
-  int& occ = occ_cache[is_spmm][cplx][full][cap];
+  static int occ_cache[2][2][2][65][MAX_IN + 1] = {};
+  int& occ = occ_cache[is_spmm][cplx][full][cap][is_spmm ? 0 : nin];
   if (occ == 0) {
     SpmmArgs sa{};
     UpdArgs ua{};
+    ua.nin = nin;
     occ = is_spmm ? launch_spmm(cplx, cap, full, sa, -1, 256, smem, nullptr)
                   : launch_upd(cplx, cap, full, ua, -1, 256, smem, nullptr);
     if (occ < 1) occ = 1;
@@ -99,11 +100,41 @@ static int finish_reds(Eng& e, const std::vector<RQ>& reds, const std::vector<in
   if (e.prof) e.prof->begin(PT_FIN, e.c->st);
   int r = launch_fin(f, e.c->st);
   if (e.prof) e.prof->end(e.c->st);
+  if (r) return r;
+  // multi-GPU: the per-rank sums become global sums (same bits on every rank)
+  if (e.c->comm && e.c->comm->nranks > 1) {
+    if (e.prof) e.prof->begin(PT_OTHER, e.c->st);
+    for (size_t i = 0; i < reds.size(); ++i)
+      if (comm_allreduce_sum(e.c->comm, e.ws + reds[i].woff, red_len(reds[i].mode, s, e.cplx), e.c->st)) r = -5;
+    if (e.prof) e.prof->end(e.c->st);
+  }
+  return r;
+}
+
+// Halo exchange of the ghost rows of P (multi-GPU operators): pack the rows the
+// peers need, then grouped ncclSend/ncclRecv straight into P's ghost tail.
+int Eng::halo(bool adj, const void* P, int s) {
+  Mat* M = const_cast<Mat*>(A);
+  const Halo& H = adj ? M->haloH : M->halo;
+  if (!M->dist || !c->comm || c->comm->nranks == 1) return 0;
+  const int dpr = s * (cplx ? 2 : 1);
+  const size_t need = (size_t)std::max<long long>(H.n_send, 1) * dpr;
+  if (need > M->sendcap) {
+    if (M->sendbuf) cudaFree(M->sendbuf);
+    if (cudaMalloc(&M->sendbuf, need * sizeof(double)) != cudaSuccess) return (int)cudaErrorMemoryAllocation;
+    M->sendcap = need;
+  }
+  if (prof) prof->begin(PT_OTHER, c->st);
+  int r = launch_gather_rows(reinterpret_cast<const double*>(P), M->sendbuf, H.send_idx, H.n_send, dpr, nullptr, c->st);
+  if (!r) r = comm_halo(c->comm, M->sendbuf, H.send_off, const_cast<double*>(reinterpret_cast<const double*>(P)) + (size_t)n * dpr,
+                        H.recv_off, dpr, c->st);
+  if (prof) prof->end(c->st);
   return r;
 }
 
 int Eng::spmm(bool adj, const void* P, void* Q, int s, std::vector<RQ> reds) {
   if (err) return err;
+  if ((err = halo(adj, P, s))) return err;
   const int cap = cap_for(s);
   bool full = false;
   for (auto& r : reds) full |= (r.mode == RED_FULL);
@@ -129,7 +160,7 @@ int Eng::spmm(bool adj, const void* P, void* Q, int s, std::vector<RQ> reds) {
   }
   a.pstride = std::max(pstride, 1);
   const size_t smem = (size_t)8 * maxlen * sizeof(double);
-  const int grid = grid_for(cap, full, true, 8 * 2 * 8 * 16 * 16);  // occupancy at the largest epilogue smem
+  const int grid = grid_for(cap, full, true, 8 * 2 * 8 * 16 * 16, 0);  // occupancy at the largest epilogue smem
   if ((err = c->ensure_partials((size_t)grid * a.pstride))) return err;
   a.partials = c->partials;
   a.done = done;
@@ -144,25 +175,30 @@ int Eng::spmm(bool adj, const void* P, void* Q, int s, std::vector<RQ> reds) {
 int Eng::upd(int s, std::vector<const void*> in, std::vector<OutSpec> outs, std::vector<RQ> reds) {
   if (err) return err;
   const int cap = cap_for(s);
-  bool full = false;
+  bool full = false;  // s x s Gram or s x s coefficient: the block-method kernel instance
   for (auto& r : reds) full |= (r.mode == RED_FULL);
+  for (auto& o : outs)
+    for (auto& t : o.t) full |= (t.c.kind == CK_FULL);
   if (full && !full_supported(cplx, cap)) return err = (int)cudaErrorNotSupported;
   if (in.size() > MAX_IN || outs.size() > MAX_OUT || reds.size() > MAX_RED) return err = (int)cudaErrorInvalidValue;
   UpdArgs a{};
   a.nin = (int)in.size();
   for (size_t i = 0; i < in.size(); ++i) a.in[i] = in[i];
   a.nout = (int)outs.size();
+  for (int o = 0; o < MAX_OUT; ++o)
+    for (int b = 0; b < MAX_SRC; ++b) a.cf[o][b].kind = CK_NONE;
+  const int pw = padded_width(cap, cplx);
   int cslot = 0;
   for (size_t o = 0; o < outs.size(); ++o) {
-    a.out[o].ptr = outs[o].ptr;
-    a.out[o].nterm = (int)outs[o].t.size();
-    if (outs[o].t.size() > 4) return err = (int)cudaErrorInvalidValue;
-    for (size_t t = 0; t < outs[o].t.size(); ++t) {
-      a.out[o].t[t].src = outs[o].t[t].src;
-      a.out[o].t[t].c = outs[o].t[t].c;
-      a.cslot[o][t] = cslot;
-      const int k = outs[o].t[t].c.kind;
-      const int pw = padded_width(cap, cplx);
+    a.out[o] = outs[o].ptr;
+    for (const TermSpec& t : outs[o].t) {
+      const int src = t.src;
+      // inputs 0..nin-1, or an earlier output (SRC_OUT + o' with o' < o); one term per source
+      const bool ok = (src >= 0 && src < (int)in.size()) || (src >= SRC_OUT && src - SRC_OUT < (int)o);
+      if (!ok || a.cf[o][src].kind != CK_NONE) return err = (int)cudaErrorInvalidValue;
+      a.cf[o][src] = t.c;
+      a.cslot[o][src] = cslot;
+      const int k = t.c.kind;
       cslot += (k == CK_FULL) ? cap * pw : (k == CK_DIAG ? pw : 1);
       if (cslot & 1) cslot++;  // keep 16-byte alignment of the following slot
     }
@@ -187,7 +223,7 @@ int Eng::upd(int s, std::vector<const void*> in, std::vector<OutSpec> outs, std:
   a.done = done;
   const size_t esz = cplx ? 16 : 8;
   const size_t smem = (size_t)cslot * esz + (size_t)8 * maxlen * sizeof(double);
-  const int grid = grid_for(cap, full, false, 48 * 1024);  // occupancy at a fixed smem budget (deterministic grid)
+  const int grid = grid_for(cap, full, false, 48 * 1024, a.nin);  // occupancy at a fixed smem budget (deterministic grid)
   if ((err = c->ensure_partials((size_t)grid * a.pstride))) return err;
   a.partials = c->partials;
   nlaunch++;
@@ -223,8 +259,10 @@ int launch_row_mean(bool cplx, const void* X, void* out, long long n, int s, con
 }
 
 // CSR validation (SPEC SparseMatrix invariants S:36): row_ptr non-decreasing,
-// row_ptr[0] = 0, row_ptr[n] = nnz, columns in [0, n) strictly increasing per row.
-__global__ void csr_check_kernel(long long n, long long nnz, const int* rp, const int* ci, int* bad) {
+// row_ptr[0] = 0, row_ptr[n] = nnz, columns in [0, ncols), strictly increasing per
+// row when `sorted` (local rows of a distributed operator keep the global order).
+__global__ void csr_check_kernel(long long n, long long ncols, long long nnz, const int* rp, const int* ci, int sorted,
+                                 int* bad) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
     const int b = rp[i], e = rp[i + 1];
     if (e < b || b < 0 || e > nnz) { atomicOr(bad, 1); continue; }
@@ -232,15 +270,36 @@ __global__ void csr_check_kernel(long long n, long long nnz, const int* rp, cons
     if (i == n - 1 && e != nnz) atomicOr(bad, 1);
     for (int j = b; j < e; ++j) {
       const int c = ci[j];
-      if (c < 0 || c >= n) atomicOr(bad, 2);
-      if (j > b && c <= ci[j - 1]) atomicOr(bad, 4);
+      if (c < 0 || c >= ncols) atomicOr(bad, 2);
+      if (sorted && j > b && c <= ci[j - 1]) atomicOr(bad, 4);
     }
   }
 }
 
-int launch_csr_check(long long n, long long nnz, const int* rp, const int* ci, int* bad, cudaStream_t st) {
+int launch_csr_check(long long n, long long ncols, long long nnz, const int* rp, const int* ci, int sorted, int* bad,
+                     cudaStream_t st) {
   const int grid = (int)std::max<long long>(1, std::min<long long>((n + 255) / 256, 148 * 8));
-  csr_check_kernel<<<grid, 256, 0, st>>>(n, nnz, rp, ci, bad);
+  csr_check_kernel<<<grid, 256, 0, st>>>(n, ncols, nnz, rp, ci, sorted, bad);
+  return (int)cudaGetLastError();
+}
+
+// halo pack: dst row k = src row idx[k] (rows of doubles_per_row doubles)
+__global__ void gather_rows_kernel(const double* src, double* dst, const int* idx, long long nrows, int dpr,
+                                   const int* done) {
+  if (done && *done) return;
+  const long long total = nrows * dpr;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
+    const long long k = t / dpr;
+    const int c = (int)(t % dpr);
+    dst[t] = src[(long long)idx[k] * dpr + c];
+  }
+}
+
+int launch_gather_rows(const double* src, double* dst, const int* idx, long long nrows, int dpr, const int* done,
+                       cudaStream_t st) {
+  if (nrows <= 0) return 0;
+  const int grid = (int)std::max<long long>(1, std::min<long long>((nrows * dpr + 255) / 256, 148 * 8));
+  gather_rows_kernel<<<grid, 256, 0, st>>>(src, dst, idx, nrows, dpr, done);
   return (int)cudaGetLastError();
 }
 

@@ -2,9 +2,11 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <string>
 #include <vector>
 
+#include "comm.h"
 #include "kernels.cuh"
 
 namespace srk {
@@ -19,7 +21,10 @@ int launch_fin(const FinArgs& a, cudaStream_t st);
 int launch_row_mean(bool cplx, const void* X, void* out, long long n, int s, const int* done, cudaStream_t st);
 int launch_csr_transpose(bool cplx, long long n, long long nnz, const int* rp, const int* ci, const void* val,
                          int* rpT, int* ciT, void* valT, int* work, cudaStream_t st);
-int launch_csr_check(long long n, long long nnz, const int* rp, const int* ci, int* bad, cudaStream_t st);
+int launch_csr_check(long long n, long long ncols, long long nnz, const int* rp, const int* ci, int sorted, int* bad,
+                     cudaStream_t st);
+int launch_gather_rows(const double* src, double* dst, const int* idx, long long nrows, int doubles_per_row,
+                       const int* done, cudaStream_t st);
 
 struct Comm;  // multi-GPU plumbing (comm.cpp)
 
@@ -44,6 +49,13 @@ struct Mat {
   int* rpH = nullptr;
   int* ciH = nullptr;
   void* valH = nullptr;
+  // multi-GPU (row-partitioned) operator: local rows, columns [0, n) owned and
+  // [n, n + n_ghost) ghost rows received from the owning ranks before each SpMM
+  bool dist = false;
+  Halo halo, haloH;
+  double* sendbuf = nullptr;  // packed rows for the halo exchange
+  size_t sendcap = 0;         // doubles
+  long long ghost_rows() const { return dist ? std::max(halo.n_ghost, haloH.n_ghost) : 0; }
 };
 
 // reduction request: X = source (or the SpMM output), Y = source or external
@@ -95,8 +107,9 @@ struct Eng {
   int err = 0;            // first CUDA error
   int nlaunch = 0;        // kernels launched (instrumentation)
   int spmm(bool adj, const void* P, void* Q, int s, std::vector<RQ> reds);
+  int halo(bool adj, const void* P, int s);
   int upd(int s, std::vector<const void*> in, std::vector<OutSpec> outs, std::vector<RQ> reds);
-  int grid_for(int cap, bool full, bool is_spmm, size_t smem) const;
+  int grid_for(int cap, bool full, bool is_spmm, size_t smem, int nin) const;
 };
 
 }  // namespace srk

@@ -30,8 +30,8 @@ __host__ __device__ inline int red_len(int mode, int s, bool cplx) {
   }
 }
 
-// source encoding for terms / reductions: 0..7 = input block, 8..11 = output j (8 + j)
-constexpr int SRC_OUT = 8;
+// source encoding for terms / reductions: 0..5 = input block b, 6..9 = output j (6 + j)
+constexpr int SRC_OUT = 6;
 
 struct Red {
   int mode;
@@ -51,31 +51,24 @@ struct Coef {
   int herm;  // CK_FULL only: use M^H instead of M
 };
 
-struct Term {
-  int src;
-  Coef c;
-};
-
-struct OutD {
-  void* ptr;  // n x s block to store (nullptr: kept in registers only, e.g. a Gram operand)
-  int nterm;
-  Term t[4];
-};
-
 constexpr int MAX_IN = 6;
 constexpr int MAX_OUT = 4;
 constexpr int MAX_RED = 3;
+constexpr int MAX_SRC = MAX_IN + MAX_OUT;  // a term's source: input b, or an earlier output (MAX_IN + o)
+constexpr int CK_NONE = -1;
 
 // Generic fused block update / Gram kernel arguments:
-//   out_j = sum_t src_t * coef_t   (row by row; coef scalar, diag or s x s)
-// plus up to MAX_RED reductions over inputs/outputs, written as per-CTA partials.
+//   out_o = sum_b in_b * cf[o][b] + sum_{o' < o} out_o' * cf[o][MAX_IN + o']   (row by row)
+// with every coefficient scalar, diagonal or s x s (CK_NONE = absent term), plus up to
+// MAX_RED reductions over inputs/outputs, written as per-CTA partials.
 struct UpdArgs {
   const void* in[MAX_IN];
-  OutD out[MAX_OUT];
+  void* out[MAX_OUT];    // nullptr: output kept in registers only (e.g. a Gram operand)
+  Coef cf[MAX_OUT][MAX_SRC];
+  int cslot[MAX_OUT][MAX_SRC];  // offset (in values of T) of each staged coefficient in smem
+  int cslot_total;
   Red red[MAX_RED];
   int nin, nout, nred;
-  int cslot[MAX_OUT][4];  // offset (in values of T) of each term's staged coefficient in smem
-  int cslot_total;
   const double* ws;    // coefficient workspace
   double* partials;    // [gridDim.x][pstride]
   int pstride;

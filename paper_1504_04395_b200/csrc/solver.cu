@@ -26,15 +26,18 @@ Solver::~Solver() {
   if (ctl_host) cudaFreeHost(ctl_host);
 }
 
+// blocks carry a tail of ghost rows (multi-GPU: filled by the halo exchange before each SpMM)
 void* Solver::blk() {
   void* p = nullptr;
-  if (cudaMalloc(&p, (size_t)n * s * esz()) != cudaSuccess) return nullptr;
+  const size_t rows = (size_t)(n + A->ghost_rows());
+  if (cudaMalloc(&p, rows * s * esz()) != cudaSuccess) return nullptr;
   owned.push_back(p);
   return p;
 }
 void* Solver::vecn() {
   void* p = nullptr;
-  if (cudaMalloc(&p, (size_t)n * esz()) != cudaSuccess) return nullptr;
+  const size_t rows = (size_t)(n + A->ghost_rows());
+  if (cudaMalloc(&p, rows * esz()) != cudaSuccess) return nullptr;
   owned.push_back(p);
   return p;
 }
