@@ -180,10 +180,23 @@ __global__ void __launch_bounds__(256, FC ? 1 : 2) spmm_kernel(SpmmArgs a) {
   const int g = lane % L::G;
   const int base = lane - g;
   const unsigned gmask = (L::G == 32) ? 0xffffffffu : (((1u << L::G) - 1u) << base);
-  const long long groups_per_cta = (blockDim.x / 32) * L::RPW;
-  const long long wgrp0 = (long long)blockIdx.x * groups_per_cta + (threadIdx.x >> 5) * L::RPW;  // warp's first group
+  // Block-cyclic row mapping: a CTA owns blocks of BC consecutive steps (step =
+  // 8 warps x RPW groups x R rows), blocks dealt round-robin over the grid. Within
+  // a block the CTA sweeps in order, so stencil neighbours a few grid lines away
+  // are re-read from L1; all CTAs sweep neighbouring blocks concurrently, so the
+  // far neighbours (other planes) are L2 hits and P streams from HBM about once.
+  constexpr int BC = 8;
   const int gin = lane / L::G;
-  const long long gstride = (long long)gridDim.x * groups_per_cta;
+  const long long step = (long long)(blockDim.x / 32) * L::RPW * R;
+  const long long warp_off = (long long)(threadIdx.x >> 5) * L::RPW * R + (long long)gin * R;
+  auto row_of = [&](long long k) {  // first row of this warp-lane-group in local step k
+    const long long blk = (long long)blockIdx.x + (k / BC) * gridDim.x;
+    return (blk * BC + (k % BC)) * step + warp_off;
+  };
+  auto step_live = [&](long long k) {  // warp-uniform
+    const long long blk = (long long)blockIdx.x + (k / BC) * gridDim.x;
+    return (blk * BC + (k % BC)) * step < a.n;
+  };
   const T* __restrict__ P = reinterpret_cast<const T*>(a.P);
   const T* __restrict__ val = reinterpret_cast<const T*>(a.val);
   const int* __restrict__ rp = a.row_ptr;
@@ -201,44 +214,62 @@ __global__ void __launch_bounds__(256, FC ? 1 : 2) spmm_kernel(SpmmArgs a) {
   red_zero(acc0);
   red_zero(acc1);
 
-  for (long long wch = wgrp0; wch * R < n; wch += gstride) {  // warp-uniform loop
-    const long long r0 = (wch + gin) * R;
-    int beg[R], len[R];
-    int maxlen = 0;
+  constexpr int CW = L::G >= 8 ? L::G : 8;  // CSR entries per step of a row
+  constexpr int EPN = CW / L::G;            // (col, val) pairs per lane per step
+  // row_ptr of one batch of R rows
+  auto load_rp = [&](long long k, int (&bg)[R], int (&ln)[R]) {
+    const long long r0 = row_of(k);
 #pragma unroll
     for (int i = 0; i < R; ++i) {
       const long long r = r0 + i;
-      int b = 0, e = 0;
-      if (r < n) {
-        b = __ldg(rp + r);
-        e = __ldg(rp + r + 1);
-      }
-      beg[i] = b;
-      len[i] = e - b;
-      maxlen = max(maxlen, e - b);
+      const bool in = r < n;
+      const int b0 = in ? __ldg(rp + r) : 0;
+      const int e0 = in ? __ldg(rp + r + 1) : 0;
+      bg[i] = b0;
+      ln[i] = e0 - b0;
     }
+  };
+  // cooperative, coalesced fetch of CW (col, val) pairs per row (streamed once with
+  // evict-first loads so L2 keeps P); absent entries: column 0, value 0
+  auto load_cv = [&](const int (&bg)[R], const int (&ln)[R], int j0, int (&cj)[R][EPN], T (&vj)[R][EPN]) {
+#pragma unroll
+    for (int i = 0; i < R; ++i)
+#pragma unroll
+      for (int u = 0; u < EPN; ++u) {
+        const int j = j0 + g + u * L::G;
+        const bool in = j < ln[i];
+        cj[i][u] = in ? __ldcs(ci + bg[i] + j) : 0;
+        vj[i][u] = in ? __ldcs(val + bg[i] + j) : Ar<T>::zero();
+      }
+  };
+
+  // Three-stage software pipeline over the warp's row batches k = 0, 1, 2, ...:
+  // while the P gathers of batch k are in flight, the (col, val) of batch k+1 and
+  // the row pointers of batch k+2 are being fetched.
+  int beg[R], len[R], begn[R], lenn[R];
+  int cj[R][EPN];
+  T vj[R][EPN];
+  load_rp(0, beg, len);
+  load_cv(beg, len, 0, cj, vj);
+  load_rp(1, begn, lenn);
+  for (long long k = 0; step_live(k); ++k) {  // warp-uniform loop
+    const long long r0 = row_of(k);
+    int cjn[R][EPN];
+    T vjn[R][EPN];
+    int begnn[R], lennn[R];
+    load_cv(begn, lenn, 0, cjn, vjn);
+    load_rp(k + 2, begnn, lennn);
+    int maxlen = 0;
+#pragma unroll
+    for (int i = 0; i < R; ++i) maxlen = max(maxlen, len[i]);
     maxlen = __reduce_max_sync(0xffffffffu, maxlen);
     T q[R][L::EPL];
 #pragma unroll
     for (int i = 0; i < R; ++i)
 #pragma unroll
       for (int e = 0; e < L::EPL; ++e) q[i][e] = Ar<T>::zero();
-    // CW entries per step: G lanes hold CW/G (col, val) pairs each, fetched cooperatively
-    // and coalesced (streamed once with evict-first loads so L2 keeps P)
-    constexpr int CW = L::G >= 8 ? L::G : 8;
-    constexpr int EPN = CW / L::G;
     for (int j0 = 0; j0 < maxlen; j0 += CW) {
-      int cj[R][EPN];
-      T vj[R][EPN];
-#pragma unroll
-      for (int i = 0; i < R; ++i)
-#pragma unroll
-        for (int u = 0; u < EPN; ++u) {
-          const int j = j0 + g + u * L::G;
-          const bool in = j < len[i];
-          cj[i][u] = in ? __ldcs(ci + beg[i] + j) : 0;
-          vj[i][u] = in ? __ldcs(val + beg[i] + j) : Ar<T>::zero();
-        }
+      if (j0 > 0) load_cv(beg, len, j0, cj, vj);  // rows longer than CW
 #pragma unroll
       for (int t = 0; t < CW; ++t) {
 #pragma unroll
@@ -282,6 +313,19 @@ __global__ void __launch_bounds__(256, FC ? 1 : 2) spmm_kernel(SpmmArgs a) {
         }
       }
     }
+    // rotate the pipeline
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      beg[i] = begn[i];
+      len[i] = lenn[i];
+      begn[i] = begnn[i];
+      lenn[i] = lennn[i];
+#pragma unroll
+      for (int u = 0; u < EPN; ++u) {
+        cj[i][u] = cjn[i][u];
+        vj[i][u] = vjn[i][u];
+      }
+    }
   }
   __syncwarp();
   if (nred > 0) red_dispatch_flush<T, S, FC>(mode0, acc0, a.partials, a.pstride, a.red[0].poff, s, smem);
@@ -295,7 +339,7 @@ __global__ void __launch_bounds__(256, FC ? 1 : 2) spmm_kernel(SpmmArgs a) {
 // rows stay in registers and all NI*R loads of a step are in flight together.
 // ============================================================================
 template <typename T, int S, bool FC, int NI, int R, bool EX>
-__global__ void __launch_bounds__(256, (NI >= 4 || FC) ? 1 : 2) upd_kernel(UpdArgs a) {
+__global__ void __launch_bounds__(256, FC ? 1 : 2) upd_kernel(UpdArgs a) {
   if (a.done && *a.done) return;
   using L = Lay<T, S>;
   constexpr int ND = Ar<T>::ND;

@@ -29,14 +29,14 @@ Solver::~Solver() {
 // blocks carry a tail of ghost rows (multi-GPU: filled by the halo exchange before each SpMM)
 void* Solver::blk() {
   void* p = nullptr;
-  const size_t rows = (size_t)(n + A->ghost_rows());
+  const size_t rows = (size_t)(n + (A ? A->ghost_rows() : 0));
   if (cudaMalloc(&p, rows * s * esz()) != cudaSuccess) return nullptr;
   owned.push_back(p);
   return p;
 }
 void* Solver::vecn() {
   void* p = nullptr;
-  const size_t rows = (size_t)(n + A->ghost_rows());
+  const size_t rows = (size_t)(n + (A ? A->ghost_rows() : 0));
   if (cudaMalloc(&p, rows * esz()) != cudaSuccess) return nullptr;
   owned.push_back(p);
   return p;

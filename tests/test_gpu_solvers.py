@@ -148,3 +148,15 @@ def test_prop1_counters(srk):
         sv.iterate(7)
         r = sv.report()
         assert r.iterations == 7 and r.matvec_cols_A == 7 * ca and r.matvec_cols_AH == 7 * cah, method
+
+
+def test_distributed_operator_single_rank_matches(srk):
+    """srk_matrix_create_dist with one rank (plan = whole matrix, no ghosts) runs the
+    same kernels: the solve is bitwise identical to the plain operator's."""
+    A, B = synth.make_config(1)
+    off = srk.partition_rows(A.row_ptr, 1)
+    Md = srk.DistMatrix(A, off, 0, need_adjoint=True)
+    M = srk.Matrix.from_csr(A)
+    X1, r1 = srk.solve(M, to_dev(B), "egl_qmr")
+    X2, r2 = srk.solve(Md, to_dev(B), "egl_qmr")
+    assert r1.iterations == r2.iterations and np.array_equal(to_np(X1), to_np(X2))
