@@ -13,6 +13,8 @@
 //                  reductions. All NI inputs of R rows are
 //                  loaded before any arithmetic (memory-level parallelism).
 #pragma once
+#include <algorithm>
+
 #include "kernels.cuh"
 
 namespace srk {
@@ -171,8 +173,8 @@ __device__ void red_dispatch_flush(int mode, RedAcc<T, S, FC>& a, double* partia
 // and every gather load is unconditional (absent entries use column 0 with a
 // zero value), so the CW*R loads of a step issue back to back.
 // ============================================================================
-template <typename T, int S, bool FC, int R, bool EX>
-__global__ void __launch_bounds__(256, FC ? 1 : 2) spmm_kernel(SpmmArgs a) {
+template <typename T, int S, bool FC, int R, bool EX, int BC = 8, bool YPRE = true, int MINB = 2>
+__global__ void __launch_bounds__(256, FC ? 1 : MINB) spmm_kernel(SpmmArgs a) {
   if (a.done && *a.done) return;
   using L = Lay<T, S>;
   extern __shared__ double smem[];
@@ -185,7 +187,6 @@ __global__ void __launch_bounds__(256, FC ? 1 : 2) spmm_kernel(SpmmArgs a) {
   // a block the CTA sweeps in order, so stencil neighbours a few grid lines away
   // are re-read from L1; all CTAs sweep neighbouring blocks concurrently, so the
   // far neighbours (other planes) are L2 hits and P streams from HBM about once.
-  constexpr int BC = 8;
   const int gin = lane / L::G;
   const long long step = (long long)(blockDim.x / 32) * L::RPW * R;
   const long long warp_off = (long long)(threadIdx.x >> 5) * L::RPW * R + (long long)gin * R;
@@ -216,18 +217,21 @@ __global__ void __launch_bounds__(256, FC ? 1 : 2) spmm_kernel(SpmmArgs a) {
 
   constexpr int CW = L::G >= 8 ? L::G : 8;  // CSR entries per step of a row
   constexpr int EPN = CW / L::G;            // (col, val) pairs per lane per step
-  // row_ptr of one batch of R rows
+  // row_ptr of one batch of R rows: (begin, end) kept raw — consuming a freshly
+  // loaded register stalls the in-order warp, so lengths are formed a step later
   auto load_rp = [&](long long k, int (&bg)[R], int (&ln)[R]) {
     const long long r0 = row_of(k);
 #pragma unroll
     for (int i = 0; i < R; ++i) {
       const long long r = r0 + i;
       const bool in = r < n;
-      const int b0 = in ? __ldg(rp + r) : 0;
-      const int e0 = in ? __ldg(rp + r + 1) : 0;
-      bg[i] = b0;
-      ln[i] = e0 - b0;
+      bg[i] = in ? __ldg(rp + r) : 0;
+      ln[i] = in ? __ldg(rp + r + 1) : 0;  // end; converted to a length by to_len
     }
+  };
+  auto to_len = [&](const int (&bg)[R], int (&ln)[R]) {
+#pragma unroll
+    for (int i = 0; i < R; ++i) ln[i] -= bg[i];
   };
   // cooperative, coalesced fetch of CW (col, val) pairs per row (streamed once with
   // evict-first loads so L2 keeps P); absent entries: column 0, value 0
@@ -250,8 +254,10 @@ __global__ void __launch_bounds__(256, FC ? 1 : 2) spmm_kernel(SpmmArgs a) {
   int cj[R][EPN];
   T vj[R][EPN];
   load_rp(0, beg, len);
+  to_len(beg, len);
   load_cv(beg, len, 0, cj, vj);
   load_rp(1, begn, lenn);
+  to_len(begn, lenn);
   for (long long k = 0; step_live(k); ++k) {  // warp-uniform loop
     const long long r0 = row_of(k);
     int cjn[R][EPN];
@@ -259,6 +265,23 @@ __global__ void __launch_bounds__(256, FC ? 1 : 2) spmm_kernel(SpmmArgs a) {
     int begnn[R], lennn[R];
     load_cv(begn, lenn, 0, cjn, vjn);
     load_rp(k + 2, begnn, lennn);
+    // epilogue operand of the first reduction, requested before the gathers
+    T yr0[R][L::EPL];
+    T yv0[R];
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      yv0[i] = Ar<T>::zero();
+#pragma unroll
+      for (int e = 0; e < L::EPL; ++e) yr0[i][e] = Ar<T>::zero();
+      const long long row = r0 + i;
+      if (YPRE && row < n && mode0 != RED_NONE) {
+        if (mode0 == RED_SUMVEC) yv0[i] = y0[row];
+        else if (mode0 != RED_NORM2 && mode0 != RED_COLNORM2) {
+          if constexpr (EX) row_load_ex_rw<T, S>(y0 + (size_t)row * S, g, yr0[i]);
+          else row_load<T, S>(y0 + (size_t)row * s, g, s, a.vec, yr0[i]);
+        }
+      }
+    }
     int maxlen = 0;
 #pragma unroll
     for (int i = 0; i < R; ++i) maxlen = max(maxlen, len[i]);
@@ -299,21 +322,26 @@ __global__ void __launch_bounds__(256, FC ? 1 : 2) spmm_kernel(SpmmArgs a) {
           const int mode = r == 0 ? mode0 : mode1;
           if (mode == RED_NONE) continue;
           const T* yp = r == 0 ? y0 : y1;
-          T y[L::EPL];
-          T yv = Ar<T>::zero();
+          if (r == 0 && YPRE) {
+            red_dispatch_row<T, S, FC>(mode, acc0, q[i], yr0[i], yv0[i], base, s, gmask);
+          } else {
+            T y[L::EPL];
+            T yv = Ar<T>::zero();
 #pragma unroll
-          for (int e = 0; e < L::EPL; ++e) y[e] = Ar<T>::zero();
-          if (mode == RED_SUMVEC) yv = yp[row];
-          else if (mode != RED_NORM2 && mode != RED_COLNORM2) {
-            if constexpr (EX) row_load_ex_rw<T, S>(yp + (size_t)row * S, g, y);
-            else row_load<T, S>(yp + (size_t)row * s, g, s, a.vec, y);
+            for (int e = 0; e < L::EPL; ++e) y[e] = Ar<T>::zero();
+            if (mode == RED_SUMVEC) yv = yp[row];
+            else if (mode != RED_NORM2 && mode != RED_COLNORM2) {
+              if constexpr (EX) row_load_ex_rw<T, S>(yp + (size_t)row * S, g, y);
+              else row_load<T, S>(yp + (size_t)row * s, g, s, a.vec, y);
+            }
+            if (r == 0) red_dispatch_row<T, S, FC>(mode, acc0, q[i], y, yv, base, s, gmask);
+            else red_dispatch_row<T, S, FC>(mode, acc1, q[i], y, yv, base, s, gmask);
           }
-          if (r == 0) red_dispatch_row<T, S, FC>(mode, acc0, q[i], y, yv, base, s, gmask);
-          else red_dispatch_row<T, S, FC>(mode, acc1, q[i], y, yv, base, s, gmask);
         }
       }
     }
     // rotate the pipeline
+    to_len(begnn, lennn);
 #pragma unroll
     for (int i = 0; i < R; ++i) {
       beg[i] = begn[i];
@@ -519,8 +547,9 @@ __global__ void __launch_bounds__(256, FC ? 1 : 2) upd_kernel(UpdArgs a) {
 }
 
 // rows per group in flight
+// rows per lane group in flight (measured on config 3: scripts/spmm_tune.cu)
 template <typename T, int S> constexpr int spmm_rows() {
-  return (Lay<T, S>::G == 1 || S >= 64) ? 1 : (Lay<T, S>::G >= 16 ? 2 : 4);
+  return (Lay<T, S>::G == 1 || S >= 64) ? 1 : 2;
 }
 template <int NI> constexpr int upd_rows() { return NI <= 1 ? 4 : (NI <= 2 ? 2 : 1); }
 template <typename T, int S> constexpr bool full_ok() { return S <= 16; }

@@ -370,14 +370,16 @@ __device__ void qmr_scalar(const CoefArgs& a, int mode) {
           W<T>(a, SL_INVXI)[c] = q;
         }
       }
-    } else if (a.phase == 2) {  // P = V - (xi delta/eps) P ; Q = W - conj(rho delta/eps) Q
+    } else if (a.phase == 2) {  // delta = <Ṽ, W̃>/(rho xi); P = V - (xi delta/eps) P ; Q = W - conj(rho delta/eps) Q
       for (int c = 0; c < ncol; ++c) {
+        const T d = Ar<T>::mul(Ar<T>::mul(W<T>(a, SL_K1)[c], W<T>(a, SL_INVRHO)[c]), W<T>(a, SL_INVXI)[c]);
+        W<T>(a, SL_DELTA)[c] = d;
         if (a.k1) {
           W<T>(a, SL_C1)[c] = Ar<T>::zero();
           W<T>(a, SL_C2)[c] = Ar<T>::zero();
           continue;
         }
-        const T d = W<T>(a, SL_DELTA)[c], e = W<T>(a, SL_EPS)[c];
+        const T e = W<T>(a, SL_EPS)[c];
         const T n1 = Ar<T>::mul(xi[c], d), n2 = Ar<T>::mul(rho[c], d);
         if (mode == 0) {
           W<T>(a, SL_C1)[c] = ldiv<T>(a, c, n1, e);
@@ -390,15 +392,17 @@ __device__ void qmr_scalar(const CoefArgs& a, int mode) {
           W<T>(a, SL_C2)[c] = Ar<T>::conj(q2);
         }
       }
-    } else if (a.phase == 3) {  // beta = eps / delta
+    } else if (a.phase == 3) {  // beta = eps / delta ; BR = beta/rho ; BX = conj(beta)/xi
       for (int c = 0; c < ncol; ++c) {
+        T be;
         if (mode == 0) {
-          W<T>(a, SL_BETA)[c] = ldiv<T>(a, c, W<T>(a, SL_EPS)[c], W<T>(a, SL_DELTA)[c]);
+          be = ldiv<T>(a, c, W<T>(a, SL_EPS)[c], W<T>(a, SL_DELTA)[c]);
         } else {
-          T q;
-          if (!sdiv<T>(a, W<T>(a, SL_EPS)[c], W<T>(a, SL_DELTA)[c], &q, BK_LANCZOS)) break;
-          W<T>(a, SL_BETA)[c] = q;
+          if (!sdiv<T>(a, W<T>(a, SL_EPS)[c], W<T>(a, SL_DELTA)[c], &be, BK_LANCZOS)) break;
         }
+        W<T>(a, SL_BETA)[c] = be;
+        W<T>(a, SL_BR)[c] = Ar<T>::mul(be, W<T>(a, SL_INVRHO)[c]);
+        W<T>(a, SL_BX)[c] = Ar<T>::mul(Ar<T>::conj(be), W<T>(a, SL_INVXI)[c]);
       }
     } else if (a.phase == 4) {  // theta, gamma, eta; f = (theta_prev gamma)^2
       for (int c = 0; c < ncol; ++c) {

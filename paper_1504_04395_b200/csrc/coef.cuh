@@ -30,7 +30,7 @@ enum Slot : int {
   SL_R2F, SL_R2I, SL_R2H, SL_R2HI, SL_SIG, SL_SIGH, SL_AC, SL_WC, SL_GQ, SL_GQN, SL_ZZ, SL_YZ, SL_YY,
   // QMR
   SL_QRHO, SL_QXI, SL_INVRHO, SL_INVXI, SL_DELTA, SL_EPS, SL_C1, SL_C2, SL_GAMP, SL_ETA, SL_THETAP, SL_F,
-  SL_RHON2, SL_XI2, SL_K1,
+  SL_RHON2, SL_XI2, SL_K1, SL_BR, SL_BX,
   // Bl-QMR
   SL_OMP, SL_TAUT, SL_TAU, SL_TOP, SL_RII, SL_RIII, SL_TR, SL_GHAT, SL_RHOB, SL_XIB, SL_RHOBN, SL_XIBN,
   SL_PEND,

@@ -530,26 +530,38 @@ struct BlBiCGStabrQ : Solver {
 // =============================================================================
 // QMR family
 // =============================================================================
-struct QMR : Solver {  // mode 0 Li, 1 Gl, 2 eGl (SURVEY App. A.2)
+// Li / Gl / eGl-QMR. The normalised Lanczos blocks V = Ṽ/ρ and
+// W = W̃/ξ are never materialised: 1/ρ and 1/ξ are folded into the coefficients
+// of the kernels that read Ṽ and W̃, and δ = <V, W> = <Ṽ, W̃>/(ρ ξ) is fused into
+// the kernel that produces Ṽ — an iteration moves 18 n x s blocks
+// instead of 20. Same recurrences as oracle/solvers.py::_qmr_li_gl.
+struct QMR : Solver {  // mode 0 Li, 1 Gl, 2 eGl
   int mode = 1;
-  void *Vt, *V, *P, *Pt, *D, *S, *Wt, *Wv, *Qv, *AHQ;
+  void *Vt, *P, *Pt, *D, *S, *Wt, *Qv, *AHQ;
   int alloc() override {
-    Vt = blk(); V = blk(); P = blk(); Pt = blk(); D = blk(); S = blk();
-    if (mode == 2) { Wt = vecn(); Wv = vecn(); Qv = vecn(); AHQ = vecn(); }
-    else { Wt = blk(); Wv = blk(); Qv = blk(); AHQ = blk(); }
+    Vt = blk(); P = blk(); Pt = blk(); D = blk(); S = blk();
+    if (mode == 2) { Wt = vecn(); Qv = vecn(); AHQ = vecn(); }
+    else { Wt = blk(); Qv = blk(); AHQ = blk(); }
     cols_A = s; cols_AH = (mode == 2) ? 1 : s;
-    return (Vt && V && P && Pt && D && S && Wt && Wv && Qv && AHQ) ? 0 : SRK_ENOMEM;
+    return (Vt && P && Pt && D && S && Wt && Qv && AHQ) ? 0 : SRK_ENOMEM;
   }
   int ws_() const { return mode == 2 ? 1 : s; }  // width of the left Lanczos block
   int nrm() const { return mode == 0 ? RED_COLNORM2 : RED_NORM2; }
+  int dmode() const { return mode == 0 ? RED_DIAG : (mode == 1 ? RED_TRACE : RED_SUMVEC); }
   Coef K(int slot, int neg = 0, int cj = 0) const { return mode == 0 ? DG(off[slot], neg, cj) : SC(off[slot], neg, cj); }
+  // Ṽ-producing reduction set: ||Ṽ||^2 and <Ṽ, W̃> (W̃ an input block, or the vector for eGl)
+  std::vector<RQ> vt_reds(int vt_src, int wt_src) const {
+    if (mode == 2) return {RQ{nrm(), vt_src, -1, nullptr, off[SL_RHON2]}, RQ{RED_SUMVEC, vt_src, -1, Wt, off[SL_K1]}};
+    return {RQ{nrm(), vt_src, -1, nullptr, off[SL_RHON2]}, RQ{dmode(), vt_src, wt_src, nullptr, off[SL_K1]}};
+  }
   int init() override {
     const size_t b = (size_t)n * s * esz();
     cudaMemcpyAsync(Vt, R, b, cudaMemcpyDeviceToDevice, c->st);
     if (mode == 2) launch_row_mean(cplx, R, Wt, n, s, nullptr, c->st);  // w̃0 = mean of the columns
     else cudaMemcpyAsync(Wt, R, b, cudaMemcpyDeviceToDevice, c->st);     // W̃0 = R0
-    e.upd(s, {Vt}, {}, {RQ{nrm(), 0, -1, nullptr, off[SL_RHON2]}});
     e.upd(ws_(), {Wt}, {}, {RQ{nrm(), 0, -1, nullptr, off[SL_XI2]}});
+    if (mode == 2) e.upd(s, {Vt}, {}, vt_reds(0, -1));
+    else e.upd(s, {Vt, Wt}, {}, vt_reds(0, 1));
     cudaMemsetAsync(P, 0, b, c->st);
     cudaMemsetAsync(D, 0, b, c->st);
     cudaMemsetAsync(S, 0, b, c->st);
@@ -557,28 +569,24 @@ struct QMR : Solver {  // mode 0 Li, 1 Gl, 2 eGl
     return coef(0);
   }
   void seg(int) override {
-    coef(1);  // 1/rho, 1/xi
-    const int dmode = mode == 0 ? RED_DIAG : (mode == 1 ? RED_TRACE : RED_SUMVEC);
+    coef(1);                   // 1/rho, 1/xi
+    coef(2, host_iter == 0);   // delta = <Ṽ, W̃>/(rho xi); c1 = xi delta/eps, c2 = conj(rho delta/eps)
+    // P = V - c1 P = Ṽ/rho - c1 P ;  Q = W - c2 Q = W̃/xi - c2 Q
     if (mode == 2) {
-      e.upd(1, {Wt}, {OutSpec{Wv, {{0, SC(off[SL_INVXI])}}}}, {});
-      e.upd(s, {Vt}, {OutSpec{V, {{0, SC(off[SL_INVRHO])}}}}, {RQ{RED_SUMVEC, O0, -1, Wv, off[SL_DELTA]}});
+      e.upd(s, {Vt, P}, {OutSpec{P, {{0, SC(off[SL_INVRHO])}, {1, SC(off[SL_C1], 1)}}}}, {});
+      e.upd(1, {Wt, Qv}, {OutSpec{Qv, {{0, SC(off[SL_INVXI])}, {1, SC(off[SL_C2], 1)}}}}, {});
     } else {
-      e.upd(s, {Vt, Wt}, {OutSpec{V, {{0, K(SL_INVRHO)}}}, OutSpec{Wv, {{1, K(SL_INVXI)}}}},
-            {RQ{dmode, O0, O1, nullptr, off[SL_DELTA]}});
+      e.upd(s, {Vt, P, Wt, Qv},
+            {OutSpec{P, {{0, K(SL_INVRHO)}, {1, K(SL_C1, 1)}}}, OutSpec{Qv, {{2, K(SL_INVXI)}, {3, K(SL_C2, 1)}}}}, {});
     }
-    coef(2, host_iter == 0);
-    if (mode == 2) {
-      e.upd(s, {V, P}, {OutSpec{P, {{0, C1()}, {1, SC(off[SL_C1], 1)}}}}, {});
-      e.upd(1, {Wv, Qv}, {OutSpec{Qv, {{0, C1()}, {1, SC(off[SL_C2], 1)}}}}, {});
-    } else {
-      e.upd(s, {V, P, Wv, Qv},
-            {OutSpec{P, {{0, C1()}, {1, K(SL_C1, 1)}}}, OutSpec{Qv, {{2, C1()}, {3, K(SL_C2, 1)}}}}, {});
-    }
-    e.spmm(false, P, Pt, s, {RQ{dmode, 0, -1, Qv, off[SL_EPS]}});  // P~ = A P ; eps = <P~, Q>
-    e.spmm(true, Qv, AHQ, ws_(), {});
-    coef(3);  // beta
-    e.upd(s, {Pt, V}, {OutSpec{Vt, {{0, C1()}, {1, K(SL_BETA, 1)}}}}, {RQ{nrm(), O0, -1, nullptr, off[SL_RHON2]}});
-    e.upd(ws_(), {AHQ, Wv}, {OutSpec{Wt, {{0, C1()}, {1, K(SL_BETA, 1, 1)}}}}, {RQ{nrm(), O0, -1, nullptr, off[SL_XI2]}});
+    e.spmm(false, P, Pt, s, {RQ{dmode(), 0, -1, Qv, off[SL_EPS]}});  // P~ = A P ; eps = <P~, Q>
+    e.spmm(true, Qv, AHQ, ws_(), {});                                // A^H Q
+    coef(3);  // beta = eps/delta ; BR = beta/rho ; BX = conj(beta)/xi
+    // W̃ = A^H Q - conj(beta) W = A^H Q - (conj(beta)/xi) W̃   (first: Ṽ's kernel reads the new W̃)
+    e.upd(ws_(), {AHQ, Wt}, {OutSpec{Wt, {{0, C1()}, {1, K(SL_BX, 1)}}}}, {RQ{nrm(), O0, -1, nullptr, off[SL_XI2]}});
+    // Ṽ = P~ - beta V = P~ - (beta/rho) Ṽ, with ||Ṽ||^2 and the next <Ṽ, W̃>
+    if (mode == 2) e.upd(s, {Pt, Vt}, {OutSpec{Vt, {{0, C1()}, {1, K(SL_BR, 1)}}}}, vt_reds(O0, -1));
+    else e.upd(s, {Pt, Vt, Wt}, {OutSpec{Vt, {{0, C1()}, {1, K(SL_BR, 1)}}}}, vt_reds(O0, 2));
     coef(4);  // theta, gamma, eta, f
     e.upd(s, {P, D, Pt, S, X, R},
           {OutSpec{D, {{0, K(SL_ETA)}, {1, K(SL_F)}}},

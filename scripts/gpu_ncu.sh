@@ -4,6 +4,6 @@ timeout 1500 python -m pytest tests/test_gpu_kernels.py tests/test_gpu_solvers.p
 timeout 900 python bench.py --no-cpu > gpurun_out/bench.log 2>&1; echo "rc=$?" >> gpurun_out/bench.log
 SMALL="python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu"
 timeout 600 $SMALL > gpurun_out/bench_small.log 2>&1; echo "plain rc=$?" >> gpurun_out/bench_small.log
-timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k 'regex:spmm_kernel<double, .int.16' -s 1 -c 1 -o gpurun_out/prof_spmm -f $SMALL > gpurun_out/ncu_spmm.log 2>&1; echo "rc=$?" >> gpurun_out/ncu_spmm.log
+timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k 'regex:spmm.*kernel<double, .int.16' -s 1 -c 1 -o gpurun_out/prof_spmm -f $SMALL > gpurun_out/ncu_spmm.log 2>&1; echo "rc=$?" >> gpurun_out/ncu_spmm.log
 timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k 'regex:upd_kernel<double, .int.16, .bool.0, .int.6' -s 1 -c 1 -o gpurun_out/prof_upd -f $SMALL > gpurun_out/ncu_upd.log 2>&1; echo "rc=$?" >> gpurun_out/ncu_upd.log
 tail -n 15 gpurun_out/t_gpu.log; tail -n 2 gpurun_out/bench.log gpurun_out/ncu_spmm.log gpurun_out/ncu_upd.log

@@ -1,0 +1,96 @@
+// spmm_tune.cu — microbenchmark of spmm_kernel variants on the config-3 operator
+// (256^3 7-point stencil, s = 16, FP64) with the eGl SUMVEC epilogue. Builds the
+// CSR on the host, times each variant with CUDA events (warm, 20 launches), and
+// prints the achieved algorithmic GB/s. Tuning aid only (not part of the product).
+//   nvcc -std=c++17 -O3 -gencode arch=compute_100a,code=sm_100a -I paper_1504_04395_b200/csrc \
+//        scripts/spmm_tune.cu -o scripts/spmm_tune
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#include "block_kernels.cuh"
+
+using namespace srk;
+
+#define CK(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) { printf("%s: %s\n", #x, cudaGetErrorString(e_)); exit(1); } } while (0)
+
+template <int R, int BC, bool YPRE, int MINB>
+float run(const SpmmArgs& a0, int nsm, double bytes, const char* name) {
+  auto k = spmm_kernel<double, 16, false, R, true, BC, YPRE, MINB>;
+  int occ = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, 256, 8 * 8 * 2));
+  const int grid = nsm * occ;
+  SpmmArgs a = a0;
+  for (int w = 0; w < 3; ++w) k<<<grid, 256, 8 * 8 * 2, 0>>>(a);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0);
+  const int it = 20;
+  for (int w = 0; w < it; ++w) k<<<grid, 256, 8 * 8 * 2, 0>>>(a);
+  cudaEventRecord(e1);
+  CK(cudaEventSynchronize(e1));
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  ms /= it;
+  printf("%-34s occ %d grid %5d  %.3f ms  %.0f GB/s\n", name, occ, grid, ms, bytes / ms / 1e6);
+  return ms;
+}
+
+int main(int argc, char** argv) {
+  const int m = argc > 1 ? atoi(argv[1]) : 256;
+  const long long n = (long long)m * m * m;
+  const int s = 16;
+  std::vector<int> rp(n + 1);
+  std::vector<int> ci;
+  std::vector<double> va;
+  ci.reserve(7 * n);
+  va.reserve(7 * n);
+  const double h = 1.0 / (m + 1), c[3] = {50, 30, 10};
+  long long strides[3] = {1, m, (long long)m * m};
+  for (long long i = 0; i < n; ++i) {
+    rp[i] = (int)ci.size();
+    const int x = i % m, y = (i / m) % m, z = i / ((long long)m * m);
+    const int co[3] = {x, y, z};
+    // ascending columns: -z, -y, -x, diag, +x, +y, +z
+    for (int d = 2; d >= 0; --d)
+      if (co[d] > 0) { ci.push_back((int)(i - strides[d])); va.push_back(-1.0 - c[d] * h / 2); }
+    ci.push_back((int)i);
+    va.push_back(6.0);
+    for (int d = 0; d < 3; ++d)
+      if (co[d] < m - 1) { ci.push_back((int)(i + strides[d])); va.push_back(-1.0 + c[d] * h / 2); }
+  }
+  rp[n] = (int)ci.size();
+  const long long nnz = ci.size();
+  int *drp, *dci;
+  double *dva, *P, *Q, *y, *part;
+  CK(cudaMalloc(&drp, sizeof(int) * (n + 1)));
+  CK(cudaMalloc(&dci, sizeof(int) * nnz));
+  CK(cudaMalloc(&dva, sizeof(double) * nnz));
+  CK(cudaMalloc(&P, sizeof(double) * n * s));
+  CK(cudaMalloc(&Q, sizeof(double) * n * s));
+  CK(cudaMalloc(&y, sizeof(double) * n));
+  CK(cudaMalloc(&part, sizeof(double) * 4096));
+  CK(cudaMemcpy(drp, rp.data(), sizeof(int) * (n + 1), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(dci, ci.data(), sizeof(int) * nnz, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(dva, va.data(), sizeof(double) * nnz, cudaMemcpyHostToDevice));
+  CK(cudaMemset(P, 0, sizeof(double) * n * s));
+  CK(cudaMemset(y, 0, sizeof(double) * n));
+  int nsm = 148;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+  SpmmArgs a{};
+  a.row_ptr = drp; a.col_idx = dci; a.val = dva; a.P = P; a.Q = Q; a.n = n; a.s = s; a.vec = 1;
+  a.nred = 1; a.red[0].mode = RED_SUMVEC; a.red[0].yext = y; a.red[0].poff = 0; a.partials = part; a.pstride = 1;
+  const double bytes = (n + 1) * 4.0 + nnz * 12.0 + 2.0 * n * s * 8 + n * 8.0;
+  printf("n %lld nnz %lld algorithmic %.3f GB\n", n, nnz, bytes / 1e9);
+  run<2, 8, true, 2>(a, nsm, bytes, "R2 BC8 ypre minb2 (library)");
+  run<2, 4, true, 2>(a, nsm, bytes, "R2 BC4 ypre minb2");
+  run<2, 16, true, 2>(a, nsm, bytes, "R2 BC16 ypre minb2");
+  run<2, 64, true, 2>(a, nsm, bytes, "R2 BC64 ypre minb2");
+  run<2, 8, true, 3>(a, nsm, bytes, "R2 BC8 ypre minb3");
+  run<3, 8, true, 2>(a, nsm, bytes, "R3 BC8 ypre minb2");
+  run<1, 8, true, 3>(a, nsm, bytes, "R1 BC8 ypre minb3");
+  run<1, 8, true, 4>(a, nsm, bytes, "R1 BC8 ypre minb4");
+  run<2, 8, true, 2>(a, nsm, bytes, "R2 BC8 ypre minb2 (repeat)");
+  return 0;
+}
