@@ -168,6 +168,60 @@ def power_law(n: int, seed: int, a: float = 1.19794, lmax: int = 512, lmin_scale
                dict(kind="power_law", seed=seed, a=a, lmax=lmax))
 
 
+def lattice_4d(L: int, kappa: float = 0.12, seed: int = 3, dof: int = 12, chunk: int = 4096) -> CSR:
+    """Config 4 (reading G23): periodic L^4 lattice, `dof`
+    complex unknowns per site, A = I - kappa*H with H a nearest-neighbour coupling
+    whose 8 blocks per site (order +x, -x, +y, -y, +z, -z, +t, -t; site index
+    x + L y + L^2 z + L^3 t, row = dof*site + a) have entries CN(0, 1/6).
+    Stands in for the paper's Wilson-Dirac Ex. 4, whose gauge field is
+    not available. Matrix RNG default_rng(seed + 1000), drawn in chunks of `chunk`
+    sites: re = standard_normal((c, 8, dof, dof)), then im of the same shape."""
+    if L < 3:
+        raise ValueError("L >= 3 keeps the 8 neighbours of a site distinct")
+    rng = np.random.default_rng(seed + 1000)
+    nsites = L ** 4
+    n = nsites * dof
+    site = np.arange(nsites, dtype=np.int64)
+    co = [(site // L ** d) % L for d in range(4)]
+    nbr = np.empty((nsites, 8), dtype=np.int64)
+    for d in range(4):
+        for k, step in enumerate((+1, -1)):
+            c2 = list(co)
+            c2[d] = (co[d] + step) % L
+            nbr[:, 2 * d + k] = c2[0] + L * c2[1] + L ** 2 * c2[2] + L ** 3 * c2[3]
+    blocks = np.empty((nsites, 8, dof, dof), dtype=np.complex128)
+    for start in range(0, nsites, chunk):
+        c = min(chunk, nsites - start)
+        re = rng.standard_normal((c, 8, dof, dof))
+        im = rng.standard_normal((c, 8, dof, dof))
+        blocks[start:start + c] = (re + 1j * im) * np.sqrt(1.0 / 12.0)
+    vals = -kappa * blocks
+    # row (site, a): the 8 neighbour blocks (dof columns each) and the identity's
+    # diagonal entry, in ascending column order -> 8*dof + 1 entries per row
+    cols_site = np.concatenate([nbr, site[:, None]], axis=1)              # (nsites, 9) block columns
+    order = np.argsort(cols_site, axis=1, kind="stable")
+    cols_site = np.take_along_axis(cols_site, order, axis=1)
+    full = np.zeros((nsites, 9, dof, dof), dtype=np.complex128)
+    full[:, :8] = vals
+    full[:, 8] = np.eye(dof)
+    full = np.take_along_axis(full, order[:, :, None, None], axis=1)
+    own = (order == 8)                                                     # (nsites, 9): the identity block
+    col = cols_site[:, None, :, None] * dof + np.arange(dof)[None, None, None, :]   # (nsites, 1, 9, dof)
+    col = np.broadcast_to(col, (nsites, dof, 9, dof))
+    val = np.transpose(full, (0, 2, 1, 3))                                 # [site, a, blk, b]
+    a_idx = np.arange(dof)[None, :, None, None]
+    b_idx = np.arange(dof)[None, None, None, :]
+    keep = ~own[:, None, :, None] | (a_idx == b_idx)                       # identity block: diagonal only
+    keep = np.broadcast_to(keep, (nsites, dof, 9, dof))
+    col = col[keep].reshape(n, 8 * dof + 1)
+    val = val[keep].reshape(n, 8 * dof + 1)
+    row_ptr = np.arange(0, n * (8 * dof + 1) + 1, 8 * dof + 1, dtype=np.int64)
+    A = CSR(n, row_ptr, np.ascontiguousarray(col.reshape(-1).astype(np.int32)),
+            np.ascontiguousarray(val.reshape(-1)))
+    A.meta = dict(kind="lattice_4d", L=L, kappa=kappa, seed=seed, dof=dof)
+    return A
+
+
 def input_hash(A: CSR, B: np.ndarray) -> str:
     h = hashlib.sha256()
     for arr in (A.row_ptr, A.col_idx, A.values, B):
@@ -186,6 +240,8 @@ CONFIGS = {
             shift=-0.1j, s=8, seed=1, methods=("bl_bicg_rq", "bl_qmr", "bl_bicgstab_rq")),
     3: dict(name="cfg3_conv_diff_3d_256", dims=3, m=256, c=(50.0, 30.0, 10.0), dtype="f64", s=16, seed=2,
             methods=("egl_qmr", "gl_bicgstab")),
+    4: dict(name="cfg4_lattice_32^4_c128", L=32, dtype="c128", s=12, seed=3, kappa=0.12,
+            methods=("li_bicgstab", "gl_bicgstab", "bl_bicgstab", "bl_bicgstab_rq")),
     5: dict(name="cfg5_power_law_4M", n=1 << 22, dtype="f64", s=32, seed=4, methods=("egl_bicg",)),
 }
 
@@ -202,6 +258,8 @@ def make_config(cfg: int, m: int | None = None, s: int | None = None, n: int | N
             A = conv_diff_2d(mm, c["c"], dt, c.get("shift", 0.0))
         else:
             A = conv_diff_3d(mm, c["c"], dt, c.get("shift", 0.0))
+    elif cfg == 4:
+        A = lattice_4d(c["L"] if m is None else m, c["kappa"], c["seed"])
     elif cfg == 5:
         nn = c["n"] if n is None else n
         A = power_law(nn, c["seed"])

@@ -155,3 +155,76 @@ def test_full_size_config3_spmm_sampled(srk):
     full = As @ B
     t_ref = np.vdot(Rtn.ravel(), full.ravel())
     assert abs(to_np(tr)[0] - t_ref) <= 1e-11 * np.linalg.norm(full) * np.linalg.norm(Rtn)
+
+
+@pytest.mark.parametrize("s", [1, 2, 4, 8, 16, 32, 64])
+def test_config5_spmm_gram_sweep(srk, s):
+    """Config 5's SpMM+Gram sweep (power-law rows up to 512, uniform columns) at
+    n = 2^16: the product and the fused reductions (FULL up to s = 16; trace, sum
+    and norms at every s) against the oracle."""
+    A = synth.power_law(1 << 16, seed=4)
+    As = A.to_scipy()
+    M = srk.Matrix.from_csr(A, need_adjoint=False)
+    P = synth.random_rhs(A.n, s, 4)
+    Y = synth.random_rhs(A.n, s, 5)
+    modes = ["trace", "norm2", "sumvec"] + (["full"] if s <= 16 else [])
+    ref = As @ P
+    for mode in modes:
+        Yd = to_dev(Y[:, 0].copy()) if mode == "sumvec" else to_dev(Y)
+        Q, g = srk.spmm_block(M, to_dev(P), gram=mode, Y=Yd)
+        Q, g = to_np(Q), to_np(g)
+        assert np.max(np.abs(Q - ref)) <= 1e-12 * np.max(np.abs(ref))
+        expect = {"trace": lambda: np.array([OL.trace_inner(ref, Y)]), "norm2": lambda: np.array([OL.fro2(ref)]),
+                  "sumvec": lambda: np.array([OL.sum_inner(Y[:, 0], ref)]), "full": lambda: OL.gram(Y, ref)}[mode]()
+        assert rel(g.reshape(expect.shape), expect) < 1e-11, mode
+
+
+def test_full_size_config5_sampled(srk):
+    """Config 5 at full size (n = 2^22, ~67M nnz, s = 32) in the launch configuration
+    of its sweep: 4096 sampled rows of A P against the oracle's products, and the
+    fused sum(y^H Q) against numpy."""
+    import torch
+    A = synth.power_law(1 << 22, seed=4)
+    M = srk.Matrix.from_csr(A, need_adjoint=False)
+    B = synth.random_rhs(A.n, 32, 4)
+    y = synth.random_rhs(A.n, 1, 6)[:, 0].copy()
+    Q, sv = srk.spmm_block(M, to_dev(B), gram="sumvec", Y=to_dev(y))
+    rows = np.sort(np.random.default_rng(1).choice(A.n, 4096, replace=False))
+    As = A.to_scipy()
+    ref = As[rows] @ B
+    Qs = to_np(Q[torch.from_numpy(rows).cuda()])
+    assert np.max(np.abs(Qs - ref)) <= 1e-12 * np.max(np.abs(ref))
+    full = As @ B
+    assert abs(to_np(sv)[0] - OL.sum_inner(y, full)) <= 1e-11 * np.linalg.norm(full) * np.linalg.norm(y) * np.sqrt(32)
+
+
+def test_full_size_config2_sampled(srk):
+    """Config 2 at full size (128^3 complex, s = 8): sampled rows of A P, of A^H P,
+    and the fused s x s Gram P^H (A P) against numpy."""
+    import torch
+    A, B = synth.make_config(2)
+    M = srk.Matrix.from_csr(A, need_adjoint=True)
+    Bd = to_dev(B)
+    Q, G = srk.spmm_block(M, Bd, gram="full", Y=Bd)
+    QH = srk.spmm_block(M, Bd, adjoint=True)
+    rows = np.sort(np.random.default_rng(2).choice(A.n, 4096, replace=False))
+    As = A.to_scipy()
+    sel = torch.from_numpy(rows).cuda()
+    assert np.max(np.abs(to_np(Q[sel]) - As[rows] @ B)) <= 1e-12 * np.max(np.abs(B)) * 8
+    AH = As.conj().T.tocsr()
+    assert np.max(np.abs(to_np(QH[sel]) - AH[rows] @ B)) <= 1e-12 * np.max(np.abs(B)) * 8
+    full = As @ B
+    assert rel(to_np(G), OL.gram(B, full)) < 1e-11
+
+
+def test_mid_size_config4_lattice_sampled(srk):
+    """Config 4's operator at 16^4 sites (n = 786,432, 76M nnz, complex, s = 12):
+    sampled rows of A P against the oracle's product."""
+    import torch
+    A, B = synth.make_config(4, m=16)
+    M = srk.Matrix.from_csr(A, need_adjoint=False)
+    Q = srk.spmm_block(M, to_dev(B))
+    rows = np.sort(np.random.default_rng(3).choice(A.n, 4096, replace=False))
+    As = A.to_scipy()
+    ref = As[rows] @ B
+    assert np.max(np.abs(to_np(Q[torch.from_numpy(rows).cuda()]) - ref)) <= 1e-12 * np.max(np.abs(ref))

@@ -270,3 +270,31 @@ def test_reduction_order_spread_economic(method, bound):
     a = oracle.solve(method, As, B, tol=1e-300, maxit=20, record=20, order="blas")
     b = oracle.solve(method, As, B, tol=1e-300, maxit=20, record=20, order="seq")
     assert max(rel(x, y) for x, y in zip(a.Xs, b.Xs)) < bound
+
+
+def test_lattice_generator_structure():
+    """Config 4 generator (reading G23): 8 dof*dof neighbour blocks + identity per
+    row (8*12 + 1 = 97 entries), periodic nearest-neighbour pattern (block (x, y)
+    present iff (y, x) present), and spectral radius of H close to the circular-law
+    value sqrt(8 * 12 * 1/6) = 4 for i.i.d. CN(0, 1/6) blocks (4.06)."""
+    import scipy.sparse.linalg as sla
+    A = synth.lattice_4d(4)
+    As = A.to_scipy()
+    assert A.nnz == 97 * A.n
+    assert np.allclose(As.diagonal(), 1.0)
+    pat = (As != 0).astype(np.int8)
+    assert (pat != pat.T).nnz == 0
+    H = (sp.identity(A.n) - As) / 0.12
+    rho = abs(sla.eigs(H.tocsc(), k=1, which="LM", return_eigenvectors=False)[0])
+    assert 3.5 < rho < 4.6
+
+
+@pytest.mark.parametrize("method", ["li_bicgstab", "gl_bicgstab", "bl_bicgstab", "bl_bicgstab_rq"])
+def test_lattice_bicgstab_converges(method):
+    """Config 4's methods on a 4^4 lattice converge to the direct solution."""
+    A, B = synth.make_config(4, m=4)
+    As = A.to_scipy()
+    r = oracle.solve(method, As, B, tol=1e-10, maxit=200)
+    assert r.outcome == "converged"
+    Xs = spla.spsolve(As.tocsc(), B)
+    assert rel(r.X, Xs) < 1e-8
