@@ -104,15 +104,20 @@ def algorithmic_spmm_bytes(A, s, esz, operand_bytes):
 
 
 def iteration_bytes_egl_qmr(A, s, esz):
-    """Algorithmic bytes of one eGl-QMR iteration in this build's phase plan
-    (DESIGN.md §Kernels): blocks moved B = n*s*esz, vectors v = n*esz."""
+    """Algorithmic bytes of one eGl-QMR iteration in this build's fused phase plan
+    (DESIGN.md §7): B = one n x s block, v = one n-vector, A = one CSR operator.
+      P = Ṽ/rho - c1 P          Ṽ r, P r, P w                 3B
+      q = w̃/xi - c2 q           w̃ r, q r, q w                 3v
+      P~ = A P, sum(q^H P~)     P r, P~ w, q r, A             2B + v + A
+      A^H q                     q r, A^H q w, A^H             2v + A
+      w̃ = A^H q - conj(b)/xi w̃  A^H q r, w̃ r, w̃ w             3v
+      Ṽ = P~ - b/rho Ṽ (+norm, <Ṽ,w̃>)  P~ r, Ṽ r, Ṽ w, w̃ r   3B + v
+      D, S, X, R (+||R||)       P, D, P~, S, X, R r; D, S, X, R w   10B
+    total 18B + 10v + 2A."""
     B = A.n * s * esz
     v = A.n * esz
     a_bytes = (A.n + 1) * 4 + A.nnz * (4 + esz)
-    # V,W scale (Vt r, V w) 2B + 2v ; P,q update (V r, P rw) 3B + 3v ; SpMM (P r, Pt w, q r) 2B + v + A ;
-    # A^H q (q r, AHq w) 2v + A^H ; Vt (Pt r, V r, Vt w) 3B ; Wt (AHq, w r, wt w) 3v ;
-    # D,S,X,R (P,D,Pt,S,X,R r; D,S,X,R w) 10B
-    return 20 * B + 12 * v + 2 * a_bytes
+    return 18 * B + 10 * v + 2 * a_bytes
 
 
 def oracle_iteration_rate(method, A, B, iters: int):

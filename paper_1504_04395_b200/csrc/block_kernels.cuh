@@ -366,8 +366,10 @@ __global__ void __launch_bounds__(256, FC ? 1 : MINB) spmm_kernel(SpmmArgs a) {
 // visited by unrolled loops, absent terms skipped by a uniform branch), so the
 // rows stay in registers and all NI*R loads of a step are in flight together.
 // ============================================================================
-template <typename T, int S, bool FC, int NI, int R, bool EX>
-__global__ void __launch_bounds__(256, FC ? 1 : 2) upd_kernel(UpdArgs a) {
+// MINB = 4 (<= 64 registers, 32 warps per SM) measured best for every input count on
+// config-3 blocks (scripts/upd_tune.cu: 90-100% of the measured copy bandwidth)
+template <typename T, int S, bool FC, int NI, int R, bool EX, bool STREAM = false, int MINB = 4>
+__global__ void __launch_bounds__(256, FC ? 1 : MINB) upd_kernel(UpdArgs a) {
   if (a.done && *a.done) return;
   using L = Lay<T, S>;
   constexpr int ND = Ar<T>::ND;
@@ -470,7 +472,8 @@ __global__ void __launch_bounds__(256, FC ? 1 : 2) upd_kernel(UpdArgs a) {
 #pragma unroll
         for (int e = 0; e < L::EPL; ++e) xin[b][i][e] = Ar<T>::zero();
         if (b < nin && r0 + i < n) {
-          if constexpr (EX) row_load_ex_rw<T, S>(reinterpret_cast<const T*>(a.in[b]) + (size_t)(r0 + i) * S, g, xin[b][i]);
+          if constexpr (EX && STREAM) row_load_ex_cs<T, S>(reinterpret_cast<const T*>(a.in[b]) + (size_t)(r0 + i) * S, g, xin[b][i]);
+          else if constexpr (EX) row_load_ex_rw<T, S>(reinterpret_cast<const T*>(a.in[b]) + (size_t)(r0 + i) * S, g, xin[b][i]);
           else row_load<T, S>(reinterpret_cast<const T*>(a.in[b]) + (size_t)(r0 + i) * s, g, s, a.vec, xin[b][i]);
         }
       }
@@ -496,7 +499,8 @@ __global__ void __launch_bounds__(256, FC ? 1 : 2) upd_kernel(UpdArgs a) {
               if (kind != CK_NONE) apply(xo[o], xo[b], kind, cs + s_cslot[o][MAX_IN + b]);
             }
             if (a.out[o]) {
-              if constexpr (EX) row_store_ex<T, S>(reinterpret_cast<T*>(a.out[o]) + (size_t)row * S, g, xo[o]);
+              if constexpr (EX && STREAM) row_store_ex_cs<T, S>(reinterpret_cast<T*>(a.out[o]) + (size_t)row * S, g, xo[o]);
+              else if constexpr (EX) row_store_ex<T, S>(reinterpret_cast<T*>(a.out[o]) + (size_t)row * S, g, xo[o]);
               else row_store<T, S>(reinterpret_cast<T*>(a.out[o]) + (size_t)row * s, g, s, a.vec, xo[o]);
             }
           }

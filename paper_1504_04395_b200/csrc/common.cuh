@@ -145,6 +145,39 @@ __device__ __forceinline__ void row_store_ex(T* __restrict__ p, int g, const T (
     }
   }
 }
+// streaming (evict-first) variants: data touched once per kernel
+template <typename T, int S>
+__device__ __forceinline__ void row_load_ex_cs(const T* p, int g, T (&v)[Lay<T, S>::EPL]) {
+  using L = Lay<T, S>;
+#pragma unroll
+  for (int c = 0; c < L::CPL; ++c) {
+    const int ch = g + c * L::G;
+    const bool ok = (L::NCH % L::G == 0) || ch < L::NCH;
+    if constexpr (L::EPC == 2) {
+      double2 t = make_double2(0.0, 0.0);
+      if (ok) t = __ldcs(reinterpret_cast<const double2*>(p) + ch);
+      v[c * 2] = t.x;
+      v[c * 2 + 1] = t.y;
+    } else {
+      T t = Ar<T>::zero();
+      if (ok) t = __ldcs(p + ch);
+      v[c] = t;
+    }
+  }
+}
+template <typename T, int S>
+__device__ __forceinline__ void row_store_ex_cs(T* p, int g, const T (&v)[Lay<T, S>::EPL]) {
+  using L = Lay<T, S>;
+#pragma unroll
+  for (int c = 0; c < L::CPL; ++c) {
+    const int ch = g + c * L::G;
+    const bool ok = (L::NCH % L::G == 0) || ch < L::NCH;
+    if (ok) {
+      if constexpr (L::EPC == 2) __stcs(reinterpret_cast<double2*>(p) + ch, make_double2(v[c * 2], v[c * 2 + 1]));
+      else __stcs(p + ch, v[c]);
+    }
+  }
+}
 // row-local loads with a plain ld.global (data written earlier in the same kernel sequence)
 template <typename T, int S>
 __device__ __forceinline__ void row_load_ex_rw(const T* p, int g, T (&v)[Lay<T, S>::EPL]) {

@@ -84,13 +84,11 @@ int main(int argc, char** argv) {
   const double bytes = (n + 1) * 4.0 + nnz * 12.0 + 2.0 * n * s * 8 + n * 8.0;
   printf("n %lld nnz %lld algorithmic %.3f GB\n", n, nnz, bytes / 1e9);
   run<2, 8, true, 2>(a, nsm, bytes, "R2 BC8 ypre minb2 (library)");
-  run<2, 4, true, 2>(a, nsm, bytes, "R2 BC4 ypre minb2");
-  run<2, 16, true, 2>(a, nsm, bytes, "R2 BC16 ypre minb2");
-  run<2, 64, true, 2>(a, nsm, bytes, "R2 BC64 ypre minb2");
-  run<2, 8, true, 3>(a, nsm, bytes, "R2 BC8 ypre minb3");
-  run<3, 8, true, 2>(a, nsm, bytes, "R3 BC8 ypre minb2");
-  run<1, 8, true, 3>(a, nsm, bytes, "R1 BC8 ypre minb3");
+  run<2, 8, true, 4>(a, nsm, bytes, "R2 BC8 ypre minb4");
+  run<2, 8, false, 4>(a, nsm, bytes, "R2 BC8 noypre minb4");
+  run<1, 8, false, 4>(a, nsm, bytes, "R1 BC8 noypre minb4");
   run<1, 8, true, 4>(a, nsm, bytes, "R1 BC8 ypre minb4");
-  run<2, 8, true, 2>(a, nsm, bytes, "R2 BC8 ypre minb2 (repeat)");
+  run<2, 1, true, 4>(a, nsm, bytes, "R2 BC1 ypre minb4");
+  run<4, 8, false, 4>(a, nsm, bytes, "R4 BC8 noypre minb4");
   return 0;
 }
