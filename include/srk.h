@@ -189,6 +189,8 @@ typedef struct {
   int poll_every;      /* host reads the device convergence flag every k iterations (default 8) */
   int record_history;  /* keep ||R_k||_F/||R0||_F per iteration (srk_solver_history) */
   int check_true_residual; /* confirm convergence with B - AX (reading G26; default 1) */
+  int use_graph;       /* replay the iterations between two polls as one CUDA graph (default 1;
+                          off while srk_solver_profile is on) */
 } srk_opts;
 
 /* Full solve (a1-a7): B, X device n x s blocks; X holds X0 on entry and the

@@ -48,7 +48,8 @@ class _Csr(ctypes.Structure):
 
 class _Opts(ctypes.Structure):
     _fields_ = [("tol", ctypes.c_double), ("maxit", ctypes.c_int), ("poll_every", ctypes.c_int),
-                ("record_history", ctypes.c_int), ("check_true_residual", ctypes.c_int)]
+                ("record_history", ctypes.c_int), ("check_true_residual", ctypes.c_int),
+                ("use_graph", ctypes.c_int)]
 
 
 class _Halo(ctypes.Structure):
@@ -472,19 +473,19 @@ def _report(r: _Report) -> Report:
                   r.seconds, r.kernel_launches)
 
 
-def _opts(tol, maxit, poll_every=8, check_true_residual=True):
-    return _Opts(float(tol), int(maxit), int(poll_every), 1, int(check_true_residual))
+def _opts(tol, maxit, poll_every=8, check_true_residual=True, use_graph=True):
+    return _Opts(float(tol), int(maxit), int(poll_every), 1, int(check_true_residual), int(use_graph))
 
 
 class Solver:
     """Stepping interface (srk_solver_*): lock-step parity and benchmarking."""
 
     def __init__(self, A: Matrix, s: int, method: str, tol: float = 1e-8, maxit: int = 2000, poll_every: int = 8,
-                 check_true_residual: bool = True):
+                 check_true_residual: bool = True, use_graph: bool = True):
         if method not in METHOD_ID:
             raise SrkError(f"unknown method {method}")
         self.A, self.s, self.method = A, s, method
-        o = _opts(tol, maxit, poll_every, check_true_residual)
+        o = _opts(tol, maxit, poll_every, check_true_residual, use_graph)
         h = ctypes.c_void_p()
         _check(_lib.srk_solver_create(A.ctx.h, A.h, s, METHOD_ID[method], ctypes.byref(o), ctypes.byref(h)),
                "srk_solver_create")

@@ -343,12 +343,14 @@ static void fill_opts(srk_opts* o, const srk_opts* in) {
   o->poll_every = 8;
   o->record_history = 1;
   o->check_true_residual = 1;
+  o->use_graph = 1;
   if (in) {
     if (in->tol > 0) o->tol = in->tol;
     if (in->maxit > 0) o->maxit = in->maxit;
     if (in->poll_every > 0) o->poll_every = in->poll_every;
     o->record_history = in->record_history;
     o->check_true_residual = in->check_true_residual;
+    o->use_graph = in->use_graph;
   }
 }
 

@@ -19,6 +19,8 @@ static size_t slot_doubles(int s) {
 }
 
 Solver::~Solver() {
+  if (gexec) cudaGraphExecDestroy(gexec);
+  if (cap_st) cudaStreamDestroy(cap_st);
   for (void* p : owned) cudaFree(p);
   if (ws) cudaFree(ws);
   if (ctl) cudaFree(ctl);
@@ -161,6 +163,16 @@ int Solver::iterate(int k) {
       host_iter = dev_iter;
       int launched = 0;
       while (host_iter < target && launched < poll) {
+        // after the first iteration every iteration launches the same kernels with the
+        // same arguments: replay a captured CUDA graph of `poll` iterations
+        if (o.use_graph && !prof.on && host_iter > 0 && launched == 0 && target - host_iter >= poll && poll > 1) {
+          if (capture(poll)) return SRK_ECUDA;
+          if (cudaGraphLaunch(gexec, c->st) != cudaSuccess) return SRK_ECUDA;
+          e.nlaunch += graph_launches;
+          host_iter += poll;
+          launched += poll;
+          continue;
+        }
         for (int q = 0; q < nseg(); ++q) seg(q);
         launch_end_iter(ctl, c->st);
         e.nlaunch++;
@@ -225,6 +237,44 @@ int Solver::iterate(int k) {
   frozen = ctl_host[CTL_NFROZEN];
   if (e.err) return SRK_ECUDA;
   return SRK_OK;
+}
+
+// Capture `iters` iterations on a private stream (the caller's stream may be the
+// legacy default stream, which cannot be captured) into an executable graph;
+// re-captured only if the graph's baked-in scratch buffer moved.
+int Solver::capture(int iters) {
+  if (gexec && graph_iters == iters && graph_partials == c->partials) return 0;
+  if (gexec) {
+    cudaGraphExecDestroy(gexec);
+    gexec = nullptr;
+  }
+  if (!cap_st && cudaStreamCreateWithFlags(&cap_st, cudaStreamNonBlocking) != cudaSuccess) return SRK_ECUDA;
+  cudaStream_t user = c->st;
+  // the scratch partials must not be reallocated inside the capture
+  cudaStreamSynchronize(user);
+  c->st = cap_st;
+  const long long l0 = e.nlaunch;
+  cudaGraph_t g = nullptr;
+  if (cudaStreamBeginCapture(cap_st, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+    c->st = user;
+    return SRK_ECUDA;
+  }
+  for (int i = 0; i < iters; ++i) {
+    for (int q = 0; q < nseg(); ++q) seg(q);
+    launch_end_iter(ctl, cap_st);
+    e.nlaunch++;
+  }
+  cudaError_t ce = cudaStreamEndCapture(cap_st, &g);
+  c->st = user;
+  if (ce != cudaSuccess || e.err) return SRK_ECUDA;
+  graph_launches = e.nlaunch - l0;
+  e.nlaunch = l0;
+  ce = cudaGraphInstantiate(&gexec, g, 0);
+  cudaGraphDestroy(g);
+  if (ce != cudaSuccess) return SRK_ECUDA;
+  graph_iters = iters;
+  graph_partials = c->partials;
+  return 0;
 }
 
 int Solver::residual(void* out, int64_t* rows) {

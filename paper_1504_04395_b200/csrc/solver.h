@@ -42,6 +42,13 @@ struct Solver {
   int cols_A = 0, cols_AH = 0;  // per iteration (Prop. 1 counters)
   long long matA = 0, matAH = 0;
   bool started = false;
+  // CUDA graph of `graph_iters` iterations (replayed between host polls)
+  cudaStream_t cap_st = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  int graph_iters = 0;
+  long long graph_launches = 0;
+  const double* graph_partials = nullptr;
+  int capture(int iters);
 
   virtual ~Solver();
   int setup();                 // allocate common state

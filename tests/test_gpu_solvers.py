@@ -205,3 +205,21 @@ def test_config5_egl_bicg_s32(srk):
     if max(its) - min(its) <= slack:  # BiCG over ~700 iterations: compare only if the oracle itself is stable
         assert min(its) - slack <= rep.iterations <= max(its) + slack, (rep.iterations, its)
     assert np.linalg.norm(B - As @ to_np(X)) / np.linalg.norm(B) <= 1e-8
+
+
+@pytest.mark.parametrize("method", ["egl_bicg", "bl_bicgstab_rq", "gl_qmr", "bl_qmr"])
+def test_cuda_graph_replay_is_bitwise_identical(srk, method):
+    """The iterations between two polls replayed as one captured CUDA graph give the
+    same bits, iteration count and report as launching them one by one."""
+    A, B = synth.make_config(1)
+    M = srk.Matrix.from_csr(A, need_adjoint=srk.NEEDS_ADJOINT[method])
+    out = []
+    for g in (False, True):
+        sv = srk.Solver(M, B.shape[1], method, tol=1e-8, maxit=2000, poll_every=16, use_graph=g)
+        sv.start(to_dev(B))
+        sv.iterate(2000)
+        r = sv.report()
+        out.append((to_np(sv.x()), r.iterations, r.outcome))
+        sv.close()
+    assert out[0][1] == out[1][1] and out[0][2] == out[1][2]
+    assert np.array_equal(out[0][0], out[1][0])
