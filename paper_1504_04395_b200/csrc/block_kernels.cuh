@@ -173,7 +173,7 @@ __device__ void red_dispatch_flush(int mode, RedAcc<T, S, FC>& a, double* partia
 // and every gather load is unconditional (absent entries use column 0 with a
 // zero value), so the CW*R loads of a step issue back to back.
 // ============================================================================
-template <typename T, int S, bool FC, int R, bool EX, int BC = 8, bool YPRE = true, int MINB = 2>
+template <typename T, int S, bool FC, int R, bool EX, int BC = 8, bool YPRE = true, int MINB = 2, int BATCH = 8>
 __global__ void __launch_bounds__(256, FC ? 1 : MINB) spmm_kernel(SpmmArgs a) {
   if (a.done && *a.done) return;
   using L = Lay<T, S>;
@@ -293,6 +293,31 @@ __global__ void __launch_bounds__(256, FC ? 1 : MINB) spmm_kernel(SpmmArgs a) {
       for (int e = 0; e < L::EPL; ++e) q[i][e] = Ar<T>::zero();
     for (int j0 = 0; j0 < maxlen; j0 += CW) {
       if (j0 > 0) load_cv(beg, len, j0, cj, vj);  // rows longer than CW
+      if constexpr (EX && BATCH > 0) {
+        // explicit batches of BATCH entries: all gathers of a batch issued before any FMA
+        static_assert(CW % BATCH == 0, "batch must divide CW");
+#pragma unroll
+        for (int t0 = 0; t0 < CW; t0 += BATCH) {
+          T pb[R][BATCH][L::EPL];
+          T vb[R][BATCH];
+#pragma unroll
+          for (int t = 0; t < BATCH; ++t)
+#pragma unroll
+            for (int i = 0; i < R; ++i) {
+              const int tt = t0 + t;
+              const int c = __shfl_sync(0xffffffffu, cj[i][tt / L::G], base + tt % L::G);
+              vb[i][t] = Ar<T>::shfl(vj[i][tt / L::G], base + tt % L::G, 0xffffffffu);
+              row_load_ex<T, S>(P + (size_t)c * S, g, pb[i][t]);
+            }
+#pragma unroll
+          for (int t = 0; t < BATCH; ++t)
+#pragma unroll
+            for (int i = 0; i < R; ++i)
+#pragma unroll
+              for (int e = 0; e < L::EPL; ++e) q[i][e] = Ar<T>::fma(vb[i][t], pb[i][t][e], q[i][e]);
+        }
+        continue;
+      }
 #pragma unroll
       for (int t = 0; t < CW; ++t) {
 #pragma unroll
@@ -478,6 +503,16 @@ __global__ void __launch_bounds__(256, FC ? 1 : MINB) upd_kernel(UpdArgs a) {
         }
       }
     }
+    // SUMVEC operands (an n-vector entry per row) requested together with the rows
+    T yvp[MAX_RED][R];
+#pragma unroll
+    for (int r = 0; r < MAX_RED; ++r)
+#pragma unroll
+      for (int i = 0; i < R; ++i) {
+        yvp[r][i] = Ar<T>::zero();
+        if (rmode[r] == RED_SUMVEC && ry[r] < 0 && r0 + i < n)
+          yvp[r][i] = reinterpret_cast<const T*>(a.red[r].yext)[r0 + i];
+      }
 #pragma unroll
     for (int i = 0; i < R; ++i) {
       const long long row = r0 + i;
@@ -533,7 +568,7 @@ __global__ void __launch_bounds__(256, FC ? 1 : MINB) upd_kernel(UpdArgs a) {
               }
             }
             if (ry[r] < 0 && a.red[r].yext) {
-              if (rmode[r] == RED_SUMVEC) yv = reinterpret_cast<const T*>(a.red[r].yext)[row];
+              if (rmode[r] == RED_SUMVEC) yv = yvp[r][i];
               else row_load<T, S>(reinterpret_cast<const T*>(a.red[r].yext) + (size_t)row * s, g, s, a.vec, y);
             }
             if (r == 0) red_dispatch_row<T, S, FC>(rmode[r], acc0, x, y, yv, base, s, gmask);

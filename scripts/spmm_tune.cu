@@ -14,9 +14,9 @@ using namespace srk;
 
 #define CK(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) { printf("%s: %s\n", #x, cudaGetErrorString(e_)); exit(1); } } while (0)
 
-template <int R, int BC, bool YPRE, int MINB>
+template <int R, int BC, bool YPRE, int MINB, int BATCH = 0>
 float run(const SpmmArgs& a0, int nsm, double bytes, const char* name) {
-  auto k = spmm_kernel<double, 16, false, R, true, BC, YPRE, MINB>;
+  auto k = spmm_kernel<double, 16, false, R, true, BC, YPRE, MINB, BATCH>;
   int occ = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, 256, 8 * 8 * 2));
   const int grid = nsm * occ;
@@ -84,11 +84,12 @@ int main(int argc, char** argv) {
   const double bytes = (n + 1) * 4.0 + nnz * 12.0 + 2.0 * n * s * 8 + n * 8.0;
   printf("n %lld nnz %lld algorithmic %.3f GB\n", n, nnz, bytes / 1e9);
   run<2, 8, true, 2>(a, nsm, bytes, "R2 BC8 ypre minb2 (library)");
-  run<2, 8, true, 4>(a, nsm, bytes, "R2 BC8 ypre minb4");
-  run<2, 8, false, 4>(a, nsm, bytes, "R2 BC8 noypre minb4");
-  run<1, 8, false, 4>(a, nsm, bytes, "R1 BC8 noypre minb4");
-  run<1, 8, true, 4>(a, nsm, bytes, "R1 BC8 ypre minb4");
-  run<2, 1, true, 4>(a, nsm, bytes, "R2 BC1 ypre minb4");
-  run<4, 8, false, 4>(a, nsm, bytes, "R4 BC8 noypre minb4");
+  run<2, 8, true, 2, 8>(a, nsm, bytes, "R2 BC8 ypre minb2 batch8");
+  run<2, 8, true, 2, 4>(a, nsm, bytes, "R2 BC8 ypre minb2 batch4");
+  run<4, 8, false, 1, 8>(a, nsm, bytes, "R4 BC8 noypre minb1 batch8");
+  run<1, 8, true, 3, 8>(a, nsm, bytes, "R1 BC8 ypre minb3 batch8");
+  run<1, 8, true, 4, 8>(a, nsm, bytes, "R1 BC8 ypre minb4 batch8");
+  run<2, 8, false, 3, 4>(a, nsm, bytes, "R2 BC8 noypre minb3 batch4");
+  run<4, 8, false, 2, 4>(a, nsm, bytes, "R4 BC8 noypre minb2 batch4");
   return 0;
 }

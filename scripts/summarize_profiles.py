@@ -1,0 +1,93 @@
+"""Summarise the ncu evidence of one GPU call into profiles/ (tracked).
+
+    python scripts/summarize_profiles.py r01
+
+Reads gpurun_out/launches.csv (ncu --metrics gpu__time_duration.sum launch list of
+`python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu`), gpurun_out/prof_*.ncu-rep
+(`ncu --set full`) and gpurun_out/bench.log, and writes
+profiles/<tag>_launches.csv, profiles/<tag>_ncu_summary.json, profiles/<tag>_bench.json,
+profiles/traffic.json (per-launch DRAM traffic of the dominant kernel for bench.py).
+"""
+import csv
+import io
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+OUT = os.path.join(ROOT, "gpurun_out")
+PROF = os.path.join(ROOT, "profiles")
+
+METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+           "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "lts__t_sector_hit_rate.pct",
+           "l1tex__t_sector_hit_rate.pct", "l1tex__m_xbar2l1tex_read_bytes.sum", "lts__throughput.avg.pct_of_peak_sustained_elapsed",
+           "launch__registers_per_thread", "launch__grid_size", "launch__occupancy_limit_registers",
+           "sm__warps_active.avg.pct_of_peak_sustained_active",
+           "smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio",
+           "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+           "sm__inst_executed_pipe_tensor_op_dmma.sum"]
+
+
+def ncu_raw(rep):
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    return dict(zip(rows[0], rows[2])), dict(zip(rows[0], rows[1]))
+
+
+def to_bytes(v, unit):
+    f = float(v)
+    return f * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
+
+
+def main(tag):
+    os.makedirs(PROF, exist_ok=True)
+    summary = {}
+    for name in ("spmm", "upd"):
+        rep = os.path.join(OUT, f"prof_{name}.ncu-rep")
+        if not os.path.exists(rep):
+            continue
+        v, u = ncu_raw(rep)
+        summary[name] = {"kernel": v.get("Kernel Name")}
+        for m in METRICS:
+            if m in v:
+                summary[name][m] = f"{v[m]} {u.get(m, '')}".strip()
+        rd = to_bytes(v["dram__bytes_read.sum"], u["dram__bytes_read.sum"])
+        wr = to_bytes(v["dram__bytes_write.sum"], u["dram__bytes_write.sum"])
+        summary[name]["dram_bytes_per_launch"] = rd + wr
+    json.dump(summary, open(os.path.join(PROF, f"{tag}_ncu_summary.json"), "w"), indent=1)
+    if "spmm" in summary:
+        json.dump({"cfg3_egl_qmr_spmm": summary["spmm"]["dram_bytes_per_launch"],
+                   "source": f"profiles/{tag}_ncu_summary.json (ncu --set full, one launch, cold cache)"},
+                  open(os.path.join(PROF, "traffic.json"), "w"), indent=1)
+    lc = os.path.join(OUT, "launches.csv")
+    if os.path.exists(lc):
+        lines = [ln for ln in open(lc) if ln.startswith('"')]
+        rows = list(csv.DictReader(io.StringIO("".join(lines))))
+        with open(os.path.join(PROF, f"{tag}_launches.csv"), "w") as f:
+            f.write("id,kernel,grid,block,ns\n")
+            for r in rows:
+                k = r["Kernel Name"].split("(")[0].replace(",", ";")
+                f.write(f'{r["ID"]},{k},{r["Grid Size"].replace(",", " ")},{r["Block Size"].replace(",", " ")},{r["Metric Value"]}\n')
+        # share of one solver iteration (the last complete iteration in the list)
+        names = [r["Kernel Name"].split("(")[0] for r in rows]
+        ends = [i for i, nm in enumerate(names) if "end_iter" in nm]
+        if len(ends) >= 2:
+            it = rows[ends[-2] + 1: ends[-1] + 1]
+            tot = sum(float(r["Metric Value"]) for r in it)
+            share = {}
+            for r in it:
+                k = r["Kernel Name"].split("(")[0]
+                share[k] = share.get(k, 0.0) + float(r["Metric Value"])
+            json.dump({"iteration_ns": tot, "share": {k: v / tot for k, v in sorted(share.items(), key=lambda x: -x[1])},
+                       "ns": share}, open(os.path.join(PROF, f"{tag}_iteration_shares.json"), "w"), indent=1)
+    bl = os.path.join(OUT, "bench.log")
+    if os.path.exists(bl):
+        for ln in open(bl):
+            if ln.startswith("{"):
+                json.dump(json.loads(ln), open(os.path.join(PROF, f"{tag}_bench.json"), "w"), indent=1)
+    print(json.dumps(summary, indent=1))
+
+
+if __name__ == "__main__":
+    main(sys.argv[1] if len(sys.argv) > 1 else "r01")
