@@ -26,33 +26,35 @@ struct RedAcc {
   // FULL (FC) needs S x EPL values; the other modes use the first EPL.
   static constexpr int N = FC ? S * L::EPL : L::EPL;
   T v[N];
-  double r[L::EPL];  // NORM2 / COLNORM2
 };
 
 template <typename T, int S, bool FC>
 __device__ __forceinline__ void red_zero(RedAcc<T, S, FC>& a) {
 #pragma unroll
   for (int i = 0; i < RedAcc<T, S, FC>::N; ++i) a.v[i] = Ar<T>::zero();
-#pragma unroll
-  for (int i = 0; i < Lay<T, S>::EPL; ++i) a.r[i] = 0.0;
 }
 
-// Accumulate one row's contribution. x: lane elements of the X row; y: lane
-// elements of the Y row (block modes) or yv the vector entry (SUMVEC).
-template <typename T, int S, int MODE, bool FC>
-__device__ __forceinline__ void red_row(RedAcc<T, S, FC>& a, const T (&x)[Lay<T, S>::EPL], const T (&y)[Lay<T, S>::EPL],
-                                        T yv, int base, int s, unsigned gmask) {
+__device__ __forceinline__ double re_of(double v) { return v; }
+__device__ __forceinline__ double re_of(double2 v) { return v.x; }
+
+// Every non-FULL reduction accumulates the same per-row form  acc += conj(y) .* x
+// (lane elements): y = x for NORM2 / COLNORM2 (|x|^2 in the real part), the
+// broadcast vector entry for SUMVEC, the Y row for DIAG / TRACE — so the per-row
+// cost is EPL fused multiply-adds and no mode dispatch; the mode only matters in
+// red_flush.
+template <typename T, int S, bool FC>
+__device__ __forceinline__ void red_acc(RedAcc<T, S, FC>& a, const T (&x)[Lay<T, S>::EPL],
+                                        const T (&y)[Lay<T, S>::EPL]) {
+#pragma unroll
+  for (int e = 0; e < Lay<T, S>::EPL; ++e) a.v[e] = Ar<T>::cfma(y[e], x[e], a.v[e]);
+}
+
+// FULL (s x s Gram X^H Y, block methods only): a.v[k][e] += conj(Y[:, k]) X[:, col(e)]
+template <typename T, int S, bool FC>
+__device__ __forceinline__ void red_full(RedAcc<T, S, FC>& a, const T (&x)[Lay<T, S>::EPL],
+                                         const T (&y)[Lay<T, S>::EPL], int base, int s, unsigned gmask) {
   using L = Lay<T, S>;
-  if constexpr (MODE == RED_NORM2 || MODE == RED_COLNORM2) {
-#pragma unroll
-    for (int e = 0; e < L::EPL; ++e) a.r[e] += Ar<T>::abs2(x[e]);
-  } else if constexpr (MODE == RED_DIAG || MODE == RED_TRACE) {
-#pragma unroll
-    for (int e = 0; e < L::EPL; ++e) a.v[e] = Ar<T>::cfma(y[e], x[e], a.v[e]);
-  } else if constexpr (MODE == RED_SUMVEC) {
-#pragma unroll
-    for (int e = 0; e < L::EPL; ++e) a.v[e] = Ar<T>::cfma(yv, x[e], a.v[e]);
-  } else if constexpr (MODE == RED_FULL && FC) {
+  if constexpr (FC) {
 #pragma unroll
     for (int k = 0; k < S; ++k) {
       if (k < s) {
@@ -62,6 +64,31 @@ __device__ __forceinline__ void red_row(RedAcc<T, S, FC>& a, const T (&x)[Lay<T,
       }
     }
   }
+}
+
+// y operand kind of a reduction (CTA-uniform): 0 = x itself, 1 = broadcast n-vector
+// entry, 2 = a row (source block or external block)
+__device__ __forceinline__ int red_ykind(int mode) {
+  return (mode == RED_NORM2 || mode == RED_COLNORM2) ? 0 : (mode == RED_SUMVEC ? 1 : 2);
+}
+
+// One row of one reduction with a runtime (CTA-uniform) mode.
+template <typename T, int S, bool FC>
+__device__ __forceinline__ void red_dispatch_row(int mode, RedAcc<T, S, FC>& a, const T (&x)[Lay<T, S>::EPL],
+                                                 const T (&y)[Lay<T, S>::EPL], T yv, int base, int s,
+                                                 unsigned gmask) {
+  using L = Lay<T, S>;
+  if constexpr (FC) {
+    if (mode == RED_FULL) {
+      red_full<T, S, FC>(a, x, y, base, s, gmask);
+      return;
+    }
+  }
+  const int yk = red_ykind(mode);
+  T yy[L::EPL];
+#pragma unroll
+  for (int e = 0; e < L::EPL; ++e) yy[e] = yk == 0 ? x[e] : (yk == 1 ? yv : y[e]);
+  red_acc<T, S, FC>(a, x, yy);
 }
 
 // CTA-level reduction of one RedAcc into partials[blockIdx.x*pstride + poff ...].
@@ -79,8 +106,6 @@ __device__ void red_flush(RedAcc<T, S, FC>& a, double* __restrict__ partials, in
   for (int m = L::G; m < 32; m <<= 1) {
 #pragma unroll
     for (int i = 0; i < RedAcc<T, S, FC>::N; ++i) a.v[i] = Ar<T>::add(a.v[i], Ar<T>::shfl_xor(a.v[i], m));
-#pragma unroll
-    for (int i = 0; i < L::EPL; ++i) a.r[i] += __shfl_xor_sync(0xffffffffu, a.r[i], m);
   }
   const int len = red_len(MODE, s, Ar<T>::cplx);
   // 2) lanes of group 0 scatter their entries into this warp's smem slice
@@ -91,7 +116,7 @@ __device__ void red_flush(RedAcc<T, S, FC>& a, double* __restrict__ partials, in
     T vs = Ar<T>::zero();
 #pragma unroll
     for (int e = 0; e < L::EPL; ++e) {
-      rs += a.r[e];
+      rs += re_of(a.v[e]);
       vs = Ar<T>::add(vs, a.v[e]);
     }
 #pragma unroll
@@ -109,7 +134,7 @@ __device__ void red_flush(RedAcc<T, S, FC>& a, double* __restrict__ partials, in
       for (int e = 0; e < L::EPL; ++e) {
         const int c = L::col(g, e);
         if (c < s) {
-          if constexpr (MODE == RED_COLNORM2) w[c] = a.r[e];
+          if constexpr (MODE == RED_COLNORM2) w[c] = re_of(a.v[e]);
           else Ar<T>::st(w + c * ND, a.v[e]);
         }
       }
@@ -139,21 +164,6 @@ __device__ void red_flush(RedAcc<T, S, FC>& a, double* __restrict__ partials, in
 }
 
 template <typename T, int S, bool FC>
-__device__ __forceinline__ void red_dispatch_row(int mode, RedAcc<T, S, FC>& a, const T (&x)[Lay<T, S>::EPL],
-                                                 const T (&y)[Lay<T, S>::EPL], T yv, int base, int s,
-                                                 unsigned gmask) {
-  switch (mode) {
-    case RED_NORM2: red_row<T, S, RED_NORM2, FC>(a, x, y, yv, base, s, gmask); break;
-    case RED_COLNORM2: red_row<T, S, RED_COLNORM2, FC>(a, x, y, yv, base, s, gmask); break;
-    case RED_DIAG: red_row<T, S, RED_DIAG, FC>(a, x, y, yv, base, s, gmask); break;
-    case RED_TRACE: red_row<T, S, RED_TRACE, FC>(a, x, y, yv, base, s, gmask); break;
-    case RED_SUMVEC: red_row<T, S, RED_SUMVEC, FC>(a, x, y, yv, base, s, gmask); break;
-    case RED_FULL: red_row<T, S, RED_FULL, FC>(a, x, y, yv, base, s, gmask); break;
-    default: break;
-  }
-}
-
-template <typename T, int S, bool FC>
 __device__ void red_dispatch_flush(int mode, RedAcc<T, S, FC>& a, double* partials, int pstride, int poff, int s,
                                    double* smem) {
   switch (mode) {
@@ -173,7 +183,7 @@ __device__ void red_dispatch_flush(int mode, RedAcc<T, S, FC>& a, double* partia
 // and every gather load is unconditional (absent entries use column 0 with a
 // zero value), so the CW*R loads of a step issue back to back.
 // ============================================================================
-template <typename T, int S, bool FC, int R, bool EX, int BC = 8, bool YPRE = true, int MINB = 2, int BATCH = 8>
+template <typename T, int S, bool FC, int R, bool EX, int BC = 8, bool YPRE = true, int MINB = 2, int BATCH = 8, int PD = 1>
 __global__ void __launch_bounds__(256, FC ? 1 : MINB) spmm_kernel(SpmmArgs a) {
   if (a.done && *a.done) return;
   using L = Lay<T, S>;
@@ -247,24 +257,30 @@ __global__ void __launch_bounds__(256, FC ? 1 : MINB) spmm_kernel(SpmmArgs a) {
       }
   };
 
-  // Three-stage software pipeline over the warp's row batches k = 0, 1, 2, ...:
-  // while the P gathers of batch k are in flight, the (col, val) of batch k+1 and
-  // the row pointers of batch k+2 are being fetched.
-  int beg[R], len[R], begn[R], lenn[R];
-  int cj[R][EPN];
-  T vj[R][EPN];
-  load_rp(0, beg, len);
-  to_len(beg, len);
-  load_cv(beg, len, 0, cj, vj);
-  load_rp(1, begn, lenn);
-  to_len(begn, lenn);
+  // Software pipeline over the warp's row batches k = 0, 1, 2, ...: while the P
+  // gathers of batch k are in flight, the (col, val) of batches up to k+PD and the
+  // row pointers of batch k+PD+1 are being fetched (PD = prefetch depth).
+  int bq[PD + 1][R], lq[PD + 1][R];  // row pointers (begin, length) of batches k..k+PD
+  int cq[PD][R][EPN];                // (col, val) of batches k..k+PD-1
+  T vq[PD][R][EPN];
+#pragma unroll
+  for (int d = 0; d <= PD; ++d) {
+    load_rp(d, bq[d], lq[d]);
+    to_len(bq[d], lq[d]);
+  }
+#pragma unroll
+  for (int d = 0; d < PD; ++d) load_cv(bq[d], lq[d], 0, cq[d], vq[d]);
   for (long long k = 0; step_live(k); ++k) {  // warp-uniform loop
     const long long r0 = row_of(k);
+    int (&beg)[R] = bq[0];
+    int (&len)[R] = lq[0];
+    int (&cj)[R][EPN] = cq[0];
+    T (&vj)[R][EPN] = vq[0];
     int cjn[R][EPN];
     T vjn[R][EPN];
     int begnn[R], lennn[R];
-    load_cv(begn, lenn, 0, cjn, vjn);
-    load_rp(k + 2, begnn, lennn);
+    load_cv(bq[PD], lq[PD], 0, cjn, vjn);
+    load_rp(k + PD + 1, begnn, lennn);
     // epilogue operand of the first reduction, requested before the gathers
     T yr0[R][L::EPL];
     T yv0[R];
@@ -369,14 +385,22 @@ __global__ void __launch_bounds__(256, FC ? 1 : MINB) spmm_kernel(SpmmArgs a) {
     to_len(begnn, lennn);
 #pragma unroll
     for (int i = 0; i < R; ++i) {
-      beg[i] = begn[i];
-      len[i] = lenn[i];
-      begn[i] = begnn[i];
-      lenn[i] = lennn[i];
+#pragma unroll
+      for (int d = 0; d < PD; ++d) {
+        bq[d][i] = bq[d + 1][i];
+        lq[d][i] = lq[d + 1][i];
+      }
+      bq[PD][i] = begnn[i];
+      lq[PD][i] = lennn[i];
 #pragma unroll
       for (int u = 0; u < EPN; ++u) {
-        cj[i][u] = cjn[i][u];
-        vj[i][u] = vjn[i][u];
+#pragma unroll
+        for (int d = 0; d + 1 < PD; ++d) {
+          cq[d][i][u] = cq[d + 1][i][u];
+          vq[d][i][u] = vq[d + 1][i][u];
+        }
+        cq[PD - 1][i][u] = cjn[i][u];
+        vq[PD - 1][i][u] = vjn[i][u];
       }
     }
   }
@@ -447,12 +471,27 @@ __global__ void __launch_bounds__(256, FC ? 1 : MINB) upd_kernel(UpdArgs a) {
   const long long grp0 = (long long)blockIdx.x * groups_per_cta + (threadIdx.x >> 5) * L::RPW + lane / L::G;
   const long long gstride = (long long)gridDim.x * groups_per_cta;
   const int nin = a.nin, nout = a.nout, nred = a.nred;
-  int rmode[MAX_RED], rx[MAX_RED], ry[MAX_RED];
+  // Reductions are applied at the first "stage" at which both operands exist
+  // (stage 0: inputs only; stage o+1: after output o), so an output's reductions
+  // consume it while it is in registers, and the common case — x is the output
+  // just formed — needs no operand selection at all.
+  int rmode[MAX_RED], rx[MAX_RED], ry[MAX_RED], ryk[MAX_RED];
+  int st_mask[MAX_OUT + 1];
+#pragma unroll
+  for (int t = 0; t <= MAX_OUT; ++t) st_mask[t] = 0;
 #pragma unroll
   for (int r = 0; r < MAX_RED; ++r) {
     rmode[r] = r < nred ? a.red[r].mode : RED_NONE;
     rx[r] = r < nred ? a.red[r].xsrc : -2;
     ry[r] = r < nred ? a.red[r].ysrc : -2;
+    ryk[r] = red_ykind(rmode[r]);
+    if (ryk[r] == 2 && ry[r] < 0) ryk[r] = 3;  // row of an external block
+    if (rmode[r] == RED_FULL) ryk[r] = ry[r] < 0 ? 3 : 2;
+    if (rmode[r] != RED_NONE) {
+      const int sx = rx[r] >= SRC_OUT ? rx[r] - SRC_OUT + 1 : 0;
+      const int sy = (ryk[r] == 2 && ry[r] >= SRC_OUT) ? ry[r] - SRC_OUT + 1 : 0;
+      st_mask[sx > sy ? sx : sy] |= 1 << r;
+    }
   }
 
   RedAcc<T, S, FC> acc0, acc1;
@@ -510,14 +549,70 @@ __global__ void __launch_bounds__(256, FC ? 1 : MINB) upd_kernel(UpdArgs a) {
 #pragma unroll
       for (int i = 0; i < R; ++i) {
         yvp[r][i] = Ar<T>::zero();
-        if (rmode[r] == RED_SUMVEC && ry[r] < 0 && r0 + i < n)
-          yvp[r][i] = reinterpret_cast<const T*>(a.red[r].yext)[r0 + i];
+        if (ryk[r] == 1 && r0 + i < n) yvp[r][i] = reinterpret_cast<const T*>(a.red[r].yext)[r0 + i];
       }
 #pragma unroll
     for (int i = 0; i < R; ++i) {
       const long long row = r0 + i;
       if (row < n) {
         T xo[MAX_OUT][L::EPL];
+        // reductions of stage t; ONLY_X: x is output t-1 (no selection)
+        auto stage = [&](int t) {
+#pragma unroll
+          for (int r = 0; r < MAX_RED; ++r) {
+            if (!((st_mask[t] >> r) & 1)) continue;
+            T x[L::EPL], y[L::EPL];
+            if (t > 0 && rx[r] == SRC_OUT + t - 1) {
+#pragma unroll
+              for (int e = 0; e < L::EPL; ++e) x[e] = xo[t > 0 ? t - 1 : 0][e];
+            } else {
+#pragma unroll
+              for (int e = 0; e < L::EPL; ++e) x[e] = Ar<T>::zero();
+#pragma unroll
+              for (int q = 0; q < NI; ++q)
+#pragma unroll
+                for (int e = 0; e < L::EPL; ++e) x[e] = opaque_sel(rx[r] == q, xin[q][i][e], x[e]);
+#pragma unroll
+              for (int q = 0; q < MAX_OUT; ++q)
+                if (q < t)
+#pragma unroll
+                  for (int e = 0; e < L::EPL; ++e) x[e] = opaque_sel(rx[r] == SRC_OUT + q, xo[q][e], x[e]);
+            }
+            if (ryk[r] == 0) {
+#pragma unroll
+              for (int e = 0; e < L::EPL; ++e) y[e] = x[e];
+            } else if (ryk[r] == 1) {
+#pragma unroll
+              for (int e = 0; e < L::EPL; ++e) y[e] = yvp[r][i];
+            } else if (ryk[r] == 3) {
+#pragma unroll
+              for (int e = 0; e < L::EPL; ++e) y[e] = Ar<T>::zero();
+              if constexpr (EX) row_load_ex_rw<T, S>(reinterpret_cast<const T*>(a.red[r].yext) + (size_t)row * S, g, y);
+              else row_load<T, S>(reinterpret_cast<const T*>(a.red[r].yext) + (size_t)row * s, g, s, a.vec, y);
+            } else {
+#pragma unroll
+              for (int e = 0; e < L::EPL; ++e) y[e] = Ar<T>::zero();
+#pragma unroll
+              for (int q = 0; q < NI; ++q)
+#pragma unroll
+                for (int e = 0; e < L::EPL; ++e) y[e] = opaque_sel(ry[r] == q, xin[q][i][e], y[e]);
+#pragma unroll
+              for (int q = 0; q < MAX_OUT; ++q)
+                if (q < t)
+#pragma unroll
+                  for (int e = 0; e < L::EPL; ++e) y[e] = opaque_sel(ry[r] == SRC_OUT + q, xo[q][e], y[e]);
+            }
+            if (FC && rmode[r] == RED_FULL) {
+              if (r == 0) red_full<T, S, FC>(acc0, x, y, base, s, gmask);
+              else if (r == 1) red_full<T, S, FC>(acc1, x, y, base, s, gmask);
+            } else {
+              if (r == 0) red_acc<T, S, FC>(acc0, x, y);
+              else if (r == 1) red_acc<T, S, FC>(acc1, x, y);
+              else red_acc<T, S, false>(acc2, x, y);
+            }
+          }
+        };
+        if (st_mask[0]) stage(0);
 #pragma unroll
         for (int o = 0; o < MAX_OUT; ++o) {
 #pragma unroll
@@ -538,42 +633,7 @@ __global__ void __launch_bounds__(256, FC ? 1 : MINB) upd_kernel(UpdArgs a) {
               else if constexpr (EX) row_store_ex<T, S>(reinterpret_cast<T*>(a.out[o]) + (size_t)row * S, g, xo[o]);
               else row_store<T, S>(reinterpret_cast<T*>(a.out[o]) + (size_t)row * s, g, s, a.vec, xo[o]);
             }
-          }
-        }
-        // ---- reductions: operands picked with compile-time indices
-#pragma unroll
-        for (int r = 0; r < MAX_RED; ++r) {
-          if (rmode[r] != RED_NONE) {
-            T x[L::EPL], y[L::EPL];
-            T yv = Ar<T>::zero();
-#pragma unroll
-            for (int e = 0; e < L::EPL; ++e) {
-              x[e] = Ar<T>::zero();
-              y[e] = Ar<T>::zero();
-            }
-#pragma unroll
-            for (int b = 0; b < NI; ++b) {
-#pragma unroll
-              for (int e = 0; e < L::EPL; ++e) {
-                x[e] = opaque_sel(rx[r] == b, xin[b][i][e], x[e]);
-                y[e] = opaque_sel(ry[r] == b, xin[b][i][e], y[e]);
-              }
-            }
-#pragma unroll
-            for (int b = 0; b < MAX_OUT; ++b) {
-#pragma unroll
-              for (int e = 0; e < L::EPL; ++e) {
-                x[e] = opaque_sel(rx[r] == SRC_OUT + b, xo[b][e], x[e]);
-                y[e] = opaque_sel(ry[r] == SRC_OUT + b, xo[b][e], y[e]);
-              }
-            }
-            if (ry[r] < 0 && a.red[r].yext) {
-              if (rmode[r] == RED_SUMVEC) yv = yvp[r][i];
-              else row_load<T, S>(reinterpret_cast<const T*>(a.red[r].yext) + (size_t)row * s, g, s, a.vec, y);
-            }
-            if (r == 0) red_dispatch_row<T, S, FC>(rmode[r], acc0, x, y, yv, base, s, gmask);
-            else if (r == 1) red_dispatch_row<T, S, FC>(rmode[r], acc1, x, y, yv, base, s, gmask);
-            else red_dispatch_row<T, S, false>(rmode[r], acc2, x, y, yv, base, s, gmask);
+            if (st_mask[o + 1]) stage(o + 1);
           }
         }
       }  // row < n
@@ -590,7 +650,7 @@ __global__ void __launch_bounds__(256, FC ? 1 : MINB) upd_kernel(UpdArgs a) {
 template <typename T, int S> constexpr int spmm_rows() {
   return (Lay<T, S>::G == 1 || S >= 64) ? 1 : 2;
 }
-template <int NI> constexpr int upd_rows() { return NI <= 1 ? 4 : (NI <= 2 ? 2 : 1); }
+template <int NI> constexpr int upd_rows() { return NI <= 2 ? 2 : 1; }
 template <typename T, int S> constexpr bool full_ok() { return S <= 16; }
 
 // grid < 0: return the number of resident CTAs per SM instead of launching

@@ -5,6 +5,7 @@
 //   nvcc -std=c++17 -O3 -gencode arch=compute_100a,code=sm_100a -I paper_1504_04395_b200/csrc \
 //        scripts/spmm_tune.cu -o scripts/spmm_tune
 #include <cstdio>
+#include <cmath>
 #include <cstdlib>
 #include <vector>
 
@@ -14,9 +15,9 @@ using namespace srk;
 
 #define CK(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) { printf("%s: %s\n", #x, cudaGetErrorString(e_)); exit(1); } } while (0)
 
-template <int R, int BC, bool YPRE, int MINB, int BATCH = 0>
+template <int R, int BC, bool YPRE, int MINB, int BATCH = 0, int PD = 1>
 float run(const SpmmArgs& a0, int nsm, double bytes, const char* name) {
-  auto k = spmm_kernel<double, 16, false, R, true, BC, YPRE, MINB, BATCH>;
+  auto k = spmm_kernel<double, 16, false, R, true, BC, YPRE, MINB, BATCH, PD>;
   int occ = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, 256, 8 * 8 * 2));
   const int grid = nsm * occ;
@@ -83,13 +84,13 @@ int main(int argc, char** argv) {
   a.nred = 1; a.red[0].mode = RED_SUMVEC; a.red[0].yext = y; a.red[0].poff = 0; a.partials = part; a.pstride = 1;
   const double bytes = (n + 1) * 4.0 + nnz * 12.0 + 2.0 * n * s * 8 + n * 8.0;
   printf("n %lld nnz %lld algorithmic %.3f GB\n", n, nnz, bytes / 1e9);
-  run<2, 8, true, 2>(a, nsm, bytes, "R2 BC8 ypre minb2 (library)");
-  run<2, 8, true, 2, 8>(a, nsm, bytes, "R2 BC8 ypre minb2 batch8");
-  run<2, 8, true, 2, 4>(a, nsm, bytes, "R2 BC8 ypre minb2 batch4");
-  run<4, 8, false, 1, 8>(a, nsm, bytes, "R4 BC8 noypre minb1 batch8");
-  run<1, 8, true, 3, 8>(a, nsm, bytes, "R1 BC8 ypre minb3 batch8");
-  run<1, 8, true, 4, 8>(a, nsm, bytes, "R1 BC8 ypre minb4 batch8");
-  run<2, 8, false, 3, 4>(a, nsm, bytes, "R2 BC8 noypre minb3 batch4");
-  run<4, 8, false, 2, 4>(a, nsm, bytes, "R4 BC8 noypre minb2 batch4");
+  run<2, 8, true, 2, 8, 1>(a, nsm, bytes, "R2 BC8 PD1 (library)");
+  run<2, 8, true, 2, 8, 2>(a, nsm, bytes, "R2 BC8 PD2");
+  run<2, 8, true, 2, 8, 3>(a, nsm, bytes, "R2 BC8 PD3");
+  run<1, 8, true, 4, 8, 2>(a, nsm, bytes, "R1 BC8 minb4 PD2");
+  run<1, 8, true, 4, 8, 4>(a, nsm, bytes, "R1 BC8 minb4 PD4");
+  run<1, 16, true, 3, 8, 3>(a, nsm, bytes, "R1 BC16 minb3 PD3");
+  run<2, 8, true, 2, 8, 1>(a, nsm, bytes, "R2 BC8 PD1 (repeat)");
+  run<2, 8, true, 2, 8, 2>(a, nsm, bytes, "R2 BC8 PD2 (repeat)");
   return 0;
 }

@@ -31,18 +31,26 @@ void run(const UpdArgs& a, size_t smem, int nsm, double bytes, const char* name)
   printf("%-30s occ %d grid %4d  %.3f ms  %.0f GB/s\n", name, occ, grid, ms, bytes / ms / 1e6);
 }
 
+__global__ void fill(double* p, long long m, int seed) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < m; i += (long long)gridDim.x * blockDim.x)
+    p[i] = (double)(((i + seed * 7919) * 2654435761ULL) % 1000003) / 1000003.0 - 0.5;
+}
+
 int main() {
   const long long n = 256LL * 256 * 256;
   const int s = 16;
   double* blk[8];
   for (int i = 0; i < 8; ++i) {
     CK(cudaMalloc(&blk[i], sizeof(double) * n * s));
-    CK(cudaMemset(blk[i], 0, sizeof(double) * n * s));
+    fill<<<1024, 256>>>(blk[i], n * s, i);
   }
+  double* yv;
+  CK(cudaMalloc(&yv, sizeof(double) * n));
+  fill<<<1024, 256>>>(yv, n, 9);
   double *ws, *part;
   CK(cudaMalloc(&ws, sizeof(double) * 64));
   CK(cudaMemset(ws, 0, sizeof(double) * 64));
-  CK(cudaMalloc(&part, sizeof(double) * 8192));
+  CK(cudaMalloc(&part, sizeof(double) * 65536));
   int nsm = 148;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
   const double B = (double)n * s * 8;
@@ -85,6 +93,25 @@ int main() {
   run<2, 2, false, 4>(b, 64, nsm, 3 * B, "NI2 R2 minb4");
   run<2, 4, false, 3>(b, 64, nsm, 3 * B, "NI2 R4 minb3");
   run<2, 1, false, 4>(b, 64, nsm, 3 * B, "NI2 R1 minb4");
+  // 2 inputs, 1 output with ||out||^2 and sum_i conj(w_i) out_i (eGl-QMR V~ update)
+  UpdArgs v = b;
+  v.nred = 2;
+  v.pstride = 17;
+  v.red[0] = Red{RED_NORM2, SRC_OUT + 0, -1, nullptr, 0};
+  v.red[1] = Red{RED_SUMVEC, SRC_OUT + 0, -1, yv, 1};
+  printf("3-block update + NORM2 + SUMVEC (%.2f GB + n-vector)\n", 3 * B / 1e9);
+  run<2, 2, false, 4>(v, 64 + 8 * 64, nsm, 3 * B, "red NI2 R2 minb4 (library)");
+  run<2, 2, false, 3>(v, 64 + 8 * 64, nsm, 3 * B, "red NI2 R2 minb3");
+  run<2, 2, false, 2>(v, 64 + 8 * 64, nsm, 3 * B, "red NI2 R2 minb2");
+  run<2, 1, false, 4>(v, 64 + 8 * 64, nsm, 3 * B, "red NI2 R1 minb4");
+  run<2, 4, false, 2>(v, 64 + 8 * 64, nsm, 3 * B, "red NI2 R4 minb2");
+  run<2, 2, false, 4>(b, 64, nsm, 3 * B, "nored NI2 R2 minb4 (library)");
+  UpdArgs v1 = v; v1.nred = 1;
+  run<2, 2, false, 4>(v1, 64 + 8 * 64, nsm, 3 * B, "NORM2 only NI2 R2 minb4");
+  UpdArgs v2 = v; v2.nred = 1; v2.red[0] = v.red[1];
+  run<2, 2, false, 4>(v2, 64 + 8 * 64, nsm, 3 * B, "SUMVEC only NI2 R2 minb4");
+  UpdArgs v3 = v; v3.red[1] = Red{RED_NORM2, SRC_OUT + 0, -1, nullptr, 1};
+  run<2, 2, false, 4>(v3, 64 + 8 * 64, nsm, 3 * B, "NORM2 x2 NI2 R2 minb4");
   // 1 input (V = c Vt)
   UpdArgs c1 = b;
   c1.nin = 1; c1.cf[0][1].kind = CK_NONE;
