@@ -94,12 +94,19 @@ __device__ __forceinline__ void red_dispatch_row(int mode, RedAcc<T, S, FC>& a, 
 // CTA-level reduction of one RedAcc into partials[blockIdx.x*pstride + poff ...].
 // Order: xor-butterfly over lane groups, then warps summed in index order by
 // thread 0..len-1 — fixed for a given launch configuration.
+// The participating warps are wfirst .. wfirst+nw-1 (all warps by default); they
+// synchronise with named barrier `bar` (0 = __syncthreads).
 template <typename T, int S, int MODE, bool FC>
 __device__ void red_flush(RedAcc<T, S, FC>& a, double* __restrict__ partials, int pstride, int poff, int s,
-                          double* smem /* >= nwarps * len doubles */) {
+                          double* smem /* >= nwarps * len doubles */, int wfirst = 0, int nw = 0, int bar = 0) {
   using L = Lay<T, S>;
   constexpr int ND = Ar<T>::ND;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const int nwarps = nw > 0 ? nw : (int)(blockDim.x >> 5);
+  const int lane = threadIdx.x & 31, warp = (int)(threadIdx.x >> 5) - wfirst;
+  auto sync = [&]() {
+    if (bar == 0) __syncthreads();
+    else asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(nwarps * 32) : "memory");
+  };
   const int g = lane % L::G;
   // 1) sum over the lane groups of this warp (lanes with equal g hold the same entries)
 #pragma unroll
@@ -153,26 +160,26 @@ __device__ void red_flush(RedAcc<T, S, FC>& a, double* __restrict__ partials, in
       }
     }
   }
-  __syncthreads();
+  sync();
   // 3) sum the warps' slices in warp order
-  for (int j = threadIdx.x; j < len; j += blockDim.x) {
+  for (int j = (int)threadIdx.x - wfirst * 32; j < len; j += nwarps * 32) {
     double acc = 0.0;
     for (int q = 0; q < nwarps; ++q) acc += smem[q * len + j];
     partials[(size_t)blockIdx.x * pstride + poff + j] = acc;
   }
-  __syncthreads();
+  sync();
 }
 
 template <typename T, int S, bool FC>
 __device__ void red_dispatch_flush(int mode, RedAcc<T, S, FC>& a, double* partials, int pstride, int poff, int s,
-                                   double* smem) {
+                                   double* smem, int wfirst = 0, int nw = 0, int bar = 0) {
   switch (mode) {
-    case RED_NORM2: red_flush<T, S, RED_NORM2, FC>(a, partials, pstride, poff, s, smem); break;
-    case RED_COLNORM2: red_flush<T, S, RED_COLNORM2, FC>(a, partials, pstride, poff, s, smem); break;
-    case RED_DIAG: red_flush<T, S, RED_DIAG, FC>(a, partials, pstride, poff, s, smem); break;
-    case RED_TRACE: red_flush<T, S, RED_TRACE, FC>(a, partials, pstride, poff, s, smem); break;
-    case RED_SUMVEC: red_flush<T, S, RED_SUMVEC, FC>(a, partials, pstride, poff, s, smem); break;
-    case RED_FULL: red_flush<T, S, RED_FULL, FC>(a, partials, pstride, poff, s, smem); break;
+    case RED_NORM2: red_flush<T, S, RED_NORM2, FC>(a, partials, pstride, poff, s, smem, wfirst, nw, bar); break;
+    case RED_COLNORM2: red_flush<T, S, RED_COLNORM2, FC>(a, partials, pstride, poff, s, smem, wfirst, nw, bar); break;
+    case RED_DIAG: red_flush<T, S, RED_DIAG, FC>(a, partials, pstride, poff, s, smem, wfirst, nw, bar); break;
+    case RED_TRACE: red_flush<T, S, RED_TRACE, FC>(a, partials, pstride, poff, s, smem, wfirst, nw, bar); break;
+    case RED_SUMVEC: red_flush<T, S, RED_SUMVEC, FC>(a, partials, pstride, poff, s, smem, wfirst, nw, bar); break;
+    case RED_FULL: red_flush<T, S, RED_FULL, FC>(a, partials, pstride, poff, s, smem, wfirst, nw, bar); break;
     default: break;
   }
 }
