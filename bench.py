@@ -15,8 +15,11 @@ flush is needed between steps.
 
 One JSON line on rank 0 with: value (whole-job RHS·it/s), e2e (the same metric
 through srk_solve_host with host B/X, copies inside the timed region),
-roofline (the dominant kernel — the fused SpMM+Gram — timed live with CUDA
-events inside the timed region), cpu_baseline (the oracle on a bounded sample:
+roofline (the dominant kernel: the kernel family with the largest share of the
+step, its launches timed live with CUDA events inside the timed region and its
+algorithmic bytes counted by the engine per SURVEY §8(d).3), roofline_spmm (the
+same for the A·P SpMM with its fused Gram), iteration.kernels (every family),
+cpu_baseline (the oracle on a bounded sample:
 one config-3 iteration on the host cores), clocks (nvidia-smi during the
 timed region), gpu_launches (kernels in the timed region).
 
@@ -39,7 +42,7 @@ sys.path.insert(0, ROOT)
 
 import numpy as np  # noqa: E402
 
-METRIC = "RHS·iterations/sec (SpMM+Gram achieved HBM GB/s in roofline)"
+METRIC = "RHS·iterations/sec"
 UNIT = "RHS·it/s"
 
 
@@ -95,29 +98,6 @@ class ClockSampler:
         reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower().startswith("active")})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
                 "reasons": reasons, "samples": len(self.rows)}
-
-
-def algorithmic_spmm_bytes(A, s, esz, operand_bytes):
-    """A's arrays once (int32 row_ptr / col, values), P read once,
-    Q written once, plus the Gram operand (here the eGl shadow vector q)."""
-    return (A.n + 1) * 4 + A.nnz * 4 + A.nnz * esz + 2 * A.n * s * esz + operand_bytes
-
-
-def iteration_bytes_egl_qmr(A, s, esz):
-    """Algorithmic bytes of one eGl-QMR iteration in this build's fused phase plan
-    (DESIGN.md §7): B = one n x s block, v = one n-vector, A = one CSR operator.
-      P = Ṽ/rho - c1 P          Ṽ r, P r, P w                 3B
-      q = w̃/xi - c2 q           w̃ r, q r, q w                 3v
-      P~ = A P, sum(q^H P~)     P r, P~ w, q r, A             2B + v + A
-      A^H q                     q r, A^H q w, A^H             2v + A
-      w̃ = A^H q - conj(b)/xi w̃  A^H q r, w̃ r, w̃ w             3v
-      Ṽ = P~ - b/rho Ṽ (+norm, <Ṽ,w̃>)  P~ r, Ṽ r, Ṽ w, w̃ r   3B + v
-      D, S, X, R (+||R||)       P, D, P~, S, X, R r; D, S, X, R w   10B
-    total 18B + 10v + 2A."""
-    B = A.n * s * esz
-    v = A.n * esz
-    a_bytes = (A.n + 1) * 4 + A.nnz * (4 + esz)
-    return 18 * B + 10 * v + 2 * a_bytes
 
 
 def oracle_iteration_rate(method, A, B, iters: int):
@@ -231,10 +211,8 @@ def main():
         o0, o1 = int(off[rank]), int(off[rank + 1])
         B = np.ascontiguousarray(B[o0:o1])
         cfgd["parallelism"] = f"row-partition x{world} (halo exchange + NCCL allreduce)"
-        nnz_local = int(A.row_ptr[o1] - A.row_ptr[o0])
     else:
         M = srk.Matrix.from_csr(A, need_adjoint=srk.NEEDS_ADJOINT[args.method])
-        nnz_local = A.nnz
     n_local = B.shape[0]
     Bd = torch.from_numpy(B).to(dev)
     K, W = args.steps, args.warmup
@@ -268,7 +246,7 @@ def main():
     torch.cuda.synchronize()
     clocks = clk.stop()
     ms = e0.elapsed_time(e1)
-    prof = sv.profile_read()
+    recs = sv.profile_launches()
     rep = sv.report()
     launches = rep.kernel_launches - l0
     assert st == 0 and rep.iterations == W + K, (st, rep)
@@ -278,26 +256,49 @@ def main():
         ms = float(t.item())
     value = s * K / (ms / 1e3)  # the whole job iterates the same s right-hand sides
 
-    # ---- roofline of the dominant kernel (SpMM A·P + fused Gram), timed live
-    spmm_ms, spmm_n = prof["spmm"]
-    class _Loc:  # this rank's share of the operator
-        n = n_local
-        nnz = nnz_local
-    operand = n_local * esz if args.method.startswith("egl") else n_local * s * esz
-    alg = algorithmic_spmm_bytes(_Loc, s, esz, operand)
-    avg_s = spmm_ms / 1e3 / max(spmm_n, 1)
+    # ---- rooflines, timed live: every launch of the timed region carries its
+    # algorithmic bytes (computed by the engine); launches are
+    # grouped into kernel families, and `roofline` reports the family with the
+    # largest share of the step (the dominant kernel)
     peak, peak_src = peaks()
-    achieved = alg / avg_s / 1e9
+    fams = {}
+    for tag, sig, t_ms, nb in recs:
+        if tag in ("spmm", "spmm_adj"):
+            name = f"{tag} s={sig}"
+        elif tag == "update":
+            name = f"update {sig // 16} in / {sig % 16} out"
+        else:
+            name = tag
+        key = (name, round(nb))
+        f = fams.setdefault(key, {"kernel": name, "ms_total": 0.0, "launches": 0, "bytes_per_launch": nb})
+        f["ms_total"] += t_ms
+        f["launches"] += 1
+    kern = []
+    for f in fams.values():
+        avg = f["ms_total"] / f["launches"] / 1e3
+        ach = f["bytes_per_launch"] / avg / 1e9 if f["bytes_per_launch"] > 0 else None
+        kern.append({"kernel": f["kernel"], "launches": f["launches"], "avg_launch_ms": avg * 1e3,
+                     "algorithmic_bytes_per_launch": f["bytes_per_launch"], "achieved_gbs": ach,
+                     "frac": (ach / peak) if ach else None, "share_of_step": f["ms_total"] / ms})
+    kern.sort(key=lambda k: -k["share_of_step"])
+    dom = next(k for k in kern if k["achieved_gbs"])
+    spm = next((k for k in kern if k["kernel"].startswith("spmm s=")), None)
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
-        traffic = json.load(open(tp)).get(f"cfg{args.config}_{args.method}_spmm")
-    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-            "traffic": traffic, "kernel": "spmm_kernel<double,16> (A·P + fused sum(q^H P~) partials)",
-            "algorithmic_bytes_per_launch": alg, "avg_launch_ms": avg_s * 1e3, "launches": spmm_n,
-            "share_of_step": spmm_ms / ms, "peak_source": peak_src}
-    it_bytes = iteration_bytes_egl_qmr(_Loc, s, esz) if args.method == "egl_qmr" else None
-    breakdown = {k: {"ms_total": v[0], "launches": v[1]} for k, v in prof.items()}
+        tj = json.load(open(tp))
+        traffic = tj.get(f"cfg{args.config}_{args.method}_" + ("spmm" if dom is spm else "dominant"))
+    roof = {"bound": "hbm", "achieved": dom["achieved_gbs"], "peak": peak, "unit": "GB/s",
+            "frac": dom["achieved_gbs"] / peak, "traffic": traffic, "kernel": dom["kernel"],
+            "algorithmic_bytes_per_launch": dom["algorithmic_bytes_per_launch"],
+            "avg_launch_ms": dom["avg_launch_ms"], "launches": dom["launches"],
+            "share_of_step": dom["share_of_step"], "peak_source": peak_src}
+    it_bytes = sum(nb for _, _, _, nb in recs) / K
+    breakdown = {}
+    for tag, _, t_ms, _ in recs:
+        e = breakdown.setdefault(tag, {"ms_total": 0.0, "launches": 0})
+        e["ms_total"] += t_ms
+        e["launches"] += 1
 
     # ---- end to end through the C-ABI with host buffers (pinned)
     e2e = None
@@ -331,11 +332,12 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
             "ms_per_step": ms / K, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64" if esz == 8 else "c128", "data": "synthetic", "config": cfgd,
-            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks,
+            "roofline": roof, "roofline_spmm": spm, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": int(launches), "clocks": clocks,
             "iteration": {"algorithmic_bytes": it_bytes,
-                          "achieved_gbs": (it_bytes / (ms / K / 1e3) / 1e9) if it_bytes else None,
-                          "frac_of_peak": (it_bytes / (ms / K / 1e3) / 1e9 / peak) if it_bytes else None,
-                          "kernel_breakdown": breakdown},
+                          "achieved_gbs": it_bytes / (ms / K / 1e3) / 1e9,
+                          "frac_of_peak": it_bytes / (ms / K / 1e3) / 1e9 / peak,
+                          "kernels": kern, "by_tag": breakdown},
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -159,13 +159,16 @@ int srk_matrix_create_dist(srk_ctx* ctx, const srk_csr* A_local, int64_t n_ghost
  * is fused into the epilogue and written to gram_out (device, dtype values):
  *   NORM2: ||Q||_F^2 (1 double); COLNORM2: s doubles; DIAG: (y_c^H q_c)_c (s);
  *   TRACE: tr(Y^H Q) (1); SUMVEC: sum(y^H Q) (1); FULL: Y^H Q (s x s).
- * Errors: SRK_EDIM (s < 1 or s > 64), SRK_EUNSUPPORTED (FULL with s > 16,
- * adjoint without A^H). */
+ * FULL with s > 16 is computed as the SpMM followed by Y^H Q on the FP64 tensor
+ * cores (DMMA, the dense contraction north_star names); s <= 16 fuses it into the
+ * SpMM epilogue. Errors: SRK_EDIM (s < 1 or s > 64), SRK_EUNSUPPORTED (adjoint
+ * without A^H). */
 int srk_spmm_block(srk_ctx* ctx, const srk_matrix* A, int adjoint, const void* P, void* Q, int s,
                    int gram, const void* Y, void* gram_out);
 
 /* out = reduction(X, Y) over n rows of two n x s blocks (mode as above; FULL gives
- * Y^H X). a3. */
+ * Y^H X, on the FP64 tensor cores for s > 16). a3, P:155-158, 178, 192-195,
+ * 243-249, 273-285, 443-447. */
 int srk_gram_block(srk_ctx* ctx, const void* X, const void* Y, int64_t n, int s, int dtype, int gram,
                    void* out);
 
@@ -224,6 +227,13 @@ int srk_solver_report(srk_solver* sv, srk_report* rep);
  * resets them. */
 int srk_solver_profile(srk_solver* sv, int enable);
 int srk_solver_profile_read(srk_solver* sv, double* ms_host, int64_t* count_host, int ntag);
+/* The same records launch by launch (instead of profile_read; resets them): tag
+ * as above, signature (SpMM: block width s; update: 16 * inputs + outputs),
+ * milliseconds, and the launch's algorithmic bytes (A's arrays
+ * once, every block operand read once and every result written once). Host
+ * arrays of max_records entries; returns the number of records (>= 0). */
+int srk_solver_profile_launches(srk_solver* sv, int32_t* tag_host, int32_t* sig_host, double* ms_host,
+                                double* bytes_host, int max_records);
 /* history (host array of length >= iterations): relative recursive residuals */
 int srk_solver_history(srk_solver* sv, double* hist_host, int cap);
 

@@ -33,7 +33,7 @@ EXPORTS = ("srk_create", "srk_destroy", "srk_last_error", "srk_version", "srk_ma
            "srk_block_update", "srk_tsqr", "srk_solve", "srk_solve_host", "srk_solver_create",
            "srk_solver_destroy", "srk_solver_start", "srk_solver_iterate", "srk_solver_get_x",
            "srk_solver_get_residual", "srk_solver_report", "srk_solver_history", "srk_solver_profile",
-           "srk_solver_profile_read", "srk_partition_rows", "srk_plan_create", "srk_plan_sizes", "srk_plan_arrays",
+           "srk_solver_profile_read", "srk_solver_profile_launches", "srk_partition_rows", "srk_plan_create", "srk_plan_sizes", "srk_plan_arrays",
            "srk_plan_destroy", "srk_nccl_unique_id", "srk_comm_init", "srk_matrix_create_dist")
 
 
@@ -103,6 +103,8 @@ def load_library(path: str | None = None):
         "srk_solver_history": ([vp, ctypes.POINTER(d), i], i),
         "srk_solver_profile": ([vp, i], i),
         "srk_solver_profile_read": ([vp, ctypes.POINTER(d), ctypes.POINTER(i64), i], i),
+        "srk_solver_profile_launches": ([vp, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32),
+                                         ctypes.POINTER(d), ctypes.POINTER(d), i], i),
         "srk_partition_rows": ([i64, vp, i, vp], i),
         "srk_plan_create": ([i64, vp, vp, i, vp, i, ctypes.POINTER(vp)], i),
         "srk_plan_sizes": ([vp, ctypes.POINTER(i64), ctypes.POINTER(i64), ctypes.POINTER(i64), ctypes.POINTER(i64)], i),
@@ -535,6 +537,17 @@ class Solver:
         cnt = (ctypes.c_int64 * n)()
         _check(_lib.srk_solver_profile_read(self.h, ms, cnt, n), "srk_solver_profile_read")
         return {t: (ms[i], cnt[i]) for i, t in enumerate(self.PROFILE_TAGS)}
+
+    def profile_launches(self, max_records: int = 1 << 16) -> list:
+        """Per-launch records [(tag, signature, ms, algorithmic_bytes)] since the last read."""
+        t = (ctypes.c_int32 * max_records)()
+        g = (ctypes.c_int32 * max_records)()
+        ms = (ctypes.c_double * max_records)()
+        nb = (ctypes.c_double * max_records)()
+        k = _lib.srk_solver_profile_launches(self.h, t, g, ms, nb, max_records)
+        _check(min(k, 0), "srk_solver_profile_launches")
+        return [(self.PROFILE_TAGS[t[i]] if t[i] < len(self.PROFILE_TAGS) else "other", g[i], ms[i], nb[i])
+                for i in range(k)]
 
     def close(self):
         if getattr(self, "h", None):

@@ -135,6 +135,10 @@ int srk_matrix_create(srk_ctx* ctx, const srk_csr* A, int need_adjoint, srk_matr
     m.nnzH = m.nnz;
   }
   cudaFree(dbad);
+  if (build_balanced_order(m, false, st) || (m.has_adj && build_balanced_order(m, true, st))) {
+    srk_matrix_destroy(M);
+    return fail(SRK_ENOMEM, "srk_matrix_create: balanced row order");
+  }
   *out = M;
   return SRK_OK;
 }
@@ -230,6 +234,10 @@ int srk_matrix_create_dist(srk_ctx* ctx, const srk_csr* A, int64_t n_ghost, cons
     srk_matrix_destroy(M);
     return fail(r, "srk_matrix_create_dist: invalid local CSR / halo (columns must be < n_local + n_ghost)");
   }
+  if (build_balanced_order(m, false, ctx->c.st) || (m.has_adj && build_balanced_order(m, true, ctx->c.st))) {
+    srk_matrix_destroy(M);
+    return fail(SRK_ENOMEM, "srk_matrix_create_dist: balanced row order");
+  }
   *out = M;
   return SRK_OK;
 }
@@ -249,6 +257,7 @@ int srk_matrix_destroy(srk_matrix* M) {
     delete[] H->recv_off;
   }
   if (m.sendbuf) cudaFree(m.sendbuf);
+  free_balanced_order(m);
   delete M;
   return SRK_OK;
 }
@@ -278,17 +287,22 @@ int srk_spmm_block(srk_ctx* ctx, const srk_matrix* A, int adjoint, const void* P
   if (adjoint && !A->m.has_adj) return fail(SRK_EUNSUPPORTED, "srk_spmm_block: matrix created without adjoint");
   if (gram != SRK_GRAM_NONE && (!gram_out || (gram != SRK_GRAM_NORM2 && gram != SRK_GRAM_COLNORM2 && !Y)))
     return fail(SRK_EINVAL, "srk_spmm_block: gram needs Y and gram_out");
-  if (gram == SRK_GRAM_FULL && !full_supported(A->m.cplx, cap_for(s)))
-    return fail(SRK_EUNSUPPORTED, "srk_spmm_block: fused FULL Gram needs s <= 16");
   Eng e;
   e.c = &ctx->c;
   e.A = &A->m;
   e.cplx = A->m.cplx;
   e.n = A->m.n;
   e.ws = reinterpret_cast<double*>(gram_out);
-  std::vector<RQ> reds;
-  if (gram != SRK_GRAM_NONE) reds.push_back(RQ{gram, 0, -1, Y, 0});
-  int r = e.spmm(adjoint != 0, P, Q, s, reds);
+  int r;
+  if (gram == SRK_GRAM_FULL && !full_supported(A->m.cplx, cap_for(s))) {
+    // s > 16: the s x s Gram is a dense contraction — SpMM, then Y^H Q on the FP64 tensor cores
+    r = e.spmm(adjoint != 0, P, Q, s, {});
+    if (!r) r = e.gram_full(Q, Y, s, 0);
+  } else {
+    std::vector<RQ> reds;
+    if (gram != SRK_GRAM_NONE) reds.push_back(RQ{gram, 0, -1, Y, 0});
+    r = e.spmm(adjoint != 0, P, Q, s, reds);
+  }
   return check_cuda(r, "srk_spmm_block");
 }
 
@@ -298,8 +312,6 @@ int srk_gram_block(srk_ctx* ctx, const void* X, const void* Y, int64_t n, int s,
   if (!gram_ok(gram) || gram == SRK_GRAM_NONE) return fail(SRK_EINVAL, "srk_gram_block: bad gram mode");
   if (gram != SRK_GRAM_NORM2 && gram != SRK_GRAM_COLNORM2 && !Y) return fail(SRK_EINVAL, "srk_gram_block: Y needed");
   const bool cplx = dtype == SRK_C128;
-  if (gram == SRK_GRAM_FULL && !full_supported(cplx, cap_for(s)))
-    return fail(SRK_EUNSUPPORTED, "srk_gram_block: FULL Gram needs s <= 16");
   Eng e;
   e.c = &ctx->c;
   e.cplx = cplx;
@@ -308,6 +320,7 @@ int srk_gram_block(srk_ctx* ctx, const void* X, const void* Y, int64_t n, int s,
   int r;
   if (gram == SRK_GRAM_SUMVEC) r = e.upd(s, {X}, {}, {RQ{gram, 0, -1, Y, 0}});
   else if (gram == SRK_GRAM_NORM2 || gram == SRK_GRAM_COLNORM2) r = e.upd(s, {X}, {}, {RQ{gram, 0, -1, nullptr, 0}});
+  else if (gram == SRK_GRAM_FULL && !full_supported(cplx, cap_for(s))) r = e.gram_full(X, Y, s, 0);  // s > 16: DMMA
   else r = e.upd(s, {X, Y}, {}, {RQ{gram, 0, 1, nullptr, 0}});
   return check_cuda(r, "srk_gram_block");
 }
@@ -490,6 +503,13 @@ int srk_solver_profile_read(srk_solver* h, double* ms_host, int64_t* count_host,
   h->sv->prof.read(ms_host, cnt.data(), ntag);
   for (int i = 0; i < ntag; ++i) count_host[i] = cnt[i];
   return SRK_OK;
+}
+
+int srk_solver_profile_launches(srk_solver* h, int32_t* tag_host, int32_t* sig_host, double* ms_host,
+                                double* bytes_host, int max_records) {
+  if (!h || !tag_host || !sig_host || !ms_host || !bytes_host || max_records < 0)
+    return fail(SRK_EINVAL, "srk_solver_profile_launches: null argument");
+  return h->sv->prof.read_launches(tag_host, sig_host, ms_host, bytes_host, max_records);
 }
 
 int srk_solver_history(srk_solver* h, double* hist_host, int cap) {

@@ -236,7 +236,10 @@ __global__ void __launch_bounds__(256, FC ? 1 : MINB) spmm_kernel(SpmmArgs a) {
   constexpr int EPN = CW / L::G;            // (col, val) pairs per lane per step
   // row_ptr of one batch of R rows: (begin, end) kept raw — consuming a freshly
   // loaded register stalls the in-order warp, so lengths are formed a step later
-  auto load_rp = [&](long long k, int (&bg)[R], int (&ln)[R]) {
+  // (balanced row order: rp/ci/val are the length-sorted copy and the output row
+  // of sorted row r is perm[r], fetched with the row pointers)
+  const int* __restrict__ perm = a.perm;
+  auto load_rp = [&](long long k, int (&bg)[R], int (&ln)[R], int (&pr)[R]) {
     const long long r0 = row_of(k);
 #pragma unroll
     for (int i = 0; i < R; ++i) {
@@ -244,6 +247,7 @@ __global__ void __launch_bounds__(256, FC ? 1 : MINB) spmm_kernel(SpmmArgs a) {
       const bool in = r < n;
       bg[i] = in ? __ldg(rp + r) : 0;
       ln[i] = in ? __ldg(rp + r + 1) : 0;  // end; converted to a length by to_len
+      pr[i] = (in && perm) ? __ldg(perm + r) : (int)r;
     }
   };
   auto to_len = [&](const int (&bg)[R], int (&ln)[R]) {
@@ -268,11 +272,12 @@ __global__ void __launch_bounds__(256, FC ? 1 : MINB) spmm_kernel(SpmmArgs a) {
   // gathers of batch k are in flight, the (col, val) of batches up to k+PD and the
   // row pointers of batch k+PD+1 are being fetched (PD = prefetch depth).
   int bq[PD + 1][R], lq[PD + 1][R];  // row pointers (begin, length) of batches k..k+PD
+  int pq[PD + 1][R];                 // output rows of batches k..k+PD
   int cq[PD][R][EPN];                // (col, val) of batches k..k+PD-1
   T vq[PD][R][EPN];
 #pragma unroll
   for (int d = 0; d <= PD; ++d) {
-    load_rp(d, bq[d], lq[d]);
+    load_rp(d, bq[d], lq[d], pq[d]);
     to_len(bq[d], lq[d]);
   }
 #pragma unroll
@@ -285,9 +290,9 @@ __global__ void __launch_bounds__(256, FC ? 1 : MINB) spmm_kernel(SpmmArgs a) {
     T (&vj)[R][EPN] = vq[0];
     int cjn[R][EPN];
     T vjn[R][EPN];
-    int begnn[R], lennn[R];
+    int begnn[R], lennn[R], prnn[R];
     load_cv(bq[PD], lq[PD], 0, cjn, vjn);
-    load_rp(k + PD + 1, begnn, lennn);
+    load_rp(k + PD + 1, begnn, lennn, prnn);
     // epilogue operand of the first reduction, requested before the gathers
     T yr0[R][L::EPL];
     T yv0[R];
@@ -296,8 +301,8 @@ __global__ void __launch_bounds__(256, FC ? 1 : MINB) spmm_kernel(SpmmArgs a) {
       yv0[i] = Ar<T>::zero();
 #pragma unroll
       for (int e = 0; e < L::EPL; ++e) yr0[i][e] = Ar<T>::zero();
-      const long long row = r0 + i;
-      if (YPRE && row < n && mode0 != RED_NONE) {
+      const long long row = pq[0][i];
+      if (YPRE && r0 + i < n && mode0 != RED_NONE) {
         if (mode0 == RED_SUMVEC) yv0[i] = y0[row];
         else if (mode0 != RED_NORM2 && mode0 != RED_COLNORM2) {
           if constexpr (EX) row_load_ex_rw<T, S>(y0 + (size_t)row * S, g, yr0[i]);
@@ -360,8 +365,8 @@ __global__ void __launch_bounds__(256, FC ? 1 : MINB) spmm_kernel(SpmmArgs a) {
     }
 #pragma unroll
     for (int i = 0; i < R; ++i) {
-      const long long row = r0 + i;
-      if (row < n) {
+      const long long row = pq[0][i];
+      if (r0 + i < n) {
         if constexpr (EX) row_store_ex<T, S>(Q + (size_t)row * S, g, q[i]);
         else row_store<T, S>(Q + (size_t)row * s, g, s, a.vec, q[i]);
         // fused epilogue: reductions with X = Q
@@ -396,9 +401,11 @@ __global__ void __launch_bounds__(256, FC ? 1 : MINB) spmm_kernel(SpmmArgs a) {
       for (int d = 0; d < PD; ++d) {
         bq[d][i] = bq[d + 1][i];
         lq[d][i] = lq[d + 1][i];
+        pq[d][i] = pq[d + 1][i];
       }
       bq[PD][i] = begnn[i];
       lq[PD][i] = lennn[i];
+      pq[PD][i] = prnn[i];
 #pragma unroll
       for (int u = 0; u < EPN; ++u) {
 #pragma unroll

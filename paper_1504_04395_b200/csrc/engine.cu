@@ -19,7 +19,7 @@ int Ctx::ensure_partials(size_t n) {
   return 0;
 }
 
-void Prof::begin(int t, cudaStream_t st) {
+void Prof::begin(int t, cudaStream_t st, int signature, double nbytes) {
   if (!on) return;
   if (used * 2 + 2 > ev.size()) {
     for (int i = 0; i < 2; ++i) {
@@ -28,9 +28,27 @@ void Prof::begin(int t, cudaStream_t st) {
       ev.push_back(e);
     }
     tag.push_back(0);
+    sig.push_back(0);
+    bytes.push_back(0.0);
   }
   tag[used] = t;
+  sig[used] = signature;
+  bytes[used] = nbytes;
   cudaEventRecord(ev[2 * used], st);
+}
+int Prof::read_launches(int* tag_out, int* sig_out, double* ms_out, double* bytes_out, int max) {
+  const int k = (int)std::min(used, (size_t)max);
+  for (int i = 0; i < k; ++i) {
+    cudaEventSynchronize(ev[2 * i + 1]);
+    float t = 0.f;
+    cudaEventElapsedTime(&t, ev[2 * i], ev[2 * i + 1]);
+    tag_out[i] = tag[i];
+    sig_out[i] = sig[i];
+    ms_out[i] = t;
+    bytes_out[i] = bytes[i];
+  }
+  used = 0;
+  return k;
 }
 void Prof::end(cudaStream_t st) {
   if (!on) return;
@@ -140,9 +158,17 @@ int Eng::spmm(bool adj, const void* P, void* Q, int s, std::vector<RQ> reds) {
   for (auto& r : reds) full |= (r.mode == RED_FULL);
   if (full && !full_supported(cplx, cap)) return err = (int)cudaErrorNotSupported;
   SpmmArgs a{};
-  a.row_ptr = adj ? A->rpH : A->rp;
-  a.col_idx = adj ? A->ciH : A->ci;
-  a.val = adj ? A->valH : A->val;
+  const Mat::Sorted& so = adj ? A->srtH : A->srt;
+  if (so.perm) {  // irregular rows: the length-sorted copy
+    a.row_ptr = so.rp;
+    a.col_idx = so.ci;
+    a.val = so.val;
+    a.perm = so.perm;
+  } else {
+    a.row_ptr = adj ? A->rpH : A->rp;
+    a.col_idx = adj ? A->ciH : A->ci;
+    a.val = adj ? A->valH : A->val;
+  }
   a.P = P;
   a.Q = Q;
   a.n = n;
@@ -165,7 +191,15 @@ int Eng::spmm(bool adj, const void* P, void* Q, int s, std::vector<RQ> reds) {
   a.partials = c->partials;
   a.done = done;
   nlaunch++;
-  if (prof) prof->begin(adj ? PT_SPMM_ADJ : PT_SPMM, c->st);
+  if (prof) {
+    const double esz = cplx ? 16.0 : 8.0;
+    const double nz = (double)(adj ? A->nnzH : A->nnz);
+    double nb = (double)(n + 1) * 4 + nz * (4 + esz) + 2.0 * (double)n * s * esz;
+    for (auto& r : reds)
+      if (r.yext && r.mode != RED_NORM2 && r.mode != RED_COLNORM2)
+        nb += (double)n * (r.mode == RED_SUMVEC ? 1 : s) * esz;
+    prof->begin(adj ? PT_SPMM_ADJ : PT_SPMM, c->st, s, nb);
+  }
   err = launch_spmm(cplx, cap, full, a, grid, 256, smem, c->st);
   if (prof) prof->end(c->st);
   if (err) return err;
@@ -227,11 +261,110 @@ int Eng::upd(int s, std::vector<const void*> in, std::vector<OutSpec> outs, std:
   if ((err = c->ensure_partials((size_t)grid * a.pstride))) return err;
   a.partials = c->partials;
   nlaunch++;
-  if (prof) prof->begin(PT_UPD, c->st);
+  if (prof) {
+    double nb = (double)n * s * esz * (double)a.nin;
+    int nw = 0;
+    for (auto& o : outs) nw += o.ptr ? 1 : 0;
+    nb += (double)n * s * esz * nw;
+    for (auto& r : reds)
+      if (r.y < 0 && r.yext && r.mode != RED_NORM2 && r.mode != RED_COLNORM2)
+        nb += (double)n * (r.mode == RED_SUMVEC ? 1 : s) * esz;
+    prof->begin(PT_UPD, c->st, 16 * a.nin + a.nout, nb);
+  }
   err = launch_upd(cplx, cap, full, a, grid, 256, smem, c->st);
   if (prof) prof->end(c->st);
   if (err) return err;
   return err = finish_reds(*this, reds, poffs, s, grid, a.pstride);
+}
+
+int Eng::gram_full(const void* X, const void* Y, int s, int woff) {
+  if (err) return err;
+  GramArgs g{};
+  g.X = reinterpret_cast<const double*>(X);
+  g.Y = reinterpret_cast<const double*>(Y);
+  g.n = n;
+  g.w = s * (cplx ? 2 : 1);
+  g.s = s;
+  g.cplx = cplx ? 1 : 0;
+  const int len = red_len(RED_FULL, s, cplx);
+  const int grid = (int)std::max(1, std::min(c->nsm, gram_mma_chunks(n)));
+  if ((err = c->ensure_partials((size_t)grid * len))) return err;
+  g.partials = c->partials;
+  g.pstride = len;
+  g.done = done;
+  nlaunch++;
+  if (prof) prof->begin(PT_UPD, c->st, 16 * 2 + 0, 2.0 * (double)n * s * (cplx ? 16 : 8));
+  err = launch_gram_mma(g, grid, c->st);
+  if (prof) prof->end(c->st);
+  if (err) return err;
+  return err = finish_reds(*this, {RQ{RED_FULL, 0, 1, nullptr, woff}}, {0}, s, grid, len);
+}
+
+// ---------------------------------------------------------------------------
+// balanced row order (SELL-C-sigma's sorting step with sigma = n, C = one warp)
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ static void gather_sorted_rows(const int* rp, const int* ci, const T* val, const int* perm, const int* rp2,
+                                          int* ci2, T* val2, long long n) {
+  const long long warp = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  for (long long l = warp; l < n; l += nw) {
+    const int src = perm[l];
+    const int b = rp[src], len = rp[src + 1] - b, d = rp2[l];
+    for (int j = lane; j < len; j += 32) {
+      ci2[d + j] = ci[b + j];
+      val2[d + j] = val[b + j];
+    }
+  }
+}
+
+int build_balanced_order(Mat& m, bool adj, cudaStream_t st) {
+  const int* rp = adj ? m.rpH : m.rp;
+  const int* ci = adj ? m.ciH : m.ci;
+  const void* val = adj ? m.valH : m.val;
+  const long long n = m.n, nnz = adj ? m.nnzH : m.nnz;
+  if (n < 1 || nnz < 1 || !rp) return 0;
+  std::vector<int> h(n + 1);
+  if (cudaMemcpyAsync(h.data(), rp, sizeof(int) * (n + 1), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess)
+    return (int)cudaErrorUnknown;
+  long long maxlen = 0;
+  for (long long i = 0; i < n; ++i) maxlen = std::max<long long>(maxlen, h[i + 1] - h[i]);
+  const double mean = (double)nnz / (double)n;
+  // regular lengths (stencils, lattices): a warp's rows already have equal work
+  if ((double)maxlen < 4.0 * mean + 8.0) return 0;
+  std::vector<int> perm(n);
+  for (long long i = 0; i < n; ++i) perm[i] = (int)i;
+  std::stable_sort(perm.begin(), perm.end(), [&](int x, int y) { return h[x + 1] - h[x] > h[y + 1] - h[y]; });
+  std::vector<int> rp2(n + 1);
+  rp2[0] = 0;
+  for (long long l = 0; l < n; ++l) rp2[l + 1] = rp2[l] + (h[perm[l] + 1] - h[perm[l]]);
+  Mat::Sorted& so = adj ? m.srtH : m.srt;
+  const size_t esz = m.cplx ? 16 : 8;
+  if (cudaMalloc(&so.rp, sizeof(int) * (n + 1)) != cudaSuccess || cudaMalloc(&so.perm, sizeof(int) * n) != cudaSuccess ||
+      cudaMalloc(&so.ci, sizeof(int) * (nnz + 1)) != cudaSuccess || cudaMalloc(&so.val, esz * (nnz + 1)) != cudaSuccess)
+    return (int)cudaErrorMemoryAllocation;
+  cudaMemcpyAsync(so.rp, rp2.data(), sizeof(int) * (n + 1), cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(so.perm, perm.data(), sizeof(int) * n, cudaMemcpyHostToDevice, st);
+  const int grid = (int)std::min<long long>((n + 7) / 8, 148 * 16);
+  if (m.cplx)
+    gather_sorted_rows<double2><<<grid, 256, 0, st>>>(rp, ci, reinterpret_cast<const double2*>(val), so.perm, so.rp, so.ci,
+                                                      reinterpret_cast<double2*>(so.val), n);
+  else
+    gather_sorted_rows<double><<<grid, 256, 0, st>>>(rp, ci, reinterpret_cast<const double*>(val), so.perm, so.rp, so.ci,
+                                                     reinterpret_cast<double*>(so.val), n);
+  return (int)cudaStreamSynchronize(st);  // rp2 / perm host buffers go out of scope
+}
+
+void free_balanced_order(Mat& m) {
+  for (Mat::Sorted* so : {&m.srt, &m.srtH}) {
+    if (so->rp) cudaFree(so->rp);
+    if (so->ci) cudaFree(so->ci);
+    if (so->val) cudaFree(so->val);
+    if (so->perm) cudaFree(so->perm);
+    *so = Mat::Sorted{};
+  }
 }
 
 // ---------------------------------------------------------------------------

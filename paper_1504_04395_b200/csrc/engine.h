@@ -18,6 +18,9 @@ int padded_width(int cap, bool cplx);
 int launch_spmm(bool cplx, int cap, bool full, const SpmmArgs& a, int grid, int block, size_t smem, cudaStream_t st);
 int launch_upd(bool cplx, int cap, bool full, const UpdArgs& a, int grid, int block, size_t smem, cudaStream_t st);
 int launch_fin(const FinArgs& a, cudaStream_t st);
+int launch_gram_mma(const GramArgs& g, int grid, cudaStream_t st);
+
+int gram_mma_chunks(long long n);
 int launch_row_mean(bool cplx, const void* X, void* out, long long n, int s, const int* done, cudaStream_t st);
 int launch_csr_transpose(bool cplx, long long n, long long nnz, const int* rp, const int* ci, const void* val,
                          int* rpT, int* ciT, void* valT, int* work, cudaStream_t st);
@@ -49,6 +52,16 @@ struct Mat {
   int* rpH = nullptr;
   int* ciH = nullptr;
   void* valH = nullptr;
+  // Balanced row order (irregular row lengths, e.g. config 5's power law): a copy
+  // of the CSR with rows sorted by decreasing length (stable), so that the rows a
+  // warp processes together have similar lengths; perm[l] = original row of
+  // sorted row l (the SpMM writes Q[perm[l]]). Null when the lengths are regular.
+  struct Sorted {
+    int* rp = nullptr;
+    int* ci = nullptr;
+    void* val = nullptr;
+    int* perm = nullptr;
+  } srt, srtH;
   // multi-GPU (row-partitioned) operator: local rows, columns [0, n) owned and
   // [n, n + n_ghost) ghost rows received from the owning ranks before each SpMM
   bool dist = false;
@@ -57,6 +70,10 @@ struct Mat {
   size_t sendcap = 0;         // doubles
   long long ghost_rows() const { return dist ? std::max(halo.n_ghost, haloH.n_ghost) : 0; }
 };
+
+// builds m.srt / m.srtH when the row lengths are irregular (engine.cu)
+int build_balanced_order(Mat& m, bool adj, cudaStream_t st);
+void free_balanced_order(Mat& m);
 
 // reduction request: X = source (or the SpMM output), Y = source or external
 struct RQ {
@@ -85,14 +102,21 @@ constexpr int O0 = SRC_OUT, O1 = SRC_OUT + 1, O2 = SRC_OUT + 2, O3 = SRC_OUT + 3
 // Kernel-call helper bound to one (ctx, operator, dtype, n).
 // Per-launch CUDA-event timing (bench.py's live roofline): tags
 enum ProfTag : int { PT_SPMM = 0, PT_SPMM_ADJ = 1, PT_UPD = 2, PT_FIN = 3, PT_COEF = 4, PT_OTHER = 5, PT_N = 6 };
+// Each record also carries the launch's algorithmic bytes (every
+// operand read once, every result written once, A's arrays once) and a signature
+// (SpMM: block width; update: 16 * inputs + outputs) so that a caller can compute
+// the achieved bandwidth of every kernel of an iteration.
 struct Prof {
   bool on = false;
   std::vector<cudaEvent_t> ev;   // pairs (start, stop)
-  std::vector<int> tag;
+  std::vector<int> tag, sig;
+  std::vector<double> bytes;
   size_t used = 0;               // pairs used since the last read
-  void begin(int t, cudaStream_t st);
+  void begin(int t, cudaStream_t st, int signature = 0, double nbytes = 0.0);
   void end(cudaStream_t st);
   int read(double* ms, long long* cnt, int ntag);  // sums per tag, resets
+  // per-launch records since the last read (resets); returns the record count
+  int read_launches(int* tag_out, int* sig_out, double* ms_out, double* bytes_out, int max);
   ~Prof();
 };
 
@@ -109,6 +133,8 @@ struct Eng {
   int spmm(bool adj, const void* P, void* Q, int s, std::vector<RQ> reds);
   int halo(bool adj, const void* P, int s);
   int upd(int s, std::vector<const void*> in, std::vector<OutSpec> outs, std::vector<RQ> reds);
+  // s x s Gram Y^H X on the FP64 tensor cores (gram_mma.cu), written to ws + woff
+  int gram_full(const void* X, const void* Y, int s, int woff);
   int grid_for(int cap, bool full, bool is_spmm, size_t smem, int nin) const;
 };
 

@@ -94,6 +94,21 @@ struct SpmmArgs {
   double* partials;
   int pstride;
   const int* done;
+  const int* perm;  // balanced row order: CSR arrays are in sorted order, output row = perm[row]
+};
+
+// s x s Gram Y^H X on the FP64 tensor cores (gram_mma.cu); the real view of the
+// blocks: n rows of w = s (real) or 2s (complex, interleaved) doubles.
+struct GramArgs {
+  const double* X;
+  const double* Y;
+  long long n;
+  int w;
+  int s;
+  int cplx;
+  double* partials;  // [gridDim.x][pstride], the Gram at offset 0 in the FULL layout
+  int pstride;
+  const int* done;
 };
 
 // Segments for the deterministic second-stage reduction of CTA partials.

@@ -56,10 +56,13 @@ def main(tag):
         wr = to_bytes(v["dram__bytes_write.sum"], u["dram__bytes_write.sum"])
         summary[name]["dram_bytes_per_launch"] = rd + wr
     json.dump(summary, open(os.path.join(PROF, f"{tag}_ncu_summary.json"), "w"), indent=1)
+    tj = {"source": f"profiles/{tag}_ncu_summary.json (ncu --set full, one launch, cold cache)"}
     if "spmm" in summary:
-        json.dump({"cfg3_egl_qmr_spmm": summary["spmm"]["dram_bytes_per_launch"],
-                   "source": f"profiles/{tag}_ncu_summary.json (ncu --set full, one launch, cold cache)"},
-                  open(os.path.join(PROF, "traffic.json"), "w"), indent=1)
+        tj["cfg3_egl_qmr_spmm"] = summary["spmm"]["dram_bytes_per_launch"]
+    if "upd" in summary:  # the 6-input / 4-output update: the dominant kernel of the eGl-QMR step
+        tj["cfg3_egl_qmr_dominant"] = summary["upd"]["dram_bytes_per_launch"]
+    if len(tj) > 1:
+        json.dump(tj, open(os.path.join(PROF, "traffic.json"), "w"), indent=1)
     lc = os.path.join(OUT, "launches.csv")
     if os.path.exists(lc):
         lines = [ln for ln in open(lc) if ln.startswith('"')]

@@ -81,8 +81,9 @@ def test_spmm_fused_reductions(srk, s, cplx, mode):
 
 
 @pytest.mark.parametrize("cplx", [False, True])
-@pytest.mark.parametrize("s", [1, 2, 5, 8, 16])
+@pytest.mark.parametrize("s", [1, 2, 5, 8, 16, 17, 24, 32, 33, 48, 64])
 def test_gram_block(srk, s, cplx):
+    """FULL Y^H X and the trace; s > 16 runs on the FP64 tensor cores (DMMA)."""
     rng = np.random.default_rng(11)
     n = 10007
     X, Y = _rand(rng, n, s, cplx), _rand(rng, n, s, cplx)
@@ -116,6 +117,18 @@ def test_tsqr_matches_oracle(srk, s, cplx):
     assert rank == s
     assert rel(C, Co) < 1e-12 and rel(Q, Qo) < 1e-12
     assert np.linalg.norm(Q.conj().T @ Q - np.eye(s)) < 1e-12
+
+
+@pytest.mark.parametrize("cplx", [False, True])
+@pytest.mark.parametrize("s", [32, 64])
+def test_gram_mma_edge_rows(srk, s, cplx):
+    """DMMA Gram on row counts around the 32-row chunk (1, 31, 32, 33 rows, and
+    fewer chunks than SMs), against the oracle's Gram."""
+    rng = np.random.default_rng(23)
+    for n in (1, 31, 32, 33, 4 * 32 * 148 + 5):
+        X, Y = _rand(rng, n, s, cplx), _rand(rng, n, s, cplx)
+        g = to_np(srk.gram_block(to_dev(X), to_dev(Y), "full"))
+        assert rel(g, OL.gram(Y, X)) < 1e-12, n
 
 
 def test_tsqr_rank_deficient(srk):
@@ -160,14 +173,14 @@ def test_full_size_config3_spmm_sampled(srk):
 @pytest.mark.parametrize("s", [1, 2, 4, 8, 16, 32, 64])
 def test_config5_spmm_gram_sweep(srk, s):
     """Config 5's SpMM+Gram sweep (power-law rows up to 512, uniform columns) at
-    n = 2^16: the product and the fused reductions (FULL up to s = 16; trace, sum
-    and norms at every s) against the oracle."""
+    n = 2^16: the product and the reductions (trace, sum, norms and the full s x s
+    Gram at every s) against the oracle."""
     A = synth.power_law(1 << 16, seed=4)
     As = A.to_scipy()
     M = srk.Matrix.from_csr(A, need_adjoint=False)
     P = synth.random_rhs(A.n, s, 4)
     Y = synth.random_rhs(A.n, s, 5)
-    modes = ["trace", "norm2", "sumvec"] + (["full"] if s <= 16 else [])
+    modes = ["trace", "norm2", "sumvec", "full"]  # FULL: fused for s <= 16, DMMA Gram after the SpMM above
     ref = As @ P
     for mode in modes:
         Yd = to_dev(Y[:, 0].copy()) if mode == "sumvec" else to_dev(Y)
