@@ -109,6 +109,17 @@ int srk_version(void);
  * A^H = conj(A)^T explicitly ("A^H P̂"). Errors: SRK_EINVAL for an
  * invalid CSR (unsorted / out-of-range columns, bad row_ptr), SRK_ENOMEM. */
 int srk_matrix_create(srk_ctx* ctx, const srk_csr* A, int need_adjoint, srk_matrix** out);
+/* Block-sparse operator (a0, "BSR-12 (lattice)" of SURVEY §8(a); PAPER.md Ex. 4,
+ * P:752-778): nb block rows of bs x bs blocks, block_row_ptr (nb+1, int64),
+ * block_col (nnzb, int32, sorted unique per block row, < nb) and values (nnzb
+ * blocks, each bs x bs row-major, complex interleaved), all DEVICE pointers, copied.
+ * unit_diag = 1: the diagonal blocks are the identity and are NOT stored
+ * (A = I + sum of the stored blocks, the A = I - kappa H form). Supported: bs = 12,
+ * dtype SRK_C128, block widths s in {4, 8, 12, 16}, methods without A^H (the
+ * BiCGStab family). Errors: SRK_EINVAL (invalid blocks), SRK_EUNSUPPORTED. */
+int srk_matrix_create_bsr(srk_ctx* ctx, int64_t nb, int bs, int64_t nnzb, const int64_t* block_row_ptr,
+                          const int32_t* block_col, const void* values, int dtype, int unit_diag,
+                          srk_matrix** out);
 int srk_matrix_destroy(srk_matrix* A);
 /* copy A^H back (CSR arrays of size n+1 / nnz, device pointers) — for tests */
 int srk_matrix_adjoint(const srk_matrix* A, int64_t* row_ptr, int32_t* col_idx, void* values);

@@ -34,7 +34,8 @@ EXPORTS = ("srk_create", "srk_destroy", "srk_last_error", "srk_version", "srk_ma
            "srk_solver_destroy", "srk_solver_start", "srk_solver_iterate", "srk_solver_get_x",
            "srk_solver_get_residual", "srk_solver_report", "srk_solver_history", "srk_solver_profile",
            "srk_solver_profile_read", "srk_solver_profile_launches", "srk_partition_rows", "srk_plan_create", "srk_plan_sizes", "srk_plan_arrays",
-           "srk_plan_destroy", "srk_nccl_unique_id", "srk_comm_init", "srk_matrix_create_dist")
+           "srk_plan_destroy", "srk_nccl_unique_id", "srk_comm_init", "srk_matrix_create_dist",
+           "srk_matrix_create_bsr")
 
 
 class SrkError(RuntimeError):
@@ -85,6 +86,7 @@ def load_library(path: str | None = None):
         "srk_last_error": ([], ctypes.c_char_p),
         "srk_version": ([], i),
         "srk_matrix_create": ([vp, ctypes.POINTER(_Csr), i, ctypes.POINTER(vp)], i),
+        "srk_matrix_create_bsr": ([vp, i64, i, i64, vp, vp, vp, i, i, ctypes.POINTER(vp)], i),
         "srk_matrix_destroy": ([vp], i),
         "srk_matrix_adjoint": ([vp, vp, vp, vp], i),
         "srk_spmm_block": ([vp, vp, i, vp, vp, i, i, vp, vp], i),
@@ -219,6 +221,31 @@ class Matrix:
         if hasattr(A, "indptr"):
             return cls(A.indptr, A.indices, A.data, need_adjoint=need_adjoint, ctx=ctx)
         return cls(A.row_ptr, A.col_idx, A.values, need_adjoint=need_adjoint, ctx=ctx)
+
+    @classmethod
+    def from_bsr(cls, block_row_ptr, block_col, blocks, unit_diag: bool = False, ctx=None):
+        """Block-sparse operator (srk_matrix_create_bsr): blocks (nnzb, 12, 12) complex
+        row-major; unit_diag: identity diagonal blocks implied, not stored."""
+        torch = _torch()
+        self = cls.__new__(cls)
+        self.ctx = ctx or default_context()
+        dev = torch.device("cuda", self.ctx.device)
+        rp = torch.as_tensor(np.asarray(block_row_ptr)).to(dev, torch.int64).contiguous()
+        ci = torch.as_tensor(np.asarray(block_col)).to(dev, torch.int32).contiguous()
+        va = blocks if isinstance(blocks, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(blocks))
+        va = va.to(dev, torch.complex128).contiguous()
+        nb = rp.numel() - 1
+        bs = int(va.shape[-1]) if va.dim() == 3 else 12
+        self.n = nb * bs
+        self.nnz = ci.numel() * bs * bs + (self.n if unit_diag else 0)
+        self.dtype = torch.complex128
+        h = ctypes.c_void_p()
+        _check(_lib.srk_matrix_create_bsr(self.ctx.h, nb, bs, ci.numel(), ctypes.c_void_p(rp.data_ptr()),
+                                          ctypes.c_void_p(ci.data_ptr()), ctypes.c_void_p(va.data_ptr()),
+                                          _dtype_code(va), int(unit_diag), ctypes.byref(h)), "srk_matrix_create_bsr")
+        self.h = h
+        self.has_adjoint = False
+        return self
 
     def adjoint_csr(self):
         torch = _torch()

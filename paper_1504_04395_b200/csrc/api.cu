@@ -143,6 +143,58 @@ int srk_matrix_create(srk_ctx* ctx, const srk_csr* A, int need_adjoint, srk_matr
   return SRK_OK;
 }
 
+int srk_matrix_create_bsr(srk_ctx* ctx, int64_t nb, int bs, int64_t nnzb, const int64_t* block_row_ptr,
+                          const int32_t* block_col, const void* values, int dtype, int unit_diag,
+                          srk_matrix** out) {
+  if (!ctx || !out || !block_row_ptr || nb < 1 || nnzb < 0 || (nnzb > 0 && (!block_col || !values)))
+    return fail(SRK_EINVAL, "srk_matrix_create_bsr: bad argument");
+  if (bs != 12 || dtype != SRK_C128)
+    return fail(SRK_EUNSUPPORTED, "srk_matrix_create_bsr: 12 x 12 complex blocks only");
+  if (nnzb >= 2147483647LL) return fail(SRK_EUNSUPPORTED, "srk_matrix_create_bsr: nnzb >= 2^31");
+  cudaStream_t st = ctx->c.st;
+  auto* M = new srk_matrix();
+  Mat& m = M->m;
+  m.ctx = &ctx->c;
+  m.cplx = true;
+  m.bsr = true;
+  m.bs = bs;
+  m.nb = nb;
+  m.nnzb = nnzb;
+  m.unit_diag = unit_diag ? 1 : 0;
+  m.n = nb * bs;
+  m.nnz = nnzb * bs * bs + (unit_diag ? m.n : 0);
+  const size_t bbytes = (size_t)bs * bs * 16;
+  int* dbad = nullptr;
+  if (cudaMalloc(&m.brp, sizeof(int) * (nb + 1)) != cudaSuccess || cudaMalloc(&m.bci, sizeof(int) * (nnzb + 1)) != cudaSuccess ||
+      cudaMalloc(&m.bval, bbytes * (nnzb + 1)) != cudaSuccess || cudaMalloc(&dbad, sizeof(int)) != cudaSuccess) {
+    if (dbad) cudaFree(dbad);
+    srk_matrix_destroy(M);
+    return fail(SRK_ENOMEM, "srk_matrix_create_bsr: out of device memory");
+  }
+  cudaMemsetAsync(dbad, 0, sizeof(int), st);
+  const int grid = (int)std::max<long long>(1, std::min<long long>((nb + 256) / 256, 148 * 8));
+  rp64to32<<<grid, 256, 0, st>>>(block_row_ptr, m.brp, nb, dbad);
+  if (nnzb > 0) {
+    cudaMemcpyAsync(m.bci, block_col, sizeof(int) * nnzb, cudaMemcpyDeviceToDevice, st);
+    cudaMemcpyAsync(m.bval, values, bbytes * nnzb, cudaMemcpyDeviceToDevice, st);
+  }
+  launch_csr_check(nb, nb, nnzb, m.brp, m.bci, 1, dbad, st);
+  int bad = 0;
+  cudaMemcpyAsync(&bad, dbad, sizeof(int), cudaMemcpyDeviceToHost, st);
+  cudaError_t e = cudaStreamSynchronize(st);
+  cudaFree(dbad);
+  if (e != cudaSuccess) {
+    srk_matrix_destroy(M);
+    return cuda_fail(e, "srk_matrix_create_bsr");
+  }
+  if (bad) {
+    srk_matrix_destroy(M);
+    return fail(SRK_EINVAL, "srk_matrix_create_bsr: invalid block structure (row pointers / sorted block columns)");
+  }
+  *out = M;
+  return SRK_OK;
+}
+
 // ---------------------------------------------------------------- multi-GPU
 int srk_nccl_unique_id(void* id128_host) {
   if (!id128_host) return fail(SRK_EINVAL, "srk_nccl_unique_id: null buffer");
@@ -257,6 +309,9 @@ int srk_matrix_destroy(srk_matrix* M) {
     delete[] H->recv_off;
   }
   if (m.sendbuf) cudaFree(m.sendbuf);
+  if (m.brp) cudaFree(m.brp);
+  if (m.bci) cudaFree(m.bci);
+  if (m.bval) cudaFree(m.bval);
   free_balanced_order(m);
   delete M;
   return SRK_OK;
@@ -408,6 +463,8 @@ int srk_solver_create(srk_ctx* ctx, const srk_matrix* A, int s, int method, cons
                      method == SRK_BL_BICGSTAB || method == SRK_BL_BICGSTAB_RQ;
   if (block && !full_supported(A->m.cplx, cap_for(s)))
     return fail(SRK_EUNSUPPORTED, "srk_solver_create: block methods need s <= 16");
+  if (A->m.bsr && !bsr_supported(A->m.bs, A->m.cplx, s))
+    return fail(SRK_EUNSUPPORTED, "srk_solver_create: BSR operators take s in {4, 8, 12, 16}");
   Solver* sv = make_solver(method);
   if (!sv) return fail(SRK_EINVAL, "srk_solver_create: unknown method");
   sv->c = &ctx->c;

@@ -1,0 +1,177 @@
+// bsr.cu — block-sparse (BSR, 12 x 12 complex blocks) SpMM Q = A P for the
+// lattice operator of config 4 ("convert to ... BSR-12
+// (lattice)"; PAPER.md P:752-778 Ex. 4's 12 dof/site Wilson-type operator, and the
+// read-A-once block product P:66-74).
+//
+// Why blocks: in scalar CSR every one of a row's 97 entries gathers a whole P row
+// (s = 12 complex = 192 B), i.e. ~18.6 KB of L2->SM traffic per row; in BSR a
+// 12 x 12 block multiplies the 12 contiguous rows of P_J once (2.3 KB per block,
+// ~1.7 KB per row), and no column index is stored per scalar entry.
+//
+// One warp per block row I: for every block J of the row the warp stages the
+// block (12 x 12 complex, contiguous) and P_J (12 rows x S complex, contiguous)
+// in its shared-memory double buffer with cp.async (the next block in flight
+// while the current one is multiplied), and multiplies on the FP64 tensor cores:
+// the complex product is the real one
+//   [Q_r Q_i](12 x 2S, interleaved) += [B_r B_i](12 x 24, interleaved) * Bm(24 x 2S)
+// with Bm[2k][c'] = P[k][c'], Bm[2k+1][2c] = -Im P[k][c], Bm[2k+1][2c+1] = Re P[k][c]
+// (formed in the fragment load), M = 12 padded to 16, so 2 x (2S/8) x 6 DMMAs
+// m8n8k4 per block. unit_diag adds the identity block (Q_I += P_I) in the epilogue.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "kernels.cuh"
+
+namespace srk {
+
+namespace {
+
+constexpr int BS = 12;         // block size (rows = cols)
+constexpr int BROW = 28;       // smem row stride of a staged block (doubles): 24 + 4 pad, 2-way banks
+constexpr int BBLK = BS * BROW;  // doubles per staged block
+
+__device__ __forceinline__ void cpa16(double* smem, const double* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+template <int S>
+struct BCfg {
+  static constexpr int NR = 2 * S;            // real columns of P / Q
+  static constexpr int NT = NR / 8;           // N tiles
+  static constexpr int PBLK = BS * NR;        // doubles of a staged P block
+  static constexpr int STAGE = BBLK + PBLK;   // one buffer
+  static constexpr int WARP_SMEM = 2 * STAGE; // double buffer (doubles)
+  static constexpr int WARPS = 8;
+  static constexpr int SMEM = WARPS * WARP_SMEM * 8;
+};
+
+template <int S>
+__global__ void __launch_bounds__(256, 2) bsr12_kernel(BsrArgs a) {
+  if (a.done && *a.done) return;
+  using C = BCfg<S>;
+  extern __shared__ __align__(16) double bsm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* wbuf = bsm + (size_t)warp * C::WARP_SMEM;
+  const double* __restrict__ val = reinterpret_cast<const double*>(a.val);
+  const double* __restrict__ P = reinterpret_cast<const double*>(a.P);
+  double* __restrict__ Q = reinterpret_cast<double*>(a.Q);
+  const long long nb = a.nb;
+  const long long gw = (long long)blockIdx.x * C::WARPS + warp;
+  const long long nw = (long long)gridDim.x * C::WARPS;
+  const int fr = lane >> 2, fk = lane & 3;
+  // B-fragment swizzle of the complex -> real lift (odd k' rows: (-Im, Re) pairs)
+  const int t = fk & 1;
+  const int poff = t ? (fr ^ 1) : fr;
+  const double psgn = (t && !(fr & 1)) ? -1.0 : 1.0;
+
+  // stage block j (values) and the P rows of its block column into buffer b
+  auto stage = [&](int j, int b) {
+    double* bs = wbuf + (size_t)b * C::STAGE;
+    double* ps = bs + BBLK;
+    const double* bv = val + (size_t)j * (BS * BS * 2);
+    const double* pj = P + (size_t)a.bci[j] * BS * C::NR;
+    for (int c = lane; c < BS * 12; c += 32) {  // 12 rows x 12 chunks of 16 B
+      const int r = c / 12, q = c % 12;
+      cpa16(bs + r * BROW + 2 * q, bv + r * 24 + 2 * q);
+    }
+    for (int c = lane; c < C::PBLK / 2; c += 32) cpa16(ps + 2 * c, pj + 2 * c);
+  };
+
+  for (long long I = gw; I < nb; I += nw) {
+    const int jb = __ldg(a.brp + I), je = __ldg(a.brp + I + 1);
+    double acc[2][C::NT][2];
+#pragma unroll
+    for (int m = 0; m < 2; ++m)
+#pragma unroll
+      for (int n = 0; n < C::NT; ++n) acc[m][n][0] = acc[m][n][1] = 0.0;
+    if (je > jb) stage(jb, 0);
+    cp_commit();
+    for (int j = jb; j < je; ++j) {
+      const int b = (j - jb) & 1;
+      if (j + 1 < je) stage(j + 1, b ^ 1);
+      cp_commit();
+      cp_wait<1>();
+      __syncwarp();
+      const double* bs = wbuf + (size_t)b * C::STAGE;
+      const double* ps = bs + BBLK;
+#pragma unroll
+      for (int ks = 0; ks < 6; ++ks) {
+        const int kr = ks * 4 + fk;  // real k' of this lane's fragments
+        const double a0 = bs[fr * BROW + kr];
+        const double a1 = fr < 4 ? bs[(8 + fr) * BROW + kr] : 0.0;
+        const int prow = kr >> 1;
+#pragma unroll
+        for (int n = 0; n < C::NT; ++n) {
+          const double bb = psgn * ps[prow * C::NR + n * 8 + poff];
+          dmma(acc[0][n], a0, bb);
+          dmma(acc[1][n], a1, bb);
+        }
+      }
+      __syncwarp();  // buffer b is restaged at j + 2
+    }
+    // epilogue: Q rows 12 I + row (row < 12), (+ P_I for the unit diagonal)
+#pragma unroll
+    for (int m = 0; m < 2; ++m) {
+      const int row = m * 8 + fr;
+      if (row < BS) {
+        const size_t base = ((size_t)I * BS + row) * C::NR;
+#pragma unroll
+        for (int n = 0; n < C::NT; ++n) {
+          const int col = n * 8 + 2 * fk;
+          double2 v = make_double2(acc[m][n][0], acc[m][n][1]);
+          if (a.unit_diag) {
+            const double2 p = __ldg(reinterpret_cast<const double2*>(P + base + col));
+            v.x += p.x;
+            v.y += p.y;
+          }
+          *reinterpret_cast<double2*>(Q + base + col) = v;
+        }
+      }
+    }
+  }
+}
+
+template <int S>
+int launch_s(const BsrArgs& a, int grid, cudaStream_t st) {
+  using C = BCfg<S>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(bsr12_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    attr = true;
+  }
+  if (grid < 0) {  // resident CTAs per SM
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bsr12_kernel<S>, 256, C::SMEM);
+    return occ;
+  }
+  bsr12_kernel<S><<<grid, 256, C::SMEM, st>>>(a);
+  return (int)cudaGetLastError();
+}
+
+}  // namespace
+
+bool bsr_supported(int bs, bool cplx, int s) { return bs == BS && cplx && (s == 4 || s == 8 || s == 12 || s == 16); }
+
+// grid < 0: returns the resident CTAs per SM
+int launch_bsr(const BsrArgs& a, int s, int grid, cudaStream_t st) {
+  switch (s) {
+    case 4: return launch_s<4>(a, grid, st);
+    case 8: return launch_s<8>(a, grid, st);
+    case 12: return launch_s<12>(a, grid, st);
+    case 16: return launch_s<16>(a, grid, st);
+    default: return (int)cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace srk

@@ -152,6 +152,7 @@ int Eng::halo(bool adj, const void* P, int s) {
 
 int Eng::spmm(bool adj, const void* P, void* Q, int s, std::vector<RQ> reds) {
   if (err) return err;
+  if (A->bsr) return spmm_bsr(adj, P, Q, s, reds);
   if ((err = halo(adj, P, s))) return err;
   const int cap = cap_for(s);
   bool full = false;
@@ -275,6 +276,37 @@ int Eng::upd(int s, std::vector<const void*> in, std::vector<OutSpec> outs, std:
   if (prof) prof->end(c->st);
   if (err) return err;
   return err = finish_reds(*this, reds, poffs, s, grid, a.pstride);
+}
+
+// Block-sparse operator: the BSR product, then the requested reductions over Q as
+// one fused update pass (X = Q; Y the external operand, as in the CSR epilogue).
+int Eng::spmm_bsr(bool adj, const void* P, void* Q, int s, const std::vector<RQ>& reds) {
+  if (adj || !bsr_supported(A->bs, cplx, s)) return err = (int)cudaErrorNotSupported;
+  BsrArgs a{};
+  a.brp = A->brp;
+  a.bci = A->bci;
+  a.val = A->bval;
+  a.P = P;
+  a.Q = Q;
+  a.nb = A->nb;
+  a.unit_diag = A->unit_diag;
+  a.done = done;
+  static int occ = 0;
+  if (occ == 0) occ = std::max(1, launch_bsr(a, s, -1, nullptr));
+  const long long need = (A->nb + 7) / 8;  // one warp per block row, 8 warps per CTA
+  const int grid = (int)std::max<long long>(1, std::min<long long>(need, (long long)c->nsm * occ));
+  nlaunch++;
+  if (prof) {
+    const double esz = 16.0;
+    const double nb = (double)(A->nb + 1) * 4 + (double)A->nnzb * (4 + A->bs * A->bs * esz) + 2.0 * (double)n * s * esz;
+    prof->begin(PT_SPMM, c->st, s, nb);
+  }
+  err = launch_bsr(a, s, grid, c->st);
+  if (prof) prof->end(c->st);
+  if (err || reds.empty()) return err;
+  std::vector<RQ> r2;
+  for (const RQ& q : reds) r2.push_back(RQ{q.mode, 0, -1, q.yext, q.woff});
+  return upd(s, {Q}, {}, r2);
 }
 
 int Eng::gram_full(const void* X, const void* Y, int s, int woff) {

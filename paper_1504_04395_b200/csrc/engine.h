@@ -19,6 +19,8 @@ int launch_spmm(bool cplx, int cap, bool full, const SpmmArgs& a, int grid, int 
 int launch_upd(bool cplx, int cap, bool full, const UpdArgs& a, int grid, int block, size_t smem, cudaStream_t st);
 int launch_fin(const FinArgs& a, cudaStream_t st);
 int launch_gram_mma(const GramArgs& g, int grid, cudaStream_t st);
+int launch_bsr(const BsrArgs& a, int s, int grid, cudaStream_t st);
+bool bsr_supported(int bs, bool cplx, int s);
 
 int gram_mma_chunks(long long n);
 int launch_row_mean(bool cplx, const void* X, void* out, long long n, int s, const int* done, cudaStream_t st);
@@ -52,6 +54,13 @@ struct Mat {
   int* rpH = nullptr;
   int* ciH = nullptr;
   void* valH = nullptr;
+  // Block-sparse form (srk_matrix_create_bsr): nb block rows of bs x bs blocks
+  bool bsr = false;
+  int bs = 0, unit_diag = 0;
+  long long nb = 0, nnzb = 0;
+  int* brp = nullptr;
+  int* bci = nullptr;
+  void* bval = nullptr;
   // Balanced row order (irregular row lengths, e.g. config 5's power law): a copy
   // of the CSR with rows sorted by decreasing length (stable), so that the rows a
   // warp processes together have similar lengths; perm[l] = original row of
@@ -135,6 +144,7 @@ struct Eng {
   int upd(int s, std::vector<const void*> in, std::vector<OutSpec> outs, std::vector<RQ> reds);
   // s x s Gram Y^H X on the FP64 tensor cores (gram_mma.cu), written to ws + woff
   int gram_full(const void* X, const void* Y, int s, int woff);
+  int spmm_bsr(bool adj, const void* P, void* Q, int s, const std::vector<RQ>& reds);
   int grid_for(int cap, bool full, bool is_spmm, size_t smem, int nin) const;
 };
 

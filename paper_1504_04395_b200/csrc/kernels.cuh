@@ -111,6 +111,18 @@ struct GramArgs {
   const int* done;
 };
 
+// Block-sparse (BSR) SpMM, 12 x 12 complex blocks (bsr.cu)
+struct BsrArgs {
+  const int* brp;   // nb + 1 block-row pointers
+  const int* bci;   // block columns (sorted within a block row)
+  const void* val;  // nnzb blocks of 12 x 12 complex, row-major
+  const void* P;
+  void* Q;
+  long long nb;
+  int unit_diag;    // Q_I += P_I (identity diagonal blocks not stored)
+  const int* done;
+};
+
 // Segments for the deterministic second-stage reduction of CTA partials.
 struct FinSeg {
   int poff, len, woff;

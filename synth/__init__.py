@@ -168,19 +168,14 @@ def power_law(n: int, seed: int, a: float = 1.19794, lmax: int = 512, lmin_scale
                dict(kind="power_law", seed=seed, a=a, lmax=lmax))
 
 
-def lattice_4d(L: int, kappa: float = 0.12, seed: int = 3, dof: int = 12, chunk: int = 4096) -> CSR:
-    """Config 4 (SURVEY §8d.1 item 4, reading G23): periodic L^4 lattice, `dof`
-    complex unknowns per site, A = I - kappa*H with H a nearest-neighbour coupling
-    whose 8 blocks per site (order +x, -x, +y, -y, +z, -z, +t, -t; site index
-    x + L y + L^2 z + L^3 t, row = dof*site + a) have entries CN(0, 1/6).
-    Stands in for the paper's Wilson-Dirac Ex. 4 (P:752-778), whose gauge field is
-    not available. Matrix RNG default_rng(seed + 1000), drawn in chunks of `chunk`
-    sites: re = standard_normal((c, 8, dof, dof)), then im of the same shape."""
+def _lattice_blocks(L: int, kappa: float, seed: int, dof: int, chunk: int):
+    """Neighbour table (nsites, 8) and the stored blocks -kappa*H (nsites, 8, dof, dof)
+    of config 4, in the draw order of SURVEY §8d.1 item 4 (shared by the CSR and
+    the BSR forms, so both describe the same matrix)."""
     if L < 3:
         raise ValueError("L >= 3 keeps the 8 neighbours of a site distinct")
     rng = np.random.default_rng(seed + 1000)
     nsites = L ** 4
-    n = nsites * dof
     site = np.arange(nsites, dtype=np.int64)
     co = [(site // L ** d) % L for d in range(4)]
     nbr = np.empty((nsites, 8), dtype=np.int64)
@@ -189,13 +184,28 @@ def lattice_4d(L: int, kappa: float = 0.12, seed: int = 3, dof: int = 12, chunk:
             c2 = list(co)
             c2[d] = (co[d] + step) % L
             nbr[:, 2 * d + k] = c2[0] + L * c2[1] + L ** 2 * c2[2] + L ** 3 * c2[3]
-    blocks = np.empty((nsites, 8, dof, dof), dtype=np.complex128)
+    vals = np.empty((nsites, 8, dof, dof), dtype=np.complex128)
     for start in range(0, nsites, chunk):
         c = min(chunk, nsites - start)
         re = rng.standard_normal((c, 8, dof, dof))
         im = rng.standard_normal((c, 8, dof, dof))
-        blocks[start:start + c] = (re + 1j * im) * np.sqrt(1.0 / 12.0)
-    vals = -kappa * blocks
+        vals[start:start + c] = (re + 1j * im) * np.sqrt(1.0 / 12.0)
+    vals *= -kappa
+    return nbr, vals
+
+
+def lattice_4d(L: int, kappa: float = 0.12, seed: int = 3, dof: int = 12, chunk: int = 4096) -> CSR:
+    """Config 4 (SURVEY §8d.1 item 4, reading G23): periodic L^4 lattice, `dof`
+    complex unknowns per site, A = I - kappa*H with H a nearest-neighbour coupling
+    whose 8 blocks per site (order +x, -x, +y, -y, +z, -z, +t, -t; site index
+    x + L y + L^2 z + L^3 t, row = dof*site + a) have entries CN(0, 1/6).
+    Stands in for the paper's Wilson-Dirac Ex. 4 (P:752-778), whose gauge field is
+    not available. Matrix RNG default_rng(seed + 1000), drawn in chunks of `chunk`
+    sites: re = standard_normal((c, 8, dof, dof)), then im of the same shape."""
+    nbr, vals = _lattice_blocks(L, kappa, seed, dof, chunk)
+    nsites = L ** 4
+    n = nsites * dof
+    site = np.arange(nsites, dtype=np.int64)
     # row (site, a): the 8 neighbour blocks (dof columns each) and the identity's
     # diagonal entry, in ascending column order -> 8*dof + 1 entries per row
     cols_site = np.concatenate([nbr, site[:, None]], axis=1)              # (nsites, 9) block columns
@@ -220,6 +230,20 @@ def lattice_4d(L: int, kappa: float = 0.12, seed: int = 3, dof: int = 12, chunk:
             np.ascontiguousarray(val.reshape(-1)))
     A.meta = dict(kind="lattice_4d", L=L, kappa=kappa, seed=seed, dof=dof)
     return A
+
+
+def lattice_4d_bsr(L: int, kappa: float = 0.12, seed: int = 3, dof: int = 12, chunk: int = 4096):
+    """The same operator as lattice_4d in block-sparse form with an implied unit
+    diagonal: A = I + sum of the 8 stored neighbour blocks per block row.
+    Returns (block_row_ptr int64 (nsites+1), block_col int32 (8 nsites, ascending
+    within a block row), blocks complex128 (8 nsites, dof, dof) row-major)."""
+    nbr, vals = _lattice_blocks(L, kappa, seed, dof, chunk)
+    nsites = L ** 4
+    order = np.argsort(nbr, axis=1, kind="stable")
+    bcol = np.take_along_axis(nbr, order, axis=1).astype(np.int32).reshape(-1)
+    blocks = np.take_along_axis(vals, order[:, :, None, None], axis=1).reshape(nsites * 8, dof, dof)
+    brp = np.arange(0, 8 * nsites + 1, 8, dtype=np.int64)
+    return brp, np.ascontiguousarray(bcol), np.ascontiguousarray(blocks)
 
 
 def input_hash(A: CSR, B: np.ndarray) -> str:

@@ -241,3 +241,68 @@ def test_mid_size_config4_lattice_sampled(srk):
     As = A.to_scipy()
     ref = As[rows] @ B
     assert np.max(np.abs(to_np(Q[torch.from_numpy(rows).cuda()]) - ref)) <= 1e-12 * np.max(np.abs(ref))
+
+
+def _bsr_from_csr(As, bs=12):
+    """Explicit block form (diagonal blocks stored) of a CSR via scipy."""
+    Bs = As.tobsr(blocksize=(bs, bs))
+    Bs.sort_indices()
+    return Bs.indptr.astype(np.int64), Bs.indices.astype(np.int32), np.ascontiguousarray(Bs.data)
+
+
+@pytest.mark.parametrize("s", [4, 8, 12, 16])
+@pytest.mark.parametrize("unit", [True, False])
+def test_bsr_spmm_matches_oracle(srk, s, unit):
+    """BSR-12 SpMM on the FP64 tensor cores (config 4's lattice at 4^4 sites: 256
+    block rows, 8 blocks each, a ragged last CTA) against the oracle's product,
+    with the identity diagonal implied (unit_diag) or stored as explicit blocks."""
+    A = synth.lattice_4d(4)
+    As = A.to_scipy()
+    if unit:
+        brp, bcol, blocks = synth.lattice_4d_bsr(4)
+    else:
+        brp, bcol, blocks = _bsr_from_csr(As)
+    M = srk.Matrix.from_bsr(brp, bcol, blocks, unit_diag=unit)
+    P = synth.random_rhs(A.n, s, 7, True)
+    Q = to_np(srk.spmm_block(M, to_dev(P)))
+    ref = As @ P
+    assert np.max(np.abs(Q - ref)) <= 1e-13 * np.max(np.abs(ref))
+
+
+@pytest.mark.parametrize("mode", ["norm2", "diag", "trace", "sumvec", "full"])
+def test_bsr_spmm_reductions(srk, mode):
+    A = synth.lattice_4d(4)
+    brp, bcol, blocks = synth.lattice_4d_bsr(4)
+    M = srk.Matrix.from_bsr(brp, bcol, blocks, unit_diag=True)
+    P = synth.random_rhs(A.n, 12, 8, True)
+    Y = synth.random_rhs(A.n, 12, 9, True)
+    y = Y[:, 0].copy()
+    Q, g = srk.spmm_block(M, to_dev(P), gram=mode, Y=to_dev(y) if mode == "sumvec" else to_dev(Y))
+    Q, g = to_np(Q), to_np(g)
+    ref = {"norm2": lambda: np.array([OL.fro2(Q)]), "diag": lambda: OL.col_inner(Q, Y),
+           "trace": lambda: np.array([OL.trace_inner(Q, Y)]), "sumvec": lambda: np.array([OL.sum_inner(y, Q)]),
+           "full": lambda: OL.gram(Y, Q)}[mode]()
+    assert rel(g.reshape(ref.shape), ref) < 1e-12
+
+
+def test_bsr_rejects_invalid(srk):
+    brp, bcol, blocks = synth.lattice_4d_bsr(3)
+    bad = bcol.copy()
+    bad[0], bad[1] = bcol[1], bcol[0]  # unsorted block columns
+    with pytest.raises(srk.SrkError):
+        srk.Matrix.from_bsr(brp, bad, blocks, unit_diag=True)
+    with pytest.raises(srk.SrkError):  # 12 x 12 blocks only
+        srk.Matrix.from_bsr(brp, bcol, np.ascontiguousarray(blocks[:, :6, :6]), unit_diag=True)
+
+
+def test_mid_size_config4_bsr_sampled(srk):
+    """Config 4's operator at 16^4 sites in BSR form (65,536 block rows, s = 12):
+    sampled rows of A P against the oracle's (scalar CSR) product."""
+    import torch
+    A, B = synth.make_config(4, m=16)
+    brp, bcol, blocks = synth.lattice_4d_bsr(16)
+    M = srk.Matrix.from_bsr(brp, bcol, blocks, unit_diag=True)
+    Q = srk.spmm_block(M, to_dev(B))
+    rows = np.sort(np.random.default_rng(3).choice(A.n, 4096, replace=False))
+    ref = A.to_scipy()[rows] @ B
+    assert np.max(np.abs(to_np(Q[torch.from_numpy(rows).cuda()]) - ref)) <= 1e-12 * np.max(np.abs(ref))

@@ -180,6 +180,26 @@ def test_lattice_lockstep_and_solve(srk, method):
     test_full_solve(srk, method, "lattice")
 
 
+@pytest.mark.parametrize("method", LATTICE_METHODS)
+def test_lattice_bsr_lockstep_and_solve(srk, method):
+    """Config 4's methods with the operator in BSR-12 form (unit diagonal implied,
+    tensor-core block product): lock-step parity with the oracle (scalar CSR) and
+    the full solve on the 4^4 lattice."""
+    A, B = _problem("lattice")
+    As = A.to_scipy()
+    tol = 1e-8
+    a, _, env = envelope(method, As, B, tol)
+    brp, bcol, blocks = synth.lattice_4d_bsr(4)
+    M = srk.Matrix.from_bsr(brp, bcol, blocks, unit_diag=True)
+    sv, xs = lockstep(srk, M, B, method, min(K, a.iterations), tol)
+    for k in range(min(len(xs), len(a.Xs))):
+        assert rel(xs[k], a.Xs[k]) <= env[k], (method, k + 1)
+    sv.close()
+    X, rep = srk.solve(M, to_dev(B), method, tol=tol, maxit=2000)
+    assert rep.outcome == "converged"
+    assert np.linalg.norm(B - As @ to_np(X)) / np.linalg.norm(B) <= tol
+
+
 @pytest.mark.parametrize("method", ["bl_bicg_rq", "bl_qmr", "bl_bicgstab_rq"])
 def test_config2_block_methods(srk, method):
     """Config 2's methods (block BiCG / QMR / BiCGStab with QR) on its operator at 16^3, s = 8 complex."""

@@ -298,3 +298,19 @@ def test_lattice_bicgstab_converges(method):
     assert r.outcome == "converged"
     Xs = spla.spsolve(As.tocsc(), B)
     assert rel(r.X, Xs) < 1e-8
+
+
+def test_lattice_bsr_form_is_the_same_operator():
+    """synth.lattice_4d_bsr (block-sparse, implied unit diagonal) describes exactly
+    the matrix of synth.lattice_4d (scalar CSR): I + BSR assembled by scipy equals
+    the CSR entry for entry (same RNG draws)."""
+    import scipy.sparse as sp
+    for L in (3, 4):
+        A = synth.lattice_4d(L)
+        brp, bcol, blocks = synth.lattice_4d_bsr(L)
+        assert blocks.shape == (8 * L ** 4, 12, 12) and len(brp) == L ** 4 + 1
+        assert np.all(np.diff(bcol.reshape(-1, 8), axis=1) > 0)  # sorted unique block columns
+        B = sp.bsr_matrix((blocks, bcol, brp), shape=(A.n, A.n)) + sp.identity(A.n, dtype=np.complex128)
+        D = (A.to_scipy() - B.tocsr()).tocsr()
+        D.eliminate_zeros()
+        assert D.nnz == 0
