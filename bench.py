@@ -140,13 +140,13 @@ def cpu_info():
     return model, th
 
 
-def run_reference(args, A, B, s, cfgd):
+def run_reference(args, A, B, s, cfgd, scale: float = 1.0, note: str | None = None):
     # one oracle iteration of config 3 takes ~10 s on the host: bound the sample
     # to <= 3 timed iterations after 1 warm-up so the run ends within minutes
     steps, warm = min(args.steps, 3), min(args.warmup, 1)
     durs, total = oracle_iteration_rate(args.method, A, B, warm + steps)
     timed = durs[warm:warm + steps] if len(durs) >= warm + steps else durs[-steps:]
-    T = float(np.sum(timed))
+    T = float(np.sum(timed)) / scale
     value = s * len(timed) / T
     model, th = cpu_info()
     line = {
@@ -154,8 +154,8 @@ def run_reference(args, A, B, s, cfgd):
         "steps": len(timed), "warmup": warm, "ms_per_step": 1e3 * T / len(timed), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": cfgd,
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": th, "kind": "oracle",
-                         "sample": f"{len(timed)} oracle iterations of {args.method} on the full workload "
-                                   f"(numpy/scipy; scipy.sparse products single-threaded), CPU {model}"},
+                         "sample": (note or f"{len(timed)} oracle iterations of {args.method} on the full workload")
+                                   + f" (numpy/scipy; scipy.sparse products single-threaded), CPU {model}"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -167,7 +167,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--method", default="egl_qmr")
+    ap.add_argument("--method", default=None, help="default: the config's method (cfg3 egl_qmr, cfg4 gl_bicgstab)")
     ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--m", type=int, default=None, help="override the grid size (tests)")
     ap.add_argument("--no-e2e", action="store_true")
@@ -179,19 +179,47 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
 
     import synth
-    A, B = synth.make_config(args.config, m=args.m)
+    if args.method is None:
+        args.method = {1: "egl_bicg", 2: "bl_bicg_rq", 3: "egl_qmr", 4: "gl_bicgstab", 5: "egl_bicg"}[args.config]
+    c = synth.CONFIGS[args.config]
+    bsr = None
+    if args.config == 4:
+        # a0: the lattice operator in BSR-12 form with the unit diagonal implied
+        # (the scalar CSR of 32^4 would be 24.4 GB and gather 18.6 KB per row)
+        L = args.m or c["L"]
+        bsr = synth.lattice_4d_bsr(L, c["kappa"], c["seed"])
+        n = L ** 4 * 12
+        B = synth.random_rhs(n, c["s"], c["seed"], True)
+
+        class A:  # the scalar view (for the config record)
+            pass
+        A.n, A.nnz = n, len(bsr[1]) * 144 + n
+        import hashlib
+        h = hashlib.sha256()
+        for arr in (*bsr, B):
+            h.update(np.ascontiguousarray(arr).view(np.uint8).data)
+        ihash = h.hexdigest()[:16]
+    else:
+        A, B = synth.make_config(args.config, m=args.m)
+        ihash = synth.input_hash(A, B)
     s = B.shape[1]
     esz = 16 if np.iscomplexobj(B) else 8
-    c = synth.CONFIGS[args.config]
-    cfgd = {"workload": f"{c['name']} ({'m=%d' % (args.m or c.get('m', 0))}) {args.method}",
+    cfgd = {"workload": f"{c['name']} ({'m=%d' % (args.m or c.get('m', c.get('L', 0)))}) {args.method}",
             "method": args.method, "n": A.n, "nnz": A.nnz, "s": s, "dtype": c["dtype"],
+            "operator": "BSR-12, unit diagonal implied" if bsr is not None else "CSR",
             "parallelism": "replicas" if world > 1 else "single",
             "l2": "no flush: every n x s block (%.2f GB) exceeds the 126 MB L2" % (A.n * s * esz / 1e9),
-            "inputs_hash": synth.input_hash(A, B)}
+            "inputs_hash": ihash}
 
     if args.impl == "reference":
         if rank == 0:
-            run_reference(args, A, B, s, cfgd)
+            if bsr is not None:  # bounded sample: the oracle on the 16^4 lattice, scaled by the row ratio
+                As, Bs = synth.make_config(4, m=16)
+                run_reference(args, As, Bs, s, cfgd, scale=As.n / A.n,
+                              note="oracle on config 4's operator at 16^4 sites (1/16 of the rows), "
+                                   "per-iteration time scaled x16")
+            else:
+                run_reference(args, A, B, s, cfgd)
         return
 
     import torch
@@ -211,6 +239,9 @@ def main():
         o0, o1 = int(off[rank]), int(off[rank + 1])
         B = np.ascontiguousarray(B[o0:o1])
         cfgd["parallelism"] = f"row-partition x{world} (halo exchange + NCCL allreduce)"
+    elif bsr is not None:
+        M = srk.Matrix.from_bsr(*bsr, unit_diag=True)
+        del bsr
     else:
         M = srk.Matrix.from_csr(A, need_adjoint=srk.NEEDS_ADJOINT[args.method])
     n_local = B.shape[0]
@@ -321,11 +352,19 @@ def main():
     # ---- CPU baseline: the oracle on one config-3 iteration (rank 0, N = 1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        durs, total = oracle_iteration_rate(args.method, A, B, 2)
         model, th = cpu_info()
-        cpu = {"value": s / float(durs[-1]), "unit": UNIT, "cores": th, "kind": "oracle",
-               "sample": f"iteration 2 of {args.method} on the full config-{args.config} workload "
-                         f"({durs[-1]:.1f} s; oracle call {total:.1f} s incl. setup), CPU {model}"}
+        if args.config == 4:  # bounded sample: the 16^4 lattice (1/16 of the rows), time scaled x16
+            As, Bs = synth.make_config(4, m=16)
+            durs, total = oracle_iteration_rate(args.method, As, Bs, 2)
+            t_it = float(durs[-1]) * A.n / As.n
+            cpu = {"value": s / t_it, "unit": UNIT, "cores": th, "kind": "oracle",
+                   "sample": f"iteration 2 of {args.method} on config 4's operator at 16^4 sites "
+                             f"({durs[-1]:.1f} s), scaled by the row ratio x{A.n // As.n}, CPU {model}"}
+        else:
+            durs, total = oracle_iteration_rate(args.method, A, B, 2)
+            cpu = {"value": s / float(durs[-1]), "unit": UNIT, "cores": th, "kind": "oracle",
+                   "sample": f"iteration 2 of {args.method} on the full config-{args.config} workload "
+                             f"({durs[-1]:.1f} s; oracle call {total:.1f} s incl. setup), CPU {model}"}
 
     if rank == 0:
         line = {

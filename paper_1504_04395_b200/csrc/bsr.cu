@@ -57,7 +57,7 @@ struct BCfg {
 };
 
 template <int S>
-__global__ void __launch_bounds__(256, 2) bsr12_kernel(BsrArgs a) {
+__global__ void __launch_bounds__(256, S >= 16 ? 1 : 2) bsr12_kernel(BsrArgs a) {
   if (a.done && *a.done) return;
   using C = BCfg<S>;
   extern __shared__ __align__(16) double bsm[];
@@ -73,7 +73,8 @@ __global__ void __launch_bounds__(256, 2) bsr12_kernel(BsrArgs a) {
   // B-fragment swizzle of the complex -> real lift (odd k' rows: (-Im, Re) pairs)
   const int t = fk & 1;
   const int poff = t ? (fr ^ 1) : fr;
-  const double psgn = (t && !(fr & 1)) ? -1.0 : 1.0;
+  // -Im P: flip the sign bit on the integer side (keeps the FP64 pipe for DMMAs)
+  const unsigned long long psgn = (t && !(fr & 1)) ? 0x8000000000000000ULL : 0ULL;
 
   // stage block j (values) and the P rows of its block column into buffer b
   auto stage = [&](int j, int b) {
@@ -88,6 +89,23 @@ __global__ void __launch_bounds__(256, 2) bsr12_kernel(BsrArgs a) {
     for (int c = lane; c < C::PBLK / 2; c += 32) cpa16(ps + 2 * c, pj + 2 * c);
   };
 
+  // epilogue reductions: per lane, over the Q entries it owns (rows fr and 8 + fr,
+  // complex columns n * 4 + fk): scalar modes in rs[r], per-column modes in rc[r][n]
+  const int nred = a.nred;
+  int rmode[2];
+  const double* ry[2];
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    rmode[r] = r < nred ? a.red[r].mode : RED_NONE;
+    ry[r] = r < nred ? reinterpret_cast<const double*>(a.red[r].yext) : nullptr;
+  }
+  double2 rs[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
+  double2 rc[2][C::NT];
+#pragma unroll
+  for (int r = 0; r < 2; ++r)
+#pragma unroll
+    for (int n = 0; n < C::NT; ++n) rc[r][n] = make_double2(0.0, 0.0);
+
   for (long long I = gw; I < nb; I += nw) {
     const int jb = __ldg(a.brp + I), je = __ldg(a.brp + I + 1);
     double acc[2][C::NT][2];
@@ -97,6 +115,29 @@ __global__ void __launch_bounds__(256, 2) bsr12_kernel(BsrArgs a) {
       for (int n = 0; n < C::NT; ++n) acc[m][n][0] = acc[m][n][1] = 0.0;
     if (je > jb) stage(jb, 0);
     cp_commit();
+    // epilogue operands requested now, consumed after the row's last block: the
+    // unit-diagonal P_I entries and reduction 0's Y entries at this lane's places
+    double2 pI[2][C::NT], y0[2][C::NT];
+#pragma unroll
+    for (int m = 0; m < 2; ++m) {
+      const int row = m * 8 + fr;
+      const size_t base = ((size_t)I * BS + (row < BS ? row : 0)) * C::NR;
+#pragma unroll
+      for (int n = 0; n < C::NT; ++n) {
+        const int col = n * 8 + 2 * fk;
+        pI[m][n] = make_double2(0.0, 0.0);
+        y0[m][n] = make_double2(0.0, 0.0);
+        if (row < BS) {
+          if (a.unit_diag) pI[m][n] = __ldg(reinterpret_cast<const double2*>(P + base + col));
+          const int md = rmode[0];
+          if (md == RED_SUMVEC) {
+            if (n == 0) y0[m][0] = __ldg(reinterpret_cast<const double2*>(ry[0]) + (size_t)I * BS + row);
+          } else if (md == RED_DIAG || md == RED_TRACE) {
+            y0[m][n] = __ldg(reinterpret_cast<const double2*>(ry[0] + base + col));
+          }
+        }
+      }
+    }
     for (int j = jb; j < je; ++j) {
       const int b = (j - jb) & 1;
       if (j + 1 < je) stage(j + 1, b ^ 1);
@@ -113,7 +154,7 @@ __global__ void __launch_bounds__(256, 2) bsr12_kernel(BsrArgs a) {
         const int prow = kr >> 1;
 #pragma unroll
         for (int n = 0; n < C::NT; ++n) {
-          const double bb = psgn * ps[prow * C::NR + n * 8 + poff];
+          const double bb = __longlong_as_double(__double_as_longlong(ps[prow * C::NR + n * 8 + poff]) ^ (long long)psgn);
           dmma(acc[0][n], a0, bb);
           dmma(acc[1][n], a1, bb);
         }
@@ -131,14 +172,86 @@ __global__ void __launch_bounds__(256, 2) bsr12_kernel(BsrArgs a) {
           const int col = n * 8 + 2 * fk;
           double2 v = make_double2(acc[m][n][0], acc[m][n][1]);
           if (a.unit_diag) {
-            const double2 p = __ldg(reinterpret_cast<const double2*>(P + base + col));
-            v.x += p.x;
-            v.y += p.y;
+            v.x += pI[m][n].x;
+            v.y += pI[m][n].y;
           }
           *reinterpret_cast<double2*>(Q + base + col) = v;
+#pragma unroll
+          for (int r = 0; r < 2; ++r) {
+            const int md = rmode[r];
+            if (md == RED_NONE) continue;
+            if (md == RED_NORM2 || md == RED_COLNORM2) {
+              const double q2 = v.x * v.x + v.y * v.y;
+              if (md == RED_NORM2) rs[r].x += q2;
+              else rc[r][n].x += q2;
+            } else {
+              // conj(y) * q with y the Y entry at the same place (SUMVEC: the row's vector entry)
+              const double2 y = r == 0 ? (md == RED_SUMVEC ? y0[m][0] : y0[m][n])
+                                       : (md == RED_SUMVEC ? __ldg(reinterpret_cast<const double2*>(ry[r]) + (size_t)I * BS + row)
+                                                           : __ldg(reinterpret_cast<const double2*>(ry[r] + base + col)));
+              const double2 pr = make_double2(y.x * v.x + y.y * v.y, y.x * v.y - y.y * v.x);
+              if (md == RED_DIAG) {
+                rc[r][n].x += pr.x;
+                rc[r][n].y += pr.y;
+              } else {
+                rs[r].x += pr.x;
+                rs[r].y += pr.y;
+              }
+            }
+          }
         }
       }
     }
+  }
+  if (nred == 0) return;
+  // CTA partials in the layout of red_len: fixed-order warp butterflies, then the
+  // warps summed in index order (deterministic)
+  __syncthreads();  // every warp is done with its staging buffers
+  double* red_sm = bsm;  // [warp][len] doubles
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    if (r >= nred) break;
+    const int md = rmode[r];
+    const int len = red_len(md, S, true);
+    double* w = red_sm + (size_t)warp * len;
+    if (md == RED_DIAG || md == RED_COLNORM2) {
+#pragma unroll
+      for (int n = 0; n < C::NT; ++n) {
+        double2 v = rc[r][n];
+#pragma unroll
+        for (int m = 4; m < 32; m <<= 1) {  // over fr: lanes with equal fk hold the same columns
+          v.x += __shfl_xor_sync(0xffffffffu, v.x, m);
+          v.y += __shfl_xor_sync(0xffffffffu, v.y, m);
+        }
+        if (fr == 0) {
+          const int c = n * 4 + fk;
+          if (md == RED_DIAG) {
+            w[2 * c] = v.x;
+            w[2 * c + 1] = v.y;
+          } else {
+            w[c] = v.x;
+          }
+        }
+      }
+    } else {
+      double2 v = rs[r];
+#pragma unroll
+      for (int m = 1; m < 32; m <<= 1) {
+        v.x += __shfl_xor_sync(0xffffffffu, v.x, m);
+        v.y += __shfl_xor_sync(0xffffffffu, v.y, m);
+      }
+      if (lane == 0) {
+        w[0] = v.x;
+        if (md != RED_NORM2) w[1] = v.y;
+      }
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < len; j += blockDim.x) {
+      double acc = 0.0;
+      for (int q = 0; q < C::WARPS; ++q) acc += red_sm[q * len + j];
+      a.partials[(size_t)blockIdx.x * a.pstride + a.red[r].poff + j] = acc;
+    }
+    __syncthreads();
   }
 }
 

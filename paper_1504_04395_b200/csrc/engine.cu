@@ -209,6 +209,15 @@ int Eng::spmm(bool adj, const void* P, void* Q, int s, std::vector<RQ> reds) {
 
 int Eng::upd(int s, std::vector<const void*> in, std::vector<OutSpec> outs, std::vector<RQ> reds) {
   if (err) return err;
+  // an external n x s reduction operand becomes one more input, so its rows are
+  // requested together with the other inputs instead of after the outputs
+  for (RQ& r : reds)
+    if (r.y < 0 && r.yext && r.mode != RED_SUMVEC && r.mode != RED_NORM2 && r.mode != RED_COLNORM2 &&
+        in.size() < (size_t)MAX_IN) {
+      in.push_back(r.yext);
+      r.y = (int)in.size() - 1;
+      r.yext = nullptr;
+    }
   const int cap = cap_for(s);
   bool full = false;  // s x s Gram or s x s coefficient: the block-method kernel instance
   for (auto& r : reds) full |= (r.mode == RED_FULL);
@@ -295,17 +304,42 @@ int Eng::spmm_bsr(bool adj, const void* P, void* Q, int s, const std::vector<RQ>
   if (occ == 0) occ = std::max(1, launch_bsr(a, s, -1, nullptr));
   const long long need = (A->nb + 7) / 8;  // one warp per block row, 8 warps per CTA
   const int grid = (int)std::max<long long>(1, std::min<long long>(need, (long long)c->nsm * occ));
+  // the epilogue fuses every reduction except the s x s Gram (a separate pass below)
+  std::vector<RQ> fused, rest;
+  for (const RQ& q : reds) (q.mode == RED_FULL ? rest : fused).push_back(q);
+  if (fused.size() > 2) {
+    rest.insert(rest.end(), fused.begin() + 2, fused.end());
+    fused.resize(2);
+  }
+  std::vector<int> poffs;
+  int pstride = 0;
+  a.nred = (int)fused.size();
+  for (size_t i = 0; i < fused.size(); ++i) {
+    fill_red(a.red[i], fused[i], pstride);
+    poffs.push_back(pstride);
+    pstride += red_len(fused[i].mode, s, true);
+  }
+  a.pstride = std::max(pstride, 1);
+  if (!fused.empty()) {
+    if ((err = c->ensure_partials((size_t)grid * a.pstride))) return err;
+    a.partials = c->partials;
+  }
   nlaunch++;
   if (prof) {
     const double esz = 16.0;
-    const double nb = (double)(A->nb + 1) * 4 + (double)A->nnzb * (4 + A->bs * A->bs * esz) + 2.0 * (double)n * s * esz;
+    double nb = (double)(A->nb + 1) * 4 + (double)A->nnzb * (4 + A->bs * A->bs * esz) + 2.0 * (double)n * s * esz;
+    for (const RQ& q : fused)
+      if (q.yext && q.mode != RED_NORM2 && q.mode != RED_COLNORM2)
+        nb += (double)n * (q.mode == RED_SUMVEC ? 1 : s) * esz;
     prof->begin(PT_SPMM, c->st, s, nb);
   }
   err = launch_bsr(a, s, grid, c->st);
   if (prof) prof->end(c->st);
-  if (err || reds.empty()) return err;
+  if (err) return err;
+  if (!fused.empty() && (err = finish_reds(*this, fused, poffs, s, grid, a.pstride))) return err;
+  if (rest.empty()) return 0;
   std::vector<RQ> r2;
-  for (const RQ& q : reds) r2.push_back(RQ{q.mode, 0, -1, q.yext, q.woff});
+  for (const RQ& q : rest) r2.push_back(RQ{q.mode, 0, -1, q.yext, q.woff});
   return upd(s, {Q}, {}, r2);
 }
 

@@ -121,6 +121,11 @@ struct BsrArgs {
   long long nb;
   int unit_diag;    // Q_I += P_I (identity diagonal blocks not stored)
   const int* done;
+  // fused epilogue reductions over X = Q (NORM2, COLNORM2, DIAG, TRACE, SUMVEC)
+  Red red[2];
+  int nred;
+  double* partials;  // [gridDim.x][pstride]
+  int pstride;
 };
 
 // Segments for the deterministic second-stage reduction of CTA partials.

@@ -236,14 +236,34 @@ def lattice_4d_bsr(L: int, kappa: float = 0.12, seed: int = 3, dof: int = 12, ch
     """The same operator as lattice_4d in block-sparse form with an implied unit
     diagonal: A = I + sum of the 8 stored neighbour blocks per block row.
     Returns (block_row_ptr int64 (nsites+1), block_col int32 (8 nsites, ascending
-    within a block row), blocks complex128 (8 nsites, dof, dof) row-major)."""
-    nbr, vals = _lattice_blocks(L, kappa, seed, dof, chunk)
+    within a block row), blocks complex128 (8 nsites, dof, dof) row-major).
+    Generated chunk by chunk (same draws and arithmetic as _lattice_blocks), so the
+    only full-size array is the output (19.3 GB at L = 32)."""
+    if L < 3:
+        raise ValueError("L >= 3 keeps the 8 neighbours of a site distinct")
+    rng = np.random.default_rng(seed + 1000)
     nsites = L ** 4
-    order = np.argsort(nbr, axis=1, kind="stable")
-    bcol = np.take_along_axis(nbr, order, axis=1).astype(np.int32).reshape(-1)
-    blocks = np.take_along_axis(vals, order[:, :, None, None], axis=1).reshape(nsites * 8, dof, dof)
+    blocks = np.empty((nsites * 8, dof, dof), dtype=np.complex128)
+    bcol = np.empty(nsites * 8, dtype=np.int32)
+    for start in range(0, nsites, chunk):
+        c = min(chunk, nsites - start)
+        site = np.arange(start, start + c, dtype=np.int64)
+        co = [(site // L ** d) % L for d in range(4)]
+        nbr = np.empty((c, 8), dtype=np.int64)
+        for d in range(4):
+            for k, step in enumerate((+1, -1)):
+                c2 = list(co)
+                c2[d] = (co[d] + step) % L
+                nbr[:, 2 * d + k] = c2[0] + L * c2[1] + L ** 2 * c2[2] + L ** 3 * c2[3]
+        re = rng.standard_normal((c, 8, dof, dof))
+        im = rng.standard_normal((c, 8, dof, dof))
+        vals = (re + 1j * im) * np.sqrt(1.0 / 12.0)
+        vals *= -kappa
+        order = np.argsort(nbr, axis=1, kind="stable")
+        bcol[8 * start:8 * (start + c)] = np.take_along_axis(nbr, order, axis=1).reshape(-1)
+        blocks[8 * start:8 * (start + c)] = np.take_along_axis(vals, order[:, :, None, None], axis=1).reshape(c * 8, dof, dof)
     brp = np.arange(0, 8 * nsites + 1, 8, dtype=np.int64)
-    return brp, np.ascontiguousarray(bcol), np.ascontiguousarray(blocks)
+    return brp, bcol, blocks
 
 
 def input_hash(A: CSR, B: np.ndarray) -> str:
