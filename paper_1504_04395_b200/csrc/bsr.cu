@@ -31,9 +31,22 @@ constexpr int BS = 12;         // block size (rows = cols)
 constexpr int BROW = 28;       // smem row stride of a staged block (doubles): 24 + 4 pad, 2-way banks
 constexpr int BBLK = BS * BROW;  // doubles per staged block
 
-__device__ __forceinline__ void cpa16(double* smem, const double* gmem) {
+// 16-byte async copy with an L2 eviction policy: the blocks of A stream through
+// once (evict_first) while the rows of P are re-read by the neighbouring block rows
+// (evict_last), so A does not push P out of L2
+__device__ __forceinline__ void cpa16(double* smem, const double* gmem, unsigned long long pol) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem), "l"(pol));
+}
+__device__ __forceinline__ unsigned long long policy_evict_first() {
+  unsigned long long p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ unsigned long long policy_evict_last() {
+  unsigned long long p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
 }
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
@@ -76,6 +89,7 @@ __global__ void __launch_bounds__(256, S >= 16 ? 1 : 2) bsr12_kernel(BsrArgs a) 
   // -Im P: flip the sign bit on the integer side (keeps the FP64 pipe for DMMAs)
   const unsigned long long psgn = (t && !(fr & 1)) ? 0x8000000000000000ULL : 0ULL;
 
+  const unsigned long long pol_a = policy_evict_first(), pol_p = policy_evict_last();
   // stage block j (values) and the P rows of its block column into buffer b
   auto stage = [&](int j, int b) {
     double* bs = wbuf + (size_t)b * C::STAGE;
@@ -84,9 +98,9 @@ __global__ void __launch_bounds__(256, S >= 16 ? 1 : 2) bsr12_kernel(BsrArgs a) 
     const double* pj = P + (size_t)a.bci[j] * BS * C::NR;
     for (int c = lane; c < BS * 12; c += 32) {  // 12 rows x 12 chunks of 16 B
       const int r = c / 12, q = c % 12;
-      cpa16(bs + r * BROW + 2 * q, bv + r * 24 + 2 * q);
+      cpa16(bs + r * BROW + 2 * q, bv + r * 24 + 2 * q, pol_a);
     }
-    for (int c = lane; c < C::PBLK / 2; c += 32) cpa16(ps + 2 * c, pj + 2 * c);
+    for (int c = lane; c < C::PBLK / 2; c += 32) cpa16(ps + 2 * c, pj + 2 * c, pol_p);
   };
 
   // epilogue reductions: per lane, over the Q entries it owns (rows fr and 8 + fr,

@@ -106,6 +106,18 @@ int comm_allreduce_sum(Comm* C, double* buf, size_t count, cudaStream_t st) {
   return N->allReduce(buf, buf, count, ncclFloat64, ncclSum, (ncclComm_t)C->nccl, st) == ncclSuccess ? 0 : -5;
 }
 
+int comm_allreduce_sum_many(Comm* C, double* const* bufs, const size_t* counts, int nbuf, cudaStream_t st) {
+  if (!C || C->nranks == 1 || nbuf == 0) return 0;
+  if (nbuf == 1) return comm_allreduce_sum(C, bufs[0], counts[0], st);
+  Nccl* N = nccl();
+  if (N->groupStart() != ncclSuccess) return -5;
+  int bad = 0;
+  for (int i = 0; i < nbuf; ++i)
+    if (counts[i] && N->allReduce(bufs[i], bufs[i], counts[i], ncclFloat64, ncclSum, (ncclComm_t)C->nccl, st) != ncclSuccess)
+      bad = 1;
+  return (N->groupEnd() == ncclSuccess && !bad) ? 0 : -5;
+}
+
 int comm_halo(Comm* C, const double* sendbuf, const int64_t* send_off, double* recvbuf, const int64_t* recv_off,
               size_t doubles_per_row, cudaStream_t st) {
   if (!C || C->nranks == 1) return 0;

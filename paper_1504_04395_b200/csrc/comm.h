@@ -16,6 +16,8 @@ Comm* comm_create(const void* id128, int nranks, int rank);
 void comm_destroy(Comm* c);
 // in-place FP64 sum over ranks (ring/tree: the same bitwise result on every rank)
 int comm_allreduce_sum(Comm* c, double* buf, size_t count, cudaStream_t st);
+// several in-place sums as one grouped NCCL call (one latency per reduction point)
+int comm_allreduce_sum_many(Comm* c, double* const* bufs, const size_t* counts, int nbuf, cudaStream_t st);
 // grouped point-to-point halo exchange: rows [send_off[p], send_off[p+1]) of sendbuf go
 // to rank p, rows [recv_off[p], recv_off[p+1]) of recvbuf come from rank p
 int comm_halo(Comm* c, const double* sendbuf, const int64_t* send_off, double* recvbuf, const int64_t* recv_off,

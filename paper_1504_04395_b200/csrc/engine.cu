@@ -122,8 +122,13 @@ static int finish_reds(Eng& e, const std::vector<RQ>& reds, const std::vector<in
   // multi-GPU: the per-rank sums become global sums (same bits on every rank)
   if (e.c->comm && e.c->comm->nranks > 1) {
     if (e.prof) e.prof->begin(PT_OTHER, e.c->st);
-    for (size_t i = 0; i < reds.size(); ++i)
-      if (comm_allreduce_sum(e.c->comm, e.ws + reds[i].woff, red_len(reds[i].mode, s, e.cplx), e.c->st)) r = -5;
+    std::vector<double*> bufs;
+    std::vector<size_t> counts;
+    for (size_t i = 0; i < reds.size(); ++i) {
+      bufs.push_back(e.ws + reds[i].woff);
+      counts.push_back((size_t)red_len(reds[i].mode, s, e.cplx));
+    }
+    if (comm_allreduce_sum_many(e.c->comm, bufs.data(), counts.data(), (int)bufs.size(), e.c->st)) r = -5;
     if (e.prof) e.prof->end(e.c->st);
   }
   return r;

@@ -165,7 +165,9 @@ int Solver::iterate(int k) {
       while (host_iter < target && launched < poll) {
         // after the first iteration every iteration launches the same kernels with the
         // same arguments: replay a captured CUDA graph of `poll` iterations
-        if (o.use_graph && !prof.on && host_iter > 0 && launched == 0 && target - host_iter >= poll && poll > 1) {
+        // (not across ranks: the NCCL calls stay eager, capture is validated on one GPU only)
+        const bool multi = c->comm && c->comm->nranks > 1;
+        if (o.use_graph && !multi && !prof.on && host_iter > 0 && launched == 0 && target - host_iter >= poll && poll > 1) {
           if (capture(poll)) return SRK_ECUDA;
           if (cudaGraphLaunch(gexec, c->st) != cudaSuccess) return SRK_ECUDA;
           e.nlaunch += graph_launches;
