@@ -208,7 +208,10 @@ def main():
             "method": args.method, "n": A.n, "nnz": A.nnz, "s": s, "dtype": c["dtype"],
             "operator": "BSR-12, unit diagonal implied" if bsr is not None else "CSR",
             "parallelism": "replicas" if world > 1 else "single",
-            "l2": "no flush: every n x s block (%.2f GB) exceeds the 126 MB L2" % (A.n * s * esz / 1e9),
+            "l2": ("no flush: every n x s block (%.2f GB) exceeds the 126 MB L2" % (A.n * s * esz / 1e9)
+                   if A.n * s * esz > 126e6 else
+                   "no flush: the whole problem (%.1f KB per block) is L2-resident by design (latency-bound)"
+                   % (A.n * s * esz / 1e3)),
             "inputs_hash": ihash}
 
     if args.impl == "reference":
@@ -255,10 +258,18 @@ def main():
             torch.cuda.synchronize()
 
     # ---- device-resident timed region
-    sv = srk.Solver(M, s, args.method, tol=1e-300, maxit=W + K + 1, poll_every=W + K + 1,
+    # config 1 is latency-bound: its step runs as the product does,
+    # W-iteration CUDA graphs replayed between polls (captured in the warm-up), and
+    # without per-launch events (which would serialise it); no roofline fraction
+    latency = args.config == 1
+    poll = W if latency else W + K + 1
+    warm = 2 * W if latency else W
+    sv = srk.Solver(M, s, args.method, tol=1e-300, maxit=warm + K + 1, poll_every=poll,
                     check_true_residual=False)
     sv.start(Bd)
     sv.iterate(W)
+    if latency:
+        sv.iterate(W)  # captures the graph
     l0 = sv.report().kernel_launches
     uuid = None
     try:
@@ -270,7 +281,7 @@ def main():
     barrier()
     clk.start()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    sv.profile(True)
+    sv.profile(not latency)
     e0.record()
     st = sv.iterate(K)
     e1.record()
@@ -280,7 +291,7 @@ def main():
     recs = sv.profile_launches()
     rep = sv.report()
     launches = rep.kernel_launches - l0
-    assert st == 0 and rep.iterations == W + K, (st, rep)
+    assert st == 0 and rep.iterations == warm + K, (st, rep)
     if world > 1:
         t = torch.tensor([ms], device=dev, dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
@@ -312,18 +323,23 @@ def main():
                      "algorithmic_bytes_per_launch": f["bytes_per_launch"], "achieved_gbs": ach,
                      "frac": (ach / peak) if ach else None, "share_of_step": f["ms_total"] / ms})
     kern.sort(key=lambda k: -k["share_of_step"])
-    dom = next(k for k in kern if k["achieved_gbs"])
+    dom = next((k for k in kern if k["achieved_gbs"]), None)
     spm = next((k for k in kern if k["kernel"].startswith("spmm s=")), None)
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
         tj = json.load(open(tp))
         traffic = tj.get(f"cfg{args.config}_{args.method}_" + ("spmm" if dom is spm else "dominant"))
-    roof = {"bound": "hbm", "achieved": dom["achieved_gbs"], "peak": peak, "unit": "GB/s",
-            "frac": dom["achieved_gbs"] / peak, "traffic": traffic, "kernel": dom["kernel"],
-            "algorithmic_bytes_per_launch": dom["algorithmic_bytes_per_launch"],
-            "avg_launch_ms": dom["avg_launch_ms"], "launches": dom["launches"],
-            "share_of_step": dom["share_of_step"], "peak_source": peak_src}
+    if dom is None:  # latency-bound config 1: the whole problem sits in L2
+        roof = {"bound": "latency", "achieved": None, "peak": None, "unit": "GB/s", "frac": None, "traffic": None,
+                "note": "config 1 (n = 1024) is latency-bound (SURVEY §8(d).2): RHS·it/s only; "
+                        "step = W-iteration CUDA graph replays"}
+    else:
+        roof = {"bound": "hbm", "achieved": dom["achieved_gbs"], "peak": peak, "unit": "GB/s",
+                "frac": dom["achieved_gbs"] / peak, "traffic": traffic, "kernel": dom["kernel"],
+                "algorithmic_bytes_per_launch": dom["algorithmic_bytes_per_launch"],
+                "avg_launch_ms": dom["avg_launch_ms"], "launches": dom["launches"],
+                "share_of_step": dom["share_of_step"], "peak_source": peak_src}
     it_bytes = sum(nb for _, _, _, nb in recs) / K
     breakdown = {}
     for tag, _, t_ms, _ in recs:
@@ -373,9 +389,9 @@ def main():
             "dtype": "f64" if esz == 8 else "c128", "data": "synthetic", "config": cfgd,
             "roofline": roof, "roofline_spmm": spm, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": int(launches), "clocks": clocks,
-            "iteration": {"algorithmic_bytes": it_bytes,
-                          "achieved_gbs": it_bytes / (ms / K / 1e3) / 1e9,
-                          "frac_of_peak": it_bytes / (ms / K / 1e3) / 1e9 / peak,
+            "iteration": {"algorithmic_bytes": it_bytes or None,
+                          "achieved_gbs": (it_bytes / (ms / K / 1e3) / 1e9) if it_bytes else None,
+                          "frac_of_peak": (it_bytes / (ms / K / 1e3) / 1e9 / peak) if it_bytes else None,
                           "kernels": kern, "by_tag": breakdown},
         }
         print(json.dumps(line), flush=True)

@@ -659,6 +659,207 @@ __global__ void __launch_bounds__(256, FC ? 1 : MINB) upd_kernel(UpdArgs a) {
   if (nred > 2) red_dispatch_flush<T, S, false>(rmode[2], acc2, a.partials, a.pstride, a.red[2].poff, s, rsm);
 }
 
+// ============================================================================
+// SpMM for narrow blocks (s * esz <= 32 bytes: the A^H vector product of the
+// economic variants, config 5's small-s sweep): a TEAM of lanes per row, each
+// lane taking every TEAM-th nonzero (coalesced (col, val) loads, TEAM gathers of
+// one short P row in flight per row), R rows per team, the partial rows summed by
+// a fixed xor butterfly over the team. The team leader stores the row and
+// accumulates the fused reductions over its W values.
+// ============================================================================
+template <typename T, int W>
+struct TeamRed {  // one reduction's accumulators in a team leader
+  T v[W];         // DIAG / COLNORM2 (Re) per column; [0]: NORM2 (Re), TRACE, SUMVEC
+  T f[W][W];      // FULL: f[k][c] += conj(y_k) q_c
+};
+
+template <typename T, int W, int TEAM, int R, bool EX>
+__global__ void __launch_bounds__(256, W * sizeof(T) >= 32 ? 2 : 4) spmv_team_kernel(SpmmArgs a) {
+  if (a.done && *a.done) return;
+  extern __shared__ double smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int t = lane % TEAM, team = lane / TEAM;
+  constexpr int TPW = 32 / TEAM;  // teams per warp
+  const long long n = a.n;
+  const int s = a.s;
+  const int* __restrict__ rp = a.row_ptr;
+  const int* __restrict__ ci = a.col_idx;
+  const T* __restrict__ val = reinterpret_cast<const T*>(a.val);
+  const T* __restrict__ P = reinterpret_cast<const T*>(a.P);
+  T* __restrict__ Q = reinterpret_cast<T*>(a.Q);
+  const int* __restrict__ perm = a.perm;
+  const int nred = a.nred;
+  int rmode[2];
+  const T* ry[2];
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    rmode[r] = r < nred ? a.red[r].mode : RED_NONE;
+    ry[r] = r < nred ? reinterpret_cast<const T*>(a.red[r].yext) : nullptr;
+  }
+  TeamRed<T, W> acc[2];
+#pragma unroll
+  for (int r = 0; r < 2; ++r)
+#pragma unroll
+    for (int c = 0; c < W; ++c) {
+      acc[r].v[c] = Ar<T>::zero();
+#pragma unroll
+      for (int k = 0; k < W; ++k) acc[r].f[k][c] = Ar<T>::zero();
+    }
+  auto load_row = [&](long long c, T (&p)[W]) {
+    const T* src = P + (size_t)c * (EX ? W : s);
+    if constexpr (EX && W * sizeof(T) % 16 == 0) {
+#pragma unroll
+      for (int q = 0; q < W * (int)sizeof(T) / 16; ++q) {
+        const double2 d = __ldg(reinterpret_cast<const double2*>(src) + q);
+        if constexpr (sizeof(T) == 16) {
+          p[q] = *reinterpret_cast<const T*>(&d);
+        } else {
+          reinterpret_cast<double*>(p)[2 * q] = d.x;
+          reinterpret_cast<double*>(p)[2 * q + 1] = d.y;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < W; ++e) p[e] = (EX || e < s) ? __ldg(src + e) : Ar<T>::zero();
+    }
+  };
+  const long long nwarp = (long long)gridDim.x * (blockDim.x >> 5);
+  const long long rows_per_it = (long long)TPW * R;
+  for (long long wi = (long long)blockIdx.x * (blockDim.x >> 5) + warp; wi * rows_per_it < n; wi += nwarp) {
+    const long long r0 = wi * rows_per_it + (long long)team * R;
+    int beg[R], len[R];
+    long long orow[R];
+    int maxlen = 0;
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const long long r = r0 + i;
+      const bool in = r < n;
+      beg[i] = in ? __ldg(rp + r) : 0;
+      len[i] = in ? __ldg(rp + r + 1) - beg[i] : 0;
+      orow[i] = (in && perm) ? __ldg(perm + r) : r;
+      maxlen = max(maxlen, len[i]);
+    }
+    T q[R][W];
+#pragma unroll
+    for (int i = 0; i < R; ++i)
+#pragma unroll
+      for (int e = 0; e < W; ++e) q[i][e] = Ar<T>::zero();
+    for (int j = t; j < maxlen; j += TEAM) {
+      int cj[R];
+      T vj[R];
+#pragma unroll
+      for (int i = 0; i < R; ++i) {
+        const bool in = j < len[i];
+        cj[i] = in ? __ldcs(ci + beg[i] + j) : 0;
+        vj[i] = in ? __ldcs(val + beg[i] + j) : Ar<T>::zero();
+      }
+      T p[R][W];
+#pragma unroll
+      for (int i = 0; i < R; ++i) load_row(cj[i], p[i]);
+#pragma unroll
+      for (int i = 0; i < R; ++i)
+#pragma unroll
+        for (int e = 0; e < W; ++e) q[i][e] = Ar<T>::fma(vj[i], p[i][e], q[i][e]);
+    }
+    // sum the team's partial rows (fixed order)
+#pragma unroll
+    for (int m = 1; m < TEAM; m <<= 1)
+#pragma unroll
+      for (int i = 0; i < R; ++i)
+#pragma unroll
+        for (int e = 0; e < W; ++e) q[i][e] = Ar<T>::add(q[i][e], Ar<T>::shfl_xor(q[i][e], m));
+    if (t == 0) {
+#pragma unroll
+      for (int i = 0; i < R; ++i) {
+        if (r0 + i >= n) continue;
+        const long long row = orow[i];
+        T* dst = Q + (size_t)row * (EX ? W : s);
+#pragma unroll
+        for (int e = 0; e < W; ++e)
+          if (EX || e < s) dst[e] = q[i][e];
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+          const int md = rmode[r];
+          if (md == RED_NONE) continue;
+          if (md == RED_NORM2) {
+#pragma unroll
+            for (int e = 0; e < W; ++e) acc[r].v[0] = Ar<T>::cfma(q[i][e], q[i][e], acc[r].v[0]);
+          } else if (md == RED_COLNORM2) {
+#pragma unroll
+            for (int e = 0; e < W; ++e) acc[r].v[e] = Ar<T>::cfma(q[i][e], q[i][e], acc[r].v[e]);
+          } else if (md == RED_SUMVEC) {
+            const T y = ry[r][row];
+#pragma unroll
+            for (int e = 0; e < W; ++e) acc[r].v[0] = Ar<T>::cfma(y, q[i][e], acc[r].v[0]);
+          } else {
+            T y[W];
+            const T* ys = ry[r] + (size_t)row * (EX ? W : s);
+#pragma unroll
+            for (int e = 0; e < W; ++e) y[e] = (EX || e < s) ? ys[e] : Ar<T>::zero();
+            if (md == RED_FULL) {
+#pragma unroll
+              for (int k = 0; k < W; ++k)
+#pragma unroll
+                for (int c = 0; c < W; ++c) acc[r].f[k][c] = Ar<T>::cfma(y[k], q[i][c], acc[r].f[k][c]);
+            } else if (md == RED_TRACE) {
+#pragma unroll
+              for (int e = 0; e < W; ++e) acc[r].v[0] = Ar<T>::cfma(y[e], q[i][e], acc[r].v[0]);
+            } else {
+#pragma unroll
+              for (int e = 0; e < W; ++e) acc[r].v[e] = Ar<T>::cfma(y[e], q[i][e], acc[r].v[e]);
+            }
+          }
+        }
+      }
+    }
+  }
+  if (nred == 0) return;
+  // team leaders -> warp (xor over the teams, fixed order) -> warps in index order
+  constexpr int ND = Ar<T>::ND;
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    if (r >= nred) break;
+    const int md = rmode[r];
+    const int len = red_len(md, s, ND == 2);
+    double* w = smem + (size_t)warp * len;
+#pragma unroll
+    for (int m = TEAM; m < 32; m <<= 1)
+#pragma unroll
+      for (int c = 0; c < W; ++c) {
+        acc[r].v[c] = Ar<T>::add(acc[r].v[c], Ar<T>::shfl_xor(acc[r].v[c], m));
+#pragma unroll
+        for (int k = 0; k < W; ++k) acc[r].f[k][c] = Ar<T>::add(acc[r].f[k][c], Ar<T>::shfl_xor(acc[r].f[k][c], m));
+      }
+    if (lane == 0) {
+      if (md == RED_NORM2) w[0] = re_of(acc[r].v[0]);
+      else if (md == RED_TRACE || md == RED_SUMVEC) Ar<T>::st(w, acc[r].v[0]);
+      else if (md == RED_COLNORM2) {
+#pragma unroll
+        for (int c = 0; c < W; ++c)
+          if (c < s) w[c] = re_of(acc[r].v[c]);
+      } else if (md == RED_DIAG) {
+#pragma unroll
+        for (int c = 0; c < W; ++c)
+          if (c < s) Ar<T>::st(w + c * ND, acc[r].v[c]);
+      } else {
+#pragma unroll
+        for (int k = 0; k < W; ++k)
+#pragma unroll
+          for (int c = 0; c < W; ++c)
+            if (k < s && c < s) Ar<T>::st(w + (k * s + c) * ND, acc[r].f[k][c]);
+      }
+    }
+    __syncthreads();
+    const int nw = blockDim.x >> 5;
+    for (int j = threadIdx.x; j < len; j += blockDim.x) {
+      double sum = 0.0;
+      for (int q2 = 0; q2 < nw; ++q2) sum += smem[q2 * len + j];
+      a.partials[(size_t)blockIdx.x * a.pstride + a.red[r].poff + j] = sum;
+    }
+    __syncthreads();
+  }
+}
+
 // rows per group in flight
 // rows per lane group in flight (measured on config 3: scripts/spmm_tune.cu)
 template <typename T, int S> constexpr int spmm_rows() {
@@ -686,9 +887,31 @@ int launch_spmm_tx(const SpmmArgs& a, int grid, int block, size_t smem, cudaStre
 }
 
 // grid < 0: return the number of resident CTAs per SM instead of launching
+template <typename T, int W, bool EX>
+int launch_team(const SpmmArgs& a, int grid, int block, size_t smem, cudaStream_t st) {
+  constexpr int TEAM = 8, R = W * sizeof(T) >= 32 ? 1 : 2;
+  if (grid < 0) {
+    int nb = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, spmv_team_kernel<T, W, TEAM, R, EX>, block, smem);
+    return nb;
+  }
+  spmv_team_kernel<T, W, TEAM, R, EX><<<grid, block, smem, st>>>(a);
+  return (int)cudaGetLastError();
+}
+
+// narrow rows (s * esz <= 32 B): team-per-row kernel
+template <typename T, int S>
+constexpr bool use_team() { return S * (int)sizeof(T) <= 32; }
+
 template <typename T, int S, bool FC>
 int launch_spmm_t(const SpmmArgs& a, int grid, int block, size_t smem, cudaStream_t st) {
   const bool ex = a.s == S && (sizeof(T) == 16 || S % 2 == 0);
+  if constexpr (use_team<T, S>()) {
+    if (a.team) {
+      if (grid < 0 || ex) return launch_team<T, S, true>(a, grid, block, smem, st);
+      return launch_team<T, S, false>(a, grid, block, smem, st);
+    }
+  }
   if (grid < 0 || ex) return launch_spmm_tx<T, S, FC, true>(a, grid, block, smem, st);
   return launch_spmm_tx<T, S, FC, false>(a, grid, block, smem, st);
 }

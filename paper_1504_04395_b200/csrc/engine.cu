@@ -77,11 +77,12 @@ int Eng::grid_for(int cap, bool full, bool is_spmm, size_t smem, int nin) const 
   const long long rpc = rows_per_cta(cap, cplx);
   long long need = (n + rpc - 1) / rpc;
   static int occ_cache[2][2][2][65][MAX_IN + 1] = {};
-  int& occ = occ_cache[is_spmm][cplx][full][cap][is_spmm ? 0 : nin];
+  int& occ = occ_cache[is_spmm][cplx][full][cap][nin];
   if (occ == 0) {
     SpmmArgs sa{};
     UpdArgs ua{};
     ua.nin = nin;
+    sa.team = is_spmm ? nin : 0;  // SpMM: nin carries the team flag
     occ = is_spmm ? launch_spmm(cplx, cap, full, sa, -1, 256, smem, nullptr)
                   : launch_upd(cplx, cap, full, ua, -1, 256, smem, nullptr);
     if (occ < 1) occ = 1;
@@ -192,7 +193,11 @@ int Eng::spmm(bool adj, const void* P, void* Q, int s, std::vector<RQ> reds) {
   }
   a.pstride = std::max(pstride, 1);
   const size_t smem = (size_t)8 * maxlen * sizeof(double);
-  const int grid = grid_for(cap, full, true, 8 * 2 * 8 * 16 * 16, 0);  // occupancy at the largest epilogue smem
+  // narrow rows: a team of lanes per row when rows are long or irregular (config 5),
+  // a lane per row for short regular rows (the stencil's A^H vector product)
+  const long long nz = adj ? A->nnzH : A->nnz;
+  a.team = (so.perm != nullptr || nz >= 12LL * std::max(1LL, n)) ? 1 : 0;
+  const int grid = grid_for(cap, full, true, 8 * 2 * 8 * 16 * 16, a.team);  // occupancy at the largest epilogue smem
   if ((err = c->ensure_partials((size_t)grid * a.pstride))) return err;
   a.partials = c->partials;
   a.done = done;
@@ -358,7 +363,8 @@ int Eng::gram_full(const void* X, const void* Y, int s, int woff) {
   g.s = s;
   g.cplx = cplx ? 1 : 0;
   const int len = red_len(RED_FULL, s, cplx);
-  const int grid = (int)std::max(1, std::min(c->nsm, gram_mma_chunks(n)));
+  const int occ = std::max(1, launch_gram_mma(g, -1, c->st));
+  const int grid = (int)std::max(1, std::min(c->nsm * occ, gram_mma_chunks(n)));
   if ((err = c->ensure_partials((size_t)grid * len))) return err;
   g.partials = c->partials;
   g.pstride = len;

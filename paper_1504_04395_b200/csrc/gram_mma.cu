@@ -60,7 +60,7 @@ struct GCfg {
 };
 
 template <int W>
-__global__ void __launch_bounds__(256, 1) gram_mma_kernel(GramArgs g) {
+__global__ void __launch_bounds__(256, W <= 64 ? 2 : 1) gram_mma_kernel(GramArgs g) {
   if (g.done && *g.done) return;
   using C = GCfg<W>;
   extern __shared__ __align__(16) double gsm[];
@@ -180,13 +180,18 @@ int launch_w(const GramArgs& g, int grid, cudaStream_t st) {
     cudaFuncSetAttribute(gram_mma_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     attr = true;
   }
+  if (grid < 0) {  // resident CTAs per SM
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gram_mma_kernel<W>, 256, C::SMEM);
+    return occ;
+  }
   gram_mma_kernel<W><<<grid, 256, C::SMEM, st>>>(g);
   return (int)cudaGetLastError();
 }
 
 }  // namespace
 
-// real width w <= 128; grid <= number of SMs
+// real width w <= 128; grid < 0: returns the resident CTAs per SM
 int launch_gram_mma(const GramArgs& g, int grid, cudaStream_t st) {
   if (g.w <= 32) return launch_w<32>(g, grid, st);
   if (g.w <= 64) return launch_w<64>(g, grid, st);

@@ -95,6 +95,7 @@ struct SpmmArgs {
   int pstride;
   const int* done;
   const int* perm;  // balanced row order: CSR arrays are in sorted order, output row = perm[row]
+  int team;         // narrow rows: a team of lanes per row (long / irregular rows) instead of a lane per row
 };
 
 // s x s Gram Y^H X on the FP64 tensor cores (gram_mma.cu); the real view of the

@@ -26,7 +26,11 @@ METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.
            "sm__warps_active.avg.pct_of_peak_sustained_active",
            "smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio",
            "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
-           "sm__inst_executed_pipe_tensor_op_dmma.sum"]
+           "sm__inst_executed_pipe_tensor_op_dmma.sum",
+           "sm__inst_executed_pipe_tensor_subpipe_dmma.avg.pct_of_peak_sustained_active",
+           "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+           "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+           "smsp__average_warps_issue_stalled_math_pipe_throttle_per_issue_active.ratio"]
 
 
 def ncu_raw(rep):
@@ -43,7 +47,7 @@ def to_bytes(v, unit):
 def main(tag):
     os.makedirs(PROF, exist_ok=True)
     summary = {}
-    for name in ("spmm", "upd"):
+    for name in ("spmm", "upd", "bsr", "gram"):
         rep = os.path.join(OUT, f"prof_{name}.ncu-rep")
         if not os.path.exists(rep):
             continue
