@@ -1,8 +1,8 @@
 // gram_mma.cu — the s x s block Gram G = Y^H X over n rows (the
 // "2s^2 inner products" of the block variants) on the FP64
 // tensor cores, for widths where the contraction is dense enough to be compute
-// bound (s > 16: 2ns^2 flops against 16ns bytes, e.g. config 5 at s = 64:
-// 34 GFLOP per Gram). mma.sync.m8n8k4.f64 (DMMA) measured 37.1 TFLOP/s on this
+// bound (s >= 16: 2ns^2 flops against 16ns bytes, e.g. config 5 at s = 64:
+// 34 GFLOP per Gram; at s = 16 the FMA epilogue costs more than this pass). mma.sync.m8n8k4.f64 (DMMA) measured 37.1 TFLOP/s on this
 // B200 against 33.9 for DFMA (scripts/fp64_probe.cu), with 8x fewer instructions.
 //
 // A complex n x s block in interleaved storage is the real n x 2s matrix
@@ -51,8 +51,9 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
 template <int W>
 struct GCfg {
   static constexpr int NT = W / 8;            // 8 x 8 tiles per dimension
-  static constexpr int WM = 2, WN = 4;        // warp grid
-  static constexpr int TM = NT / WM, TN = (NT / WN) > 0 ? NT / WN : 1;
+  static constexpr int WM = NT < 2 ? NT : 2;  // warp grid (warps >= WM * WN only stage data)
+  static constexpr int WN = NT < 4 ? NT : 4;
+  static constexpr int TM = NT / WM, TN = NT / WN;
   static constexpr int LDS = W + PADW;        // smem row stride (doubles)
   static constexpr int BUF = 2 * KC * LDS;    // Y chunk + X chunk (doubles)
   static constexpr int NBUF = W <= 64 ? 3 : 2;
@@ -133,6 +134,7 @@ __global__ void __launch_bounds__(256, W <= 64 ? 2 : 1) gram_mma_kernel(GramArgs
     const double* xs = ys + KC * C::LDS;
 #pragma unroll
     for (int k0 = 0; k0 < KC; k0 += 4) {
+      if (warp >= C::WM * C::WN) break;
       double a[C::TM], bb[C::TN];
 #pragma unroll
       for (int i = 0; i < C::TM; ++i) a[i] = ys[(k0 + fk) * C::LDS + (wm * C::TM + i) * 8 + fr];
@@ -149,6 +151,7 @@ __global__ void __launch_bounds__(256, W <= 64 ? 2 : 1) gram_mma_kernel(GramArgs
   __syncthreads();
   // CTA partial: B (W x W real) through shared memory, then the FULL layout
   double* bsm = gsm;  // W * W doubles <= the ring
+  if (warp < C::WM * C::WN)
 #pragma unroll
   for (int i = 0; i < C::TM; ++i)
 #pragma unroll
@@ -193,6 +196,7 @@ int launch_w(const GramArgs& g, int grid, cudaStream_t st) {
 
 // real width w <= 128; grid < 0: returns the resident CTAs per SM
 int launch_gram_mma(const GramArgs& g, int grid, cudaStream_t st) {
+  if (g.w <= 16) return launch_w<16>(g, grid, st);
   if (g.w <= 32) return launch_w<32>(g, grid, st);
   if (g.w <= 64) return launch_w<64>(g, grid, st);
   if (g.w <= 128) return launch_w<128>(g, grid, st);

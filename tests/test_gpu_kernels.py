@@ -120,7 +120,7 @@ def test_tsqr_matches_oracle(srk, s, cplx):
 
 
 @pytest.mark.parametrize("cplx", [False, True])
-@pytest.mark.parametrize("s", [32, 64])
+@pytest.mark.parametrize("s", [16, 32, 64])
 def test_gram_mma_edge_rows(srk, s, cplx):
     """DMMA Gram on row counts around the 32-row chunk (1, 31, 32, 33 rows, and
     fewer chunks than SMs), against the oracle's Gram."""
