@@ -603,10 +603,18 @@ def solve(A: Matrix, B, method: str = "egl_bicg", tol: float = 1e-8, maxit: int 
 
 
 def solve_host(A: Matrix, B: np.ndarray, method: str = "egl_bicg", tol: float = 1e-8, maxit: int = 2000,
-               X0: np.ndarray | None = None, poll_every: int = 8):
-    """srk_solve_host: B, X in host memory (numpy, C-contiguous (n, s))."""
+               X0: np.ndarray | None = None, poll_every: int = 8, inplace: bool = False):
+    """srk_solve_host: B, X in host memory (numpy, C-contiguous (n, s)). inplace=True
+    overwrites X0 with the solution (keeps a pinned X0 buffer pinned: no staging copy)."""
     B = np.ascontiguousarray(B)
-    X = np.zeros_like(B) if X0 is None else np.ascontiguousarray(X0).copy()
+    if X0 is None:
+        X = np.zeros_like(B)
+    elif inplace:
+        if not (X0.flags.c_contiguous and X0.flags.writeable and X0.dtype == B.dtype and X0.shape == B.shape):
+            raise SrkError("solve_host(inplace=True): X0 must be a writable C-contiguous array like B")
+        X = X0
+    else:
+        X = np.ascontiguousarray(X0).copy()
     n, s = B.shape
     o = _opts(tol, maxit, poll_every)
     r = _Report()

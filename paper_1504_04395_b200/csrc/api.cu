@@ -1,6 +1,7 @@
 // api.cu — the C-ABI of include/srk.h. Argument checking and marshalling only;
 // all arithmetic happens in the kernels of block_kernels.cu / coef.cu.
 #include <cstdio>
+#include <atomic>
 #include <cstring>
 #include <string>
 
@@ -9,10 +10,21 @@
 using namespace srk;
 
 struct srk_ctx {
-  Ctx c;
+  Ctx c;  // first member: a Mat's Ctx* identifies its srk_ctx
+  // srk_solve keeps the last solver (its n x s workspace) for the next call with the
+  // same operator, width, method and options, and srk_solve_host its staging blocks,
+  // so repeated solves do not reallocate gigabytes of device memory
+  srk_solver* cached = nullptr;
+  unsigned long long cached_mat = 0;
+  int cached_s = 0, cached_method = -1;
+  srk_opts cached_opts{};
+  void* hbuf[2] = {nullptr, nullptr};
+  size_t hcap = 0;
 };
+static std::atomic<unsigned long long> g_matrix_id{0};
 struct srk_matrix {
   Mat m;
+  unsigned long long id = ++g_matrix_id;
 };
 struct srk_solver {
   Solver* sv;
@@ -53,8 +65,17 @@ int srk_create(srk_ctx** out, int device, void* stream) {
   return SRK_OK;
 }
 
+static void drop_cache(srk_ctx* ctx) {
+  if (ctx->cached) srk_solver_destroy(ctx->cached);
+  ctx->cached = nullptr;
+  ctx->cached_mat = 0;
+}
+
 int srk_destroy(srk_ctx* ctx) {
   if (!ctx) return SRK_OK;
+  drop_cache(ctx);
+  for (void* p : ctx->hbuf)
+    if (p) cudaFree(p);
   if (ctx->c.partials) cudaFree(ctx->c.partials);
   if (ctx->c.comm) comm_destroy(ctx->c.comm);
   delete ctx;
@@ -297,6 +318,10 @@ int srk_matrix_create_dist(srk_ctx* ctx, const srk_csr* A, int64_t n_ghost, cons
 int srk_matrix_destroy(srk_matrix* M) {
   if (!M) return SRK_OK;
   Mat& m = M->m;
+  if (m.ctx) {  // a cached solver of this operator dies with it
+    srk_ctx* owner = reinterpret_cast<srk_ctx*>(m.ctx);
+    if (owner->cached_mat == M->id) drop_cache(owner);
+  }
   if (m.rp) cudaFree(m.rp);
   if (m.ci) cudaFree(m.ci);
   if (m.val) cudaFree(m.val);
@@ -580,15 +605,28 @@ int srk_solver_history(srk_solver* h, double* hist_host, int cap) {
 
 int srk_solve(srk_ctx* ctx, const srk_matrix* A, const void* B, void* X, int s, int method, const srk_opts* opts,
               srk_report* rep) {
-  if (!B || !X) return fail(SRK_EINVAL, "srk_solve: null B or X");
+  if (!ctx || !A || !B || !X) return fail(SRK_EINVAL, "srk_solve: null argument");
+  srk_opts o{};
+  fill_opts(&o, opts);
   srk_solver* h = nullptr;
-  int r = srk_solver_create(ctx, A, s, method, opts, &h);
-  if (r) return r;
-  r = srk_solver_start(h, B, X);
+  if (ctx->cached && ctx->cached_mat == A->id && ctx->cached_s == s && ctx->cached_method == method &&
+      std::memcmp(&ctx->cached_opts, &o, sizeof o) == 0) {
+    h = ctx->cached;  // same operator, width, method and options: reuse the workspace
+  } else {
+    drop_cache(ctx);
+    int r = srk_solver_create(ctx, A, s, method, opts, &h);
+    if (r) return r;
+    ctx->cached = h;
+    ctx->cached_mat = A->id;
+    ctx->cached_s = s;
+    ctx->cached_method = method;
+    ctx->cached_opts = o;
+  }
+  int r = srk_solver_start(h, B, X);
   if (!r) r = srk_solver_iterate(h, h->sv->o.maxit, nullptr);
   if (!r) r = srk_solver_get_x(h, X);
   if (!r && rep) r = srk_solver_report(h, rep);
-  srk_solver_destroy(h);
+  if (r) drop_cache(ctx);
   return r;
 }
 
@@ -596,11 +634,17 @@ int srk_solve_host(srk_ctx* ctx, const srk_matrix* A, const void* B_host, void* 
                    const srk_opts* opts, srk_report* rep) {
   if (!ctx || !A || !B_host || !X_host) return fail(SRK_EINVAL, "srk_solve_host: null argument");
   const size_t bytes = (size_t)A->m.n * s * (A->m.cplx ? 16 : 8);
-  void *Bd = nullptr, *Xd = nullptr;
-  if (cudaMalloc(&Bd, bytes) != cudaSuccess || cudaMalloc(&Xd, bytes) != cudaSuccess) {
-    if (Bd) cudaFree(Bd);
-    return fail(SRK_ENOMEM, "srk_solve_host: out of device memory");
+  if (ctx->hcap < bytes) {  // staging blocks, kept by the context
+    for (void*& p : ctx->hbuf) {
+      if (p) cudaFree(p);
+      p = nullptr;
+    }
+    ctx->hcap = 0;
+    if (cudaMalloc(&ctx->hbuf[0], bytes) != cudaSuccess || cudaMalloc(&ctx->hbuf[1], bytes) != cudaSuccess)
+      return fail(SRK_ENOMEM, "srk_solve_host: out of device memory");
+    ctx->hcap = bytes;
   }
+  void *Bd = ctx->hbuf[0], *Xd = ctx->hbuf[1];
   cudaMemcpyAsync(Bd, B_host, bytes, cudaMemcpyHostToDevice, ctx->c.st);
   cudaMemcpyAsync(Xd, X_host, bytes, cudaMemcpyHostToDevice, ctx->c.st);
   int r = srk_solve(ctx, A, Bd, Xd, s, method, opts, rep);
@@ -609,8 +653,6 @@ int srk_solve_host(srk_ctx* ctx, const srk_matrix* A, const void* B_host, void* 
     cudaError_t e = cudaStreamSynchronize(ctx->c.st);
     if (e != cudaSuccess) r = cuda_fail(e, "srk_solve_host");
   }
-  cudaFree(Bd);
-  cudaFree(Xd);
   return r;
 }
 
