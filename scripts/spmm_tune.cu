@@ -161,11 +161,13 @@ int main(int argc, char** argv) {
     for (int i = 0; i < 148; ++i) s2 += p2[i];
     printf("tma vs library: max |dQ| = %.3e   sumvec %.15e vs %.15e\n", md, s1, s2);
   }
-  run<2, 8, true, 2, 8, 1>(a, nsm, bytes, "R2 BC8 PD1 (library)");
-  run_tma<228, 5, 4>(a, map, nsm, bytes, "tma NP4 NST5");
-  run_tma<228, 3, 4>(a, map, nsm, bytes, "tma NP4 NST3");
-  run_tma<228, 5, 8>(a, map, nsm, bytes, "tma NP8 NST5");
-  run_tma<228, 2, 4>(a, map, nsm, bytes, "tma NP4 NST2");
-  run_tma<228, 2, 8>(a, map, nsm, bytes, "tma NP8 NST2");
+  run<2, 8, true, 2, 8, 1>(a, nsm, bytes, "R2 minb2 batch8 (library)");
+  run<2, 8, true, 3, 8, 1>(a, nsm, bytes, "R2 minb3 batch8");
+  run<2, 8, true, 3, 4, 1>(a, nsm, bytes, "R2 minb3 batch4");
+  run<2, 8, true, 4, 4, 1>(a, nsm, bytes, "R2 minb4 batch4");
+  run<1, 8, true, 3, 8, 1>(a, nsm, bytes, "R1 minb3 batch8");
+  run<1, 8, true, 4, 8, 1>(a, nsm, bytes, "R1 minb4 batch8");
+  run<1, 16, true, 4, 8, 1>(a, nsm, bytes, "R1 BC16 minb4 batch8");
+  run<2, 8, true, 2, 8, 1>(a, nsm, bytes, "R2 minb2 batch8 (repeat)");
   return 0;
 }
