@@ -208,7 +208,12 @@ typedef struct {
 } srk_opts;
 
 /* Full solve (a1-a7): B, X device n x s blocks; X holds X0 on entry and the
- * iterate on exit. opts may be NULL (tol 1e-8, maxit 2000). */
+ * iterate on exit. opts may be NULL (tol 1e-8, maxit 2000). s <= 64; the block
+ * methods (s x s coefficients) take s <= 32, their s x s Grams beyond s = 16 on the
+ * FP64 tensor cores. The context keeps the last solver's workspace for the next
+ * call with the same operator, s, method and options (freed by srk_destroy or
+ * when the operator is destroyed). Errors: SRK_EUNSUPPORTED (e.g. a block method
+ * with s > 32, a method needing A^H on an operator created without it). */
 int srk_solve(srk_ctx* ctx, const srk_matrix* A, const void* B, void* X, int s, int method,
               const srk_opts* opts, srk_report* rep);
 /* Same with HOST B and X (pinned or pageable): copies in, solves, copies out. */

@@ -452,7 +452,7 @@ int srk_tsqr(srk_ctx* ctx, const void* Z, void* Q, void* C, int64_t n, int s, in
   if (!ctx || !Z || !Q || !C) return fail(SRK_EINVAL, "srk_tsqr: null argument");
   if (s < 1 || s > 64 || n < s) return fail(SRK_EDIM, "srk_tsqr: need 1 <= s <= 64 and n >= s");
   const bool cplx = dtype == SRK_C128;
-  if (!full_supported(cplx, cap_for(s))) return fail(SRK_EUNSUPPORTED, "srk_tsqr: s <= 16");
+  if (!full_supported(cplx, cap_for(s))) return fail(SRK_EUNSUPPORTED, "srk_tsqr: s <= 32");
   TsqrSolver T;
   T.c = &ctx->c;
   T.s = s;
@@ -488,7 +488,7 @@ int srk_solver_create(srk_ctx* ctx, const srk_matrix* A, int s, int method, cons
   const bool block = method == SRK_BL_BICG || method == SRK_BL_BICG_RQ || method == SRK_BL_QMR ||
                      method == SRK_BL_BICGSTAB || method == SRK_BL_BICGSTAB_RQ;
   if (block && !full_supported(A->m.cplx, cap_for(s)))
-    return fail(SRK_EUNSUPPORTED, "srk_solver_create: block methods need s <= 16");
+    return fail(SRK_EUNSUPPORTED, "srk_solver_create: block methods need s <= 32");
   if (A->m.bsr && !bsr_supported(A->m.bs, A->m.cplx, s))
     return fail(SRK_EUNSUPPORTED, "srk_solver_create: BSR operators take s in {4, 8, 12, 16}");
   Solver* sv = make_solver(method);

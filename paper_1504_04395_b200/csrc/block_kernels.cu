@@ -61,7 +61,10 @@ int launch_upd(bool cplx, int cap, bool full, const UpdArgs& a, int grid, int bl
   return cplx ? launch_upd_c128(cap, full, a, grid, block, smem, st) : launch_upd_f64(cap, full, a, grid, block, smem, st);
 }
 
-bool full_supported(bool cplx, int cap) { (void)cplx; return cap <= 16; }
+// block-method instances (s x s coefficients) up to capacity 32; the in-kernel s x s
+// Gram up to 16 (wider ones are routed to the tensor-core Gram by the engine)
+bool full_supported(bool cplx, int cap) { (void)cplx; return cap <= 32; }
+bool full_red_supported(bool cplx, int cap) { (void)cplx; return cap <= 16; }
 
 int padded_width(int cap, bool cplx) {
   const int esz = cplx ? 16 : 8;

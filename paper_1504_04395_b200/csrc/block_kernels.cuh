@@ -24,7 +24,8 @@ template <typename T, int S, bool FC>
 struct RedAcc {
   using L = Lay<T, S>;
   // FULL (FC) needs S x EPL values; the other modes use the first EPL.
-  static constexpr int N = FC ? S * L::EPL : L::EPL;
+  // (the in-kernel s x s Gram is compiled up to S = 16; wider Grams run on the tensor cores)
+  static constexpr int N = (FC && S <= 16) ? S * L::EPL : L::EPL;
   T v[N];
 };
 
@@ -54,7 +55,7 @@ template <typename T, int S, bool FC>
 __device__ __forceinline__ void red_full(RedAcc<T, S, FC>& a, const T (&x)[Lay<T, S>::EPL],
                                          const T (&y)[Lay<T, S>::EPL], int base, int s, unsigned gmask) {
   using L = Lay<T, S>;
-  if constexpr (FC) {
+  if constexpr (FC && S <= 16) {
 #pragma unroll
     for (int k = 0; k < S; ++k) {
       if (k < s) {
@@ -146,7 +147,7 @@ __device__ void red_flush(RedAcc<T, S, FC>& a, double* __restrict__ partials, in
         }
       }
     }
-  } else if constexpr (MODE == RED_FULL && FC) {
+  } else if constexpr (MODE == RED_FULL && FC && S <= 16) {
     if (lane < L::G) {
 #pragma unroll
       for (int k = 0; k < S; ++k) {
@@ -866,7 +867,7 @@ template <typename T, int S> constexpr int spmm_rows() {
   return (Lay<T, S>::G == 1 || S >= 64) ? 1 : 2;
 }
 template <int NI> constexpr int upd_rows() { return NI <= 2 ? 2 : 1; }
-template <typename T, int S> constexpr bool full_ok() { return S <= 16; }
+template <typename T, int S> constexpr bool full_ok() { return S <= 32; }
 
 // grid < 0: return the number of resident CTAs per SM instead of launching
 template <typename T, int S, bool FC, bool EX>

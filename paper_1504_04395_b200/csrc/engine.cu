@@ -161,6 +161,23 @@ int Eng::spmm(bool adj, const void* P, void* Q, int s, std::vector<RQ> reds) {
   if (A->bsr) return spmm_bsr(adj, P, Q, s, reds);
   if ((err = halo(adj, P, s))) return err;
   const int cap = cap_for(s);
+  // s x s Grams wider than the in-kernel epilogue: Y^H Q on the tensor cores afterwards
+  std::vector<RQ> wide;
+  if (!full_red_supported(cplx, cap)) {
+    for (auto it = reds.begin(); it != reds.end();)
+      if (it->mode == RED_FULL) {
+        wide.push_back(*it);
+        it = reds.erase(it);
+      } else {
+        ++it;
+      }
+  }
+  if (!wide.empty()) {
+    if ((err = spmm(adj, P, Q, s, reds))) return err;
+    for (const RQ& q : wide)
+      if ((err = gram_full(Q, q.yext, s, q.woff))) return err;
+    return 0;
+  }
   bool full = false;
   for (auto& r : reds) full |= (r.mode == RED_FULL);
   if (full && !full_supported(cplx, cap)) return err = (int)cudaErrorNotSupported;
@@ -229,6 +246,55 @@ int Eng::upd(int s, std::vector<const void*> in, std::vector<OutSpec> outs, std:
       r.yext = nullptr;
     }
   const int cap = cap_for(s);
+  // s x s Grams wider than the in-kernel epilogue run on the tensor cores: before the
+  // update when they read only inputs, after it when they read an output
+  struct Wide {
+    const void *x, *y;
+    int woff;
+  };
+  std::vector<Wide> pre, post;
+  if (!full_red_supported(cplx, cap)) {
+    auto ptr = [&](int src) -> const void* {
+      if (src >= 0 && src < (int)in.size()) return in[src];
+      if (src >= SRC_OUT && src - SRC_OUT < (int)outs.size()) {
+        const OutSpec& o = outs[src - SRC_OUT];
+        if (o.ptr) return o.ptr;
+        // a register-only output that is a plain copy of an input is that input
+        if (o.t.size() == 1 && o.t[0].c.kind == CK_ONE && !o.t[0].c.neg && o.t[0].src >= 0 && o.t[0].src < (int)in.size())
+          return in[o.t[0].src];
+      }
+      return nullptr;
+    };
+    auto overwritten = [&](int src) {  // an input whose buffer an output rewrites
+      if (src < 0 || src >= (int)in.size()) return false;
+      for (auto& o : outs)
+        if (o.ptr == in[src]) return true;
+      return false;
+    };
+    for (auto it = reds.begin(); it != reds.end();) {
+      if (it->mode != RED_FULL) {
+        ++it;
+        continue;
+      }
+      const void* x = ptr(it->x);
+      const void* y = it->y >= 0 ? ptr(it->y) : it->yext;
+      auto is_copy = [&](int src) {
+        return src >= SRC_OUT && src - SRC_OUT < (int)outs.size() && !outs[src - SRC_OUT].ptr;
+      };
+      const bool after = (it->x >= SRC_OUT && !is_copy(it->x)) || (it->y >= SRC_OUT && !is_copy(it->y));
+      if (!x || !y || (after && (overwritten(it->x) || overwritten(it->y)))) return err = (int)cudaErrorNotSupported;
+      (after ? post : pre).push_back(Wide{x, y, it->woff});
+      it = reds.erase(it);
+    }
+  }
+  for (const Wide& w : pre)
+    if ((err = gram_full(w.x, w.y, s, w.woff))) return err;
+  if (!post.empty()) {
+    if ((err = upd(s, in, outs, reds))) return err;
+    for (const Wide& w : post)
+      if ((err = gram_full(w.x, w.y, s, w.woff))) return err;
+    return 0;
+  }
   bool full = false;  // s x s Gram or s x s coefficient: the block-method kernel instance
   for (auto& r : reds) full |= (r.mode == RED_FULL);
   for (auto& o : outs)

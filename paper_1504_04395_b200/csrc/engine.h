@@ -14,6 +14,7 @@ namespace srk {
 int cap_for(int s);
 int rows_per_cta(int cap, bool cplx);
 bool full_supported(bool cplx, int cap);
+bool full_red_supported(bool cplx, int cap);
 int padded_width(int cap, bool cplx);
 int launch_spmm(bool cplx, int cap, bool full, const SpmmArgs& a, int grid, int block, size_t smem, cudaStream_t st);
 int launch_upd(bool cplx, int cap, bool full, const UpdArgs& a, int grid, int block, size_t smem, cudaStream_t st);

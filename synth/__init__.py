@@ -113,6 +113,98 @@ def conv_diff_3d(m: int, c=(50.0, 30.0, 10.0), dtype=np.float64, shift=0.0) -> C
     return A
 
 
+def _boundary_rhs(m: int, dims: int, coup_vals: dict, g) -> np.ndarray:
+    """b = -sum over boundary neighbours of (coupling * g(boundary point)) for the
+    h^2-scaled stencil on the m^dims interior grid (unknown index x fastest).
+    coup_vals[(axis, direction)] is the neighbour coupling; g(points) evaluates the
+    Dirichlet data at an (N, dims) array of boundary points."""
+    h = 1.0 / (m + 1)
+    n = m ** dims
+    idx = np.arange(n, dtype=np.int64)
+    co = [(idx // m ** d) % m + 1 for d in range(dims)]  # 1-based grid coordinates
+    b = np.zeros(n)
+    for (axis, direction), val in coup_vals.items():
+        edge = m if direction > 0 else 1
+        sel = co[axis] == edge
+        pts = np.stack([c[sel] * h for c in co], axis=1)
+        pts[:, axis] = 1.0 if direction > 0 else 0.0
+        b[sel] -= val * g(pts)
+    return b
+
+
+def paper_ex1(m: int = 200, alpha=(5.0, 5.0, 5.0)):
+    """Ex. 1 of the paper: -u_xx - u_yy + 2 a1 u_x + 2 a2 u_y - 2 a3 u = 0 on
+    the unit square, Dirichlet data, a = (5, 5, 5), central differences on the m x m
+    interior grid (h^2-scaled). Four right-hand sides, one per corner: the boundary
+    data is continuous and piecewise linear along the boundary, 1 at that corner and
+    0 at the other three. Returns (A, B) with B of shape (m^2, 4); corners in the order
+    (0,0), (1,0), (0,1), (1,1)."""
+    h = 1.0 / (m + 1)
+    a1, a2, a3 = alpha
+    A = conv_diff_2d(m, c=(2 * a1, 2 * a2), shift=-2 * a3 * h * h)
+    coup = {(0, +1): -1.0 + a1 * h, (0, -1): -1.0 - a1 * h, (1, +1): -1.0 + a2 * h, (1, -1): -1.0 - a2 * h}
+
+    def corner(cx, cy):
+        # piecewise linear hat along the boundary: on the two edges through the corner
+        # it falls linearly from 1 to 0, elsewhere it is 0
+        def g(pts):
+            x, y = pts[:, 0], pts[:, 1]
+            on_vx = np.isclose(x, cx)  # edge x = cx: linear in y
+            on_hy = np.isclose(y, cy)  # edge y = cy: linear in x
+            return np.where(on_vx, 1.0 - np.abs(y - cy), 0.0) + np.where(on_hy & ~on_vx, 1.0 - np.abs(x - cx), 0.0)
+        return g
+
+    B = np.stack([_boundary_rhs(m, 2, coup, corner(cx, cy)) for cx, cy in ((0, 0), (1, 0), (0, 1), (1, 1))], axis=1)
+    A.meta = dict(kind="paper_ex1", m=m, alpha=tuple(alpha))
+    return A, B
+
+
+def paper_ex2(m: int = 50, nu: float = 1000.0):
+    """Ex. 2 of the paper (Ex. 3 = nu 10): u_xx + u_yy + u_zz +
+    nu u_x = f on the unit cube, central differences on the m^3 interior grid, written
+    as the h^2-scaled -Delta u - nu u_x = -f (conv_diff_3d with c = (-nu, 0, 0)).
+    19 right-hand sides: (1) f such that u = exp(xyz) sin(pi x) sin(pi y) sin(pi z) with
+    zero boundary data; (2-19) f = 0 with, for each face in the order x=0, x=1, y=0,
+    y=1, z=0, z=1, the boundary data equal to its first free coordinate, its second
+    free coordinate and 1 on that face (0 on the others)."""
+    h = 1.0 / (m + 1)
+    A = conv_diff_3d(m, c=(-nu, 0.0, 0.0))
+    coup = {}
+    for axis in range(3):
+        cval = -nu if axis == 0 else 0.0
+        coup[(axis, +1)] = -1.0 + cval * h / 2
+        coup[(axis, -1)] = -1.0 - cval * h / 2
+    n = m ** 3
+    idx = np.arange(n, dtype=np.int64)
+    x, y, z = [((idx // m ** d) % m + 1) * h for d in range(3)]
+    E = np.exp(x * y * z)
+    sx, sy, sz = np.sin(np.pi * x), np.sin(np.pi * y), np.sin(np.pi * z)
+    cx, cy, cz = np.cos(np.pi * x), np.cos(np.pi * y), np.cos(np.pi * z)
+    S = sx * sy * sz
+    pi = np.pi
+    uxx = E * ((y * z) ** 2 * S + 2 * y * z * pi * cx * sy * sz - pi * pi * S)
+    uyy = E * ((x * z) ** 2 * S + 2 * x * z * pi * sx * cy * sz - pi * pi * S)
+    uzz = E * ((x * y) ** 2 * S + 2 * x * y * pi * sx * sy * cz - pi * pi * S)
+    ux = E * (y * z * S + pi * cx * sy * sz)
+    f = uxx + uyy + uzz + nu * ux
+    cols = [-h * h * f]
+    for axis in range(3):
+        for side in (0.0, 1.0):
+            free = [d for d in range(3) if d != axis]
+
+            def face(which, axis=axis, side=side, free=free):
+                def g(pts):
+                    on = np.isclose(pts[:, axis], side)
+                    val = np.ones(len(pts)) if which == 2 else pts[:, free[which]]
+                    return np.where(on, val, 0.0)
+                return g
+            for which in range(3):
+                cols.append(_boundary_rhs(m, 3, coup, face(which)))
+    B = np.stack(cols, axis=1)
+    A.meta = dict(kind="paper_ex2", m=m, nu=nu)
+    return A, B
+
+
 def random_rhs(n: int, s: int, seed: int, complex_: bool = False) -> np.ndarray:
     """Gaussian right-hand sides, row-major draw order."""
     rng = np.random.default_rng(seed)

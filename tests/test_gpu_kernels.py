@@ -94,7 +94,7 @@ def test_gram_block(srk, s, cplx):
 
 
 @pytest.mark.parametrize("cplx", [False, True])
-@pytest.mark.parametrize("s", [1, 4, 7, 12, 16])
+@pytest.mark.parametrize("s", [1, 4, 7, 12, 16, 19, 32])
 @pytest.mark.parametrize("kind", ["scalar", "diag", "full"])
 def test_block_update(srk, s, cplx, kind):
     rng = np.random.default_rng(13)
@@ -107,7 +107,7 @@ def test_block_update(srk, s, cplx, kind):
 
 
 @pytest.mark.parametrize("cplx", [False, True])
-@pytest.mark.parametrize("s", [1, 3, 8, 16])
+@pytest.mark.parametrize("s", [1, 3, 8, 16, 19, 32])
 def test_tsqr_matches_oracle(srk, s, cplx):
     rng = np.random.default_rng(17)
     Z = _rand(rng, 20011, s, cplx)

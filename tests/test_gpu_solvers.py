@@ -200,6 +200,29 @@ def test_lattice_bsr_lockstep_and_solve(srk, method):
     assert np.linalg.norm(B - As @ to_np(X)) / np.linalg.norm(B) <= tol
 
 
+@pytest.mark.parametrize("cplx", [False, True])
+@pytest.mark.parametrize("method", ["bl_bicg", "bl_bicg_rq", "bl_qmr", "bl_bicgstab", "bl_bicgstab_rq"])
+def test_block_methods_wide(srk, method, cplx):
+    """Block methods at s = 19 (the paper's Ex. 2/3 width): s x s coefficient
+    updates in the capacity-32 kernels and the s x s Grams on the tensor cores;
+    lock-step parity and the full solve on a 3D convection-diffusion operator."""
+    A = synth.conv_diff_3d(9, (10.0, 5.0, 2.0), np.complex128 if cplx else np.float64, -0.1j if cplx else 0.0)
+    B = synth.random_rhs(A.n, 19, 3, cplx)
+    As = A.to_scipy()
+    tol = 1e-8
+    a, _, env = envelope(method, As, B, tol)
+    M = srk.Matrix.from_csr(A, need_adjoint=srk.NEEDS_ADJOINT[method])
+    sv, xs = lockstep(srk, M, B, method, min(K, a.iterations), tol)
+    for k in range(min(len(xs), len(a.Xs))):
+        assert rel(xs[k], a.Xs[k]) <= env[k], (method, k + 1, rel(xs[k], a.Xs[k]), env[k])
+    sv.close()
+    X, rep = srk.solve(M, to_dev(B), method, tol=tol, maxit=2000)
+    if rep.outcome == "converged":
+        assert np.linalg.norm(B - As @ to_np(X)) / np.linalg.norm(B) <= tol
+    else:  # the oracle must see the same outcome
+        assert rep.outcome in {r.outcome for r in oracle_ensemble(method, As, B, tol, n_pert=1)}
+
+
 @pytest.mark.parametrize("method", ["bl_bicg_rq", "bl_qmr", "bl_bicgstab_rq"])
 def test_config2_block_methods(srk, method):
     """Config 2's methods (block BiCG / QMR / BiCGStab with QR) on its operator at 16^3, s = 8 complex."""
