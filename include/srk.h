@@ -120,6 +120,18 @@ int srk_matrix_create(srk_ctx* ctx, const srk_csr* A, int need_adjoint, srk_matr
 int srk_matrix_create_bsr(srk_ctx* ctx, int64_t nb, int bs, int64_t nnzb, const int64_t* block_row_ptr,
                           const int32_t* block_col, const void* values, int dtype, int unit_diag,
                           srk_matrix** out);
+/* Right ILU(0) preconditioning (the
+ * no-fill incomplete LU of A, M = L U, computed once on the host from the operator's
+ * CSR and attached to it). Every later solve with this operator iterates on
+ * A M^-1 Y = B (A^H products as M^-H A^H) and returns X = M^-1 Y; X0 enters as Y0 = M X0.
+ * The triangular solves run level-scheduled on the device. Scalar single-GPU CSR
+ * operators only. Errors: SRK_EINVAL (zero pivot), SRK_EUNSUPPORTED, SRK_ENOMEM. */
+int srk_matrix_ilu0(srk_matrix* A);
+/* the factor values on A's pattern (L strictly below, U on and above the diagonal),
+ * nnz values (complex interleaved) into a HOST buffer — for tests */
+int srk_matrix_ilu0_factor(const srk_matrix* A, void* values_host);
+/* Z = M^-1 P (adjoint: M^-H P), n x s device blocks, stream-ordered */
+int srk_precond_apply(srk_ctx* ctx, const srk_matrix* A, int adjoint, const void* P, void* Z, int s);
 int srk_matrix_destroy(srk_matrix* A);
 /* copy A^H back (CSR arrays of size n+1 / nnz, device pointers) — for tests */
 int srk_matrix_adjoint(const srk_matrix* A, int64_t* row_ptr, int32_t* col_idx, void* values);

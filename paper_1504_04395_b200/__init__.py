@@ -35,7 +35,7 @@ EXPORTS = ("srk_create", "srk_destroy", "srk_last_error", "srk_version", "srk_ma
            "srk_solver_get_residual", "srk_solver_report", "srk_solver_history", "srk_solver_profile",
            "srk_solver_profile_read", "srk_solver_profile_launches", "srk_partition_rows", "srk_plan_create", "srk_plan_sizes", "srk_plan_arrays",
            "srk_plan_destroy", "srk_nccl_unique_id", "srk_comm_init", "srk_matrix_create_dist",
-           "srk_matrix_create_bsr")
+           "srk_matrix_create_bsr", "srk_matrix_ilu0", "srk_matrix_ilu0_factor", "srk_precond_apply")
 
 
 class SrkError(RuntimeError):
@@ -88,6 +88,9 @@ def load_library(path: str | None = None):
         "srk_matrix_create": ([vp, ctypes.POINTER(_Csr), i, ctypes.POINTER(vp)], i),
         "srk_matrix_create_bsr": ([vp, i64, i, i64, vp, vp, vp, i, i, ctypes.POINTER(vp)], i),
         "srk_matrix_destroy": ([vp], i),
+        "srk_matrix_ilu0": ([vp], i),
+        "srk_matrix_ilu0_factor": ([vp, vp], i),
+        "srk_precond_apply": ([vp, vp, i, vp, vp, i], i),
         "srk_matrix_adjoint": ([vp, vp, vp, vp], i),
         "srk_spmm_block": ([vp, vp, i, vp, vp, i, i, vp, vp], i),
         "srk_gram_block": ([vp, vp, vp, i64, i, i, i, vp], i),
@@ -246,6 +249,20 @@ class Matrix:
         self.h = h
         self.has_adjoint = False
         return self
+
+    def ilu0(self):
+        """Attach the right ILU(0) preconditioner (srk_matrix_ilu0); returns self."""
+        _check(_lib.srk_matrix_ilu0(self.h), "srk_matrix_ilu0")
+        self.preconditioned = True
+        return self
+
+    def ilu0_factor(self) -> np.ndarray:
+        """The ILU(0) factor values on the operator's pattern (host copy)."""
+        torch = _torch()
+        cplx = self.dtype == torch.complex128
+        out = np.empty(self.nnz, dtype=np.complex128 if cplx else np.float64)
+        _check(_lib.srk_matrix_ilu0_factor(self.h, out.ctypes.data_as(ctypes.c_void_p)), "srk_matrix_ilu0_factor")
+        return out
 
     def adjoint_csr(self):
         torch = _torch()
@@ -438,6 +455,15 @@ def spmm_block(A: Matrix, P, adjoint: bool = False, gram: str = "none", Y=None, 
                                _dev(Y, "Y") if Y is not None else None,
                                ctypes.c_void_p(out.data_ptr()) if out is not None else None), "srk_spmm_block")
     return Q if out is None else (Q, out)
+
+
+def precond_apply(A: Matrix, P, adjoint: bool = False):
+    """Z = M^-1 P (or M^-H P) with the operator's ILU(0) (srk_precond_apply)."""
+    torch = _torch()
+    Z = torch.empty_like(P)
+    s = P.shape[1] if P.dim() == 2 else 1
+    _check(_lib.srk_precond_apply(A.ctx.h, A.h, int(adjoint), _dev(P, "P"), _dev(Z, "Z"), s), "srk_precond_apply")
+    return Z
 
 
 def gram_block(X, Y=None, mode: str = "full", ctx: Context | None = None):

@@ -216,6 +216,41 @@ int srk_matrix_create_bsr(srk_ctx* ctx, int64_t nb, int bs, int64_t nnzb, const 
   return SRK_OK;
 }
 
+int srk_matrix_ilu0(srk_matrix* A) {
+  if (!A) return fail(SRK_EINVAL, "srk_matrix_ilu0: null matrix");
+  Mat& m = A->m;
+  if (m.bsr || m.dist) return fail(SRK_EUNSUPPORTED, "srk_matrix_ilu0: scalar single-GPU CSR operators only");
+  srk_ctx* owner = reinterpret_cast<srk_ctx*>(m.ctx);
+  if (owner && owner->cached_mat == A->id) drop_cache(owner);  // the operator changes
+  const int r = build_ilu0(m, m.ctx->st);
+  if (r == 1) return fail(SRK_EINVAL, "srk_matrix_ilu0: zero pivot (missing or vanishing diagonal)");
+  if (r == 2) return fail(SRK_ENOMEM, "srk_matrix_ilu0: out of device memory");
+  if (r) return fail(SRK_ECUDA, "srk_matrix_ilu0: CUDA error");
+  return SRK_OK;
+}
+
+int srk_matrix_ilu0_factor(const srk_matrix* A, void* values_host) {
+  if (!A || !values_host) return fail(SRK_EINVAL, "srk_matrix_ilu0_factor: null argument");
+  if (!A->m.prec) return fail(SRK_EINVAL, "srk_matrix_ilu0_factor: no ILU(0) attached");
+  const std::vector<double>& f = A->m.prec->factor;
+  std::memcpy(values_host, f.data(), f.size() * sizeof(double));
+  return SRK_OK;
+}
+
+int srk_precond_apply(srk_ctx* ctx, const srk_matrix* A, int adjoint, const void* P, void* Z, int s) {
+  if (!ctx || !A || !P || !Z) return fail(SRK_EINVAL, "srk_precond_apply: null argument");
+  if (!A->m.prec) return fail(SRK_EINVAL, "srk_precond_apply: no ILU(0) attached");
+  if (s < 1 || s > 64) return fail(SRK_EDIM, "srk_precond_apply: s must be in [1, 64]");
+  Eng e;
+  e.c = &ctx->c;
+  e.A = &A->m;
+  e.cplx = A->m.cplx;
+  e.n = A->m.n;
+  int r = e.prec_solve(adjoint != 0, P, Z, s);
+  if (!r) r = (int)cudaStreamSynchronize(ctx->c.st);
+  return check_cuda(r, "srk_precond_apply");
+}
+
 // ---------------------------------------------------------------- multi-GPU
 int srk_nccl_unique_id(void* id128_host) {
   if (!id128_host) return fail(SRK_EINVAL, "srk_nccl_unique_id: null buffer");
@@ -334,6 +369,8 @@ int srk_matrix_destroy(srk_matrix* M) {
     delete[] H->recv_off;
   }
   if (m.sendbuf) cudaFree(m.sendbuf);
+  free_prec(m.prec);
+  m.prec = nullptr;
   if (m.brp) cudaFree(m.brp);
   if (m.bci) cudaFree(m.bci);
   if (m.bval) cudaFree(m.bval);
@@ -537,7 +574,11 @@ int srk_solver_iterate(srk_solver* h, int k, int* state) {
 int srk_solver_get_x(srk_solver* h, void* X) {
   if (!h || !X) return fail(SRK_EINVAL, "srk_solver_get_x: null argument");
   Solver* sv = h->sv;
-  cudaMemcpyAsync(X, sv->X, (size_t)sv->n * sv->s * sv->esz(), cudaMemcpyDeviceToDevice, sv->c->st);
+  if (sv->A && sv->A->prec) {  // X = M^-1 Y (right preconditioning)
+    if (sv->e.prec_solve(false, sv->X, X, sv->s)) return fail(SRK_ECUDA, "srk_solver_get_x: preconditioner");
+  } else {
+    cudaMemcpyAsync(X, sv->X, (size_t)sv->n * sv->s * sv->esz(), cudaMemcpyDeviceToDevice, sv->c->st);
+  }
   cudaError_t e = cudaStreamSynchronize(sv->c->st);
   return e == cudaSuccess ? SRK_OK : cuda_fail(e, "srk_solver_get_x");
 }

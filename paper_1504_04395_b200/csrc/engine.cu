@@ -158,6 +158,7 @@ int Eng::halo(bool adj, const void* P, int s) {
 
 int Eng::spmm(bool adj, const void* P, void* Q, int s, std::vector<RQ> reds) {
   if (err) return err;
+  if (A->prec && !raw) return spmm_prec(adj, P, Q, s, reds);
   if (A->bsr) return spmm_bsr(adj, P, Q, s, reds);
   if ((err = halo(adj, P, s))) return err;
   const int cap = cap_for(s);
@@ -417,6 +418,73 @@ int Eng::spmm_bsr(bool adj, const void* P, void* Q, int s, const std::vector<RQ>
   std::vector<RQ> r2;
   for (const RQ& q : rest) r2.push_back(RQ{q.mode, 0, -1, q.yext, q.woff});
   return upd(s, {Q}, {}, r2);
+}
+
+// Right preconditioning: the solvers iterate on
+// A M^-1 Y = B. A-products become Q = A (U^-1 L^-1 P) with the reductions fused as
+// usual; A^H-products Q = L^-H U^-H (A^H P), reductions in one pass afterwards.
+int Eng::spmm_prec(bool adj, const void* P, void* Q, int s, const std::vector<RQ>& reds) {
+  Prec* M = A->prec;
+  const size_t bytes = (size_t)n * s * (cplx ? 16 : 8);
+  if (M->scratch_bytes < bytes) {  // (never inside a graph capture: the first iteration runs eagerly)
+    for (void*& p : M->scratch) {
+      if (p) cudaFree(p);
+      p = nullptr;
+    }
+    M->scratch_bytes = 0;
+    if (cudaMalloc(&M->scratch[0], bytes) != cudaSuccess) return err = (int)cudaErrorMemoryAllocation;
+    M->scratch_bytes = bytes;
+  }
+  void* T = M->scratch[0];
+  auto tri = [&](const DevTri& t, const void* R, void* Z) {
+    if (prof) prof->begin(PT_OTHER, c->st, s, 0.0);
+    const int r = launch_trsv(t, cplx, n, s, R, Z, done, c->st);
+    if (prof) prof->end(c->st);
+    if (r < 0) return err = -r;
+    nlaunch += r;
+    return 0;
+  };
+  if (!adj) {
+    if (tri(M->L, P, T) || tri(M->U, T, T)) return err;
+    raw = true;
+    const int r = spmm(false, T, Q, s, reds);
+    raw = false;
+    return r;
+  }
+  raw = true;
+  int r = spmm(true, P, T, s, {});
+  raw = false;
+  if (r) return r;
+  if (tri(M->UH, T, T) || tri(M->LH, T, Q)) return err;
+  if (reds.empty()) return 0;
+  std::vector<RQ> r2;
+  for (const RQ& q : reds) r2.push_back(RQ{q.mode, 0, -1, q.yext, q.woff});
+  return upd(s, {Q}, {}, r2);
+}
+
+int Eng::prec_solve(bool adj, const void* Y, void* X, int s) {
+  Prec* M = A->prec;
+  if (!M) return err = (int)cudaErrorInvalidValue;
+  const DevTri& first = adj ? M->UH : M->L;
+  const DevTri& second = adj ? M->LH : M->U;
+  int r = launch_trsv(first, cplx, n, s, Y, X, nullptr, c->st);
+  if (r < 0) return err = -r;
+  r = launch_trsv(second, cplx, n, s, X, X, nullptr, c->st);
+  if (r < 0) return err = -r;
+  return 0;
+}
+
+int Eng::prec_mul(const void* X, void* Y, int s) {  // Y = L (U X)
+  Prec* M = A->prec;
+  if (!M) return err = (int)cudaErrorInvalidValue;
+  const size_t bytes = (size_t)n * s * (cplx ? 16 : 8);
+  void* T = nullptr;
+  if (cudaMalloc(&T, bytes) != cudaSuccess) return err = (int)cudaErrorMemoryAllocation;
+  int r = launch_trimul(M->U, cplx, n, s, X, T, c->st);
+  if (!r) r = launch_trimul(M->L, cplx, n, s, T, Y, c->st);
+  cudaStreamSynchronize(c->st);
+  cudaFree(T);
+  return err = r;
 }
 
 int Eng::gram_full(const void* X, const void* Y, int s, int woff) {

@@ -44,6 +44,28 @@ struct Ctx {
   int ensure_partials(size_t n);
 };
 
+// One triangular factor of the ILU(0) preconditioner on the device: the off-diagonal
+// part as CSR, the inverse diagonal (null: unit), and the rows ordered by level
+// (host level boundaries; every row of a level is independent of the others).
+struct DevTri {
+  int* rp = nullptr;
+  int* ci = nullptr;
+  void* val = nullptr;
+  void* dinv = nullptr;
+  void* diag = nullptr;  // the diagonal itself (null: unit), for products with the factor
+  int* order = nullptr;
+  std::vector<int> lvl;
+};
+// Right ILU(0) preconditioner M = L U (ilu.cu): M^-1 = U^-1 L^-1, M^-H = L^-H U^-H
+struct Prec {
+  long long n = 0;
+  bool cplx = false;
+  DevTri L, U, UH, LH;
+  std::vector<double> factor;  // the factor values on A's pattern (host copy, for parity tests)
+  void* scratch[2] = {nullptr, nullptr};
+  size_t scratch_bytes = 0;
+};
+
 struct Mat {
   Ctx* ctx = nullptr;
   long long n = 0, nnz = 0, nnzH = 0;
@@ -62,6 +84,7 @@ struct Mat {
   int* brp = nullptr;
   int* bci = nullptr;
   void* bval = nullptr;
+  Prec* prec = nullptr;  // right ILU(0) preconditioner (srk_matrix_ilu0), or null
   // Balanced row order (irregular row lengths, e.g. config 5's power law): a copy
   // of the CSR with rows sorted by decreasing length (stable), so that the rows a
   // warp processes together have similar lengths; perm[l] = original row of
@@ -84,6 +107,14 @@ struct Mat {
 // builds m.srt / m.srtH when the row lengths are irregular (engine.cu)
 int build_balanced_order(Mat& m, bool adj, cudaStream_t st);
 void free_balanced_order(Mat& m);
+
+int build_ilu0(Mat& m, cudaStream_t st);  // 0, or 1 zero pivot / 2 out of memory / 3 CUDA error
+void free_prec(Prec* p);
+// Z = T^-1 R for one triangular factor (n x s row-major blocks; Z may alias R); returns
+// the number of launches (>= 0) or a negative CUDA error
+int launch_trsv(const DevTri& t, bool cplx, long long n, int s, const void* R, void* Z, const int* done, cudaStream_t st);
+// Z = T R (the factor itself, diagonal included; Z must not alias R)
+int launch_trimul(const DevTri& t, bool cplx, long long n, int s, const void* R, void* Z, cudaStream_t st);
 
 // reduction request: X = source (or the SpMM output), Y = source or external
 struct RQ {
@@ -146,6 +177,13 @@ struct Eng {
   // s x s Gram Y^H X on the FP64 tensor cores (gram_mma.cu), written to ws + woff
   int gram_full(const void* X, const void* Y, int s, int woff);
   int spmm_bsr(bool adj, const void* P, void* Q, int s, const std::vector<RQ>& reds);
+  // right-preconditioned operator A M^-1 (adjoint: M^-H A^H), M = the operator's ILU(0)
+  int spmm_prec(bool adj, const void* P, void* Q, int s, const std::vector<RQ>& reds);
+  // X = M^-1 Y (the iterate of the preconditioned system back to the original one)
+  int prec_solve(bool adj, const void* Y, void* X, int s);
+  // Y = M X
+  int prec_mul(const void* X, void* Y, int s);
+  bool raw = false;  // inside spmm_prec: the plain operator
   int grid_for(int cap, bool full, bool is_spmm, size_t smem, int nin) const;
 };
 

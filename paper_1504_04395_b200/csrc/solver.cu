@@ -126,7 +126,9 @@ int Solver::start(const void* Bd, const void* X0d) {
   e.err = 0;
   e.nlaunch = 0;
   if (X0d) {
-    cudaMemcpyAsync(X, X0d, (size_t)n * s * esz(), cudaMemcpyDeviceToDevice, st);
+    // right preconditioning iterates on Y = M X: Y0 = M X0 (then R0 = B - A M^-1 Y0 = B - A X0)
+    if (A && A->prec) e.prec_mul(X0d, X, s);
+    else cudaMemcpyAsync(X, X0d, (size_t)n * s * esz(), cudaMemcpyDeviceToDevice, st);
     e.spmm(false, X, tmp, s, {});
     e.upd(s, {B, tmp}, {OutSpec{R, {{0, C1()}, {1, Coef{CK_ONE, 0, 1, 0, 0}}}}},
           {RQ{RED_NORM2, O0, -1, nullptr, off[SL_R0N2]}});

@@ -1,0 +1,92 @@
+// trsv.cu — the level-scheduled triangular solves of the right ILU(0)
+// preconditioner on n x s row-major blocks:
+//   z_i = (r_i - sum_{j in T_i} t_ij z_j) * dinv_i        (dinv = 1 for a unit factor)
+// One launch per level (ilu.cu's schedule): every row of a level depends only on rows
+// of earlier levels, so a warp takes one row and its lanes the s columns (coalesced
+// row-major accesses, s <= 64 in two lane passes). Deterministic: each z_i is one
+// fixed-order sum.
+#include <cuda_runtime.h>
+
+#include "engine.h"
+
+namespace srk {
+
+namespace {
+
+template <typename T>
+__global__ void trsv_level_kernel(const int* __restrict__ order, int lo, int hi, const int* __restrict__ rp,
+                                  const int* __restrict__ ci, const T* __restrict__ val, const T* __restrict__ dinv,
+                                  const T* R, T* Z, int s, const int* done) {
+  if (done && *done) return;
+  const int w = (int)((blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  const int k = lo + w;
+  if (k >= hi) return;
+  const int i = __ldg(order + k);
+  const int b = __ldg(rp + i), e = __ldg(rp + i + 1);
+  for (int c = lane; c < s; c += 32) {
+    T acc = R[(size_t)i * s + c];
+    for (int p = b; p < e; ++p) {
+      const T t = __ldg(val + p);
+      const T z = Z[(size_t)__ldg(ci + p) * s + c];
+      acc = Ar<T>::sub(acc, Ar<T>::mul(t, z));
+    }
+    if (dinv) acc = Ar<T>::mul(acc, __ldg(dinv + i));
+    Z[(size_t)i * s + c] = acc;
+  }
+}
+
+template <typename T>
+__global__ void trimul_kernel(long long n, const int* __restrict__ rp, const int* __restrict__ ci, const T* __restrict__ val,
+                              const T* __restrict__ diag, const T* __restrict__ R, T* __restrict__ Z, int s) {
+  const long long i = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (i >= n) return;
+  const int b = __ldg(rp + i), e = __ldg(rp + i + 1);
+  for (int c = lane; c < s; c += 32) {
+    T acc = R[(size_t)i * s + c];
+    if (diag) acc = Ar<T>::mul(__ldg(diag + i), acc);
+    for (int p = b; p < e; ++p) acc = Ar<T>::add(acc, Ar<T>::mul(__ldg(val + p), R[(size_t)__ldg(ci + p) * s + c]));
+    Z[(size_t)i * s + c] = acc;
+  }
+}
+
+template <typename T>
+int run(const DevTri& t, long long n, int s, const void* R, void* Z, const int* done, cudaStream_t st) {
+  (void)n;
+  const int nlev = (int)t.lvl.size() - 1;
+  for (int l = 0; l < nlev; ++l) {
+    const int lo = t.lvl[l], hi = t.lvl[l + 1];
+    const int rows = hi - lo;
+    if (rows <= 0) continue;
+    const int warps_per_cta = 8;
+    const int grid = (rows + warps_per_cta - 1) / warps_per_cta;
+    // level 0 rows have no dependencies but still need Z = R * dinv: same kernel
+    trsv_level_kernel<T><<<grid, warps_per_cta * 32, 0, st>>>(
+        t.order, lo, hi, t.rp, t.ci, reinterpret_cast<const T*>(t.val), reinterpret_cast<const T*>(t.dinv),
+        reinterpret_cast<const T*>(R), reinterpret_cast<T*>(Z), s, done);
+  }
+  const int e = (int)cudaGetLastError();
+  return e ? -e : nlev;
+}
+
+}  // namespace
+
+int launch_trsv(const DevTri& t, bool cplx, long long n, int s, const void* R, void* Z, const int* done, cudaStream_t st) {
+  return cplx ? run<double2>(t, n, s, R, Z, done, st) : run<double>(t, n, s, R, Z, done, st);
+}
+
+int launch_trimul(const DevTri& t, bool cplx, long long n, int s, const void* R, void* Z, cudaStream_t st) {
+  const int grid = (int)((n + 7) / 8);
+  if (cplx)
+    trimul_kernel<double2><<<grid, 256, 0, st>>>(n, t.rp, t.ci, reinterpret_cast<const double2*>(t.val),
+                                                  reinterpret_cast<const double2*>(t.diag),
+                                                  reinterpret_cast<const double2*>(R), reinterpret_cast<double2*>(Z), s);
+  else
+    trimul_kernel<double><<<grid, 256, 0, st>>>(n, t.rp, t.ci, reinterpret_cast<const double*>(t.val),
+                                                reinterpret_cast<const double*>(t.diag), reinterpret_cast<const double*>(R),
+                                                reinterpret_cast<double*>(Z), s);
+  return (int)cudaGetLastError();
+}
+
+}  // namespace srk

@@ -5,7 +5,8 @@ Q of its thin QR, shadow R^0 = R0 (economic: the mean), stop at ||R||_F <= 1e-10
 ||R0||_F or 500 iterations, the final relative residual recomputed — for all 13
 methods on the GPU path. The final residuals are recomputed by scipy from the GPU's
 X. Table 2's block-method entries (no preconditioning) are printed beside ours:
-the paper reports "div." when the recomputed residual exceeds 1.
+the paper reports "div." when the recomputed residual exceeds 1. Then the same with
+the right no-fill ILU preconditioner (srk_matrix_ilu0; Table 2's lower half).
 
     python scripts/paper_grid.py r01     ->  profiles/r01_paper_grid.json
 """
@@ -25,6 +26,11 @@ import paper_1504_04395_b200 as srk  # noqa: E402
 import synth  # noqa: E402
 
 # Table 2 of the paper, no preconditioning: (#it, final ||R||; None = "div.")
+TABLE2_ILU = {  # lower half of Table 2: right no-fill ILU
+    "ex1": {"bl_bicg": (500, 0.04), "bl_bicg_rq": (163, 1e-10), "bl_bicgstab": (113, 3e-10), "bl_bicgstab_rq": (115, 3e-11)},
+    "ex2": {"bl_bicg": (28, 2e-10), "bl_bicg_rq": (28, 8e-11), "bl_bicgstab": (16, 4e-11), "bl_bicgstab_rq": (16, 3e-11)},
+    "ex3": {"bl_bicg": (50, 3e-10), "bl_bicg_rq": (50, 3e-10), "bl_bicgstab": (33, 6e-11), "bl_bicgstab_rq": (33, 5e-11)},
+}
 TABLE2 = {
     "ex1": {"bl_bicg": (500, None), "bl_bicg_rq": (500, 1e-8), "bl_bicgstab": (500, 0.093), "bl_bicgstab_rq": (355, 1e-10)},
     "ex2": {"bl_bicg": (500, None), "bl_bicg_rq": (500, None), "bl_bicgstab": (500, None), "bl_bicgstab_rq": (500, None)},
@@ -50,26 +56,32 @@ def main(tag):
         As = A.to_scipy()
         s = Q.shape[1]
         rows = {}
-        Mh = srk.Matrix.from_csr(A, need_adjoint=True)
         Bd = torch.from_numpy(np.ascontiguousarray(Q)).cuda()
-        for method in oracle.METHODS:
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            X, rep = srk.solve(Mh, Bd, method, tol=1e-10, maxit=500)
-            torch.cuda.synchronize()
-            dt = time.perf_counter() - t0
-            Xn = X.cpu().numpy()
-            res = float(np.linalg.norm(Q - As @ Xn) / np.linalg.norm(Q))
-            rows[method] = {"outcome": rep.outcome, "iterations": rep.iterations,
-                            "final_rel_residual": res, "matvec_cols_A": rep.matvec_cols_A,
-                            "matvec_cols_AH": rep.matvec_cols_AH, "seconds": dt}
-            if method in TABLE2[name]:
-                it, r = TABLE2[name][method]
-                rows[method]["paper"] = {"iterations": it, "final_rel_residual": r if r is not None else "div."}
-            p = rows[method].get("paper")
-            print(f"{name} {method:15s} {rep.outcome:10s} it {rep.iterations:4d}  ||R|| {res:9.2e}  "
-                  f"mv {rep.matvec_cols_A + rep.matvec_cols_AH:6d}  {dt * 1e3:7.1f} ms"
-                  + (f"   paper: it {p['iterations']}, ||R|| {p['final_rel_residual']}" if p else ""), flush=True)
+        for prec in ("none", "ilu0"):
+            Mh = srk.Matrix.from_csr(A, need_adjoint=True)
+            if prec == "ilu0":
+                Mh.ilu0()
+            table = TABLE2 if prec == "none" else TABLE2_ILU
+            for method in oracle.METHODS:
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                X, rep = srk.solve(Mh, Bd, method, tol=1e-10, maxit=500)
+                torch.cuda.synchronize()
+                dt = time.perf_counter() - t0
+                Xn = X.cpu().numpy()
+                res = float(np.linalg.norm(Q - As @ Xn) / np.linalg.norm(Q))
+                key = method if prec == "none" else method + "+ilu0"
+                rows[key] = {"outcome": rep.outcome, "iterations": rep.iterations,
+                             "final_rel_residual": res, "matvec_cols_A": rep.matvec_cols_A,
+                             "matvec_cols_AH": rep.matvec_cols_AH, "seconds": dt}
+                if method in table[name]:
+                    it, r = table[name][method]
+                    rows[key]["paper"] = {"iterations": it, "final_rel_residual": r if r is not None else "div."}
+                p = rows[key].get("paper")
+                print(f"{name} {key:20s} {rep.outcome:10s} it {rep.iterations:4d}  ||R|| {res:9.2e}  "
+                      f"mv {rep.matvec_cols_A + rep.matvec_cols_AH:6d}  {dt * 1e3:7.1f} ms"
+                      + (f"   paper: it {p['iterations']}, ||R|| {p['final_rel_residual']}" if p else ""), flush=True)
+            Mh.close()
         out["examples"][name] = {"n": A.n, "nnz": A.nnz, "s": s, "rho": s * A.n / A.nnz, "methods": rows}
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
     json.dump(out, open(os.path.join(ROOT, "profiles", f"{tag}_paper_grid.json"), "w"), indent=1)

@@ -1,0 +1,115 @@
+"""GPU parity of the right ILU(0) preconditioner (srk_matrix_ilu0, srk_precond_apply,
+preconditioned solves) against the oracle (oracle/precond.py)."""
+import numpy as np
+import pytest
+
+import oracle.precond as OP
+import synth
+from tests.gpu_util import rel, to_dev, to_np
+
+pytestmark = pytest.mark.gpu
+
+K = 20
+
+
+@pytest.fixture(scope="module")
+def srk():
+    import paper_1504_04395_b200 as srk
+    srk.load_library()
+    return srk
+
+
+def _ops():
+    return {
+        "cd2": synth.conv_diff_2d(14, (20.0, 10.0)),
+        "cd3c": synth.conv_diff_3d(6, (10.0, 5.0, 2.0), np.complex128, -0.1j),
+        "rand": synth.random_sparse(700, 6, seed=5, dominance=1.5),
+    }
+
+
+def _pattern_values(L, U, A):
+    import scipy.sparse as sp
+    Fl = ((L.tocsr() - sp.identity(A.shape[0], format="csr")) + U).tocsr()
+    A = A.tocsr()
+    A.sort_indices()
+    rows = np.repeat(np.arange(A.shape[0]), np.diff(A.indptr))
+    return np.asarray(Fl[rows, A.indices]).ravel()
+
+
+@pytest.mark.parametrize("name", ["cd2", "cd3c", "rand"])
+def test_ilu0_factor_matches_oracle(srk, name):
+    A = _ops()[name]
+    As = A.to_scipy()
+    M = srk.Matrix.from_csr(A, need_adjoint=True).ilu0()
+    L, U = OP.ilu0(As)
+    ref = _pattern_values(L, U, As)
+    got = M.ilu0_factor()
+    assert np.max(np.abs(got - ref)) <= 1e-12 * np.max(np.abs(ref))
+
+
+@pytest.mark.parametrize("name", ["cd2", "cd3c", "rand"])
+@pytest.mark.parametrize("s", [1, 4, 19])
+def test_precond_apply_matches_oracle(srk, name, s):
+    A = _ops()[name]
+    As = A.to_scipy()
+    cplx = np.iscomplexobj(A.values)
+    M = srk.Matrix.from_csr(A, need_adjoint=True).ilu0()
+    L, U = OP.ilu0(As)
+    P = synth.random_rhs(A.n, s, 9, cplx)
+    Z = to_np(srk.precond_apply(M, to_dev(P)))
+    assert rel(Z, OP.apply_inv(L, U, P)) < 1e-12
+    ZH = to_np(srk.precond_apply(M, to_dev(P), adjoint=True))
+    assert rel(ZH, OP.apply_inv_adj(L, U, P)) < 1e-12
+
+
+METHODS = ["egl_bicg", "gl_bicg", "li_bicg", "bl_bicg_rq", "egl_qmr", "bl_qmr", "li_bicgstab", "gl_bicgstab",
+           "bl_bicgstab", "bl_bicgstab_rq"]
+
+
+@pytest.mark.parametrize("method", METHODS)
+def test_preconditioned_lockstep_and_solve(srk, method):
+    """Right-preconditioned iterates X_k = M^-1 Y_k in lock step with the oracle on
+    Ex. 1's operator (30^2, s = 4, B -> Q), then the full solve to 1e-10."""
+    A, B = synth.paper_ex1(30)
+    Q, _ = np.linalg.qr(B)
+    Q = np.ascontiguousarray(Q)
+    As = A.to_scipy()
+    L, U = OP.ilu0(As)
+    a = OP.solve_right(method, As, Q, L, U, tol=1e-10, maxit=500, record=K, order="blas")
+    b = OP.solve_right(method, As, Q, L, U, tol=1e-10, maxit=500, record=K, order="seq")
+    d = [rel(x, y) for x, y in zip(a.Xs, b.Xs)]
+    env = np.maximum(1e-10, 100 * np.maximum.accumulate(d)) if d else np.array([])
+    M = srk.Matrix.from_csr(A, need_adjoint=srk.NEEDS_ADJOINT[method]).ilu0()
+    sv = srk.Solver(M, Q.shape[1], method, tol=1e-10, maxit=500, poll_every=1)
+    sv.start(to_dev(Q))
+    for k in range(min(K, a.iterations)):
+        st = sv.iterate(1)
+        x = to_np(sv.x())
+        if k < len(a.Xs):
+            assert rel(x, a.Xs[k]) <= env[k], (method, k + 1, rel(x, a.Xs[k]), env[k])
+        if st != 0:
+            break
+    sv.close()
+    X, rep = srk.solve(M, to_dev(Q), method, tol=1e-10, maxit=500)
+    assert rep.outcome == a.outcome, (rep.outcome, a.outcome)
+    if rep.outcome == "converged":
+        assert np.linalg.norm(Q - As @ to_np(X)) / np.linalg.norm(Q) <= 1e-10
+        assert abs(rep.iterations - a.iterations) <= max(2, 0.05 * a.iterations)
+
+
+def test_preconditioned_x0(srk):
+    """A nonzero X0 enters as Y0 = M X0: the solver's initial residual is B - A X0 and
+    its iterate maps back to X0; the solve from there converges."""
+    A, B = synth.paper_ex1(16)
+    As = A.to_scipy()
+    X0 = synth.random_rhs(A.n, B.shape[1], 11)
+    M = srk.Matrix.from_csr(A, need_adjoint=True).ilu0()
+    sv = srk.Solver(M, B.shape[1], "gl_bicgstab", tol=1e-10, maxit=200, poll_every=1)
+    sv.start(to_dev(B), to_dev(X0))
+    assert rel(to_np(sv.residual()), B - As @ X0) < 1e-12
+    assert rel(to_np(sv.x()), X0) < 1e-12
+    sv.iterate(200)
+    rep = sv.report()
+    assert rep.outcome == "converged"
+    assert np.linalg.norm(B - As @ to_np(sv.x())) <= 1e-10 * np.linalg.norm(B - As @ X0) * 1.01
+    sv.close()
