@@ -3,7 +3,7 @@
 // CSR on the host, times each variant with CUDA events (warm, 20 launches), and
 // prints the achieved algorithmic GB/s. Tuning aid only (not part of the product).
 //   nvcc -std=c++17 -O3 -gencode arch=compute_100a,code=sm_100a -I paper_1504_04395_b200/csrc \
-//        scripts/spmm_tune.cu -o scripts/spmm_tune
+//        -I scripts scripts/spmm_tune.cu -o scripts/spmm_tune -lcuda
 #include <cstdio>
 #include <cmath>
 #include <cstdlib>
@@ -11,7 +11,7 @@
 
 #include <cuda.h>
 
-#include "spmm_tma.cuh"
+#include "spmm_tma.cuh"  // scripts/ (experiment, not part of the library)
 
 using namespace srk;
 

@@ -5,7 +5,7 @@
 #include <cstdio>
 #include <cstdlib>
 
-#include "spmm_tma.cuh"
+#include "spmm_tma.cuh"  // scripts/ (experiment, not part of the library)
 
 using namespace srk;
 #define CK(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) { printf("%s: %s\n", #x, cudaGetErrorString(e_)); exit(1); } } while (0)
