@@ -149,6 +149,37 @@ def test_invalid_csr_rejected(srk):
         srk.Matrix(rp, torch.tensor([0, 5, 1], dtype=torch.int32), va)  # column out of range
 
 
+def test_limits_and_unsupported_combinations(srk):
+    """The documented error paths (include/srk.h): nnz >= 2^31 (int32 indices) is
+    refused before any allocation; s outside [1, 64]; block methods beyond s = 32;
+    BSR widths outside {4, 8, 12, 16}; methods needing A^H on an operator without it."""
+    import ctypes
+
+    import torch
+    ctx = srk.default_context()
+    csr = srk._Csr(1 << 20, 1 << 31, 1, 1, 1, 0)  # header only: never dereferenced
+    h = ctypes.c_void_p()
+    assert srk._lib.srk_matrix_create(ctx.h, ctypes.byref(csr), 0, ctypes.byref(h)) == -3  # SRK_EUNSUPPORTED
+    A = synth.conv_diff_2d(10)
+    M = srk.Matrix.from_csr(A, need_adjoint=False)
+    P = to_dev(synth.random_rhs(A.n, 65, 1))
+    with pytest.raises(srk.SrkError):
+        srk.spmm_block(M, P)
+    with pytest.raises(srk.SrkError):  # Gl-BiCG needs A^H
+        srk.Solver(M, 4, "gl_bicg")
+    M2 = srk.Matrix.from_csr(A, need_adjoint=True)
+    with pytest.raises(srk.SrkError):  # block methods: s <= 32
+        srk.Solver(M2, 33, "bl_bicg")
+    srk.Solver(M2, 32, "bl_bicg").close()
+    brp, bcol, blocks = synth.lattice_4d_bsr(3)
+    Mb = srk.Matrix.from_bsr(brp, bcol, blocks, unit_diag=True)
+    with pytest.raises(srk.SrkError):  # BSR widths
+        srk.Solver(Mb, 6, "gl_bicgstab")
+    with pytest.raises(srk.SrkError):  # no A^H for BSR operators
+        srk.Solver(Mb, 4, "gl_bicg")
+    del torch
+
+
 def test_full_size_config3_spmm_sampled(srk):
     """Config 3 at full size (n = 256^3, s = 16) in the bench launch configuration:
     sampled rows of A P against the oracle, and the fused trace against numpy."""
