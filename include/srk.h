@@ -217,6 +217,8 @@ typedef struct {
   int check_true_residual; /* confirm convergence with B - AX (reading G26; default 1) */
   int use_graph;       /* replay the iterations between two polls as one CUDA graph (default 1;
                           off while srk_solver_profile is on) */
+  int x0_zero;         /* X0 = 0 (the paper's protocol): X is output only — srk_solve does
+                          not read it and srk_solve_host does not copy it in (default 0) */
 } srk_opts;
 
 /* Full solve (a1-a7): B, X device n x s blocks; X holds X0 on entry and the

@@ -50,7 +50,7 @@ class _Csr(ctypes.Structure):
 class _Opts(ctypes.Structure):
     _fields_ = [("tol", ctypes.c_double), ("maxit", ctypes.c_int), ("poll_every", ctypes.c_int),
                 ("record_history", ctypes.c_int), ("check_true_residual", ctypes.c_int),
-                ("use_graph", ctypes.c_int)]
+                ("use_graph", ctypes.c_int), ("x0_zero", ctypes.c_int)]
 
 
 class _Halo(ctypes.Structure):
@@ -528,8 +528,8 @@ def _report(r: _Report) -> Report:
                   r.seconds, r.kernel_launches)
 
 
-def _opts(tol, maxit, poll_every=8, check_true_residual=True, use_graph=True):
-    return _Opts(float(tol), int(maxit), int(poll_every), 1, int(check_true_residual), int(use_graph))
+def _opts(tol, maxit, poll_every=8, check_true_residual=True, use_graph=True, x0_zero=False):
+    return _Opts(float(tol), int(maxit), int(poll_every), 1, int(check_true_residual), int(use_graph), int(x0_zero))
 
 
 class Solver:
@@ -620,8 +620,8 @@ def solve(A: Matrix, B, method: str = "egl_bicg", tol: float = 1e-8, maxit: int 
     (B: contiguous (n, s) float64/complex128 CUDA tensor)."""
     torch = _torch()
     n, s = B.shape
-    X = torch.zeros_like(B) if X0 is None else X0.clone()
-    o = _opts(tol, maxit, poll_every)
+    X = torch.empty_like(B) if X0 is None else X0.clone()
+    o = _opts(tol, maxit, poll_every, x0_zero=X0 is None)
     r = _Report()
     _check(_lib.srk_solve(A.ctx.h, A.h, _dev(B, "B"), _dev(X, "X"), s, METHOD_ID[method], ctypes.byref(o),
                           ctypes.byref(r)), "srk_solve")
@@ -629,9 +629,10 @@ def solve(A: Matrix, B, method: str = "egl_bicg", tol: float = 1e-8, maxit: int 
 
 
 def solve_host(A: Matrix, B: np.ndarray, method: str = "egl_bicg", tol: float = 1e-8, maxit: int = 2000,
-               X0: np.ndarray | None = None, poll_every: int = 8, inplace: bool = False):
+               X0: np.ndarray | None = None, poll_every: int = 8, inplace: bool = False, x0_zero: bool = False):
     """srk_solve_host: B, X in host memory (numpy, C-contiguous (n, s)). inplace=True
-    overwrites X0 with the solution (keeps a pinned X0 buffer pinned: no staging copy)."""
+    overwrites X0 with the solution (keeps a pinned X0 buffer pinned: no staging copy);
+    x0_zero=True (or X0=None) starts from X0 = 0 without copying X0 in."""
     B = np.ascontiguousarray(B)
     if X0 is None:
         X = np.zeros_like(B)
@@ -642,7 +643,7 @@ def solve_host(A: Matrix, B: np.ndarray, method: str = "egl_bicg", tol: float = 
     else:
         X = np.ascontiguousarray(X0).copy()
     n, s = B.shape
-    o = _opts(tol, maxit, poll_every)
+    o = _opts(tol, maxit, poll_every, x0_zero=x0_zero or X0 is None)
     r = _Report()
     _check(_lib.srk_solve_host(A.ctx.h, A.h, B.ctypes.data_as(ctypes.c_void_p), X.ctypes.data_as(ctypes.c_void_p),
                                s, METHOD_ID[method], ctypes.byref(o), ctypes.byref(r)), "srk_solve_host")

@@ -475,6 +475,7 @@ static void fill_opts(srk_opts* o, const srk_opts* in) {
   o->record_history = 1;
   o->check_true_residual = 1;
   o->use_graph = 1;
+  o->x0_zero = 0;
   if (in) {
     if (in->tol > 0) o->tol = in->tol;
     if (in->maxit > 0) o->maxit = in->maxit;
@@ -482,6 +483,7 @@ static void fill_opts(srk_opts* o, const srk_opts* in) {
     o->record_history = in->record_history;
     o->check_true_residual = in->check_true_residual;
     o->use_graph = in->use_graph;
+    o->x0_zero = in->x0_zero;
   }
 }
 
@@ -663,7 +665,7 @@ int srk_solve(srk_ctx* ctx, const srk_matrix* A, const void* B, void* X, int s, 
     ctx->cached_method = method;
     ctx->cached_opts = o;
   }
-  int r = srk_solver_start(h, B, X);
+  int r = srk_solver_start(h, B, o.x0_zero ? nullptr : X);
   if (!r) r = srk_solver_iterate(h, h->sv->o.maxit, nullptr);
   if (!r) r = srk_solver_get_x(h, X);
   if (!r && rep) r = srk_solver_report(h, rep);
@@ -687,7 +689,7 @@ int srk_solve_host(srk_ctx* ctx, const srk_matrix* A, const void* B_host, void* 
   }
   void *Bd = ctx->hbuf[0], *Xd = ctx->hbuf[1];
   cudaMemcpyAsync(Bd, B_host, bytes, cudaMemcpyHostToDevice, ctx->c.st);
-  cudaMemcpyAsync(Xd, X_host, bytes, cudaMemcpyHostToDevice, ctx->c.st);
+  if (!(opts && opts->x0_zero)) cudaMemcpyAsync(Xd, X_host, bytes, cudaMemcpyHostToDevice, ctx->c.st);
   int r = srk_solve(ctx, A, Bd, Xd, s, method, opts, rep);
   if (!r) {
     cudaMemcpyAsync(X_host, Xd, bytes, cudaMemcpyDeviceToHost, ctx->c.st);
