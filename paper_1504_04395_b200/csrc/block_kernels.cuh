@@ -192,7 +192,7 @@ __device__ void red_dispatch_flush(int mode, RedAcc<T, S, FC>& a, double* partia
 // zero value), so the CW*R loads of a step issue back to back.
 // ============================================================================
 template <typename T, int S, bool FC, int R, bool EX, int BC = 8, bool YPRE = true, int MINB = 2, int BATCH = 8, int PD = 1>
-__global__ void __launch_bounds__(256, FC ? 1 : MINB) spmm_kernel(SpmmArgs a) {
+__global__ void __launch_bounds__(256, FC ? (S <= 8 ? 2 : 1) : MINB) spmm_kernel(SpmmArgs a) {
   if (a.done && *a.done) return;
   using L = Lay<T, S>;
   extern __shared__ double smem[];
@@ -432,8 +432,11 @@ __global__ void __launch_bounds__(256, FC ? 1 : MINB) spmm_kernel(SpmmArgs a) {
 // ============================================================================
 // MINB = 4 (<= 64 registers, 32 warps per SM) measured best for every input count on
 // config-3 blocks (scripts/upd_tune.cu: 90-100% of the measured copy bandwidth)
-template <typename T, int S, bool FC, int NI, int R, bool EX, bool STREAM = false, int MINB = 4>
-__global__ void __launch_bounds__(256, FC ? 1 : MINB) upd_kernel(UpdArgs a) {
+// (complex rows and the s x s-coefficient instances need more registers: 2 CTAs/SM,
+// measured on config 2's block updates)
+template <typename T, int S, bool FC, int NI, int R, bool EX, bool STREAM = false,
+          int MINB = (FC || sizeof(T) == 16) ? 2 : 4>
+__global__ void __launch_bounds__(256, MINB) upd_kernel(UpdArgs a) {
   if (a.done && *a.done) return;
   using L = Lay<T, S>;
   constexpr int ND = Ar<T>::ND;

@@ -3,6 +3,7 @@
 // explicit A^H = conj(A)^T copy used by the BiCG/QMR families).
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 
 #include "engine.h"
 
@@ -162,9 +163,10 @@ int Eng::spmm(bool adj, const void* P, void* Q, int s, std::vector<RQ> reds) {
   if (A->bsr) return spmm_bsr(adj, P, Q, s, reds);
   if ((err = halo(adj, P, s))) return err;
   const int cap = cap_for(s);
-  // s x s Grams wider than the in-kernel epilogue: Y^H Q on the tensor cores afterwards
+  // s x s Grams of 8 columns and more: Y^H Q on the tensor cores afterwards (the FMA
+  // epilogue's s x s accumulators cost the SpMM more than the extra pass: config 2)
   std::vector<RQ> wide;
-  if (!full_red_supported(cplx, cap)) {
+  if (!full_red_supported(cplx, cap) || s >= 8) {
     for (auto it = reds.begin(); it != reds.end();)
       if (it->mode == RED_FULL) {
         wide.push_back(*it);
@@ -254,7 +256,14 @@ int Eng::upd(int s, std::vector<const void*> in, std::vector<OutSpec> outs, std:
     int woff;
   };
   std::vector<Wide> pre, post;
-  if (!full_red_supported(cplx, cap)) {
+  // updates with s x s coefficients run on the tensor cores (blk_mma.cu); their s x s
+  // Grams then go to the tensor-core Gram kernel as well
+  bool full_coef = false;
+  for (auto& o : outs)
+    for (auto& t : o.t) full_coef |= (t.c.kind == CK_FULL);
+  static const bool no_mma = getenv("SRK_NO_DMMA_UPDATE") != nullptr;  // A/B switch for measurements
+  const bool use_mma = full_coef && !no_mma && upd_mma_width(s * (cplx ? 2 : 1)) > 0;
+  if (!full_red_supported(cplx, cap) || use_mma) {
     auto ptr = [&](int src) -> const void* {
       if (src >= 0 && src < (int)in.size()) return in[src];
       if (src >= SRC_OUT && src - SRC_OUT < (int)outs.size()) {
@@ -343,6 +352,29 @@ int Eng::upd(int s, std::vector<const void*> in, std::vector<OutSpec> outs, std:
   a.vec = cplx ? 1 : (s % 2 == 0);
   a.done = done;
   const size_t esz = cplx ? 16 : 8;
+  if (use_mma) {
+    int nterm = 0;
+    for (int o = 0; o < MAX_OUT; ++o)
+      for (int q = 0; q < MAX_SRC; ++q) a.cslot[o][q] = a.cf[o][q].kind == CK_NONE ? -1 : nterm++;
+    const int w = s * (cplx ? 2 : 1);
+    static int occ_mma[3] = {0, 0, 0};
+    int& occ = occ_mma[upd_mma_width(w) == 8 ? 0 : (upd_mma_width(w) == 16 ? 1 : 2)];
+    if (occ == 0) occ = std::max(1, launch_upd_mma(a, cplx, MAX_OUT * 2, -1, nullptr));
+    const long long need = (n + 63) / 64;  // 8 warps x 8 rows per CTA step
+    const int grid = (int)std::max<long long>(1, std::min<long long>(need, (long long)c->nsm * occ));
+    if ((err = c->ensure_partials((size_t)grid * a.pstride))) return err;
+    a.partials = c->partials;
+    nlaunch++;
+    if (prof) {
+      int nw = 0;
+      for (auto& o : outs) nw += o.ptr ? 1 : 0;
+      prof->begin(PT_UPD, c->st, 16 * a.nin + a.nout, (double)n * s * esz * (a.nin + nw));
+    }
+    err = launch_upd_mma(a, cplx, nterm, grid, c->st);
+    if (prof) prof->end(c->st);
+    if (err) return err;
+    return err = finish_reds(*this, reds, poffs, s, grid, a.pstride);
+  }
   const size_t smem = (size_t)cslot * esz + (size_t)8 * maxlen * sizeof(double);
   const int grid = grid_for(cap, full, false, 48 * 1024, a.nin);  // occupancy at a fixed smem budget (deterministic grid)
   if ((err = c->ensure_partials((size_t)grid * a.pstride))) return err;
@@ -504,7 +536,7 @@ int Eng::gram_full(const void* X, const void* Y, int s, int woff) {
   g.pstride = len;
   g.done = done;
   nlaunch++;
-  if (prof) prof->begin(PT_UPD, c->st, 16 * 2 + 0, 2.0 * (double)n * s * (cplx ? 16 : 8));
+  if (prof) prof->begin(PT_UPD, c->st, 16 * (X == Y ? 1 : 2) + 0, (X == Y ? 1.0 : 2.0) * (double)n * s * (cplx ? 16 : 8));
   err = launch_gram_mma(g, grid, c->st);
   if (prof) prof->end(c->st);
   if (err) return err;

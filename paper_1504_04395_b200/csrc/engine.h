@@ -21,6 +21,10 @@ int launch_upd(bool cplx, int cap, bool full, const UpdArgs& a, int grid, int bl
 int launch_fin(const FinArgs& a, cudaStream_t st);
 int launch_gram_mma(const GramArgs& g, int grid, cudaStream_t st);
 int launch_bsr(const BsrArgs& a, int s, int grid, cudaStream_t st);
+// block updates with s x s coefficients on the FP64 tensor cores (blk_mma.cu)
+int upd_mma_width(int w);
+size_t upd_mma_smem(int w, int nterm);
+int launch_upd_mma(const UpdArgs& a, bool cplx, int nterm, int grid, cudaStream_t st);
 bool bsr_supported(int bs, bool cplx, int s);
 
 int gram_mma_chunks(long long n);

@@ -10,7 +10,7 @@
 //   G[j][k] = (B[2j][2k] + B[2j+1][2k+1]) + i (B[2j][2k+1] - B[2j+1][2k]),
 // so one real kernel serves both dtypes (real width w = s or 2s <= 128).
 //
-// Each CTA (8 warps, persistent, one per SM) streams chunks of KC consecutive
+// Each CTA (8 warps, 2 per SM) streams chunks of KC consecutive
 // rows of Y and X (contiguous in the row-major layout) into an NBUF-deep
 // shared-memory ring with cp.async, and every warp accumulates its TM x TN
 // grid of 8 x 8 output tiles in registers over the CTA's rows (k = 4 rows per
@@ -27,7 +27,7 @@ namespace srk {
 
 namespace {
 
-constexpr int KC = 32;   // rows per chunk
+constexpr int KCMIN = 32;  // rows per chunk (at least; narrow blocks take longer chunks)
 constexpr int PADW = 8;  // smem row padding (doubles): rows k and k+1 land 16 banks apart
 
 __device__ __forceinline__ void cp_async8(double* smem, const double* gmem) {
@@ -55,6 +55,7 @@ struct GCfg {
   static constexpr int WN = NT < 4 ? NT : 4;
   static constexpr int TM = NT / WM, TN = NT / WN;
   static constexpr int LDS = W + PADW;        // smem row stride (doubles)
+  static constexpr int KC = W <= 16 ? 2 * KCMIN : KCMIN;  // rows per chunk: >= 24 KB in flight per stage
   static constexpr int BUF = 2 * KC * LDS;    // Y chunk + X chunk (doubles)
   static constexpr int NBUF = W <= 64 ? 3 : 2;
   static constexpr int SMEM = NBUF * BUF * 8;
@@ -69,19 +70,21 @@ __global__ void __launch_bounds__(256, W <= 64 ? 2 : 1) gram_mma_kernel(GramArgs
   const int wm = warp / C::WN, wn = warp % C::WN;
   const long long n = g.n;
   const int w = g.w;
-  const long long nchunk = (n + KC - 1) / KC;
+  const long long nchunk = (n + C::KC - 1) / C::KC;
   const bool vec = (w % 2) == 0;  // 16-byte rows
+  const bool same = g.X == g.Y;   // a block's own Gram (CholQR): one copy serves both operands
+  const int nops = same ? 1 : 2;
 
   // stage chunk c of Y and X into buffer b (columns >= w and rows >= n are zero)
   auto stage = [&](long long c, int b) {
     double* ys = gsm + (size_t)b * C::BUF;
-    double* xs = ys + KC * C::LDS;
-    const long long r0 = c * KC;
+    double* xs = ys + C::KC * C::LDS;
+    const long long r0 = c * C::KC;
     if (vec) {
       const int pairs = W / 2;
-      for (int t = threadIdx.x; t < 2 * KC * pairs; t += blockDim.x) {
-        const int which = t / (KC * pairs);
-        const int rem = t % (KC * pairs);
+      for (int t = threadIdx.x; t < nops * C::KC * pairs; t += blockDim.x) {
+        const int which = t / (C::KC * pairs);
+        const int rem = t % (C::KC * pairs);
         const int k = rem / pairs, cp = rem % pairs;
         double* dst = (which ? xs : ys) + k * C::LDS + 2 * cp;
         const long long r = r0 + k;
@@ -93,9 +96,9 @@ __global__ void __launch_bounds__(256, W <= 64 ? 2 : 1) gram_mma_kernel(GramArgs
         }
       }
     } else {
-      for (int t = threadIdx.x; t < 2 * KC * W; t += blockDim.x) {
-        const int which = t / (KC * W);
-        const int rem = t % (KC * W);
+      for (int t = threadIdx.x; t < nops * C::KC * W; t += blockDim.x) {
+        const int which = t / (C::KC * W);
+        const int rem = t % (C::KC * W);
         const int k = rem / W, col = rem % W;
         double* dst = (which ? xs : ys) + k * C::LDS + col;
         const long long r = r0 + k;
@@ -131,9 +134,9 @@ __global__ void __launch_bounds__(256, W <= 64 ? 2 : 1) gram_mma_kernel(GramArgs
     cp_wait<C::NBUF - 1>();
     __syncthreads();
     const double* ys = gsm + (size_t)(it % C::NBUF) * C::BUF;
-    const double* xs = ys + KC * C::LDS;
+    const double* xs = same ? ys : ys + C::KC * C::LDS;
 #pragma unroll
-    for (int k0 = 0; k0 < KC; k0 += 4) {
+    for (int k0 = 0; k0 < C::KC; k0 += 4) {
       if (warp >= C::WM * C::WN) break;
       double a[C::TM], bb[C::TN];
 #pragma unroll
@@ -203,6 +206,6 @@ int launch_gram_mma(const GramArgs& g, int grid, cudaStream_t st) {
   return (int)cudaErrorInvalidValue;
 }
 
-int gram_mma_chunks(long long n) { return (int)std::min<long long>((n + KC - 1) / KC, 1LL << 30); }
+int gram_mma_chunks(long long n) { return (int)std::min<long long>((n + KCMIN - 1) / KCMIN, 1LL << 30); }
 
 }  // namespace srk
