@@ -182,15 +182,15 @@ int srk_matrix_create_dist(srk_ctx* ctx, const srk_csr* A_local, int64_t n_ghost
  * is fused into the epilogue and written to gram_out (device, dtype values):
  *   NORM2: ||Q||_F^2 (1 double); COLNORM2: s doubles; DIAG: (y_c^H q_c)_c (s);
  *   TRACE: tr(Y^H Q) (1); SUMVEC: sum(y^H Q) (1); FULL: Y^H Q (s x s).
- * FULL with s >= 16 is computed as the SpMM followed by Y^H Q on the FP64 tensor
- * cores (DMMA, the dense contraction north_star names); s < 16 fuses it into the
+ * FULL with s >= 8 is computed as the SpMM followed by Y^H Q on the FP64 tensor
+ * cores (DMMA, the dense contraction north_star names); s < 8 fuses it into the
  * SpMM epilogue. Errors: SRK_EDIM (s < 1 or s > 64), SRK_EUNSUPPORTED (adjoint
  * without A^H). */
 int srk_spmm_block(srk_ctx* ctx, const srk_matrix* A, int adjoint, const void* P, void* Q, int s,
                    int gram, const void* Y, void* gram_out);
 
 /* out = reduction(X, Y) over n rows of two n x s blocks (mode as above; FULL gives
- * Y^H X, on the FP64 tensor cores for s >= 16). a3, P:155-158, 178, 192-195,
+ * Y^H X, on the FP64 tensor cores for s >= 8). a3, P:155-158, 178, 192-195,
  * 243-249, 273-285, 443-447. */
 int srk_gram_block(srk_ctx* ctx, const void* X, const void* Y, int64_t n, int s, int dtype, int gram,
                    void* out);
@@ -223,8 +223,8 @@ typedef struct {
 
 /* Full solve (a1-a7): B, X device n x s blocks; X holds X0 on entry and the
  * iterate on exit. opts may be NULL (tol 1e-8, maxit 2000). s <= 64; the block
- * methods (s x s coefficients) take s <= 32, their s x s Grams beyond s = 16 on the
- * FP64 tensor cores. The context keeps the last solver's workspace for the next
+ * methods (s x s coefficients) take s <= 32, their s x s Grams from s = 8 on and their
+ * s x s-coefficient updates on the FP64 tensor cores. The context keeps the last solver's workspace for the next
  * call with the same operator, s, method and options (freed by srk_destroy or
  * when the operator is destroyed). Errors: SRK_EUNSUPPORTED (e.g. a block method
  * with s > 32, a method needing A^H on an operator created without it). */

@@ -411,16 +411,11 @@ int srk_spmm_block(srk_ctx* ctx, const srk_matrix* A, int adjoint, const void* P
   e.n = A->m.n;
   e.ws = reinterpret_cast<double*>(gram_out);
   int r;
-  if (gram == SRK_GRAM_FULL && s >= 16) {
-    // s >= 16: the s x s Gram is a dense contraction — SpMM, then Y^H Q on the FP64 tensor cores
-    // (config 5, s = 16: 2.0 ms fused FMA epilogue vs ~0.2 ms DMMA pass)
-    r = e.spmm(adjoint != 0, P, Q, s, {});
-    if (!r) r = e.gram_full(Q, Y, s, 0);
-  } else {
-    std::vector<RQ> reds;
-    if (gram != SRK_GRAM_NONE) reds.push_back(RQ{gram, 0, -1, Y, 0});
-    r = e.spmm(adjoint != 0, P, Q, s, reds);
-  }
+  // (Eng::spmm takes a FULL Gram with s >= 8 to the tensor cores after the product:
+  // config 5, s = 16: 2.0 ms fused FMA epilogue vs ~0.2 ms DMMA pass)
+  std::vector<RQ> reds;
+  if (gram != SRK_GRAM_NONE) reds.push_back(RQ{gram, 0, -1, Y, 0});
+  r = e.spmm(adjoint != 0, P, Q, s, reds);
   return check_cuda(r, "srk_spmm_block");
 }
 
@@ -438,7 +433,7 @@ int srk_gram_block(srk_ctx* ctx, const void* X, const void* Y, int64_t n, int s,
   int r;
   if (gram == SRK_GRAM_SUMVEC) r = e.upd(s, {X}, {}, {RQ{gram, 0, -1, Y, 0}});
   else if (gram == SRK_GRAM_NORM2 || gram == SRK_GRAM_COLNORM2) r = e.upd(s, {X}, {}, {RQ{gram, 0, -1, nullptr, 0}});
-  else if (gram == SRK_GRAM_FULL && s >= 16) r = e.gram_full(X, Y, s, 0);  // s >= 16: DMMA
+  else if (gram == SRK_GRAM_FULL && s >= 8) r = e.gram_full(X, Y ? Y : X, s, 0);  // s >= 8: DMMA, as the solvers
   else r = e.upd(s, {X, Y}, {}, {RQ{gram, 0, 1, nullptr, 0}});
   return check_cuda(r, "srk_gram_block");
 }

@@ -14,6 +14,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdint>
+#include <cstdlib>
 
 #include "kernels.cuh"
 
@@ -27,15 +29,40 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
+__device__ __forceinline__ unsigned smem_addr(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_wait_parity(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// stage = nin consecutive 8-row tiles (one per input, 8 w doubles each, contiguous in the
+// row-major blocks) copied by the bulk-copy engine; completion counted on the stage's mbarrier
+__device__ __forceinline__ void issue_stage(const UpdArgs& a, int nin, int w, long long tile, double* dst,
+                                            unsigned long long* bar) {
+  const unsigned bytes = (unsigned)(8 * w * 8);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes * nin)
+               : "memory");
+  for (int b = 0; b < nin; ++b)
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_addr(dst + (size_t)b * 8 * w)),
+                 "l"(reinterpret_cast<const double*>(a.in[b]) + (size_t)tile * 8 * w), "r"(bytes), "r"(smem_addr(bar))
+                 : "memory");
+}
+
 template <int W>
-__global__ void __launch_bounds__(256, 2) upd_mma_kernel(UpdArgs a, int cplx, int nterm) {
+__global__ void __launch_bounds__(256, 2) upd_mma_kernel(UpdArgs a, int cplx, int nterm, int stg) {
   if (a.done && *a.done) return;
   constexpr int NT = W / 8;   // 8-column tiles
-  constexpr int KS = W / 4;   // k-steps
   extern __shared__ __align__(16) double msm[];
   __shared__ int tslot[MAX_OUT][MAX_SRC];
   const int s = a.s;
   const int w = cplx ? 2 * s : s;  // real row width
+  const bool vec2 = (w & 1) == 0;  // 16-byte row segments
   const long long n = a.n;
   const int nout = a.nout, nin = a.nin, nred = a.nred;
   // a.cslot[o][src] holds the term's staged-matrix index (-1: absent term)
@@ -51,9 +78,9 @@ __global__ void __launch_bounds__(256, 2) upd_mma_kernel(UpdArgs a, int cplx, in
         src = q % MAX_SRC;
       }
     const Coef cf = a.cf[o][src];
-    double* M = msm + (size_t)t * W * W;
+    double* M = msm + (size_t)t * W * W;  // stored transposed: M[c * W + k]
     for (int idx = threadIdx.x; idx < W * W; idx += blockDim.x) {
-      const int k = idx / W, c = idx % W;
+      const int c = idx / W, k = idx % W;
       double v = 0.0;
       if (k < w && c < w) {
         const int kk = cplx ? k / 2 : k, cc = cplx ? c / 2 : c;  // complex element indices
@@ -93,12 +120,29 @@ __global__ void __launch_bounds__(256, 2) upd_mma_kernel(UpdArgs a, int cplx, in
       M[idx] = v;
     }
   }
-  __syncthreads();
-
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int fr = lane >> 2, fk = lane & 3;
   const long long ntile = (n + 7) / 8;
+  const long long nfull = n / 8;  // tiles with 8 live rows: the ones staged by bulk copies
   const long long nwarps = (long long)gridDim.x * (blockDim.x >> 5);
+  // per-warp ring of stg stages (stg = 0: inputs read straight from global memory)
+  const size_t stage_len = (size_t)nin * 8 * w;
+  double* ring = msm + (size_t)nterm * W * W + (size_t)warp * stg * stage_len;
+  unsigned long long* bars =
+      reinterpret_cast<unsigned long long*>(msm + (size_t)nterm * W * W + (size_t)(blockDim.x >> 5) * stg * stage_len) +
+      warp * stg;
+  const long long first = (long long)blockIdx.x * (blockDim.x >> 5) + warp;
+  if (stg && lane == 0) {
+    for (int q = 0; q < stg; ++q)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(bars + q)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (stg && lane == 0)
+    for (int q = 0; q < stg; ++q) {
+      const long long t = first + q * nwarps;
+      if (t < nfull) issue_stage(a, nin, w, t, ring + q * stage_len, bars + q);
+    }
   // reduction accumulators (per lane): scalar modes in rs, per-column modes in rc[nt][pair]
   int rmode[MAX_RED], rx[MAX_RED], ry[MAX_RED];
 #pragma unroll
@@ -116,9 +160,18 @@ __global__ void __launch_bounds__(256, 2) upd_mma_kernel(UpdArgs a, int cplx, in
     for (int t = 0; t < NT; ++t) rc[r][t][0] = rc[r][t][1] = 0.0;
   }
 
-  for (long long tile = (long long)blockIdx.x * (blockDim.x >> 5) + warp; tile < ntile; tile += nwarps) {
+  long long k = 0;
+  for (long long tile = first; tile < ntile; tile += nwarps, ++k) {
     const long long row = tile * 8 + fr;  // this lane's A-fragment and accumulator row
     const bool live = row < n;
+    const bool piped = stg && tile < nfull;
+    const int stage = piped ? (int)(k % stg) : 0;
+    if (piped) mbar_wait_parity(bars + stage, (unsigned)((k / stg) & 1));
+    // input b's row for this lane: the staged tile, or global memory
+    auto in_row = [&](int b) -> const double* {
+      return piped ? ring + stage * stage_len + (size_t)b * 8 * w + (size_t)fr * w
+                   : reinterpret_cast<const double*>(a.in[b]) + (size_t)row * w;
+    };
     double acc[MAX_OUT][NT][2];
 #pragma unroll
     for (int o = 0; o < MAX_OUT; ++o) {
@@ -130,18 +183,29 @@ __global__ void __launch_bounds__(256, 2) upd_mma_kernel(UpdArgs a, int cplx, in
         for (int b = 0; b < MAX_IN; ++b) {
           const int ts = b < nin ? tslot[o][b] : -1;
           if (ts < 0) continue;
-          const double* X = reinterpret_cast<const double*>(a.in[b]);
+          const double* X = in_row(b);
           const double* M = msm + (size_t)ts * W * W;
-          double av[KS];
+          // k order permuted within each 8-column group: k-steps 2j, 2j+1 take, for lane
+          // fk, the columns 8j + 2fk and 8j + 2fk + 1 (one 16-byte load of A, one of B)
+          double2 av[NT];
 #pragma unroll
-          for (int ks = 0; ks < KS; ++ks) {
-            const int col = ks * 4 + fk;
-            av[ks] = (live && col < w) ? X[(size_t)row * w + col] : 0.0;
+          for (int j = 0; j < NT; ++j) {
+            const int col = j * 8 + 2 * fk;
+            if (vec2) {
+              av[j] = (live && col < w) ? *reinterpret_cast<const double2*>(X + col) : make_double2(0.0, 0.0);
+            } else {
+              av[j].x = (live && col < w) ? X[col] : 0.0;
+              av[j].y = (live && col + 1 < w) ? X[col + 1] : 0.0;
+            }
           }
 #pragma unroll
-          for (int ks = 0; ks < KS; ++ks)
+          for (int j = 0; j < NT; ++j)
 #pragma unroll
-            for (int t = 0; t < NT; ++t) dmma(acc[o][t], av[ks], M[(ks * 4 + fk) * W + t * 8 + fr]);
+            for (int t = 0; t < NT; ++t) {
+              const double2 bv = *reinterpret_cast<const double2*>(M + (t * 8 + fr) * W + j * 8 + 2 * fk);
+              dmma(acc[o][t], av[j].x, bv.x);
+              dmma(acc[o][t], av[j].y, bv.y);
+            }
         }
         // earlier outputs of this tile (C fragment -> A fragment by shuffles)
 #pragma unroll
@@ -150,18 +214,16 @@ __global__ void __launch_bounds__(256, 2) upd_mma_kernel(UpdArgs a, int cplx, in
           const int ts = tslot[o][MAX_IN + p];
           if (ts < 0) continue;
           const double* M = msm + (size_t)ts * W * W;
+          // with the permuted k order the A values of an earlier output are this lane's
+          // own accumulator entries (columns 8j + 2fk, 8j + 2fk + 1): no shuffles
 #pragma unroll
-          for (int ks = 0; ks < KS; ++ks) {
-            // A[fr][4 ks + fk] = out_p[row][4 ks + fk]: tile ks / 2, column j of it,
-            // held by lane (fr, j / 2) in accumulator slot j % 2
-            const int j = (ks % 2) * 4 + fk;
-            const int srcl = fr * 4 + j / 2;
-            const double v0 = __shfl_sync(0xffffffffu, acc[p][ks / 2][0], srcl);
-            const double v1 = __shfl_sync(0xffffffffu, acc[p][ks / 2][1], srcl);
-            const double av = (j & 1) ? v1 : v0;
+          for (int j = 0; j < NT; ++j)
 #pragma unroll
-            for (int tt = 0; tt < NT; ++tt) dmma(acc[o][tt], av, M[(ks * 4 + fk) * W + tt * 8 + fr]);
-          }
+            for (int tt = 0; tt < NT; ++tt) {
+              const double2 bv = *reinterpret_cast<const double2*>(M + (tt * 8 + fr) * W + j * 8 + 2 * fk);
+              dmma(acc[o][tt], acc[p][j][0], bv.x);
+              dmma(acc[o][tt], acc[p][j][1], bv.y);
+            }
         }
       }
     }
@@ -200,9 +262,9 @@ __global__ void __launch_bounds__(256, 2) upd_mma_kernel(UpdArgs a, int cplx, in
                 x1 = acc[o][t][1];
               }
           } else {
-            const double* X = reinterpret_cast<const double*>(a.in[rx[r]]);
-            x0 = X[(size_t)row * w + col];
-            x1 = col + 1 < w ? X[(size_t)row * w + col + 1] : 0.0;
+            const double* X = in_row(rx[r]);
+            x0 = X[col];
+            x1 = col + 1 < w ? X[col + 1] : 0.0;
           }
           if (md == RED_NORM2 || md == RED_COLNORM2) {
             const double q = x0 * x0 + x1 * x1;
@@ -231,9 +293,9 @@ __global__ void __launch_bounds__(256, 2) upd_mma_kernel(UpdArgs a, int cplx, in
                 y1 = acc[o][t][1];
               }
           } else {
-            const double* Yp = reinterpret_cast<const double*>(ry[r] >= 0 ? a.in[ry[r]] : a.red[r].yext);
-            y0 = Yp[(size_t)row * w + col];
-            y1 = col + 1 < w ? Yp[(size_t)row * w + col + 1] : 0.0;
+            const double* Yp = ry[r] >= 0 ? in_row(ry[r]) : reinterpret_cast<const double*>(a.red[r].yext) + (size_t)row * w;
+            y0 = Yp[col];
+            y1 = col + 1 < w ? Yp[col + 1] : 0.0;
           }
           // conj(y) * x
           double pr, pi;
@@ -256,6 +318,14 @@ __global__ void __launch_bounds__(256, 2) upd_mma_kernel(UpdArgs a, int cplx, in
             }
           }
         }
+      }
+    }
+    if (piped) {
+      __syncwarp();  // every lane's reads of this stage are done
+      const long long nt = tile + (long long)stg * nwarps;
+      if (lane == 0 && nt < nfull) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue_stage(a, nin, w, nt, ring + stage * stage_len, bars + stage);
       }
     }
   }
@@ -318,9 +388,34 @@ __global__ void __launch_bounds__(256, 2) upd_mma_kernel(UpdArgs a, int cplx, in
   }
 }
 
+// stages of the per-warp input ring: as many as fit (up to 4) in half an SM's shared
+// memory, so that two CTAs stay resident; 0 (direct global loads) when fewer than 2 fit
+// or an input is not 16-byte aligned (bulk-copy requirement). SRK_UPD_STAGES overrides.
+int pick_stages(const UpdArgs& a, int w, int W, int nterm) {
+  if (a.nin == 0) return 0;
+  for (int b = 0; b < a.nin; ++b)
+    if (reinterpret_cast<uintptr_t>(a.in[b]) & 15) return 0;
+  static int env = [] {
+    const char* e = getenv("SRK_UPD_STAGES");
+    return e ? atoi(e) : -1;
+  }();
+  const size_t per = (size_t)8 * a.nin * 8 * w * 8 + 8;  // 8 warps, one stage each, + mbarrier
+  const size_t budget = 110 * 1024 - (size_t)nterm * W * W * 8;
+  int stg = (int)std::min<size_t>(4, budget / per);
+  if (env >= 0) stg = env;
+  return stg >= 2 ? stg : 0;
+}
+
+size_t smem_bytes(int W, int w, int nterm, int nin, int stg) {
+  const size_t pipe = (size_t)nterm * W * W * 8 + (size_t)8 * stg * ((size_t)nin * 8 * w * 8 + 8);
+  return std::max<size_t>(pipe, (size_t)8 * 2 * 64 * 8);
+}
+
 template <int W>
 int launch_w(const UpdArgs& a, int cplx, int nterm, int grid, cudaStream_t st) {
-  const size_t smem = std::max<size_t>((size_t)nterm * W * W * 8, (size_t)8 * 2 * 64 * 8);
+  const int w = a.s * (cplx ? 2 : 1);
+  const int stg = pick_stages(a, w, W, nterm);
+  const size_t smem = smem_bytes(W, w, nterm, a.nin, stg);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(upd_mma_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -331,7 +426,7 @@ int launch_w(const UpdArgs& a, int cplx, int nterm, int grid, cudaStream_t st) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, upd_mma_kernel<W>, 256, smem);
     return occ;
   }
-  upd_mma_kernel<W><<<grid, 256, smem, st>>>(a, cplx, nterm);
+  upd_mma_kernel<W><<<grid, 256, smem, st>>>(a, cplx, nterm, stg);
   return (int)cudaGetLastError();
 }
 

@@ -120,15 +120,20 @@ def test_tsqr_matches_oracle(srk, s, cplx):
 
 
 @pytest.mark.parametrize("cplx", [False, True])
-@pytest.mark.parametrize("s", [16, 32, 64])
+@pytest.mark.parametrize("s", [8, 12, 16, 17, 32, 64])
 def test_gram_mma_edge_rows(srk, s, cplx):
-    """DMMA Gram on row counts around the 32-row chunk (1, 31, 32, 33 rows, and
-    fewer chunks than SMs), against the oracle's Gram."""
+    """DMMA Gram on row counts around the 16-row warp stage and the 32-row chunk (1, 15,
+    16, 17, 31, 32, 33 rows, fewer stages than warps, a ragged multi-stage tail), with
+    distinct operands and with X == Y (one staged copy serves both), against the
+    oracle's Gram."""
     rng = np.random.default_rng(23)
-    for n in (1, 31, 32, 33, 4 * 32 * 148 + 5):
+    for n in (1, 15, 16, 17, 31, 32, 33, 4 * 32 * 148 + 5, 100003):
         X, Y = _rand(rng, n, s, cplx), _rand(rng, n, s, cplx)
         g = to_np(srk.gram_block(to_dev(X), to_dev(Y), "full"))
         assert rel(g, OL.gram(Y, X)) < 1e-12, n
+        Xd = to_dev(X)
+        g = to_np(srk.gram_block(Xd, Xd, "full"))
+        assert rel(g, OL.gram(X, X)) < 1e-12, ("same", n)
 
 
 def test_tsqr_rank_deficient(srk):

@@ -47,12 +47,20 @@ KNOWN_ILU = {
 }
 
 
+# Ex. 1's Bl-BiCGStab-rQ converges only after a long plateau, and where it leaves the
+# plateau depends on rounding: the oracle takes 394 iterations on Q, 349 and 352 on Q with
+# its columns reversed / pair-swapped (the same iterates in exact arithmetic), the GPU
+# 356 (CUDA-core updates) or 428 (tensor-core updates); the paper 355. Only "converged
+# within 500" is asserted for it.
+ROUNDING_SENSITIVE = {("ex1", "bl_bicgstab_rq")}
+
+
 def _check(ex, method, it, res, outcome, iters):
     conv = outcome == "converged"
     if (ex, method) in KNOWN:
         pytest.xfail("Ex. 3 plain Bl-BiCGStab: [Jbilou05]'s variant in the paper vs App. A.4 here (DESIGN.md §3)")
     assert conv == _paper_converged(it, res), (ex, method, outcome, iters, it, res)
-    if conv:
+    if conv and (ex, method) not in ROUNDING_SENSITIVE:
         assert abs(iters - it) <= 0.05 * it, (ex, method, iters, it)
 
 
@@ -107,7 +115,4 @@ def test_table2_oracle(row):
     ex, method, it, res = row
     A, Q = _problem(ex)
     r = oracle.solve(method, A.to_scipy(), Q, tol=1e-10, maxit=500, record=0)
-    if ex == "ex1":  # Ex. 1's Bl-BiCGStab-rQ is rounding-sensitive: 394 (oracle) / 354 (GPU) / 355 (paper)
-        assert r.outcome == "converged" and r.iterations <= 500
-        return
     _check(ex, method, it, res, r.outcome, r.iterations)
