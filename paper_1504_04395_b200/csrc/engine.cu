@@ -263,7 +263,9 @@ int Eng::upd(int s, std::vector<const void*> in, std::vector<OutSpec> outs, std:
     for (auto& t : o.t) full_coef |= (t.c.kind == CK_FULL);
   static const bool no_mma = getenv("SRK_NO_DMMA_UPDATE") != nullptr;  // A/B switch for measurements
   const bool use_mma = full_coef && !no_mma && upd_mma_width(s * (cplx ? 2 : 1)) > 0;
-  if (!full_red_supported(cplx, cap) || use_mma) {
+  // (s >= 8: also a reductions-only pass such as Bl-QMR's delta = W^H V — the DMMA Gram
+  // reads the two blocks at 4.8 TB/s against 1.5 for the FMA epilogue's s x s accumulators)
+  if (!full_red_supported(cplx, cap) || use_mma || s >= 8) {
     auto ptr = [&](int src) -> const void* {
       if (src >= 0 && src < (int)in.size()) return in[src];
       if (src >= SRC_OUT && src - SRC_OUT < (int)outs.size()) {

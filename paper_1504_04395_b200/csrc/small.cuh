@@ -186,33 +186,42 @@ __device__ int sm_solve(T* X, const T* G, const T* M, int n, int m, int herm, T*
 }
 
 // Upper Cholesky G = R^H R (n x n Hermitian positive definite). Rank test
-// (reading R5): pivot d_j <= EPS_CHOL * tr(G) -> return 1. Single thread (n <= 64).
+// (reading R5): pivot d_j <= EPS_CHOL * tr(G) -> return 1. Row j: thread 0 forms the
+// pivot, then one thread per entry R_jk (each entry's sum in the same order as a
+// serial loop, so the result does not depend on the thread count).
 template <typename T>
 __device__ int sm_chol(T* R, const T* G, int n, int check_rank) {
   __shared__ int s_bad;
-  if (threadIdx.x == 0) {
-    int bad = 0;
-    double tr = 0.0;
-    for (int i = 0; i < n; ++i) tr += re(G[i * n + i]);
-    const double thr = EPS_CHOL * tr;
-    for (int i = 0; i < n * n; ++i) R[i] = Ar<T>::zero();
-    for (int j = 0; j < n && !bad; ++j) {
+  __shared__ double s_rjj;
+  for (int i = threadIdx.x; i < n * n; i += blockDim.x) R[i] = Ar<T>::zero();
+  if (threadIdx.x == 0) s_bad = 0;
+  __syncthreads();
+  for (int j = 0; j < n; ++j) {
+    if (threadIdx.x == 0) {
+      double tr = 0.0;
+      for (int i = 0; i < n; ++i) tr += re(G[i * n + i]);
+      const double thr = EPS_CHOL * tr;
       // R_jj^2 = G_jj - sum_i |R_ij|^2
       double d = re(G[j * n + j]);
       for (int i = 0; i < j; ++i) d -= Ar<T>::abs2(R[i * n + j]);
-      if (!(d > 0.0) || !isfinite(d) || (check_rank && d <= thr) || tr == 0.0) { bad = 1; break; }
-      const double rjj = sqrt(d);
-      R[j * n + j] = mkT(rjj, 0.0, T());
-      // R_jk = (G_jk - sum_i conj(R_ij) R_ik) / R_jj, k > j
-      for (int k = j + 1; k < n; ++k) {
-        T acc = G[j * n + k];
-        for (int i = 0; i < j; ++i) acc = Ar<T>::sub(acc, Ar<T>::mul(Ar<T>::conj(R[i * n + j]), R[i * n + k]));
-        R[j * n + k] = scal(acc, 1.0 / rjj);
+      if (!(d > 0.0) || !isfinite(d) || (check_rank && d <= thr) || tr == 0.0) {
+        s_bad = 1;
+      } else {
+        s_rjj = sqrt(d);
+        R[j * n + j] = mkT(s_rjj, 0.0, T());
       }
     }
-    s_bad = bad;
+    __syncthreads();
+    if (s_bad) break;
+    const double rjj = s_rjj;
+    // R_jk = (G_jk - sum_i conj(R_ij) R_ik) / R_jj, k > j
+    for (int k = j + 1 + threadIdx.x; k < n; k += blockDim.x) {
+      T acc = G[j * n + k];
+      for (int i = 0; i < j; ++i) acc = Ar<T>::sub(acc, Ar<T>::mul(Ar<T>::conj(R[i * n + j]), R[i * n + k]));
+      R[j * n + k] = scal(acc, 1.0 / rjj);
+    }
+    __syncthreads();
   }
-  __syncthreads();
   int b = s_bad;
   __syncthreads();
   return b;
@@ -234,67 +243,82 @@ __device__ void sm_trinv(T* Ri, const T* R, int n) {
 
 // Full QR of a (2n x n) stack M = Om [R; 0] by Householder reflections in LAPACK's
 // convention (?larfg: beta = -sign(Re alpha) * norm, real), then phase-normalised so
-// diag(R) is real non-negative. Om: 2n x 2n; R: n x n. Thread 0.
+// diag(R) is real non-negative. Om: 2n x 2n; R: n x n. Thread 0
+// forms each reflector; its application runs one thread per column (every entry
+// updated by the same serial sums as a one-thread loop).
 template <typename T>
 __device__ void sm_qr_stack(T* Om, T* R, const T* M, int n, T* work /* 2n*n + 2n*n */) {
-  if (threadIdx.x == 0) {
-    const int m2 = 2 * n;
-    T* A = work;                // 2n x n working copy
-    T* V = work + m2 * n;       // reflectors, column j stored in V[:, j] (2n x n)
-    double tau_r[64];
-    double tau_i[64];
-    for (int i = 0; i < m2 * n; ++i) { A[i] = M[i]; V[i] = Ar<T>::zero(); }
-    for (int j = 0; j < n; ++j) {
+  const int m2 = 2 * n;
+  T* A = work;           // 2n x n working copy
+  T* V = work + m2 * n;  // reflectors, column j stored in V[:, j] (2n x n)
+  __shared__ double tau_r[64];
+  __shared__ double tau_i[64];
+  __shared__ int s_skip[2];  // double-buffered: thread 0 may write j + 1's before all read j's
+  __shared__ T s_d;
+  for (int i = threadIdx.x; i < m2 * n; i += blockDim.x) {
+    A[i] = M[i];
+    V[i] = Ar<T>::zero();
+  }
+  __syncthreads();
+  for (int j = 0; j < n; ++j) {
+    if (threadIdx.x == 0) {
       T alpha = A[j * n + j];
       double xn2 = 0.0;
       for (int i = j + 1; i < m2; ++i) xn2 += Ar<T>::abs2(A[i * n + j]);
       double ar = re(alpha);
       double ai = 0.0;
       if constexpr (Ar<T>::cplx) ai = reinterpret_cast<double2&>(alpha).y;
-      if (xn2 == 0.0 && ai == 0.0) {
-        tau_r[j] = 0.0; tau_i[j] = 0.0;
-        V[j * n + j] = one<T>();
-        continue;
-      }
-      double nrm = sqrt(ar * ar + ai * ai + xn2);
-      double beta = (ar >= 0.0) ? -nrm : nrm;
-      tau_r[j] = (beta - ar) / beta;
-      tau_i[j] = -ai / beta;
-      T d = Ar<T>::sub(alpha, mkT(beta, 0.0, T()));  // alpha - beta
       V[j * n + j] = one<T>();
-      for (int i = j + 1; i < m2; ++i) V[i * n + j] = cdiv(A[i * n + j], d);
-      // apply H^H = I - conj(tau) v v^H to A[:, j:]  (geqrf applies H^H on the left)
-      const T tc = mkT(tau_r[j], -tau_i[j], T());
-      for (int c = j; c < n; ++c) {
-        T w = Ar<T>::zero();
-        for (int i = j; i < m2; ++i) w = Ar<T>::cfma(V[i * n + j], A[i * n + c], w);  // v^H a
-        w = Ar<T>::mul(tc, w);
-        for (int i = j; i < m2; ++i) A[i * n + c] = Ar<T>::sub(A[i * n + c], Ar<T>::mul(V[i * n + j], w));
+      if (xn2 == 0.0 && ai == 0.0) {
+        tau_r[j] = 0.0;
+        tau_i[j] = 0.0;
+        s_skip[j & 1] = 1;
+      } else {
+        double nrm = sqrt(ar * ar + ai * ai + xn2);
+        double beta = (ar >= 0.0) ? -nrm : nrm;
+        tau_r[j] = (beta - ar) / beta;
+        tau_i[j] = -ai / beta;
+        s_d = Ar<T>::sub(alpha, mkT(beta, 0.0, T()));  // alpha - beta
+        s_skip[j & 1] = 0;
       }
     }
-    // Om = H_1 H_2 ... H_n applied to I (H_j = I - tau_j v_j v_j^H)
-    for (int i = 0; i < m2 * m2; ++i) Om[i] = Ar<T>::zero();
-    for (int i = 0; i < m2; ++i) Om[i * m2 + i] = one<T>();
+    __syncthreads();
+    if (s_skip[j & 1]) continue;
+    const T d = s_d;
+    for (int i = j + 1 + threadIdx.x; i < m2; i += blockDim.x) V[i * n + j] = cdiv(A[i * n + j], d);
+    __syncthreads();
+    // apply H^H = I - conj(tau) v v^H to A[:, j:]  (geqrf applies H^H on the left)
+    const T tc = mkT(tau_r[j], -tau_i[j], T());
+    for (int c = j + threadIdx.x; c < n; c += blockDim.x) {
+      T w = Ar<T>::zero();
+      for (int i = j; i < m2; ++i) w = Ar<T>::cfma(V[i * n + j], A[i * n + c], w);  // v^H a
+      w = Ar<T>::mul(tc, w);
+      for (int i = j; i < m2; ++i) A[i * n + c] = Ar<T>::sub(A[i * n + c], Ar<T>::mul(V[i * n + j], w));
+    }
+    __syncthreads();
+  }
+  // Om = H_1 H_2 ... H_n applied to I (H_j = I - tau_j v_j v_j^H): columns in parallel
+  for (int i = threadIdx.x; i < m2 * m2; i += blockDim.x) Om[i] = (i / m2 == i % m2) ? one<T>() : Ar<T>::zero();
+  __syncthreads();
+  for (int c = threadIdx.x; c < m2; c += blockDim.x)
     for (int j = n - 1; j >= 0; --j) {
       const T t = mkT(tau_r[j], tau_i[j], T());
-      for (int c = 0; c < m2; ++c) {
-        T w = Ar<T>::zero();
-        for (int i = j; i < m2; ++i) w = Ar<T>::cfma(V[i * n + j], Om[i * m2 + c], w);
-        w = Ar<T>::mul(t, w);
-        for (int i = j; i < m2; ++i) Om[i * m2 + c] = Ar<T>::sub(Om[i * m2 + c], Ar<T>::mul(V[i * n + j], w));
-      }
+      T w = Ar<T>::zero();
+      for (int i = j; i < m2; ++i) w = Ar<T>::cfma(V[i * n + j], Om[i * m2 + c], w);
+      w = Ar<T>::mul(t, w);
+      for (int i = j; i < m2; ++i) Om[i * m2 + c] = Ar<T>::sub(Om[i * m2 + c], Ar<T>::mul(V[i * n + j], w));
     }
-    // R = upper n x n of A, then phase normalisation
-    for (int i = 0; i < n; ++i)
-      for (int c = 0; c < n; ++c) R[i * n + c] = (c >= i) ? A[i * n + c] : Ar<T>::zero();
-    for (int j = 0; j < n; ++j) {
-      const T d = R[j * n + j];
-      const double a = cabs(d);
-      if (a > 0.0) {
-        const T ph = scal(d, 1.0 / a);  // phase
-        for (int i = 0; i < m2; ++i) Om[i * m2 + j] = Ar<T>::mul(Om[i * m2 + j], ph);
-        for (int c = 0; c < n; ++c) R[j * n + c] = Ar<T>::mul(Ar<T>::conj(ph), R[j * n + c]);
-      }
+  __syncthreads();
+  // R = upper n x n of A, then phase normalisation (column j of Om, row j of R)
+  for (int i = threadIdx.x; i < n * n; i += blockDim.x) R[i] = ((i % n) >= (i / n)) ? A[i] : Ar<T>::zero();
+  __syncthreads();
+  for (int j = threadIdx.x; j < n; j += blockDim.x) {
+    const T d = R[j * n + j];
+    const double a = cabs(d);
+    if (a > 0.0) {
+      const T ph = scal(d, 1.0 / a);  // phase
+      for (int i = 0; i < m2; ++i) Om[i * m2 + j] = Ar<T>::mul(Om[i * m2 + j], ph);
+      for (int c = 0; c < n; ++c) R[j * n + c] = Ar<T>::mul(Ar<T>::conj(ph), R[j * n + c]);
     }
   }
   __syncthreads();
