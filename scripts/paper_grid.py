@@ -8,7 +8,7 @@ X. Table 2's block-method entries (no preconditioning) are printed beside ours:
 the paper reports "div." when the recomputed residual exceeds 1. Then the same with
 the right no-fill ILU preconditioner (srk_matrix_ilu0; Table 2's lower half).
 
-    python scripts/paper_grid.py r01     ->  profiles/r01_paper_grid.json
+    python scripts/paper_grid.py r01 [outdir]   ->  <outdir, default profiles>/r01_paper_grid.json
 """
 import json
 import os
@@ -46,7 +46,7 @@ def problem(name):
     return synth.paper_ex2(50, 10.0)
 
 
-def main(tag):
+def main(tag, outdir="profiles"):
     srk.load_library()
     out = {"protocol": "X0 = 0, B -> Q (thin QR), R^0 = R0 (economic: mean), tol 1e-10, maxit 500, "
                        "true residual recomputed by scipy", "examples": {}}
@@ -83,9 +83,11 @@ def main(tag):
                       + (f"   paper: it {p['iterations']}, ||R|| {p['final_rel_residual']}" if p else ""), flush=True)
             Mh.close()
         out["examples"][name] = {"n": A.n, "nnz": A.nnz, "s": s, "rho": s * A.n / A.nnz, "methods": rows}
-    os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
-    json.dump(out, open(os.path.join(ROOT, "profiles", f"{tag}_paper_grid.json"), "w"), indent=1)
+    odir = os.path.join(ROOT, outdir)
+    os.makedirs(odir, exist_ok=True)
+    json.dump(out, open(os.path.join(odir, f"{tag}_paper_grid.json"), "w"), indent=1)
 
 
 if __name__ == "__main__":
-    main(sys.argv[1] if len(sys.argv) > 1 else "r01")
+    # on a gpurun box write under gpurun_out/ (merged back), then copy into profiles/
+    main(sys.argv[1] if len(sys.argv) > 1 else "r01", sys.argv[2] if len(sys.argv) > 2 else "profiles")
