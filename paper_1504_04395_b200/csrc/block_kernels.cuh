@@ -432,10 +432,10 @@ __global__ void __launch_bounds__(256, FC ? (S <= 8 ? 2 : 1) : MINB) spmm_kernel
 // ============================================================================
 // MINB = 4 (<= 64 registers, 32 warps per SM) measured best for every input count on
 // config-3 blocks (scripts/upd_tune.cu: 90-100% of the measured copy bandwidth)
-// (complex rows and the s x s-coefficient instances need more registers: 2 CTAs/SM,
-// measured on config 2's block updates)
+// (the s x s-coefficient instances need more registers: 2 CTAs/SM; complex rows, one per
+// lane group, fit 4 CTAs/SM with up to 2 inputs and 3 with more, without spills)
 template <typename T, int S, bool FC, int NI, int R, bool EX, bool STREAM = false,
-          int MINB = (FC || sizeof(T) == 16) ? 2 : 4>
+          int MINB = FC ? 2 : (sizeof(T) == 16 ? (NI <= 2 ? 4 : 3) : 4)>
 __global__ void __launch_bounds__(256, MINB) upd_kernel(UpdArgs a) {
   if (a.done && *a.done) return;
   using L = Lay<T, S>;
@@ -869,7 +869,9 @@ __global__ void __launch_bounds__(256, W * sizeof(T) >= 32 ? 2 : 4) spmv_team_ke
 template <typename T, int S> constexpr int spmm_rows() {
   return (Lay<T, S>::G == 1 || S >= 64) ? 1 : 2;
 }
-template <int NI> constexpr int upd_rows() { return NI <= 2 ? 2 : 1; }
+// rows per lane group: 2 for real blocks with few inputs; complex rows one at a time, at
+// 3-4 CTAs/SM (config 4's complex updates: 49-50% -> 65-69% of HBM against 2 rows at 2 CTAs/SM)
+template <typename T, int NI> constexpr int upd_rows() { return (sizeof(T) == 16) ? 1 : (NI <= 2 ? 2 : 1); }
 template <typename T, int S> constexpr bool full_ok() { return S <= 32; }
 
 // grid < 0: return the number of resident CTAs per SM instead of launching
@@ -922,7 +924,7 @@ int launch_spmm_t(const SpmmArgs& a, int grid, int block, size_t smem, cudaStrea
 
 template <typename T, int S, bool FC, int NI, bool EX>
 int launch_upd_nix(const UpdArgs& a, int grid, int block, size_t smem, cudaStream_t st) {
-  constexpr int R = upd_rows<NI>();
+  constexpr int R = upd_rows<T, NI>();
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(upd_kernel<T, S, FC, NI, R, EX>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
