@@ -168,6 +168,12 @@ int main(int argc, char** argv) {
   run<1, 8, true, 3, 8, 1>(a, nsm, bytes, "R1 minb3 batch8");
   run<1, 8, true, 4, 8, 1>(a, nsm, bytes, "R1 minb4 batch8");
   run<1, 16, true, 4, 8, 1>(a, nsm, bytes, "R1 BC16 minb4 batch8");
+  run<2, 2, true, 2, 8, 1>(a, nsm, bytes, "R2 BC2 minb2 batch8");
+  run<2, 4, true, 2, 8, 1>(a, nsm, bytes, "R2 BC4 minb2 batch8");
+  run<2, 16, true, 2, 8, 1>(a, nsm, bytes, "R2 BC16 minb2 batch8");
+  run<2, 32, true, 2, 8, 1>(a, nsm, bytes, "R2 BC32 minb2 batch8");
+  run<2, 64, true, 2, 8, 1>(a, nsm, bytes, "R2 BC64 minb2 batch8");
+  run<2, 8, true, 2, 8, 2>(a, nsm, bytes, "R2 minb2 batch8 PD2");
   run<2, 8, true, 2, 8, 1>(a, nsm, bytes, "R2 minb2 batch8 (repeat)");
   return 0;
 }
