@@ -198,14 +198,17 @@ __global__ void __launch_bounds__(256, 2) upd_mma_kernel(UpdArgs a, int cplx, in
               av[j].y = (live && col + 1 < w) ? X[col + 1] : 0.0;
             }
           }
+          // consecutive DMMAs go to different accumulators (NT independent chains)
 #pragma unroll
-          for (int j = 0; j < NT; ++j)
+          for (int j = 0; j < NT; ++j) {
+            double2 bv[NT];
 #pragma unroll
-            for (int t = 0; t < NT; ++t) {
-              const double2 bv = *reinterpret_cast<const double2*>(M + (t * 8 + fr) * W + j * 8 + 2 * fk);
-              dmma(acc[o][t], av[j].x, bv.x);
-              dmma(acc[o][t], av[j].y, bv.y);
-            }
+            for (int t = 0; t < NT; ++t) bv[t] = *reinterpret_cast<const double2*>(M + (t * 8 + fr) * W + j * 8 + 2 * fk);
+#pragma unroll
+            for (int t = 0; t < NT; ++t) dmma(acc[o][t], av[j].x, bv[t].x);
+#pragma unroll
+            for (int t = 0; t < NT; ++t) dmma(acc[o][t], av[j].y, bv[t].y);
+          }
         }
         // earlier outputs of this tile (C fragment -> A fragment by shuffles)
 #pragma unroll
@@ -217,13 +220,15 @@ __global__ void __launch_bounds__(256, 2) upd_mma_kernel(UpdArgs a, int cplx, in
           // with the permuted k order the A values of an earlier output are this lane's
           // own accumulator entries (columns 8j + 2fk, 8j + 2fk + 1): no shuffles
 #pragma unroll
-          for (int j = 0; j < NT; ++j)
+          for (int j = 0; j < NT; ++j) {
+            double2 bv[NT];
 #pragma unroll
-            for (int tt = 0; tt < NT; ++tt) {
-              const double2 bv = *reinterpret_cast<const double2*>(M + (tt * 8 + fr) * W + j * 8 + 2 * fk);
-              dmma(acc[o][tt], acc[p][j][0], bv.x);
-              dmma(acc[o][tt], acc[p][j][1], bv.y);
-            }
+            for (int tt = 0; tt < NT; ++tt) bv[tt] = *reinterpret_cast<const double2*>(M + (tt * 8 + fr) * W + j * 8 + 2 * fk);
+#pragma unroll
+            for (int tt = 0; tt < NT; ++tt) dmma(acc[o][tt], acc[p][j][0], bv[tt].x);
+#pragma unroll
+            for (int tt = 0; tt < NT; ++tt) dmma(acc[o][tt], acc[p][j][1], bv[tt].y);
+          }
         }
       }
     }
