@@ -1,6 +1,8 @@
 // coef.cu — single-CTA coefficient phases for the 13 methods.
 // Each phase follows oracle/solvers.py's order of operations and breakdown
 // rules line by line (readings G11, G12, G13, G26 in DESIGN.md).
+#include <algorithm>
+
 #include "coef.cuh"
 
 namespace srk {
@@ -610,6 +612,137 @@ int launch_coef(bool cplx, const CoefArgs& a, size_t smem, cudaStream_t st) {
   }
   if (cplx) coef_kernel<double2><<<1, 256, smem, st>>>(a);
   else coef_kernel<double><<<1, 256, smem, st>>>(a);
+  return (int)cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ small eGl-BiCG
+// fixed-order CTA sum: warp butterflies, then warp 0 adds the warps in index order
+template <typename T>
+__device__ T cta_sum(T v, T* sh) {
+  for (int m = 16; m > 0; m >>= 1) v = Ar<T>::add(v, Ar<T>::shfl_xor(v, m));
+  const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  __syncthreads();  // sh may still be read by a previous sum
+  if ((threadIdx.x & 31) == 0) sh[w] = v;
+  __syncthreads();
+  T r = Ar<T>::zero();
+  for (int q = 0; q < nw; ++q) r = Ar<T>::add(r, sh[q]);
+  return r;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(1024) egl_bicg_small_kernel(SmallBiCGArgs g) {
+  CoefArgs a = g.ca;
+  if (a.ctl[CTL_FLAG] != FLAG_RUN) return;
+  __shared__ T red[32];
+  __shared__ double redd[32];
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const long long n = g.n;
+  const int s = a.s;
+  const T* val = reinterpret_cast<const T*>(g.val);
+  const T* valH = reinterpret_cast<const T*>(g.valH);
+  T* X = reinterpret_cast<T*>(g.X);
+  T* R = reinterpret_cast<T*>(g.R);
+  T* P = reinterpret_cast<T*>(g.P);
+  T* Q = reinterpret_cast<T*>(g.Q);
+  T* rh = reinterpret_cast<T*>(g.rh);
+  T* ph = reinterpret_cast<T*>(g.ph);
+  T* qh = reinterpret_cast<T*>(g.qh);
+  // Q = A P ; den = sum(p̂^H Q)   and   q̂ = A^H p̂
+  T part = Ar<T>::zero();
+  for (long long i = tid; i < n; i += nt) {
+    const int b = g.rp[i], e = g.rp[i + 1];
+    T rs = Ar<T>::zero();
+    if (s <= 8) {  // entries outer, the row's s accumulators in registers
+      T acc[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) acc[c] = Ar<T>::zero();
+      for (int p = b; p < e; ++p) {
+        const T v = val[p];
+        const T* Pr = P + (size_t)g.ci[p] * s;
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          if (c < s) acc[c] = Ar<T>::fma(v, Pr[c], acc[c]);
+      }
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        if (c < s) {
+          Q[(size_t)i * s + c] = acc[c];
+          rs = Ar<T>::add(rs, acc[c]);
+        }
+    } else {
+      for (int c = 0; c < s; ++c) {
+        T acc = Ar<T>::zero();
+        for (int p = b; p < e; ++p) acc = Ar<T>::fma(val[p], P[(size_t)g.ci[p] * s + c], acc);
+        Q[(size_t)i * s + c] = acc;
+        rs = Ar<T>::add(rs, acc);
+      }
+    }
+    part = Ar<T>::cfma(ph[i], rs, part);
+    const int bh = g.rpH[i], eh = g.rpH[i + 1];
+    T acc = Ar<T>::zero();
+    for (int p = bh; p < eh; ++p) acc = Ar<T>::fma(valH[p], ph[g.ciH[p]], acc);
+    qh[i] = acc;
+  }
+  const T den = cta_sum(part, red);
+  if (tid == 0) *W<T>(a, SL_DEN) = den;
+  __syncthreads();
+  a.phase = 1;
+  gl_bicg<T>(a);  // alpha = rho / den (ends with a CTA barrier)
+  if (a.ctl[CTL_FLAG] != FLAG_RUN) return;
+  const T alpha = *W<T>(a, SL_ALPHA);
+  const T malc = Ar<T>::sub(Ar<T>::zero(), Ar<T>::conj(alpha));  // r̂ -= conj(alpha) q̂
+  const T mal = Ar<T>::sub(Ar<T>::zero(), alpha);
+  // r̂, X, R ; rho_new = sum(r̂^H R), ||R||^2 (each thread owns its rows: no barrier needed
+  // between the r̂ update and its use in the same row)
+  T rpart = Ar<T>::zero();
+  double r2 = 0.0;
+  for (long long i = tid; i < n; i += nt) {
+    const T rhi = Ar<T>::fma(qh[i], malc, rh[i]);
+    rh[i] = rhi;
+    T rs = Ar<T>::zero();
+    for (int c = 0; c < s; ++c) {
+      const size_t k = (size_t)i * s + c;
+      X[k] = Ar<T>::fma(P[k], alpha, X[k]);
+      const T r = Ar<T>::fma(Q[k], mal, R[k]);
+      R[k] = r;
+      rs = Ar<T>::add(rs, r);
+      r2 += Ar<T>::abs2(r);
+    }
+    rpart = Ar<T>::cfma(rhi, rs, rpart);
+  }
+  const T rhon = cta_sum(rpart, red);
+  const double r2s = cta_sum(r2, redd);
+  if (tid == 0) {
+    *W<T>(a, SL_RHON) = rhon;
+    *D(a, SL_R2) = r2s;
+  }
+  __syncthreads();
+  a.phase = 2;
+  gl_bicg<T>(a);  // beta = rho_new / rho, convergence test
+  if (a.ctl[CTL_FLAG] != FLAG_RUN) return;
+  const T beta = *W<T>(a, SL_BETA);
+  const T bc = Ar<T>::conj(beta);
+  for (long long i = tid; i < n; i += nt) {
+    for (int c = 0; c < s; ++c) {
+      const size_t k = (size_t)i * s + c;
+      P[k] = Ar<T>::fma(P[k], beta, R[k]);
+    }
+    ph[i] = Ar<T>::fma(ph[i], bc, rh[i]);
+  }
+  // end of the iteration (end_iter_kernel's step): count it, commit a pending convergence
+  if (tid == 0) {
+    a.ctl[CTL_ITER] += 1;
+    if (a.ctl[CTL_CONVPEND]) {
+      a.ctl[CTL_CONVPEND] = 0;
+      a.ctl[CTL_FLAG] = FLAG_CONV;
+    }
+  }
+}
+
+int launch_egl_bicg_small(bool cplx, const SmallBiCGArgs& g, cudaStream_t st) {
+  const int threads = (int)std::min<long long>(1024, std::max<long long>(32, (g.n + 31) / 32 * 32));
+  if (cplx) egl_bicg_small_kernel<double2><<<1, threads, 0, st>>>(g);
+  else egl_bicg_small_kernel<double><<<1, threads, 0, st>>>(g);
   return (int)cudaGetLastError();
 }
 

@@ -57,4 +57,25 @@ struct CoefArgs {
   int off[NSLOT];
 };
 
+// One eGl-BiCG iteration (Alg. 4) for a small operator in ONE kernel on one
+// CTA (latency-bound sizes, e.g. config 1: n = 1024): the same steps as the
+// multi-kernel sequence of EglBiCG::seg — Q = A P with sum(p̂^H Q), q̂ = A^H p̂, the
+// alpha phase, r̂ and X / R updates with sum(r̂^H R) and ||R||^2, the beta phase (with the
+// convergence test), P and p̂ — separated by CTA barriers instead of kernel boundaries,
+// reductions in a fixed order, the coefficient phases the same device code; it also
+// ends the iteration (end_iter_kernel's counting and convergence commit).
+struct SmallBiCGArgs {
+  const int* rp;
+  const int* ci;
+  const void* val;
+  const int* rpH;
+  const int* ciH;
+  const void* valH;
+  void *X, *R, *P, *Q, *rh, *ph, *qh;
+  long long n;
+  CoefArgs ca;
+};
+int launch_egl_bicg_small(bool cplx, const SmallBiCGArgs& g, cudaStream_t st);
+constexpr long long SMALL_N_MAX = 16384;  // one-CTA eGl-BiCG up to this many rows
+
 }  // namespace srk

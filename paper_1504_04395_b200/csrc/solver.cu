@@ -178,8 +178,10 @@ int Solver::iterate(int k) {
           continue;
         }
         for (int q = 0; q < nseg(); ++q) seg(q);
-        launch_end_iter(ctl, c->st);
-        e.nlaunch++;
+        if (!ends_iter()) {
+          launch_end_iter(ctl, c->st);
+          e.nlaunch++;
+        }
         host_iter++;
         launched++;
       }
@@ -265,8 +267,10 @@ int Solver::capture(int iters) {
   }
   for (int i = 0; i < iters; ++i) {
     for (int q = 0; q < nseg(); ++q) seg(q);
-    launch_end_iter(ctl, cap_st);
-    e.nlaunch++;
+    if (!ends_iter()) {
+      launch_end_iter(ctl, cap_st);
+      e.nlaunch++;
+    }
   }
   cudaError_t ce = cudaStreamEndCapture(cap_st, &g);
   c->st = user;
@@ -353,7 +357,39 @@ struct EglBiCG : Solver {  // Alg. 4
     e.upd(s, {R}, {}, {RQ{RED_SUMVEC, 0, -1, rh, off[SL_RHO]}});
     return coef(0);
   }
+  // small operators (latency-bound): the whole iteration as one single-CTA kernel
+  bool small() const {
+    static const bool off_env = getenv("SRK_NO_SMALL_KERNEL") != nullptr;  // A/B switch
+    return !off_env && A && !A->bsr && !A->prec && !A->dist && A->has_adj && n <= SMALL_N_MAX &&
+           !(c->comm && c->comm->nranks > 1);
+  }
+  bool ends_iter() const override { return small(); }
   void seg(int) override {
+    if (small()) {
+      if (e.err) return;
+      SmallBiCGArgs g{};
+      g.rp = A->rp;
+      g.ci = A->ci;
+      g.val = A->val;
+      g.rpH = A->rpH;
+      g.ciH = A->ciH;
+      g.valH = A->valH;
+      g.X = X; g.R = R; g.P = P; g.Q = Q; g.rh = rh; g.ph = ph; g.qh = qh;
+      g.n = n;
+      g.ca.method = method;
+      g.ca.s = s;
+      g.ca.tol = o.tol;
+      g.ca.ws = ws;
+      g.ca.ctl = ctl;
+      g.ca.hist = hist;
+      g.ca.hist_cap = hist_cap;
+      for (int i = 0; i < NSLOT; ++i) g.ca.off[i] = off[i];
+      e.nlaunch++;
+      prof.begin(PT_OTHER, c->st);
+      e.err = launch_egl_bicg_small(cplx, g, c->st);
+      prof.end(c->st);
+      return;
+    }
     e.spmm(false, P, Q, s, {RQ{RED_SUMVEC, 0, -1, ph, off[SL_DEN]}});  // sum(p̂^H Q)
     e.spmm(true, ph, qh, 1, {});                                        // A^H p̂ (one vector)
     coef(1);

@@ -67,6 +67,7 @@ struct Solver {
   virtual int nseg() const { return 1; }
   virtual void half_x(void* Xh) { (void)Xh; }
   virtual bool is_rq() const { return false; }
+  virtual bool ends_iter() const { return false; }  // seg() also ends the iteration (fused kernel)
   virtual int residual(void* out, int64_t* rows);
 };
 

@@ -266,3 +266,45 @@ def test_cuda_graph_replay_is_bitwise_identical(srk, method):
         sv.close()
     assert out[0][1] == out[1][1] and out[0][2] == out[1][2]
     assert np.array_equal(out[0][0], out[1][0])
+
+
+@pytest.mark.parametrize("cplx", [False, True])
+def test_small_operator_single_kernel_iteration(srk, cplx):
+    """eGl-BiCG on a small operator runs each iteration as ONE single-CTA kernel
+    (egl_bicg_small_kernel: Alg. 4's steps separated by CTA barriers, the coefficient
+    phases the same device code): one launch per iteration, iterates in lock step with
+    the oracle (envelope rule), and the same outcome as the multi-kernel sequence
+    (SRK_NO_SMALL_KERNEL=1, checked in a subprocess: the switch is read once)."""
+    import os
+    import subprocess
+    import sys
+    A, B = _problem("cplx" if cplx else "cfg1")
+    M = srk.Matrix.from_csr(A, need_adjoint=True)
+    sv = srk.Solver(M, B.shape[1], "egl_bicg", tol=1e-8, maxit=2000, poll_every=1)
+    sv.start(to_dev(B))
+    sv.iterate(2)
+    sv.profile(True)
+    sv.iterate(5)
+    recs = sv.profile_launches()
+    assert len(recs) == 5, recs  # one launch per iteration (the end-of-iteration step included)
+    sv.close()
+    a, _, env = envelope("egl_bicg", A.to_scipy(), B, 1e-8)
+    sv, xs = lockstep(srk, M, B, "egl_bicg", min(K, a.iterations), 1e-8)
+    for k, x in enumerate(xs):
+        assert rel(x, a.Xs[k]) <= env[k], (k, rel(x, a.Xs[k]), env[k])
+    sv.close()
+    X, rep = srk.solve(M, to_dev(B), "egl_bicg", tol=1e-8, maxit=2000)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = (f"import sys; sys.path.insert(0, {root!r})\n"
+            "import numpy as np, torch, paper_1504_04395_b200 as srk\n"
+            "from tests.test_gpu_solvers import _problem\n"
+            "srk.load_library()\n"
+            f"A, B = _problem({'cplx' if cplx else 'cfg1'!r})\n"
+            "M = srk.Matrix.from_csr(A, need_adjoint=True)\n"
+            "X, rep = srk.solve(M, torch.from_numpy(B).cuda(), 'egl_bicg', tol=1e-8, maxit=2000)\n"
+            "print(rep.outcome, rep.iterations)\n")
+    out = subprocess.run([sys.executable, "-c", code], env={**os.environ, "SRK_NO_SMALL_KERNEL": "1"},
+                         capture_output=True, text=True, timeout=600)
+    outcome, its = out.stdout.split()[-2:]
+    assert outcome == rep.outcome and abs(int(its) - rep.iterations) <= max(2, 0.02 * rep.iterations), \
+        (out.stdout, out.stderr[-400:], rep)
