@@ -647,6 +647,10 @@ __global__ void __launch_bounds__(1024) egl_bicg_small_kernel(SmallBiCGArgs g) {
   T* rh = reinterpret_cast<T*>(g.rh);
   T* ph = reinterpret_cast<T*>(g.ph);
   T* qh = reinterpret_cast<T*>(g.qh);
+  // g.iters iterations in one launch: the operator and the blocks stay in L1 between them
+  // (L1 is invalidated at kernel boundaries only)
+  for (int it = 0; it < g.iters; ++it) {
+  if (it > 0 && a.ctl[CTL_FLAG] != FLAG_RUN) return;
   // Q = A P ; den = sum(p̂^H Q)   and   q̂ = A^H p̂
   T part = Ar<T>::zero();
   for (long long i = tid; i < n; i += nt) {
@@ -737,6 +741,8 @@ __global__ void __launch_bounds__(1024) egl_bicg_small_kernel(SmallBiCGArgs g) {
       a.ctl[CTL_FLAG] = FLAG_CONV;
     }
   }
+  __syncthreads();
+  }  // iterations
 }
 
 int launch_egl_bicg_small(bool cplx, const SmallBiCGArgs& g, cudaStream_t st) {

@@ -73,6 +73,7 @@ struct SmallBiCGArgs {
   const void* valH;
   void *X, *R, *P, *Q, *rh, *ph, *qh;
   long long n;
+  int iters;  // iterations in this launch (stops early once the control flag leaves RUN)
   CoefArgs ca;
 };
 int launch_egl_bicg_small(bool cplx, const SmallBiCGArgs& g, cudaStream_t st);

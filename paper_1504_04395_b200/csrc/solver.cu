@@ -165,6 +165,13 @@ int Solver::iterate(int k) {
       host_iter = dev_iter;
       int launched = 0;
       while (host_iter < target && launched < poll) {
+        // a method with a whole-iteration kernel runs the iterations up to the next poll in
+        // one launch
+        if (const int m = seg_multi(std::min(poll - launched, target - host_iter)); m > 0) {
+          host_iter += m;
+          launched += m;
+          continue;
+        }
         // after the first iteration every iteration launches the same kernels with the
         // same arguments: replay a captured CUDA graph of `poll` iterations
         // (not across ranks: the NCCL calls stay eager, capture is validated on one GPU only)
@@ -364,30 +371,38 @@ struct EglBiCG : Solver {  // Alg. 4
            !(c->comm && c->comm->nranks > 1);
   }
   bool ends_iter() const override { return small(); }
+  int seg_multi(int k) override {
+    if (!small() || k < 1 || e.err) return 0;
+    launch_small(k);
+    return k;
+  }
+  void launch_small(int iters) {
+    SmallBiCGArgs g{};
+    g.rp = A->rp;
+    g.ci = A->ci;
+    g.val = A->val;
+    g.rpH = A->rpH;
+    g.ciH = A->ciH;
+    g.valH = A->valH;
+    g.X = X; g.R = R; g.P = P; g.Q = Q; g.rh = rh; g.ph = ph; g.qh = qh;
+    g.n = n;
+    g.iters = iters;
+    g.ca.method = method;
+    g.ca.s = s;
+    g.ca.tol = o.tol;
+    g.ca.ws = ws;
+    g.ca.ctl = ctl;
+    g.ca.hist = hist;
+    g.ca.hist_cap = hist_cap;
+    for (int i = 0; i < NSLOT; ++i) g.ca.off[i] = off[i];
+    e.nlaunch++;
+    prof.begin(PT_OTHER, c->st);
+    e.err = launch_egl_bicg_small(cplx, g, c->st);
+    prof.end(c->st);
+  }
   void seg(int) override {
     if (small()) {
-      if (e.err) return;
-      SmallBiCGArgs g{};
-      g.rp = A->rp;
-      g.ci = A->ci;
-      g.val = A->val;
-      g.rpH = A->rpH;
-      g.ciH = A->ciH;
-      g.valH = A->valH;
-      g.X = X; g.R = R; g.P = P; g.Q = Q; g.rh = rh; g.ph = ph; g.qh = qh;
-      g.n = n;
-      g.ca.method = method;
-      g.ca.s = s;
-      g.ca.tol = o.tol;
-      g.ca.ws = ws;
-      g.ca.ctl = ctl;
-      g.ca.hist = hist;
-      g.ca.hist_cap = hist_cap;
-      for (int i = 0; i < NSLOT; ++i) g.ca.off[i] = off[i];
-      e.nlaunch++;
-      prof.begin(PT_OTHER, c->st);
-      e.err = launch_egl_bicg_small(cplx, g, c->st);
-      prof.end(c->st);
+      if (!e.err) launch_small(1);
       return;
     }
     e.spmm(false, P, Q, s, {RQ{RED_SUMVEC, 0, -1, ph, off[SL_DEN]}});  // sum(p̂^H Q)

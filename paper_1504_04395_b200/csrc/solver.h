@@ -68,6 +68,7 @@ struct Solver {
   virtual void half_x(void* Xh) { (void)Xh; }
   virtual bool is_rq() const { return false; }
   virtual bool ends_iter() const { return false; }  // seg() also ends the iteration (fused kernel)
+  virtual int seg_multi(int k) { (void)k; return 0; }  // enqueue up to k whole iterations as one launch
   virtual int residual(void* out, int64_t* rows);
 };
 
