@@ -59,6 +59,7 @@ struct DevTri {
   void* diag = nullptr;  // the diagonal itself (null: unit), for products with the factor
   int* order = nullptr;
   std::vector<int> lvl;
+  int* flags = nullptr;  // n row-done flags + a work counter (sync-free solve; allocated on first use)
 };
 // Right ILU(0) preconditioner M = L U (ilu.cu): M^-1 = U^-1 L^-1, M^-H = L^-H U^-H
 struct Prec {

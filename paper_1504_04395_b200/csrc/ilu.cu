@@ -198,6 +198,7 @@ void free_tri(DevTri& d) {
   if (d.dinv) cudaFree(d.dinv);
   if (d.diag) cudaFree(d.diag);
   if (d.order) cudaFree(d.order);
+  if (d.flags) cudaFree(d.flags);
   d = DevTri{};
 }
 

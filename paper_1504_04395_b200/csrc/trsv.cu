@@ -7,6 +7,9 @@
 // fixed-order sum.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <cstdlib>
+
 #include "engine.h"
 
 namespace srk {
@@ -52,8 +55,103 @@ __global__ void trimul_kernel(long long n, const int* __restrict__ rp, const int
 }
 
 template <typename T>
+__device__ __forceinline__ T nan_of();
+template <>
+__device__ __forceinline__ double nan_of<double>() { return __longlong_as_double(0x7ff8000000000000LL); }
+template <>
+__device__ __forceinline__ double2 nan_of<double2>() {
+  return make_double2(__longlong_as_double(0x7ff8000000000000LL), __longlong_as_double(0x7ff8000000000000LL));
+}
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Sync-free variant (one launch per solve): warps take rows in level order from an atomic
+// work counter, so every row a warp waits on was taken earlier by a running warp (no
+// deadlock whatever the residency). A row waits for its dependencies' done flags
+// (acquire loads), reads their Z rows through L2 (ld.global.cg: L1 is not coherent across
+// SMs), writes its own row, and one lane fences and raises the row's flag. Same fixed-order sums as the
+// level kernel (bitwise-identical results). A spin that outlives ~2^26 polls (a broken
+// schedule) writes NaN instead of hanging, so the solver reports a non-finite breakdown.
+template <typename T>
+__global__ void trsv_syncfree_kernel(const int* __restrict__ order, int nrows, const int* __restrict__ rp,
+                                     const int* __restrict__ ci, const T* __restrict__ val,
+                                     const T* __restrict__ dinv, const T* R, T* Z, int s, int* flags,
+                                     const int* done) {
+  if (done && *done) return;
+  const int lane = threadIdx.x & 31;
+  int* counter = flags + nrows;
+  volatile int* vflags = flags;
+  while (true) {
+    int k = 0;
+    if (lane == 0) k = atomicAdd(counter, 1);
+    k = __shfl_sync(0xffffffffu, k, 0);
+    if (k >= nrows) break;
+    const int i = __ldg(order + k);
+    const int b = __ldg(rp + i), e = __ldg(rp + i + 1);
+    bool bad = false;
+    for (int p = b + lane; p < e; p += 32) {
+      const int j = __ldg(ci + p);
+      long long spin = 0;
+      while (ld_acquire(flags + j) == 0) {  // acquire: the row's Z was written before its flag
+        if (++spin > (1LL << 26)) {
+          bad = true;
+          break;
+        }
+      }
+    }
+    bad = __any_sync(0xffffffffu, bad);  // (also orders the observing lanes before the reads)
+    for (int c = lane; c < s; c += 32) {
+      T acc = R[(size_t)i * s + c];
+      for (int p = b; p < e; ++p) {
+        const T tv = __ldg(val + p);
+        const T z = __ldcg(Z + (size_t)__ldg(ci + p) * s + c);
+        acc = Ar<T>::sub(acc, Ar<T>::mul(tv, z));
+      }
+      if (dinv) acc = Ar<T>::mul(acc, __ldg(dinv + i));
+      if (bad) acc = nan_of<T>();
+      Z[(size_t)i * s + c] = acc;
+    }
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence();  // release, cumulative over the warp's writes ordered by the barrier
+      vflags[i] = 1;
+    }
+  }
+}
+
+template <typename T>
+int run_syncfree(const DevTri& t, long long n, int s, const void* R, void* Z, const int* done, cudaStream_t st) {
+  const int nrows = t.lvl.empty() ? 0 : t.lvl.back();
+  if (nrows == 0) return 0;
+  DevTri& tm = const_cast<DevTri&>(t);  // the flag array is scratch owned by the factor
+  if (!tm.flags) {  // first use runs eagerly (never inside a graph capture)
+    if (cudaMalloc(&tm.flags, sizeof(int) * ((size_t)n + 1)) != cudaSuccess) return -(int)cudaErrorMemoryAllocation;
+  }
+  cudaMemsetAsync(tm.flags, 0, sizeof(int) * ((size_t)n + 1), st);
+  static int grid = 0;
+  if (!grid) {
+    int dev = 0, nsm = 0, occ = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, trsv_syncfree_kernel<T>, 256, 0);
+    grid = nsm * std::max(1, occ);
+  }
+  const int g = (int)std::min<long long>(grid, ((long long)nrows + 7) / 8);
+  trsv_syncfree_kernel<T><<<g, 256, 0, st>>>(t.order, nrows, t.rp, t.ci, reinterpret_cast<const T*>(t.val),
+                                             reinterpret_cast<const T*>(t.dinv), reinterpret_cast<const T*>(R),
+                                             reinterpret_cast<T*>(Z), s, tm.flags, done);
+  const int e = (int)cudaGetLastError();
+  return e ? -e : 1;
+}
+
+template <typename T>
 int run(const DevTri& t, long long n, int s, const void* R, void* Z, const int* done, cudaStream_t st) {
-  (void)n;
+  static const bool levels = getenv("SRK_TRSV_LEVELS") != nullptr;  // A/B: one launch per level
+  if (!levels) return run_syncfree<T>(t, n, s, R, Z, done, st);
   const int nlev = (int)t.lvl.size() - 1;
   for (int l = 0; l < nlev; ++l) {
     const int lo = t.lvl[l], hi = t.lvl[l + 1];
