@@ -165,9 +165,10 @@ int Solver::iterate(int k) {
       host_iter = dev_iter;
       int launched = 0;
       while (host_iter < target && launched < poll) {
-        // a method with a whole-iteration kernel runs the iterations up to the next poll in
-        // one launch
-        if (const int m = seg_multi(std::min(poll - launched, target - host_iter)); m > 0) {
+        // a method with a whole-iteration kernel runs the remaining iterations in one launch
+        // (the kernel stops by itself once the control flag leaves RUN, so the host polls
+        // right after a convergence candidate, a breakdown or the last iteration)
+        if (const int m = seg_multi(std::min(target - host_iter, 4096)); m > 0) {
           host_iter += m;
           launched += m;
           continue;

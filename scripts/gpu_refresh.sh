@@ -10,3 +10,5 @@ timeout 900 python bench.py --config 4 --steps 10 --warmup 3 > gpurun_out/bench_
 timeout 900 bash scripts/cfg2_methods.sh 10 > gpurun_out/cfg2_methods.log 2>&1
 timeout 900 python scripts/paper_grid.py r01 gpurun_out > gpurun_out/paper_grid.log 2>&1
 tail -2 gpurun_out/t_gpu.log; head -c 300 gpurun_out/bench.log; echo; cat gpurun_out/cfg2_methods.log | cut -c1-60
+timeout 300 python bench.py --config 1 --method bl_bicgstab_rq --steps 50 --warmup 8 > gpurun_out/bench_cfg1_blbicgstabrq.log 2>&1
+timeout 300 python scripts/ilu_timing.py > gpurun_out/ilu_timing.log 2>&1

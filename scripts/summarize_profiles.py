@@ -5,7 +5,8 @@
 Captures: prof_spmm (config 3 SpMM), prof_upd (config 3's dominant 6-in / 4-out update),
 prof_bsr (config 4 BSR-12 product), prof_gram (s = 64 CTA-tiled DMMA Gram), prof_updmma
 (config 2 tensor-core block update), prof_gramwarp (config 2 per-warp Gram of a block with
-itself). Reads gpurun_out/launches.csv (ncu --metrics gpu__time_duration.sum launch list of
+itself), prof_small (config 1's single-CTA eGl-BiCG iteration kernel; a launch covers the
+iterations between two polls). Reads gpurun_out/launches.csv (ncu --metrics gpu__time_duration.sum launch list of
 `python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu`), gpurun_out/prof_*.ncu-rep
 (`ncu --set full`) and gpurun_out/bench.log, and writes
 profiles/<tag>_launches.csv, profiles/<tag>_ncu_summary.json, profiles/<tag>_bench.json,
@@ -50,7 +51,7 @@ def to_bytes(v, unit):
 def main(tag):
     os.makedirs(PROF, exist_ok=True)
     summary = {}
-    for name in ("spmm", "upd", "bsr", "gram", "updmma", "gramwarp"):
+    for name in ("spmm", "upd", "bsr", "gram", "updmma", "gramwarp", "small"):
         rep = os.path.join(OUT, f"prof_{name}.ncu-rep")
         if not os.path.exists(rep):
             continue

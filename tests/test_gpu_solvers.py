@@ -270,9 +270,9 @@ def test_cuda_graph_replay_is_bitwise_identical(srk, method):
 
 @pytest.mark.parametrize("cplx", [False, True])
 def test_small_operator_single_kernel_iteration(srk, cplx):
-    """eGl-BiCG on a small operator runs each iteration as ONE single-CTA kernel
+    """eGl-BiCG on a small operator runs its iterations as ONE single-CTA kernel
     (egl_bicg_small_kernel: Alg. 4's steps separated by CTA barriers, the coefficient
-    phases the same device code): one launch per iteration, iterates in lock step with
+    phases the same device code): one launch per iterate() call, iterates in lock step with
     the oracle (envelope rule), and the same outcome as the multi-kernel sequence
     (SRK_NO_SMALL_KERNEL=1, checked in a subprocess: the switch is read once)."""
     import os
@@ -286,7 +286,9 @@ def test_small_operator_single_kernel_iteration(srk, cplx):
     sv.profile(True)
     sv.iterate(5)
     recs = sv.profile_launches()
-    assert len(recs) == 5, recs  # one launch per iteration (the end-of-iteration step included)
+    assert len(recs) == 1, recs  # the five iterations (end-of-iteration steps included) in one launch
+    sv.profile(False)
+    assert sv.report().iterations == 7
     sv.close()
     a, _, env = envelope("egl_bicg", A.to_scipy(), B, 1e-8)
     sv, xs = lockstep(srk, M, B, "egl_bicg", min(K, a.iterations), 1e-8)
