@@ -745,6 +745,146 @@ __global__ void __launch_bounds__(1024) egl_bicg_small_kernel(SmallBiCGArgs g) {
   }  // iterations
 }
 
+template <typename T>
+__global__ void __launch_bounds__(1024) egl_qmr_small_kernel(SmallQMRArgs g) {
+  CoefArgs a = g.ca;
+  if (a.ctl[CTL_FLAG] != FLAG_RUN) return;
+  __shared__ T red[32];
+  __shared__ double redd[32];
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const long long n = g.n;
+  const int s = a.s;
+  const T* val = reinterpret_cast<const T*>(g.val);
+  const T* valH = reinterpret_cast<const T*>(g.valH);
+  T* X = reinterpret_cast<T*>(g.X);
+  T* R = reinterpret_cast<T*>(g.R);
+  T* Vt = reinterpret_cast<T*>(g.Vt);
+  T* P = reinterpret_cast<T*>(g.P);
+  T* Pt = reinterpret_cast<T*>(g.Pt);
+  T* Dd = reinterpret_cast<T*>(g.D);
+  T* S = reinterpret_cast<T*>(g.S);
+  T* Wt = reinterpret_cast<T*>(g.Wt);
+  T* Qv = reinterpret_cast<T*>(g.Qv);
+  T* AHQ = reinterpret_cast<T*>(g.AHQ);
+  const T zero = Ar<T>::zero();
+  auto neg = [&](T v) { return Ar<T>::sub(zero, v); };
+  for (int it = 0; it < g.iters; ++it) {
+  if (it > 0 && a.ctl[CTL_FLAG] != FLAG_RUN) return;
+  a.phase = 1;
+  a.k1 = 0;
+  qmr_scalar<T>(a, 2);  // 1/rho, 1/xi
+  if (a.ctl[CTL_FLAG] != FLAG_RUN) return;
+  a.phase = 2;
+  a.k1 = a.ctl[CTL_ITER] == 0 ? 1 : 0;  // the first iteration (host_iter == 0 in QMR::seg)
+  qmr_scalar<T>(a, 2);  // delta, c1, c2
+  if (a.ctl[CTL_FLAG] != FLAG_RUN) return;
+  {
+    const T ir = *W<T>(a, SL_INVRHO), ix = *W<T>(a, SL_INVXI);
+    const T mc1 = neg(*W<T>(a, SL_C1)), mc2 = neg(*W<T>(a, SL_C2));
+    for (long long i = tid; i < n; i += nt) {  // P = Ṽ/rho - c1 P ; q = w̃/xi - c2 q
+      for (int c = 0; c < s; ++c) {
+        const size_t k = (size_t)i * s + c;
+        P[k] = Ar<T>::fma(P[k], mc1, Ar<T>::mul(Vt[k], ir));
+      }
+      Qv[i] = Ar<T>::fma(Qv[i], mc2, Ar<T>::mul(Wt[i], ix));
+    }
+  }
+  __syncthreads();
+  // P~ = A P ; eps = sum(q^H P~) ; A^H q
+  T part = zero;
+  for (long long i = tid; i < n; i += nt) {
+    const int b = g.rp[i], e = g.rp[i + 1];
+    T rs = zero;
+    for (int c = 0; c < s; ++c) {
+      T acc = zero;
+      for (int p = b; p < e; ++p) acc = Ar<T>::fma(val[p], P[(size_t)g.ci[p] * s + c], acc);
+      Pt[(size_t)i * s + c] = acc;
+      rs = Ar<T>::add(rs, acc);
+    }
+    part = Ar<T>::cfma(Qv[i], rs, part);
+    const int bh = g.rpH[i], eh = g.rpH[i + 1];
+    T acc = zero;
+    for (int p = bh; p < eh; ++p) acc = Ar<T>::fma(valH[p], Qv[g.ciH[p]], acc);
+    AHQ[i] = acc;
+  }
+  const T eps = cta_sum(part, red);
+  if (tid == 0) *W<T>(a, SL_EPS) = eps;
+  __syncthreads();
+  a.phase = 3;
+  qmr_scalar<T>(a, 2);  // beta, BR, BX
+  if (a.ctl[CTL_FLAG] != FLAG_RUN) return;
+  {
+    const T mbx = neg(*W<T>(a, SL_BX)), mbr = neg(*W<T>(a, SL_BR));
+    double xi2 = 0.0, rn2 = 0.0;
+    T k1 = zero;
+    for (long long i = tid; i < n; i += nt) {  // W̃ = A^H q - (conj(beta)/xi) W̃ ; Ṽ = P~ - (beta/rho) Ṽ
+      const T w = Ar<T>::fma(Wt[i], mbx, AHQ[i]);
+      Wt[i] = w;
+      xi2 += Ar<T>::abs2(w);
+      T rs = zero;
+      for (int c = 0; c < s; ++c) {
+        const size_t k = (size_t)i * s + c;
+        const T v = Ar<T>::fma(Vt[k], mbr, Pt[k]);
+        Vt[k] = v;
+        rn2 += Ar<T>::abs2(v);
+        rs = Ar<T>::add(rs, v);
+      }
+      k1 = Ar<T>::cfma(w, rs, k1);
+    }
+    const double xs = cta_sum(xi2, redd);
+    const double rs2 = cta_sum(rn2, redd);
+    const T k1s = cta_sum(k1, red);
+    if (tid == 0) {
+      *D(a, SL_XI2) = xs;
+      *D(a, SL_RHON2) = rs2;
+      *W<T>(a, SL_K1) = k1s;
+    }
+    __syncthreads();
+  }
+  a.phase = 4;
+  qmr_scalar<T>(a, 2);  // theta, gamma, eta, f
+  if (a.ctl[CTL_FLAG] != FLAG_RUN) return;
+  {
+    const T eta = *W<T>(a, SL_ETA), f = *W<T>(a, SL_F);
+    double r2 = 0.0;
+    for (long long i = tid; i < n; i += nt) {  // D = P eta + D f ; S = P~ eta + S f ; X += D ; R -= S
+      for (int c = 0; c < s; ++c) {
+        const size_t k = (size_t)i * s + c;
+        const T d = Ar<T>::fma(Dd[k], f, Ar<T>::mul(P[k], eta));
+        const T sv = Ar<T>::fma(S[k], f, Ar<T>::mul(Pt[k], eta));
+        Dd[k] = d;
+        S[k] = sv;
+        X[k] = Ar<T>::add(X[k], d);
+        const T r = Ar<T>::sub(R[k], sv);
+        R[k] = r;
+        r2 += Ar<T>::abs2(r);
+      }
+    }
+    const double r2s = cta_sum(r2, redd);
+    if (tid == 0) *D(a, SL_R2) = r2s;
+    __syncthreads();
+  }
+  a.phase = 5;
+  qmr_scalar<T>(a, 2);  // convergence test
+  if (a.ctl[CTL_FLAG] != FLAG_RUN) return;
+  if (tid == 0) {
+    a.ctl[CTL_ITER] += 1;
+    if (a.ctl[CTL_CONVPEND]) {
+      a.ctl[CTL_CONVPEND] = 0;
+      a.ctl[CTL_FLAG] = FLAG_CONV;
+    }
+  }
+  __syncthreads();
+  }  // iterations
+}
+
+int launch_egl_qmr_small(bool cplx, const SmallQMRArgs& g, cudaStream_t st) {
+  const int threads = (int)std::min<long long>(1024, std::max<long long>(32, (g.n + 31) / 32 * 32));
+  if (cplx) egl_qmr_small_kernel<double2><<<1, threads, 0, st>>>(g);
+  else egl_qmr_small_kernel<double><<<1, threads, 0, st>>>(g);
+  return (int)cudaGetLastError();
+}
+
 int launch_egl_bicg_small(bool cplx, const SmallBiCGArgs& g, cudaStream_t st) {
   const int threads = (int)std::min<long long>(1024, std::max<long long>(32, (g.n + 31) / 32 * 32));
   if (cplx) egl_bicg_small_kernel<double2><<<1, threads, 0, st>>>(g);

@@ -77,6 +77,22 @@ struct SmallBiCGArgs {
   CoefArgs ca;
 };
 int launch_egl_bicg_small(bool cplx, const SmallBiCGArgs& g, cudaStream_t st);
+// The same for eGl-QMR (the 18-block plan of QMR::seg): the coefficient
+// phases 1-5 of qmr_scalar, the P / q and W̃ / Ṽ / (D, S, X, R) updates with their
+// reductions, and Q~ = A P with sum(q^H P~), A^H q.
+struct SmallQMRArgs {
+  const int* rp;
+  const int* ci;
+  const void* val;
+  const int* rpH;
+  const int* ciH;
+  const void* valH;
+  void *X, *R, *Vt, *P, *Pt, *D, *S, *Wt, *Qv, *AHQ;
+  long long n;
+  int iters;
+  CoefArgs ca;
+};
+int launch_egl_qmr_small(bool cplx, const SmallQMRArgs& g, cudaStream_t st);
 constexpr long long SMALL_N_MAX = 16384;  // one-CTA eGl-BiCG up to this many rows
 
 }  // namespace srk

@@ -368,7 +368,7 @@ struct EglBiCG : Solver {  // Alg. 4
   // small operators (latency-bound): the whole iteration as one single-CTA kernel
   bool small() const {
     static const bool off_env = getenv("SRK_NO_SMALL_KERNEL") != nullptr;  // A/B switch
-    return !off_env && A && !A->bsr && !A->prec && !A->dist && A->has_adj && n <= SMALL_N_MAX &&
+    return !off_env && A && !A->bsr && !A->prec && A->ghost_rows() == 0 && A->has_adj && n <= SMALL_N_MAX &&
            !(c->comm && c->comm->nranks > 1);
   }
   bool ends_iter() const override { return small(); }
@@ -674,7 +674,47 @@ struct QMR : Solver {  // mode 0 Li, 1 Gl, 2 eGl
     cudaMemsetAsync(Qv, 0, (size_t)n * ws_() * esz(), c->st);
     return coef(0);
   }
+  // small operators (latency-bound), eGl only: the whole iteration as one single-CTA kernel
+  bool small() const {
+    static const bool off_env = getenv("SRK_NO_SMALL_KERNEL") != nullptr;  // A/B switch
+    return mode == 2 && !off_env && A && !A->bsr && !A->prec && A->ghost_rows() == 0 && A->has_adj && n <= SMALL_N_MAX &&
+           !(c->comm && c->comm->nranks > 1);
+  }
+  bool ends_iter() const override { return small(); }
+  int seg_multi(int k) override {
+    if (!small() || k < 1 || e.err) return 0;
+    launch_small(k);
+    return k;
+  }
+  void launch_small(int iters) {
+    SmallQMRArgs g{};
+    g.rp = A->rp;
+    g.ci = A->ci;
+    g.val = A->val;
+    g.rpH = A->rpH;
+    g.ciH = A->ciH;
+    g.valH = A->valH;
+    g.X = X; g.R = R; g.Vt = Vt; g.P = P; g.Pt = Pt; g.D = D; g.S = S; g.Wt = Wt; g.Qv = Qv; g.AHQ = AHQ;
+    g.n = n;
+    g.iters = iters;
+    g.ca.method = method;
+    g.ca.s = s;
+    g.ca.tol = o.tol;
+    g.ca.ws = ws;
+    g.ca.ctl = ctl;
+    g.ca.hist = hist;
+    g.ca.hist_cap = hist_cap;
+    for (int i = 0; i < NSLOT; ++i) g.ca.off[i] = off[i];
+    e.nlaunch++;
+    prof.begin(PT_OTHER, c->st);
+    e.err = launch_egl_qmr_small(cplx, g, c->st);
+    prof.end(c->st);
+  }
   void seg(int) override {
+    if (small()) {
+      if (!e.err) launch_small(1);
+      return;
+    }
     coef(1);                   // 1/rho, 1/xi
     coef(2, host_iter == 0);   // delta = <Ṽ, W̃>/(rho xi); c1 = xi delta/eps, c2 = conj(rho delta/eps)
     // P = V - c1 P = Ṽ/rho - c1 P ;  Q = W - c2 Q = W̃/xi - c2 Q

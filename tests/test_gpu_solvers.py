@@ -268,19 +268,21 @@ def test_cuda_graph_replay_is_bitwise_identical(srk, method):
     assert np.array_equal(out[0][0], out[1][0])
 
 
+@pytest.mark.parametrize("method", ["egl_bicg", "egl_qmr"])
 @pytest.mark.parametrize("cplx", [False, True])
-def test_small_operator_single_kernel_iteration(srk, cplx):
-    """eGl-BiCG on a small operator runs its iterations as ONE single-CTA kernel
-    (egl_bicg_small_kernel: Alg. 4's steps separated by CTA barriers, the coefficient
-    phases the same device code): one launch per iterate() call, iterates in lock step with
-    the oracle (envelope rule), and the same outcome as the multi-kernel sequence
+def test_small_operator_single_kernel_iteration(srk, cplx, method):
+    """eGl-BiCG / eGl-QMR on a small operator run their iterations as ONE single-CTA
+    kernel (egl_bicg_small_kernel / egl_qmr_small_kernel: the steps of Alg. 4 / App. A.2
+    separated by CTA barriers, the coefficient phases the same device code): one launch
+    per iterate() call, iterates in lock step with the oracle (envelope rule), and the
+    same outcome as the multi-kernel sequence
     (SRK_NO_SMALL_KERNEL=1, checked in a subprocess: the switch is read once)."""
     import os
     import subprocess
     import sys
     A, B = _problem("cplx" if cplx else "cfg1")
     M = srk.Matrix.from_csr(A, need_adjoint=True)
-    sv = srk.Solver(M, B.shape[1], "egl_bicg", tol=1e-8, maxit=2000, poll_every=1)
+    sv = srk.Solver(M, B.shape[1], method, tol=1e-8, maxit=2000, poll_every=1)
     sv.start(to_dev(B))
     sv.iterate(2)
     sv.profile(True)
@@ -290,12 +292,12 @@ def test_small_operator_single_kernel_iteration(srk, cplx):
     sv.profile(False)
     assert sv.report().iterations == 7
     sv.close()
-    a, _, env = envelope("egl_bicg", A.to_scipy(), B, 1e-8)
-    sv, xs = lockstep(srk, M, B, "egl_bicg", min(K, a.iterations), 1e-8)
+    a, _, env = envelope(method, A.to_scipy(), B, 1e-8)
+    sv, xs = lockstep(srk, M, B, method, min(K, a.iterations), 1e-8)
     for k, x in enumerate(xs):
         assert rel(x, a.Xs[k]) <= env[k], (k, rel(x, a.Xs[k]), env[k])
     sv.close()
-    X, rep = srk.solve(M, to_dev(B), "egl_bicg", tol=1e-8, maxit=2000)
+    X, rep = srk.solve(M, to_dev(B), method, tol=1e-8, maxit=2000)
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     code = (f"import sys; sys.path.insert(0, {root!r})\n"
             "import numpy as np, torch, paper_1504_04395_b200 as srk\n"
@@ -303,7 +305,7 @@ def test_small_operator_single_kernel_iteration(srk, cplx):
             "srk.load_library()\n"
             f"A, B = _problem({'cplx' if cplx else 'cfg1'!r})\n"
             "M = srk.Matrix.from_csr(A, need_adjoint=True)\n"
-            "X, rep = srk.solve(M, torch.from_numpy(B).cuda(), 'egl_bicg', tol=1e-8, maxit=2000)\n"
+            f"X, rep = srk.solve(M, torch.from_numpy(B).cuda(), {method!r}, tol=1e-8, maxit=2000)\n"
             "print(rep.outcome, rep.iterations)\n")
     out = subprocess.run([sys.executable, "-c", code], env={**os.environ, "SRK_NO_SMALL_KERNEL": "1"},
                          capture_output=True, text=True, timeout=600)
