@@ -312,3 +312,23 @@ def test_small_operator_single_kernel_iteration(srk, cplx, method):
     outcome, its = out.stdout.split()[-2:]
     assert outcome == rep.outcome and abs(int(its) - rep.iterations) <= max(2, 0.02 * rep.iterations), \
         (out.stdout, out.stderr[-400:], rep)
+
+
+@pytest.mark.parametrize("method", ["egl_bicg", "egl_qmr"])
+@pytest.mark.parametrize("s", [1, 12])
+def test_small_operator_widths(srk, method, s):
+    """The single-CTA kernels at the widths their register paths do not cover by
+    default (s = 1; s = 12 > 8 takes the column-loop product), on a ragged row count
+    (n = 29^2 = 841, not a multiple of the CTA's warps): lock step with the oracle
+    over 20 iterations, then a full solve meeting the tolerance."""
+    A = synth.conv_diff_2d(29, (20.0, 20.0))
+    B = synth.random_rhs(A.n, s, 5)
+    M = srk.Matrix.from_csr(A, need_adjoint=True)
+    a, _, env = envelope(method, A.to_scipy(), B, 1e-8)
+    sv, xs = lockstep(srk, M, B, method, min(K, a.iterations), 1e-8)
+    for k, x in enumerate(xs):
+        assert rel(x, a.Xs[k]) <= env[k], (k, rel(x, a.Xs[k]), env[k])
+    sv.close()
+    X, rep = srk.solve(M, to_dev(B), method, tol=1e-8, maxit=2000)
+    assert rep.outcome == "converged"
+    assert np.linalg.norm(B - A.to_scipy() @ to_np(X)) / np.linalg.norm(B) <= 1e-8
