@@ -113,3 +113,33 @@ def test_preconditioned_x0(srk):
     assert rep.outcome == "converged"
     assert np.linalg.norm(B - As @ to_np(sv.x())) <= 1e-10 * np.linalg.norm(B - As @ X0) * 1.01
     sv.close()
+
+
+def test_precond_apply_large_many_levels(srk):
+    """The sync-free triangular solves at the paper's Ex. 2 size (50^3 = 125,000 rows,
+    ~150 levels, every CTA of the grid taking rows): M^-1 P against the oracle's
+    triangular solves, and bitwise equal to the one-launch-per-level schedule
+    (SRK_TRSV_LEVELS=1, run in a subprocess: the switch is read once)."""
+    import os
+    import subprocess
+    import sys
+    A, _ = synth.paper_ex2(50, 1000.0)
+    As = A.to_scipy()
+    M = srk.Matrix.from_csr(A, need_adjoint=True).ilu0()
+    L, U = OP.ilu0(As)
+    P = synth.random_rhs(A.n, 4, 13)
+    Z = to_np(srk.precond_apply(M, to_dev(P)))
+    assert rel(Z, OP.apply_inv(L, U, P)) < 1e-12
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = (f"import sys; sys.path.insert(0, {root!r})\n"
+            "import numpy as np, torch, synth, paper_1504_04395_b200 as srk\n"
+            "srk.load_library()\n"
+            "A, _ = synth.paper_ex2(50, 1000.0)\n"
+            "M = srk.Matrix.from_csr(A, need_adjoint=True).ilu0()\n"
+            "P = synth.random_rhs(A.n, 4, 13)\n"
+            "Z = srk.precond_apply(M, torch.from_numpy(P).cuda()).cpu().numpy()\n"
+            "sys.stdout.buffer.write(Z.tobytes())\n")
+    out = subprocess.run([sys.executable, "-c", code], env={**os.environ, "SRK_TRSV_LEVELS": "1"},
+                         capture_output=True, timeout=600)
+    Zl = np.frombuffer(out.stdout, dtype=np.float64).reshape(Z.shape)
+    assert np.array_equal(Z, Zl)
