@@ -239,6 +239,22 @@ int Eng::spmm(bool adj, const void* P, void* Q, int s, std::vector<RQ> reds) {
 
 int Eng::upd(int s, std::vector<const void*> in, std::vector<OutSpec> outs, std::vector<RQ> reds) {
   if (err) return err;
+  // An n-vector update (s = 1) with one-or-scalar coefficients and only norm / trace
+  // reductions does not depend on the row structure: run it as an (n/4) x 4 block
+  // (two lanes per row with 16-byte loads instead of one 8-byte element per lane).
+  if (s == 1 && n % 4 == 0 && n >= 4) {
+    bool flat = true;
+    for (const OutSpec& o : outs)
+      for (const TermSpec& t : o.t) flat &= (t.c.kind == CK_ONE || t.c.kind == CK_SCALAR);
+    for (const RQ& r : reds) flat &= (r.mode == RED_NORM2 || r.mode == RED_TRACE);
+    if (flat) {
+      const long long n0 = n;
+      n = n0 / 4;
+      const int r = upd(4, std::move(in), std::move(outs), std::move(reds));
+      n = n0;
+      return r;
+    }
+  }
   // an external n x s reduction operand becomes one more input, so its rows are
   // requested together with the other inputs instead of after the outputs
   for (RQ& r : reds)
