@@ -922,9 +922,8 @@ int launch_spmm_t(const SpmmArgs& a, int grid, int block, size_t smem, cudaStrea
   return launch_spmm_tx<T, S, FC, false>(a, grid, block, smem, st);
 }
 
-template <typename T, int S, bool FC, int NI, bool EX>
+template <typename T, int S, bool FC, int NI, bool EX, int R = upd_rows<T, NI>()>
 int launch_upd_nix(const UpdArgs& a, int grid, int block, size_t smem, cudaStream_t st) {
-  constexpr int R = upd_rows<T, NI>();
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(upd_kernel<T, S, FC, NI, R, EX>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -944,6 +943,11 @@ int launch_upd_ni(const UpdArgs& a, int grid, int block, size_t smem, cudaStream
   // exact-width variant only for the scalar/diagonal (non-block) instances
   if constexpr (!FC) {
     const bool ex = a.s == S && (sizeof(T) == 16 || S % 2 == 0);
+    // two-input updates with fused reductions: one row per lane group (the reduction
+    // path's registers no longer spill; config 3's V~ update 1.243 -> 1.195 ms), two
+    // rows without reductions (the plain axpy keeps its 96%)
+    if constexpr (NI == 2 && upd_rows<T, 2>() == 2)
+      if (grid >= 0 && ex && a.nred > 0) return launch_upd_nix<T, S, FC, NI, true, 1>(a, grid, block, smem, st);
     if (grid < 0 || ex) return launch_upd_nix<T, S, FC, NI, true>(a, grid, block, smem, st);
   }
   return launch_upd_nix<T, S, FC, NI, false>(a, grid, block, smem, st);
