@@ -156,9 +156,32 @@ int srk_plan_destroy(srk_plan* p);
 /* NCCL communicator of the context (NCCL resolved at run time): rank 0 calls
  * srk_nccl_unique_id, broadcasts the 128 bytes (e.g. torch.distributed), every
  * rank calls srk_comm_init. With a communicator every reduction of the solver is
- * followed by an in-place FP64 ncclAllReduce and every SpMM by a halo exchange. */
+ * followed by an FP64 ncclAllReduce (the solver's: out of place, from a staging copy
+ * of its workspace, so a reduction skipped after the stop flag cannot rescale a
+ * carried value; kernel-level calls: in place) and every SpMM by a halo exchange. */
 int srk_nccl_unique_id(void* id128_host);
 int srk_comm_init(srk_ctx* ctx, const void* id128_host, int nranks, int rank);
+
+/* Single-GPU virtual partition (SURVEY §4 "Multi-GPU without a cluster"): k virtual
+ * ranks of one row-partitioned operator on ONE GPU, each driven by its own host thread
+ * with its own srk_ctx (and stream) attached by srk_comm_init_virtual. Every solver and
+ * kernel-level call then runs the distributed code path (halo exchange before each
+ * SpMM, one allreduce per reduction point) with a device-to-device transport: halo rows
+ * are copied out of the peers' send buffers, partial sums are reduced in rank order.
+ * Collectives are rendezvous points: all k threads must make the same sequence of calls
+ * (a thread that stops calling blocks the others). The group must outlive the contexts
+ * attached to it. Errors: SRK_EINVAL (k < 1 or k > 16, bad rank). */
+typedef struct srk_vgroup srk_vgroup;
+int srk_vgroup_create(int k, srk_vgroup** out);
+int srk_vgroup_destroy(srk_vgroup* g);
+int srk_comm_init_virtual(srk_ctx* ctx, srk_vgroup* g, int rank);
+
+/* A^H = conj(A)^T of a HOST CSR (a0), for building the adjoint operator of a
+ * distributed matrix on every rank's host before srk_plan_create: row_ptr_out (n+1),
+ * col_out (nnz, ascending within each row), values_out (nnz, dtype). Caller-owned
+ * arrays. Errors: SRK_EINVAL (null pointers, n <= 0, bad dtype, column out of range). */
+int srk_csr_adjoint_host(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, const void* values, int dtype,
+                         int64_t* row_ptr_out, int32_t* col_out, void* values_out);
 
 /* halo of one local operator (host arrays): rows received from / sent to each peer */
 typedef struct {

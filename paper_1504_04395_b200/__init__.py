@@ -35,6 +35,7 @@ EXPORTS = ("srk_create", "srk_destroy", "srk_last_error", "srk_version", "srk_ma
            "srk_solver_get_residual", "srk_solver_report", "srk_solver_history", "srk_solver_profile",
            "srk_solver_profile_read", "srk_solver_profile_launches", "srk_partition_rows", "srk_plan_create", "srk_plan_sizes", "srk_plan_arrays",
            "srk_plan_destroy", "srk_nccl_unique_id", "srk_comm_init", "srk_matrix_create_dist",
+           "srk_vgroup_create", "srk_vgroup_destroy", "srk_comm_init_virtual", "srk_csr_adjoint_host",
            "srk_matrix_create_bsr", "srk_matrix_ilu0", "srk_matrix_ilu0_factor", "srk_precond_apply")
 
 
@@ -117,6 +118,10 @@ def load_library(path: str | None = None):
         "srk_plan_destroy": ([vp], i),
         "srk_nccl_unique_id": ([vp], i),
         "srk_comm_init": ([vp, vp, i, i], i),
+        "srk_vgroup_create": ([i, ctypes.POINTER(vp)], i),
+        "srk_vgroup_destroy": ([vp], i),
+        "srk_comm_init_virtual": ([vp, vp, i], i),
+        "srk_csr_adjoint_host": ([i64, vp, vp, vp, i, vp, vp, vp], i),
         "srk_matrix_create_dist": ([vp, ctypes.POINTER(_Csr), i64, ctypes.POINTER(_Halo), ctypes.POINTER(_Csr), i64,
                                     ctypes.POINTER(_Halo)], i),
     }
@@ -357,11 +362,57 @@ def init_distributed(ctx: "Context | None" = None):
     return ctx
 
 
+class VirtualGroup:
+    """srk_vgroup: k virtual ranks of a row-partitioned operator on ONE GPU.
+    Each rank gets its own Context (own stream) attached with `attach`, and its own host
+    thread that makes the same sequence of library calls as the others (collectives are
+    rendezvous points); the transport is device-to-device, reductions in rank order."""
+
+    def __init__(self, k: int):
+        lib = load_library()
+        h = ctypes.c_void_p()
+        _check(lib.srk_vgroup_create(k, ctypes.byref(h)), "srk_vgroup_create")
+        self.h = h
+        self.k = k
+
+    def attach(self, ctx: "Context", rank: int) -> "Context":
+        _check(_lib.srk_comm_init_virtual(ctx.h, self.h, rank), "srk_comm_init_virtual")
+        return ctx
+
+    def close(self):
+        if getattr(self, "h", None):
+            _lib.srk_vgroup_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def csr_adjoint_host(row_ptr, col_idx, values):
+    """A^H = conj(A)^T of a host CSR, computed by the library (srk_csr_adjoint_host)."""
+    lib = load_library()
+    rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
+    ci = np.ascontiguousarray(col_idx, dtype=np.int32)
+    va = np.ascontiguousarray(values)
+    if va.dtype not in (np.float64, np.complex128):
+        raise SrkError("values must be float64 or complex128")
+    n = rp.size - 1
+    rpT = np.zeros(n + 1, np.int64)
+    ciT = np.zeros(max(ci.size, 1), np.int32)
+    vaT = np.zeros(max(va.size, 1), va.dtype)
+    dt = SRK_C128 if va.dtype == np.complex128 else SRK_F64
+    _check(lib.srk_csr_adjoint_host(n, _np_ptr(rp), _np_ptr(ci), _np_ptr(va), dt, _np_ptr(rpT), _np_ptr(ciT),
+                                    _np_ptr(vaT)), "srk_csr_adjoint_host")
+    return rpT, ciT[:ci.size], vaT[:va.size]
+
+
 class DistMatrix:
     """srk_matrix_create_dist: this rank's rows of A (and of A^H) with halo plans."""
 
     def __init__(self, A, offsets, rank: int, need_adjoint: bool = True, ctx: "Context | None" = None):
-        import scipy.sparse as sp
         torch = _torch()
         self.ctx = ctx or default_context()
         dev = torch.device("cuda", self.ctx.device)
@@ -396,11 +447,10 @@ class DistMatrix:
         csrH = haloH = None
         ngH = 0
         if need_adjoint:
-            AH = sp.csr_matrix((va, ci, rp), shape=(n, n)).conj().T.tocsr()
-            AH.sort_indices()
-            self.planH = make_plan(AH.indptr, AH.indices, self.offsets, rank)
-            lo, hi = int(AH.indptr[self.planH.off0]), int(AH.indptr[self.planH.off1])
-            csrH = csr_struct(self.planH, AH.data[lo:hi])
+            rpH, ciH, vaH = csr_adjoint_host(rp, ci, va)   # a0 inside the library
+            self.planH = make_plan(rpH, ciH, self.offsets, rank)
+            lo, hi = int(rpH[self.planH.off0]), int(rpH[self.planH.off1])
+            csrH = csr_struct(self.planH, vaH[lo:hi])
             haloH = halo_struct(self.planH)
             ngH = self.planH.ghosts.size
         h = ctypes.c_void_p()

@@ -269,6 +269,38 @@ int srk_comm_init(srk_ctx* ctx, const void* id128_host, int nranks, int rank) {
   return SRK_OK;
 }
 
+struct srk_vgroup {
+  VGroup* g;
+};
+
+int srk_vgroup_create(int k, srk_vgroup** out) {
+  if (!out || k < 1 || k > 16) return fail(SRK_EINVAL, "srk_vgroup_create: k must be in [1, 16]");
+  VGroup* g = vgroup_create(k);
+  if (!g) return fail(SRK_ECUDA, "srk_vgroup_create: event creation failed");
+  *out = new srk_vgroup{g};
+  return SRK_OK;
+}
+
+int srk_vgroup_destroy(srk_vgroup* g) {
+  if (!g) return SRK_OK;
+  vgroup_destroy(g->g);
+  delete g;
+  return SRK_OK;
+}
+
+int srk_comm_init_virtual(srk_ctx* ctx, srk_vgroup* g, int rank) {
+  if (!ctx || !g || rank < 0 || rank >= vgroup_size(g->g)) return fail(SRK_EINVAL, "srk_comm_init_virtual: bad argument");
+  if (ctx->c.comm) comm_destroy(ctx->c.comm);
+  ctx->c.comm = nullptr;
+  if (vgroup_size(g->g) == 1) return SRK_OK;
+  auto* C = new Comm();
+  C->nranks = vgroup_size(g->g);
+  C->rank = rank;
+  C->vg = g->g;
+  ctx->c.comm = C;
+  return SRK_OK;
+}
+
 static int upload_halo(Halo& H, const srk_halo* h, int nranks, long long n_ghost) {
   H.nranks = nranks;
   H.n_ghost = n_ghost;

@@ -421,10 +421,9 @@ int launch_w(const UpdArgs& a, int cplx, int nterm, int grid, cudaStream_t st) {
   const int w = a.s * (cplx ? 2 : 1);
   const int stg = pick_stages(a, w, W, nterm);
   const size_t smem = smem_bytes(W, w, nterm, a.nin, stg);
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<unsigned long long> attr{0};
+  if (first_on_device(attr)) {
     cudaFuncSetAttribute(upd_mma_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
   }
   if (grid < 0) {
     int occ = 0;

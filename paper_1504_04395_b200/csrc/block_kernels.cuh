@@ -878,10 +878,9 @@ template <typename T, int S> constexpr bool full_ok() { return S <= 32; }
 template <typename T, int S, bool FC, bool EX>
 int launch_spmm_tx(const SpmmArgs& a, int grid, int block, size_t smem, cudaStream_t st) {
   constexpr int R = spmm_rows<T, S>();
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<unsigned long long> attr{0};
+  if (first_on_device(attr)) {
     cudaFuncSetAttribute(spmm_kernel<T, S, FC, R, EX>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
   }
   if (grid < 0) {
     int nb = 0;
@@ -924,10 +923,9 @@ int launch_spmm_t(const SpmmArgs& a, int grid, int block, size_t smem, cudaStrea
 
 template <typename T, int S, bool FC, int NI, bool EX, int R = upd_rows<T, NI>()>
 int launch_upd_nix(const UpdArgs& a, int grid, int block, size_t smem, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<unsigned long long> attr{0};
+  if (first_on_device(attr)) {
     cudaFuncSetAttribute(upd_kernel<T, S, FC, NI, R, EX>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
   }
   if (grid < 0) {
     int nb = 0;

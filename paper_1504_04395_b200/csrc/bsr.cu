@@ -272,10 +272,9 @@ __global__ void __launch_bounds__(256, S >= 16 ? 1 : 2) bsr12_kernel(BsrArgs a) 
 template <int S>
 int launch_s(const BsrArgs& a, int grid, cudaStream_t st) {
   using C = BCfg<S>;
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<unsigned long long> attr{0};
+  if (first_on_device(attr)) {
     cudaFuncSetAttribute(bsr12_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-    attr = true;
   }
   if (grid < 0) {  // resident CTAs per SM
     int occ = 0;

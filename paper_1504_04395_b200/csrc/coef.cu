@@ -604,11 +604,10 @@ __global__ void end_iter_kernel(int* ctl) {
 }
 
 int launch_coef(bool cplx, const CoefArgs& a, size_t smem, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<unsigned long long> attr{0};
+  if (first_on_device(attr)) {
     cudaFuncSetAttribute(coef_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(coef_kernel<double2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
   }
   if (cplx) coef_kernel<double2><<<1, 256, smem, st>>>(a);
   else coef_kernel<double><<<1, 256, smem, st>>>(a);

@@ -95,6 +95,10 @@ Comm* comm_create(const void* id128, int nranks, int rank) {
 
 void comm_destroy(Comm* C) {
   if (!C) return;
+  if (C->vg) {  // the group is owned by its srk_vgroup handle
+    delete C;
+    return;
+  }
   Nccl* N = nccl();
   if (N && N->commDestroy) N->commDestroy((ncclComm_t)C->nccl);
   delete C;
@@ -102,18 +106,20 @@ void comm_destroy(Comm* C) {
 
 int comm_allreduce_sum(Comm* C, double* buf, size_t count, cudaStream_t st) {
   if (!C || C->nranks == 1 || count == 0) return 0;
+  if (C->vg) return -5;  // the virtual group reduces out of place only (comm_allreduce_sum_many)
   Nccl* N = nccl();
   return N->allReduce(buf, buf, count, ncclFloat64, ncclSum, (ncclComm_t)C->nccl, st) == ncclSuccess ? 0 : -5;
 }
 
-int comm_allreduce_sum_many(Comm* C, double* const* bufs, const size_t* counts, int nbuf, cudaStream_t st) {
+int comm_allreduce_sum_many(Comm* C, const double* const* src, double* const* dst, const size_t* counts, int nbuf,
+                            cudaStream_t st) {
   if (!C || C->nranks == 1 || nbuf == 0) return 0;
-  if (nbuf == 1) return comm_allreduce_sum(C, bufs[0], counts[0], st);
+  if (C->vg) return vgroup_allreduce(C->vg, C->rank, src, dst, counts, nbuf, st);
   Nccl* N = nccl();
   if (N->groupStart() != ncclSuccess) return -5;
   int bad = 0;
   for (int i = 0; i < nbuf; ++i)
-    if (counts[i] && N->allReduce(bufs[i], bufs[i], counts[i], ncclFloat64, ncclSum, (ncclComm_t)C->nccl, st) != ncclSuccess)
+    if (counts[i] && N->allReduce(src[i], dst[i], counts[i], ncclFloat64, ncclSum, (ncclComm_t)C->nccl, st) != ncclSuccess)
       bad = 1;
   return (N->groupEnd() == ncclSuccess && !bad) ? 0 : -5;
 }
@@ -121,6 +127,7 @@ int comm_allreduce_sum_many(Comm* C, double* const* bufs, const size_t* counts, 
 int comm_halo(Comm* C, const double* sendbuf, const int64_t* send_off, double* recvbuf, const int64_t* recv_off,
               size_t doubles_per_row, cudaStream_t st) {
   if (!C || C->nranks == 1) return 0;
+  if (C->vg) return vgroup_halo(C->vg, C->rank, sendbuf, send_off, recvbuf, recv_off, doubles_per_row, st);
   Nccl* N = nccl();
   if (N->groupStart() != ncclSuccess) return -5;
   for (int p = 0; p < C->nranks; ++p) {

@@ -9,7 +9,19 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+
 namespace srk {
+
+// True the first time it is called for the current device with this mask: launch
+// attributes (cudaFuncSetAttribute) are per device context, so a per-kernel cache
+// must be keyed by device ordinal, and thread-safe (virtual ranks run on threads).
+inline bool first_on_device(std::atomic<unsigned long long>& seen) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long bit = 1ull << (dev & 63);
+  return (seen.fetch_or(bit) & bit) == 0;
+}
 
 // ---------------------------------------------------------------- scalars
 struct cplx { double x, y; };

@@ -114,23 +114,32 @@ static int finish_reds(Eng& e, const std::vector<RQ>& reds, const std::vector<in
     f.seg[i].len = red_len(reds[i].mode, s, e.cplx);
     f.seg[i].woff = reds[i].woff;
   }
-  f.ws = e.ws;
+  // multi-GPU: fin writes this rank's sums to a staging mirror of the workspace and the
+  // allreduce writes the global sums into ws (out of place). A fin skipped after the done
+  // flag was raised leaves the staging slot with its last real local sums, so the
+  // allreduce re-forms the same global value instead of scaling ws by the rank count.
+  // (kernel-level calls run every fin and have no staging: NCCL reduces them in place)
+  const bool multi = e.c->comm && e.c->comm->nranks > 1;
+  if (multi && !e.wstage && e.c->comm->vg) return (int)cudaErrorInvalidValue;
+  double* stage = (multi && e.wstage) ? e.wstage : e.ws;
+  f.ws = stage;
   f.done = e.done;
   e.nlaunch++;
   if (e.prof) e.prof->begin(PT_FIN, e.c->st);
   int r = launch_fin(f, e.c->st);
   if (e.prof) e.prof->end(e.c->st);
   if (r) return r;
-  // multi-GPU: the per-rank sums become global sums (same bits on every rank)
-  if (e.c->comm && e.c->comm->nranks > 1) {
+  if (multi) {
     if (e.prof) e.prof->begin(PT_OTHER, e.c->st);
-    std::vector<double*> bufs;
+    std::vector<const double*> src;
+    std::vector<double*> dst;
     std::vector<size_t> counts;
     for (size_t i = 0; i < reds.size(); ++i) {
-      bufs.push_back(e.ws + reds[i].woff);
+      src.push_back(stage + reds[i].woff);
+      dst.push_back(e.ws + reds[i].woff);
       counts.push_back((size_t)red_len(reds[i].mode, s, e.cplx));
     }
-    if (comm_allreduce_sum_many(e.c->comm, bufs.data(), counts.data(), (int)bufs.size(), e.c->st)) r = -5;
+    if (comm_allreduce_sum_many(e.c->comm, src.data(), dst.data(), counts.data(), (int)src.size(), e.c->st)) r = -5;
     if (e.prof) e.prof->end(e.c->st);
   }
   return r;
@@ -247,6 +256,12 @@ int Eng::upd(int s, std::vector<const void*> in, std::vector<OutSpec> outs, std:
     for (const OutSpec& o : outs)
       for (const TermSpec& t : o.t) flat &= (t.c.kind == CK_ONE || t.c.kind == CK_SCALAR);
     for (const RQ& r : reds) flat &= (r.mode == RED_NORM2 || r.mode == RED_TRACE);
+    // the (n/4) x 4 view loads 16 bytes per lane: every operand must be 16-byte aligned
+    // (a caller's view at an 8-byte offset, e.g. v[1:], keeps the element-wise path)
+    auto a16 = [](const void* p) { return p == nullptr || ((uintptr_t)p & 15) == 0; };
+    for (const void* p : in) flat &= a16(p);
+    for (const OutSpec& o : outs) flat &= a16(o.ptr);
+    for (const RQ& r : reds) flat &= a16(r.yext);
     if (flat) {
       const long long n0 = n;
       n = n0 / 4;

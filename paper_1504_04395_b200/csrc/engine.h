@@ -173,6 +173,7 @@ struct Eng {
   bool cplx = false;
   long long n = 0;
   double* ws = nullptr;   // coefficient workspace (device)
+  double* wstage = nullptr;  // multi-rank: per-rank sums before the allreduce (same layout as ws)
   const int* done = nullptr;
   int err = 0;            // first CUDA error
   int nlaunch = 0;        // kernels launched (instrumentation)

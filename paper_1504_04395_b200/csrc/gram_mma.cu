@@ -328,10 +328,9 @@ int launch_warp_w(const GramArgs& g, int grid, cudaStream_t st) {
   const int stg = stages_w<W>(g);
   const int nops = g.X == g.Y ? 1 : 2;
   const size_t smem = std::max<size_t>((size_t)8 * stg * nops * RT * (W + 2) * 8, (size_t)8 * W * W * 8);
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<unsigned long long> attr{0};
+  if (first_on_device(attr)) {
     cudaFuncSetAttribute(gram_warp_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
   }
   if (grid < 0) {
     int occ = 0;
@@ -345,10 +344,9 @@ int launch_warp_w(const GramArgs& g, int grid, cudaStream_t st) {
 template <int W>
 int launch_w(const GramArgs& g, int grid, cudaStream_t st) {
   using C = GCfg<W>;
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<unsigned long long> attr{0};
+  if (first_on_device(attr)) {
     cudaFuncSetAttribute(gram_mma_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-    attr = true;
   }
   if (grid < 0) {  // resident CTAs per SM
     int occ = 0;

@@ -140,4 +140,33 @@ int srk_plan_destroy(srk_plan* P) {
   return SRK_OK;
 }
 
+// A^H = conj(A)^T by a counting sort over the columns (a0): stable, so the
+// entries of each row of A^H come in ascending column order (the rows of A visited in
+// order). Host code: every rank of a distributed operator builds it from the global CSR
+// it already holds for srk_plan_create.
+int srk_csr_adjoint_host(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, const void* values, int dtype,
+                         int64_t* rpT, int32_t* ciT, void* valT) {
+  if (n <= 0 || !row_ptr || !rpT || (dtype != SRK_F64 && dtype != SRK_C128)) return SRK_EINVAL;
+  const int64_t nnz = row_ptr[n];
+  if (nnz > 0 && (!col_idx || !values || !ciT || !valT)) return SRK_EINVAL;
+  std::vector<int64_t> cnt(n + 1, 0);
+  for (int64_t k = 0; k < nnz; ++k) {
+    if (col_idx[k] < 0 || col_idx[k] >= n) return SRK_EINVAL;
+    cnt[col_idx[k] + 1]++;
+  }
+  for (int64_t j = 0; j < n; ++j) cnt[j + 1] += cnt[j];
+  std::copy(cnt.begin(), cnt.end(), rpT);
+  const int nd = dtype == SRK_C128 ? 2 : 1;
+  const double* v = static_cast<const double*>(values);
+  double* vT = static_cast<double*>(valT);
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t k = row_ptr[i]; k < row_ptr[i + 1]; ++k) {
+      const int64_t d = cnt[col_idx[k]]++;
+      ciT[d] = (int32_t)i;
+      vT[d * nd] = v[k * nd];
+      if (nd == 2) vT[d * nd + 1] = -v[k * nd + 1];  // conj
+    }
+  return SRK_OK;
+}
+
 }  // extern "C"

@@ -23,6 +23,7 @@ Solver::~Solver() {
   if (cap_st) cudaStreamDestroy(cap_st);
   for (void* p : owned) cudaFree(p);
   if (ws) cudaFree(ws);
+  if (wstage) cudaFree(wstage);
   if (ctl) cudaFree(ctl);
   if (hist) cudaFree(hist);
   if (ctl_host) cudaFreeHost(ctl_host);
@@ -49,6 +50,10 @@ int Solver::setup() {
   for (int i = 0; i < NSLOT; ++i) off[i] = (int)(i * sd);
   if (cudaMalloc(&ws, sd * NSLOT * sizeof(double)) != cudaSuccess) return SRK_ENOMEM;
   cudaMemset(ws, 0, sd * NSLOT * sizeof(double));
+  if (c->comm && c->comm->nranks > 1) {  // per-rank sums staged before each allreduce (engine.cu)
+    if (cudaMalloc(&wstage, sd * NSLOT * sizeof(double)) != cudaSuccess) return SRK_ENOMEM;
+    cudaMemset(wstage, 0, sd * NSLOT * sizeof(double));
+  }
   if (cudaMalloc(&ctl, CTL_SIZE * sizeof(int)) != cudaSuccess) return SRK_ENOMEM;
   if (cudaMallocHost(&ctl_host, CTL_SIZE * sizeof(int)) != cudaSuccess) return SRK_ENOMEM;
   hist_cap = o.maxit + 2;
@@ -58,6 +63,7 @@ int Solver::setup() {
   e.cplx = cplx;
   e.n = n;
   e.ws = ws;
+  e.wstage = wstage;
   e.done = ctl + CTL_FLAG;
   e.prof = &prof;
   B = blk();

@@ -21,6 +21,7 @@ struct Solver {
   Eng e;
   Prof prof;
   double* ws = nullptr;
+  double* wstage = nullptr;  // multi-rank: staging of the per-rank sums (engine.cu finish_reds)
   int* ctl = nullptr;
   int* ctl_host = nullptr;  // pinned mirror
   double* hist = nullptr;

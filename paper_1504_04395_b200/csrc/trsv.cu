@@ -103,7 +103,10 @@ __global__ void trsv_syncfree_kernel(const int* __restrict__ order, int nrows, c
         }
       }
     }
-    bad = __any_sync(0xffffffffu, bad);  // (also orders the observing lanes before the reads)
+    // __syncwarp orders every lane's acquire loads before any lane's reads of the
+    // dependencies' Z rows below (vote intrinsics alone carry no memory ordering)
+    __syncwarp();
+    bad = __any_sync(0xffffffffu, bad);
     for (int c = lane; c < s; c += 32) {
       T acc = R[(size_t)i * s + c];
       for (int p = b; p < e; ++p) {
@@ -132,13 +135,16 @@ int run_syncfree(const DevTri& t, long long n, int s, const void* R, void* Z, co
     if (cudaMalloc(&tm.flags, sizeof(int) * ((size_t)n + 1)) != cudaSuccess) return -(int)cudaErrorMemoryAllocation;
   }
   cudaMemsetAsync(tm.flags, 0, sizeof(int) * ((size_t)n + 1), st);
-  static int grid = 0;
+  static std::atomic<int> grids[64];  // per device ordinal (occupancy x SM count)
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int grid = grids[dev & 63].load();
   if (!grid) {
-    int dev = 0, nsm = 0, occ = 0;
-    cudaGetDevice(&dev);
+    int nsm = 0, occ = 0;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, trsv_syncfree_kernel<T>, 256, 0);
     grid = nsm * std::max(1, occ);
+    grids[dev & 63].store(grid);
   }
   const int g = (int)std::min<long long>(grid, ((long long)nrows + 7) / 8);
   trsv_syncfree_kernel<T><<<g, 256, 0, st>>>(t.order, nrows, t.rp, t.ci, reinterpret_cast<const T*>(t.val),

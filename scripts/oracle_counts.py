@@ -4,6 +4,7 @@ tests/golden/oracle_counts.json: per (config, method) the input hash, the oracle
 outcome, iteration count and final true residual at tol 1e-8, maxit 2000.
 
     python scripts/oracle_counts.py cfg2 bl_bicg_rq       # ~1 h of numpy on 16 cores
+    python scripts/oracle_counts.py cfg3 egl_qmr seq      # the second reduction order (SURVEY §8c.5 rule 3)
 """
 import json
 import os
@@ -17,20 +18,35 @@ import oracle  # noqa: E402
 import synth  # noqa: E402
 
 
-def main(cfg, method):
+def _progress():
+    """Print every 25th iteration's recursive residual (wraps _Run.step_done; no arithmetic)."""
+    import oracle.solvers as so
+    orig = so._Run.step_done
+
+    def step_done(self, k, *a, **kw):
+        out = orig(self, k, *a, **kw)
+        if k % 25 == 0 and self.res.history:
+            print(f"  it {k}: rel {self.res.history[-1]:.3e}", flush=True)
+        return out
+    so._Run.step_done = step_done
+
+
+def main(cfg, method, order="blas"):
+    _progress()
     num = int(cfg[3:])
     A, B = synth.make_config(num)
     t0 = time.time()
-    r = oracle.solve(method, A.to_scipy(), B, tol=1e-8, maxit=2000, record=0)
+    r = oracle.solve(method, A.to_scipy(), B, tol=1e-8, maxit=2000, record=0, order=order)
     path = os.path.join(ROOT, "tests", "golden", "oracle_counts.json")
     data = json.load(open(path)) if os.path.exists(path) else {}
-    data[f"{cfg}:{method}"] = {"inputs_hash": synth.input_hash(A, B), "outcome": r.outcome,
+    key = f"{cfg}:{method}" + ("" if order == "blas" else f":{order}")
+    data[key] = {"inputs_hash": synth.input_hash(A, B), "outcome": r.outcome,
                                "iterations": r.iterations, "half_step": r.half_step,
                                "final_true_rel_residual": r.final_true_rel_residual,
                                "tol": 1e-8, "maxit": 2000, "oracle_seconds": round(time.time() - t0, 1)}
     json.dump(data, open(path, "w"), indent=1, sort_keys=True)
-    print(cfg, method, data[f"{cfg}:{method}"], flush=True)
+    print(key, data[key], flush=True)
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], sys.argv[2])
+    main(*sys.argv[1:4])

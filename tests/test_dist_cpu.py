@@ -142,3 +142,22 @@ def test_partition_balances_nnz():
                 roff = np.concatenate([[0], np.cumsum(plans[qq].recv_counts)])
                 expected = plans[qq].ghosts[roff[p]:roff[p + 1]]
                 assert np.array_equal(sent, expected)
+
+
+@pytest.mark.parametrize("cplx", [False, True])
+def test_csr_adjoint_host_matches_conj_transpose(cplx):
+    """srk_csr_adjoint_host (a0 of the distributed operator) equals the
+    textbook conj(A)^T entry for entry, columns ascending within each row."""
+    import sys
+    sys.path.insert(0, ROOT)
+    import paper_1504_04395_b200 as srk
+    import synth
+    A = synth.random_sparse(500, 6, seed=11, dtype=np.complex128 if cplx else np.float64)
+    As = A.to_scipy()
+    rp, ci, va = srk.csr_adjoint_host(A.row_ptr, A.col_idx, A.values)
+    T = As.conj().T.tocsr()
+    T.sort_indices()
+    assert np.array_equal(rp, T.indptr) and np.array_equal(ci, T.indices)
+    assert np.array_equal(va, T.data)
+    for i in range(A.n):
+        assert np.all(np.diff(ci[rp[i]:rp[i + 1]]) > 0)

@@ -22,10 +22,21 @@ def srk():
     return srk
 
 
+def crel(a, b, method):
+    """Relative error of a block: whole-block Frobenius ratio, or for the Li variants
+    (s independent column recurrences) the worst per-column ratio, so a
+    column-local error in a small-norm column is not diluted by the others."""
+    if method.startswith("li_") and np.ndim(b) == 2:
+        return max(rel(a[:, j], b[:, j]) for j in range(b.shape[1]))
+    return rel(a, b)
+
+
 def envelope(method, As, B, tol, maxit=2000, k=K):
+    """SURVEY §8c.5 rule 2: the per-iteration bound max(1e-10, 100 max_{j<=k} delta_j),
+    delta the oracle's own spread between two reduction orders over X_k and R_k (C_k)."""
     a = oracle.solve(method, As, B, tol=tol, maxit=maxit, record=k, order="blas")
     b = oracle.solve(method, As, B, tol=tol, maxit=maxit, record=k, order="seq")
-    d = [rel(x, y) for x, y in zip(a.Xs, b.Xs)]
+    d = [max(crel(x, y, method), crel(r, q, method)) for x, y, r, q in zip(a.Xs, b.Xs, a.Rs, b.Rs)]
     env = np.maximum(1e-10, 100 * np.maximum.accumulate(d)) if d else np.array([])
     return a, b, env
 
@@ -33,12 +44,14 @@ def envelope(method, As, B, tol, maxit=2000, k=K):
 def lockstep(srk, M, B, method, n_it, tol):
     sv = srk.Solver(M, B.shape[1], method, tol=tol, maxit=2000, poll_every=1)
     sv.start(to_dev(B))
-    xs = []
+    xs, rs = [], []
     for _ in range(n_it):
         st = sv.iterate(1)
         xs.append(to_np(sv.x()))
+        rs.append(to_np(sv.residual()))
         if st != 0:
             break
+    sv.rs = rs
     return sv, xs
 
 
@@ -69,8 +82,10 @@ def test_lockstep_parity(srk, method, prob):
     n_cmp = min(len(xs), len(a.Xs))
     assert n_cmp >= 1
     for k in range(n_cmp):
-        err = rel(xs[k], a.Xs[k])
-        assert err <= env[k], (method, prob, k + 1, err, env[k])
+        err = crel(xs[k], a.Xs[k], method)
+        assert err <= env[k], (method, prob, k + 1, "X", err, env[k])
+        err = crel(sv.rs[k], a.Rs[k], method)
+        assert err <= env[k], (method, prob, k + 1, "R" if a.Rs[k].shape == B.shape else "C", err, env[k])
     sv.close()
 
 
@@ -103,11 +118,9 @@ def test_full_solve(srk, method, prob):
     hi = max(r.iterations for r in same)
     if rep.outcome == "converged":
         slack = max(0.02 * a.iterations, 2)
-        # the count is compared only where the method itself is stable under rounding
-        # (one outcome, spread within the north star's 2%); chaotic block variants on
-        # config 1 (Bl-BiCG) are held to the lock-step envelope and the true residual
-        if len(outcomes) == 1 and hi - lo <= slack:
-            assert lo - slack <= rep.iterations <= hi + slack, (rep.iterations, lo, hi)
+        # within the oracle ensemble's range (its reduction orders and 1e-15 perturbations
+        # of B) widened by max(2%, 2): SURVEY §8c.5 rule 3 with the ensemble's spread
+        assert lo - slack <= rep.iterations <= hi + slack, (rep.iterations, lo, hi)
         # the oracle's own SpMM recomputes the true residual from the GPU's X
         true = np.linalg.norm(B - As @ X) / np.linalg.norm(B)
         assert true <= tol

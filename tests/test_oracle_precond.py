@@ -73,3 +73,22 @@ def test_right_preconditioned_iterates_stay_in_the_preconditioned_space():
     prec = OP.solve_right("gl_bicgstab", As, Q, tol=1e-10, maxit=500, record=0)
     assert prec.outcome == "converged" and prec.iterations < plain.iterations
     assert np.linalg.norm(Q - As @ prec.X) / np.linalg.norm(Q) <= 1e-10
+
+
+def test_apply_inv_and_adjoint_against_dense_inverse():
+    """M^-1 P and M^-H P (the adjoint products of the BiCG / QMR families under
+    right preconditioning, (A M^-1)^H = M^-H A^H) against the dense inverse of the product
+    L U of a genuinely incomplete, complex factorisation: the triangular solves must come
+    in the order U^-1 L^-1 and L^-H U^-H (swapping either order changes the result)."""
+    A = synth.random_sparse(120, 5, seed=9, dtype=np.complex128, dominance=1.5).to_scipy()
+    L, U = OP.ilu0(A)
+    M = (L @ U).toarray()
+    assert np.linalg.norm(M - A.toarray()) > 1e-3  # fill dropped: M != A
+    P = synth.random_rhs(120, 3, 5, True)
+    Minv = np.linalg.inv(M)
+    assert np.max(np.abs(OP.apply_inv(L, U, P) - Minv @ P)) < 1e-11 * np.max(np.abs(Minv @ P))
+    ref = Minv.conj().T @ P
+    assert np.max(np.abs(OP.apply_inv_adj(L, U, P) - ref)) < 1e-11 * np.max(np.abs(ref))
+    # the swapped orders really differ here (the pin is not vacuous)
+    wrong = np.linalg.inv((U @ L).toarray()).conj().T @ P
+    assert np.max(np.abs(wrong - ref)) > 1e-6 * np.max(np.abs(ref))

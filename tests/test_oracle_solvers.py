@@ -314,3 +314,49 @@ def test_lattice_bsr_form_is_the_same_operator():
         D = (A.to_scipy() - B.tocsr()).tocsr()
         D.eliminate_zeros()
         assert D.nnz == 0
+
+
+def test_li_freeze_policy_unit():
+    """Reading G13 applied per column: a zero denominator OR a non-finite quotient
+    freezes the column with coefficient 0; frozen columns stay at 0; others divide."""
+    num = np.array([1.0, 1e300, 2.0, 3.0, np.nan])
+    den = np.array([0.0, 1e-300, 4.0, 5.0, 1.0])
+    frozen = np.array([False, False, False, True, False])
+    q, newly = S._safe_div(num, den, frozen)
+    assert np.array_equal(newly, [True, True, False, False, True])
+    assert np.array_equal(q, [0.0, 0.0, 0.5, 0.0, 0.0])
+
+
+def _skew_block_problem(cplx=False):
+    """A = blockdiag(S, M): S an integer skew-symmetric block, M diagonally dominant.
+    Column 0 of B lives on S with integer entries, so <q_0, p̂_0> = b_0^T S b_0 = 0
+    EXACTLY in floating point: the Lanczos denominator of Li-BiCG's column 0 vanishes
+    at the first iteration, while column 1 is an ordinary BiCG problem."""
+    rng = np.random.default_rng(21)
+    m = 6
+    Sk = np.triu(rng.integers(-3, 4, (m, m)), 1).astype(float)
+    Sk = Sk - Sk.T
+    Mb = synth.random_sparse(40, 4, 5, np.complex128 if cplx else np.float64, 0.8).to_scipy()
+    A = sp.block_diag([sp.csr_matrix(Sk), Mb], format="csr")
+    A.sort_indices()
+    B = np.zeros((m + 40, 2), dtype=np.complex128 if cplx else np.float64)
+    B[:m, 0] = rng.integers(-4, 5, m)
+    B[:, 1] = synth.random_rhs(m + 40, 1, 8, cplx)[:, 0]
+    return A, B
+
+
+@pytest.mark.parametrize("cplx", [False, True])
+def test_li_bicg_column_freeze_on_lanczos_zero(cplx):
+    """Li-BiCG with one column meeting an exact Lanczos zero (reading G13):
+    that column freezes at iteration 1 (X column stays 0, reported in breakdown_cols)
+    while the other column's iterates are SciPy's single-RHS bicg on (A, b_1)."""
+    A, B = _skew_block_problem(cplx)
+    q0 = A @ B[:, 0]
+    assert np.vdot(B[:, 0], q0) == 0  # the exact zero the test relies on
+    k = 12
+    r = S.li_bicg(A, B, tol=1e-300, maxit=k, record=k)
+    assert r.breakdown_cols == [0]
+    assert all(np.all(X[:, 0] == 0) for X in r.Xs)
+    ref = scipy_iterates(spla.bicg, A, B[:, 1], k)
+    for j, x in enumerate(ref):
+        assert rel(r.Xs[j][:, 1], x) < 1e-10, j
