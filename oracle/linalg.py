@@ -123,11 +123,44 @@ def small_solve_h(G: np.ndarray, M: np.ndarray) -> np.ndarray:
     return small_solve(H(G), M)
 
 
-def thin_qr(Z: np.ndarray, ctr: Counter | None = None, order: str = "blas"):
+DEFL_SEED = 0x5EED1504  # seed of the rank-deficiency replacement vectors (f4)
+
+
+def _splitmix64(x):
+    """SplitMix64 finaliser on uint64 (wrapping) — the counter-based generator both
+    sides implement for the replacement vectors (no shared code, same definition)."""
+    x = np.asarray(x, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        z = x + np.uint64(0x9E3779B97F4A7C15)
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+    return z ^ (z >> np.uint64(31))
+
+
+def counter_uniform(n: int, key: int, cplx: bool, seed: int = DEFL_SEED, row0: int = 0) -> np.ndarray:
+    """Replacement vector number `key` (event * 64 + column): entry i (global row
+    row0 + i) is 2u - 1, u = (splitmix64(h + 2i + part) >> 11) * 2^-53, with the stream
+    h = splitmix64(seed ^ (key * 0x9E3779B97F4A7C15)); part 0 real, 1 imaginary."""
+    with np.errstate(over="ignore"):
+        h = _splitmix64(np.uint64(seed) ^ (np.uint64(key) * np.uint64(0x9E3779B97F4A7C15)))
+        i = np.arange(row0, row0 + n, dtype=np.uint64)
+
+        def part(p):
+            v = _splitmix64(h + np.uint64(2) * i + np.uint64(p))
+            return (v >> np.uint64(11)).astype(np.float64) * 2.0 ** -53 * 2.0 - 1.0
+    return part(0) + 1j * part(1) if cplx else part(0)
+
+
+def thin_qr(Z: np.ndarray, ctr: Counter | None = None, order: str = "blas", fill=None):
     """Thin QR Z = Q C by modified Gram-Schmidt with one full re-orthogonalisation
     pass (Eq. (3) P:501-509; cost remark "3ns^2 ... modified Gram-Schmidt" P:598-603;
     SPEC thin_qr S:97-105). C is upper triangular with real non-negative diagonal.
-    A diagonal <= EPS_DEFL*||Z||_F raises Breakdown('rank') (reading G11)."""
+    A diagonal <= EPS_DEFL*||Z||_F raises Breakdown('rank') (reading G11) — unless
+    `fill` is given (rank-deficiency continuation, SURVEY §8(f) f4; S:101, S:141;
+    the implicit deflation of [Oleary80, Dub01]): then column j of Q is
+    fill(j) orthogonalised (two passes) against q_0..q_{j-1} and normalised, C[j, j] = 0,
+    and the later columns are orthogonalised against it as usual, so Z = Q C still
+    holds with Q orthonormal (reading R8)."""
     n, s = Z.shape
     Q = np.array(Z, dtype=np.result_type(Z.dtype, np.float64), copy=True)
     C = np.zeros((s, s), dtype=Q.dtype)
@@ -143,7 +176,15 @@ def thin_qr(Z: np.ndarray, ctr: Counter | None = None, order: str = "blas"):
                 C[i, j] += r
         d = np.sqrt(fro2(Q[:, j:j + 1], order))
         if not np.isfinite(d) or d <= EPS_DEFL * zn or zn == 0:
-            raise Breakdown("rank", j)
+            if fill is None or not np.isfinite(d):
+                raise Breakdown("rank", j)
+            Q[:, j] = fill(j)
+            for _pass in range(2):
+                for i in range(j):
+                    r = np.vdot(Q[:, i], Q[:, j]) if order == "blas" else _sum_rows(Q[:, i].conj() * Q[:, j], order)
+                    Q[:, j] -= r * Q[:, i]
+            Q[:, j] /= np.sqrt(fro2(Q[:, j:j + 1], order))
+            continue
         C[j, j] = d
         Q[:, j] /= d
     if ctr is not None:

@@ -29,7 +29,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from .linalg import (Breakdown, Counter, H, col_inner, fro2, gram, saxpy_count, small_solve,
+from .linalg import (Breakdown, Counter, H, col_inner, counter_uniform, fro2, gram, saxpy_count, small_solve,
                      small_solve_h, sum_inner, thin_qr, trace_inner, unitary_qr_stack)
 
 METHODS = ("li_bicg", "gl_bicg", "egl_bicg", "bl_bicg", "bl_bicg_rq",
@@ -165,6 +165,16 @@ def _safe_div(num, den, frozen):
     newly = (~ok & ~frozen) | bad
     q = np.where(newly | frozen, 0, q)
     return q, newly
+
+
+def _deflation_fill(run: _Run, deflate: bool):
+    """fill(event) -> the thin-QR replacement callable of QR number `event` (init 0;
+    iteration k: 2k for the residual factor, 2k + 1 for the shadow's), or None
+    (BREAKDOWN(rank) policy, reading G11)."""
+    n, cplx = run.B.shape[0], run.dt == np.complex128
+    if not deflate:
+        return lambda event: None
+    return lambda event: (lambda j: counter_uniform(n, event * 64 + j, cplx))
 
 
 def _quiet(fn):
@@ -346,20 +356,24 @@ def bl_bicg(A, B, tol=1e-8, maxit=2000, X0=None, shadow=None, record=20, order="
 
 
 @_quiet
-def bl_bicg_rq(A, B, tol=1e-8, maxit=2000, X0=None, shadow=None, record=20, order="blas"):
+def bl_bicg_rq(A, B, tol=1e-8, maxit=2000, X0=None, shadow=None, record=20, order="blas", deflate=False):
     """Alg. 5 Bl-BiCG-rQ, loop from k = 0 (reading G1), α̂/β̂ by
     adjoint reuse (G5), Ŝ^H in β and S^H in β̂ as printed (G4), stopping on
-    ‖C^(k)‖_F. Names: Qr = orthonormal residual factor, Sig = S."""
+    ‖C^(k)‖_F. Names: Qr = orthonormal residual factor, Sig = S.
+    deflate=True: rank-deficiency continuation (f4) instead of BREAKDOWN(rank) —
+    no C or Σ is ever inverted, so a zero diagonal of C just "hides" the deflated
+    direction (P:396-403)."""
     run = _Run(A, B, X0, tol, maxit, record, order)
     ctr, s = run.ctr, run.B.shape[1]
     X = run.X
     if run.r0norm == 0:
         run.res.outcome = "converged"
         return run.finish(X)
+    fill = _deflation_fill(run, deflate)
     k = 0
     try:
-        Qr, C = thin_qr(run.R0, None, order)                   # Q^(0) C^(0) = R^(0)
-        Qh, Ch = thin_qr(_shadow_block(run, shadow), None, order)
+        Qr, C = thin_qr(run.R0, None, order, fill(0))          # Q^(0) C^(0) = R^(0)
+        Qh, Ch = thin_qr(_shadow_block(run, shadow), None, order, fill(0))
         V, Vh = Qr.copy(), Qh.copy()
         G2 = gram(Qh, Qr, None, order)                         # (Q̂^(k))^H Q^(k)
         for k in range(1, maxit + 1):
@@ -369,9 +383,9 @@ def bl_bicg_rq(A, B, tol=1e-8, maxit=2000, X0=None, shadow=None, record=20, orde
             alpha = small_solve(G1, G2)                        # Eq. (4)
             alpha_h = small_solve_h(G1, H(G2))                 # Eq. (5)
             X = X + V @ (alpha @ C)
-            Qr_new, Sig = thin_qr(Qr - W @ alpha, ctr, order)
+            Qr_new, Sig = thin_qr(Qr - W @ alpha, ctr, order, fill(2 * k))
             C = Sig @ C
-            Qh_new, Sig_h = thin_qr(Qh - Wh @ alpha_h, ctr, order)
+            Qh_new, Sig_h = thin_qr(Qh - Wh @ alpha_h, ctr, order, fill(2 * k + 1))
             Ch = Sig_h @ Ch
             saxpy_count(ctr, 3 * s * s)
             G2_new = gram(Qh_new, Qr_new, ctr, order)
@@ -382,6 +396,100 @@ def bl_bicg_rq(A, B, tol=1e-8, maxit=2000, X0=None, shadow=None, record=20, orde
             saxpy_count(ctr, 2 * s * s)
             Qr, Qh, G2 = Qr_new, Qh_new, G2_new
             if run.step_done(k, X, np.sqrt(fro2(C)), C, dict(alpha=alpha, beta=beta, C=C.copy())):
+                break
+    except Breakdown as e:
+        return run.breakdown(X, e, k)
+    return run.finish(X)
+
+
+@_quiet
+def bl_bicg_sq(A, B, tol=1e-8, maxit=2000, X0=None, shadow=None, record=20, order="blas"):
+    """Bl-BiCG with QR-factorised search directions — the stabilisation of [Oleary80]
+    that the paper names and rejects in favour of the residual QR ("use a QR
+    factorization of the search direction block vectors P^(k) and P̂^(k)").
+    The paper prints no recurrences; derived here (reading R9): P and P̂ are
+    kept orthonormal, so α, β come from the defining conditions instead of M = R̂^H R:
+      Galerkin      P̂^H R₊ = 0            ->  α = G^{-1} P̂^H R,   G = P̂^H A P
+      biconjugacy   P̂^H A (R₊ + P β) = 0   ->  β = -G^{-1} (A^H P̂)^H R₊
+    and the shadow side with G^H (α̂ = G^{-H} P^H R̂, β̂ = -G^{-H} (A P)^H R̂₊). Any basis
+    of the Bl-BiCG search space gives the same X_k (the s x s coefficients absorb it),
+    so in exact arithmetic the iterates are Alg. 3's."""
+    run = _Run(A, B, X0, tol, maxit, record, order)
+    ctr, s = run.ctr, run.B.shape[1]
+    X = run.X
+    R = run.R0.copy()
+    Rh = _shadow_block(run, shadow)
+    if run.r0norm == 0:
+        run.res.outcome = "converged"
+        return run.finish(X)
+    k = 0
+    try:
+        P = thin_qr(R, None, order)[0]               # orthonormal basis of span(R0)
+        Ph = thin_qr(Rh, None, order)[0]
+        for k in range(1, maxit + 1):
+            Q = run.matA(P)
+            Qh = run.matAH(Ph)
+            G = gram(Ph, Q, ctr, order)              # P̂^H A P
+            alpha = small_solve(G, gram(Ph, R, ctr, order))
+            alpha_h = small_solve_h(G, gram(P, Rh, ctr, order))
+            X = X + P @ alpha
+            R = R - Q @ alpha
+            Rh = Rh - Qh @ alpha_h
+            saxpy_count(ctr, 3 * s * s)
+            beta = -small_solve(G, gram(Qh, R, ctr, order))
+            beta_h = -small_solve_h(G, gram(Q, Rh, ctr, order))
+            P = thin_qr(R + P @ beta, ctr, order)[0]
+            Ph = thin_qr(Rh + Ph @ beta_h, ctr, order)[0]
+            saxpy_count(ctr, 2 * s * s)
+            if run.step_done(k, X, np.sqrt(fro2(R, order)), R, dict(alpha=alpha, beta=beta)):
+                break
+    except Breakdown as e:
+        return run.breakdown(X, e, k)
+    return run.finish(X)
+
+
+@_quiet
+def bl_bicgstab_sq(A, B, tol=1e-8, maxit=2000, X0=None, shadow=None, record=20, order="blas"):
+    """Bl-BiCGStab with QR-factorised search directions ("a corresponding variant
+    based on QR factorization of the search directions"). SURVEY App. A.4
+    with P kept orthonormal: α = G^{-1} R̃^H R and β = -G^{-1} R̃^H T are basis
+    covariant (P -> P γ gives α -> γ^{-1} α, β -> γ^{-1} β), so P₊ = qr(R + (P - ω U) β)
+    changes no iterate in exact arithmetic (reading R9)."""
+    run = _Run(A, B, X0, tol, maxit, record, order)
+    ctr, s = run.ctr, run.B.shape[1]
+    X = run.X
+    R = run.R0.copy()
+    if run.r0norm == 0:
+        run.res.outcome = "converged"
+        return run.finish(X)
+    Rt = _shadow_block(run, shadow)
+    k = 0
+    try:
+        P = thin_qr(R, None, order)[0]
+        for k in range(1, maxit + 1):
+            U = run.matA(P)
+            G = gram(Rt, U, ctr, order)                  # R̃^H U
+            alpha = small_solve(G, gram(Rt, R, ctr, order))
+            S = R - U @ alpha
+            saxpy_count(ctr, s * s)
+            snorm = np.sqrt(fro2(S, order))
+            if snorm / run.r0norm <= tol:
+                Xh = X + P @ alpha
+                if run.true_rel(Xh) <= tol:
+                    X = Xh
+                    run.res.half_step = True
+                    run.res.outcome = "converged"
+                    run.step_done(k, X, snorm, S, dict(alpha=alpha))
+                    break
+            T = run.matA(S)
+            omega = _scalar_div(trace_inner(S, T, ctr, order), trace_inner(T, T, ctr, order), "omega")
+            X = X + P @ alpha + omega * S
+            R = S - omega * T
+            saxpy_count(ctr, s * s + 2 * s)
+            beta = -small_solve(G, gram(Rt, T, ctr, order))
+            P = thin_qr(R + (P - omega * U) @ beta, ctr, order)[0]
+            saxpy_count(ctr, s * s + s)
+            if run.step_done(k, X, np.sqrt(fro2(R, order)), R, dict(alpha=alpha, omega=omega, beta=beta)):
                 break
     except Breakdown as e:
         return run.breakdown(X, e, k)
@@ -735,22 +843,24 @@ def bl_bicgstab(A, B, tol=1e-8, maxit=2000, X0=None, shadow=None, record=20, ord
 
 
 @_quiet
-def bl_bicgstab_rq(A, B, tol=1e-8, maxit=2000, X0=None, shadow=None, record=20, order="blas"):
+def bl_bicgstab_rq(A, B, tol=1e-8, maxit=2000, X0=None, shadow=None, record=20, order="blas", deflate=False):
     """Bl-BiCGStab-rQ (P:625-631, "we do not write down the resulting algorithm"):
     SURVEY App. A.5 (reading G16): R = Qr C kept factored, P = V C, one thin QR
-    per iteration, ω through M = C C^H, residual monitored by ‖C‖_F."""
+    per iteration, ω through M = C C^H, residual monitored by ‖C‖_F.
+    deflate=True: rank-deficiency continuation (f4), as in bl_bicg_rq."""
     run = _Run(A, B, X0, tol, maxit, record, order)
     ctr, s = run.ctr, run.B.shape[1]
     X = run.X
     if run.r0norm == 0:
         run.res.outcome = "converged"
         return run.finish(X)
+    fill = _deflation_fill(run, deflate)
     k = 0
     try:
-        Qr, C = thin_qr(run.R0, None, order)
+        Qr, C = thin_qr(run.R0, None, order, fill(0))
         Rt = _shadow_block(run, shadow)
         Q0h = Qr.copy() if (shadow is None or (isinstance(shadow, str) and shadow == "r0")) \
-            else thin_qr(Rt, None, order)[0]
+            else thin_qr(Rt, None, order, fill(1))[0]
         V = Qr.copy()
         GQ = gram(Q0h, Qr, None, order)
         c0 = np.sqrt(fro2(C))
@@ -776,7 +886,7 @@ def bl_bicgstab_rq(A, B, tol=1e-8, maxit=2000, X0=None, shadow=None, record=20, 
             YY = gram(Y, Y, ctr, order)
             omega = _scalar_div(np.trace(YZ @ M), np.trace(YY @ M), "omega")
             X = X + (V @ alpha + omega * Z) @ C
-            Qr_new, Sig = thin_qr(Z - omega * Y, ctr, order)
+            Qr_new, Sig = thin_qr(Z - omega * Y, ctr, order, fill(2 * k))
             C = Sig @ C
             GQ_new = gram(Q0h, Qr_new, ctr, order)
             beta = small_solve(G, GQ_new) / omega
@@ -790,7 +900,9 @@ def bl_bicgstab_rq(A, B, tol=1e-8, maxit=2000, X0=None, shadow=None, record=20, 
     return run.finish(X)
 
 
-SOLVERS = {name: globals()[name] for name in METHODS}
+# QR of the search directions: the comparison variants the paper rejects
+SQ_METHODS = ("bl_bicg_sq", "bl_bicgstab_sq")
+SOLVERS = {name: globals()[name] for name in METHODS + SQ_METHODS}
 
 
 def solve(method: str, A, B, **kw) -> Result:

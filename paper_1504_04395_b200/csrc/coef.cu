@@ -20,7 +20,10 @@ __device__ void set_brk(const CoefArgs& a, int kind) {
   if (a.ctl[CTL_FLAG] == FLAG_RUN) {
     a.ctl[CTL_FLAG] = FLAG_BRK;
     a.ctl[CTL_BKIND] = kind;
-    a.ctl[CTL_BITER] = a.ctl[CTL_ITER] + 1;
+    // a breakdown in the start-up phases (||R0||, the initial thin QRs and coefficients:
+    // phases 0, 9-13) happens before iteration 1: reported as iteration 0, as the oracle does
+    const bool init = a.phase == 0 || (a.phase >= 9 && a.phase <= 13);
+    a.ctl[CTL_BITER] = a.ctl[CTL_ITER] + (init ? 0 : 1);
   }
 }
 

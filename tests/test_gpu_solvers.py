@@ -84,6 +84,8 @@ def test_lockstep_parity(srk, method, prob):
     for k in range(n_cmp):
         err = crel(xs[k], a.Xs[k], method)
         assert err <= env[k], (method, prob, k + 1, "X", err, env[k])
+        if a.half_step and k == a.iterations - 1:
+            continue  # a half-step exit records S (never materialised on the GPU): X only
         err = crel(sv.rs[k], a.Rs[k], method)
         assert err <= env[k], (method, prob, k + 1, "R" if a.Rs[k].shape == B.shape else "C", err, env[k])
     sv.close()
@@ -117,10 +119,11 @@ def test_full_solve(srk, method, prob):
     lo = min(r.iterations for r in same)
     hi = max(r.iterations for r in same)
     if rep.outcome == "converged":
-        slack = max(0.02 * a.iterations, 2)
-        # within the oracle ensemble's range (its reduction orders and 1e-15 perturbations
-        # of B) widened by max(2%, 2): SURVEY §8c.5 rule 3 with the ensemble's spread
-        assert lo - slack <= rep.iterations <= hi + slack, (rep.iterations, lo, hi)
+        # SURVEY §8c.5 rule 3: within max(2%, spread + 2) of the oracle's count, the spread
+        # being the oracle ensemble's own (its reduction orders and 1e-15 perturbations of
+        # B; |it_O - it_O'| in the rule's two-order form)
+        slack = max(0.02 * a.iterations, (hi - lo) + 2)
+        assert abs(rep.iterations - a.iterations) <= slack, (rep.iterations, a.iterations, lo, hi)
         # the oracle's own SpMM recomputes the true residual from the GPU's X
         true = np.linalg.norm(B - As @ X) / np.linalg.norm(B)
         assert true <= tol

@@ -112,6 +112,8 @@ def test_virtual_lockstep(srk, method, prob, k):
         X = np.concatenate([out[r][0][it] for r in range(k)])
         err = rel(X, a.Xs[it])
         assert err <= env[it], (method, prob, k, it + 1, "X", err, env[it])
+        if a.half_step and it == a.iterations - 1:
+            continue  # a half-step exit records S, which the GPU never materialises
         if rq:  # C_k is s x s, replicated on every rank
             for r in range(k):
                 assert rel(out[r][1][it], a.Rs[it]) <= env[it], (method, k, it + 1, "C", r)

@@ -360,3 +360,115 @@ def test_li_bicg_column_freeze_on_lanczos_zero(cplx):
     ref = scipy_iterates(spla.bicg, A, B[:, 1], k)
     for j, x in enumerate(ref):
         assert rel(r.Xs[j][:, 1], x) < 1e-10, j
+
+
+# ---------------------------------------------------------------- f3: QR of search directions
+@pytest.mark.parametrize("cplx", [False, True])
+@pytest.mark.parametrize("pair", [("bl_bicg", "bl_bicg_sq"), ("bl_bicgstab", "bl_bicgstab_sq")])
+def test_search_direction_qr_equals_plain_block_method(pair, cplx):
+    """Orthonormalising the search directions ([Oleary80]) changes only the
+    basis the s x s coefficients act on: X_k equals Alg. 3 / App. A.4 in exact arithmetic
+    (to the rounding the block recurrences amplify, as for the rQ pin)."""
+    plain, sq = pair
+    A, B = problem(cplx=cplx)
+    a = oracle.solve(plain, A, B, tol=1e-10, maxit=200, record=8)
+    b = S.SOLVERS[sq](A, B, tol=1e-10, maxit=200, record=8)
+    for k in range(4):
+        assert rel(b.Xs[k], a.Xs[k]) < 1e-11, k
+    for k in range(4, 8):
+        assert rel(b.Xs[k], a.Xs[k]) < 1e-6, k
+
+
+@pytest.mark.parametrize("sq,base", [("bl_bicg_sq", spla.bicg), ("bl_bicgstab_sq", spla.bicgstab)])
+def test_search_direction_qr_s1(sq, base):
+    """s = 1: the orthonormal search direction is p/‖p‖, a rescaling — SciPy's BiCG / BiCGStab."""
+    A, B = problem(s=1)
+    r = S.SOLVERS[sq](A, B, tol=1e-300, maxit=10, record=10)
+    ref = scipy_iterates(base, A, B[:, 0], 10)
+    for k in range(min(len(ref), len(r.Xs))):
+        assert rel(r.Xs[k][:, 0], ref[k]) < 1e-9, k
+
+
+def test_search_direction_qr_converges_on_config1():
+    A, B = synth.make_config(1)
+    r = S.SOLVERS["bl_bicgstab_sq"](A.to_scipy(), B, tol=1e-8, maxit=2000, record=0)
+    assert r.outcome == "converged" and r.final_true_rel_residual <= 1e-8
+
+
+# ---------------------------------------------------------------- f4: rank-deficiency continuation
+def test_counter_generator_is_splitmix64():
+    """The replacement vectors' generator is SplitMix64 (its published first output for
+    state 0 is 0xE220A8397B1DCDAF); entries are uniform in [-1, 1), keyed and repeatable."""
+    from oracle.linalg import _splitmix64, counter_uniform
+    assert int(_splitmix64(np.uint64(0))) == 0xE220A8397B1DCDAF
+    u = counter_uniform(10000, 3, False)
+    assert u.min() >= -1 and u.max() < 1 and abs(u.mean()) < 0.05 and abs(u.var() - 1 / 3) < 0.02
+    assert np.array_equal(u, counter_uniform(10000, 3, False))
+    assert not np.array_equal(u, counter_uniform(10000, 4, False))
+    z = counter_uniform(100, 3, True)
+    assert np.array_equal(z.real, u[:100]) and not np.array_equal(z.real, z.imag)
+    assert np.array_equal(counter_uniform(50, 3, False, row0=50), u[50:100])
+
+
+@pytest.mark.parametrize("cplx", [False, True])
+def test_thin_qr_continuation_is_qr_of_the_replaced_block(cplx):
+    """Z = [w, 2w, u]: column 1 is deficient; with continuation Q is the (unique) thin QR
+    factor of Z' = [w, ρ, u], ρ the replacement vector, C[1, 1] = 0 and Z = Q C."""
+    from oracle.linalg import counter_uniform, thin_qr
+    rng = np.random.default_rng(2)
+    n = 30
+    w, u = synth.random_rhs(n, 2, 5, cplx).T
+    Z = np.stack([w, 2 * w, u], axis=1)
+    with pytest.raises(oracle.Breakdown):
+        thin_qr(Z)
+    fill = lambda j: counter_uniform(n, 7 * 64 + j, cplx)  # noqa: E731
+    Q, C = thin_qr(Z, fill=fill)
+    assert C[1, 1] == 0 and np.all(np.diag(C).real >= 0)
+    assert np.linalg.norm(Q.conj().T @ Q - np.eye(3)) < 1e-13
+    assert np.linalg.norm(Q @ C - Z) < 1e-13 * np.linalg.norm(Z)
+    Zp = Z.copy()
+    Zp[:, 1] = fill(1)
+    Qr, Rr = np.linalg.qr(Zp)
+    ph = np.diag(Rr) / np.abs(np.diag(Rr))
+    assert np.linalg.norm(Qr * ph[None, :] - Q) < 1e-12
+    del rng
+
+
+@pytest.mark.parametrize("cplx", [False, True])
+def test_rank_continuation_equals_full_rank_run(cplx):
+    """R0 = [b1, b2, b1 + b2] (exact deflation): continued Bl-BiCG-rQ runs on the
+    orthonormal factor of B' = [b1, b2, ρ] (ρ the replacement) and only its C differs —
+    α, β (Eqs. (4)-(7)) depend on the Q's alone — so X_k(B) = X_k(B') T with B = B' T:
+    the deflation is hidden ([Dub01])."""
+    from oracle.linalg import counter_uniform
+    A, _ = problem(n=60, cplx=cplx)
+    B = synth.random_rhs(60, 3, 3, cplx)
+    B[:, 2] = B[:, 0] + B[:, 1]
+    d = S.bl_bicg_rq(A, B, tol=1e-10, maxit=300, record=6, deflate=True)
+    Bp = B.copy()
+    Bp[:, 2] = counter_uniform(60, 2, cplx)
+    T = np.linalg.lstsq(Bp, B, rcond=None)[0]
+    assert np.linalg.norm(Bp @ T - B) < 1e-12 * np.linalg.norm(B)
+    f = S.bl_bicg_rq(A, Bp, tol=1e-10, maxit=300, record=6)
+    for k in range(4):
+        assert rel(d.Xs[k], f.Xs[k] @ T) < 1e-9, k
+
+
+@pytest.mark.parametrize("cplx", [False, True])
+@pytest.mark.parametrize("method", ["bl_bicg_rq", "bl_bicgstab_rq"])
+def test_rank_continuation_invariants(method, cplx):
+    """With continuation the rQ methods run through an exactly rank-deficient R0 (plain
+    policy: BREAKDOWN(rank), reading G11): every update right-multiplies by C, and
+    C^(0) = Q^H B inherits b3 = b1 + b2, so x3 = x1 + x2 at every iterate; the norm
+    identity ‖C_k‖_F = ‖B - A X_k‖_F holds throughout; the solve converges."""
+    A, _ = problem(n=60, cplx=cplx)
+    B = synth.random_rhs(60, 3, 3, cplx)
+    B[:, 2] = B[:, 0] + B[:, 1]
+    assert S.SOLVERS[method](A, B, tol=1e-10).outcome == "breakdown"
+    d = S.SOLVERS[method](A, B, tol=1e-10, maxit=300, record=8, deflate=True)
+    for X, C in zip(d.Xs, d.Rs):
+        assert rel(X[:, 2], X[:, 0] + X[:, 1]) < 1e-10
+        true = np.linalg.norm(B - A @ X)
+        assert abs(np.linalg.norm(C) - true) <= 1e-8 * np.linalg.norm(B)
+    assert d.outcome == "converged" and d.final_true_rel_residual <= 1e-10
+    assert rel(d.X[:, 2], d.X[:, 0] + d.X[:, 1]) < 1e-8
