@@ -45,7 +45,11 @@ typedef enum { SRK_F64 = 0, SRK_C128 = 1 } srk_dtype;
 typedef enum {
   SRK_LI_BICG = 0, SRK_GL_BICG = 1, SRK_EGL_BICG = 2, SRK_BL_BICG = 3, SRK_BL_BICG_RQ = 4,
   SRK_LI_QMR = 5, SRK_GL_QMR = 6, SRK_EGL_QMR = 7, SRK_BL_QMR = 8,
-  SRK_LI_BICGSTAB = 9, SRK_GL_BICGSTAB = 10, SRK_BL_BICGSTAB = 11, SRK_BL_BICGSTAB_RQ = 12
+  SRK_LI_BICGSTAB = 9, SRK_GL_BICGSTAB = 10, SRK_BL_BICGSTAB = 11, SRK_BL_BICGSTAB_RQ = 12,
+  /* QR of the search directions [O'Leary]: the
+   * stabilisation the paper compares with and rejects; iterates equal Bl-BiCG /
+   * Bl-BiCGStab in exact arithmetic (reading R9) */
+  SRK_BL_BICG_SQ = 13, SRK_BL_BICGSTAB_SQ = 14
 } srk_method;
 
 enum { SRK_OK = 0, SRK_EINVAL = -1, SRK_EDIM = -2, SRK_EUNSUPPORTED = -3, SRK_ECUDA = -4,
@@ -94,6 +98,11 @@ typedef struct {
   double final_recursive_rel_residual; /* ||R||_F (or ||C||_F for rQ) / ||R0||_F */
   double seconds;                      /* wall time of the iteration loop */
   int64_t kernel_launches;             /* kernels launched by the loop */
+  int64_t vector_ops;   /* Prop. 1's count: inner products and SAXPYs of length n, per
+                           iteration 7s (Li / Gl) or 7s^2 (Bl) for BiCG, summed over the solve */
+  int breakdown_col;    /* Li variants: first frozen column (reading G13); thin QR: first
+                           deficient column; else -1 */
+  int deflated_cols;    /* rank_policy 1: columns replaced by the continuation so far */
 } srk_report;
 
 /* ------------------------------------------------------------------ context */
@@ -242,6 +251,19 @@ typedef struct {
                           off while srk_solver_profile is on) */
   int x0_zero;         /* X0 = 0 (the paper's protocol): X is output only — srk_solve does
                           not read it and srk_solve_host does not copy it in (default 0) */
+  int shadow;          /* shadow block R̂0 / R̃: 0 = the paper's choice
+                          (R0; the economic variants the column mean), 1 = conj(R0),
+                          2 = column mean (every variant), 3 = shadow_given */
+  const void* shadow_given; /* shadow == 3: DEVICE n x s block (economic variants: n-vector) */
+  int preprocess_rhs;  /* 1: solve for the orthonormal factor Q of B = Q C and return X = Y C
+                          (the paper's QR preprocessing of the right-hand sides; reading G9,
+                          default 0); the tolerance is then relative to ||Q||_F = sqrt(s) */
+  double eps_brk;      /* s x s LU pivot / scalar breakdown threshold, relative (0: 1e-14, G12) */
+  double eps_defl;     /* CholQR pivot threshold relative to tr(Z^H Z) (0: 1e-14, R5) */
+  int rank_policy;     /* rQ variants, rank-deficient thin QR: 0 = BREAKDOWN(rank) (reading G11),
+                          1 = continue with the deficient columns of Q replaced by counter-based
+                          random vectors orthogonalised against the others, C_jj = 0 (the implicit
+                          deflation of P:396-403) */
 } srk_opts;
 
 /* Full solve (a1-a7): B, X device n x s blocks; X holds X0 on entry and the

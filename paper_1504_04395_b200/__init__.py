@@ -19,7 +19,8 @@ _LIBPATH = os.path.join(_HERE, "libsrk.so")
 
 METHODS = ("li_bicg", "gl_bicg", "egl_bicg", "bl_bicg", "bl_bicg_rq",
            "li_qmr", "gl_qmr", "egl_qmr", "bl_qmr",
-           "li_bicgstab", "gl_bicgstab", "bl_bicgstab", "bl_bicgstab_rq")
+           "li_bicgstab", "gl_bicgstab", "bl_bicgstab", "bl_bicgstab_rq",
+           "bl_bicg_sq", "bl_bicgstab_sq")  # the last two: QR of the search directions (f3)
 METHOD_ID = {m: i for i, m in enumerate(METHODS)}
 NEEDS_ADJOINT = {m: ("bicgstab" not in m) for m in METHODS}
 GRAM = {"none": 0, "norm2": 1, "diag": 2, "trace": 3, "sumvec": 4, "full": 5, "colnorm2": 6}
@@ -51,7 +52,9 @@ class _Csr(ctypes.Structure):
 class _Opts(ctypes.Structure):
     _fields_ = [("tol", ctypes.c_double), ("maxit", ctypes.c_int), ("poll_every", ctypes.c_int),
                 ("record_history", ctypes.c_int), ("check_true_residual", ctypes.c_int),
-                ("use_graph", ctypes.c_int), ("x0_zero", ctypes.c_int)]
+                ("use_graph", ctypes.c_int), ("x0_zero", ctypes.c_int), ("shadow", ctypes.c_int),
+                ("shadow_given", ctypes.c_void_p), ("preprocess_rhs", ctypes.c_int), ("eps_brk", ctypes.c_double),
+                ("eps_defl", ctypes.c_double), ("rank_policy", ctypes.c_int)]
 
 
 class _Halo(ctypes.Structure):
@@ -64,7 +67,8 @@ class _Report(ctypes.Structure):
                 ("breakdown_kind", ctypes.c_int), ("breakdown_iter", ctypes.c_int), ("frozen_cols", ctypes.c_int),
                 ("matvec_cols_A", ctypes.c_int64), ("matvec_cols_AH", ctypes.c_int64),
                 ("final_true_rel_residual", ctypes.c_double), ("final_recursive_rel_residual", ctypes.c_double),
-                ("seconds", ctypes.c_double), ("kernel_launches", ctypes.c_int64)]
+                ("seconds", ctypes.c_double), ("kernel_launches", ctypes.c_int64), ("vector_ops", ctypes.c_int64),
+                ("breakdown_col", ctypes.c_int), ("deflated_cols", ctypes.c_int)]
 
 
 _lib = None
@@ -569,28 +573,46 @@ class Report:
     final_recursive_rel_residual: float
     seconds: float
     kernel_launches: int
+    vector_ops: int = 0
+    breakdown_col: int = -1
+    deflated_cols: int = 0
 
 
 def _report(r: _Report) -> Report:
     return Report(OUTCOME.get(r.outcome, str(r.outcome)), r.iterations, bool(r.half_step),
                   BREAKDOWN.get(r.breakdown_kind, str(r.breakdown_kind)), r.breakdown_iter, r.frozen_cols,
                   r.matvec_cols_A, r.matvec_cols_AH, r.final_true_rel_residual, r.final_recursive_rel_residual,
-                  r.seconds, r.kernel_launches)
+                  r.seconds, r.kernel_launches, r.vector_ops, r.breakdown_col, r.deflated_cols)
 
 
-def _opts(tol, maxit, poll_every=8, check_true_residual=True, use_graph=True, x0_zero=False):
-    return _Opts(float(tol), int(maxit), int(poll_every), 1, int(check_true_residual), int(use_graph), int(x0_zero))
+SHADOW = {"default": 0, "conj": 1, "mean": 2, "given": 3}
+
+
+def _opts(tol, maxit, poll_every=8, check_true_residual=True, use_graph=True, x0_zero=False, shadow="default",
+          shadow_given=None, preprocess_rhs=False, eps_brk=0.0, eps_defl=0.0, rank_policy="breakdown"):
+    """srk_opts. rank_policy: "breakdown" (reading G11) or "continue" (f4, the rQ variants)."""
+    if rank_policy not in ("breakdown", "continue"):
+        raise SrkError(f"rank_policy must be 'breakdown' or 'continue', not {rank_policy!r}")
+    if shadow not in SHADOW:
+        raise SrkError(f"shadow must be one of {sorted(SHADOW)}")
+    if (shadow == "given") != (shadow_given is not None):
+        raise SrkError("shadow='given' needs shadow_given (and only then)")
+    sg = _dev(shadow_given, "shadow_given") if shadow_given is not None else None
+    return _Opts(float(tol), int(maxit), int(poll_every), 1, int(check_true_residual), int(use_graph), int(x0_zero),
+                 SHADOW[shadow], sg, int(preprocess_rhs), float(eps_brk), float(eps_defl),
+                 1 if rank_policy == "continue" else 0)
 
 
 class Solver:
     """Stepping interface (srk_solver_*): lock-step parity and benchmarking."""
 
     def __init__(self, A: Matrix, s: int, method: str, tol: float = 1e-8, maxit: int = 2000, poll_every: int = 8,
-                 check_true_residual: bool = True, use_graph: bool = True):
+                 check_true_residual: bool = True, use_graph: bool = True, **opts):
         if method not in METHOD_ID:
             raise SrkError(f"unknown method {method}")
         self.A, self.s, self.method = A, s, method
-        o = _opts(tol, maxit, poll_every, check_true_residual, use_graph)
+        o = _opts(tol, maxit, poll_every, check_true_residual, use_graph, **opts)
+        self._shadow = opts.get("shadow_given")
         h = ctypes.c_void_p()
         _check(_lib.srk_solver_create(A.ctx.h, A.h, s, METHOD_ID[method], ctypes.byref(o), ctypes.byref(h)),
                "srk_solver_create")
@@ -665,13 +687,15 @@ class Solver:
 
 
 def solve(A: Matrix, B, method: str = "egl_bicg", tol: float = 1e-8, maxit: int = 2000, X0=None,
-          poll_every: int = 8):
-    """X, report = solve(A, B, method, tol, maxit) — srk_solve on device tensors
-    (B: contiguous (n, s) float64/complex128 CUDA tensor)."""
+          poll_every: int = 8, **opts):
+    """X, report = solve(A, B, method, tol, maxit, **opts) — srk_solve on device tensors
+    (B: contiguous (n, s) float64/complex128 CUDA tensor). opts: shadow ("default",
+    "conj", "mean", "given" + shadow_given), preprocess_rhs, eps_brk, eps_defl,
+    rank_policy ("breakdown" / "continue")."""
     torch = _torch()
     n, s = B.shape
     X = torch.empty_like(B) if X0 is None else X0.clone()
-    o = _opts(tol, maxit, poll_every, x0_zero=X0 is None)
+    o = _opts(tol, maxit, poll_every, x0_zero=X0 is None, **opts)
     r = _Report()
     _check(_lib.srk_solve(A.ctx.h, A.h, _dev(B, "B"), _dev(X, "X"), s, METHOD_ID[method], ctypes.byref(o),
                           ctypes.byref(r)), "srk_solve")

@@ -511,6 +511,12 @@ static void fill_opts(srk_opts* o, const srk_opts* in) {
     o->check_true_residual = in->check_true_residual;
     o->use_graph = in->use_graph;
     o->x0_zero = in->x0_zero;
+    o->shadow = in->shadow;
+    o->shadow_given = in->shadow_given;
+    o->preprocess_rhs = in->preprocess_rhs;
+    o->eps_brk = in->eps_brk;
+    o->eps_defl = in->eps_defl;
+    o->rank_policy = in->rank_policy;
   }
 }
 
@@ -546,13 +552,18 @@ int srk_tsqr(srk_ctx* ctx, const void* Z, void* Q, void* C, int64_t n, int s, in
 int srk_solver_create(srk_ctx* ctx, const srk_matrix* A, int s, int method, const srk_opts* opts, srk_solver** out) {
   if (!ctx || !A || !out) return fail(SRK_EINVAL, "srk_solver_create: null argument");
   if (s < 1 || s > 64) return fail(SRK_EDIM, "srk_solver_create: s must be in [1, 64]");
-  if (method < 0 || method > SRK_BL_BICGSTAB_RQ) return fail(SRK_EINVAL, "srk_solver_create: unknown method");
+  if (method < 0 || method > SRK_BL_BICGSTAB_SQ) return fail(SRK_EINVAL, "srk_solver_create: unknown method");
   if (opts && (opts->tol < 0 || opts->maxit < 0)) return fail(SRK_EINVAL, "srk_solver_create: tol/maxit");
   const bool needs_adj = !(method == SRK_LI_BICGSTAB || method == SRK_GL_BICGSTAB || method == SRK_BL_BICGSTAB ||
-                           method == SRK_BL_BICGSTAB_RQ);
+                           method == SRK_BL_BICGSTAB_RQ || method == SRK_BL_BICGSTAB_SQ);
   if (needs_adj && !A->m.has_adj) return fail(SRK_EUNSUPPORTED, "srk_solver_create: method needs A^H (need_adjoint=1)");
   const bool block = method == SRK_BL_BICG || method == SRK_BL_BICG_RQ || method == SRK_BL_QMR ||
-                     method == SRK_BL_BICGSTAB || method == SRK_BL_BICGSTAB_RQ;
+                     method == SRK_BL_BICGSTAB || method == SRK_BL_BICGSTAB_RQ || method == SRK_BL_BICG_SQ ||
+                     method == SRK_BL_BICGSTAB_SQ;
+  if (opts && (opts->rank_policy < 0 || opts->rank_policy > 1)) return fail(SRK_EINVAL, "srk_solver_create: rank_policy");
+  if (opts && (opts->eps_brk < 0 || opts->eps_defl < 0)) return fail(SRK_EINVAL, "srk_solver_create: eps");
+  if (opts && opts->rank_policy && method != SRK_BL_BICG_RQ && method != SRK_BL_BICGSTAB_RQ)
+    return fail(SRK_EUNSUPPORTED, "srk_solver_create: rank_policy 1 applies to the rQ variants");
   if (block && !full_supported(A->m.cplx, cap_for(s)))
     return fail(SRK_EUNSUPPORTED, "srk_solver_create: block methods need s <= 32");
   if (A->m.bsr && !bsr_supported(A->m.bs, A->m.cplx, s))
@@ -637,6 +648,13 @@ int srk_solver_report(srk_solver* h, srk_report* rep) {
   rep->final_recursive_rel_residual = last;
   rep->seconds = sv->seconds;
   rep->kernel_launches = sv->launches;
+  rep->deflated_cols = sv->ctl_host[CTL_DEFL];
+  rep->breakdown_col = -1;
+  for (int c = 0; c < sv->s && c < 64; ++c)
+    if (sv->ctl_host[CTL_FROZEN + c]) {
+      rep->breakdown_col = c;
+      break;
+    }
   if (sv->state == 1) rep->outcome = SRK_CONVERGED;
   else if (sv->state == 2) rep->outcome = SRK_BREAKDOWN;
   else rep->outcome = rep->final_true_rel_residual > 1.0 ? SRK_DIVERGED : SRK_MAXIT;

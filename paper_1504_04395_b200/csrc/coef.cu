@@ -22,7 +22,7 @@ __device__ void set_brk(const CoefArgs& a, int kind) {
     a.ctl[CTL_BKIND] = kind;
     // a breakdown in the start-up phases (||R0||, the initial thin QRs and coefficients:
     // phases 0, 9-13) happens before iteration 1: reported as iteration 0, as the oracle does
-    const bool init = a.phase == 0 || (a.phase >= 9 && a.phase <= 13);
+    const bool init = a.phase == 0 || (a.phase >= 9 && a.phase <= 13) || (a.phase >= 20 && (a.k1 & 4));
     a.ctl[CTL_BITER] = a.ctl[CTL_ITER] + (init ? 0 : 1);
   }
 }
@@ -123,13 +123,13 @@ template <typename T>
 __device__ void bl_bicg(const CoefArgs& a, T* sh) {
   const int s = a.s;
   if (a.phase == 1) {  // alpha = G^-1 M, alpha_hat = G^-H M^H
-    if (sm_solve<T>(W<T>(a, SL_ALPHA), W<T>(a, SL_G), W<T>(a, SL_M), s, s, 0, sh)) { T0 set_brk(a, BK_GRAM); SYNC; return; }
+    if (sm_solve<T>(W<T>(a, SL_ALPHA), W<T>(a, SL_G), W<T>(a, SL_M), s, s, 0, sh, a.eps_brk)) { T0 set_brk(a, BK_GRAM); SYNC; return; }
     sm_copy<T>(W<T>(a, SL_TMP0), W<T>(a, SL_M), s, s, 1);
-    if (sm_solve<T>(W<T>(a, SL_AH), W<T>(a, SL_G), W<T>(a, SL_TMP0), s, s, 1, sh)) { T0 set_brk(a, BK_GRAM); SYNC; return; }
+    if (sm_solve<T>(W<T>(a, SL_AH), W<T>(a, SL_G), W<T>(a, SL_TMP0), s, s, 1, sh, a.eps_brk)) { T0 set_brk(a, BK_GRAM); SYNC; return; }
   } else if (a.phase == 2) {  // beta = M^-1 M+, beta_hat = M^-H M+^H, M = M+
-    if (sm_solve<T>(W<T>(a, SL_BETA), W<T>(a, SL_M), W<T>(a, SL_MN), s, s, 0, sh)) { T0 set_brk(a, BK_GRAM); SYNC; return; }
+    if (sm_solve<T>(W<T>(a, SL_BETA), W<T>(a, SL_M), W<T>(a, SL_MN), s, s, 0, sh, a.eps_brk)) { T0 set_brk(a, BK_GRAM); SYNC; return; }
     sm_copy<T>(W<T>(a, SL_TMP0), W<T>(a, SL_MN), s, s, 1);
-    if (sm_solve<T>(W<T>(a, SL_BH), W<T>(a, SL_M), W<T>(a, SL_TMP0), s, s, 1, sh)) { T0 set_brk(a, BK_GRAM); SYNC; return; }
+    if (sm_solve<T>(W<T>(a, SL_BH), W<T>(a, SL_M), W<T>(a, SL_TMP0), s, s, 1, sh, a.eps_brk)) { T0 set_brk(a, BK_GRAM); SYNC; return; }
     sm_copy<T>(W<T>(a, SL_M), W<T>(a, SL_MN), s, s, 0);
     conv_check(a, *D(a, SL_R2));
   }
@@ -138,7 +138,7 @@ __device__ void bl_bicg(const CoefArgs& a, T* sh) {
 // CholQR2 helper phases (reading G10): pass 1 R1 = chol(G) (rank test), pass 2 R2.
 template <typename T>
 __device__ bool cholqr_pass(const CoefArgs& a, int gslot, int rslot, int rislot, int rank_check) {
-  if (sm_chol<T>(W<T>(a, rslot), W<T>(a, gslot), a.s, rank_check)) { T0 set_brk(a, BK_RANK); SYNC; return false; }
+  if (sm_chol<T>(W<T>(a, rslot), W<T>(a, gslot), a.s, rank_check, a.eps_chol)) { T0 set_brk(a, BK_RANK); SYNC; return false; }
   sm_trinv<T>(W<T>(a, rislot), W<T>(a, rslot), a.s);
   return true;
 }
@@ -154,6 +154,26 @@ __device__ void cholqr_sigma(const CoefArgs& a, int r2, int r1, int sig, int csl
   }
 }
 
+// Pass 1 of an rQ thin QR under rank_policy 1: the masked Cholesky finds every deficient
+// column; if there is one, the mask goes to the control block and CTL_DIDLE drops to 0,
+// which arms the repair kernels that follow (fill, Gram, phase 20, ..., phase 21).
+template <typename T>
+__device__ bool cholqr_pass1_cont(const CoefArgs& a, int gslot, int rslot, int rislot, int maskctl) {
+  const unsigned long long m = sm_chol_mask<T>(W<T>(a, rslot), W<T>(a, gslot), a.s, a.eps_chol);
+  if (m == ~0ull) { T0 set_brk(a, BK_RANK); SYNC; return false; }
+  if (m) {
+    T0 {
+      a.ctl[maskctl] = (int)(unsigned)(m & 0xffffffffull);
+      a.ctl[maskctl + 1] = (int)(unsigned)(m >> 32);
+      a.ctl[CTL_DIDLE] = 0;
+    }
+    SYNC;
+    return true;
+  }
+  sm_trinv<T>(W<T>(a, rislot), W<T>(a, rslot), a.s);
+  return true;
+}
+
 // Bl-BiCG-rQ (Alg. 5, Eqs. (4)-(7))
 template <typename T>
 __device__ void bl_bicg_rq(const CoefArgs& a, T* sh) {
@@ -163,11 +183,16 @@ __device__ void bl_bicg_rq(const CoefArgs& a, T* sh) {
     T0 *D(a, SL_C0N) = sqrt(c2);
     SYNC;
   } else if (a.phase == 1) {  // alpha = G1^-1 G2, alpha_hat = G1^-H G2^H, AC = alpha C
-    if (sm_solve<T>(W<T>(a, SL_ALPHA), W<T>(a, SL_G1), W<T>(a, SL_G2), s, s, 0, sh)) { T0 set_brk(a, BK_GRAM); SYNC; return; }
+    if (sm_solve<T>(W<T>(a, SL_ALPHA), W<T>(a, SL_G1), W<T>(a, SL_G2), s, s, 0, sh, a.eps_brk)) { T0 set_brk(a, BK_GRAM); SYNC; return; }
     sm_copy<T>(W<T>(a, SL_TMP0), W<T>(a, SL_G2), s, s, 1);
-    if (sm_solve<T>(W<T>(a, SL_AH), W<T>(a, SL_G1), W<T>(a, SL_TMP0), s, s, 1, sh)) { T0 set_brk(a, BK_GRAM); SYNC; return; }
+    if (sm_solve<T>(W<T>(a, SL_AH), W<T>(a, SL_G1), W<T>(a, SL_TMP0), s, s, 1, sh, a.eps_brk)) { T0 set_brk(a, BK_GRAM); SYNC; return; }
     sm_gemm<T>(W<T>(a, SL_AC), W<T>(a, SL_ALPHA), W<T>(a, SL_C), s, s, s, 0, 0, one<T>());
   } else if (a.phase == 2) {  // CholQR pass 1 of Z and Z_hat
+    if (a.defl) {
+      if (!cholqr_pass1_cont<T>(a, SL_GZ, SL_R1, SL_R1I, CTL_DMASK)) return;
+      cholqr_pass1_cont<T>(a, SL_GZH, SL_R1H, SL_R1HI, CTL_DMASKH);
+      return;
+    }
     if (!cholqr_pass<T>(a, SL_GZ, SL_R1, SL_R1I, 1)) return;
     if (!cholqr_pass<T>(a, SL_GZH, SL_R1H, SL_R1HI, 1)) return;
   } else if (a.phase == 3) {  // pass 2, Sig = R2 R1, C = Sig C
@@ -177,9 +202,9 @@ __device__ void bl_bicg_rq(const CoefArgs& a, T* sh) {
     cholqr_sigma<T>(a, SL_R2H, SL_R1H, SL_SIGH, SL_CH);
   } else if (a.phase == 4) {  // beta = G2^-1 Sig_h^H G2+, beta_hat = G2^-H Sig^H G2+^H (Eqs. 6-7)
     sm_gemm<T>(W<T>(a, SL_TMP1), W<T>(a, SL_SIGH), W<T>(a, SL_G2N), s, s, s, 1, 0, one<T>());
-    if (sm_solve<T>(W<T>(a, SL_BETA), W<T>(a, SL_G2), W<T>(a, SL_TMP1), s, s, 0, sh)) { T0 set_brk(a, BK_GRAM); SYNC; return; }
+    if (sm_solve<T>(W<T>(a, SL_BETA), W<T>(a, SL_G2), W<T>(a, SL_TMP1), s, s, 0, sh, a.eps_brk)) { T0 set_brk(a, BK_GRAM); SYNC; return; }
     sm_gemm<T>(W<T>(a, SL_TMP1), W<T>(a, SL_SIG), W<T>(a, SL_G2N), s, s, s, 1, 1, one<T>());
-    if (sm_solve<T>(W<T>(a, SL_BH), W<T>(a, SL_G2), W<T>(a, SL_TMP1), s, s, 1, sh)) { T0 set_brk(a, BK_GRAM); SYNC; return; }
+    if (sm_solve<T>(W<T>(a, SL_BH), W<T>(a, SL_G2), W<T>(a, SL_TMP1), s, s, 1, sh, a.eps_brk)) { T0 set_brk(a, BK_GRAM); SYNC; return; }
     sm_copy<T>(W<T>(a, SL_G2), W<T>(a, SL_G2N), s, s, 0);
     double c2 = sm_fro2<T>(W<T>(a, SL_C), s * s, reinterpret_cast<double*>(sh));
     conv_check(a, c2);
@@ -267,7 +292,7 @@ template <typename T>
 __device__ void bl_bicgstab(const CoefArgs& a, T* sh) {
   const int s = a.s;
   if (a.phase == 1) {  // alpha = G^-1 (Rt^H R)
-    if (sm_solve<T>(W<T>(a, SL_ALPHA), W<T>(a, SL_G), W<T>(a, SL_M), s, s, 0, sh)) { T0 set_brk(a, BK_GRAM); SYNC; }
+    if (sm_solve<T>(W<T>(a, SL_ALPHA), W<T>(a, SL_G), W<T>(a, SL_M), s, s, 0, sh, a.eps_brk)) { T0 set_brk(a, BK_GRAM); SYNC; }
   } else if (a.phase == 2) {
     half_check(a, *D(a, SL_S2), *D(a, SL_R0N));
   } else if (a.phase == 3) {
@@ -277,7 +302,7 @@ __device__ void bl_bicgstab(const CoefArgs& a, T* sh) {
     }
     SYNC;
   } else if (a.phase == 4) {  // beta = -G^-1 (Rt^H T); BW = omega beta
-    if (sm_solve<T>(W<T>(a, SL_TMP1), W<T>(a, SL_G), W<T>(a, SL_MN), s, s, 0, sh)) { T0 set_brk(a, BK_GRAM); SYNC; return; }
+    if (sm_solve<T>(W<T>(a, SL_TMP1), W<T>(a, SL_G), W<T>(a, SL_MN), s, s, 0, sh, a.eps_brk)) { T0 set_brk(a, BK_GRAM); SYNC; return; }
     sm_scale<T>(W<T>(a, SL_BETA), W<T>(a, SL_TMP1), s * s, mkT(-1.0, 0.0, T()));
     sm_scale<T>(W<T>(a, SL_BW), W<T>(a, SL_BETA), s * s, *W<T>(a, SL_OMEGA));
     conv_check(a, *D(a, SL_R2));
@@ -294,7 +319,7 @@ __device__ void bl_bicgstab_rq(const CoefArgs& a, T* sh) {
     T0 *D(a, SL_C0N) = sqrt(c2);
     SYNC;
   } else if (a.phase == 1) {  // alpha = G^-1 GQ ; AC = alpha C
-    if (sm_solve<T>(W<T>(a, SL_ALPHA), W<T>(a, SL_G), W<T>(a, SL_GQ), s, s, 0, sh)) { T0 set_brk(a, BK_GRAM); SYNC; return; }
+    if (sm_solve<T>(W<T>(a, SL_ALPHA), W<T>(a, SL_G), W<T>(a, SL_GQ), s, s, 0, sh, a.eps_brk)) { T0 set_brk(a, BK_GRAM); SYNC; return; }
     sm_gemm<T>(W<T>(a, SL_AC), W<T>(a, SL_ALPHA), W<T>(a, SL_C), s, s, s, 0, 0, one<T>());
   } else if (a.phase == 2) {  // ||S||^2 = tr(C^H (Z^H Z) C)
     sm_gemm<T>(W<T>(a, SL_TMP0), W<T>(a, SL_ZZ), W<T>(a, SL_C), s, s, s, 0, 0, one<T>());
@@ -324,12 +349,13 @@ __device__ void bl_bicgstab_rq(const CoefArgs& a, T* sh) {
     if (a.ctl[CTL_FLAG] != FLAG_RUN) return;
     sm_scale<T>(W<T>(a, SL_WC), W<T>(a, SL_C), s * s, *W<T>(a, SL_OMEGA));
   } else if (a.phase == 4) {
-    cholqr_pass<T>(a, SL_GZ, SL_R1, SL_R1I, 1);
+    if (a.defl) cholqr_pass1_cont<T>(a, SL_GZ, SL_R1, SL_R1I, CTL_DMASK);
+    else cholqr_pass<T>(a, SL_GZ, SL_R1, SL_R1I, 1);
   } else if (a.phase == 5) {
     if (!cholqr_pass<T>(a, SL_GZ, SL_R2F, SL_R2I, 0)) return;
     cholqr_sigma<T>(a, SL_R2F, SL_R1, SL_SIG, SL_C);
   } else if (a.phase == 6) {  // beta = omega^-1 G^-1 GQ+ ; BW = omega beta ; GQ = GQ+
-    if (sm_solve<T>(W<T>(a, SL_TMP1), W<T>(a, SL_G), W<T>(a, SL_GQN), s, s, 0, sh)) { T0 set_brk(a, BK_GRAM); SYNC; return; }
+    if (sm_solve<T>(W<T>(a, SL_TMP1), W<T>(a, SL_G), W<T>(a, SL_GQN), s, s, 0, sh, a.eps_brk)) { T0 set_brk(a, BK_GRAM); SYNC; return; }
     const T om = *W<T>(a, SL_OMEGA);
     for (int i = threadIdx.x; i < s * s; i += blockDim.x) {
       const T b = cdiv(W<T>(a, SL_TMP1)[i], om);
@@ -459,17 +485,17 @@ __device__ void bl_qmr(const CoefArgs& a, T* sh) {
       return;
     }
     sm_gemm<T>(W<T>(a, SL_TMP0), W<T>(a, SL_XIB), W<T>(a, SL_DELTA), s, s, s, 1, 0, one<T>());
-    if (sm_solve<T>(W<T>(a, SL_C1), W<T>(a, SL_EPS), W<T>(a, SL_TMP0), s, s, 0, sh)) { T0 set_brk(a, BK_GRAM); SYNC; return; }
+    if (sm_solve<T>(W<T>(a, SL_C1), W<T>(a, SL_EPS), W<T>(a, SL_TMP0), s, s, 0, sh, a.eps_brk)) { T0 set_brk(a, BK_GRAM); SYNC; return; }
     sm_gemm<T>(W<T>(a, SL_TMP0), W<T>(a, SL_RHOB), W<T>(a, SL_DELTA), s, s, s, 1, 1, one<T>());
-    if (sm_solve<T>(W<T>(a, SL_C2), W<T>(a, SL_EPS), W<T>(a, SL_TMP0), s, s, 1, sh)) { T0 set_brk(a, BK_GRAM); SYNC; return; }
+    if (sm_solve<T>(W<T>(a, SL_C2), W<T>(a, SL_EPS), W<T>(a, SL_TMP0), s, s, 1, sh, a.eps_brk)) { T0 set_brk(a, BK_GRAM); SYNC; return; }
   } else if (a.phase == 2) {  // beta = delta^-1 eps ; gamma_hat = delta^-H eps^H
-    if (sm_solve<T>(W<T>(a, SL_BETA), W<T>(a, SL_DELTA), W<T>(a, SL_EPS), s, s, 0, sh)) { T0 set_brk(a, BK_GRAM); SYNC; return; }
+    if (sm_solve<T>(W<T>(a, SL_BETA), W<T>(a, SL_DELTA), W<T>(a, SL_EPS), s, s, 0, sh, a.eps_brk)) { T0 set_brk(a, BK_GRAM); SYNC; return; }
     sm_copy<T>(W<T>(a, SL_TMP0), W<T>(a, SL_EPS), s, s, 1);
-    if (sm_solve<T>(W<T>(a, SL_GHAT), W<T>(a, SL_DELTA), W<T>(a, SL_TMP0), s, s, 1, sh)) { T0 set_brk(a, BK_GRAM); SYNC; return; }
+    if (sm_solve<T>(W<T>(a, SL_GHAT), W<T>(a, SL_DELTA), W<T>(a, SL_TMP0), s, s, 1, sh, a.eps_brk)) { T0 set_brk(a, BK_GRAM); SYNC; return; }
   } else if (a.phase == 3) {  // CholQR pass 1 of V~ and W~ (rank deficiency of V~ with V~ == 0 -> rho+ = 0, deferred)
     T0 *D(a, SL_PEND) = 0.0;
     SYNC;
-    if (sm_chol<T>(W<T>(a, SL_R1), W<T>(a, SL_GZ), s, 1)) {
+    if (sm_chol<T>(W<T>(a, SL_R1), W<T>(a, SL_GZ), s, 1, a.eps_chol)) {
       double g2 = sm_fro2<T>(W<T>(a, SL_GZ), s * s, dsh);
       if (g2 != 0.0) { T0 set_brk(a, BK_RANK); SYNC; return; }
       T0 *D(a, SL_PEND) = 1.0;  // exactly zero block: rho+ = 0, breakdown deferred past the X update
@@ -479,7 +505,7 @@ __device__ void bl_qmr(const CoefArgs& a, T* sh) {
     } else {
       sm_trinv<T>(W<T>(a, SL_R1I), W<T>(a, SL_R1), s);
     }
-    if (sm_chol<T>(W<T>(a, SL_R1H), W<T>(a, SL_GZH), s, 1)) {
+    if (sm_chol<T>(W<T>(a, SL_R1H), W<T>(a, SL_GZH), s, 1, a.eps_chol)) {
       double g2 = sm_fro2<T>(W<T>(a, SL_GZH), s * s, dsh);
       if (g2 != 0.0) { T0 set_brk(a, BK_RANK); SYNC; return; }
       T0 *D(a, SL_PEND) = 1.0;
@@ -544,7 +570,7 @@ __device__ void bl_qmr(const CoefArgs& a, T* sh) {
     // Rii^-1 (solve against I, as the oracle) and TR = top Rii^-1
     for (int i = threadIdx.x; i < s * s; i += blockDim.x) W<T>(a, SL_TMP0)[i] = (i / s == i % s) ? one<T>() : Ar<T>::zero();
     SYNC;
-    if (sm_solve<T>(W<T>(a, SL_RIII), W<T>(a, SL_RII), W<T>(a, SL_TMP0), s, s, 0, sh)) { T0 set_brk(a, BK_GRAM); SYNC; return; }
+    if (sm_solve<T>(W<T>(a, SL_RIII), W<T>(a, SL_RII), W<T>(a, SL_TMP0), s, s, 0, sh, a.eps_brk)) { T0 set_brk(a, BK_GRAM); SYNC; return; }
     sm_gemm<T>(W<T>(a, SL_TR), top, W<T>(a, SL_RIII), s, s, s, 0, 0, one<T>());
   } else if (a.phase == 5) {  // after X, R updates: rho, xi = rho+, xi+ ; convergence, deferred breakdown
     sm_copy<T>(W<T>(a, SL_RHOB), W<T>(a, SL_RHOBN), s, s, 0);
@@ -552,6 +578,93 @@ __device__ void bl_qmr(const CoefArgs& a, T* sh) {
     conv_check(a, *D(a, SL_R2));
     T0 {
       if (*D(a, SL_PEND) != 0.0 && a.ctl[CTL_CONVPEND] == 0) set_brk(a, BK_RANK);
+    }
+    SYNC;
+  }
+}
+
+// ------------------------------------------------- QR of the search directions (f3)
+// Bl-BiCG-sQ (oracle bl_bicg_sq, reading R9): P, P̂ orthonormal, so
+// alpha = G^-1 (P̂^H R), alpha_hat = G^-H (P^H R̂), beta = -G^-1 (Q̂^H R+),
+// beta_hat = -G^-H (Q^H R̂+), G = P̂^H A P; then CholQR2 of R + P beta and R̂ + P̂ beta_hat.
+template <typename T>
+__device__ void bl_bicg_sq(const CoefArgs& a, T* sh) {
+  const int s = a.s;
+  if (a.phase == 1) {
+    if (sm_solve<T>(W<T>(a, SL_ALPHA), W<T>(a, SL_G), W<T>(a, SL_M), s, s, 0, sh, a.eps_brk)) { T0 set_brk(a, BK_GRAM); SYNC; return; }
+    if (sm_solve<T>(W<T>(a, SL_AH), W<T>(a, SL_G), W<T>(a, SL_MH), s, s, 1, sh, a.eps_brk)) { T0 set_brk(a, BK_GRAM); SYNC; return; }
+  } else if (a.phase == 2) {
+    if (sm_solve<T>(W<T>(a, SL_TMP1), W<T>(a, SL_G), W<T>(a, SL_MN), s, s, 0, sh, a.eps_brk)) { T0 set_brk(a, BK_GRAM); SYNC; return; }
+    sm_scale<T>(W<T>(a, SL_BETA), W<T>(a, SL_TMP1), s * s, mkT(-1.0, 0.0, T()));
+    if (sm_solve<T>(W<T>(a, SL_TMP1), W<T>(a, SL_G), W<T>(a, SL_MNH), s, s, 1, sh, a.eps_brk)) { T0 set_brk(a, BK_GRAM); SYNC; return; }
+    sm_scale<T>(W<T>(a, SL_BH), W<T>(a, SL_TMP1), s * s, mkT(-1.0, 0.0, T()));
+    conv_check(a, *D(a, SL_R2));
+  } else if (a.phase == 3) {  // CholQR pass 1 of the new search directions (rank test)
+    if (!cholqr_pass<T>(a, SL_GZ, SL_R1, SL_R1I, 1)) return;
+    cholqr_pass<T>(a, SL_GZH, SL_R1H, SL_R1HI, 1);
+  } else if (a.phase == 4) {  // pass 2
+    if (!cholqr_pass<T>(a, SL_GZ, SL_R2F, SL_R2I, 0)) return;
+    cholqr_pass<T>(a, SL_GZH, SL_R2H, SL_R2HI, 0);
+  }
+}
+
+// Bl-BiCGStab-sQ: App. A.4's phases 1-4, then CholQR2 of the new search direction block
+template <typename T>
+__device__ void bl_bicgstab_sq(const CoefArgs& a, T* sh) {
+  if (a.phase <= 4) bl_bicgstab<T>(a, sh);
+  else if (a.phase == 5) cholqr_pass<T>(a, SL_GZ, SL_R1, SL_R1I, 1);
+  else if (a.phase == 6) cholqr_pass<T>(a, SL_GZ, SL_R2F, SL_R2I, 0);
+}
+
+// --------------------------------------------- rank-deficiency continuation (f4)
+// Phase 20 (repair, after the fill kernel replaced the deficient columns and the Gram of
+// the modified block was formed): keep C_old, redo pass 1 strictly (a replacement vector
+// in the span of the others would be a genuine rank breakdown). k1: bit 0 the residual
+// side, bit 1 the shadow side, bit 2 the initial QR (C_old = I).
+// Phase 21 (fix-up, after Q of the modified block exists and SIGT = Q^H Z_orig): the true
+// factor Sig = triu(SIGT) with the replaced diagonal entries 0 and the others real, and
+// C = Sig C_old; then the repair is disarmed.
+template <typename T>
+__device__ void defl_phase(const CoefArgs& a) {
+  if (a.ctl[CTL_DIDLE]) return;
+  const int s = a.s;
+  const bool init = (a.k1 & 4) != 0;
+  for (int side = 0; side < 2; ++side) {
+    if (!(a.k1 & (1 << side))) continue;
+    const int gz = side ? SL_GZH : SL_GZ, r1 = side ? SL_R1H : SL_R1, r1i = side ? SL_R1HI : SL_R1I;
+    const int cs = side ? SL_CH : SL_C, co = side ? SL_COLDH : SL_COLD;
+    const int sg = side ? SL_SIGH : SL_SIG, st = side ? SL_SIGTH : SL_SIGT;
+    const int mk = side ? CTL_DMASKH : CTL_DMASK;
+    if (a.phase == 20) {
+      if (init) {
+        for (int i = threadIdx.x; i < s * s; i += blockDim.x)
+          W<T>(a, co)[i] = (i / s == i % s) ? one<T>() : Ar<T>::zero();
+      } else {
+        sm_copy<T>(W<T>(a, co), W<T>(a, cs), s, s, 0);
+      }
+      SYNC;
+      if (!cholqr_pass<T>(a, gz, r1, r1i, 1)) return;
+    } else {
+      const unsigned long long m = (unsigned long long)(unsigned)a.ctl[mk] | ((unsigned long long)(unsigned)a.ctl[mk + 1] << 32);
+      for (int i = threadIdx.x; i < s * s; i += blockDim.x) {
+        const int r = i / s, c = i % s;
+        T v = W<T>(a, st)[i];
+        if (r > c || (r == c && ((m >> c) & 1ull))) v = Ar<T>::zero();
+        else if (r == c) v = mkT(re(v), 0.0, T());
+        W<T>(a, sg)[i] = v;
+      }
+      SYNC;
+      sm_gemm<T>(W<T>(a, cs), W<T>(a, sg), W<T>(a, co), s, s, s, 0, 0, one<T>());
+      SYNC;
+    }
+  }
+  if (a.phase == 21) {
+    T0 {
+      int nrep = 0;
+      for (int q = 0; q < 4; ++q) nrep += __popc((unsigned)a.ctl[CTL_DMASK + q]);
+      a.ctl[CTL_DEFL] += nrep;
+      for (int q = 0; q < 4; ++q) a.ctl[CTL_DMASK + q] = 0;
+      a.ctl[CTL_DIDLE] = 1;
     }
     SYNC;
   }
@@ -571,14 +684,21 @@ __global__ void __launch_bounds__(256) coef_kernel(CoefArgs a) {
     const bool hat = a.phase >= 12;
     const int gz = hat ? SL_GZH : SL_GZ;
     if ((a.phase & 1) == 0) {
-      cholqr_pass<T>(a, gz, hat ? SL_R1H : SL_R1, hat ? SL_R1HI : SL_R1I, 1);
+      if (a.defl) cholqr_pass1_cont<T>(a, gz, hat ? SL_R1H : SL_R1, hat ? SL_R1HI : SL_R1I, hat ? CTL_DMASKH : CTL_DMASK);
+      else cholqr_pass<T>(a, gz, hat ? SL_R1H : SL_R1, hat ? SL_R1HI : SL_R1I, 1);
     } else {
       if (!cholqr_pass<T>(a, gz, hat ? SL_R2H : SL_R2F, hat ? SL_R2HI : SL_R2I, 0)) return;
       cholqr_sigma<T>(a, hat ? SL_R2H : SL_R2F, hat ? SL_R1H : SL_R1, hat ? SL_CH : SL_C, -1);
     }
     return;
   }
+  if (a.phase == 20 || a.phase == 21) {  // rank-deficiency continuation (f4)
+    defl_phase<T>(a);
+    return;
+  }
   switch (a.method) {
+    case M_BL_BICG_SQ: bl_bicg_sq<T>(a, sh); break;
+    case M_BL_BICGSTAB_SQ: bl_bicgstab_sq<T>(a, sh); break;
     case M_GL_BICG:
     case M_EGL_BICG: gl_bicg<T>(a); break;
     case M_LI_BICG: li_bicg<T>(a); break;

@@ -15,6 +15,10 @@ enum Ctl : int {
   CTL_BITER = 3,
   CTL_CONVPEND = 4,  // set by the last coefficient phase, committed by end_iter
   CTL_NFROZEN = 5,
+  CTL_DIDLE = 6,     // rank continuation (f4): 1 = no thin-QR repair pending (block kernels skip on it)
+  CTL_DMASK = 8,     // deficient columns of the pending repair: Z (2 ints, 64 bits), Ẑ (2 ints)
+  CTL_DMASKH = 10,
+  CTL_DEFL = 12,     // columns replaced so far (report)
   CTL_FROZEN = 16,   // 64 per-column frozen flags (Li variants, reading G13)
   CTL_SIZE = 96
 };
@@ -34,6 +38,8 @@ enum Slot : int {
   // Bl-QMR
   SL_OMP, SL_TAUT, SL_TAU, SL_TOP, SL_RII, SL_RIII, SL_TR, SL_GHAT, SL_RHOB, SL_XIB, SL_RHOBN, SL_XIBN,
   SL_PEND,
+  // QR of the search directions (f3) and the rank continuation (f4)
+  SL_MH, SL_MNH, SL_COLD, SL_COLDH, SL_SIGT, SL_SIGTH,
   SL_TMP0, SL_TMP1, SL_TMP2, SL_TMP3, SL_TMP4,
   NSLOT
 };
@@ -41,7 +47,8 @@ enum Slot : int {
 enum MethodId : int {
   M_LI_BICG = 0, M_GL_BICG, M_EGL_BICG, M_BL_BICG, M_BL_BICG_RQ,
   M_LI_QMR, M_GL_QMR, M_EGL_QMR, M_BL_QMR,
-  M_LI_BICGSTAB, M_GL_BICGSTAB, M_BL_BICGSTAB, M_BL_BICGSTAB_RQ
+  M_LI_BICGSTAB, M_GL_BICGSTAB, M_BL_BICGSTAB, M_BL_BICGSTAB_RQ,
+  M_BL_BICG_SQ, M_BL_BICGSTAB_SQ  // QR of the search directions (f3)
 };
 
 struct CoefArgs {
@@ -49,6 +56,9 @@ struct CoefArgs {
   int phase;
   int s;
   int k1;            // 1 on the first iteration (QMR)
+  int defl;          // rank policy of the rQ thin QRs: 0 BREAKDOWN(rank) (G11), 1 continuation (f4)
+  double eps_brk;    // s x s LU pivot threshold relative to max|G| (G12)
+  double eps_chol;   // CholQR pivot threshold relative to tr(G) (R5)
   double tol;
   double* ws;
   int* ctl;

@@ -100,7 +100,7 @@ __device__ double sm_fro2(const T* A, int cnt, double* red) {
 // i?amax). Returns 1 (breakdown) if a pivot <= EPS_BRK * max|G_ij| (reading G12)
 // or any entry is not finite. Scratch: (n*n + n*m) T + 2 doubles in `sh`.
 template <typename T>
-__device__ int sm_solve(T* X, const T* G, const T* M, int n, int m, int herm, T* sh) {
+__device__ int sm_solve(T* X, const T* G, const T* M, int n, int m, int herm, T* sh, double eps = EPS_BRK) {
   T* L = sh;
   T* B = sh + n * n;
   __shared__ int s_piv;
@@ -138,7 +138,7 @@ __device__ int sm_solve(T* X, const T* G, const T* M, int n, int m, int herm, T*
         if (v > best) { best = v; p = i; }
       }
       s_piv = p;
-      if (cabs(L[p * n + k]) <= EPS_BRK * s_gmax) s_bad = 1;
+      if (cabs(L[p * n + k]) <= eps * s_gmax) s_bad = 1;
     }
     __syncthreads();
     if (s_bad) return 1;
@@ -190,7 +190,7 @@ __device__ int sm_solve(T* X, const T* G, const T* M, int n, int m, int herm, T*
 // pivot, then one thread per entry R_jk (each entry's sum in the same order as a
 // serial loop, so the result does not depend on the thread count).
 template <typename T>
-__device__ int sm_chol(T* R, const T* G, int n, int check_rank) {
+__device__ int sm_chol(T* R, const T* G, int n, int check_rank, double eps = EPS_CHOL) {
   __shared__ int s_bad;
   __shared__ double s_rjj;
   for (int i = threadIdx.x; i < n * n; i += blockDim.x) R[i] = Ar<T>::zero();
@@ -200,7 +200,7 @@ __device__ int sm_chol(T* R, const T* G, int n, int check_rank) {
     if (threadIdx.x == 0) {
       double tr = 0.0;
       for (int i = 0; i < n; ++i) tr += re(G[i * n + i]);
-      const double thr = EPS_CHOL * tr;
+      const double thr = eps * tr;
       // R_jj^2 = G_jj - sum_i |R_ij|^2
       double d = re(G[j * n + j]);
       for (int i = 0; i < j; ++i) d -= Ar<T>::abs2(R[i * n + j]);
@@ -225,6 +225,53 @@ __device__ int sm_chol(T* R, const T* G, int n, int check_rank) {
   int b = s_bad;
   __syncthreads();
   return b;
+}
+
+// Cholesky with the deficient pivots skipped (rank-deficiency continuation, SURVEY §8(f)
+// f4): a pivot d_j <= eps * tr(G) sets bit j of the returned mask and leaves row j of R
+// zero (column j is dependent on the earlier ones, so the later pivots are those of the
+// block without it); ~0 on a non-finite value or a zero Gram. Same order of operations
+// as sm_chol otherwise.
+template <typename T>
+__device__ unsigned long long sm_chol_mask(T* R, const T* G, int n, double eps) {
+  __shared__ unsigned long long s_mask;
+  __shared__ int s_skip;
+  __shared__ double s_rjj;
+  for (int i = threadIdx.x; i < n * n; i += blockDim.x) R[i] = Ar<T>::zero();
+  if (threadIdx.x == 0) s_mask = 0ull;
+  __syncthreads();
+  for (int j = 0; j < n; ++j) {
+    if (threadIdx.x == 0) {
+      double tr = 0.0;
+      for (int i = 0; i < n; ++i) tr += re(G[i * n + i]);
+      double d = re(G[j * n + j]);
+      for (int i = 0; i < j; ++i) d -= Ar<T>::abs2(R[i * n + j]);
+      s_skip = 0;
+      if (!isfinite(d) || !(tr > 0.0) || !isfinite(tr)) {
+        s_mask = ~0ull;
+      } else if (d <= eps * tr) {
+        s_mask |= 1ull << j;
+        s_skip = 1;
+      } else {
+        s_rjj = sqrt(d);
+        R[j * n + j] = mkT(s_rjj, 0.0, T());
+      }
+    }
+    __syncthreads();
+    if (s_mask == ~0ull) break;
+    if (!s_skip) {
+      const double rjj = s_rjj;
+      for (int k = j + 1 + threadIdx.x; k < n; k += blockDim.x) {
+        T acc = G[j * n + k];
+        for (int i = 0; i < j; ++i) acc = Ar<T>::sub(acc, Ar<T>::mul(Ar<T>::conj(R[i * n + j]), R[i * n + k]));
+        R[j * n + k] = scal(acc, 1.0 / rjj);
+      }
+    }
+    __syncthreads();
+  }
+  const unsigned long long m = s_mask;
+  __syncthreads();
+  return m;
 }
 
 // Ri = R^{-1} for upper-triangular R; one thread per column (back substitution).

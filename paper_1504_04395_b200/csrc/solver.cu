@@ -82,6 +82,9 @@ int Solver::coef(int phase, int k1) {
   a.s = s;
   a.k1 = k1;
   a.tol = o.tol;
+  a.defl = o.rank_policy;
+  a.eps_brk = eps_brk();
+  a.eps_chol = eps_chol();
   a.ws = ws;
   a.ctl = ctl;
   a.hist = hist;
@@ -118,10 +121,13 @@ double Solver::true_rel(const void* Xc) {
   return sqrt(v[0]) / v[1];
 }
 
+__global__ static void ctl_init_kernel(int* ctl) { ctl[CTL_DIDLE] = 1; }
+
 int Solver::start(const void* Bd, const void* X0d) {
   cudaStream_t st = c->st;
   cudaMemcpyAsync(B, Bd, (size_t)n * s * esz(), cudaMemcpyDeviceToDevice, st);
   cudaMemsetAsync(ctl, 0, CTL_SIZE * sizeof(int), st);
+  ctl_init_kernel<<<1, 1, 0, st>>>(ctl);  // CTL_DIDLE = 1: no thin-QR repair pending (f4)
   host_iter = 0;
   state = 0;
   half = 0;
@@ -306,17 +312,90 @@ int Solver::residual(void* out, int64_t* rows) {
 }
 
 // ---------------------------------------------------------------------------
+// Rank-deficiency continuation (reading R8): the replacement vectors
+// come from a counter-based generator (SplitMix64, the definition oracle/linalg.py's
+// counter_uniform also implements — no shared code): vector `key` = event * 64 + column,
+// entry i = 2u - 1 with u = (splitmix64(h + 2i + part) >> 11) 2^-53, stream
+// h = splitmix64(seed ^ (key * 0x9E3779B97F4A7C15)), part 0 real / 1 imaginary.
+// ---------------------------------------------------------------------------
+constexpr unsigned long long DEFL_SEED = 0x5EED1504ull;
+
+__device__ __forceinline__ unsigned long long splitmix64(unsigned long long x) {
+  unsigned long long z = x + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+__device__ __forceinline__ double counter_u(unsigned long long h, unsigned long long i, int part) {
+  return (double)(splitmix64(h + 2ull * i + (unsigned long long)part) >> 11) * 0x1.0p-53 * 2.0 - 1.0;
+}
+
+// Armed only while a repair is pending (ctl[CTL_DIDLE] == 0): Zsave = Z, and every
+// deficient column j of Z (mask in ctl[maskoff..+1]) becomes replacement vector
+// (event, j), event = 0 for the initial QR, else 2 k + hat in iteration k.
+__global__ void defl_fill_kernel(double* Z, double* Zsave, long long n, int s, int cplx, const int* ctl, int maskoff,
+                                 int hat, int init) {
+  if (ctl[CTL_DIDLE]) return;
+  const unsigned long long m = (unsigned long long)(unsigned)ctl[maskoff] |
+                               ((unsigned long long)(unsigned)ctl[maskoff + 1] << 32);
+  const unsigned long long event = init ? 0ull : 2ull * (unsigned long long)(ctl[CTL_ITER] + 1) + (unsigned long long)hat;
+  const int nd = cplx ? 2 : 1;
+  const long long total = n * s;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x) {
+    const long long i = e / s;
+    const int c = (int)(e % s);
+    for (int p = 0; p < nd; ++p) Zsave[e * nd + p] = Z[e * nd + p];
+    if ((m >> c) & 1ull) {
+      const unsigned long long key = event * 64ull + (unsigned long long)c;
+      const unsigned long long h = splitmix64(DEFL_SEED ^ (key * 0x9E3779B97F4A7C15ull));
+      for (int p = 0; p < nd; ++p) Z[e * nd + p] = counter_u(h, (unsigned long long)i, p);
+    }
+  }
+}
+
+// The repair sequence between pass 1 and the rest of a thin QR (all no-ops unless armed):
+// fill Z (and Ẑ), the Gram of the modified blocks, phase 20 (redo pass 1, keep C_old).
+void Solver::defl_repair(void* Z, void* Zs, void* Zh, void* Zhs, bool init) {
+  const int g = std::max(1, std::min(c->nsm * 8, (int)((n * s + 255) / 256)));
+  const int* saved = e.done;
+  e.done = ctl + CTL_DIDLE;
+  defl_fill_kernel<<<g, 256, 0, c->st>>>((double*)Z, (double*)Zs, n, s, cplx, ctl, CTL_DMASK, 0, init);
+  e.nlaunch++;
+  e.upd(s, {Z}, {}, {RQ{RED_FULL, 0, 0, nullptr, off[SL_GZ]}});
+  if (Zh) {
+    defl_fill_kernel<<<g, 256, 0, c->st>>>((double*)Zh, (double*)Zhs, n, s, cplx, ctl, CTL_DMASKH, 1, init);
+    e.nlaunch++;
+    e.upd(s, {Zh}, {}, {RQ{RED_FULL, 0, 0, nullptr, off[SL_GZH]}});
+  }
+  e.done = saved;
+  coef(20, (Zh ? 3 : 1) | (init ? 4 : 0));
+}
+
+// After Q (and Q̂) of the modified blocks exist: SIGT = Q^H Z_orig, then phase 21.
+void Solver::defl_fixup(const void* Q, const void* Zs, const void* Qh, const void* Zhs, bool init) {
+  const int* saved = e.done;
+  e.done = ctl + CTL_DIDLE;
+  e.upd(s, {Zs, Q}, {}, {RQ{RED_FULL, 0, 1, nullptr, off[SL_SIGT]}});
+  if (Qh) e.upd(s, {Zhs, Qh}, {}, {RQ{RED_FULL, 0, 1, nullptr, off[SL_SIGTH]}});
+  e.done = saved;
+  coef(21, (Qh ? 3 : 1) | (init ? 4 : 0));
+}
+
+// ---------------------------------------------------------------------------
 // device thin QR (CholQR2) used by the rQ variants' initialisation and srk_tsqr
 // Phases 10/11 (slots GZ -> R1, C) and 12/13 (GZH -> R1H, CH) of the coefficient kernel.
 // ---------------------------------------------------------------------------
-static void dev_tsqr(Solver& S, const void* Z, void* Q, bool hat) {
+// (zsave != null: the rQ rank continuation is on — Z may be modified in place by the repair)
+static void dev_tsqr(Solver& S, const void* Z, void* Q, bool hat, void* zsave = nullptr) {
   Eng& e = S.e;
   const int gz = hat ? SL_GZH : SL_GZ;
   e.upd(S.s, {Z}, {OutSpec{nullptr, {{0, C1()}}}}, {RQ{RED_FULL, O0, O0, nullptr, S.off[gz]}});
   S.coef(hat ? 12 : 10);
+  if (zsave) S.defl_repair(const_cast<void*>(Z), zsave, nullptr, nullptr, true);
   e.upd(S.s, {Z}, {OutSpec{Q, {{0, FU(S.off[hat ? SL_R1HI : SL_R1I])}}}}, {RQ{RED_FULL, O0, O0, nullptr, S.off[gz]}});
   S.coef(hat ? 13 : 11);
   e.upd(S.s, {Q}, {OutSpec{Q, {{0, FU(S.off[hat ? SL_R2HI : SL_R2I])}}}}, {});
+  if (zsave) S.defl_fixup(Q, zsave, nullptr, nullptr, true);
 }
 
 static inline Coef NEG1() { return Coef{CK_ONE, 0, 1, 0, 0}; }
@@ -397,6 +476,8 @@ struct EglBiCG : Solver {  // Alg. 4
     g.ca.method = method;
     g.ca.s = s;
     g.ca.tol = o.tol;
+    g.ca.eps_brk = eps_brk();
+    g.ca.eps_chol = eps_chol();
     g.ca.ws = ws;
     g.ca.ctl = ctl;
     g.ca.hist = hist;
@@ -457,15 +538,21 @@ struct BlBiCG : Solver {  // Alg. 3
 
 struct BlBiCGrQ : Solver {  // Alg. 5
   void *Qr, *Qh, *V, *Vh, *W, *Wh, *Z, *Zh;
+  void *Zs = nullptr, *Zhs = nullptr;  // rank continuation (f4): the blocks before the repair
   bool is_rq() const override { return true; }
   int alloc() override {
     Qr = blk(); Qh = blk(); V = blk(); Vh = blk(); W = blk(); Wh = blk(); Z = blk(); Zh = blk();
+    if (o.rank_policy) {
+      Zs = blk();
+      Zhs = blk();
+      if (!Zs || !Zhs) return SRK_ENOMEM;
+    }
     cols_A = s; cols_AH = s;
     return (Qr && Qh && V && Vh && W && Wh && Z && Zh) ? 0 : SRK_ENOMEM;
   }
   int init() override {
     const size_t b = (size_t)n * s * esz();
-    dev_tsqr(*this, R, Qr, false);  // Q(0) C(0) = R(0)
+    dev_tsqr(*this, R, Qr, false, Zs);  // Q(0) C(0) = R(0)
     // shadow R̂0 = R0: Q̂(0) = Q(0), Ĉ(0) = C(0)
     cudaMemcpyAsync(Qh, Qr, b, cudaMemcpyDeviceToDevice, c->st);
     cudaMemcpyAsync(ws + off[SL_CH], ws + off[SL_C], s * s * esz(), cudaMemcpyDeviceToDevice, c->st);
@@ -484,11 +571,13 @@ struct BlBiCGrQ : Solver {  // Alg. 5
            OutSpec{Zh, {{4, C1()}, {5, FU(off[SL_AH], 1)}}}},
           {RQ{RED_FULL, O1, O1, nullptr, off[SL_GZ]}, RQ{RED_FULL, O2, O2, nullptr, off[SL_GZH]}});
     coef(2);
+    if (Zs) defl_repair(Z, Zs, Zh, Zhs, false);
     e.upd(s, {Z, Zh}, {OutSpec{Z, {{0, FU(off[SL_R1I])}}}, OutSpec{Zh, {{1, FU(off[SL_R1HI])}}}},
           {RQ{RED_FULL, O0, O0, nullptr, off[SL_GZ]}, RQ{RED_FULL, O1, O1, nullptr, off[SL_GZH]}});
     coef(3);
     e.upd(s, {Z, Zh}, {OutSpec{Qr, {{0, FU(off[SL_R2I])}}}, OutSpec{Qh, {{1, FU(off[SL_R2HI])}}}},
           {RQ{RED_FULL, O0, O1, nullptr, off[SL_G2N]}});
+    if (Zs) defl_fixup(Qr, Zs, Qh, Zhs, false);
     coef(4);
     e.upd(s, {Qr, V, Qh, Vh},
           {OutSpec{V, {{0, C1()}, {1, FU(off[SL_BETA])}}}, OutSpec{Vh, {{2, C1()}, {3, FU(off[SL_BH])}}}}, {});
@@ -590,16 +679,18 @@ struct BlBiCGStab : Solver {  // [ELg03], SURVEY App. A.4
 
 struct BlBiCGStabrQ : Solver {
   void *Qr, *Q0, *V, *W, *Z, *Y;
+  void* Zs = nullptr;  // rank continuation (f4)
   bool is_rq() const override { return true; }
   int nseg() const override { return 2; }
   int alloc() override {
     Qr = blk(); Q0 = blk(); V = blk(); W = blk(); Z = blk(); Y = blk(); tmp2 = blk();
+    if (o.rank_policy && !(Zs = blk())) return SRK_ENOMEM;
     cols_A = 2 * s; cols_AH = 0;
     return (Qr && Q0 && V && W && Z && Y && tmp2) ? 0 : SRK_ENOMEM;
   }
   int init() override {
     const size_t b = (size_t)n * s * esz();
-    dev_tsqr(*this, R, Qr, false);
+    dev_tsqr(*this, R, Qr, false, Zs);
     cudaMemcpyAsync(Q0, Qr, b, cudaMemcpyDeviceToDevice, c->st);  // Q̂0 = Qr when R̃ = R0
     cudaMemcpyAsync(V, Qr, b, cudaMemcpyDeviceToDevice, c->st);
     e.upd(s, {Qr, Q0}, {}, {RQ{RED_FULL, 0, 1, nullptr, off[SL_GQ]}});
@@ -619,9 +710,11 @@ struct BlBiCGStabrQ : Solver {
              OutSpec{Z, {{2, C1()}, {3, SC(off[SL_OMEGA], 1)}}}},
             {RQ{RED_FULL, O1, O1, nullptr, off[SL_GZ]}});
       coef(4);
+      if (Zs) defl_repair(Z, Zs, nullptr, nullptr, false);
       e.upd(s, {Z}, {OutSpec{Z, {{0, FU(off[SL_R1I])}}}}, {RQ{RED_FULL, O0, O0, nullptr, off[SL_GZ]}});
       coef(5);
       e.upd(s, {Z, Q0}, {OutSpec{Qr, {{0, FU(off[SL_R2I])}}}}, {RQ{RED_FULL, O0, 1, nullptr, off[SL_GQN]}});
+      if (Zs) defl_fixup(Qr, Zs, nullptr, nullptr, false);
       coef(6);
       e.upd(s, {Qr, V, W}, {OutSpec{V, {{0, C1()}, {1, FU(off[SL_BETA])}, {2, FU(off[SL_BW], 1)}}}}, {});
     }
@@ -706,6 +799,8 @@ struct QMR : Solver {  // mode 0 Li, 1 Gl, 2 eGl
     g.ca.method = method;
     g.ca.s = s;
     g.ca.tol = o.tol;
+    g.ca.eps_brk = eps_brk();
+    g.ca.eps_chol = eps_chol();
     g.ca.ws = ws;
     g.ca.ctl = ctl;
     g.ca.hist = hist;
@@ -794,6 +889,94 @@ struct BlQMR : Solver {
   }
 };
 
+// =============================================================================
+// QR of the search directions: the
+// [O'Leary] stabilisation the paper compares with; oracle bl_bicg_sq / bl_bicgstab_sq
+// (reading R9). P (and P̂) are kept orthonormal by a CholQR2 per iteration.
+// =============================================================================
+struct BlBiCGsQ : Solver {
+  void *P, *Q, *Rh, *Ph, *Qh;
+  int alloc() override {
+    P = blk(); Q = blk(); Rh = blk(); Ph = blk(); Qh = blk();
+    cols_A = s; cols_AH = s;
+    return (P && Q && Rh && Ph && Qh) ? 0 : SRK_ENOMEM;
+  }
+  int init() override {
+    const size_t b = (size_t)n * s * esz();
+    cudaMemcpyAsync(Rh, R, b, cudaMemcpyDeviceToDevice, c->st);  // R̂0 = R0
+    dev_tsqr(*this, R, P, false);                                 // P = orthonormal basis of R0
+    cudaMemcpyAsync(Ph, P, b, cudaMemcpyDeviceToDevice, c->st);
+    e.upd(s, {R, Ph, Rh, P}, {}, {RQ{RED_FULL, 0, 1, nullptr, off[SL_M]}, RQ{RED_FULL, 2, 3, nullptr, off[SL_MH]}});
+    return coef(0);
+  }
+  void seg(int) override {
+    e.spmm(false, P, Q, s, {RQ{RED_FULL, 0, -1, Ph, off[SL_G]}});  // G = P̂^H A P
+    e.spmm(true, Ph, Qh, s, {});
+    coef(1);  // alpha = G^-1 P̂^H R, alpha_hat = G^-H P^H R̂
+    e.upd(s, {X, P, R, Q, Rh, Qh},
+          {OutSpec{X, {{0, C1()}, {1, FU(off[SL_ALPHA])}}},
+           OutSpec{R, {{2, C1()}, {3, FU(off[SL_ALPHA], 1)}}},
+           OutSpec{Rh, {{4, C1()}, {5, FU(off[SL_AH], 1)}}}},
+          {RQ{RED_NORM2, O1, -1, nullptr, off[SL_R2]}, RQ{RED_FULL, O1, 5, nullptr, off[SL_MN]},
+           RQ{RED_FULL, O2, 3, nullptr, off[SL_MNH]}});
+    coef(2);  // beta = -G^-1 Q̂^H R+, beta_hat = -G^-H Q^H R̂+
+    e.upd(s, {R, P, Rh, Ph}, {OutSpec{P, {{0, C1()}, {1, FU(off[SL_BETA])}}}, OutSpec{Ph, {{2, C1()}, {3, FU(off[SL_BH])}}}},
+          {RQ{RED_FULL, O0, O0, nullptr, off[SL_GZ]}, RQ{RED_FULL, O1, O1, nullptr, off[SL_GZH]}});
+    coef(3);  // CholQR2 pass 1 (rank test)
+    e.upd(s, {P, Ph}, {OutSpec{P, {{0, FU(off[SL_R1I])}}}, OutSpec{Ph, {{1, FU(off[SL_R1HI])}}}},
+          {RQ{RED_FULL, O0, O0, nullptr, off[SL_GZ]}, RQ{RED_FULL, O1, O1, nullptr, off[SL_GZH]}});
+    coef(4);  // pass 2; the next alpha's Grams with the new orthonormal directions
+    e.upd(s, {P, Ph, R, Rh}, {OutSpec{P, {{0, FU(off[SL_R2I])}}}, OutSpec{Ph, {{1, FU(off[SL_R2HI])}}}},
+          {RQ{RED_FULL, 2, O1, nullptr, off[SL_M]}, RQ{RED_FULL, 3, O0, nullptr, off[SL_MH]}});
+  }
+};
+
+struct BlBiCGStabsQ : Solver {
+  void *P, *U, *S, *T, *Rt;
+  int nseg() const override { return 2; }
+  int alloc() override {
+    P = blk(); U = blk(); S = blk(); T = blk(); Rt = blk(); tmp2 = blk();
+    cols_A = 2 * s; cols_AH = 0;
+    return (P && U && S && T && Rt && tmp2) ? 0 : SRK_ENOMEM;
+  }
+  int init() override {
+    const size_t b = (size_t)n * s * esz();
+    cudaMemcpyAsync(Rt, R, b, cudaMemcpyDeviceToDevice, c->st);
+    dev_tsqr(*this, R, P, false);  // P = orthonormal basis of R0
+    e.upd(s, {R, Rt}, {}, {RQ{RED_FULL, 0, 1, nullptr, off[SL_M]}});  // R̃^H R
+    return coef(0);
+  }
+  void seg(int q) override {
+    if (q == 0) {
+      e.spmm(false, P, U, s, {RQ{RED_FULL, 0, -1, Rt, off[SL_G]}});  // G = R̃^H U
+      coef(1);
+      e.upd(s, {R, U}, {OutSpec{S, {{0, C1()}, {1, FU(off[SL_ALPHA], 1)}}}}, {RQ{RED_NORM2, O0, -1, nullptr, off[SL_S2]}});
+      coef(2);
+    } else {
+      e.spmm(false, S, T, s, {RQ{RED_TRACE, 0, -1, S, off[SL_ST]}, RQ{RED_NORM2, 0, -1, nullptr, off[SL_TT]}});
+      coef(3);
+      e.upd(s, {X, P, S, T, Rt},
+            {OutSpec{X, {{0, C1()}, {1, FU(off[SL_ALPHA])}, {2, SC(off[SL_OMEGA])}}},
+             OutSpec{R, {{2, C1()}, {3, SC(off[SL_OMEGA], 1)}}}},
+            {RQ{RED_FULL, 3, 4, nullptr, off[SL_MN]}, RQ{RED_FULL, O1, 4, nullptr, off[SL_M]},
+             RQ{RED_NORM2, O1, -1, nullptr, off[SL_R2]}});
+      coef(4);
+      e.upd(s, {R, P, U}, {OutSpec{P, {{0, C1()}, {1, FU(off[SL_BETA])}, {2, FU(off[SL_BW], 1)}}}},
+            {RQ{RED_FULL, O0, O0, nullptr, off[SL_GZ]}});
+      coef(5);  // CholQR2 of the new search directions
+      e.upd(s, {P}, {OutSpec{P, {{0, FU(off[SL_R1I])}}}}, {RQ{RED_FULL, O0, O0, nullptr, off[SL_GZ]}});
+      coef(6);
+      e.upd(s, {P}, {OutSpec{P, {{0, FU(off[SL_R2I])}}}}, {});
+    }
+  }
+  void half_x(void* Xh) override {
+    const int* sv = e.done;
+    e.done = nullptr;
+    e.upd(s, {X, P}, {OutSpec{Xh, {{0, C1()}, {1, FU(off[SL_ALPHA])}}}}, {});
+    e.done = sv;
+  }
+};
+
 Solver* make_solver(int m) {
   switch (m) {
     case M_LI_BICG: { auto* p = new GlBiCG(); p->li = true; return p; }
@@ -809,6 +992,8 @@ Solver* make_solver(int m) {
     case M_GL_BICGSTAB: return new GlBiCGStab();
     case M_BL_BICGSTAB: return new BlBiCGStab();
     case M_BL_BICGSTAB_RQ: return new BlBiCGStabrQ();
+    case M_BL_BICG_SQ: return new BlBiCGsQ();
+    case M_BL_BICGSTAB_SQ: return new BlBiCGStabsQ();
     default: return nullptr;
   }
 }

@@ -56,7 +56,12 @@ struct Solver {
   void* blk();                 // allocate an n x s block
   void* vecn();                // allocate an n-vector
   int coef(int phase, int k1 = 0);
+  // rank-deficiency continuation of the rQ thin QRs (f4): armed by pass 1, else no-ops
+  void defl_repair(void* Z, void* Zs, void* Zh, void* Zhs, bool init);
+  void defl_fixup(const void* Q, const void* Zs, const void* Qh, const void* Zhs, bool init);
   size_t esz() const { return cplx ? 16 : 8; }
+  double eps_brk() const { return o.eps_brk > 0 ? o.eps_brk : 1e-14; }    // reading G12
+  double eps_chol() const { return o.eps_defl > 0 ? o.eps_defl : 1e-14; }  // reading R5
   int start(const void* Bd, const void* X0d);
   int iterate(int k);
   double true_rel(const void* Xc);  // sync
