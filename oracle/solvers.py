@@ -148,9 +148,12 @@ def _shadow_block(run: _Run, shadow):
 
 
 def _shadow_vector(run: _Run, shadow):
-    """Economic r̂0: arithmetic mean of the initial residuals."""
+    """Economic r̂0: arithmetic mean of the initial residuals; 'conj' its
+    complex conjugate (the economic analogue of R̂0 = conj(R0)), or a given vector."""
     if shadow is None or (isinstance(shadow, str) and shadow == "mean"):
         return run.R0.mean(axis=1)
+    if isinstance(shadow, str) and shadow == "conj":
+        return run.R0.mean(axis=1).conj()
     return np.array(shadow, dtype=run.dt).reshape(-1)
 
 

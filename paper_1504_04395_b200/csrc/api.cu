@@ -619,6 +619,12 @@ int srk_solver_get_x(srk_solver* h, void* X) {
   } else {
     cudaMemcpyAsync(X, sv->X, (size_t)sv->n * sv->s * sv->esz(), cudaMemcpyDeviceToDevice, sv->c->st);
   }
+  if (sv->o.preprocess_rhs) {  // X = Y C_B (the solution for the original B)
+    const int* saved = sv->e.done;
+    sv->e.done = nullptr;
+    sv->e.upd(sv->s, {X}, {OutSpec{X, {{0, FU(sv->off[SL_CB])}}}}, {});
+    sv->e.done = saved;
+  }
   cudaError_t e = cudaStreamSynchronize(sv->c->st);
   return e == cudaSuccess ? SRK_OK : cuda_fail(e, "srk_solver_get_x");
 }
@@ -627,6 +633,31 @@ int srk_solver_get_residual(srk_solver* h, void* out, int64_t* rows) {
   if (!h || !out) return fail(SRK_EINVAL, "srk_solver_get_residual: null argument");
   int r = h->sv->residual(out, rows);
   return r ? fail(r, "srk_solver_get_residual") : SRK_OK;
+}
+
+// Vector operations of k iterations in Proposition 1's convention (an inner
+// product or a SAXPY of length n counts one; the s x s algebra is neglected):
+// BiCG 7s (Li / Gl) and 7s^2 (Bl) as the proposition states; the other variants by the
+// same count of their step lists (a thin QR counts 3s^2; QMR's
+// first iteration skips the P / Q and D / S recurrences). A BiCGStab half-step exit is
+// counted as a whole iteration.
+static int64_t vector_ops(int m, int64_t s, int64_t k) {
+  const int64_t s2 = s * s;
+  switch (m) {
+    case SRK_LI_BICG: case SRK_GL_BICG: return 7 * s * k;
+    case SRK_EGL_BICG: return (5 * s + 2) * k;
+    case SRK_BL_BICG: return 7 * s2 * k;
+    case SRK_BL_BICG_RQ: return 13 * s2 * k;
+    case SRK_LI_QMR: case SRK_GL_QMR: return k > 0 ? 10 * s * k - 2 * s : 0;
+    case SRK_EGL_QMR: return k > 0 ? (8 * s + 2) * k - (s + 1) : 0;
+    case SRK_BL_QMR: return k > 0 ? 16 * s2 * k - 2 * s2 : 0;
+    case SRK_LI_BICGSTAB: case SRK_GL_BICGSTAB: return 10 * s * k;
+    case SRK_BL_BICGSTAB: return (6 * s2 + 5 * s) * k;
+    case SRK_BL_BICGSTAB_RQ: return (12 * s2 + s) * k;
+    case SRK_BL_BICG_SQ: return 16 * s2 * k;
+    case SRK_BL_BICGSTAB_SQ: return (9 * s2 + 5 * s) * k;
+    default: return 0;
+  }
 }
 
 int srk_solver_report(srk_solver* h, srk_report* rep) {
@@ -648,6 +679,7 @@ int srk_solver_report(srk_solver* h, srk_report* rep) {
   rep->final_recursive_rel_residual = last;
   rep->seconds = sv->seconds;
   rep->kernel_launches = sv->launches;
+  rep->vector_ops = vector_ops(sv->method, sv->s, it);
   rep->deflated_cols = sv->ctl_host[CTL_DEFL];
   rep->breakdown_col = -1;
   for (int c = 0; c < sv->s && c < 64; ++c)

@@ -40,6 +40,7 @@ enum Slot : int {
   SL_PEND,
   // QR of the search directions (f3) and the rank continuation (f4)
   SL_MH, SL_MNH, SL_COLD, SL_COLDH, SL_SIGT, SL_SIGTH,
+  SL_CB,  // R factor of the right-hand sides under preprocess_rhs (B = Q C_B)
   SL_TMP0, SL_TMP1, SL_TMP2, SL_TMP3, SL_TMP4,
   NSLOT
 };

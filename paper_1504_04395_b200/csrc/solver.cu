@@ -122,12 +122,18 @@ double Solver::true_rel(const void* Xc) {
 }
 
 __global__ static void ctl_init_kernel(int* ctl) { ctl[CTL_DIDLE] = 1; }
+static void dev_tsqr(Solver& S, const void* Z, void* Q, bool hat, void* zsave = nullptr);
 
 int Solver::start(const void* Bd, const void* X0d) {
   cudaStream_t st = c->st;
+  if (o.preprocess_rhs && X0d) return SRK_EUNSUPPORTED;  // X0 = 0 with the QR preprocessing
   cudaMemcpyAsync(B, Bd, (size_t)n * s * esz(), cudaMemcpyDeviceToDevice, st);
   cudaMemsetAsync(ctl, 0, CTL_SIZE * sizeof(int), st);
   ctl_init_kernel<<<1, 1, 0, st>>>(ctl);  // CTL_DIDLE = 1: no thin-QR repair pending (f4)
+  if (o.preprocess_rhs) {  // B = Q C_B; solve A Y = Q and return X = Y C_B (reading G9)
+    dev_tsqr(*this, B, B, false);
+    cudaMemcpyAsync(ws + off[SL_CB], ws + off[SL_C], (size_t)s * s * esz(), cudaMemcpyDeviceToDevice, st);
+  }
   host_iter = 0;
   state = 0;
   half = 0;
@@ -382,11 +388,63 @@ void Solver::defl_fixup(const void* Q, const void* Zs, const void* Qh, const voi
 }
 
 // ---------------------------------------------------------------------------
+// Shadow residuals (srk_opts.shadow): 0 the paper's choice (R̂0 =
+// R0, economic r̂0 = mean of the columns), 1 conj(R0) (economic: conj of the mean),
+// 2 the column mean (rank-one block r̂0 1^T for the non-economic variants),
+// 3 a caller-given block / vector.
+// ---------------------------------------------------------------------------
+__global__ static void conj_copy_kernel(const double2* src, double2* dst, long long cnt) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < cnt; i += (long long)gridDim.x * blockDim.x) {
+    const double2 v = src[i];
+    dst[i] = make_double2(v.x, -v.y);
+  }
+}
+template <typename T>
+__global__ static void bcast_cols_kernel(const T* v, T* dst, long long n, int s) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n * s; e += (long long)gridDim.x * blockDim.x)
+    dst[e] = v[e / s];
+}
+
+int Solver::shadow_vec_into(void* dst) {
+  const int g = std::max(1, std::min(c->nsm * 8, (int)((n + 255) / 256)));
+  if (o.shadow == 3) {
+    if (!o.shadow_given) return SRK_EINVAL;
+    cudaMemcpyAsync(dst, o.shadow_given, (size_t)n * esz(), cudaMemcpyDeviceToDevice, c->st);
+    return 0;
+  }
+  launch_row_mean(cplx, R, dst, n, s, nullptr, c->st);
+  if (o.shadow == 1 && cplx) conj_copy_kernel<<<g, 256, 0, c->st>>>((const double2*)dst, (double2*)dst, n);
+  return 0;
+}
+
+int Solver::shadow_into(void* dst) {
+  const size_t b = (size_t)n * s * esz();
+  const int g = std::max(1, std::min(c->nsm * 8, (int)((n * s + 255) / 256)));
+  switch (o.shadow) {
+    case 0: cudaMemcpyAsync(dst, R, b, cudaMemcpyDeviceToDevice, c->st); return 0;
+    case 1:
+      if (cplx) conj_copy_kernel<<<g, 256, 0, c->st>>>((const double2*)R, (double2*)dst, n * s);
+      else cudaMemcpyAsync(dst, R, b, cudaMemcpyDeviceToDevice, c->st);
+      return 0;
+    case 2:
+      launch_row_mean(cplx, R, tmp, n, s, nullptr, c->st);  // tmp: scratch (its first n entries)
+      if (cplx) bcast_cols_kernel<double2><<<g, 256, 0, c->st>>>((const double2*)tmp, (double2*)dst, n, s);
+      else bcast_cols_kernel<double><<<g, 256, 0, c->st>>>((const double*)tmp, (double*)dst, n, s);
+      return 0;
+    case 3:
+      if (!o.shadow_given) return SRK_EINVAL;
+      cudaMemcpyAsync(dst, o.shadow_given, b, cudaMemcpyDeviceToDevice, c->st);
+      return 0;
+    default: return SRK_EINVAL;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // device thin QR (CholQR2) used by the rQ variants' initialisation and srk_tsqr
 // Phases 10/11 (slots GZ -> R1, C) and 12/13 (GZH -> R1H, CH) of the coefficient kernel.
 // ---------------------------------------------------------------------------
 // (zsave != null: the rQ rank continuation is on — Z may be modified in place by the repair)
-static void dev_tsqr(Solver& S, const void* Z, void* Q, bool hat, void* zsave = nullptr) {
+static void dev_tsqr(Solver& S, const void* Z, void* Q, bool hat, void* zsave) {
   Eng& e = S.e;
   const int gz = hat ? SL_GZH : SL_GZ;
   e.upd(S.s, {Z}, {OutSpec{nullptr, {{0, C1()}}}}, {RQ{RED_FULL, O0, O0, nullptr, S.off[gz]}});
@@ -415,9 +473,9 @@ struct GlBiCG : Solver {  // Alg. 2 (Gl) and Alg. 1 (Li: diag coefficients)
   Coef K(int slot, int neg = 0, int cj = 0) const { return li ? DG(off[slot], neg, cj) : SC(off[slot], neg, cj); }
   int init() override {
     const size_t b = (size_t)n * s * esz();
-    cudaMemcpyAsync(Rh, R, b, cudaMemcpyDeviceToDevice, c->st);  // shadow R̂0 = R0
+    if (int r = shadow_into(Rh)) return r;  // shadow R̂0 (default R0)
     cudaMemcpyAsync(P, R, b, cudaMemcpyDeviceToDevice, c->st);
-    cudaMemcpyAsync(Ph, R, b, cudaMemcpyDeviceToDevice, c->st);
+    cudaMemcpyAsync(Ph, Rh, b, cudaMemcpyDeviceToDevice, c->st);
     e.upd(s, {R, Rh}, {}, {RQ{rmode(), 0, 1, nullptr, off[SL_RHO]}});
     return coef(0);
   }
@@ -445,7 +503,7 @@ struct EglBiCG : Solver {  // Alg. 4
   }
   int init() override {
     cudaMemcpyAsync(P, R, (size_t)n * s * esz(), cudaMemcpyDeviceToDevice, c->st);
-    launch_row_mean(cplx, R, rh, n, s, nullptr, c->st);  // r̂0 = mean of the columns
+    if (int r = shadow_vec_into(rh)) return r;  // r̂0 (default: mean of the columns)
     cudaMemcpyAsync(ph, rh, (size_t)n * esz(), cudaMemcpyDeviceToDevice, c->st);
     e.upd(s, {R}, {}, {RQ{RED_SUMVEC, 0, -1, rh, off[SL_RHO]}});
     return coef(0);
@@ -515,9 +573,9 @@ struct BlBiCG : Solver {  // Alg. 3
   }
   int init() override {
     const size_t b = (size_t)n * s * esz();
-    cudaMemcpyAsync(Rh, R, b, cudaMemcpyDeviceToDevice, c->st);
+    if (int r = shadow_into(Rh)) return r;
     cudaMemcpyAsync(P, R, b, cudaMemcpyDeviceToDevice, c->st);
-    cudaMemcpyAsync(Ph, R, b, cudaMemcpyDeviceToDevice, c->st);
+    cudaMemcpyAsync(Ph, Rh, b, cudaMemcpyDeviceToDevice, c->st);
     e.upd(s, {R, Rh}, {}, {RQ{RED_FULL, 0, 1, nullptr, off[SL_M]}});  // M = R̂^H R
     return coef(0);
   }
@@ -553,9 +611,13 @@ struct BlBiCGrQ : Solver {  // Alg. 5
   int init() override {
     const size_t b = (size_t)n * s * esz();
     dev_tsqr(*this, R, Qr, false, Zs);  // Q(0) C(0) = R(0)
-    // shadow R̂0 = R0: Q̂(0) = Q(0), Ĉ(0) = C(0)
-    cudaMemcpyAsync(Qh, Qr, b, cudaMemcpyDeviceToDevice, c->st);
-    cudaMemcpyAsync(ws + off[SL_CH], ws + off[SL_C], s * s * esz(), cudaMemcpyDeviceToDevice, c->st);
+    if (o.shadow == 0) {  // shadow R̂0 = R0: Q̂(0) = Q(0), Ĉ(0) = C(0)
+      cudaMemcpyAsync(Qh, Qr, b, cudaMemcpyDeviceToDevice, c->st);
+      cudaMemcpyAsync(ws + off[SL_CH], ws + off[SL_C], s * s * esz(), cudaMemcpyDeviceToDevice, c->st);
+    } else {              // Q̂(0) Ĉ(0) = R̂0
+      if (int r = shadow_into(Zh)) return r;
+      dev_tsqr(*this, Zh, Qh, true);
+    }
     cudaMemcpyAsync(V, Qr, b, cudaMemcpyDeviceToDevice, c->st);
     cudaMemcpyAsync(Vh, Qh, b, cudaMemcpyDeviceToDevice, c->st);
     e.upd(s, {Qr, Qh}, {}, {RQ{RED_FULL, 0, 1, nullptr, off[SL_G2]}});  // G2 = Q̂^H Q
@@ -605,7 +667,7 @@ struct GlBiCGStab : Solver {  // Gl (scalar) and Li (diag)
   Coef K(int slot, int neg = 0) const { return li ? DG(off[slot], neg) : SC(off[slot], neg); }
   int init() override {
     const size_t b = (size_t)n * s * esz();
-    cudaMemcpyAsync(Rt, R, b, cudaMemcpyDeviceToDevice, c->st);  // R̃ = R0
+    if (int r = shadow_into(Rt)) return r;  // R̃ (default R0)
     cudaMemcpyAsync(P, R, b, cudaMemcpyDeviceToDevice, c->st);
     e.upd(s, {R, Rt}, {}, {RQ{rmode(), 0, 1, nullptr, off[SL_RHO]}});
     return coef(0);
@@ -646,7 +708,7 @@ struct BlBiCGStab : Solver {  // [ELg03], SURVEY App. A.4
   }
   int init() override {
     const size_t b = (size_t)n * s * esz();
-    cudaMemcpyAsync(Rt, R, b, cudaMemcpyDeviceToDevice, c->st);
+    if (int r = shadow_into(Rt)) return r;
     cudaMemcpyAsync(P, R, b, cudaMemcpyDeviceToDevice, c->st);
     e.upd(s, {R, Rt}, {}, {RQ{RED_FULL, 0, 1, nullptr, off[SL_M]}});  // R̃^H R
     return coef(0);
@@ -691,7 +753,12 @@ struct BlBiCGStabrQ : Solver {
   int init() override {
     const size_t b = (size_t)n * s * esz();
     dev_tsqr(*this, R, Qr, false, Zs);
-    cudaMemcpyAsync(Q0, Qr, b, cudaMemcpyDeviceToDevice, c->st);  // Q̂0 = Qr when R̃ = R0
+    if (o.shadow == 0) {
+      cudaMemcpyAsync(Q0, Qr, b, cudaMemcpyDeviceToDevice, c->st);  // Q̂0 = Qr when R̃ = R0
+    } else {  // Q̂0 = orthonormal factor of R̃ (its R factor cancels, App. A.5)
+      if (int r = shadow_into(Z)) return r;
+      dev_tsqr(*this, Z, Q0, true);
+    }
     cudaMemcpyAsync(V, Qr, b, cudaMemcpyDeviceToDevice, c->st);
     e.upd(s, {Qr, Q0}, {}, {RQ{RED_FULL, 0, 1, nullptr, off[SL_GQ]}});
     return coef(0);
@@ -762,8 +829,7 @@ struct QMR : Solver {  // mode 0 Li, 1 Gl, 2 eGl
   int init() override {
     const size_t b = (size_t)n * s * esz();
     cudaMemcpyAsync(Vt, R, b, cudaMemcpyDeviceToDevice, c->st);
-    if (mode == 2) launch_row_mean(cplx, R, Wt, n, s, nullptr, c->st);  // w̃0 = mean of the columns
-    else cudaMemcpyAsync(Wt, R, b, cudaMemcpyDeviceToDevice, c->st);     // W̃0 = R0
+    if (int r = (mode == 2) ? shadow_vec_into(Wt) : shadow_into(Wt)) return r;  // w̃0 = mean / W̃0 = R0 by default
     e.upd(ws_(), {Wt}, {}, {RQ{nrm(), 0, -1, nullptr, off[SL_XI2]}});
     if (mode == 2) e.upd(s, {Vt}, {}, vt_reds(0, -1));
     else e.upd(s, {Vt, Wt}, {}, vt_reds(0, 1));
@@ -856,8 +922,14 @@ struct BlQMR : Solver {
     const size_t b = (size_t)n * s * esz();
     dev_tsqr(*this, R, V, false);  // V rho = R0
     cudaMemcpyAsync(ws + off[SL_RHOB], ws + off[SL_C], (size_t)s * s * esz(), cudaMemcpyDeviceToDevice, c->st);
-    cudaMemcpyAsync(Wb, V, b, cudaMemcpyDeviceToDevice, c->st);  // W xi = R̂0 = R0
-    cudaMemcpyAsync(ws + off[SL_XIB], ws + off[SL_C], (size_t)s * s * esz(), cudaMemcpyDeviceToDevice, c->st);
+    if (o.shadow == 0) {
+      cudaMemcpyAsync(Wb, V, b, cudaMemcpyDeviceToDevice, c->st);  // W xi = R̂0 = R0
+      cudaMemcpyAsync(ws + off[SL_XIB], ws + off[SL_C], (size_t)s * s * esz(), cudaMemcpyDeviceToDevice, c->st);
+    } else {  // W xi = R̂0 (thin QR)
+      if (int r = shadow_into(Wb)) return r;
+      dev_tsqr(*this, Wb, Wb, true);
+      cudaMemcpyAsync(ws + off[SL_XIB], ws + off[SL_CH], (size_t)s * s * esz(), cudaMemcpyDeviceToDevice, c->st);
+    }
     cudaMemsetAsync(P, 0, b, c->st);
     cudaMemsetAsync(Qb, 0, b, c->st);
     cudaMemsetAsync(D, 0, b, c->st);
@@ -903,9 +975,10 @@ struct BlBiCGsQ : Solver {
   }
   int init() override {
     const size_t b = (size_t)n * s * esz();
-    cudaMemcpyAsync(Rh, R, b, cudaMemcpyDeviceToDevice, c->st);  // R̂0 = R0
-    dev_tsqr(*this, R, P, false);                                 // P = orthonormal basis of R0
-    cudaMemcpyAsync(Ph, P, b, cudaMemcpyDeviceToDevice, c->st);
+    if (int r = shadow_into(Rh)) return r;  // R̂0 (default R0)
+    dev_tsqr(*this, R, P, false);           // P = orthonormal basis of R0
+    if (o.shadow == 0) cudaMemcpyAsync(Ph, P, b, cudaMemcpyDeviceToDevice, c->st);
+    else dev_tsqr(*this, Rh, Ph, true);
     e.upd(s, {R, Ph, Rh, P}, {}, {RQ{RED_FULL, 0, 1, nullptr, off[SL_M]}, RQ{RED_FULL, 2, 3, nullptr, off[SL_MH]}});
     return coef(0);
   }
@@ -941,7 +1014,7 @@ struct BlBiCGStabsQ : Solver {
   }
   int init() override {
     const size_t b = (size_t)n * s * esz();
-    cudaMemcpyAsync(Rt, R, b, cudaMemcpyDeviceToDevice, c->st);
+    if (int r = shadow_into(Rt)) return r;
     dev_tsqr(*this, R, P, false);  // P = orthonormal basis of R0
     e.upd(s, {R, Rt}, {}, {RQ{RED_FULL, 0, 1, nullptr, off[SL_M]}});  // R̃^H R
     return coef(0);

@@ -56,6 +56,8 @@ struct Solver {
   void* blk();                 // allocate an n x s block
   void* vecn();                // allocate an n-vector
   int coef(int phase, int k1 = 0);
+  int shadow_into(void* dst);      // n x s shadow block per o.shadow
+  int shadow_vec_into(void* dst);  // economic shadow vector
   // rank-deficiency continuation of the rQ thin QRs (f4): armed by pass 1, else no-ops
   void defl_repair(void* Z, void* Zs, void* Zh, void* Zhs, bool init);
   void defl_fixup(const void* Q, const void* Zs, const void* Qh, const void* Zhs, bool init);
