@@ -207,6 +207,12 @@ int srk_matrix_create_dist(srk_ctx* ctx, const srk_csr* A_local, int64_t n_ghost
                            const srk_csr* AH_local, int64_t n_ghost_adj, const srk_halo* halo_adj,
                            srk_matrix** out);
 
+/* Storage the SpMM of op(A) uses (a0): 0 CSR (lane-group kernel), 1 CSR in
+ * length-sorted row order (irregular rows), 2 banded (<= 8 diagonals, the bulk-copy kernel
+ * of band.cu; *ndiag = the diagonal count), 3 BSR-12. adjoint = 1: A^H's storage.
+ * Errors: SRK_EINVAL (null matrix, adjoint without A^H). */
+int srk_matrix_format(const srk_matrix* A, int adjoint, int* ndiag);
+
 /* ------------------------------------------------------ kernel-level calls */
 /* Q = op(A) P, op = A (adjoint = 0) or A^H (adjoint = 1, needs need_adjoint),
  * P, Q: n x s row-major (a1/a2). If gram != SRK_GRAM_NONE the

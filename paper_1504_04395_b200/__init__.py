@@ -37,6 +37,7 @@ EXPORTS = ("srk_create", "srk_destroy", "srk_last_error", "srk_version", "srk_ma
            "srk_solver_profile_read", "srk_solver_profile_launches", "srk_partition_rows", "srk_plan_create", "srk_plan_sizes", "srk_plan_arrays",
            "srk_plan_destroy", "srk_nccl_unique_id", "srk_comm_init", "srk_matrix_create_dist",
            "srk_vgroup_create", "srk_vgroup_destroy", "srk_comm_init_virtual", "srk_csr_adjoint_host",
+           "srk_matrix_format",
            "srk_matrix_create_bsr", "srk_matrix_ilu0", "srk_matrix_ilu0_factor", "srk_precond_apply")
 
 
@@ -123,6 +124,7 @@ def load_library(path: str | None = None):
         "srk_nccl_unique_id": ([vp], i),
         "srk_comm_init": ([vp, vp, i, i], i),
         "srk_vgroup_create": ([i, ctypes.POINTER(vp)], i),
+        "srk_matrix_format": ([vp, i, ctypes.POINTER(i)], i),
         "srk_vgroup_destroy": ([vp], i),
         "srk_comm_init_virtual": ([vp, vp, i], i),
         "srk_csr_adjoint_host": ([i64, vp, vp, vp, i, vp, vp, vp], i),
@@ -258,6 +260,15 @@ class Matrix:
         self.h = h
         self.has_adjoint = False
         return self
+
+    FORMATS = ("csr", "csr_sorted", "band", "bsr")
+
+    def format(self, adjoint: bool = False):
+        """(storage, diagonals) the SpMM of A (or A^H) uses (srk_matrix_format)."""
+        nd = ctypes.c_int(0)
+        f = _lib.srk_matrix_format(self.h, int(adjoint), ctypes.byref(nd))
+        _check(min(f, 0), "srk_matrix_format")
+        return self.FORMATS[f], nd.value
 
     def ilu0(self):
         """Attach the right ILU(0) preconditioner (srk_matrix_ilu0); returns self."""

@@ -160,6 +160,15 @@ int srk_matrix_create(srk_ctx* ctx, const srk_csr* A, int need_adjoint, srk_matr
     srk_matrix_destroy(M);
     return fail(SRK_ENOMEM, "srk_matrix_create: balanced row order");
   }
+  // regular operators on <= 8 diagonals (the stencils): the banded form of a0 (band.cu)
+  static const bool no_band = getenv("SRK_NO_BAND") != nullptr;  // A/B switch for measurements
+  if (!no_band && !m.srt.perm) {
+    if (build_band(m.cplx, m.n, m.rp, m.ci, m.val, m.band, st) ||
+        (m.has_adj && build_band(m.cplx, m.n, m.rpH, m.ciH, m.valH, m.bandH, st))) {
+      srk_matrix_destroy(M);
+      return fail(SRK_ENOMEM, "srk_matrix_create: banded form");
+    }
+  }
   *out = M;
   return SRK_OK;
 }
@@ -382,6 +391,17 @@ int srk_matrix_create_dist(srk_ctx* ctx, const srk_csr* A, int64_t n_ghost, cons
   return SRK_OK;
 }
 
+int srk_matrix_format(const srk_matrix* M, int adjoint, int* ndiag) {
+  if (!M || (adjoint && !M->m.has_adj)) return fail(SRK_EINVAL, "srk_matrix_format: bad argument");
+  const Mat& m = M->m;
+  const Mat::Band& b = adjoint ? m.bandH : m.band;
+  if (ndiag) *ndiag = b.K;
+  if (m.bsr) return 3;
+  if (b.K > 0) return 2;
+  if ((adjoint ? m.srtH.perm : m.srt.perm) != nullptr) return 1;
+  return 0;
+}
+
 int srk_matrix_destroy(srk_matrix* M) {
   if (!M) return SRK_OK;
   Mat& m = M->m;
@@ -407,6 +427,8 @@ int srk_matrix_destroy(srk_matrix* M) {
   if (m.bci) cudaFree(m.bci);
   if (m.bval) cudaFree(m.bval);
   free_balanced_order(m);
+  if (m.band.val) cudaFree(m.band.val);
+  if (m.bandH.val) cudaFree(m.bandH.val);
   delete M;
   return SRK_OK;
 }

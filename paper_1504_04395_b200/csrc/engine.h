@@ -100,6 +100,14 @@ struct Mat {
     void* val = nullptr;
     int* perm = nullptr;
   } srt, srtH;
+  // Banded form (band.cu): K <= 8 diagonals d_k (ascending), K arrays of npad values
+  // (zero where a row has no entry on the diagonal); K = 0 when A is not banded
+  struct Band {
+    int K = 0;
+    int off[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    long long npad = 0;
+    void* val = nullptr;
+  } band, bandH;
   // multi-GPU (row-partitioned) operator: local rows, columns [0, n) owned and
   // [n, n + n_ghost) ghost rows received from the owning ranks before each SpMM
   bool dist = false;
@@ -108,6 +116,12 @@ struct Mat {
   size_t sendcap = 0;         // doubles
   long long ghost_rows() const { return dist ? std::max(halo.n_ghost, haloH.n_ghost) : 0; }
 };
+
+// banded operators (band.cu): detection + diagonal storage at a0, the bulk-copy SpMM
+int build_band(bool cplx, long long n, const int* rp, const int* ci, const void* val, Mat::Band& b, cudaStream_t st);
+bool band_supported(bool cplx, int s);
+int launch_band(bool cplx, int s, const Mat::Band& b, const void* P, void* Q, long long n, const Red* red, int nred,
+                double* partials, int pstride, const int* done, int nsm, cudaStream_t st, int* grid_out);
 
 // builds m.srt / m.srtH when the row lengths are irregular (engine.cu)
 int build_balanced_order(Mat& m, bool adj, cudaStream_t st);
