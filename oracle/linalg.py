@@ -162,6 +162,8 @@ def thin_qr(Z: np.ndarray, ctr: Counter | None = None, order: str = "blas", fill
     and the later columns are orthogonalised against it as usual, so Z = Q C still
     holds with Q orthonormal (reading R8)."""
     n, s = Z.shape
+    if order == "cholqr":
+        return _cholqr2(Z, ctr)
     Q = np.array(Z, dtype=np.result_type(Z.dtype, np.float64), copy=True)
     C = np.zeros((s, s), dtype=Q.dtype)
     zn = np.sqrt(fro2(Z))
@@ -189,6 +191,33 @@ def thin_qr(Z: np.ndarray, ctr: Counter | None = None, order: str = "blas", fill
         Q[:, j] /= d
     if ctr is not None:
         ctr.vector_ops += 3 * s * s  # "at least a cost of 3ns^2", counted as vector ops
+    return Q, C
+
+
+def _cholqr2(Z: np.ndarray, ctr: Counter | None = None):
+    """The second thin-QR algorithm of reading G10 ("e.g. MGS", P:603 leaves it open):
+    Cholesky QR applied twice, G = Z^H Z = R1^H R1, Z1 = Z R1^{-1}, Z1^H Z1 = R2^H R2,
+    Q = Z1 R2^{-1}, C = R2 R1 (real positive diagonal). Used only as the oracle's
+    alternative order (order="cholqr") to measure the method's rounding spread under the
+    QR algorithm; a pivot <= 1e-14 tr(G) is rank deficiency (reading R5)."""
+    s = Z.shape[1]
+    Q = np.array(Z, dtype=np.result_type(Z.dtype, np.float64), copy=True)
+    C = np.eye(s, dtype=Q.dtype)
+    for _pass in range(2):
+        G = H(Q) @ Q
+        tr = float(np.trace(G).real)
+        try:
+            L = np.linalg.cholesky(G)
+        except np.linalg.LinAlgError:
+            raise Breakdown("rank")
+        if tr <= 0 or np.min(np.abs(np.diag(L))) ** 2 <= 1e-14 * tr:
+            raise Breakdown("rank")
+        R = H(L)
+        Q = sla.solve_triangular(R, Q.T, trans="T", lower=False).T if not np.iscomplexobj(Q) else \
+            H(sla.solve_triangular(R, H(Q), trans="C", lower=False))
+        C = R @ C
+    if ctr is not None:
+        ctr.vector_ops += 3 * s * s
     return Q, C
 
 

@@ -4,9 +4,10 @@ input hash). tests/golden/oracle_counts.json is written by scripts/oracle_counts
 which calls only oracle/ and synth/ (hours of numpy per entry); this test solves the
 same seeded configuration on the GPU and compares the outcome, the iteration count and
 the final true residual (recomputed on the host from the GPU's X). The count rule is
-SURVEY §8c.5 rule 3: within max(2%, |it_O - it_O'| + 2), where it_O' is the ORACLE's
-count under its second reduction order (`order="seq"`, cached as "cfgN:method:seq");
-without that entry the north star's plain max(2, 2%) applies."""
+SURVEY §8c.5 rule 3: within max(2%, |it_O - it_O'| + 2), where it_O' ranges over the
+ORACLE's counts under its other orders (`order="seq"` reductions, `order="cholqr"` thin
+QR — reading G10 leaves the QR algorithm open), cached as "cfgN:method:<order>"; without
+such entries the north star's plain max(2, 2%) applies."""
 import json
 import os
 
@@ -51,13 +52,14 @@ def test_full_size_counts(entry):
     X, rep = srk.solve(M, to_dev(B), method, tol=e["tol"], maxit=e["maxit"])
     assert rep.outcome == e["outcome"], (rep, e)
     it = e["iterations"]
-    alt = _all().get(key + ":seq")
-    if alt is not None:
+    # the oracle's other orders of the same input: reduction order "seq" and the alternative
+    # thin QR "cholqr" (reading G10) — SURVEY §8c.5 rule 3 with their largest deviation
+    alts = [v for k, v in _all().items() if k.startswith(key + ":")]
+    for alt in alts:
         assert alt["inputs_hash"] == e["inputs_hash"] and alt["outcome"] == e["outcome"], alt
-        slack = max(0.02 * it, abs(it - alt["iterations"]) + 2)
-    else:
-        slack = max(2, 0.02 * it)
-    assert abs(rep.iterations - it) <= slack, (rep.iterations, it, alt and alt["iterations"])
+    spread = max([abs(it - alt["iterations"]) for alt in alts], default=None)
+    slack = max(0.02 * it, spread + 2) if spread is not None else max(2, 0.02 * it)
+    assert abs(rep.iterations - it) <= slack, (rep.iterations, it, [alt["iterations"] for alt in alts])
     if rep.outcome == "converged":
         Xh = to_np(X)
         true = np.linalg.norm(B - A.to_scipy() @ Xh) / np.linalg.norm(B)

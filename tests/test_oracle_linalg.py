@@ -91,3 +91,20 @@ def test_unitary_qr_stack(rng):
     full = np.vstack([R, np.zeros((4, 4))])
     assert np.linalg.norm(Om @ full - M) < 1e-13
     assert np.all(np.diag(R).real > 0) and np.allclose(np.diag(R).imag, 0)
+
+
+def test_cholqr2_alternative_equals_mgs2():
+    """The oracle's alternative thin QR (CholQR2, order="cholqr", used only to measure the
+    method's spread under the QR algorithm — reading G10) returns the same unique thin QR
+    with real positive diagonal as MGS2, and detects rank deficiency."""
+    import synth
+    from oracle.linalg import Breakdown, thin_qr
+    for cplx in (False, True):
+        Z = synth.random_rhs(300, 6, 4, cplx)
+        Q1, C1 = thin_qr(Z)
+        Q2, C2 = thin_qr(Z, order="cholqr")
+        assert np.linalg.norm(Q1 - Q2) < 1e-12 and np.linalg.norm(C1 - C2) < 1e-12 * np.linalg.norm(C1)
+        assert np.all(np.diag(C2).real > 0) and np.allclose(np.diag(C2).imag, 0)
+        Z[:, 5] = Z[:, 0] + Z[:, 1]
+        with pytest.raises(Breakdown):
+            thin_qr(Z, order="cholqr")
