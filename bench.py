@@ -43,6 +43,7 @@ sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
 
 METRIC = "RHS·iterations/sec"
+P64_TFLOPS = 37.1  # FP64 tensor-core (DMMA) peak measured by scripts/fp64_probe.cu on this B200 model
 UNIT = "RHS·it/s"
 
 
@@ -184,6 +185,7 @@ def main():
         args.method = {1: "egl_bicg", 2: "bl_bicg_rq", 3: "egl_qmr", 4: "gl_bicgstab", 5: "egl_bicg"}[args.config]
     c = synth.CONFIGS[args.config]
     bsr = None
+    bsr_nnzb = 0
     if args.config == 4:
         # a0: the lattice operator in BSR-12 form with the unit diagonal implied
         # (the scalar CSR of 32^4 would be 24.4 GB and gather 18.6 KB per row)
@@ -195,6 +197,7 @@ def main():
         class A:  # the scalar view (for the config record)
             pass
         A.n, A.nnz = n, len(bsr[1]) * 144 + n
+        bsr_nnzb = len(bsr[1])
         import hashlib
         h = hashlib.sha256()
         for arr in (*bsr, B):
@@ -234,15 +237,27 @@ def main():
         dist.init_process_group("nccl")
     dev = torch.device("cuda", torch.cuda.current_device())
     srk.load_library()
-    if world > 1:
+    if world > 1 and bsr is not None:
+        # config 4: the lattice's block rows split into t-slabs (contiguous lexicographic
+        # site ranges, nnz-balanced); each product exchanges the 12 rows of every ghost block
+        srk.init_distributed()
+        boff = srk.partition_rows(bsr[0], world)
+        M = srk.DistMatrix.from_bsr(*bsr, boff, rank, unit_diag=True)
+        o0, o1 = int(boff[rank]) * 12, int(boff[rank + 1]) * 12
+        B = np.ascontiguousarray(B[o0:o1])
+        del bsr
+        bsr = True
+        cfgd["parallelism"] = f"t-slabs x{world} (BSR-12 block halo + NCCL allreduce)"
+    elif world > 1:
         # a8: A and every n x s block row-partitioned (nnz-balanced contiguous ranges);
-        # halo exchange before each SpMM and an NCCL allreduce of every reduction
+        # halo exchange before each SpMM (overlapped with the interior rows' product) and an
+        # NCCL allreduce of every reduction
         srk.init_distributed()
         off = srk.partition_rows(A.row_ptr, world)
         M = srk.DistMatrix(A, off, rank, need_adjoint=srk.NEEDS_ADJOINT[args.method])
         o0, o1 = int(off[rank]), int(off[rank + 1])
         B = np.ascontiguousarray(B[o0:o1])
-        cfgd["parallelism"] = f"row-partition x{world} (halo exchange + NCCL allreduce)"
+        cfgd["parallelism"] = f"row-partition x{world} (halo exchange overlapped with the interior rows + NCCL allreduce)"
     elif bsr is not None:
         M = srk.Matrix.from_bsr(*bsr, unit_diag=True)
         del bsr
@@ -265,7 +280,8 @@ def main():
     latency = args.config == 1
     poll = W if latency else W + K + 1
     warm = 2 * W if latency else W
-    sv = srk.Solver(M, s, args.method, tol=1e-300, maxit=warm + K + 1, poll_every=poll,
+    REPEATS = 5  # the median of 5 timed windows is reported beside the first
+    sv = srk.Solver(M, s, args.method, tol=1e-300, maxit=warm + REPEATS * K + 1, poll_every=poll,
                     check_true_residual=False)
     sv.start(Bd)
     sv.iterate(W)
@@ -293,11 +309,27 @@ def main():
     rep = sv.report()
     launches = rep.kernel_launches - l0
     assert st == 0 and rep.iterations == warm + K, (st, rep)
+    # four more windows of exactly K steps (same solver, no profiling), for the median of 5
+    windows = [ms]
+    for _ in range(REPEATS - 1):
+        barrier()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record()
+        sv.iterate(K)
+        f1.record()
+        torch.cuda.synchronize()
+        windows.append(f0.elapsed_time(f1))
     if world > 1:
-        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        t = torch.tensor(windows, device=dev, dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms = float(t.item())
+        windows = [float(x) for x in t.tolist()]
+        ms = windows[0]
     value = s * K / (ms / 1e3)  # the whole job iterates the same s right-hand sides
+    med = statistics.median(windows)
+    median5 = {"value": s * K / (med / 1e3), "ms_per_step": med / K,
+               "windows_ms_per_step": [w / K for w in windows],
+               "note": "median of 5 timed windows of K steps (SURVEY §8(d).4); the first window is `value`, "
+                       "timed with per-launch events (the profile of `roofline`), the other four without"}
 
     # ---- rooflines, timed live: every launch of the timed region carries its
     # algorithmic bytes (computed by the engine); launches are
@@ -341,6 +373,20 @@ def main():
                 "algorithmic_bytes_per_launch": dom["algorithmic_bytes_per_launch"],
                 "avg_launch_ms": dom["avg_launch_ms"], "launches": dom["launches"],
                 "share_of_step": dom["share_of_step"], "peak_source": peak_src}
+    if bsr_nnzb and spm:
+        # config 4's BSR-12 product sits near the FP64 ridge: its bound is
+        # max(bytes / BW, flops / P64); useful flops = 8 real flops per complex multiply-add,
+        # 144 entries per block, s columns (the implied identity is not counted)
+        fl = bsr_nnzb * 144 * 8 * s
+        t_mem = spm["algorithmic_bytes_per_launch"] / (peak * 1e9)
+        t_fl = fl / (P64_TFLOPS * 1e12)
+        t_act = spm["avg_launch_ms"] / 1e3
+        spm["flops_per_launch"] = fl
+        spm["achieved_tflops"] = fl / t_act / 1e12
+        spm["bound"] = "fp64" if t_fl > t_mem else "hbm"
+        spm["frac_of_bound"] = max(t_mem, t_fl) / t_act
+        spm["p64_tflops"] = P64_TFLOPS
+        spm["p64_source"] = "measured DMMA peak of this B200 model (scripts/fp64_probe.cu, DESIGN.md §7)"
     it_bytes = sum(nb for _, _, _, nb in recs) / K
     breakdown = {}
     for tag, _, t_ms, _ in recs:
@@ -372,6 +418,23 @@ def main():
                "note": "srk_solve_host (after one untimed call that sizes the cached workspace), X0 = 0 (P:639): "
                        "H2D of B, R0 = B, K iterations, the final true residual, D2H of X"}
 
+    # ---- end to end, full solve: B on the host to the converged X on the host (tol 1e-8)
+    e2e_full = None
+    if not args.no_e2e and world == 1 and not latency:
+        Bh = torch.from_numpy(B).pin_memory()
+        Xh = torch.zeros_like(Bh).pin_memory()
+        srk.solve_host(M, Bh.numpy(), args.method, tol=1e-8, maxit=2000, X0=Xh.numpy(), inplace=True, x0_zero=True)
+        barrier()
+        t0 = time.perf_counter()
+        X, r3 = srk.solve_host(M, Bh.numpy(), args.method, tol=1e-8, maxit=2000, X0=Xh.numpy(), inplace=True,
+                               x0_zero=True)
+        T = time.perf_counter() - t0
+        e2e_full = {"value": s * r3.iterations / T, "unit": UNIT, "seconds": T, "iterations": r3.iterations,
+                    "outcome": r3.outcome, "final_true_rel_residual": r3.final_true_rel_residual,
+                    "h2d_bytes": B.nbytes, "d2h_bytes": B.nbytes,
+                    "note": "srk_solve_host to convergence (tol 1e-8, maxit 2000, X0 = 0), host buffers, "
+                            "after one untimed identical call (workspace sizing)"}
+
     # ---- CPU baseline: the oracle on one config-3 iteration (rank 0, N = 1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -394,7 +457,8 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
             "ms_per_step": ms / K, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64" if esz == 8 else "c128", "data": "synthetic", "config": cfgd,
-            "roofline": roof, "roofline_spmm": spm, "cpu_baseline": cpu, "e2e": e2e,
+            "roofline": roof, "roofline_spmm": spm, "cpu_baseline": cpu, "e2e": e2e, "e2e_full_solve": e2e_full,
+            "median_of_5": median5,
             "gpu_launches": int(launches), "clocks": clocks,
             "iteration": {"algorithmic_bytes": it_bytes or None,
                           "achieved_gbs": (it_bytes / (ms / K / 1e3) / 1e9) if it_bytes else None,

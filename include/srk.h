@@ -213,6 +213,17 @@ int srk_matrix_create_dist(srk_ctx* ctx, const srk_csr* A_local, int64_t n_ghost
  * Errors: SRK_EINVAL (null matrix, adjoint without A^H). */
 int srk_matrix_format(const srk_matrix* A, int adjoint, int* ndiag);
 
+/* Distributed BSR-12 operator (config 4's lattice split into t-slabs): this
+ * rank's nb_local block rows (DEVICE arrays, block columns renumbered as srk_plan_create does
+ * for a block-row CSR: [0, nb_local) owned, nb_local + position in the sorted ghost list
+ * for ghost block rows), and the halo in BLOCK units (host arrays). Every n x s block passed
+ * to this operator holds (nb_local + nb_ghost) * 12 rows; the solver allocates its blocks
+ * that way and each product first exchanges the 12 rows of every ghost block.
+ * Errors: as srk_matrix_create_bsr; SRK_EINVAL for an inconsistent halo. */
+int srk_matrix_create_bsr_dist(srk_ctx* ctx, int64_t nb_local, int bs, int64_t nnzb, const int64_t* block_row_ptr,
+                               const int32_t* block_col, const void* values, int dtype, int unit_diag,
+                               int64_t nb_ghost, const srk_halo* halo_blocks, srk_matrix** out);
+
 /* ------------------------------------------------------ kernel-level calls */
 /* Q = op(A) P, op = A (adjoint = 0) or A^H (adjoint = 1, needs need_adjoint),
  * P, Q: n x s row-major (a1/a2). If gram != SRK_GRAM_NONE the

@@ -37,7 +37,7 @@ EXPORTS = ("srk_create", "srk_destroy", "srk_last_error", "srk_version", "srk_ma
            "srk_solver_profile_read", "srk_solver_profile_launches", "srk_partition_rows", "srk_plan_create", "srk_plan_sizes", "srk_plan_arrays",
            "srk_plan_destroy", "srk_nccl_unique_id", "srk_comm_init", "srk_matrix_create_dist",
            "srk_vgroup_create", "srk_vgroup_destroy", "srk_comm_init_virtual", "srk_csr_adjoint_host",
-           "srk_matrix_format",
+           "srk_matrix_format", "srk_matrix_create_bsr_dist",
            "srk_matrix_create_bsr", "srk_matrix_ilu0", "srk_matrix_ilu0_factor", "srk_precond_apply")
 
 
@@ -125,6 +125,8 @@ def load_library(path: str | None = None):
         "srk_comm_init": ([vp, vp, i, i], i),
         "srk_vgroup_create": ([i, ctypes.POINTER(vp)], i),
         "srk_matrix_format": ([vp, i, ctypes.POINTER(i)], i),
+        "srk_matrix_create_bsr_dist": ([vp, i64, i, i64, vp, vp, vp, i, i, i64, ctypes.POINTER(_Halo),
+                                        ctypes.POINTER(vp)], i),
         "srk_vgroup_destroy": ([vp], i),
         "srk_comm_init_virtual": ([vp, vp, i], i),
         "srk_csr_adjoint_host": ([i64, vp, vp, vp, i, vp, vp, vp], i),
@@ -477,6 +479,43 @@ class DistMatrix:
         self.h = h
         self.n = self.n_local
         self.has_adjoint = need_adjoint
+
+    @classmethod
+    def from_bsr(cls, block_row_ptr, block_col, blocks, offsets_blocks, rank: int, unit_diag: bool = True,
+                 ctx: "Context | None" = None):
+        """srk_matrix_create_bsr_dist: this rank's block rows of a BSR-12 operator (config 4's
+        lattice as t-slabs when the offsets split the lexicographic site order), planned on the
+        block-row CSR pattern by the library's planner; the halo moves 12 rows per ghost block."""
+        torch = _torch()
+        self = cls.__new__(cls)
+        self.ctx = ctx or default_context()
+        dev = torch.device("cuda", self.ctx.device)
+        brp = np.ascontiguousarray(block_row_ptr, np.int64)
+        bci = np.ascontiguousarray(block_col, np.int32)
+        self.offsets = np.asarray(offsets_blocks, np.int64)
+        self.rank = rank
+        self.plan = make_plan(brp, bci, self.offsets, rank)
+        nb_local, bs = self.plan.n_local, 12
+        lo, hi = int(brp[self.plan.off0]), int(brp[self.plan.off1])
+        t_rp = torch.from_numpy(self.plan.row_ptr).to(dev)
+        t_ci = torch.from_numpy(self.plan.col).to(dev)
+        t_bv = torch.from_numpy(np.ascontiguousarray(blocks[lo:hi])).to(dev)
+        keep = [self.plan.recv_counts, self.plan.send_counts, self.plan.send_local]
+        halo = _Halo(self.plan.recv_counts.ctypes.data, self.plan.send_counts.ctypes.data,
+                     self.plan.send_local.ctypes.data if self.plan.send_local.size else None, self.plan.send_local.size)
+        h = ctypes.c_void_p()
+        _check(_lib.srk_matrix_create_bsr_dist(self.ctx.h, nb_local, bs, hi - lo, ctypes.c_void_p(t_rp.data_ptr()),
+                                               ctypes.c_void_p(t_ci.data_ptr()), ctypes.c_void_p(t_bv.data_ptr()),
+                                               SRK_C128, int(unit_diag), self.plan.ghosts.size, ctypes.byref(halo),
+                                               ctypes.byref(h)), "srk_matrix_create_bsr_dist")
+        torch.cuda.synchronize()
+        del keep
+        self.h = h
+        self.n_local = nb_local * bs
+        self.n = self.n_local
+        self.n_ghost = self.plan.ghosts.size * bs
+        self.has_adjoint = False
+        return self
 
     def close(self):
         if getattr(self, "h", None):

@@ -77,6 +77,9 @@ int srk_destroy(srk_ctx* ctx) {
   for (void* p : ctx->hbuf)
     if (p) cudaFree(p);
   if (ctx->c.partials) cudaFree(ctx->c.partials);
+  if (ctx->c.side) cudaStreamDestroy(ctx->c.side);
+  if (ctx->c.ev_p) cudaEventDestroy(ctx->c.ev_p);
+  if (ctx->c.ev_h) cudaEventDestroy(ctx->c.ev_h);
   if (ctx->c.comm) comm_destroy(ctx->c.comm);
   delete ctx;
   return SRK_OK;
@@ -173,9 +176,31 @@ int srk_matrix_create(srk_ctx* ctx, const srk_csr* A, int need_adjoint, srk_matr
   return SRK_OK;
 }
 
+static int create_bsr(srk_ctx* ctx, int64_t nb, int bs, int64_t nnzb, const int64_t* block_row_ptr,
+                      const int32_t* block_col, const void* values, int dtype, int unit_diag, int64_t nb_ghost,
+                      const srk_halo* halo_blocks, srk_matrix** out);
+static int upload_halo(Halo& H, const srk_halo* h, int nranks, long long n_ghost);
+
 int srk_matrix_create_bsr(srk_ctx* ctx, int64_t nb, int bs, int64_t nnzb, const int64_t* block_row_ptr,
                           const int32_t* block_col, const void* values, int dtype, int unit_diag,
                           srk_matrix** out) {
+  return create_bsr(ctx, nb, bs, nnzb, block_row_ptr, block_col, values, dtype, unit_diag, 0, nullptr, out);
+}
+
+int srk_matrix_create_bsr_dist(srk_ctx* ctx, int64_t nb_local, int bs, int64_t nnzb, const int64_t* block_row_ptr,
+                               const int32_t* block_col, const void* values, int dtype, int unit_diag,
+                               int64_t nb_ghost, const srk_halo* halo_blocks, srk_matrix** out) {
+  if (nb_ghost < 0) return fail(SRK_EINVAL, "srk_matrix_create_bsr_dist: nb_ghost < 0");
+  const int nranks = ctx && ctx->c.comm ? ctx->c.comm->nranks : 1;
+  if ((nb_ghost > 0 || (halo_blocks && halo_blocks->n_send > 0)) && nranks == 1)
+    return fail(SRK_EINVAL, "srk_matrix_create_bsr_dist: halo given but no communicator");
+  return create_bsr(ctx, nb_local, bs, nnzb, block_row_ptr, block_col, values, dtype, unit_diag, nb_ghost, halo_blocks,
+                    out);
+}
+
+static int create_bsr(srk_ctx* ctx, int64_t nb, int bs, int64_t nnzb, const int64_t* block_row_ptr,
+                      const int32_t* block_col, const void* values, int dtype, int unit_diag, int64_t nb_ghost,
+                      const srk_halo* halo_blocks, srk_matrix** out) {
   if (!ctx || !out || !block_row_ptr || nb < 1 || nnzb < 0 || (nnzb > 0 && (!block_col || !values)))
     return fail(SRK_EINVAL, "srk_matrix_create_bsr: bad argument");
   if (bs != 12 || dtype != SRK_C128)
@@ -208,7 +233,9 @@ int srk_matrix_create_bsr(srk_ctx* ctx, int64_t nb, int bs, int64_t nnzb, const 
     cudaMemcpyAsync(m.bci, block_col, sizeof(int) * nnzb, cudaMemcpyDeviceToDevice, st);
     cudaMemcpyAsync(m.bval, values, bbytes * nnzb, cudaMemcpyDeviceToDevice, st);
   }
-  launch_csr_check(nb, nb, nnzb, m.brp, m.bci, 1, dbad, st);
+  // distributed (t-slab) operators: block columns >= nb are ghost block rows; the entries keep
+  // the global block order, so a row's local columns need not ascend (sorted check off)
+  launch_csr_check(nb, nb + nb_ghost, nnzb, m.brp, m.bci, nb_ghost > 0 ? 0 : 1, dbad, st);
   int bad = 0;
   cudaMemcpyAsync(&bad, dbad, sizeof(int), cudaMemcpyDeviceToHost, st);
   cudaError_t e = cudaStreamSynchronize(st);
@@ -220,6 +247,24 @@ int srk_matrix_create_bsr(srk_ctx* ctx, int64_t nb, int bs, int64_t nnzb, const 
   if (bad) {
     srk_matrix_destroy(M);
     return fail(SRK_EINVAL, "srk_matrix_create_bsr: invalid block structure (row pointers / sorted block columns)");
+  }
+  if (nb_ghost > 0 || (halo_blocks && halo_blocks->n_send > 0)) {
+    // the block halo as a halo of P rows: block b -> rows 12 b .. 12 b + 11
+    const int nranks = ctx->c.comm->nranks;
+    std::vector<int32_t> rc(nranks), sc(nranks), sl;
+    for (int p = 0; p < nranks; ++p) {
+      rc[p] = halo_blocks ? halo_blocks->recv_counts[p] * bs : 0;
+      sc[p] = halo_blocks ? halo_blocks->send_counts[p] * bs : 0;
+    }
+    for (int64_t q = 0; halo_blocks && q < halo_blocks->n_send; ++q)
+      for (int r = 0; r < bs; ++r) sl.push_back(halo_blocks->send_local[q] * bs + r);
+    srk_halo hr{rc.data(), sc.data(), sl.empty() ? nullptr : sl.data(), (int64_t)sl.size()};
+    m.dist = true;
+    const int r = upload_halo(m.halo, &hr, nranks, nb_ghost * bs);
+    if (r) {
+      srk_matrix_destroy(M);
+      return fail(r, "srk_matrix_create_bsr_dist: inconsistent block halo");
+    }
   }
   *out = M;
   return SRK_OK;
@@ -386,6 +431,10 @@ int srk_matrix_create_dist(srk_ctx* ctx, const srk_csr* A, int64_t n_ghost, cons
   if (build_balanced_order(m, false, ctx->c.st) || (m.has_adj && build_balanced_order(m, true, ctx->c.st))) {
     srk_matrix_destroy(M);
     return fail(SRK_ENOMEM, "srk_matrix_create_dist: balanced row order");
+  }
+  if (build_halo_split(m, false, ctx->c.st) || (m.has_adj && build_halo_split(m, true, ctx->c.st))) {
+    srk_matrix_destroy(M);
+    return fail(SRK_ENOMEM, "srk_matrix_create_dist: interior / boundary rows");
   }
   *out = M;
   return SRK_OK;

@@ -147,7 +147,8 @@ static int finish_reds(Eng& e, const std::vector<RQ>& reds, const std::vector<in
 
 // Halo exchange of the ghost rows of P (multi-GPU operators): pack the rows the
 // peers need, then grouped ncclSend/ncclRecv straight into P's ghost tail.
-int Eng::halo(bool adj, const void* P, int s) {
+int Eng::halo(bool adj, const void* P, int s, cudaStream_t hs) {
+  if (!hs) hs = c->st;
   Mat* M = const_cast<Mat*>(A);
   const Halo& H = adj ? M->haloH : M->halo;
   if (!M->dist || !c->comm || c->comm->nranks == 1) return 0;
@@ -158,11 +159,11 @@ int Eng::halo(bool adj, const void* P, int s) {
     if (cudaMalloc(&M->sendbuf, need * sizeof(double)) != cudaSuccess) return (int)cudaErrorMemoryAllocation;
     M->sendcap = need;
   }
-  if (prof) prof->begin(PT_OTHER, c->st);
-  int r = launch_gather_rows(reinterpret_cast<const double*>(P), M->sendbuf, H.send_idx, H.n_send, dpr, nullptr, c->st);
+  if (prof && hs == c->st) prof->begin(PT_OTHER, c->st);
+  int r = launch_gather_rows(reinterpret_cast<const double*>(P), M->sendbuf, H.send_idx, H.n_send, dpr, nullptr, hs);
   if (!r) r = comm_halo(c->comm, M->sendbuf, H.send_off, const_cast<double*>(reinterpret_cast<const double*>(P)) + (size_t)n * dpr,
-                        H.recv_off, dpr, c->st);
-  if (prof) prof->end(c->st);
+                        H.recv_off, dpr, hs);
+  if (prof && hs == c->st) prof->end(c->st);
   return r;
 }
 
@@ -170,6 +171,17 @@ int Eng::spmm(bool adj, const void* P, void* Q, int s, std::vector<RQ> reds) {
   if (err) return err;
   if (A->prec && !raw) return spmm_prec(adj, P, Q, s, reds);
   if (A->bsr) return spmm_bsr(adj, P, Q, s, reds);
+  // distributed operator with a halo: interior rows while the halo is in flight
+  {
+    const Mat::Sorted& in = adj ? A->innerH : A->inner;
+    const Mat::Sorted& bd = adj ? A->bndH : A->bnd;
+    const long long ni = adj ? A->n_innerH : A->n_inner, nbd = adj ? A->n_bndH : A->n_bnd;
+    static const bool no_overlap = getenv("SRK_NO_HALO_OVERLAP") != nullptr;  // A/B switch
+    bool full_any = false;
+    for (auto& r : reds) full_any |= (r.mode == RED_FULL);
+    if (!no_overlap && A->dist && c->comm && c->comm->nranks > 1 && in.perm && bd.perm && !full_any)
+      return err = spmm_split(adj, P, Q, s, reds, in, ni, bd, nbd);
+  }
   if ((err = halo(adj, P, s))) return err;
   const int cap = cap_for(s);
   // s x s Grams of 8 columns and more: Y^H Q on the tensor cores afterwards (the FMA
@@ -473,6 +485,8 @@ int Eng::upd(int s, std::vector<const void*> in, std::vector<OutSpec> outs, std:
 // one fused update pass (X = Q; Y the external operand, as in the CSR epilogue).
 int Eng::spmm_bsr(bool adj, const void* P, void* Q, int s, const std::vector<RQ>& reds) {
   if (adj || !bsr_supported(A->bs, cplx, s)) return err = (int)cudaErrorNotSupported;
+  // distributed lattice (t-slabs): the ghost block rows (12 P rows each) arrive first
+  if ((err = halo(false, P, s))) return err;
   BsrArgs a{};
   a.brp = A->brp;
   a.bci = A->bci;
@@ -674,6 +688,13 @@ int build_balanced_order(Mat& m, bool adj, cudaStream_t st) {
 }
 
 void free_balanced_order(Mat& m) {
+  for (Mat::Sorted* so : {&m.inner, &m.bnd, &m.innerH, &m.bndH}) {
+    if (so->rp) cudaFree(so->rp);
+    if (so->ci) cudaFree(so->ci);
+    if (so->val) cudaFree(so->val);
+    if (so->perm) cudaFree(so->perm);
+    *so = Mat::Sorted{};
+  }
   for (Mat::Sorted* so : {&m.srt, &m.srtH}) {
     if (so->rp) cudaFree(so->rp);
     if (so->ci) cudaFree(so->ci);
@@ -844,6 +865,133 @@ int launch_csr_transpose(bool cplx, long long n, long long nnz, const int* rp, c
     rowsort_kernel<double><<<gridn, 256, 0, st>>>(n, rpT, ciT, (double*)valT);
   }
   return (int)cudaGetLastError();
+}
+
+
+// Interior / boundary SpMM of a distributed operator: the halo (pack + exchange) runs on the
+// context's side stream while the interior rows (no ghost column) are multiplied on the main
+// stream; the boundary rows follow once the ghost rows have arrived. The two launches write
+// consecutive blocks of CTA partials, reduced together in fixed order by fin_kernel.
+int Eng::spmm_split(bool adj, const void* P, void* Q, int s, const std::vector<RQ>& reds, const Mat::Sorted& in,
+                    long long ni, const Mat::Sorted& bd, long long nbd) {
+  if (!c->side) {
+    if (cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_p, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_h, cudaEventDisableTiming) != cudaSuccess)
+      return (int)cudaErrorUnknown;
+  }
+  const int cap = cap_for(s);
+  SpmmArgs a{};
+  a.P = P;
+  a.Q = Q;
+  a.s = s;
+  a.vec = cplx ? 1 : (s % 2 == 0);
+  a.nred = (int)reds.size();
+  std::vector<int> poffs;
+  int pstride = 0, maxlen = 0;
+  for (size_t i = 0; i < reds.size(); ++i) {
+    fill_red(a.red[i], reds[i], pstride);
+    poffs.push_back(pstride);
+    const int len = red_len(reds[i].mode, s, cplx);
+    pstride += len;
+    maxlen = std::max(maxlen, len);
+  }
+  a.pstride = std::max(pstride, 1);
+  const size_t smem = (size_t)8 * maxlen * sizeof(double);
+  a.done = done;
+  a.team = 0;
+  // grids sized to each part's rows (both in the persistent-grid budget of one launch)
+  auto part_grid = [&](long long rows) {
+    const int g = grid_for(cap, false, true, 8 * 2 * 8 * 16 * 16, 0);
+    const long long need = std::max(1LL, (rows + 255) / 256);
+    return (int)std::min<long long>(g, need);
+  };
+  const int g1 = ni > 0 ? part_grid(ni) : 0, g2 = nbd > 0 ? part_grid(nbd) : 0;
+  if ((err = c->ensure_partials((size_t)(g1 + g2) * a.pstride))) return err;
+  cudaEventRecord(c->ev_p, c->st);
+  cudaStreamWaitEvent(c->side, c->ev_p, 0);
+  if ((err = halo(adj, P, s, c->side))) return err;
+  cudaEventRecord(c->ev_h, c->side);
+  const double esz = cplx ? 16.0 : 8.0;
+  const double nz = (double)(adj ? A->nnzH : A->nnz);
+  if (g1 > 0) {
+    a.row_ptr = in.rp;
+    a.col_idx = in.ci;
+    a.val = in.val;
+    a.perm = in.perm;
+    a.n = ni;
+    a.partials = c->partials;
+    nlaunch++;
+    if (prof) prof->begin(adj ? PT_SPMM_ADJ : PT_SPMM, c->st, s, ((double)ni / n) * ((n + 1) * 4.0 + nz * (4 + esz) + 2.0 * n * s * esz));
+    err = launch_spmm(cplx, cap, false, a, g1, 256, smem, c->st);
+    if (prof) prof->end(c->st);
+    if (err) return err;
+  }
+  cudaStreamWaitEvent(c->st, c->ev_h, 0);
+  if (g2 > 0) {
+    a.row_ptr = bd.rp;
+    a.col_idx = bd.ci;
+    a.val = bd.val;
+    a.perm = bd.perm;
+    a.n = nbd;
+    a.partials = c->partials + (size_t)g1 * a.pstride;
+    nlaunch++;
+    if (prof) prof->begin(adj ? PT_SPMM_ADJ : PT_SPMM, c->st, s, ((double)nbd / n) * ((n + 1) * 4.0 + nz * (4 + esz) + 2.0 * n * s * esz));
+    err = launch_spmm(cplx, cap, false, a, g2, 256, smem, c->st);
+    if (prof) prof->end(c->st);
+    if (err) return err;
+  }
+  if (g1 + g2 == 0) return 0;
+  // both launches' partials: [g1 + g2][pstride], one fixed-order finalisation
+  return finish_reds(*this, reds, poffs, s, g1 + g2, a.pstride);
+}
+
+int build_halo_split(Mat& m, bool adj, cudaStream_t st) {
+  const int* rp = adj ? m.rpH : m.rp;
+  const int* ci = adj ? m.ciH : m.ci;
+  const void* val = adj ? m.valH : m.val;
+  const long long n = m.n, nnz = adj ? m.nnzH : m.nnz;
+  if (!m.dist || n < 1 || !rp || (adj ? m.srtH.perm : m.srt.perm)) return 0;  // (irregular: the sorted order)
+  std::vector<int> h(n + 1), hc(std::max(1LL, nnz));
+  if (cudaMemcpyAsync(h.data(), rp, sizeof(int) * (n + 1), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      (nnz > 0 && cudaMemcpyAsync(hc.data(), ci, sizeof(int) * nnz, cudaMemcpyDeviceToHost, st) != cudaSuccess) ||
+      cudaStreamSynchronize(st) != cudaSuccess)
+    return (int)cudaErrorUnknown;
+  std::vector<int> lst[2];  // 0 interior, 1 boundary
+  for (long long i = 0; i < n; ++i) {
+    bool ghost = false;
+    for (int p = h[i]; p < h[i + 1]; ++p) ghost |= hc[p] >= n;
+    lst[ghost ? 1 : 0].push_back((int)i);
+  }
+  if (lst[1].empty()) return 0;  // no halo: the plain product
+  const size_t esz = m.cplx ? 16 : 8;
+  for (int q = 0; q < 2; ++q) {
+    Mat::Sorted& so = q ? (adj ? m.bndH : m.bnd) : (adj ? m.innerH : m.inner);
+    long long& cnt = q ? (adj ? m.n_bndH : m.n_bnd) : (adj ? m.n_innerH : m.n_inner);
+    const std::vector<int>& L = lst[q];
+    cnt = (long long)L.size();
+    std::vector<int> rp2(L.size() + 1);
+    rp2[0] = 0;
+    for (size_t l = 0; l < L.size(); ++l) rp2[l + 1] = rp2[l] + (h[L[l] + 1] - h[L[l]]);
+    const long long nz = rp2.back();
+    if (cudaMalloc(&so.rp, sizeof(int) * (L.size() + 1)) != cudaSuccess ||
+        cudaMalloc(&so.perm, sizeof(int) * std::max<size_t>(1, L.size())) != cudaSuccess ||
+        cudaMalloc(&so.ci, sizeof(int) * (nz + 1)) != cudaSuccess || cudaMalloc(&so.val, esz * (nz + 1)) != cudaSuccess)
+      return (int)cudaErrorMemoryAllocation;
+    cudaMemcpyAsync(so.rp, rp2.data(), sizeof(int) * (L.size() + 1), cudaMemcpyHostToDevice, st);
+    if (!L.empty()) cudaMemcpyAsync(so.perm, L.data(), sizeof(int) * L.size(), cudaMemcpyHostToDevice, st);
+    const int grid = (int)std::max<long long>(1, std::min<long long>(((long long)L.size() + 7) / 8, 148 * 16));
+    if (!L.empty()) {
+      if (m.cplx)
+        gather_sorted_rows<double2><<<grid, 256, 0, st>>>(rp, ci, reinterpret_cast<const double2*>(val), so.perm, so.rp,
+                                                          so.ci, reinterpret_cast<double2*>(so.val), (long long)L.size());
+      else
+        gather_sorted_rows<double><<<grid, 256, 0, st>>>(rp, ci, reinterpret_cast<const double*>(val), so.perm, so.rp,
+                                                         so.ci, reinterpret_cast<double*>(so.val), (long long)L.size());
+    }
+    if (cudaStreamSynchronize(st) != cudaSuccess) return (int)cudaErrorUnknown;
+  }
+  return 0;
 }
 
 }  // namespace srk

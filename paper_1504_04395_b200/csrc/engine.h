@@ -41,6 +41,8 @@ struct Comm;  // multi-GPU plumbing (comm.cpp)
 struct Ctx {
   int dev = 0;
   cudaStream_t st = nullptr;
+  cudaStream_t side = nullptr;         // multi-GPU: the halo exchange overlapped with the interior SpMM
+  cudaEvent_t ev_p = nullptr, ev_h = nullptr;
   int nsm = 148;
   double* partials = nullptr;
   size_t pcap = 0;  // doubles
@@ -100,6 +102,11 @@ struct Mat {
     void* val = nullptr;
     int* perm = nullptr;
   } srt, srtH;
+  // multi-GPU (dist): the local rows split into interior rows (owned columns only) and
+  // boundary rows (at least one ghost column), each as a row-list copy (Sorted layout,
+  // perm = output row), so the interior product runs while the halo is in flight
+  Sorted inner, bnd, innerH, bndH;
+  long long n_inner = 0, n_bnd = 0, n_innerH = 0, n_bndH = 0;
   // Banded form (band.cu): K <= 8 diagonals d_k (ascending), K arrays of npad values
   // (zero where a row has no entry on the diagonal); K = 0 when A is not banded
   struct Band {
@@ -126,6 +133,7 @@ int launch_band(bool cplx, int s, const Mat::Band& b, const void* P, void* Q, lo
 // builds m.srt / m.srtH when the row lengths are irregular (engine.cu)
 int build_balanced_order(Mat& m, bool adj, cudaStream_t st);
 void free_balanced_order(Mat& m);
+int build_halo_split(Mat& m, bool adj, cudaStream_t st);  // interior / boundary rows (dist operators)
 
 int build_ilu0(Mat& m, cudaStream_t st);  // 0, or 1 zero pivot / 2 out of memory / 3 CUDA error
 void free_prec(Prec* p);
@@ -192,7 +200,9 @@ struct Eng {
   int err = 0;            // first CUDA error
   int nlaunch = 0;        // kernels launched (instrumentation)
   int spmm(bool adj, const void* P, void* Q, int s, std::vector<RQ> reds);
-  int halo(bool adj, const void* P, int s);
+  int halo(bool adj, const void* P, int s, cudaStream_t hs = nullptr);
+  int spmm_split(bool adj, const void* P, void* Q, int s, const std::vector<RQ>& reds, const Mat::Sorted& in,
+                 long long ni, const Mat::Sorted& bd, long long nbd);
   int upd(int s, std::vector<const void*> in, std::vector<OutSpec> outs, std::vector<RQ> reds);
   // s x s Gram Y^H X on the FP64 tensor cores (gram_mma.cu), written to ws + woff
   int gram_full(const void* X, const void* Y, int s, int woff);
