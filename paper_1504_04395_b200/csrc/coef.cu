@@ -1014,6 +1014,194 @@ int launch_egl_bicg_small(bool cplx, const SmallBiCGArgs& g, cudaStream_t st) {
   return (int)cudaGetLastError();
 }
 
+// ------------------------------------------------------- small Bl-BiCGStab-rQ
+// s x s Gram Y^H X over this thread's rows, then a fixed-order CTA sum into ws + slot
+// (warp butterflies, then the warps in index order): G[a][c] = sum_i conj(Y[i][a]) X[i][c]
+template <typename T, int SK>
+__device__ void small_gram(const CoefArgs& a, int slot, const T* Xb, const T* Yb, long long n, int s, T* red) {
+  T acc[SK * SK];
+#pragma unroll
+  for (int q = 0; q < SK * SK; ++q) acc[q] = Ar<T>::zero();
+  for (long long i = threadIdx.x; i < n; i += blockDim.x) {
+#pragma unroll
+    for (int r = 0; r < SK; ++r)
+#pragma unroll
+      for (int c = 0; c < SK; ++c)
+        if (r < s && c < s) acc[r * SK + c] = Ar<T>::cfma(Yb[(size_t)i * s + r], Xb[(size_t)i * s + c], acc[r * SK + c]);
+  }
+#pragma unroll
+  for (int r = 0; r < SK; ++r)
+#pragma unroll
+    for (int c = 0; c < SK; ++c)
+      if (r < s && c < s) {
+        const T v = cta_sum(acc[r * SK + c], red);
+        if (threadIdx.x == 0) W<T>(a, slot)[r * s + c] = v;
+      }
+  __syncthreads();
+}
+
+// out[i] = sum_t src_t[i] . C_t (row vector times s x s, C row-major), up to 3 terms
+template <typename T, int SK>
+__device__ __forceinline__ void row_times(T (&o)[SK], const T* x, const T* C, int s, bool neg) {
+#pragma unroll
+  for (int c = 0; c < SK; ++c) {
+    if (c >= s) continue;
+    T acc = Ar<T>::zero();
+#pragma unroll
+    for (int k = 0; k < SK; ++k)
+      if (k < s) acc = Ar<T>::fma(x[k], C[k * s + c], acc);
+    o[c] = neg ? Ar<T>::sub(o[c], acc) : Ar<T>::add(o[c], acc);
+  }
+}
+
+template <typename T, int SK>
+__device__ void small_spmm(const int* rp, const int* ci, const T* val, const T* P, T* Q, long long n, int s) {
+  for (long long i = threadIdx.x; i < n; i += blockDim.x) {
+    T acc[SK];
+#pragma unroll
+    for (int c = 0; c < SK; ++c) acc[c] = Ar<T>::zero();
+    for (int p = rp[i]; p < rp[i + 1]; ++p) {
+      const T v = val[p];
+      const T* Pr = P + (size_t)ci[p] * s;
+#pragma unroll
+      for (int c = 0; c < SK; ++c)
+        if (c < s) acc[c] = Ar<T>::fma(v, Pr[c], acc[c]);
+    }
+#pragma unroll
+    for (int c = 0; c < SK; ++c)
+      if (c < s) Q[(size_t)i * s + c] = acc[c];
+  }
+  __syncthreads();
+}
+
+template <typename T, int SK>
+__global__ void __launch_bounds__(256) bl_bicgstab_rq_small_kernel(SmallBlStabArgs g) {
+  CoefArgs a = g.ca;
+  if (a.ctl[CTL_FLAG] != FLAG_RUN) return;
+  extern __shared__ double smraw[];
+  T* sh = reinterpret_cast<T*>(smraw);
+  __shared__ T red[32];
+  const long long n = g.n;
+  const int s = a.s;
+  const T* val = reinterpret_cast<const T*>(g.val);
+  T* X = reinterpret_cast<T*>(g.X);
+  T* Qr = reinterpret_cast<T*>(g.Qr);
+  const T* Q0 = reinterpret_cast<const T*>(g.Q0);
+  T* V = reinterpret_cast<T*>(g.V);
+  T* Wb = reinterpret_cast<T*>(g.W);
+  T* Z = reinterpret_cast<T*>(g.Z);
+  T* Y = reinterpret_cast<T*>(g.Y);
+  for (int it = 0; it < g.iters; ++it) {
+    if (it > 0 && a.ctl[CTL_FLAG] != FLAG_RUN) return;
+    // W = A V ; G = Q̂0^H W
+    small_spmm<T, SK>(g.rp, g.ci, val, V, Wb, n, s);
+    small_gram<T, SK>(a, SL_G, Wb, Q0, n, s, red);
+    a.phase = 1;
+    bl_bicgstab_rq<T>(a, sh);  // alpha = G^-1 GQ, AC = alpha C
+    if (a.ctl[CTL_FLAG] != FLAG_RUN) return;
+    // Z = Qr - W alpha ; ZZ = Z^H Z
+    for (long long i = threadIdx.x; i < n; i += blockDim.x) {
+      T o[SK];
+#pragma unroll
+      for (int c = 0; c < SK; ++c) o[c] = c < s ? Qr[(size_t)i * s + c] : Ar<T>::zero();
+      row_times<T, SK>(o, Wb + (size_t)i * s, W<T>(a, SL_ALPHA), s, true);
+#pragma unroll
+      for (int c = 0; c < SK; ++c)
+        if (c < s) Z[(size_t)i * s + c] = o[c];
+    }
+    __syncthreads();
+    small_gram<T, SK>(a, SL_ZZ, Z, Z, n, s, red);
+    a.phase = 2;
+    bl_bicgstab_rq<T>(a, sh);  // half-step test (FLAG_HALF: the host finishes the iteration)
+    if (a.ctl[CTL_FLAG] != FLAG_RUN) return;
+    // Y = A Z ; YZ = Z^H Y, YY = Y^H Y
+    small_spmm<T, SK>(g.rp, g.ci, val, Z, Y, n, s);
+    small_gram<T, SK>(a, SL_YZ, Y, Z, n, s, red);
+    small_gram<T, SK>(a, SL_YY, Y, Y, n, s, red);
+    a.phase = 3;
+    bl_bicgstab_rq<T>(a, sh);  // omega, WC = omega C
+    if (a.ctl[CTL_FLAG] != FLAG_RUN) return;
+    const T om = *W<T>(a, SL_OMEGA);
+    // X += V AC + Z WC ; Z = Z - omega Y ; GZ = Z^H Z
+    for (long long i = threadIdx.x; i < n; i += blockDim.x) {
+      T xo[SK], zo[SK];
+#pragma unroll
+      for (int c = 0; c < SK; ++c) {
+        xo[c] = c < s ? X[(size_t)i * s + c] : Ar<T>::zero();
+        zo[c] = c < s ? Z[(size_t)i * s + c] : Ar<T>::zero();
+      }
+      row_times<T, SK>(xo, V + (size_t)i * s, W<T>(a, SL_AC), s, false);
+      row_times<T, SK>(xo, Z + (size_t)i * s, W<T>(a, SL_WC), s, false);
+#pragma unroll
+      for (int c = 0; c < SK; ++c)
+        if (c < s) {
+          X[(size_t)i * s + c] = xo[c];
+          Z[(size_t)i * s + c] = Ar<T>::sub(zo[c], Ar<T>::mul(Y[(size_t)i * s + c], om));
+        }
+    }
+    __syncthreads();
+    small_gram<T, SK>(a, SL_GZ, Z, Z, n, s, red);
+    a.phase = 4;
+    bl_bicgstab_rq<T>(a, sh);  // CholQR pass 1
+    if (a.ctl[CTL_FLAG] != FLAG_RUN) return;
+    for (long long i = threadIdx.x; i < n; i += blockDim.x) {
+      T o[SK];
+#pragma unroll
+      for (int c = 0; c < SK; ++c) o[c] = Ar<T>::zero();
+      row_times<T, SK>(o, Z + (size_t)i * s, W<T>(a, SL_R1I), s, false);
+#pragma unroll
+      for (int c = 0; c < SK; ++c)
+        if (c < s) Z[(size_t)i * s + c] = o[c];
+    }
+    __syncthreads();
+    small_gram<T, SK>(a, SL_GZ, Z, Z, n, s, red);
+    a.phase = 5;
+    bl_bicgstab_rq<T>(a, sh);  // pass 2, Sig, C = Sig C
+    if (a.ctl[CTL_FLAG] != FLAG_RUN) return;
+    for (long long i = threadIdx.x; i < n; i += blockDim.x) {
+      T o[SK];
+#pragma unroll
+      for (int c = 0; c < SK; ++c) o[c] = Ar<T>::zero();
+      row_times<T, SK>(o, Z + (size_t)i * s, W<T>(a, SL_R2I), s, false);
+#pragma unroll
+      for (int c = 0; c < SK; ++c)
+        if (c < s) Qr[(size_t)i * s + c] = o[c];
+    }
+    __syncthreads();
+    small_gram<T, SK>(a, SL_GQN, Qr, Q0, n, s, red);
+    a.phase = 6;
+    bl_bicgstab_rq<T>(a, sh);  // beta, BW = omega beta, convergence test on ||C||
+    if (a.ctl[CTL_FLAG] != FLAG_RUN) return;
+    // V = Qr + V beta - W BW
+    for (long long i = threadIdx.x; i < n; i += blockDim.x) {
+      T o[SK];
+#pragma unroll
+      for (int c = 0; c < SK; ++c) o[c] = c < s ? Qr[(size_t)i * s + c] : Ar<T>::zero();
+      row_times<T, SK>(o, V + (size_t)i * s, W<T>(a, SL_BETA), s, false);
+      row_times<T, SK>(o, Wb + (size_t)i * s, W<T>(a, SL_BW), s, true);
+#pragma unroll
+      for (int c = 0; c < SK; ++c)
+        if (c < s) V[(size_t)i * s + c] = o[c];
+    }
+    if (threadIdx.x == 0) {  // end of the iteration (end_iter_kernel's step)
+      a.ctl[CTL_ITER] += 1;
+      if (a.ctl[CTL_CONVPEND]) {
+        a.ctl[CTL_CONVPEND] = 0;
+        a.ctl[CTL_FLAG] = FLAG_CONV;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+int launch_bl_bicgstab_rq_small(bool cplx, const SmallBlStabArgs& g, cudaStream_t st) {
+  const int s = g.ca.s;
+  const size_t sm = (size_t)(3 * s * s + 64) * (cplx ? 16 : 8) + 1024;
+  if (cplx) bl_bicgstab_rq_small_kernel<double2, SMALL_BL_SMAX><<<1, 256, sm, st>>>(g);
+  else bl_bicgstab_rq_small_kernel<double, SMALL_BL_SMAX><<<1, 256, sm, st>>>(g);
+  return (int)cudaGetLastError();
+}
+
 int launch_end_iter(int* ctl, cudaStream_t st) {
   end_iter_kernel<<<1, 1, 0, st>>>(ctl);
   return (int)cudaGetLastError();

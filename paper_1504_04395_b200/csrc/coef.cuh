@@ -104,6 +104,20 @@ struct SmallQMRArgs {
   CoefArgs ca;
 };
 int launch_egl_qmr_small(bool cplx, const SmallQMRArgs& g, cudaStream_t st);
+// Bl-BiCGStab-rQ for a small operator, one iteration per pass of ONE CTA
+// (config 1's second method): the products, the s x s Grams (fixed-order CTA sums), the
+// coefficient phases 1-6 (the same device code as the multi-kernel path), the updates.
+struct SmallBlStabArgs {
+  const int* rp;
+  const int* ci;
+  const void* val;
+  void *X, *Qr, *Q0, *V, *W, *Z, *Y;
+  long long n;
+  int iters;
+  CoefArgs ca;
+};
+int launch_bl_bicgstab_rq_small(bool cplx, const SmallBlStabArgs& g, cudaStream_t st);
+constexpr int SMALL_BL_SMAX = 4;  // widths of the one-CTA block kernel
 constexpr long long SMALL_N_MAX = 16384;  // one-CTA eGl-BiCG up to this many rows
 
 }  // namespace srk

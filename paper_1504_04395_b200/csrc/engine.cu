@@ -783,38 +783,78 @@ __global__ void colcount_kernel(long long nnz, const int* ci, int* cnt) {
 }
 
 // single-CTA exclusive scan of n+1 ints (cnt -> rpT), chunked
-__global__ void scan_kernel(long long n, const int* cnt, int* rpT) {
-  __shared__ long long carry;
-  __shared__ long long part[1024];
-  if (threadIdx.x == 0) carry = 0;
+// Exclusive prefix sum of the column counts (row pointers of A^H), multi-CTA: 1) every
+// CTA sums its segment, 2) one CTA scans the segment sums, 3) every CTA scans its segment
+// from its offset (block scans by warp shuffles; integer, so any order gives the same bits).
+__device__ long long block_excl_scan(long long v, long long* sh /* >= 33 */, long long* total) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  long long x = v;
+  for (int o = 1; o < 32; o <<= 1) {
+    const long long y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) sh[w] = x;
   __syncthreads();
-  for (long long base = 0; base < n; base += 1024 * 16) {
-    // each thread sums 16 consecutive entries
-    long long loc = 0;
-    const long long b0 = base + threadIdx.x * 16;
-    for (int k = 0; k < 16; ++k)
-      if (b0 + k < n) loc += cnt[b0 + k];
-    part[threadIdx.x] = loc;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      long long acc = carry;
-      for (int t = 0; t < 1024; ++t) {
-        long long v = part[t];
-        part[t] = acc;
-        acc += v;
-      }
-      carry = acc;
+  if (w == 0) {
+    long long t = lane < nw ? sh[lane] : 0;
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long y = __shfl_up_sync(0xffffffffu, t, o);
+      if (lane >= o) t += y;
     }
-    __syncthreads();
-    long long acc = part[threadIdx.x];
-    for (int k = 0; k < 16; ++k)
-      if (b0 + k < n) {
-        rpT[b0 + k] = (int)acc;
-        acc += cnt[b0 + k];
+    if (lane < nw) sh[lane] = t;  // inclusive warp-total prefix
+  }
+  __syncthreads();
+  const long long before = (w > 0 ? sh[w - 1] : 0) + x - v;
+  if (total) *total = sh[nw - 1];
+  __syncthreads();
+  return before;
+}
+
+__global__ void seg_sum_kernel(long long n, long long seg, const int* cnt, long long* bsum) {
+  __shared__ long long sh[33];
+  const long long b0 = blockIdx.x * seg, b1 = b0 + seg < n ? b0 + seg : n;
+  long long loc = 0;
+  for (long long i = b0 + threadIdx.x; i < b1; i += blockDim.x) loc += cnt[i];
+  long long tot = 0;
+  block_excl_scan(loc, sh, &tot);
+  if (threadIdx.x == 0) bsum[blockIdx.x] = tot;
+}
+
+__global__ void seg_offsets_kernel(int nb, long long* bsum, long long n, int* rpT) {
+  if (threadIdx.x == 0) {
+    long long acc = 0;
+    for (int b = 0; b < nb; ++b) {
+      const long long v = bsum[b];
+      bsum[b] = acc;
+      acc += v;
+    }
+    rpT[n] = (int)acc;
+  }
+}
+
+__global__ void seg_scan_kernel(long long n, long long seg, const int* cnt, const long long* boff, int* rpT) {
+  __shared__ long long sh[33];
+  __shared__ long long carry;
+  const long long b0 = blockIdx.x * seg, b1 = b0 + seg < n ? b0 + seg : n;
+  if (threadIdx.x == 0) carry = boff[blockIdx.x];
+  __syncthreads();
+  constexpr int PER = 8;
+  for (long long base = b0; base < b1; base += (long long)blockDim.x * PER) {
+    const long long t0 = base + (long long)threadIdx.x * PER;
+    long long loc = 0;
+    for (int k = 0; k < PER; ++k)
+      if (t0 + k < b1) loc += cnt[t0 + k];
+    long long tot = 0;
+    long long acc = carry + block_excl_scan(loc, sh, &tot);
+    for (int k = 0; k < PER; ++k)
+      if (t0 + k < b1) {
+        rpT[t0 + k] = (int)acc;
+        acc += cnt[t0 + k];
       }
+    __syncthreads();
+    if (threadIdx.x == 0) carry += tot;
     __syncthreads();
   }
-  if (threadIdx.x == 0) rpT[n] = (int)carry;
 }
 
 template <typename T>
@@ -855,7 +895,15 @@ int launch_csr_transpose(bool cplx, long long n, long long nnz, const int* rp, c
   const int gridz = (int)std::max<long long>(1, std::min<long long>((nnz + 255) / 256, 148 * 8));
   cudaMemsetAsync(work, 0, sizeof(int) * n, st);
   colcount_kernel<<<gridz, 256, 0, st>>>(nnz, ci, work);
-  scan_kernel<<<1, 1024, 0, st>>>(n, work, rpT);
+  const int nseg = (int)std::max<long long>(1, std::min<long long>(148 * 8, (n + 4095) / 4096));
+  const long long seg = (n + nseg - 1) / nseg;
+  long long* bsum = nullptr;
+  if (cudaMalloc(&bsum, sizeof(long long) * nseg) != cudaSuccess) return (int)cudaErrorMemoryAllocation;
+  seg_sum_kernel<<<nseg, 256, 0, st>>>(n, seg, work, bsum);
+  seg_offsets_kernel<<<1, 32, 0, st>>>(nseg, bsum, n, rpT);
+  seg_scan_kernel<<<nseg, 256, 0, st>>>(n, seg, work, bsum, rpT);
+  cudaStreamSynchronize(st);
+  cudaFree(bsum);
   cudaMemcpyAsync(work, rpT, sizeof(int) * n, cudaMemcpyDeviceToDevice, st);
   if (cplx) {
     scatter_kernel<double2><<<gridn, 256, 0, st>>>(n, rp, ci, (const double2*)val, work, ciT, (double2*)valT);

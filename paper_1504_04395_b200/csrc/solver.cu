@@ -744,6 +744,38 @@ struct BlBiCGStabrQ : Solver {
   void* Zs = nullptr;  // rank continuation (f4)
   bool is_rq() const override { return true; }
   int nseg() const override { return 2; }
+  // small operators (latency-bound, config 1): whole iterations in one single-CTA kernel
+  bool small() const {
+    static const bool off_env = getenv("SRK_NO_SMALL_KERNEL") != nullptr;  // A/B switch
+    return !off_env && A && !A->bsr && !A->prec && A->ghost_rows() == 0 && n <= SMALL_N_MAX && s <= SMALL_BL_SMAX &&
+           !o.rank_policy && !(c->comm && c->comm->nranks > 1);
+  }
+  bool ends_iter() const override { return small(); }
+  int seg_multi(int k) override {
+    if (!small() || k < 1 || e.err) return 0;
+    SmallBlStabArgs g{};
+    g.rp = A->rp;
+    g.ci = A->ci;
+    g.val = A->val;
+    g.X = X; g.Qr = Qr; g.Q0 = Q0; g.V = V; g.W = W; g.Z = Z; g.Y = Y;
+    g.n = n;
+    g.iters = k;
+    g.ca.method = method;
+    g.ca.s = s;
+    g.ca.tol = o.tol;
+    g.ca.eps_brk = eps_brk();
+    g.ca.eps_chol = eps_chol();
+    g.ca.ws = ws;
+    g.ca.ctl = ctl;
+    g.ca.hist = hist;
+    g.ca.hist_cap = hist_cap;
+    for (int i = 0; i < NSLOT; ++i) g.ca.off[i] = off[i];
+    e.nlaunch++;
+    prof.begin(PT_OTHER, c->st);
+    e.err = launch_bl_bicgstab_rq_small(cplx, g, c->st);
+    prof.end(c->st);
+    return k;
+  }
   int alloc() override {
     Qr = blk(); Q0 = blk(); V = blk(); W = blk(); Z = blk(); Y = blk(); tmp2 = blk();
     if (o.rank_policy && !(Zs = blk())) return SRK_ENOMEM;

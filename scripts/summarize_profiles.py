@@ -1,6 +1,7 @@
 """Summarise the ncu evidence of one GPU call into profiles/ (tracked).
 
-    python scripts/summarize_profiles.py r01
+    python scripts/summarize_profiles.py r01            # gpurun_out/prof_*.ncu-rep, launches.csv, bench.log
+    python scripts/summarize_profiles.py r02 r02_       # gpurun_out/r02_prof_*.ncu-rep, r02_launches.csv, ...
 
 Captures: prof_spmm (config 3 SpMM), prof_upd (config 3's dominant 6-in / 4-out update),
 prof_bsr (config 4 BSR-12 product), prof_gram (s = 64 CTA-tiled DMMA Gram), prof_updmma
@@ -48,11 +49,11 @@ def to_bytes(v, unit):
     return f * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
 
 
-def main(tag):
+def main(tag, pre=""):
     os.makedirs(PROF, exist_ok=True)
     summary = {}
-    for name in ("spmm", "upd", "bsr", "gram", "updmma", "gramwarp", "small"):
-        rep = os.path.join(OUT, f"prof_{name}.ncu-rep")
+    for name in ("spmm", "upd", "bsr", "gram", "updmma", "gramwarp", "small", "band"):
+        rep = os.path.join(OUT, f"{pre}prof_{name}.ncu-rep")
         if not os.path.exists(rep):
             continue
         v, u = ncu_raw(rep)
@@ -71,7 +72,7 @@ def main(tag):
         tj["cfg3_egl_qmr_dominant"] = summary["upd"]["dram_bytes_per_launch"]
     if len(tj) > 1:
         json.dump(tj, open(os.path.join(PROF, "traffic.json"), "w"), indent=1)
-    lc = os.path.join(OUT, "launches.csv")
+    lc = os.path.join(OUT, f"{pre}launches.csv")
     if os.path.exists(lc):
         lines = [ln for ln in open(lc) if ln.startswith('"')]
         rows = list(csv.DictReader(io.StringIO("".join(lines))))
@@ -92,7 +93,7 @@ def main(tag):
                 share[k] = share.get(k, 0.0) + float(r["Metric Value"])
             json.dump({"iteration_ns": tot, "share": {k: v / tot for k, v in sorted(share.items(), key=lambda x: -x[1])},
                        "ns": share}, open(os.path.join(PROF, f"{tag}_iteration_shares.json"), "w"), indent=1)
-    bl = os.path.join(OUT, "bench.log")
+    bl = os.path.join(OUT, f"{pre}bench.log")
     if os.path.exists(bl):
         for ln in open(bl):
             if ln.startswith("{"):
@@ -101,4 +102,4 @@ def main(tag):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1] if len(sys.argv) > 1 else "r01")
+    main(sys.argv[1] if len(sys.argv) > 1 else "r01", sys.argv[2] if len(sys.argv) > 2 else "")
