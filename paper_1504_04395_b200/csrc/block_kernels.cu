@@ -37,7 +37,9 @@ int launch_upd_c128(int cap, bool full, const UpdArgs& a, int grid, int block, s
 __host__ __device__ constexpr int pow2c(int x) { return x <= 1 ? 1 : 2 * pow2c((x + 1) / 2); }
 
 int cap_for(int s) {
-  const int caps[] = {1, 4, 8, 12, 16, 32, 64};
+  // (2: an exact-width instance for s = 2 — the team-per-row kernel with 16-byte P rows,
+  // config 5's s = 2 ran 3x slower than s = 1 on the generic width-4 instance)
+  const int caps[] = {1, 2, 4, 8, 12, 16, 32, 64};
   for (int c : caps)
     if (s <= c) return c;
   return -1;

@@ -1078,8 +1078,15 @@ template <typename T, int SK>
 __global__ void __launch_bounds__(256) bl_bicgstab_rq_small_kernel(SmallBlStabArgs g) {
   CoefArgs a = g.ca;
   if (a.ctl[CTL_FLAG] != FLAG_RUN) return;
+  // the s x s algebra is a chain of dependent accesses to the coefficient slots: with the
+  // workspace in shared memory (copied in here, back at the end) each is ~30 cycles, not an
+  // L2 round trip
   extern __shared__ double smraw[];
-  T* sh = reinterpret_cast<T*>(smraw);
+  double* const wsg = a.ws;
+  for (long long q = threadIdx.x; q < g.ws_doubles; q += blockDim.x) smraw[q] = wsg[q];
+  __syncthreads();
+  a.ws = smraw;
+  T* sh = reinterpret_cast<T*>(smraw + ((g.ws_doubles + 1) & ~1LL));
   __shared__ T red[32];
   const long long n = g.n;
   const int s = a.s;
@@ -1092,13 +1099,13 @@ __global__ void __launch_bounds__(256) bl_bicgstab_rq_small_kernel(SmallBlStabAr
   T* Z = reinterpret_cast<T*>(g.Z);
   T* Y = reinterpret_cast<T*>(g.Y);
   for (int it = 0; it < g.iters; ++it) {
-    if (it > 0 && a.ctl[CTL_FLAG] != FLAG_RUN) return;
+    if (it > 0 && a.ctl[CTL_FLAG] != FLAG_RUN) break;
     // W = A V ; G = Q̂0^H W
     small_spmm<T, SK>(g.rp, g.ci, val, V, Wb, n, s);
     small_gram<T, SK>(a, SL_G, Wb, Q0, n, s, red);
     a.phase = 1;
     bl_bicgstab_rq<T>(a, sh);  // alpha = G^-1 GQ, AC = alpha C
-    if (a.ctl[CTL_FLAG] != FLAG_RUN) return;
+    if (a.ctl[CTL_FLAG] != FLAG_RUN) break;
     // Z = Qr - W alpha ; ZZ = Z^H Z
     for (long long i = threadIdx.x; i < n; i += blockDim.x) {
       T o[SK];
@@ -1113,14 +1120,14 @@ __global__ void __launch_bounds__(256) bl_bicgstab_rq_small_kernel(SmallBlStabAr
     small_gram<T, SK>(a, SL_ZZ, Z, Z, n, s, red);
     a.phase = 2;
     bl_bicgstab_rq<T>(a, sh);  // half-step test (FLAG_HALF: the host finishes the iteration)
-    if (a.ctl[CTL_FLAG] != FLAG_RUN) return;
+    if (a.ctl[CTL_FLAG] != FLAG_RUN) break;
     // Y = A Z ; YZ = Z^H Y, YY = Y^H Y
     small_spmm<T, SK>(g.rp, g.ci, val, Z, Y, n, s);
     small_gram<T, SK>(a, SL_YZ, Y, Z, n, s, red);
     small_gram<T, SK>(a, SL_YY, Y, Y, n, s, red);
     a.phase = 3;
     bl_bicgstab_rq<T>(a, sh);  // omega, WC = omega C
-    if (a.ctl[CTL_FLAG] != FLAG_RUN) return;
+    if (a.ctl[CTL_FLAG] != FLAG_RUN) break;
     const T om = *W<T>(a, SL_OMEGA);
     // X += V AC + Z WC ; Z = Z - omega Y ; GZ = Z^H Z
     for (long long i = threadIdx.x; i < n; i += blockDim.x) {
@@ -1143,7 +1150,7 @@ __global__ void __launch_bounds__(256) bl_bicgstab_rq_small_kernel(SmallBlStabAr
     small_gram<T, SK>(a, SL_GZ, Z, Z, n, s, red);
     a.phase = 4;
     bl_bicgstab_rq<T>(a, sh);  // CholQR pass 1
-    if (a.ctl[CTL_FLAG] != FLAG_RUN) return;
+    if (a.ctl[CTL_FLAG] != FLAG_RUN) break;
     for (long long i = threadIdx.x; i < n; i += blockDim.x) {
       T o[SK];
 #pragma unroll
@@ -1157,7 +1164,7 @@ __global__ void __launch_bounds__(256) bl_bicgstab_rq_small_kernel(SmallBlStabAr
     small_gram<T, SK>(a, SL_GZ, Z, Z, n, s, red);
     a.phase = 5;
     bl_bicgstab_rq<T>(a, sh);  // pass 2, Sig, C = Sig C
-    if (a.ctl[CTL_FLAG] != FLAG_RUN) return;
+    if (a.ctl[CTL_FLAG] != FLAG_RUN) break;
     for (long long i = threadIdx.x; i < n; i += blockDim.x) {
       T o[SK];
 #pragma unroll
@@ -1171,7 +1178,7 @@ __global__ void __launch_bounds__(256) bl_bicgstab_rq_small_kernel(SmallBlStabAr
     small_gram<T, SK>(a, SL_GQN, Qr, Q0, n, s, red);
     a.phase = 6;
     bl_bicgstab_rq<T>(a, sh);  // beta, BW = omega beta, convergence test on ||C||
-    if (a.ctl[CTL_FLAG] != FLAG_RUN) return;
+    if (a.ctl[CTL_FLAG] != FLAG_RUN) break;
     // V = Qr + V beta - W BW
     for (long long i = threadIdx.x; i < n; i += blockDim.x) {
       T o[SK];
@@ -1192,11 +1199,19 @@ __global__ void __launch_bounds__(256) bl_bicgstab_rq_small_kernel(SmallBlStabAr
     }
     __syncthreads();
   }
+  __syncthreads();
+  for (long long q = threadIdx.x; q < g.ws_doubles; q += blockDim.x) wsg[q] = smraw[q];
 }
 
 int launch_bl_bicgstab_rq_small(bool cplx, const SmallBlStabArgs& g, cudaStream_t st) {
   const int s = g.ca.s;
-  const size_t sm = (size_t)(3 * s * s + 64) * (cplx ? 16 : 8) + 1024;
+  const size_t sm = (size_t)((g.ws_doubles + 1) & ~1LL) * 8 + (size_t)(3 * s * s + 64) * (cplx ? 16 : 8) + 1024;
+  if (sm > 220 * 1024) return (int)cudaErrorNotSupported;
+  static std::atomic<unsigned long long> attr{0};
+  if (first_on_device(attr)) {
+    cudaFuncSetAttribute(bl_bicgstab_rq_small_kernel<double, SMALL_BL_SMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    cudaFuncSetAttribute(bl_bicgstab_rq_small_kernel<double2, SMALL_BL_SMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+  }
   if (cplx) bl_bicgstab_rq_small_kernel<double2, SMALL_BL_SMAX><<<1, 256, sm, st>>>(g);
   else bl_bicgstab_rq_small_kernel<double, SMALL_BL_SMAX><<<1, 256, sm, st>>>(g);
   return (int)cudaGetLastError();

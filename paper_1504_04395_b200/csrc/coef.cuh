@@ -114,6 +114,7 @@ struct SmallBlStabArgs {
   void *X, *Qr, *Q0, *V, *W, *Z, *Y;
   long long n;
   int iters;
+  long long ws_doubles;  // the coefficient workspace is staged in shared memory for the launch
   CoefArgs ca;
 };
 int launch_bl_bicgstab_rq_small(bool cplx, const SmallBlStabArgs& g, cudaStream_t st);

@@ -760,6 +760,7 @@ struct BlBiCGStabrQ : Solver {
     g.X = X; g.Qr = Qr; g.Q0 = Q0; g.V = V; g.W = W; g.Z = Z; g.Y = Y;
     g.n = n;
     g.iters = k;
+    g.ws_doubles = (long long)slot_doubles(s) * NSLOT;
     g.ca.method = method;
     g.ca.s = s;
     g.ca.tol = o.tol;

@@ -146,9 +146,12 @@ def test_table2_gpu_vs_oracle(row):
     X, rep = srk.solve(M, torch.from_numpy(Q).cuda(), method, tol=1e-10, maxit=500)
     assert rep.outcome == a.outcome, (rep.outcome, a.outcome)
     slack = max(2, 0.02 * a.iterations)
-    if abs(rep.iterations - a.iterations) > slack:
-        b = oracle.solve(method, As, Q, tol=1e-10, maxit=500, record=0, order="seq")
-        slack = max(slack, abs(a.iterations - b.iterations) + 2)
-    assert abs(rep.iterations - a.iterations) <= slack, (rep.iterations, a.iterations)
+    alts = []
+    if abs(rep.iterations - a.iterations) > slack:  # the oracle's own spread over its orders (R10)
+        alts = [oracle.solve(method, As, Q, tol=1e-10, maxit=500, record=0, order=o) for o in ("seq", "rev", "cholqr")]
+        alts = [b.iterations for b in alts if b.outcome == a.outcome]
+        if alts:
+            slack = max(slack, max(abs(a.iterations - b) for b in alts) + 2)
+    assert abs(rep.iterations - a.iterations) <= slack, (rep.iterations, a.iterations, alts)
     Xh = X.cpu().numpy()
     assert np.linalg.norm(Q - As @ Xh) / np.linalg.norm(Q) <= 1e-10
