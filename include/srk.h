@@ -139,6 +139,25 @@ int srk_matrix_ilu0(srk_matrix* A);
 /* the factor values on A's pattern (L strictly below, U on and above the diagonal),
  * nnz values (complex interleaved) into a HOST buffer — for tests */
 int srk_matrix_ilu0_factor(const srk_matrix* A, void* values_host);
+/* Right ILUTP preconditioning: the incomplete LU "with threshold and pivoting with a drop
+ * tolerance of 5e-2" of Ex. 4. The paper names only
+ * Matlab's ilu; reading R14 fixes the algorithm: left-looking column ILU with
+ * partial pivoting, a multiplier or L entry of column j dropped when its magnitude is below
+ * droptol * ||A(:, j)||_2 (the pivot never), pivot = the largest candidate of the rows not yet
+ * pivoted unless the original diagonal row's candidate reaches thresh times that (thresh = 1:
+ * partial pivoting, 0: no pivoting while the diagonal is nonzero). Pi A ~ L U; solves then
+ * iterate on A M^-1 Y = B with M = Pi^T L U (A^H products as M^-H A^H = Pi^T L^-H U^-H A^H),
+ * the row permutation applied on the device around the level-scheduled triangular solves.
+ * Computed once on the HOST from the operator's CSR (a0 work). Scalar single-GPU CSR
+ * operators only. Errors: SRK_EINVAL (droptol < 0, thresh outside [0, 1], a column with no
+ * nonzero pivot candidate), SRK_EUNSUPPORTED, SRK_ENOMEM. */
+int srk_matrix_ilutp(srk_matrix* A, double droptol, double thresh);
+/* kind 0 = ILU(0), 1 = ILUTP; nnz of the factor (L strictly lower + U); pivoted = a row moved */
+int srk_matrix_prec_info(const srk_matrix* A, int* kind, int64_t* nnz_factor, int* pivoted);
+/* the ILUTP factor F = (L - I) + U in the pivot order as a CSR (row_ptr n+1, col_idx /
+ * values nnz_factor, complex interleaved) and perm (n: row of A pivoted at step k), all
+ * HOST buffers — for tests */
+int srk_matrix_ilutp_factor(const srk_matrix* A, int64_t* row_ptr, int32_t* col_idx, void* values, int64_t* perm);
 /* Z = M^-1 P (adjoint: M^-H P), n x s device blocks, stream-ordered */
 int srk_precond_apply(srk_ctx* ctx, const srk_matrix* A, int adjoint, const void* P, void* Z, int s);
 int srk_matrix_destroy(srk_matrix* A);

@@ -38,7 +38,8 @@ EXPORTS = ("srk_create", "srk_destroy", "srk_last_error", "srk_version", "srk_ma
            "srk_plan_destroy", "srk_nccl_unique_id", "srk_comm_init", "srk_matrix_create_dist",
            "srk_vgroup_create", "srk_vgroup_destroy", "srk_comm_init_virtual", "srk_csr_adjoint_host",
            "srk_matrix_format", "srk_matrix_create_bsr_dist",
-           "srk_matrix_create_bsr", "srk_matrix_ilu0", "srk_matrix_ilu0_factor", "srk_precond_apply")
+           "srk_matrix_create_bsr", "srk_matrix_ilu0", "srk_matrix_ilu0_factor", "srk_precond_apply",
+           "srk_matrix_ilutp", "srk_matrix_prec_info", "srk_matrix_ilutp_factor")
 
 
 class SrkError(RuntimeError):
@@ -96,6 +97,9 @@ def load_library(path: str | None = None):
         "srk_matrix_destroy": ([vp], i),
         "srk_matrix_ilu0": ([vp], i),
         "srk_matrix_ilu0_factor": ([vp, vp], i),
+        "srk_matrix_ilutp": ([vp, d, d], i),
+        "srk_matrix_prec_info": ([vp, ctypes.POINTER(i), ctypes.POINTER(i64), ctypes.POINTER(i)], i),
+        "srk_matrix_ilutp_factor": ([vp, vp, vp, vp, vp], i),
         "srk_precond_apply": ([vp, vp, i, vp, vp, i], i),
         "srk_matrix_adjoint": ([vp, vp, vp, vp], i),
         "srk_spmm_block": ([vp, vp, i, vp, vp, i, i, vp, vp], i),
@@ -277,6 +281,41 @@ class Matrix:
         _check(_lib.srk_matrix_ilu0(self.h), "srk_matrix_ilu0")
         self.preconditioned = True
         return self
+
+    def ilutp(self, droptol: float = 5e-2, thresh: float = 1.0):
+        """Attach the right ILUTP preconditioner (srk_matrix_ilutp, reading R14):
+        threshold ILU with partial pivoting, M = Pi^T L U; returns self."""
+        _check(_lib.srk_matrix_ilutp(self.h, float(droptol), float(thresh)), "srk_matrix_ilutp")
+        self.preconditioned = True
+        return self
+
+    def prec_info(self):
+        """(kind: 'ilu0' | 'ilutp', nnz of the factor, pivoted)"""
+        k, nz, pv = ctypes.c_int(0), ctypes.c_int64(0), ctypes.c_int(0)
+        _check(_lib.srk_matrix_prec_info(self.h, ctypes.byref(k), ctypes.byref(nz), ctypes.byref(pv)),
+               "srk_matrix_prec_info")
+        return ("ilu0", "ilutp")[k.value], nz.value, bool(pv.value)
+
+    def ilutp_factor(self):
+        """(L, U, perm) of the attached ILUTP as scipy CSR (pivot order; host copy):
+        A[perm] ~ L @ U."""
+        import scipy.sparse as sp
+        torch = _torch()
+        cplx = self.dtype == torch.complex128
+        _, nz, _ = self.prec_info()
+        rp = np.empty(self.n + 1, dtype=np.int64)
+        ci = np.empty(max(nz, 1), dtype=np.int32)
+        va = np.empty(max(nz, 1), dtype=np.complex128 if cplx else np.float64)
+        perm = np.empty(self.n, dtype=np.int64)
+        _check(_lib.srk_matrix_ilutp_factor(self.h, rp.ctypes.data_as(ctypes.c_void_p), ci.ctypes.data_as(ctypes.c_void_p),
+                                            va.ctypes.data_as(ctypes.c_void_p), perm.ctypes.data_as(ctypes.c_void_p)),
+               "srk_matrix_ilutp_factor")
+        F = sp.csr_matrix((va[:nz], ci[:nz], rp), shape=(self.n, self.n))
+        L = sp.tril(F, k=-1, format="csr") + sp.identity(self.n, dtype=va.dtype, format="csr")
+        U = sp.triu(F, k=0, format="csr")
+        L.sort_indices()
+        U.sort_indices()
+        return L, U, perm
 
     def ilu0_factor(self) -> np.ndarray:
         """The ILU(0) factor values on the operator's pattern (host copy)."""

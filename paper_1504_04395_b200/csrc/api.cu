@@ -283,9 +283,45 @@ int srk_matrix_ilu0(srk_matrix* A) {
   return SRK_OK;
 }
 
+int srk_matrix_ilutp(srk_matrix* A, double droptol, double thresh) {
+  if (!A) return fail(SRK_EINVAL, "srk_matrix_ilutp: null matrix");
+  if (!(droptol >= 0.0) || !(thresh >= 0.0) || !(thresh <= 1.0))
+    return fail(SRK_EINVAL, "srk_matrix_ilutp: droptol >= 0 and 0 <= thresh <= 1 required");
+  Mat& m = A->m;
+  if (m.bsr || m.dist) return fail(SRK_EUNSUPPORTED, "srk_matrix_ilutp: scalar single-GPU CSR operators only");
+  srk_ctx* owner = reinterpret_cast<srk_ctx*>(m.ctx);
+  if (owner && owner->cached_mat == A->id) drop_cache(owner);
+  const int r = build_ilutp(m, droptol, thresh, m.ctx->st);
+  if (r == 1) return fail(SRK_EINVAL, "srk_matrix_ilutp: a column without a nonzero pivot (structurally singular)");
+  if (r == 2) return fail(SRK_ENOMEM, "srk_matrix_ilutp: out of memory");
+  if (r) return fail(SRK_ECUDA, "srk_matrix_ilutp: CUDA error");
+  return SRK_OK;
+}
+
+int srk_matrix_prec_info(const srk_matrix* A, int* kind, int64_t* nnz_factor, int* pivoted) {
+  if (!A || !kind || !nnz_factor || !pivoted) return fail(SRK_EINVAL, "srk_matrix_prec_info: null argument");
+  const Prec* P = A->m.prec;
+  if (!P) return fail(SRK_EINVAL, "srk_matrix_prec_info: no preconditioner attached");
+  *kind = P->kind;
+  *nnz_factor = P->kind ? (int64_t)P->fci.size() : A->m.nnz;
+  *pivoted = P->perm ? 1 : 0;
+  return SRK_OK;
+}
+
+int srk_matrix_ilutp_factor(const srk_matrix* A, int64_t* row_ptr, int32_t* col_idx, void* values, int64_t* perm) {
+  if (!A || !row_ptr || !col_idx || !values || !perm) return fail(SRK_EINVAL, "srk_matrix_ilutp_factor: null argument");
+  const Prec* P = A->m.prec;
+  if (!P || P->kind != 1) return fail(SRK_EINVAL, "srk_matrix_ilutp_factor: no ILUTP attached");
+  for (size_t i = 0; i < P->frp.size(); ++i) row_ptr[i] = P->frp[i];
+  for (size_t i = 0; i < P->fci.size(); ++i) col_idx[i] = P->fci[i];
+  std::memcpy(values, P->factor.data(), P->factor.size() * sizeof(double));
+  for (size_t i = 0; i < P->hperm.size(); ++i) perm[i] = P->hperm[i];
+  return SRK_OK;
+}
+
 int srk_matrix_ilu0_factor(const srk_matrix* A, void* values_host) {
   if (!A || !values_host) return fail(SRK_EINVAL, "srk_matrix_ilu0_factor: null argument");
-  if (!A->m.prec) return fail(SRK_EINVAL, "srk_matrix_ilu0_factor: no ILU(0) attached");
+  if (!A->m.prec || A->m.prec->kind != 0) return fail(SRK_EINVAL, "srk_matrix_ilu0_factor: no ILU(0) attached");
   const std::vector<double>& f = A->m.prec->factor;
   std::memcpy(values_host, f.data(), f.size() * sizeof(double));
   return SRK_OK;

@@ -538,6 +538,311 @@ __global__ void __launch_bounds__(32 * NWT, 1) band_cp_kernel(BandArgs a) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Plane-marching SpMM for the 7-point pattern (round 2, session 3). Operators whose
+// diagonals are exactly {-F, -m, -1, 0, +1, +m, +F} with F a multiple of m (the 3D
+// convection-diffusion stencils of configs 2 / 3, and their adjoints) are
+// multiplied as a 2.5D sweep: row i = z F + y m + x is point (x, y) of plane z. A work item
+// is a TX x TY tile of (x, y) points and a segment of ZL planes; the CTA marches z through
+// the segment keeping a ring of NB plane WINDOWS in shared memory, each window = the
+// (TX + 2) x (TY + 2) rows around the tile (rows addressed by index, so the +-1 / +-m
+// neighbours of every tile row lie inside the window whatever the matrix's values at the
+// grid edges), filled by TY + 2 bulk copies of TX + 2 consecutive rows. The -F neighbour of
+// a row is the centre row of the previous plane, held in registers from the previous step;
+// the +F neighbour is the centre row of the next window. So every P row is copied into shared
+// memory (TX+2)(TY+2)/(TX TY) ~ 1.4 times instead of the band kernel's three times (ring +
+// two far windows) — the far windows' L2 -> SM traffic was the band kernel's limit on
+// config 3. Concurrent items are neighbouring tiles of one plane segment, so the halo rows
+// a tile shares with its neighbours are L2 hits. Summation order per row = ascending offset
+// (= ascending column, the CSR order), as in band_kernel.
+constexpr int PL_NBMAX = 4;   // plane windows in flight (runtime NB <= 4)
+constexpr int PL_TX = 32;     // tile width (points along x)
+constexpr int PL_TY = 6;      // tile height (lines along y)
+constexpr int PL_K = 7;
+
+struct PlaneArgs {
+  const void* dia;  // [npad][7] diagonal values, row-major
+  const void* P;
+  void* Q;
+  long long n, F;
+  int m, ny;        // points per line, lines per plane (F = m ny)
+  long long nz;     // planes (ceil(n / F))
+  int ntx, nty;     // tiles per plane along x / y
+  int zl, nzs;      // planes per segment, segments
+  long long nitems; // ntx * nty * nzs
+  int NB;           // ring depth
+  Red red[2];
+  int nred;
+  int ystage[2];    // 1: SUMVEC vector staged per plane
+  double* partials;
+  int pstride;
+  const int* done;
+};
+
+template <typename T, int S>
+struct PlaneCfg {
+  static constexpr int RB = S * (int)sizeof(T);
+  static constexpr int WX = PL_TX + 2, WY = PL_TY + 2;
+  static constexpr int WR = WX * WY;                       // rows per window
+  static constexpr int VL = (PL_TX + 2) * PL_K;            // values per line slot (+2: alignment shift)
+  static constexpr int YL = PL_TX + 2;                     // vector entries per line slot
+  static constexpr size_t WIN = (size_t)WR * RB;           // bytes per window
+  static constexpr size_t VAL = (size_t)PL_TY * VL * sizeof(T);
+  static constexpr size_t YV = (size_t)PL_TY * YL * sizeof(T);
+};
+
+template <typename T, int S>
+size_t plane_smem(int NB, int ny) {
+  using C = PlaneCfg<T, S>;
+  return 128 + (size_t)NB * (C::WIN + C::VAL + (size_t)ny * C::YV);
+}
+
+template <typename T, int S, int NW>
+__global__ void __launch_bounds__(32 * (NW + 1), 1) band_plane_kernel(PlaneArgs a) {
+  if (a.done && *a.done) return;
+  using L = Lay<T, S>;
+  using C = PlaneCfg<T, S>;
+  constexpr int TROWS = PL_TX * PL_TY;
+  constexpr int SLOTS = NW * L::RPW;
+  constexpr int RPL = (TROWS + SLOTS - 1) / SLOTS;  // tile rows per lane group
+  const int NB = a.NB;
+  extern __shared__ __align__(128) unsigned char bsm[];
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(bsm);
+  unsigned long long* empty = full + PL_NBMAX;
+  T* win = reinterpret_cast<T*>(bsm + 128);                      // [NB][WY][WX][S]
+  T* vals = win + (size_t)NB * C::WR * S;                        // [NB][TY][VL]
+  T* ybuf = vals + (size_t)NB * PL_TY * C::VL;                   // [NB][ny][TY][YL]
+  int ny = 0;
+  int yslot[2] = {-1, -1};
+  for (int q = 0; q < a.nred && q < 2; ++q)
+    if (a.ystage[q]) yslot[q] = ny++;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long n = a.n, F = a.F;
+  const int m = a.m;
+  const long long ntile = (long long)a.ntx * a.nty;
+  {  // windows start finite (clamped rows are never copied; their diagonal values are zero)
+    double* z = reinterpret_cast<double*>(win);
+    const size_t nd = (size_t)NB * C::WIN / 8;
+    for (size_t i = threadIdx.x; i < nd; i += blockDim.x) z[i] = 0.0;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < NB; ++q) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bsmem(full + q)));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bsmem(empty + q)), "r"(NW));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ producer
+    // per window: TY + 2 P line segments; for computed planes also TY value segments and TY
+    // vector segments per staged reduction — one copy per lane (looping for wide tiles)
+    const char* P = reinterpret_cast<const char*>(a.P);
+    const char* dia = reinterpret_cast<const char*>(a.dia);
+    constexpr int ESZ = (int)sizeof(T);
+    long long g = 0;
+    int st = 0;
+    unsigned ph = 0;
+    for (long long it = blockIdx.x; it < a.nitems; it += gridDim.x) {
+      const long long zs0 = (it / ntile) * a.zl;
+      const int tile = (int)(it % ntile);
+      const int y0 = (tile / a.ntx) * PL_TY, x0 = (tile % a.ntx) * PL_TX;
+      const long long ze = (zs0 + a.zl < a.nz) ? zs0 + a.zl : a.nz;
+      for (long long p = zs0 - 1; p <= ze; ++p, ++g) {
+        if (g >= NB) bwait(empty + st, ph ^ 1u);
+        const bool comp = p >= zs0 && p < ze;
+        const int ncp = (PL_TY + 2) + (comp ? PL_TY * (1 + ny) : 0);
+        unsigned myb = 0;
+        // descriptors (at most two per lane for the tile sizes used)
+        const void* src[2] = {nullptr, nullptr};
+        void* dst[2] = {nullptr, nullptr};
+        unsigned by[2] = {0, 0};
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int c = lane + 32 * u;
+          if (c >= ncp) break;
+          if (c < PL_TY + 2) {  // P line segment j = c of plane p
+            const long long lo = p * F + (long long)(y0 - 1 + c) * m + x0 - 1;
+            long long clo = lo < 0 ? 0 : lo, chi = lo + C::WX;
+            if (chi > n) chi = n;
+            if (chi > clo) {
+              by[u] = (unsigned)((chi - clo) * C::RB);
+              src[u] = P + (size_t)clo * C::RB;
+              dst[u] = win + ((size_t)st * C::WR + (size_t)c * C::WX + (size_t)(clo - lo)) * S;
+            }
+          } else {
+            const int c2 = c - (PL_TY + 2);
+            const int yl = c2 % PL_TY, kind = c2 / PL_TY;  // 0 values, 1.. staged vectors
+            if (y0 + yl < a.ny) {
+              const long long i0 = p * F + (long long)(y0 + yl) * m + x0;
+              long long cnt = m - x0 < PL_TX ? m - x0 : PL_TX;
+              if (i0 + cnt > n) cnt = n - i0;
+              if (cnt > 0) {
+                const long long a0 = (ESZ == 8) ? (i0 & ~1LL) : i0;  // 16-byte aligned source row
+                const long long rows = cnt + (i0 - a0);
+                if (kind == 0) {
+                  by[u] = (unsigned)(((rows * PL_K * ESZ) + 15) / 16 * 16);
+                  src[u] = dia + (size_t)a0 * PL_K * ESZ;
+                  dst[u] = vals + ((size_t)st * PL_TY + yl) * C::VL;
+                } else {
+                  int q = 0;
+                  for (int qq = 0; qq < 2; ++qq)
+                    if (yslot[qq] == kind - 1) q = qq;
+                  by[u] = (unsigned)(((rows * ESZ) + 15) / 16 * 16);
+                  src[u] = reinterpret_cast<const char*>(a.red[q].yext) + (size_t)a0 * ESZ;
+                  dst[u] = ybuf + (((size_t)st * ny + (kind - 1)) * PL_TY + yl) * C::YL;
+                }
+              }
+            }
+          }
+          myb += by[u];
+        }
+        const unsigned bytes = __reduce_add_sync(0xffffffffu, myb);
+        if (lane == 0)
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bsmem(full + st)), "r"(bytes)
+                       : "memory");
+        __syncwarp();
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+          if (by[u]) bcopy(dst[u], src[u], by[u], full + st);
+        if (++st == NB) {
+          st = 0;
+          ph ^= 1u;
+        }
+      }
+    }
+    return;
+  }
+
+  // -------------------------------------------------------------- consumers
+  const int cw = warp - 1;
+  const int g = lane % L::G;
+  const int slot = cw * L::RPW + lane / L::G;
+  RedAcc<T, S, false> acc0, acc1;
+  red_zero<T, S, false>(acc0);
+  red_zero<T, S, false>(acc1);
+  const int m0 = a.nred > 0 ? a.red[0].mode : RED_NONE;
+  const int m1 = a.nred > 1 ? a.red[1].mode : RED_NONE;
+  int st = 0;
+  unsigned ph = 0;
+  auto release = [&]() {
+    __syncwarp();
+    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bsmem(empty + st)) : "memory");
+    if (++st == NB) {
+      st = 0;
+      ph ^= 1u;
+    }
+  };
+  for (long long it = blockIdx.x; it < a.nitems; it += gridDim.x) {
+    const long long zs0 = (it / ntile) * a.zl;
+    const int tile = (int)(it % ntile);
+    const int y0 = (tile / a.ntx) * PL_TY, x0 = (tile % a.ntx) * PL_TX;
+    const long long ze = (zs0 + a.zl < a.nz) ? zs0 + a.zl : a.nz;
+    // this lane group's tile rows: (yl, xl) and the window offset of their centre row
+    int woff[RPL];
+    bool live[RPL];
+#pragma unroll
+    for (int k = 0; k < RPL; ++k) {
+      const int rr = slot + k * SLOTS;
+      const int yl = rr / PL_TX, xl = rr % PL_TX;
+      live[k] = rr < TROWS && y0 + yl < a.ny && x0 + xl < m;
+      woff[k] = rr < TROWS ? ((yl + 1) * C::WX + xl + 1) * S : (C::WX + 1) * S;  // (idle slots read row 0)
+    }
+    T prev[RPL][L::EPL], cur[RPL][L::EPL];
+    // window zs0 - 1: its centre rows are the -F neighbours of plane zs0
+    bwait(full + st, ph);
+    {
+      const T* w = win + (size_t)st * C::WR * S;
+#pragma unroll
+      for (int k = 0; k < RPL; ++k) row_load_ex_rw<T, S>(w + woff[k], g, prev[k]);
+    }
+    release();
+    bwait(full + st, ph);  // window zs0: centre rows
+    {
+      const T* w = win + (size_t)st * C::WR * S;
+#pragma unroll
+      for (int k = 0; k < RPL; ++k) row_load_ex_rw<T, S>(w + woff[k], g, cur[k]);
+    }
+    for (long long z = zs0; z < ze; ++z) {
+      const int cs = st;
+      int ns = st + 1;
+      unsigned nph = ph;
+      if (ns == NB) {
+        ns = 0;
+        nph ^= 1u;
+      }
+      bwait(full + ns, nph);  // window z + 1
+      const T* wc = win + (size_t)cs * C::WR * S;
+      const T* wn = win + (size_t)ns * C::WR * S;
+      const T* sv = vals + (size_t)cs * PL_TY * C::VL;
+      const T* sy = ybuf + (size_t)cs * ny * PL_TY * C::YL;
+#pragma unroll
+      for (int k = 0; k < RPL; ++k) {
+        const int rr = slot + k * SLOTS;
+        const int yl = rr / PL_TX, xl = rr % PL_TX;
+        T nx[L::EPL], pm[L::EPL], p1[L::EPL], q1[L::EPL], qm[L::EPL];
+        row_load_ex_rw<T, S>(wn + woff[k], g, nx);
+        row_load_ex_rw<T, S>(wc + woff[k] - C::WX * S, g, pm);
+        row_load_ex_rw<T, S>(wc + woff[k] - S, g, p1);
+        row_load_ex_rw<T, S>(wc + woff[k] + S, g, q1);
+        row_load_ex_rw<T, S>(wc + woff[k] + C::WX * S, g, qm);
+        if (live[k]) {
+          const long long i = z * F + (long long)(y0 + yl) * m + x0 + xl;
+          const long long i0 = z * F + (long long)(y0 + yl) * m + x0;
+          const int sh = (sizeof(T) == 8) ? (int)(i0 & 1) : 0;
+          const T* v = sv + (size_t)yl * C::VL + (size_t)(sh + xl) * PL_K;
+          T x[L::EPL];
+#pragma unroll
+          for (int e = 0; e < L::EPL; ++e) {
+            T acc = Ar<T>::zero();
+            acc = Ar<T>::fma(v[0], prev[k][e], acc);
+            acc = Ar<T>::fma(v[1], pm[e], acc);
+            acc = Ar<T>::fma(v[2], p1[e], acc);
+            acc = Ar<T>::fma(v[3], cur[k][e], acc);
+            acc = Ar<T>::fma(v[4], q1[e], acc);
+            acc = Ar<T>::fma(v[5], qm[e], acc);
+            acc = Ar<T>::fma(v[6], nx[e], acc);
+            x[e] = acc;
+          }
+          if (i < n) {
+            row_store_ex_cs<T, S>(reinterpret_cast<T*>(a.Q) + (size_t)i * S, g, x);
+            if (m0 != RED_NONE || m1 != RED_NONE) {
+#pragma unroll
+              for (int q = 0; q < 2; ++q) {
+                const int md = q ? m1 : m0;
+                if (md == RED_NONE) continue;
+                const int yk = red_ykind(md);
+                T yy[L::EPL];
+                const T yv = yk == 1 ? sy[((size_t)yslot[q] * PL_TY + yl) * C::YL + sh + xl] : Ar<T>::zero();
+#pragma unroll
+                for (int e = 0; e < L::EPL; ++e) yy[e] = yk == 0 ? x[e] : yv;
+                if (q == 0) red_acc<T, S, false>(acc0, x, yy);
+                else red_acc<T, S, false>(acc1, x, yy);
+              }
+            }
+          }
+        }
+#pragma unroll
+        for (int e = 0; e < L::EPL; ++e) {
+          prev[k][e] = cur[k][e];
+          cur[k][e] = nx[e];
+        }
+      }
+      release();  // window z (its last reader was this step)
+    }
+    release();  // window ze: only its centre rows were read
+  }
+  if (a.nred > 0) {
+    double* red_smem = reinterpret_cast<double*>(vals);  // the stages are no longer read
+    asm volatile("bar.sync 1, %0;" ::"r"(NW * 32) : "memory");
+    red_dispatch_flush<T, S, false>(m0, acc0, a.partials, a.pstride, a.red[0].poff, S, red_smem, 1, NW, 1);
+    if (a.nred > 1)
+      red_dispatch_flush<T, S, false>(m1, acc1, a.partials, a.pstride, a.red[1].poff, S, red_smem, 1, NW, 1);
+  }
+}
+
 // ---------------------------------------------------------------- host side
 template <typename T, int S>
 static int launch_band_t(const BandArgs& a0, int nsm, cudaStream_t st, int* grid_out) {
@@ -611,6 +916,83 @@ static int launch_band_t(const BandArgs& a0, int nsm, cudaStream_t st, int* grid
   return (int)cudaGetLastError();
 }
 
+
+// 7-point pattern {-F, -m, -1, 0, 1, m, F}, F a multiple of m (band_plane_kernel)
+bool band_plane_pattern(const Mat::Band& b) {
+  static const int env = getenv("SRK_BAND_PLANE") ? atoi(getenv("SRK_BAND_PLANE")) : 1;
+  if (!env || b.K != PL_K) return false;
+  const long long F = b.off[6], m = b.off[5];
+  if (b.off[0] != -F || b.off[1] != -m || b.off[2] != -1 || b.off[3] != 0 || b.off[4] != 1) return false;
+  return m >= 2 && F > m && F % m == 0;
+}
+
+template <typename T, int S>
+static int launch_plane_t(const BandArgs& ba, const Mat::Band& b, int nsm, cudaStream_t st, int* grid_out) {
+  constexpr int NW = 16;
+  PlaneArgs a{};
+  a.dia = ba.dia;
+  a.P = ba.P;
+  a.Q = ba.Q;
+  a.n = ba.n;
+  a.F = b.off[6];
+  a.m = b.off[5];
+  a.ny = (int)(a.F / a.m);
+  a.nz = (a.n + a.F - 1) / a.F;
+  a.ntx = (a.m + PL_TX - 1) / PL_TX;
+  a.nty = (a.ny + PL_TY - 1) / PL_TY;
+  a.nred = ba.nred;
+  int ny = 0;
+  for (int q = 0; q < a.nred; ++q) {
+    a.red[q] = ba.red[q];
+    const int md = a.red[q].mode;
+    const int yk = (md == RED_NORM2 || md == RED_COLNORM2) ? 0 : (md == RED_SUMVEC ? 1 : 2);
+    if (yk == 2) return (int)cudaErrorNotSupported;  // row operands: the band / CSR kernels
+    if (yk == 1 && (!a.red[q].yext || ((uintptr_t)a.red[q].yext & 15) || a.red[q].ysrc >= 0))
+      return (int)cudaErrorNotSupported;
+    a.ystage[q] = yk;
+    ny += yk;
+  }
+  a.partials = ba.partials;
+  a.pstride = ba.pstride;
+  a.done = ba.done;
+  static const int env_nb = getenv("SRK_PLANE_NB") ? atoi(getenv("SRK_PLANE_NB")) : 0;
+  a.NB = 0;
+  for (int nb = (env_nb >= 3 && env_nb <= PL_NBMAX) ? env_nb : PL_NBMAX; nb >= 3; --nb)
+    if (plane_smem<T, S>(nb, ny) <= 220 * 1024) {
+      a.NB = nb;
+      break;
+    }
+  if (!a.NB) return (int)cudaErrorNotSupported;
+  // plane segment length: fewest window loads per CTA (ceil(items / grid) rounds of ZL + 2
+  // windows), ties to the longer segment
+  const long long ntile = (long long)a.ntx * a.nty;
+  static const int env_zl = getenv("SRK_PLANE_ZL") ? atoi(getenv("SRK_PLANE_ZL")) : 0;
+  long long best = -1;
+  for (long long zl = 1; zl <= a.nz; ++zl) {
+    const long long nzs = (a.nz + zl - 1) / zl;
+    const long long items = ntile * nzs;
+    const long long grid = std::min<long long>(nsm, items);
+    const long long cost = (items + grid - 1) / grid * (zl + 2);
+    if (env_zl > 0 ? zl == std::min<long long>(env_zl, a.nz) : (best < 0 || cost <= best)) {
+      best = cost;
+      a.zl = (int)zl;
+    }
+  }
+  a.nzs = (int)((a.nz + a.zl - 1) / a.zl);
+  a.nitems = ntile * a.nzs;
+  const int grid = (int)std::min<long long>(nsm, a.nitems);
+  if (grid_out) {
+    *grid_out = grid;
+    return 0;
+  }
+  const size_t smem = plane_smem<T, S>(a.NB, ny);
+  static std::atomic<unsigned long long> attr{0};
+  if (first_on_device(attr))
+    cudaFuncSetAttribute(band_plane_kernel<T, S, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+  band_plane_kernel<T, S, NW><<<grid, 32 * (NW + 1), smem, st>>>(a);
+  return (int)cudaGetLastError();
+}
+
 bool band_supported(bool cplx, int s) {
   if (cplx) return s == 1 || s == 4 || s == 8;
   return s == 2 || s == 4 || s == 8 || s == 16;
@@ -627,6 +1009,33 @@ int launch_band(bool cplx, int s, const Mat::Band& b, const void* P, void* Q, lo
   a.dia = b.val;
   a.npad = b.npad;
   a.K = b.K;
+  if (band_plane_pattern(b)) {  // the 7-point pattern: the plane-marching kernel
+    BandArgs pa = a;
+    pa.P = P;
+    pa.Q = Q;
+    pa.n = n;
+    pa.nred = nred;
+    for (int i = 0; i < nred; ++i) pa.red[i] = red[i];
+    pa.partials = partials;
+    pa.pstride = pstride;
+    pa.done = done;
+    int r = (int)cudaErrorNotSupported;
+    if (cplx) {
+      switch (s) {
+        case 1: r = launch_plane_t<double2, 1>(pa, b, nsm, st, grid_out); break;
+        case 4: r = launch_plane_t<double2, 4>(pa, b, nsm, st, grid_out); break;
+        case 8: r = launch_plane_t<double2, 8>(pa, b, nsm, st, grid_out); break;
+      }
+    } else {
+      switch (s) {
+        case 2: r = launch_plane_t<double, 2>(pa, b, nsm, st, grid_out); break;
+        case 4: r = launch_plane_t<double, 4>(pa, b, nsm, st, grid_out); break;
+        case 8: r = launch_plane_t<double, 8>(pa, b, nsm, st, grid_out); break;
+        case 16: r = launch_plane_t<double, 16>(pa, b, nsm, st, grid_out); break;
+      }
+    }
+    if (r != (int)cudaErrorNotSupported) return r;
+  }
   const int hcap = band_hcap(s * (cplx ? 16 : 8));
   a.H = 0;
   for (int k = 0; k < b.K; ++k)

@@ -1029,14 +1029,26 @@ __device__ void small_gram(const CoefArgs& a, int slot, const T* Xb, const T* Yb
       for (int c = 0; c < SK; ++c)
         if (r < s && c < s) acc[r * SK + c] = Ar<T>::cfma(Yb[(size_t)i * s + r], Xb[(size_t)i * s + c], acc[r * SK + c]);
   }
+  // all s^2 entries at once: the same xor butterfly per entry, then the warps' values summed
+  // in warp order (bitwise cta_sum's result), with two CTA barriers instead of 2 s^2
+  // (red holds >= 32 values: the per-warp partials go to a private slice of shared memory)
 #pragma unroll
-  for (int r = 0; r < SK; ++r)
+  for (int q = 0; q < SK * SK; ++q)
+    for (int m = 16; m > 0; m >>= 1) acc[q] = Ar<T>::add(acc[q], Ar<T>::shfl_xor(acc[q], m));
+  __shared__ T wpart[(SK * SK) * 8];  // [warp][entry], up to 8 warps (the kernel runs 256 threads)
+  const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if ((threadIdx.x & 31) == 0)
 #pragma unroll
-    for (int c = 0; c < SK; ++c)
-      if (r < s && c < s) {
-        const T v = cta_sum(acc[r * SK + c], red);
-        if (threadIdx.x == 0) W<T>(a, slot)[r * s + c] = v;
-      }
+    for (int q = 0; q < SK * SK; ++q) wpart[w * SK * SK + q] = acc[q];
+  __syncthreads();
+  if (threadIdx.x < SK * SK) {
+    const int r = threadIdx.x / SK, c = threadIdx.x % SK;
+    if (r < s && c < s) {
+      T v = Ar<T>::zero();
+      for (int q = 0; q < nw; ++q) v = Ar<T>::add(v, wpart[q * SK * SK + threadIdx.x]);
+      W<T>(a, slot)[r * s + c] = v;
+    }
+  }
   __syncthreads();
 }
 

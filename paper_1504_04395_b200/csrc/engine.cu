@@ -211,8 +211,12 @@ int Eng::spmm(bool adj, const void* P, void* Q, int s, std::vector<RQ> reds) {
   // keep the CSR kernel unless SRK_BAND_ALL is set)
   const Mat::Band& bd = adj ? A->bandH : A->band;
   static const bool band_all = getenv("SRK_BAND_ALL") != nullptr;
-  bool yred = false;
-  for (auto& q : reds) yred |= (q.mode != RED_NORM2 && q.mode != RED_COLNORM2);
+  bool yred = false, yrow = false;
+  for (auto& q : reds) {
+    yred |= (q.mode != RED_NORM2 && q.mode != RED_COLNORM2);
+    yrow |= (q.mode != RED_NORM2 && q.mode != RED_COLNORM2 && q.mode != RED_SUMVEC);
+  }
+  if (yred && !yrow && bd.K > 0 && band_plane_pattern(bd)) yred = false;  // staged by the plane kernel
   if (bd.K > 0 && !full && (band_all || !yred) && A->ghost_rows() == 0 && band_supported(cplx, s) && reds.size() <= 2) {
     std::vector<Red> rr(reds.size());
     std::vector<int> poffs;
@@ -564,7 +568,13 @@ int Eng::spmm_prec(bool adj, const void* P, void* Q, int s, const std::vector<RQ
     return 0;
   };
   if (!adj) {
-    if (tri(M->L, P, T) || tri(M->U, T, T)) return err;
+    if (M->perm) {  // ILUTP: U^-1 L^-1 (Pi P)
+      nlaunch++;
+      if ((err = launch_permute(M->perm, true, cplx, n, s, P, T, c->st))) return err;
+      if (tri(M->L, T, T) || tri(M->U, T, T)) return err;
+    } else if (tri(M->L, P, T) || tri(M->U, T, T)) {
+      return err;
+    }
     raw = true;
     const int r = spmm(false, T, Q, s, reds);
     raw = false;
@@ -574,7 +584,13 @@ int Eng::spmm_prec(bool adj, const void* P, void* Q, int s, const std::vector<RQ
   int r = spmm(true, P, T, s, {});
   raw = false;
   if (r) return r;
-  if (tri(M->UH, T, T) || tri(M->LH, T, Q)) return err;
+  if (M->perm) {  // ILUTP: Pi^T L^-H U^-H (A^H P)
+    if (tri(M->UH, T, T) || tri(M->LH, T, T)) return err;
+    nlaunch++;
+    if ((err = launch_permute(M->perm, false, cplx, n, s, T, Q, c->st))) return err;
+  } else if (tri(M->UH, T, T) || tri(M->LH, T, Q)) {
+    return err;
+  }
   if (reds.empty()) return 0;
   std::vector<RQ> r2;
   for (const RQ& q : reds) r2.push_back(RQ{q.mode, 0, -1, q.yext, q.woff});
@@ -586,10 +602,37 @@ int Eng::prec_solve(bool adj, const void* Y, void* X, int s) {
   if (!M) return err = (int)cudaErrorInvalidValue;
   const DevTri& first = adj ? M->UH : M->L;
   const DevTri& second = adj ? M->LH : M->U;
-  int r = launch_trsv(first, cplx, n, s, Y, X, nullptr, c->st);
+  int r;
+  if (M->perm && !adj) {  // U^-1 L^-1 (Pi Y)
+    if (Y == X) {  // in place: the gather needs a copy of Y
+      void* T = nullptr;
+      const size_t bytes = (size_t)n * s * (cplx ? 16 : 8);
+      if (cudaMalloc(&T, bytes) != cudaSuccess) return err = (int)cudaErrorMemoryAllocation;
+      cudaMemcpyAsync(T, Y, bytes, cudaMemcpyDeviceToDevice, c->st);
+      r = launch_permute(M->perm, true, cplx, n, s, T, X, c->st);
+      cudaStreamSynchronize(c->st);
+      cudaFree(T);
+    } else {
+      r = launch_permute(M->perm, true, cplx, n, s, Y, X, c->st);
+    }
+    if (r) return err = r;
+    r = launch_trsv(first, cplx, n, s, X, X, nullptr, c->st);
+  } else {
+    r = launch_trsv(first, cplx, n, s, Y, X, nullptr, c->st);
+  }
   if (r < 0) return err = -r;
   r = launch_trsv(second, cplx, n, s, X, X, nullptr, c->st);
   if (r < 0) return err = -r;
+  if (M->perm && adj) {  // Pi^T (L^-H U^-H Y)
+    void* T = nullptr;
+    const size_t bytes = (size_t)n * s * (cplx ? 16 : 8);
+    if (cudaMalloc(&T, bytes) != cudaSuccess) return err = (int)cudaErrorMemoryAllocation;
+    cudaMemcpyAsync(T, X, bytes, cudaMemcpyDeviceToDevice, c->st);
+    r = launch_permute(M->perm, false, cplx, n, s, T, X, c->st);
+    cudaStreamSynchronize(c->st);
+    cudaFree(T);
+    if (r) return err = r;
+  }
   return 0;
 }
 
@@ -601,6 +644,10 @@ int Eng::prec_mul(const void* X, void* Y, int s) {  // Y = L (U X)
   if (cudaMalloc(&T, bytes) != cudaSuccess) return err = (int)cudaErrorMemoryAllocation;
   int r = launch_trimul(M->U, cplx, n, s, X, T, c->st);
   if (!r) r = launch_trimul(M->L, cplx, n, s, T, Y, c->st);
+  if (!r && M->perm) {  // ILUTP: M X = Pi^T (L U X)
+    cudaMemcpyAsync(T, Y, bytes, cudaMemcpyDeviceToDevice, c->st);
+    r = launch_permute(M->perm, false, cplx, n, s, T, Y, c->st);
+  }
   cudaStreamSynchronize(c->st);
   cudaFree(T);
   return err = r;

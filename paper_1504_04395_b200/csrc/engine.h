@@ -69,6 +69,11 @@ struct Prec {
   bool cplx = false;
   DevTri L, U, UH, LH;
   std::vector<double> factor;  // the factor values on A's pattern (host copy, for parity tests)
+  // ILUTP (kind 1): M = Pi^T L U; perm[k] = the row of A pivoted at step k (device, null when
+  // no row moved); host copies of the factor's pivot-order CSR and of perm, for tests
+  int kind = 0;
+  int* perm = nullptr;
+  std::vector<int> frp, fci, hperm;
   void* scratch[2] = {nullptr, nullptr};
   size_t scratch_bytes = 0;
 };
@@ -127,6 +132,7 @@ struct Mat {
 // banded operators (band.cu): detection + diagonal storage at a0, the bulk-copy SpMM
 int build_band(bool cplx, long long n, const int* rp, const int* ci, const void* val, Mat::Band& b, cudaStream_t st);
 bool band_supported(bool cplx, int s);
+bool band_plane_pattern(const Mat::Band& b);  // 7-point operators: band_plane_kernel (takes SUMVEC epilogues)
 int launch_band(bool cplx, int s, const Mat::Band& b, const void* P, void* Q, long long n, const Red* red, int nred,
                 double* partials, int pstride, const int* done, int nsm, cudaStream_t st, int* grid_out);
 
@@ -135,6 +141,7 @@ int build_balanced_order(Mat& m, bool adj, cudaStream_t st);
 void free_balanced_order(Mat& m);
 int build_halo_split(Mat& m, bool adj, cudaStream_t st);  // interior / boundary rows (dist operators)
 
+int build_ilutp(Mat& m, double droptol, double thresh, cudaStream_t st);  // as build_ilu0
 int build_ilu0(Mat& m, cudaStream_t st);  // 0, or 1 zero pivot / 2 out of memory / 3 CUDA error
 void free_prec(Prec* p);
 // Z = T^-1 R for one triangular factor (n x s row-major blocks; Z may alias R); returns
@@ -142,6 +149,8 @@ void free_prec(Prec* p);
 int launch_trsv(const DevTri& t, bool cplx, long long n, int s, const void* R, void* Z, const int* done, cudaStream_t st);
 // Z = T R (the factor itself, diagonal included; Z must not alias R)
 int launch_trimul(const DevTri& t, bool cplx, long long n, int s, const void* R, void* Z, cudaStream_t st);
+int launch_permute(const int* perm, bool gather, bool cplx, long long n, int s, const void* src, void* dst,
+                   cudaStream_t st);
 
 // reduction request: X = source (or the SpMM output), Y = source or external
 struct RQ {

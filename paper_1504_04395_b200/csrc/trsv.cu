@@ -180,6 +180,29 @@ int launch_trsv(const DevTri& t, bool cplx, long long n, int s, const void* R, v
   return cplx ? run<double2>(t, n, s, R, Z, done, st) : run<double>(t, n, s, R, Z, done, st);
 }
 
+// ILUTP row permutation of an n x s block (rows of w doubles): gather dst[k] = src[perm[k]]
+// (Pi P, before the L solve) or scatter dst[perm[k]] = src[k] (Pi^T, after the L^H solve)
+__global__ static void permute_kernel(const int* __restrict__ perm, int gather, long long n, int w,
+                                      const double* __restrict__ src, double* __restrict__ dst) {
+  const long long tot = n * (long long)w;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < tot; e += (long long)gridDim.x * blockDim.x) {
+    const long long k = e / w, c = e % w;
+    const long long r = perm[k];
+    if (gather) dst[k * w + c] = src[r * w + c];
+    else dst[r * w + c] = src[k * w + c];
+  }
+}
+
+int launch_permute(const int* perm, bool gather, bool cplx, long long n, int s, const void* src, void* dst,
+                   cudaStream_t st) {
+  const int w = s * (cplx ? 2 : 1);
+  const long long tot = n * (long long)w;
+  const int grid = (int)std::max<long long>(1, std::min<long long>((tot + 255) / 256, 148LL * 16));
+  permute_kernel<<<grid, 256, 0, st>>>(perm, gather ? 1 : 0, n, w, reinterpret_cast<const double*>(src),
+                                       reinterpret_cast<double*>(dst));
+  return (int)cudaGetLastError();
+}
+
 int launch_trimul(const DevTri& t, bool cplx, long long n, int s, const void* R, void* Z, cudaStream_t st) {
   const int grid = (int)((n + 7) / 8);
   if (cplx)

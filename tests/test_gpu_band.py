@@ -133,3 +133,103 @@ def test_band_equals_csr_kernel_solver(srk):
         sv.iterate(1)
         assert rel(to_np(sv.x()), a.Xs[k]) <= 1e-10, k
     sv.close()
+
+
+# ---------------------------------------------------------------- plane-marching kernel
+def _seven_point(m, ny, nplanes_extra, seed, cplx=False):
+    """A random matrix on exactly the diagonals {-F, -m, -1, 0, 1, m, F}, F = m ny, with
+    n = F * nz + a ragged tail (n not a multiple of F) and nonzero values where a grid
+    stencil would have none (row-index semantics across line / plane ends)."""
+    F = m * ny
+    n = F * nplanes_extra[0] + nplanes_extra[1]
+    rng = np.random.default_rng(seed)
+    offs = [-F, -m, -1, 0, 1, m, F]
+    diags = []
+    for d in offs:
+        L = n - abs(d)
+        v = rng.standard_normal(L)
+        if cplx:
+            v = v + 1j * rng.standard_normal(L)
+        diags.append(v)
+    A = sp.diags(diags, offs, shape=(n, n), format="csr", dtype=np.complex128 if cplx else np.float64)
+    A.sort_indices()
+    return A
+
+
+def _plane_ops():
+    return {
+        "even": _seven_point(34, 10, (5, 17), 1),            # ragged x (34 = 32 + 2) and y (10 = 6 + 4) tiles, tail plane
+        "odd": _seven_point(21, 7, (6, 0), 2),               # odd m: shifted value / vector copies
+        "cplx": _seven_point(18, 13, (4, 101), 3, True),     # complex, m < tile width
+        "cube": synth.conv_diff_3d(40, (50.0, 30.0, 10.0)),  # a grid stencil (zero values at the edges)
+    }
+
+
+@pytest.mark.parametrize("adj", [False, True])
+@pytest.mark.parametrize("name", ["even", "odd", "cplx", "cube"])
+def test_plane_spmm_matches_oracle_product(srk, name, adj):
+    """The 7-point plane-marching kernel against the CSR product for every supported width,
+    A and A^H, with the fused norm / column-norm / vector-sum epilogues."""
+    A = _plane_ops()[name]
+    As = A.to_scipy() if hasattr(A, "to_scipy") else A
+    cplx = As.dtype == np.complex128
+    op = As.conj().T.tocsr() if adj else As
+    M = srk.Matrix.from_csr(A)
+    assert M.format(adjoint=adj) == ("band", 7)
+    n = As.shape[0]
+    for s in ((1, 4, 8) if cplx else (2, 4, 8, 16)):
+        P = synth.random_rhs(n, s, s + 3, cplx)
+        R = op @ P
+        Q = to_np(srk.spmm_block(M, to_dev(P), adjoint=adj))
+        assert rel(Q, R) <= 1e-14, (name, adj, s, rel(Q, R))
+        y = synth.random_rhs(n, 1, s + 7, cplx)[:, 0].copy()
+        for gram, ref, mag in (("norm2", [np.vdot(R, R).real], np.vdot(R, R).real),
+                               ("colnorm2", np.sum(np.abs(R) ** 2, axis=0), np.sum(np.abs(R) ** 2, axis=0)),
+                               ("sumvec", [np.sum(y.conj()[:, None] * R)], np.sum(np.abs(y)[:, None] * np.abs(R)))):
+            Q2, gv = srk.spmm_block(M, to_dev(P), adjoint=adj, gram=gram, Y=to_dev(y) if gram == "sumvec" else None)
+            assert rel(to_np(Q2), R) <= 1e-14, (name, gram)
+            # summation-order rounding: bounded by the sum of the terms' magnitudes (the vector
+            # sum cancels, so a bound relative to the result alone would be order dependent)
+            assert np.all(np.abs(to_np(gv).ravel() - np.asarray(ref).ravel()) <= 1e-13 * np.asarray(mag).ravel()), \
+                (name, adj, s, gram)
+
+
+_PLANE_VS_RING = r"""
+import sys, numpy as np
+sys.path.insert(0, {root!r})
+import synth, paper_1504_04395_b200 as srk
+from tests.gpu_util import to_dev, to_np
+from tests.test_gpu_band import _plane_ops
+srk.load_library()
+out = {{}}
+for name, A in _plane_ops().items():
+    M = srk.Matrix.from_csr(A)
+    n = M.n
+    cplx = name == "cplx"
+    for s in ((1, 4, 8) if cplx else (2, 4, 8, 16)):
+        P = synth.random_rhs(n, s, s + 3, cplx)
+        for adj in (False, True):
+            out[f"{{name}}_{{s}}_{{int(adj)}}"] = to_np(srk.spmm_block(M, to_dev(P), adjoint=adj))
+np.savez({path!r}, **out)
+print("PLANE_DUMP_OK")
+"""
+
+
+def test_plane_kernel_bitwise_equals_ring_kernel(tmp_path):
+    """Same summation order (ascending offset, FMA chain from zero) as the ring / far-window
+    band kernel: the two products are bitwise equal (SRK_BAND_PLANE=0 selects the ring one)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for flag in ("1", "0"):
+        path = str(tmp_path / f"q{flag}.npz")
+        out = subprocess.run([sys.executable, "-c", _PLANE_VS_RING.format(root=root, path=path)],
+                             env={**os.environ, "SRK_BAND_PLANE": flag}, capture_output=True, text=True,
+                             timeout=600, cwd=root)
+        assert "PLANE_DUMP_OK" in out.stdout, out.stderr[-2000:]
+        res[flag] = dict(np.load(path))
+    assert res["1"].keys() == res["0"].keys()
+    for k in res["1"]:
+        assert np.array_equal(res["1"][k], res["0"][k]), k

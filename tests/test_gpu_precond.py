@@ -143,3 +143,98 @@ def test_precond_apply_large_many_levels(srk):
                          capture_output=True, timeout=600)
     Zl = np.frombuffer(out.stdout, dtype=np.float64).reshape(Z.shape)
     assert np.array_equal(Z, Zl)
+
+
+# ------------------------------------------------------------- ILUTP (R14)
+def _pivoting_sparse(n, seed, cplx=False):
+    """Sparse, nonsymmetric, weak diagonal: partial pivoting moves rows (as in the oracle pins)."""
+    import scipy.sparse as sp
+    rng = np.random.default_rng(seed)
+    A = sp.random(n, n, density=6.0 / n, random_state=rng, format="csr")
+    if cplx:
+        A = A + 1j * sp.random(n, n, density=6.0 / n, random_state=rng, format="csr")
+    A = A + sp.diags(0.05 * rng.standard_normal(n)) + sp.diags(np.ones(n - 1), -1) + 2.0 * sp.identity(n)
+    A = sp.csr_matrix(A)
+    A.sort_indices()
+    return A
+
+
+def _ilutp_ops():
+    import scipy.sparse as sp
+    weak = _pivoting_sparse(400, 21)
+    weak = sp.csr_matrix(weak - 2.0 * sp.identity(400))  # weak diagonal: rows move
+    weak.sort_indices()
+    return {
+        "pivot": weak,
+        "pivot_c": _pivoting_sparse(300, 22, True),
+        "lattice": synth.lattice_4d(4, kappa=0.12, seed=3).to_scipy(),  # Ex. 4's operator at 4^4
+    }
+
+
+@pytest.mark.parametrize("name", ["pivot", "pivot_c", "lattice"])
+def test_ilutp_factor_matches_oracle(srk, name):
+    """The library's ILUTP (host factorisation) against the oracle's: the same pivot order
+    and the same L, U entries (to rounding)."""
+    A = _ilutp_ops()[name]
+    M = srk.Matrix.from_csr(A, need_adjoint=True).ilutp(5e-2)
+    L, U, perm = OP.ilutp(A, 5e-2)
+    Lg, Ug, pg = M.ilutp_factor()
+    kind, nz, pivoted = M.prec_info()
+    assert kind == "ilutp" and pivoted == bool(np.any(perm != np.arange(A.shape[0])))
+    assert np.array_equal(pg, perm)
+    assert (Lg != 0).sum() == (L != 0).sum() and (Ug != 0).sum() == (U != 0).sum()
+    assert rel(Lg.toarray(), L.toarray()) <= 1e-12 and rel(Ug.toarray(), U.toarray()) <= 1e-12
+    if name == "pivot":
+        assert pivoted
+
+
+@pytest.mark.parametrize("name", ["pivot", "pivot_c", "lattice"])
+def test_ilutp_apply_matches_oracle(srk, name):
+    """Z = M^-1 P = U^-1 L^-1 (Pi P) and M^-H P = Pi^T L^-H U^-H P on the device (the row
+    permutation kernels around the level-scheduled solves) against the oracle's, from the
+    oracle's factor."""
+    A = _ilutp_ops()[name]
+    cplx = A.dtype == np.complex128
+    M = srk.Matrix.from_csr(A, need_adjoint=True).ilutp(5e-2)
+    L, U, perm = OP.ilutp(A, 5e-2)
+    for s in (1, 4, 7):
+        P = synth.random_rhs(A.shape[0], s, s, cplx)
+        Z = to_np(srk.precond_apply(M, to_dev(P)))
+        assert rel(Z, OP.apply_inv(L, U, P, perm)) <= 1e-11, (name, s)
+        ZH = to_np(srk.precond_apply(M, to_dev(P), adjoint=True))
+        assert rel(ZH, OP.apply_inv_adj(L, U, P, perm)) <= 1e-11, (name, s)
+
+
+@pytest.mark.parametrize("method", ["gl_bicgstab", "bl_bicgstab_rq", "egl_qmr", "bl_bicg_rq"])
+def test_ilutp_preconditioned_lockstep(srk, method):
+    """Right-ILUTP-preconditioned iterates in lock step with the oracle on a pivoting operator
+    (X_k = M^-1 Y_k, M = Pi^T L U; A^H products through M^-H), then the full solve on Ex. 4's
+    lattice operator (preconditioning reduces the iteration count)."""
+    import oracle
+    A = _ilutp_ops()["pivot"]
+    B = synth.random_rhs(A.shape[0], 4, 3)
+    L, U, perm = OP.ilutp(A, 5e-2)
+    a = OP.solve_right(method, A, B, L, U, perm, tol=1e-10, maxit=300, record=10, order="blas")
+    b = OP.solve_right(method, A, B, L, U, perm, tol=1e-10, maxit=300, record=10, order="seq")
+    d = [rel(x, y) for x, y in zip(a.Xs, b.Xs)]
+    env = np.maximum(1e-10, 100 * np.maximum.accumulate(d)) if d else np.array([])
+    M = srk.Matrix.from_csr(A, need_adjoint=srk.NEEDS_ADJOINT[method]).ilutp(5e-2)
+    sv = srk.Solver(M, 4, method, tol=1e-10, maxit=300, poll_every=1)
+    sv.start(to_dev(B))
+    for k in range(min(10, len(a.Xs))):
+        st = sv.iterate(1)
+        assert rel(to_np(sv.x()), a.Xs[k]) <= env[k], (method, k + 1)
+        if st != 0:
+            break
+    sv.close()
+    Al = _ilutp_ops()["lattice"]
+    Bl = synth.random_rhs(Al.shape[0], 4, 0, True)
+    Ml = srk.Matrix.from_csr(Al, need_adjoint=srk.NEEDS_ADJOINT[method]).ilutp(5e-2)
+    Lq, Uq, pq = OP.ilutp(Al, 5e-2)
+    ref = OP.solve_right(method, Al, Bl, Lq, Uq, pq, tol=1e-8, maxit=500, record=0)
+    plain = oracle.solve(method, Al, Bl, tol=1e-8, maxit=500, record=0)
+    X, rep = srk.solve(Ml, to_dev(Bl), method, tol=1e-8, maxit=500)
+    assert rep.outcome == ref.outcome == "converged"
+    assert abs(rep.iterations - ref.iterations) <= max(2, 0.05 * ref.iterations)
+    assert rep.iterations < plain.iterations
+    assert np.linalg.norm(Bl - Al @ to_np(X)) / np.linalg.norm(Bl) <= 1e-8
