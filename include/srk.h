@@ -129,6 +129,18 @@ int srk_matrix_create(srk_ctx* ctx, const srk_csr* A, int need_adjoint, srk_matr
 int srk_matrix_create_bsr(srk_ctx* ctx, int64_t nb, int bs, int64_t nnzb, const int64_t* block_row_ptr,
                           const int32_t* block_col, const void* values, int dtype, int unit_diag,
                           srk_matrix** out);
+/* Traversal hint for a block-sparse operator (a1; the read-A-once product of P:66-74 reads
+ * every P row once only if its readers run close together in time): order_host (HOST array,
+ * n = nb entries, a permutation of the block rows) is the order in which the product's warps
+ * visit the block rows; null restores the natural order. Only the schedule changes: every entry
+ * of Q is the same sum in the same order, so Q is bitwise independent of the hint (fused
+ * reductions are summed in visiting order: deterministic, equal to rounding). For the
+ * lexicographic 4D lattice of config 4 (site = x + L y + L^2 z + L^3 t) an order that walks
+ * z-tiles of w planes through all t before the next tile brings the +-t neighbours within w
+ * planes of each other (synth.lattice_tile_order). Not supported on distributed operators'
+ * ghost rows (local rows only). Errors: SRK_EINVAL (not a permutation), SRK_EDIM (n != nb),
+ * SRK_EUNSUPPORTED (not block-sparse), SRK_ENOMEM. */
+int srk_matrix_set_row_order(srk_matrix* A, const int32_t* order_host, int64_t n);
 /* Right ILU(0) preconditioning (the
  * no-fill incomplete LU of A, M = L U, computed once on the host from the operator's
  * CSR and attached to it). Every later solve with this operator iterates on
@@ -231,6 +243,16 @@ int srk_matrix_create_dist(srk_ctx* ctx, const srk_csr* A_local, int64_t n_ghost
  * of band.cu; *ndiag = the diagonal count), 3 BSR-12. adjoint = 1: A^H's storage.
  * Errors: SRK_EINVAL (null matrix, adjoint without A^H). */
 int srk_matrix_format(const srk_matrix* A, int adjoint, int* ndiag);
+
+/* SELL-32-sigma form of op(A) (a0, SURVEY §8(a) "convert to SELL-C-sigma"; the read-A-once
+ * product of P:66-74 for narrow blocks): built beside the length-sorted CSR when the row lengths
+ * are irregular (max >= 4 mean + 8) and the padding stays under 25% of nnz — rows sorted by
+ * decreasing length inside windows of sigma rows, chunks of C = 32 rows stored column-major and
+ * padded to the chunk's longest row. Products with s * esz <= 32 bytes (one row per lane) use it;
+ * wider blocks keep the lane-group CSR kernel. Returns 1 when the form exists (then *nchunk =
+ * chunks, *entries = stored entries including padding, *sigma = the window; any may be null),
+ * 0 when it does not. Errors: SRK_EINVAL (null matrix, adjoint without A^H). */
+int srk_matrix_sell_info(const srk_matrix* A, int adjoint, int64_t* nchunk, int64_t* entries, int* sigma);
 
 /* Distributed BSR-12 operator (config 4's lattice split into t-slabs): this
  * rank's nb_local block rows (DEVICE arrays, block columns renumbered as srk_plan_create does

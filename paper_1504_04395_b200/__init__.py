@@ -37,7 +37,7 @@ EXPORTS = ("srk_create", "srk_destroy", "srk_last_error", "srk_version", "srk_ma
            "srk_solver_profile_read", "srk_solver_profile_launches", "srk_partition_rows", "srk_plan_create", "srk_plan_sizes", "srk_plan_arrays",
            "srk_plan_destroy", "srk_nccl_unique_id", "srk_comm_init", "srk_matrix_create_dist",
            "srk_vgroup_create", "srk_vgroup_destroy", "srk_comm_init_virtual", "srk_csr_adjoint_host",
-           "srk_matrix_format", "srk_matrix_create_bsr_dist",
+           "srk_matrix_format", "srk_matrix_sell_info", "srk_matrix_set_row_order", "srk_matrix_create_bsr_dist",
            "srk_matrix_create_bsr", "srk_matrix_ilu0", "srk_matrix_ilu0_factor", "srk_precond_apply",
            "srk_matrix_ilutp", "srk_matrix_prec_info", "srk_matrix_ilutp_factor")
 
@@ -129,6 +129,8 @@ def load_library(path: str | None = None):
         "srk_comm_init": ([vp, vp, i, i], i),
         "srk_vgroup_create": ([i, ctypes.POINTER(vp)], i),
         "srk_matrix_format": ([vp, i, ctypes.POINTER(i)], i),
+        "srk_matrix_sell_info": ([vp, i, ctypes.POINTER(i64), ctypes.POINTER(i64), ctypes.POINTER(i)], i),
+        "srk_matrix_set_row_order": ([vp, vp, i64], i),
         "srk_matrix_create_bsr_dist": ([vp, i64, i, i64, vp, vp, vp, i, i, i64, ctypes.POINTER(_Halo),
                                         ctypes.POINTER(vp)], i),
         "srk_vgroup_destroy": ([vp], i),
@@ -275,6 +277,24 @@ class Matrix:
         f = _lib.srk_matrix_format(self.h, int(adjoint), ctypes.byref(nd))
         _check(min(f, 0), "srk_matrix_format")
         return self.FORMATS[f], nd.value
+
+    def set_row_order(self, order=None):
+        """Visiting order of a block-sparse operator's block rows (srk_matrix_set_row_order):
+        a host int32 permutation, or None for the natural order; returns self."""
+        if order is None:
+            _check(_lib.srk_matrix_set_row_order(self.h, None, 0), "srk_matrix_set_row_order")
+            return self
+        o = np.ascontiguousarray(order, dtype=np.int32)
+        _check(_lib.srk_matrix_set_row_order(self.h, o.ctypes.data_as(ctypes.c_void_p), o.size), "srk_matrix_set_row_order")
+        return self
+
+    def sell_info(self, adjoint: bool = False):
+        """None, or (chunks, stored entries incl. padding, sigma) of the SELL-32-sigma form
+        narrow products of A (or A^H) use (srk_matrix_sell_info)."""
+        nc, ne, sg = ctypes.c_int64(0), ctypes.c_int64(0), ctypes.c_int(0)
+        f = _lib.srk_matrix_sell_info(self.h, int(adjoint), ctypes.byref(nc), ctypes.byref(ne), ctypes.byref(sg))
+        _check(min(f, 0), "srk_matrix_sell_info")
+        return (nc.value, ne.value, sg.value) if f == 1 else None
 
     def ilu0(self):
         """Attach the right ILU(0) preconditioner (srk_matrix_ilu0); returns self."""

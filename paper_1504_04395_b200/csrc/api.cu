@@ -487,6 +487,40 @@ int srk_matrix_format(const srk_matrix* M, int adjoint, int* ndiag) {
   return 0;
 }
 
+int srk_matrix_set_row_order(srk_matrix* M, const int32_t* order_host, int64_t n) {
+  if (!M) return fail(SRK_EINVAL, "srk_matrix_set_row_order: null matrix");
+  Mat& m = M->m;
+  if (!m.bsr) return fail(SRK_EUNSUPPORTED, "srk_matrix_set_row_order: block-sparse operators only");
+  if (m.border) {
+    cudaFree(m.border);
+    m.border = nullptr;
+  }
+  if (!order_host) return SRK_OK;  // back to the natural order
+  if (n != m.nb) return fail(SRK_EDIM, "srk_matrix_set_row_order: the order must list every block row");
+  std::vector<char> seen((size_t)n, 0);
+  for (int64_t k = 0; k < n; ++k) {
+    const int32_t r = order_host[k];
+    if (r < 0 || r >= n || seen[(size_t)r]) return fail(SRK_EINVAL, "srk_matrix_set_row_order: not a permutation");
+    seen[(size_t)r] = 1;
+  }
+  if (cudaMalloc(&m.border, sizeof(int) * (size_t)n) != cudaSuccess) {
+    m.border = nullptr;
+    return fail(SRK_ENOMEM, "srk_matrix_set_row_order: out of device memory");
+  }
+  cudaError_t e = cudaMemcpy(m.border, order_host, sizeof(int) * (size_t)n, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return cuda_fail(e, "srk_matrix_set_row_order");
+  return SRK_OK;
+}
+
+int srk_matrix_sell_info(const srk_matrix* M, int adjoint, int64_t* nchunk, int64_t* entries, int* sigma) {
+  if (!M || (adjoint && !M->m.has_adj)) return fail(SRK_EINVAL, "srk_matrix_sell_info: bad argument");
+  const Mat::Sell& se = adjoint ? M->m.sellH : M->m.sell;
+  if (nchunk) *nchunk = se.nchunk;
+  if (entries) *entries = se.entries;
+  if (sigma) *sigma = se.sigma;
+  return se.cs != nullptr ? 1 : 0;
+}
+
 int srk_matrix_destroy(srk_matrix* M) {
   if (!M) return SRK_OK;
   Mat& m = M->m;
@@ -494,6 +528,7 @@ int srk_matrix_destroy(srk_matrix* M) {
     srk_ctx* owner = reinterpret_cast<srk_ctx*>(m.ctx);
     if (owner->cached_mat == M->id) drop_cache(owner);
   }
+  if (m.border) cudaFree(m.border);
   if (m.rp) cudaFree(m.rp);
   if (m.ci) cudaFree(m.ci);
   if (m.val) cudaFree(m.val);

@@ -677,6 +677,102 @@ struct TeamRed {  // one reduction's accumulators in a team leader
   T f[W][W];      // FULL: f[k][c] += conj(y_k) q_c
 };
 
+
+// one finished row of a narrow-width product (team or SELL kernel): store it and add its terms to
+// the fused reductions of the lane that owns it
+template <typename T, int W, bool EX>
+__device__ __forceinline__ void narrow_row_out(const T (&q)[W], long long row, int s, T* __restrict__ Q,
+                                               const int (&rmode)[2], const T* (&ry)[2], TeamRed<T, W> (&acc)[2]) {
+  T* dst = Q + (size_t)row * (EX ? W : s);
+#pragma unroll
+  for (int e = 0; e < W; ++e)
+    if (EX || e < s) dst[e] = q[e];
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    const int md = rmode[r];
+    if (md == RED_NONE) continue;
+    if (md == RED_NORM2) {
+#pragma unroll
+      for (int e = 0; e < W; ++e) acc[r].v[0] = Ar<T>::cfma(q[e], q[e], acc[r].v[0]);
+    } else if (md == RED_COLNORM2) {
+#pragma unroll
+      for (int e = 0; e < W; ++e) acc[r].v[e] = Ar<T>::cfma(q[e], q[e], acc[r].v[e]);
+    } else if (md == RED_SUMVEC) {
+      const T y = ry[r][row];
+#pragma unroll
+      for (int e = 0; e < W; ++e) acc[r].v[0] = Ar<T>::cfma(y, q[e], acc[r].v[0]);
+    } else {
+      T y[W];
+      const T* ys = ry[r] + (size_t)row * (EX ? W : s);
+#pragma unroll
+      for (int e = 0; e < W; ++e) y[e] = (EX || e < s) ? ys[e] : Ar<T>::zero();
+      if (md == RED_FULL) {
+#pragma unroll
+        for (int k = 0; k < W; ++k)
+#pragma unroll
+          for (int c = 0; c < W; ++c) acc[r].f[k][c] = Ar<T>::cfma(y[k], q[c], acc[r].f[k][c]);
+      } else if (md == RED_TRACE) {
+#pragma unroll
+        for (int e = 0; e < W; ++e) acc[r].v[0] = Ar<T>::cfma(y[e], q[e], acc[r].v[0]);
+      } else {
+#pragma unroll
+        for (int e = 0; e < W; ++e) acc[r].v[e] = Ar<T>::cfma(y[e], q[e], acc[r].v[e]);
+      }
+    }
+  }
+}
+
+// CTA partials of the narrow-width kernels: the lanes that own rows (every FIRST-th lane) are
+// summed by a fixed xor butterfly, then the warps in index order
+template <typename T, int W, int FIRST>
+__device__ __forceinline__ void narrow_flush(const SpmmArgs& a, int s, const int (&rmode)[2], TeamRed<T, W> (&acc)[2],
+                                             double* smem) {
+  constexpr int ND = Ar<T>::ND;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    if (r >= a.nred) break;
+    const int md = rmode[r];
+    const int len = red_len(md, s, ND == 2);
+    double* w = smem + (size_t)warp * len;
+#pragma unroll
+    for (int m = FIRST; m < 32; m <<= 1)
+#pragma unroll
+      for (int c = 0; c < W; ++c) {
+        acc[r].v[c] = Ar<T>::add(acc[r].v[c], Ar<T>::shfl_xor(acc[r].v[c], m));
+#pragma unroll
+        for (int k = 0; k < W; ++k) acc[r].f[k][c] = Ar<T>::add(acc[r].f[k][c], Ar<T>::shfl_xor(acc[r].f[k][c], m));
+      }
+    if (lane == 0) {
+      if (md == RED_NORM2) w[0] = re_of(acc[r].v[0]);
+      else if (md == RED_TRACE || md == RED_SUMVEC) Ar<T>::st(w, acc[r].v[0]);
+      else if (md == RED_COLNORM2) {
+#pragma unroll
+        for (int c = 0; c < W; ++c)
+          if (c < s) w[c] = re_of(acc[r].v[c]);
+      } else if (md == RED_DIAG) {
+#pragma unroll
+        for (int c = 0; c < W; ++c)
+          if (c < s) Ar<T>::st(w + c * ND, acc[r].v[c]);
+      } else {
+#pragma unroll
+        for (int k = 0; k < W; ++k)
+#pragma unroll
+          for (int c = 0; c < W; ++c)
+            if (k < s && c < s) Ar<T>::st(w + (k * s + c) * ND, acc[r].f[k][c]);
+      }
+    }
+    __syncthreads();
+    const int nw = blockDim.x >> 5;
+    for (int j = threadIdx.x; j < len; j += blockDim.x) {
+      double sum = 0.0;
+      for (int q2 = 0; q2 < nw; ++q2) sum += smem[q2 * len + j];
+      a.partials[(size_t)blockIdx.x * a.pstride + a.red[r].poff + j] = sum;
+    }
+    __syncthreads();
+  }
+}
+
 template <typename T, int W, int TEAM, int R, bool EX>
 __global__ void __launch_bounds__(256, W * sizeof(T) >= 32 ? 2 : 4) spmv_team_kernel(SpmmArgs a) {
   if (a.done && *a.done) return;
@@ -748,6 +844,9 @@ __global__ void __launch_bounds__(256, W * sizeof(T) >= 32 ? 2 : 4) spmv_team_ke
     for (int i = 0; i < R; ++i)
 #pragma unroll
       for (int e = 0; e < W; ++e) q[i][e] = Ar<T>::zero();
+#ifdef TEAM_UNROLL1
+#pragma unroll 1
+#endif
     for (int j = t; j < maxlen; j += TEAM) {
       int cj[R];
       T vj[R];
@@ -776,92 +875,112 @@ __global__ void __launch_bounds__(256, W * sizeof(T) >= 32 ? 2 : 4) spmv_team_ke
 #pragma unroll
       for (int i = 0; i < R; ++i) {
         if (r0 + i >= n) continue;
-        const long long row = orow[i];
-        T* dst = Q + (size_t)row * (EX ? W : s);
-#pragma unroll
-        for (int e = 0; e < W; ++e)
-          if (EX || e < s) dst[e] = q[i][e];
-#pragma unroll
-        for (int r = 0; r < 2; ++r) {
-          const int md = rmode[r];
-          if (md == RED_NONE) continue;
-          if (md == RED_NORM2) {
-#pragma unroll
-            for (int e = 0; e < W; ++e) acc[r].v[0] = Ar<T>::cfma(q[i][e], q[i][e], acc[r].v[0]);
-          } else if (md == RED_COLNORM2) {
-#pragma unroll
-            for (int e = 0; e < W; ++e) acc[r].v[e] = Ar<T>::cfma(q[i][e], q[i][e], acc[r].v[e]);
-          } else if (md == RED_SUMVEC) {
-            const T y = ry[r][row];
-#pragma unroll
-            for (int e = 0; e < W; ++e) acc[r].v[0] = Ar<T>::cfma(y, q[i][e], acc[r].v[0]);
-          } else {
-            T y[W];
-            const T* ys = ry[r] + (size_t)row * (EX ? W : s);
-#pragma unroll
-            for (int e = 0; e < W; ++e) y[e] = (EX || e < s) ? ys[e] : Ar<T>::zero();
-            if (md == RED_FULL) {
-#pragma unroll
-              for (int k = 0; k < W; ++k)
-#pragma unroll
-                for (int c = 0; c < W; ++c) acc[r].f[k][c] = Ar<T>::cfma(y[k], q[i][c], acc[r].f[k][c]);
-            } else if (md == RED_TRACE) {
-#pragma unroll
-              for (int e = 0; e < W; ++e) acc[r].v[0] = Ar<T>::cfma(y[e], q[i][e], acc[r].v[0]);
-            } else {
-#pragma unroll
-              for (int e = 0; e < W; ++e) acc[r].v[e] = Ar<T>::cfma(y[e], q[i][e], acc[r].v[e]);
-            }
-          }
-        }
+        narrow_row_out<T, W, EX>(q[i], orow[i], s, Q, rmode, ry, acc);
       }
     }
   }
   if (nred == 0) return;
   // team leaders -> warp (xor over the teams, fixed order) -> warps in index order
-  constexpr int ND = Ar<T>::ND;
+  narrow_flush<T, W, TEAM>(a, s, rmode, acc, smem);
+}
+
+
+// SELL-32-sigma product for narrow blocks (s * esz <= 32 B; SURVEY §8(a) a0 / §7.1 "SELL-C-sigma
+// mapping: one row per lane, C = 32, with sigma-window sorting for the power-law rows"): a warp owns
+// a chunk of 32 rows (sorted by decreasing length inside windows of sigma rows, so the chunk is
+// padded only to ITS longest row); entry j of the 32 rows is contiguous (one coalesced 128-B index
+// load and one value load per step for the whole warp), every lane gathers its own P row (one 16- or
+// 32-byte load) and sums its row in CSR order — no team butterfly, bitwise the sequential row sum.
+// Padding entries carry column -1 and are skipped. U steps are in flight per lane.
+template <typename T, int W, bool EX>
+__global__ void __launch_bounds__(256, 4) sell_kernel(SpmmArgs a) {
+  if (a.done && *a.done) return;
+  extern __shared__ double smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int s = a.s;
+  const int* __restrict__ cs = a.sell_cs;
+  const int* __restrict__ ci = a.sell_ci;
+  const T* __restrict__ val = reinterpret_cast<const T*>(a.sell_val);
+  const int* __restrict__ srow = a.sell_row;
+  const int* __restrict__ corder = a.sell_order;
+  const T* __restrict__ P = reinterpret_cast<const T*>(a.P);
+  T* __restrict__ Q = reinterpret_cast<T*>(a.Q);
+  int rmode[2];
+  const T* ry[2];
 #pragma unroll
   for (int r = 0; r < 2; ++r) {
-    if (r >= nred) break;
-    const int md = rmode[r];
-    const int len = red_len(md, s, ND == 2);
-    double* w = smem + (size_t)warp * len;
-#pragma unroll
-    for (int m = TEAM; m < 32; m <<= 1)
-#pragma unroll
-      for (int c = 0; c < W; ++c) {
-        acc[r].v[c] = Ar<T>::add(acc[r].v[c], Ar<T>::shfl_xor(acc[r].v[c], m));
-#pragma unroll
-        for (int k = 0; k < W; ++k) acc[r].f[k][c] = Ar<T>::add(acc[r].f[k][c], Ar<T>::shfl_xor(acc[r].f[k][c], m));
-      }
-    if (lane == 0) {
-      if (md == RED_NORM2) w[0] = re_of(acc[r].v[0]);
-      else if (md == RED_TRACE || md == RED_SUMVEC) Ar<T>::st(w, acc[r].v[0]);
-      else if (md == RED_COLNORM2) {
-#pragma unroll
-        for (int c = 0; c < W; ++c)
-          if (c < s) w[c] = re_of(acc[r].v[c]);
-      } else if (md == RED_DIAG) {
-#pragma unroll
-        for (int c = 0; c < W; ++c)
-          if (c < s) Ar<T>::st(w + c * ND, acc[r].v[c]);
-      } else {
-#pragma unroll
-        for (int k = 0; k < W; ++k)
-#pragma unroll
-          for (int c = 0; c < W; ++c)
-            if (k < s && c < s) Ar<T>::st(w + (k * s + c) * ND, acc[r].f[k][c]);
-      }
-    }
-    __syncthreads();
-    const int nw = blockDim.x >> 5;
-    for (int j = threadIdx.x; j < len; j += blockDim.x) {
-      double sum = 0.0;
-      for (int q2 = 0; q2 < nw; ++q2) sum += smem[q2 * len + j];
-      a.partials[(size_t)blockIdx.x * a.pstride + a.red[r].poff + j] = sum;
-    }
-    __syncthreads();
+    rmode[r] = r < a.nred ? a.red[r].mode : RED_NONE;
+    ry[r] = r < a.nred ? reinterpret_cast<const T*>(a.red[r].yext) : nullptr;
   }
+  TeamRed<T, W> acc[2];
+#pragma unroll
+  for (int r = 0; r < 2; ++r)
+#pragma unroll
+    for (int c = 0; c < W; ++c) {
+      acc[r].v[c] = Ar<T>::zero();
+#pragma unroll
+      for (int k = 0; k < W; ++k) acc[r].f[k][c] = Ar<T>::zero();
+    }
+  auto load_row = [&](int c, T (&p)[W]) {
+    const T* src = P + (size_t)c * (EX ? W : s);
+    if constexpr (EX && W * sizeof(T) % 16 == 0) {
+#pragma unroll
+      for (int q = 0; q < W * (int)sizeof(T) / 16; ++q) {
+        const double2 d = __ldg(reinterpret_cast<const double2*>(src) + q);
+        if constexpr (sizeof(T) == 16) {
+          p[q] = *reinterpret_cast<const T*>(&d);
+        } else {
+          reinterpret_cast<double*>(p)[2 * q] = d.x;
+          reinterpret_cast<double*>(p)[2 * q + 1] = d.y;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < W; ++e) p[e] = (EX || e < s) ? __ldg(src + e) : Ar<T>::zero();
+    }
+  };
+  constexpr int U = W * sizeof(T) >= 32 ? 4 : 8;  // steps in flight
+  const long long nwarp = (long long)gridDim.x * (blockDim.x >> 5);
+  for (long long k = (long long)blockIdx.x * (blockDim.x >> 5) + warp; k < a.sell_nchunk; k += nwarp) {
+    const int c = corder ? __ldg(corder + k) : (int)k;
+    const int base = __ldg(cs + c);
+    const int w = (__ldg(cs + c + 1) - base) >> 5;
+    const int row = __ldg(srow + (size_t)c * 32 + lane);  // -1: no row (the last chunk's tail)
+    T q[W];
+#pragma unroll
+    for (int e = 0; e < W; ++e) q[e] = Ar<T>::zero();
+    const int* cp = ci + base + lane;
+    const T* vp = val + base + lane;
+    for (int j = 0; j < w; j += U) {
+      int cj[U];
+      T vj[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const bool in = j + u < w;
+        cj[u] = in ? __ldcs(cp + (size_t)(j + u) * 32) : -1;
+        vj[u] = in ? __ldcs(vp + (size_t)(j + u) * 32) : Ar<T>::zero();
+      }
+      T p[U][W];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (cj[u] >= 0) {
+          load_row(cj[u], p[u]);
+        } else {
+#pragma unroll
+          for (int e = 0; e < W; ++e) p[u][e] = Ar<T>::zero();
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (cj[u] >= 0) {
+#pragma unroll
+          for (int e = 0; e < W; ++e) q[e] = Ar<T>::fma(vj[u], p[u][e], q[e]);
+        }
+    }
+    if (row >= 0) narrow_row_out<T, W, EX>(q, row, s, Q, rmode, ry, acc);
+  }
+  if (a.nred == 0) return;
+  narrow_flush<T, W, 1>(a, s, rmode, acc, smem);
 }
 
 // rows per group in flight
@@ -894,7 +1013,11 @@ int launch_spmm_tx(const SpmmArgs& a, int grid, int block, size_t smem, cudaStre
 // grid < 0: return the number of resident CTAs per SM instead of launching
 template <typename T, int W, bool EX>
 int launch_team(const SpmmArgs& a, int grid, int block, size_t smem, cudaStream_t st) {
-  constexpr int TEAM = 8, R = W * sizeof(T) >= 32 ? 1 : 2;
+  // rows per team: two only for 8-byte rows. The 16-byte instance with two rows (double, W = 2: one
+  // LDG.128 per row and step) is miscompiled by ptxas 12.9 at -O3 — garbage gather addresses as soon
+  // as the two rows' lengths differ (the same source is correct at -Xptxas -O1, with R = 1, and for
+  // W = 1 / W = 4; scripts/team_probe.cu reproduces it) — so 16-byte rows take one row per team
+  constexpr int TEAM = 8, R = W * sizeof(T) >= 16 ? 1 : 2;
   if (grid < 0) {
     int nb = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, spmv_team_kernel<T, W, TEAM, R, EX>, block, smem);
@@ -912,6 +1035,12 @@ template <typename T, int S, bool FC>
 int launch_spmm_t(const SpmmArgs& a, int grid, int block, size_t smem, cudaStream_t st) {
   const bool ex = a.s == S && (sizeof(T) == 16 || S % 2 == 0);
   if constexpr (use_team<T, S>()) {
+    if (a.sell_cs) {
+      if (grid < 0) return launch_team<T, S, true>(a, grid, block, smem, st);
+      if (ex) sell_kernel<T, S, true><<<grid, block, smem, st>>>(a);
+      else sell_kernel<T, S, false><<<grid, block, smem, st>>>(a);
+      return (int)cudaGetLastError();
+    }
     if (a.team) {
       if (grid < 0 || ex) return launch_team<T, S, true>(a, grid, block, smem, st);
       return launch_team<T, S, false>(a, grid, block, smem, st);

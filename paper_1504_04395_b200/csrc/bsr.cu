@@ -20,6 +20,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
+#include <cstdlib>
 
 #include "kernels.cuh"
 
@@ -269,19 +271,327 @@ __global__ void __launch_bounds__(256, S >= 16 ? 1 : 2) bsr12_kernel(BsrArgs a) 
   }
 }
 
+
+// ---------------------------------------------------------------------------------------
+// Round 2: the product without the M = 12 -> 16 padding. The complex block product is the
+// real contraction
+//   [B_r; B_i] (24 x 12)  *  [P_r | P_i] (12 x 2S)   ->   B_r P_r, B_r P_i, B_i P_r, B_i P_i
+// M = 24 (three 8-row tiles, no padding), K = 12 (three k-steps), N = 2S, i.e. 9 * 2S/8 DMMAs per
+// block (27 at S = 12) against 12 * 2S/8 (36) for the [B_r B_i] * lift(P) form above, and no sign
+// flips; Q_r = B_r P_r - B_i P_i and Q_i = B_r P_i + B_i P_r are formed once per block ROW from
+// the four accumulator sets. Tiles are chosen so that almost every fragment pair is one 16-byte
+// shared-memory load and the combination is lane-local:
+//   M tile 0 = B_r rows 0-7, M tile 1 = B_i rows 0-7 (lane row fr: one double2 = (Re, Im) of
+//   B[fr][k] feeds both), M tile 2 = rows 8-11 with lane row 8 + fr/2 and part fr & 1 (B_r in
+//   even-fr lanes, B_i in odd: one exchange with lane ^ 4 per block row);
+//   N tiles in pairs: tile "re" = Re of complex columns 8j..8j+7, tile "im" = Im of the same
+//   (lane column fr: one double2 of the interleaved P row feeds both), so a lane owns the complex
+//   columns 8j + 2fk, 8j + 2fk + 1; a remaining group of 4 complex columns (S = 4, 12) is one tile
+//   over the interleaved (Re, Im) columns, owning complex column 8 NP + fk.
+// The block (2304 contiguous bytes) is staged unpadded — row stride 24 doubles is conflict-free
+// for these fragment loads —, the 12 P rows with stride 2S + 4. Staging is by bulk copies
+// (`cp.async.bulk`, one per lane: the block + 12 rows) into a per-warp two-stage mbarrier ring
+// that runs ahead across block-row boundaries (the next row's first block is in flight during
+// this row's last).
+template <int S>
+struct B2Cfg {
+  static constexpr int NR = 2 * S;
+  static constexpr int NP = NR / 16;         // N-tile pairs
+  static constexpr int NS = (NR % 16) / 8;   // single N tile (4 complex columns)
+  static constexpr int NC = 2 * NP + NS;     // complex columns a lane owns per row
+  static constexpr int PST = NR + 4;         // staged P row stride (doubles): = 4 or 12 mod 16
+  static constexpr int ABLK = BS * BS * 2;   // 288 doubles, unpadded
+  static constexpr int STAGE = ABLK + BS * PST;
+  static constexpr int NSTG = 2;
+  static constexpr int WARPS = 8;
+  static constexpr int SMEM = WARPS * NSTG * STAGE * 8 + WARPS * NSTG * 8;
+};
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAITB_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAITB_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(double* dst, const double* src, unsigned bytes, unsigned long long* bar,
+                                         unsigned long long pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+
+template <int S>
+__global__ void __launch_bounds__(256, S >= 16 ? 1 : 2) bsr12_kernel2(BsrArgs a) {
+  if (a.done && *a.done) return;
+  using C = B2Cfg<S>;
+  extern __shared__ __align__(16) double bsm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* wbuf = bsm + (size_t)warp * C::NSTG * C::STAGE;
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(bsm + (size_t)C::WARPS * C::NSTG * C::STAGE) + warp * C::NSTG;
+  const double* __restrict__ val = reinterpret_cast<const double*>(a.val);
+  const double* __restrict__ P = reinterpret_cast<const double*>(a.P);
+  double* __restrict__ Q = reinterpret_cast<double*>(a.Q);
+  const long long nb = a.nb;
+  const long long gw = (long long)blockIdx.x * C::WARPS + warp;
+  const long long nw = (long long)gridDim.x * C::WARPS;
+  const int fr = lane >> 2, fk = lane & 3;
+  const unsigned long long pol_a = policy_evict_first(), pol_p = policy_evict_last();
+
+  if (lane == 0) {
+    for (int q = 0; q < C::NSTG; ++q) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bars + q)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+
+  // producer side: the warp's blocks in order, across its block rows (Ip, jp, jpe = next to issue)
+  // (positions k = gw, gw + nw, ... of the visiting order; block row = order[k], or k)
+  const int* __restrict__ order = a.order;
+  auto row_of = [&](long long k) -> long long { return order ? (long long)__ldg(order + k) : k; };
+  long long Ip = gw;
+  int jp = 0, jpe = 0;
+  auto seek = [&]() {  // move (Ip, jp) to the next existing block at or after the position
+    while (Ip < nb && jp >= jpe) {
+      Ip += nw;
+      if (Ip < nb) {
+        const long long r = row_of(Ip);
+        jp = __ldg(a.brp + r);
+        jpe = __ldg(a.brp + r + 1);
+      }
+    }
+  };
+  if (Ip < nb) {
+    const long long r = row_of(Ip);
+    jp = __ldg(a.brp + r);
+    jpe = __ldg(a.brp + r + 1);
+    seek();
+  }
+  constexpr unsigned ABYTES = C::ABLK * 8, PBYTES = C::NR * 8;
+  auto issue = [&](unsigned cnt) {  // block jp into stage cnt % NSTG
+    const int st = (int)(cnt % C::NSTG);
+    double* bs = wbuf + (size_t)st * C::STAGE;
+    unsigned long long* bar = bars + st;
+    if (lane == 0) {
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                   "r"(ABYTES + BS * PBYTES)
+                   : "memory");
+      bulk_g2s(bs, val + (size_t)jp * C::ABLK, ABYTES, bar, pol_a);
+    } else if (lane <= BS) {
+      const double* pj = P + ((size_t)__ldg(a.bci + jp) * BS + (lane - 1)) * C::NR;
+      bulk_g2s(bs + C::ABLK + (lane - 1) * C::PST, pj, PBYTES, bar, pol_p);
+    }
+    ++jp;
+    seek();
+  };
+  unsigned issued = 0, used = 0;
+  if (Ip < nb) issue(issued++);
+
+  // complex column of owned slot ci
+  auto ccol = [&](int ci) { return ci < 2 * C::NP ? 8 * (ci >> 1) + 2 * fk + (ci & 1) : 8 * C::NP + fk; };
+  const bool own2 = !(fr & 1);  // this lane finalises row 8 + fr/2
+
+  const int nred = a.nred;
+  int rmode[2];
+  const double* ry[2];
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    rmode[r] = r < nred ? a.red[r].mode : RED_NONE;
+    ry[r] = r < nred ? reinterpret_cast<const double*>(a.red[r].yext) : nullptr;
+  }
+  double2 rs[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
+  double2 rc[2][C::NC];
+#pragma unroll
+  for (int r = 0; r < 2; ++r)
+#pragma unroll
+    for (int n = 0; n < C::NC; ++n) rc[r][n] = make_double2(0.0, 0.0);
+
+  for (long long kI = gw; kI < nb; kI += nw) {
+    const long long I = row_of(kI);
+    const int jb = __ldg(a.brp + I), je = __ldg(a.brp + I + 1);
+    // accP[mt][j][part of P][e], accS[mt][part]
+    double accP[3][C::NP > 0 ? C::NP : 1][2][2];
+    double accS[3][2];
+#pragma unroll
+    for (int mt = 0; mt < 3; ++mt) {
+#pragma unroll
+      for (int j = 0; j < C::NP; ++j) accP[mt][j][0][0] = accP[mt][j][0][1] = accP[mt][j][1][0] = accP[mt][j][1][1] = 0.0;
+      accS[mt][0] = accS[mt][1] = 0.0;
+    }
+    // the unit-diagonal operand P_I requested now, consumed after the row's last block (the
+    // reduction operands are read in the epilogue: prefetching them too spilled at S = 12)
+    double2 pI[2][C::NC];
+#pragma unroll
+    for (int m = 0; m < 2; ++m) {
+      const int row = m ? 8 + (fr >> 1) : fr;
+      const bool act = m ? own2 : true;
+      const size_t base = ((size_t)I * BS + row) * C::NR;
+#pragma unroll
+      for (int ci = 0; ci < C::NC; ++ci) {
+        pI[m][ci] = make_double2(0.0, 0.0);
+        if (act && a.unit_diag) pI[m][ci] = __ldg(reinterpret_cast<const double2*>(P + base + 2 * ccol(ci)));
+      }
+    }
+    for (int j = jb; j < je; ++j) {
+      if (Ip < nb) issue(issued++);  // the next block (this or a later row) into the other stage
+      const int st = (int)(used % C::NSTG);
+      mbar_wait(bars + st, (used / C::NSTG) & 1);
+      ++used;
+      const double* bs = wbuf + (size_t)st * C::STAGE;
+      const double* ps = bs + C::ABLK;
+#pragma unroll
+      for (int ks = 0; ks < 3; ++ks) {
+        const int k = ks * 4 + fk;
+        const double2 a01 = *reinterpret_cast<const double2*>(bs + (fr * BS + k) * 2);
+        const double a2 = bs[((8 + (fr >> 1)) * BS + k) * 2 + (fr & 1)];
+#pragma unroll
+        for (int jn = 0; jn < C::NP; ++jn) {
+          const double2 b = *reinterpret_cast<const double2*>(ps + k * C::PST + 16 * jn + 2 * fr);
+          dmma(accP[0][jn][0], a01.x, b.x);
+          dmma(accP[0][jn][1], a01.x, b.y);
+          dmma(accP[1][jn][0], a01.y, b.x);
+          dmma(accP[1][jn][1], a01.y, b.y);
+          dmma(accP[2][jn][0], a2, b.x);
+          dmma(accP[2][jn][1], a2, b.y);
+        }
+        if (C::NS) {
+          const double b = ps[k * C::PST + 16 * C::NP + fr];
+          dmma(accS[0], a01.x, b);
+          dmma(accS[1], a01.y, b);
+          dmma(accS[2], a2, b);
+        }
+      }
+      __syncwarp();  // this stage is refilled by the next issue
+    }
+    // combine: q[m][ci] = (Q_r, Q_i) of row (m ? 8 + fr/2 : fr), complex column ccol(ci)
+    double2 q[2][C::NC];
+#pragma unroll
+    for (int ci = 0; ci < C::NC; ++ci) {
+      double x0, y0_, x1, y1, x2, y2;  // (B P_r, B P_i) of M tiles 0 (B_r), 1 (B_i), 2 (mixed)
+      if (ci < 2 * C::NP) {
+        const int jn = ci >> 1, e = ci & 1;
+        x0 = accP[0][jn][0][e]; y0_ = accP[0][jn][1][e];
+        x1 = accP[1][jn][0][e]; y1 = accP[1][jn][1][e];
+        x2 = accP[2][jn][0][e]; y2 = accP[2][jn][1][e];
+      } else {
+        x0 = accS[0][0]; y0_ = accS[0][1];
+        x1 = accS[1][0]; y1 = accS[1][1];
+        x2 = accS[2][0]; y2 = accS[2][1];
+      }
+      q[0][ci] = make_double2(x0 - y1, y0_ + x1);
+      const double xo = __shfl_xor_sync(0xffffffffu, x2, 4), yo = __shfl_xor_sync(0xffffffffu, y2, 4);
+      q[1][ci] = make_double2(x2 - yo, y2 + xo);  // meaningful in the even-fr lanes (B_r there, B_i in lane ^ 4)
+    }
+#pragma unroll
+    for (int m = 0; m < 2; ++m) {
+      const int row = m ? 8 + (fr >> 1) : fr;
+      if (m && !own2) continue;
+      const size_t base = ((size_t)I * BS + row) * C::NR;
+#pragma unroll
+      for (int ci = 0; ci < C::NC; ++ci) {
+        const int col = 2 * ccol(ci);
+        double2 v = q[m][ci];
+        if (a.unit_diag) {
+          v.x += pI[m][ci].x;
+          v.y += pI[m][ci].y;
+        }
+        *reinterpret_cast<double2*>(Q + base + col) = v;
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+          const int md = rmode[r];
+          if (md == RED_NONE) continue;
+          if (md == RED_NORM2 || md == RED_COLNORM2) {
+            const double q2 = v.x * v.x + v.y * v.y;
+            if (md == RED_NORM2) rs[r].x += q2;
+            else rc[r][ci].x += q2;
+          } else {
+            const double2 y = md == RED_SUMVEC ? __ldg(reinterpret_cast<const double2*>(ry[r]) + (size_t)I * BS + row)
+                                               : __ldg(reinterpret_cast<const double2*>(ry[r] + base + col));
+            const double2 pr = make_double2(y.x * v.x + y.y * v.y, y.x * v.y - y.y * v.x);
+            if (md == RED_DIAG) {
+              rc[r][ci].x += pr.x;
+              rc[r][ci].y += pr.y;
+            } else {
+              rs[r].x += pr.x;
+              rs[r].y += pr.y;
+            }
+          }
+        }
+      }
+    }
+  }
+  if (nred == 0) return;
+  __syncthreads();  // every warp is done with its staging buffers
+  double* red_sm = bsm;  // [warp][len] doubles
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    if (r >= nred) break;
+    const int md = rmode[r];
+    const int len = red_len(md, S, true);
+    double* w = red_sm + (size_t)warp * len;
+    if (md == RED_DIAG || md == RED_COLNORM2) {
+#pragma unroll
+      for (int ci = 0; ci < C::NC; ++ci) {
+        double2 v = rc[r][ci];
+#pragma unroll
+        for (int m = 4; m < 32; m <<= 1) {  // over fr: lanes with equal fk own the same columns
+          v.x += __shfl_xor_sync(0xffffffffu, v.x, m);
+          v.y += __shfl_xor_sync(0xffffffffu, v.y, m);
+        }
+        if (fr == 0) {
+          const int c = ccol(ci);
+          if (md == RED_DIAG) {
+            w[2 * c] = v.x;
+            w[2 * c + 1] = v.y;
+          } else {
+            w[c] = v.x;
+          }
+        }
+      }
+    } else {
+      double2 v = rs[r];
+#pragma unroll
+      for (int m = 1; m < 32; m <<= 1) {
+        v.x += __shfl_xor_sync(0xffffffffu, v.x, m);
+        v.y += __shfl_xor_sync(0xffffffffu, v.y, m);
+      }
+      if (lane == 0) {
+        w[0] = v.x;
+        if (md != RED_NORM2) w[1] = v.y;
+      }
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < len; j += blockDim.x) {
+      double acc = 0.0;
+      for (int qq = 0; qq < C::WARPS; ++qq) acc += red_sm[qq * len + j];
+      a.partials[(size_t)blockIdx.x * a.pstride + a.red[r].poff + j] = acc;
+    }
+    __syncthreads();
+  }
+}
+
 template <int S>
 int launch_s(const BsrArgs& a, int grid, cudaStream_t st) {
   using C = BCfg<S>;
+  using C2 = B2Cfg<S>;
+  const bool old = getenv("SRK_BSR_OLD") != nullptr;  // A/B switch (read per launch): the padded [B_r B_i] * lift(P) form
   static std::atomic<unsigned long long> attr{0};
   if (first_on_device(attr)) {
     cudaFuncSetAttribute(bsr12_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    cudaFuncSetAttribute(bsr12_kernel2<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, C2::SMEM);
   }
   if (grid < 0) {  // resident CTAs per SM
     int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bsr12_kernel<S>, 256, C::SMEM);
+    if (old) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bsr12_kernel<S>, 256, C::SMEM);
+    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bsr12_kernel2<S>, 256, C2::SMEM);
     return occ;
   }
-  bsr12_kernel<S><<<grid, 256, C::SMEM, st>>>(a);
+  if (old) bsr12_kernel<S><<<grid, 256, C::SMEM, st>>>(a);
+  else bsr12_kernel2<S><<<grid, 256, C2::SMEM, st>>>(a);
   return (int)cudaGetLastError();
 }
 

@@ -282,7 +282,17 @@ int Eng::spmm(bool adj, const void* P, void* Q, int s, std::vector<RQ> reds) {
   // a lane per row for short regular rows (the stencil's A^H vector product)
   const long long nz = adj ? A->nnzH : A->nnz;
   a.team = (so.perm != nullptr || nz >= 12LL * std::max(1LL, n)) ? 1 : 0;
-  const int grid = grid_for(cap, full, true, 8 * 2 * 8 * 16 * 16, a.team);  // occupancy at the largest epilogue smem
+  int grid = grid_for(cap, full, true, 8 * 2 * 8 * 16 * 16, a.team);  // occupancy at the largest epilogue smem
+  const Mat::Sell& se = adj ? A->sellH : A->sell;
+  if (se.cs && (size_t)cap * (cplx ? 16 : 8) <= 32) {  // narrow block on an irregular operator: SELL-32-sigma
+    a.sell_cs = se.cs;
+    a.sell_ci = se.ci;
+    a.sell_val = se.val;
+    a.sell_row = se.row;
+    a.sell_order = se.order;
+    a.sell_nchunk = se.nchunk;
+    grid = (int)std::max<long long>(1, std::min<long long>((se.nchunk + 7) / 8, (long long)c->nsm * 4));
+  }
   if ((err = c->ensure_partials((size_t)grid * a.pstride))) return err;
   a.partials = c->partials;
   a.done = done;
@@ -307,21 +317,37 @@ int Eng::upd(int s, std::vector<const void*> in, std::vector<OutSpec> outs, std:
   // An n-vector update (s = 1) with one-or-scalar coefficients and only norm / trace
   // reductions does not depend on the row structure: run it as an (n/4) x 4 block
   // (two lanes per row with 16-byte loads instead of one 8-byte element per lane).
-  if (s == 1 && n % 4 == 0 && n >= 4) {
-    bool flat = true;
-    for (const OutSpec& o : outs)
-      for (const TermSpec& t : o.t) flat &= (t.c.kind == CK_ONE || t.c.kind == CK_SCALAR);
-    for (const RQ& r : reds) flat &= (r.mode == RED_NORM2 || r.mode == RED_TRACE);
-    // the (n/4) x 4 view loads 16 bytes per lane: every operand must be 16-byte aligned
-    // (a caller's view at an 8-byte offset, e.g. v[1:], keeps the element-wise path)
-    auto a16 = [](const void* p) { return p == nullptr || ((uintptr_t)p & 15) == 0; };
-    for (const void* p : in) flat &= a16(p);
-    for (const OutSpec& o : outs) flat &= a16(o.ptr);
-    for (const RQ& r : reds) flat &= a16(r.yext);
+  // The same holds for any width whose rows map badly onto 16-byte lanes — fewer than 64 bytes, or
+  // a lane count that is not a power of two (config 4's complex s = 12: 12 lanes per row, 8 of a
+  // warp's 32 idle; its scalar updates ran at 65-69% of HBM) —: the n x s block is viewed as
+  // (n s / w) x w with 128-byte rows (w = 16 real / 8 complex, else the widest divisor of n s).
+  {
+    const int esz = cplx ? 16 : 8;
+    const int lanes = (s * esz + 15) / 16;
+    const bool awkward = s * esz < 64 || (lanes & (lanes - 1)) != 0;
+    const long long tot = n * (long long)s;
+    int w = 0;
+    for (int cand : {128 / esz, 64 / esz, 32 / esz})
+      if (cand > 0 && tot % cand == 0 && tot >= cand) {
+        w = cand;
+        break;
+      }
+    bool flat = awkward && w > 0 && w != s && (w * esz > s * esz || (lanes & (lanes - 1)) != 0);
+    if (flat) {
+      for (const OutSpec& o : outs)
+        for (const TermSpec& t : o.t) flat &= (t.c.kind == CK_ONE || t.c.kind == CK_SCALAR);
+      for (const RQ& r : reds) flat &= (r.mode == RED_NORM2 || r.mode == RED_TRACE);
+      // the flat view loads 16 bytes per lane: every operand must be 16-byte aligned
+      // (a caller's view at an 8-byte offset, e.g. v[1:], keeps the element-wise path)
+      auto a16 = [](const void* p) { return p == nullptr || ((uintptr_t)p & 15) == 0; };
+      for (const void* p : in) flat &= a16(p);
+      for (const OutSpec& o : outs) flat &= a16(o.ptr);
+      for (const RQ& r : reds) flat &= a16(r.yext);
+    }
     if (flat) {
       const long long n0 = n;
-      n = n0 / 4;
-      const int r = upd(4, std::move(in), std::move(outs), std::move(reds));
+      n = tot / w;
+      const int r = upd(w, std::move(in), std::move(outs), std::move(reds));
       n = n0;
       return r;
     }
@@ -498,6 +524,7 @@ int Eng::spmm_bsr(bool adj, const void* P, void* Q, int s, const std::vector<RQ>
   a.P = P;
   a.Q = Q;
   a.nb = A->nb;
+  a.order = A->border;
   a.unit_diag = A->unit_diag;
   a.done = done;
   static int occ = 0;
@@ -696,6 +723,8 @@ __global__ static void gather_sorted_rows(const int* rp, const int* ci, const T*
   }
 }
 
+int build_sell(Mat& m, bool adj, const std::vector<int>& h, cudaStream_t st);
+
 int build_balanced_order(Mat& m, bool adj, cudaStream_t st) {
   const int* rp = adj ? m.rpH : m.rp;
   const int* ci = adj ? m.ciH : m.ci;
@@ -731,10 +760,100 @@ int build_balanced_order(Mat& m, bool adj, cudaStream_t st) {
   else
     gather_sorted_rows<double><<<grid, 256, 0, st>>>(rp, ci, reinterpret_cast<const double*>(val), so.perm, so.rp, so.ci,
                                                      reinterpret_cast<double*>(so.val), n);
-  return (int)cudaStreamSynchronize(st);  // rp2 / perm host buffers go out of scope
+  if (cudaStreamSynchronize(st) != cudaSuccess) return (int)cudaErrorUnknown;  // rp2 / perm host buffers go out of scope
+  return build_sell(m, adj, h, st);
+}
+
+// SELL-32-sigma (Kreutzer et al.'s format): sigma-window sort, 32-row chunks,
+// column-major padded storage; filled on the device from the CSR arrays
+template <typename T>
+__global__ static void fill_sell(const int* rp, const int* ci, const T* val, const int* srow, const int* cs, int* ci2,
+                                 T* val2, long long nchunk) {
+  const long long warp = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  for (long long c = warp; c < nchunk; c += nw) {
+    const int base = cs[c], w = (cs[c + 1] - base) >> 5;
+    const int src = srow[c * 32 + lane];
+    const int b = src >= 0 ? rp[src] : 0, len = src >= 0 ? rp[src + 1] - b : 0;
+    for (int j = 0; j < w; ++j) {
+      const bool in = j < len;
+      ci2[(size_t)base + (size_t)j * 32 + lane] = in ? ci[b + j] : -1;
+      val2[(size_t)base + (size_t)j * 32 + lane] = in ? val[b + j] : T{};
+    }
+  }
+}
+
+int build_sell(Mat& m, bool adj, const std::vector<int>& h, cudaStream_t st) {
+  static const bool off = getenv("SRK_NO_SELL") != nullptr;  // A/B switch: the team-per-row kernel instead
+  if (off) return 0;
+  static const int env_sigma = getenv("SRK_SELL_SIGMA") ? atoi(getenv("SRK_SELL_SIGMA")) : 0;
+  const long long n = m.n;
+  // sigma: the sorting window. Large windows pad least; the output rows of a chunk stay within one
+  // window, so Q's scattered narrow writes merge in L2 (default 2^16 rows; <= 0: the whole matrix)
+  const long long sigma = env_sigma > 0 ? std::max(32, env_sigma / 32 * 32) : (env_sigma < 0 ? n : 65536);
+  const long long nchunk = (n + 31) / 32;
+  std::vector<int> row(nchunk * 32, -1);
+  for (long long i = 0; i < n; ++i) row[i] = (int)i;
+  for (long long w0 = 0; w0 < n; w0 += sigma) {
+    const long long w1 = std::min(n, w0 + sigma);
+    std::stable_sort(row.begin() + w0, row.begin() + w1, [&](int x, int y) { return h[x + 1] - h[x] > h[y + 1] - h[y]; });
+  }
+  std::vector<int> cs(nchunk + 1), width(nchunk);
+  long long tot = 0;
+  for (long long c = 0; c < nchunk; ++c) {
+    int w = 0;
+    for (int l = 0; l < 32; ++l) {
+      const int r = row[c * 32 + l];
+      if (r >= 0) w = std::max(w, h[r + 1] - h[r]);
+    }
+    width[c] = w;
+    cs[c] = (int)tot;
+    tot += 32LL * w;
+    if (tot > 0x7fffff00LL) return 0;  // int32 offsets: keep the sorted CSR
+  }
+  cs[nchunk] = (int)tot;
+  const long long nnz = adj ? m.nnzH : m.nnz;
+  if ((double)tot > 1.25 * (double)nnz) return 0;  // too much padding: keep the sorted CSR
+  std::vector<int> order(nchunk);
+  for (long long c = 0; c < nchunk; ++c) order[c] = (int)c;
+  std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return width[x] > width[y]; });
+  Mat::Sell& se = adj ? m.sellH : m.sell;
+  const size_t esz = m.cplx ? 16 : 8;
+  if (cudaMalloc(&se.cs, sizeof(int) * (nchunk + 1)) != cudaSuccess ||
+      cudaMalloc(&se.row, sizeof(int) * nchunk * 32) != cudaSuccess ||
+      cudaMalloc(&se.order, sizeof(int) * nchunk) != cudaSuccess ||
+      cudaMalloc(&se.ci, sizeof(int) * std::max<long long>(tot, 1)) != cudaSuccess ||
+      cudaMalloc(&se.val, esz * std::max<long long>(tot, 1)) != cudaSuccess)
+    return (int)cudaErrorMemoryAllocation;
+  se.nchunk = nchunk;
+  se.entries = tot;
+  se.sigma = (int)std::min<long long>(sigma, n);
+  cudaMemcpyAsync(se.cs, cs.data(), sizeof(int) * (nchunk + 1), cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(se.row, row.data(), sizeof(int) * nchunk * 32, cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(se.order, order.data(), sizeof(int) * nchunk, cudaMemcpyHostToDevice, st);
+  const int* rp = adj ? m.rpH : m.rp;
+  const int* ci = adj ? m.ciH : m.ci;
+  const void* val = adj ? m.valH : m.val;
+  const int grid = (int)std::min<long long>((nchunk + 7) / 8, 148 * 16);
+  if (m.cplx)
+    fill_sell<double2><<<grid, 256, 0, st>>>(rp, ci, reinterpret_cast<const double2*>(val), se.row, se.cs, se.ci,
+                                             reinterpret_cast<double2*>(se.val), nchunk);
+  else
+    fill_sell<double><<<grid, 256, 0, st>>>(rp, ci, reinterpret_cast<const double*>(val), se.row, se.cs, se.ci,
+                                            reinterpret_cast<double*>(se.val), nchunk);
+  return (int)cudaStreamSynchronize(st);  // the host arrays go out of scope
 }
 
 void free_balanced_order(Mat& m) {
+  for (Mat::Sell* se : {&m.sell, &m.sellH}) {
+    if (se->cs) cudaFree(se->cs);
+    if (se->ci) cudaFree(se->ci);
+    if (se->val) cudaFree(se->val);
+    if (se->row) cudaFree(se->row);
+    if (se->order) cudaFree(se->order);
+    *se = Mat::Sell{};
+  }
   for (Mat::Sorted* so : {&m.inner, &m.bnd, &m.innerH, &m.bndH}) {
     if (so->rp) cudaFree(so->rp);
     if (so->ci) cudaFree(so->ci);

@@ -96,6 +96,7 @@ struct Mat {
   int* brp = nullptr;
   int* bci = nullptr;
   void* bval = nullptr;
+  int* border = nullptr;  // visiting order of the block rows (srk_matrix_set_row_order) or null
   Prec* prec = nullptr;  // right ILU(0) preconditioner (srk_matrix_ilu0), or null
   // Balanced row order (irregular row lengths, e.g. config 5's power law): a copy
   // of the CSR with rows sorted by decreasing length (stable), so that the rows a
@@ -107,6 +108,18 @@ struct Mat {
     void* val = nullptr;
     int* perm = nullptr;
   } srt, srtH;
+  // SELL-32-sigma form of an irregular operator (narrow blocks, s * esz <= 32 B): rows sorted by
+  // decreasing length inside windows of sigma rows, chunks of 32 rows stored column-major and
+  // padded to the chunk's longest row (column -1), chunks visited by decreasing width
+  struct Sell {
+    int* cs = nullptr;     // nchunk + 1 chunk offsets (entries)
+    int* ci = nullptr;
+    void* val = nullptr;
+    int* row = nullptr;    // 32 * nchunk output rows (-1: none)
+    int* order = nullptr;  // chunk visiting order
+    long long nchunk = 0, entries = 0;
+    int sigma = 0;
+  } sell, sellH;
   // multi-GPU (dist): the local rows split into interior rows (owned columns only) and
   // boundary rows (at least one ghost column), each as a row-list copy (Sorted layout,
   // perm = output row), so the interior product runs while the halo is in flight

@@ -96,6 +96,15 @@ struct SpmmArgs {
   const int* done;
   const int* perm;  // balanced row order: CSR arrays are in sorted order, output row = perm[row]
   int team;         // narrow rows: a team of lanes per row (long / irregular rows) instead of a lane per row
+  // SELL-32-sigma form (narrow blocks on irregular operators; null: not used): chunk c holds the
+  // entries of 32 rows column-major at [cs[c], cs[c + 1]) (width = that / 32, padding column -1),
+  // row[32 c + lane] = the output row (-1: none), order = chunks by decreasing width (or null)
+  const int* sell_cs;
+  const int* sell_ci;
+  const void* sell_val;
+  const int* sell_row;
+  const int* sell_order;
+  long long sell_nchunk;
 };
 
 // s x s Gram Y^H X on the FP64 tensor cores (gram_mma.cu); the real view of the
@@ -120,6 +129,7 @@ struct BsrArgs {
   const void* P;
   void* Q;
   long long nb;
+  const int* order;  // visiting order of the block rows (a permutation of [0, nb)) or null
   int unit_diag;    // Q_I += P_I (identity diagonal blocks not stored)
   const int* done;
   // fused epilogue reductions over X = Q (NORM2, COLNORM2, DIAG, TRACE, SUMVEC)

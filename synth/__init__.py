@@ -358,6 +358,17 @@ def lattice_4d_bsr(L: int, kappa: float = 0.12, seed: int = 3, dof: int = 12, ch
     return brp, bcol, blocks
 
 
+def lattice_tile_order(L: int, w: int) -> np.ndarray:
+    """Visiting order of the L^4 lattice sites (site = x + L y + L^2 z + L^3 t) that walks one
+    tile of w z-planes through every t before the next tile: the +-t neighbours of a site are
+    then w planes (w L^2 sites) apart in the order instead of L planes (index arithmetic only;
+    the traversal hint of srk_matrix_set_row_order)."""
+    if L % w:
+        raise ValueError("w must divide L")
+    zt, t, zi, yx = np.meshgrid(np.arange(L // w), np.arange(L), np.arange(w), np.arange(L * L), indexing="ij")
+    return (yx + L * L * (zt * w + zi) + L ** 3 * t).reshape(-1).astype(np.int32)
+
+
 def input_hash(A: CSR, B: np.ndarray) -> str:
     h = hashlib.sha256()
     for arr in (A.row_ptr, A.col_idx, A.values, B):

@@ -321,6 +321,41 @@ def test_bsr_spmm_reductions(srk, mode):
     assert rel(g.reshape(ref.shape), ref) < 1e-12
 
 
+@pytest.mark.parametrize("L,w", [(4, 2), (8, 2), (8, 4)])
+def test_bsr_row_order_hint(srk, L, w):
+    """srk_matrix_set_row_order: a visiting order of the block rows changes the schedule only —
+    Q is bitwise the natural-order product (and matches the oracle), the fused trace equals the
+    oracle's to rounding; a non-permutation and a wrong length are rejected; None restores."""
+    brp, bcol, blocks = synth.lattice_4d_bsr(L)
+    M = srk.Matrix.from_bsr(brp, bcol, blocks, unit_diag=True)
+    n = L ** 4 * 12
+    P = synth.random_rhs(n, 12, 7, True)
+    Y = synth.random_rhs(n, 12, 9, True)
+    Q0, t0 = srk.spmm_block(M, to_dev(P), gram="trace", Y=to_dev(Y))
+    Q0, t0 = to_np(Q0), to_np(t0)
+    order = synth.lattice_tile_order(L, w)
+    assert np.array_equal(np.sort(order), np.arange(L ** 4))
+    M.set_row_order(order)
+    Q1, t1 = srk.spmm_block(M, to_dev(P), gram="trace", Y=to_dev(Y))
+    Q1, t1 = to_np(Q1), to_np(t1)
+    assert np.array_equal(Q1, Q0)
+    ref = OL.trace_inner(Q0, Y)
+    assert abs(t1[0] - ref) <= 1e-12 * abs(ref) and abs(t0[0] - ref) <= 1e-12 * abs(ref)
+    if L == 4:
+        As = synth.lattice_4d(4).to_scipy()
+        assert np.max(np.abs(Q1 - As @ P)) <= 1e-13 * np.max(np.abs(Q1))
+    bad = order.copy()
+    bad[0] = bad[1]
+    with pytest.raises(srk.SrkError):
+        M.set_row_order(bad)
+    with pytest.raises(srk.SrkError):
+        M.set_row_order(order[:-1])
+    M.set_row_order(None)
+    assert np.array_equal(to_np(srk.spmm_block(M, to_dev(P))), Q0)
+    with pytest.raises(srk.SrkError):  # block-sparse operators only
+        srk.Matrix.from_csr(synth.conv_diff_2d(8, (20.0, 20.0))).set_row_order(np.arange(64))
+
+
 def test_bsr_rejects_invalid(srk):
     brp, bcol, blocks = synth.lattice_4d_bsr(3)
     bad = bcol.copy()
