@@ -32,6 +32,7 @@ namespace {
 constexpr int BS = 12;         // block size (rows = cols)
 constexpr int BROW = 28;       // smem row stride of a staged block (doubles): 24 + 4 pad, 2-way banks
 constexpr int BBLK = BS * BROW;  // doubles per staged block
+constexpr int BSR_CFG_DEFAULT = 3;  // see launch_s (measured: scripts/bsr_probe.py, profiles/r02_bsr_probe.txt)
 
 // 16-byte async copy with an L2 eviction policy: the blocks of A stream through
 // once (evict_first) while the rows of P are re-read by the neighbouring block rows
@@ -293,18 +294,24 @@ __global__ void __launch_bounds__(256, S >= 16 ? 1 : 2) bsr12_kernel(BsrArgs a) 
 // (`cp.async.bulk`, one per lane: the block + 12 rows) into a per-warp two-stage mbarrier ring
 // that runs ahead across block-row boundaries (the next row's first block is in flight during
 // this row's last).
-template <int S>
+template <int S, int NWARP = 8, int NSTAGE = 2, bool EST = false, bool PAD = true>
 struct B2Cfg {
   static constexpr int NR = 2 * S;
   static constexpr int NP = NR / 16;         // N-tile pairs
   static constexpr int NS = (NR % 16) / 8;   // single N tile (4 complex columns)
   static constexpr int NC = 2 * NP + NS;     // complex columns a lane owns per row
-  static constexpr int PST = NR + 4;         // staged P row stride (doubles): = 4 or 12 mod 16
+  // staged P row stride (doubles): NR + 4 (= 4 or 12 mod 16: conflict-free fragment loads, one copy
+  // per row) or NR (one copy per block, 2-way conflicts on the P fragments)
+  static constexpr int PST = PAD ? NR + 4 : NR;
+  static constexpr bool PADDED = PAD;
   static constexpr int ABLK = BS * BS * 2;   // 288 doubles, unpadded
   static constexpr int STAGE = ABLK + BS * PST;
-  static constexpr int NSTG = 2;
-  static constexpr int WARPS = 8;
-  static constexpr int SMEM = WARPS * NSTG * STAGE * 8 + WARPS * NSTG * 8;
+  static constexpr int NSTG = NSTAGE;         // ring stages per warp
+  static constexpr int WARPS = NWARP;
+  static constexpr bool ESTG = EST;           // epilogue operands (P_I, Y_I) staged by bulk copy too
+  static constexpr int EBUF = EST ? 2 * BS * NR : 0;  // doubles per warp
+  static constexpr int WARP_D = NSTG * STAGE + EBUF;
+  static constexpr int SMEM = WARPS * WARP_D * 8 + WARPS * (NSTG + 1) * 8;
 };
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
@@ -326,14 +333,16 @@ __device__ __forceinline__ void bulk_g2s(double* dst, const double* src, unsigne
       : "memory");
 }
 
-template <int S>
-__global__ void __launch_bounds__(256, S >= 16 ? 1 : 2) bsr12_kernel2(BsrArgs a) {
+template <int S, int NWARP, int NSTAGE, bool EST, bool PAD>
+__global__ void __launch_bounds__(32 * NWARP, S >= 16 ? 1 : 2) bsr12_kernel2(BsrArgs a) {
   if (a.done && *a.done) return;
-  using C = B2Cfg<S>;
+  using C = B2Cfg<S, NWARP, NSTAGE, EST, PAD>;
   extern __shared__ __align__(16) double bsm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double* wbuf = bsm + (size_t)warp * C::NSTG * C::STAGE;
-  unsigned long long* bars = reinterpret_cast<unsigned long long*>(bsm + (size_t)C::WARPS * C::NSTG * C::STAGE) + warp * C::NSTG;
+  double* wbuf = bsm + (size_t)warp * C::WARP_D;
+  double* ebuf = wbuf + (size_t)C::NSTG * C::STAGE;  // [P_I rows | Y_I rows] (ESTG)
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(bsm + (size_t)C::WARPS * C::WARP_D) + warp * (C::NSTG + 1);
+  unsigned long long* ebar = bars + C::NSTG;
   const double* __restrict__ val = reinterpret_cast<const double*>(a.val);
   const double* __restrict__ P = reinterpret_cast<const double*>(a.P);
   double* __restrict__ Q = reinterpret_cast<double*>(a.Q);
@@ -344,7 +353,7 @@ __global__ void __launch_bounds__(256, S >= 16 ? 1 : 2) bsr12_kernel2(BsrArgs a)
   const unsigned long long pol_a = policy_evict_first(), pol_p = policy_evict_last();
 
   if (lane == 0) {
-    for (int q = 0; q < C::NSTG; ++q) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bars + q)));
+    for (int q = 0; q <= C::NSTG; ++q) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bars + q)));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncwarp();
@@ -376,20 +385,31 @@ __global__ void __launch_bounds__(256, S >= 16 ? 1 : 2) bsr12_kernel2(BsrArgs a)
     const int st = (int)(cnt % C::NSTG);
     double* bs = wbuf + (size_t)st * C::STAGE;
     unsigned long long* bar = bars + st;
-    if (lane == 0) {
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-                   "r"(ABYTES + BS * PBYTES)
-                   : "memory");
-      bulk_g2s(bs, val + (size_t)jp * C::ABLK, ABYTES, bar, pol_a);
-    } else if (lane <= BS) {
-      const double* pj = P + ((size_t)__ldg(a.bci + jp) * BS + (lane - 1)) * C::NR;
-      bulk_g2s(bs + C::ABLK + (lane - 1) * C::PST, pj, PBYTES, bar, pol_p);
+    if constexpr (C::PADDED) {
+      // (a bulk copy is a per-warp instruction with uniform operands: copies issued by different
+      // lanes are serialised by a loop over the active lanes, ~10 instructions per copy)
+      if (lane == 0) {
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                     "r"(ABYTES + BS * PBYTES)
+                     : "memory");
+        bulk_g2s(bs, val + (size_t)jp * C::ABLK, ABYTES, bar, pol_a);
+      } else if (lane <= BS) {
+        const double* pj = P + ((size_t)__ldg(a.bci + jp) * BS + (lane - 1)) * C::NR;
+        bulk_g2s(bs + C::ABLK + (lane - 1) * C::PST, pj, PBYTES, bar, pol_p);
+      }
+    } else {
+      if (lane == 0) {  // two copies per block: the block and its 12 contiguous P rows
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                     "r"(ABYTES + BS * PBYTES)
+                     : "memory");
+        bulk_g2s(bs, val + (size_t)jp * C::ABLK, ABYTES, bar, pol_a);
+        bulk_g2s(bs + C::ABLK, P + (size_t)__ldg(a.bci + jp) * BS * C::NR, BS * PBYTES, bar, pol_p);
+      }
     }
     ++jp;
     seek();
   };
-  unsigned issued = 0, used = 0;
-  if (Ip < nb) issue(issued++);
+  unsigned issued = 0, used = 0, rows_done = 0;
 
   // complex column of owned slot ci
   auto ccol = [&](int ci) { return ci < 2 * C::NP ? 8 * (ci >> 1) + 2 * fk + (ci & 1) : 8 * C::NP + fk; };
@@ -422,22 +442,40 @@ __global__ void __launch_bounds__(256, S >= 16 ? 1 : 2) bsr12_kernel2(BsrArgs a)
       for (int j = 0; j < C::NP; ++j) accP[mt][j][0][0] = accP[mt][j][0][1] = accP[mt][j][1][0] = accP[mt][j][1][1] = 0.0;
       accS[mt][0] = accS[mt][1] = 0.0;
     }
-    // the unit-diagonal operand P_I requested now, consumed after the row's last block (the
-    // reduction operands are read in the epilogue: prefetching them too spilled at S = 12)
-    double2 pI[2][C::NC];
+    // epilogue operands requested now, consumed after the row's last block: the unit-diagonal
+    // operand P_I and reduction 0's Y rows (or y entries) — by bulk copy into the warp's epilogue
+    // buffer (ESTG), else P_I in registers and Y read in the epilogue (prefetching both in
+    // registers spilled at S = 12)
+    const int md0 = rmode[0];
+    const bool y0rows = md0 == RED_DIAG || md0 == RED_TRACE, y0vec = md0 == RED_SUMVEC;
+    double2 pI[2][C::ESTG ? 1 : C::NC];
+    if constexpr (C::ESTG) {
+      constexpr unsigned RB = BS * C::NR * 8;
+      if (lane == 0) {
+        const unsigned bytes = (a.unit_diag ? RB : 0u) + (y0rows ? RB : (y0vec ? (unsigned)(BS * 16) : 0u));
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(ebar)), "r"(bytes) : "memory");
+        if (a.unit_diag) bulk_g2s(ebuf, P + (size_t)I * BS * C::NR, RB, ebar, pol_p);
+      } else if (lane == 1) {
+        if (y0rows) bulk_g2s(ebuf + BS * C::NR, ry[0] + (size_t)I * BS * C::NR, RB, ebar, pol_a);
+        else if (y0vec) bulk_g2s(ebuf + BS * C::NR, ry[0] + (size_t)I * BS * 2, BS * 16, ebar, pol_a);
+      }
+    } else {
 #pragma unroll
-    for (int m = 0; m < 2; ++m) {
-      const int row = m ? 8 + (fr >> 1) : fr;
-      const bool act = m ? own2 : true;
-      const size_t base = ((size_t)I * BS + row) * C::NR;
+      for (int m = 0; m < 2; ++m) {
+        const int row = m ? 8 + (fr >> 1) : fr;
+        const bool act = m ? own2 : true;
+        const size_t base = ((size_t)I * BS + row) * C::NR;
 #pragma unroll
-      for (int ci = 0; ci < C::NC; ++ci) {
-        pI[m][ci] = make_double2(0.0, 0.0);
-        if (act && a.unit_diag) pI[m][ci] = __ldg(reinterpret_cast<const double2*>(P + base + 2 * ccol(ci)));
+        for (int ci = 0; ci < C::NC; ++ci) {
+          pI[m][ci] = make_double2(0.0, 0.0);
+          if (act && a.unit_diag) pI[m][ci] = __ldg(reinterpret_cast<const double2*>(P + base + 2 * ccol(ci)));
+        }
       }
     }
     for (int j = jb; j < je; ++j) {
-      if (Ip < nb) issue(issued++);  // the next block (this or a later row) into the other stage
+      // keep the ring full: blocks used .. used + NSTG - 1 (this row's or later rows'); the stage of
+      // block used - 1 was released by the __syncwarp that ended its multiplication
+      while (Ip < nb && issued < used + C::NSTG) issue(issued++);
       const int st = (int)(used % C::NSTG);
       mbar_wait(bars + st, (used / C::NSTG) & 1);
       ++used;
@@ -486,6 +524,8 @@ __global__ void __launch_bounds__(256, S >= 16 ? 1 : 2) bsr12_kernel2(BsrArgs a)
       const double xo = __shfl_xor_sync(0xffffffffu, x2, 4), yo = __shfl_xor_sync(0xffffffffu, y2, 4);
       q[1][ci] = make_double2(x2 - yo, y2 + xo);  // meaningful in the even-fr lanes (B_r there, B_i in lane ^ 4)
     }
+    if constexpr (C::ESTG) mbar_wait(ebar, rows_done & 1);
+    ++rows_done;
 #pragma unroll
     for (int m = 0; m < 2; ++m) {
       const int row = m ? 8 + (fr >> 1) : fr;
@@ -496,8 +536,9 @@ __global__ void __launch_bounds__(256, S >= 16 ? 1 : 2) bsr12_kernel2(BsrArgs a)
         const int col = 2 * ccol(ci);
         double2 v = q[m][ci];
         if (a.unit_diag) {
-          v.x += pI[m][ci].x;
-          v.y += pI[m][ci].y;
+          const double2 pi = C::ESTG ? *reinterpret_cast<const double2*>(ebuf + row * C::NR + col) : pI[m][C::ESTG ? 0 : ci];
+          v.x += pi.x;
+          v.y += pi.y;
         }
         *reinterpret_cast<double2*>(Q + base + col) = v;
 #pragma unroll
@@ -509,8 +550,12 @@ __global__ void __launch_bounds__(256, S >= 16 ? 1 : 2) bsr12_kernel2(BsrArgs a)
             if (md == RED_NORM2) rs[r].x += q2;
             else rc[r][ci].x += q2;
           } else {
-            const double2 y = md == RED_SUMVEC ? __ldg(reinterpret_cast<const double2*>(ry[r]) + (size_t)I * BS + row)
-                                               : __ldg(reinterpret_cast<const double2*>(ry[r] + base + col));
+            double2 y;
+            if (C::ESTG && r == 0)
+              y = *reinterpret_cast<const double2*>(ebuf + BS * C::NR + (md == RED_SUMVEC ? 2 * row : row * C::NR + col));
+            else
+              y = md == RED_SUMVEC ? __ldg(reinterpret_cast<const double2*>(ry[r]) + (size_t)I * BS + row)
+                                   : __ldg(reinterpret_cast<const double2*>(ry[r] + base + col));
             const double2 pr = make_double2(y.x * v.x + y.y * v.y, y.x * v.y - y.y * v.x);
             if (md == RED_DIAG) {
               rc[r][ci].x += pr.x;
@@ -523,6 +568,7 @@ __global__ void __launch_bounds__(256, S >= 16 ? 1 : 2) bsr12_kernel2(BsrArgs a)
         }
       }
     }
+    if constexpr (C::ESTG) __syncwarp();  // the epilogue buffer is rewritten by the next row's request
   }
   if (nred == 0) return;
   __syncthreads();  // every warp is done with its staging buffers
@@ -574,28 +620,64 @@ __global__ void __launch_bounds__(256, S >= 16 ? 1 : 2) bsr12_kernel2(BsrArgs a)
   }
 }
 
-template <int S>
-int launch_s(const BsrArgs& a, int grid, cudaStream_t st) {
-  using C = BCfg<S>;
-  using C2 = B2Cfg<S>;
-  const bool old = getenv("SRK_BSR_OLD") != nullptr;  // A/B switch (read per launch): the padded [B_r B_i] * lift(P) form
+template <int S, int NWARP, int NSTAGE, bool EST, bool PAD = true>
+int launch_k2(const BsrArgs& a, int grid, cudaStream_t st) {
+  using C2 = B2Cfg<S, NWARP, NSTAGE, EST, PAD>;
   static std::atomic<unsigned long long> attr{0};
-  if (first_on_device(attr)) {
-    cudaFuncSetAttribute(bsr12_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-    cudaFuncSetAttribute(bsr12_kernel2<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, C2::SMEM);
-  }
-  if (grid < 0) {  // resident CTAs per SM
+  if (first_on_device(attr))
+    cudaFuncSetAttribute(bsr12_kernel2<S, NWARP, NSTAGE, EST, PAD>, cudaFuncAttributeMaxDynamicSharedMemorySize, C2::SMEM);
+  if (grid < 0) {  // resident warps per SM
     int occ = 0;
-    if (old) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bsr12_kernel<S>, 256, C::SMEM);
-    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bsr12_kernel2<S>, 256, C2::SMEM);
-    return occ;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bsr12_kernel2<S, NWARP, NSTAGE, EST, PAD>, 32 * NWARP, C2::SMEM);
+    return occ * NWARP;
   }
-  if (old) bsr12_kernel<S><<<grid, 256, C::SMEM, st>>>(a);
-  else bsr12_kernel2<S><<<grid, 256, C2::SMEM, st>>>(a);
+  bsr12_kernel2<S, NWARP, NSTAGE, EST, PAD><<<grid, 32 * NWARP, C2::SMEM, st>>>(a);
   return (int)cudaGetLastError();
 }
 
+// launch configuration of the M = 24 form: (warps per CTA, ring stages per warp, epilogue staging).
+// SRK_BSR_CFG selects one for measurements (scripts/bsr_probe.py); read per launch.
+static int bsr_cfg() {
+  const char* e = getenv("SRK_BSR_CFG");
+  return e ? atoi(e) : BSR_CFG_DEFAULT;
+}
+
+template <int S>
+int launch_s(const BsrArgs& a, int grid, cudaStream_t st) {
+  using C = BCfg<S>;
+  const bool old = getenv("SRK_BSR_OLD") != nullptr;  // A/B switch (read per launch): the padded [B_r B_i] * lift(P) form
+  if (old) {
+    static std::atomic<unsigned long long> attr{0};
+    if (first_on_device(attr)) cudaFuncSetAttribute(bsr12_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    if (grid < 0) {
+      int occ = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bsr12_kernel<S>, 256, C::SMEM);
+      return occ * 8;
+    }
+    bsr12_kernel<S><<<grid, 256, C::SMEM, st>>>(a);
+    return (int)cudaGetLastError();
+  }
+  switch (bsr_cfg()) {
+    case 1: return launch_k2<S, 8, 2, false, false>(a, grid, st);  // one P copy per block (unpadded)
+    case 2: return launch_k2<S, 6, 2, true, true>(a, grid, st);
+    case 3: return launch_k2<S, 6, 2, true, false>(a, grid, st);
+    case 4: return launch_k2<S, 6, 3, false, false>(a, grid, st);
+    case 5: return launch_k2<S, 4, 4, true, true>(a, grid, st);     // fewer warps, deeper ring (measured slower)
+    default: return launch_k2<S, 8, 2, false, true>(a, grid, st);
+  }
+}
+
 }  // namespace
+
+// warps per CTA of the configuration a launch will use (the engine sizes the grid with it)
+int bsr_warps_per_cta() {
+  if (getenv("SRK_BSR_OLD")) return 8;
+  switch (bsr_cfg()) {
+    case 2: case 3: case 4: return 6;
+    case 5: return 4;
+    default: return 8;
+  }
+}
 
 bool bsr_supported(int bs, bool cplx, int s) { return bs == BS && cplx && (s == 4 || s == 8 || s == 12 || s == 16); }
 

@@ -527,10 +527,10 @@ int Eng::spmm_bsr(bool adj, const void* P, void* Q, int s, const std::vector<RQ>
   a.order = A->border;
   a.unit_diag = A->unit_diag;
   a.done = done;
-  static int occ = 0;
-  if (occ == 0) occ = std::max(1, launch_bsr(a, s, -1, nullptr));
-  const long long need = (A->nb + 7) / 8;  // one warp per block row, 8 warps per CTA
-  const int grid = (int)std::max<long long>(1, std::min<long long>(need, (long long)c->nsm * occ));
+  const int wpc = bsr_warps_per_cta();  // one warp per block row
+  const int wsm = std::max(wpc, launch_bsr(a, s, -1, nullptr));  // resident warps per SM
+  const long long need = (A->nb + wpc - 1) / wpc;
+  const int grid = (int)std::max<long long>(1, std::min<long long>(need, (long long)c->nsm * (wsm / wpc)));
   // the epilogue fuses every reduction except the s x s Gram (a separate pass below)
   std::vector<RQ> fused, rest;
   for (const RQ& q : reds) (q.mode == RED_FULL ? rest : fused).push_back(q);

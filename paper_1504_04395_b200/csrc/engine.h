@@ -20,7 +20,8 @@ int launch_spmm(bool cplx, int cap, bool full, const SpmmArgs& a, int grid, int 
 int launch_upd(bool cplx, int cap, bool full, const UpdArgs& a, int grid, int block, size_t smem, cudaStream_t st);
 int launch_fin(const FinArgs& a, cudaStream_t st);
 int launch_gram_mma(const GramArgs& g, int grid, cudaStream_t st);
-int launch_bsr(const BsrArgs& a, int s, int grid, cudaStream_t st);
+int launch_bsr(const BsrArgs& a, int s, int grid, cudaStream_t st);  // grid < 0: resident WARPS per SM
+int bsr_warps_per_cta();
 // block updates with s x s coefficients on the FP64 tensor cores (blk_mma.cu)
 int upd_mma_width(int w);
 size_t upd_mma_smem(int w, int nterm);

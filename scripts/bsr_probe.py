@@ -50,7 +50,17 @@ def main():
     Q = torch.empty_like(P)
     abytes = (nb + 1) * 4 + 8 * nb * (4 + 2304) + 2 * n * s * 16
     flops = 8.0 * nb * 8 * 12 * 12 * s
-    for w in [int(x) for x in os.environ.get("BSR_TILES", "0,2,4,8,16").split(",")]:
+    ref0 = None
+    for cfg in [int(x) for x in os.environ.get("BSR_CFGS", "0,1,2,3,4,5").split(",")]:
+        os.environ["SRK_BSR_CFG"] = str(cfg)   # (warps per CTA, ring stages, epilogue staging): see bsr.cu launch_s
+        t = med_ms(lambda: srk.spmm_block(M, P, Q=Q), reps)
+        q = Q.clone()
+        tt = med_ms(lambda: srk.spmm_block(M, P, gram="trace", Y=Y, Q=Q), reps)
+        ref0 = q if ref0 is None else ref0
+        print(f"launch cfg {cfg}: {t:.3f} ms  {abytes / t / 1e6:.0f} GB/s  {flops / t / 1e9:.1f} TFLOP/s | with trace operand {tt:.3f} ms"
+              f" | bitwise equal to cfg 0: {bool(torch.equal(q, ref0))}", flush=True)
+    os.environ.pop("SRK_BSR_CFG", None)
+    for w in [int(x) for x in os.environ.get("BSR_TILES", "0,4").split(",")]:
         M.set_row_order(synth.lattice_tile_order(L, w) if w else None)
         t = med_ms(lambda: srk.spmm_block(M, P, Q=Q), reps)
         tt = med_ms(lambda: srk.spmm_block(M, P, gram="trace", Y=Y, Q=Q), reps)

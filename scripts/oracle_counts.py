@@ -42,6 +42,10 @@ def main(cfg, method, order="blas"):
     if cfg.startswith("cfg"):
         A, B = synth.make_config(int(cfg[3:]))
         path = os.path.join(ROOT, "tests", "golden", "oracle_counts.json")
+    elif cfg.startswith("c"):  # "c<cfg>m<k>": that config's operator and right-hand sides at grid size k
+        num, mm = cfg[1:].split("m")
+        A, B = synth.make_config(int(num), m=int(mm))
+        path = os.path.join(ROOT, "profiles", "r02_count_ensemble.json")
     else:  # "m<k>": config 3's operator and right-hand sides at k^3 (the count-ensemble study)
         A = synth.conv_diff_3d(int(cfg[1:]), (50.0, 30.0, 10.0))
         B = synth.random_rhs(A.n, 16, 2)
