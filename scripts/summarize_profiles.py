@@ -6,7 +6,7 @@
 Captures: prof_spmm (config 3 SpMM), prof_upd (config 3's dominant 6-in / 4-out update),
 prof_bsr (config 4 BSR-12 product), prof_gram (s = 64 CTA-tiled DMMA Gram), prof_updmma
 (config 2 tensor-core block update), prof_gramwarp (config 2 per-warp Gram of a block with
-itself), prof_small (config 1's single-CTA eGl-BiCG iteration kernel; a launch covers the
+itself), prof_plane (config 3's plane-marching SpMM), prof_small (config 1's single-CTA eGl-BiCG iteration kernel; a launch covers the
 iterations between two polls). Reads gpurun_out/launches.csv (ncu --metrics gpu__time_duration.sum launch list of
 `python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu`), gpurun_out/prof_*.ncu-rep
 (`ncu --set full`) and gpurun_out/bench.log, and writes
@@ -51,8 +51,9 @@ def to_bytes(v, unit):
 
 def main(tag, pre=""):
     os.makedirs(PROF, exist_ok=True)
-    summary = {}
-    for name in ("spmm", "upd", "bsr", "gram", "updmma", "gramwarp", "small", "band"):
+    spath = os.path.join(PROF, f"{tag}_ncu_summary.json")
+    summary = json.load(open(spath)) if os.path.exists(spath) else {}  # later captures of a round update the file
+    for name in ("spmm", "upd", "bsr", "gram", "updmma", "gramwarp", "small", "band", "plane"):
         rep = os.path.join(OUT, f"{pre}prof_{name}.ncu-rep")
         if not os.path.exists(rep):
             continue
@@ -64,9 +65,11 @@ def main(tag, pre=""):
         rd = to_bytes(v["dram__bytes_read.sum"], u["dram__bytes_read.sum"])
         wr = to_bytes(v["dram__bytes_write.sum"], u["dram__bytes_write.sum"])
         summary[name]["dram_bytes_per_launch"] = rd + wr
-    json.dump(summary, open(os.path.join(PROF, f"{tag}_ncu_summary.json"), "w"), indent=1)
+    json.dump(summary, open(spath, "w"), indent=1)
     tj = {"source": f"profiles/{tag}_ncu_summary.json (ncu --set full, one launch, cold cache)"}
-    if "spmm" in summary:
+    if "plane" in summary:  # config 3's SpMM is the plane-marching kernel since round 2
+        tj["cfg3_egl_qmr_spmm"] = summary["plane"]["dram_bytes_per_launch"]
+    elif "spmm" in summary:
         tj["cfg3_egl_qmr_spmm"] = summary["spmm"]["dram_bytes_per_launch"]
     if "upd" in summary:  # the 6-input / 4-output update: the dominant kernel of the eGl-QMR step
         tj["cfg3_egl_qmr_dominant"] = summary["upd"]["dram_bytes_per_launch"]
