@@ -55,7 +55,7 @@ __device__ __forceinline__ void issue_stage(const UpdArgs& a, int nin, int w, lo
 }
 
 template <int W>
-__global__ void __launch_bounds__(256, 2) upd_mma_kernel(UpdArgs a, int cplx, int nterm, int stg, int nring) {
+__global__ void __launch_bounds__(256, 2) upd_mma_kernel(UpdArgs a, int cplx, int nterm, int stg) {
   if (a.done && *a.done) return;
   constexpr int NT = W / 8;   // 8-column tiles
   extern __shared__ __align__(16) double msm[];
@@ -126,9 +126,7 @@ __global__ void __launch_bounds__(256, 2) upd_mma_kernel(UpdArgs a, int cplx, in
   const long long nfull = n / 8;  // tiles with 8 live rows: the ones staged by bulk copies
   const long long nwarps = (long long)gridDim.x * (blockDim.x >> 5);
   // per-warp ring of stg stages (stg = 0: inputs read straight from global memory)
-  // (the first nring inputs go through the ring; with 6 inputs two stages of all of them do not
-  // fit beside a second CTA, so the last input is read from global memory)
-  const size_t stage_len = (size_t)nring * 8 * w;
+  const size_t stage_len = (size_t)nin * 8 * w;
   double* ring = msm + (size_t)nterm * W * W + (size_t)warp * stg * stage_len;
   unsigned long long* bars =
       reinterpret_cast<unsigned long long*>(msm + (size_t)nterm * W * W + (size_t)(blockDim.x >> 5) * stg * stage_len) +
@@ -143,7 +141,7 @@ __global__ void __launch_bounds__(256, 2) upd_mma_kernel(UpdArgs a, int cplx, in
   if (stg && lane == 0)
     for (int q = 0; q < stg; ++q) {
       const long long t = first + q * nwarps;
-      if (t < nfull) issue_stage(a, nring, w, t, ring + q * stage_len, bars + q);
+      if (t < nfull) issue_stage(a, nin, w, t, ring + q * stage_len, bars + q);
     }
   // reduction accumulators (per lane): scalar modes in rs, per-column modes in rc[nt][pair]
   int rmode[MAX_RED], rx[MAX_RED], ry[MAX_RED];
@@ -171,7 +169,7 @@ __global__ void __launch_bounds__(256, 2) upd_mma_kernel(UpdArgs a, int cplx, in
     if (piped) mbar_wait_parity(bars + stage, (unsigned)((k / stg) & 1));
     // input b's row for this lane: the staged tile, or global memory
     auto in_row = [&](int b) -> const double* {
-      return (piped && b < nring) ? ring + stage * stage_len + (size_t)b * 8 * w + (size_t)fr * w
+      return piped ? ring + stage * stage_len + (size_t)b * 8 * w + (size_t)fr * w
                    : reinterpret_cast<const double*>(a.in[b]) + (size_t)row * w;
     };
     double acc[MAX_OUT][NT][2];
@@ -332,7 +330,7 @@ __global__ void __launch_bounds__(256, 2) upd_mma_kernel(UpdArgs a, int cplx, in
       const long long nt = tile + (long long)stg * nwarps;
       if (lane == 0 && nt < nfull) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        issue_stage(a, nring, w, nt, ring + stage * stage_len, bars + stage);
+        issue_stage(a, nin, w, nt, ring + stage * stage_len, bars + stage);
       }
     }
   }
@@ -398,8 +396,7 @@ __global__ void __launch_bounds__(256, 2) upd_mma_kernel(UpdArgs a, int cplx, in
 // stages of the per-warp input ring: as many as fit (up to 4) in half an SM's shared
 // memory, so that two CTAs stay resident; 0 (direct global loads) when fewer than 2 fit
 // or an input is not 16-byte aligned (bulk-copy requirement). SRK_UPD_STAGES overrides.
-int pick_stages(const UpdArgs& a, int w, int W, int nterm, int* nring) {
-  *nring = a.nin;
+int pick_stages(const UpdArgs& a, int w, int W, int nterm) {
   if (a.nin == 0) return 0;
   for (int b = 0; b < a.nin; ++b)
     if (reinterpret_cast<uintptr_t>(a.in[b]) & 15) return 0;
@@ -407,20 +404,11 @@ int pick_stages(const UpdArgs& a, int w, int W, int nterm, int* nring) {
     const char* e = getenv("SRK_UPD_STAGES");
     return e ? atoi(e) : -1;
   }();
+  const size_t per = (size_t)8 * a.nin * 8 * w * 8 + 8;  // 8 warps, one stage each, + mbarrier
   const size_t budget = 110 * 1024 - (size_t)nterm * W * W * 8;
-  // all inputs through the ring when two stages fit; otherwise as many inputs as two stages hold
-  // (6 inputs at w = 16: five staged, the sixth read directly — it ran without a ring before)
-  for (int nr = a.nin; nr >= std::max(1, a.nin - 2); --nr) {
-    const size_t per = (size_t)8 * nr * 8 * w * 8 + 8;  // 8 warps, one stage each, + mbarrier
-    int stg = (int)std::min<size_t>(4, budget / per);
-    if (env >= 0 && nr == a.nin) stg = env;
-    if (stg >= 2) {
-      *nring = nr;
-      return stg;
-    }
-    if (env >= 0) break;
-  }
-  return 0;
+  int stg = (int)std::min<size_t>(4, budget / per);
+  if (env >= 0) stg = env;
+  return stg >= 2 ? stg : 0;
 }
 
 size_t smem_bytes(int W, int w, int nterm, int nin, int stg) {
@@ -431,9 +419,8 @@ size_t smem_bytes(int W, int w, int nterm, int nin, int stg) {
 template <int W>
 int launch_w(const UpdArgs& a, int cplx, int nterm, int grid, cudaStream_t st) {
   const int w = a.s * (cplx ? 2 : 1);
-  int nring = a.nin;
-  const int stg = pick_stages(a, w, W, nterm, &nring);
-  const size_t smem = smem_bytes(W, w, nterm, nring, stg);
+  const int stg = pick_stages(a, w, W, nterm);
+  const size_t smem = smem_bytes(W, w, nterm, a.nin, stg);
   static std::atomic<unsigned long long> attr{0};
   if (first_on_device(attr)) {
     cudaFuncSetAttribute(upd_mma_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -443,7 +430,7 @@ int launch_w(const UpdArgs& a, int cplx, int nterm, int grid, cudaStream_t st) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, upd_mma_kernel<W>, 256, smem);
     return occ;
   }
-  upd_mma_kernel<W><<<grid, 256, smem, st>>>(a, cplx, nterm, stg, nring);
+  upd_mma_kernel<W><<<grid, 256, smem, st>>>(a, cplx, nterm, stg);
   return (int)cudaGetLastError();
 }
 
