@@ -80,3 +80,24 @@ def test_ex2_manufactured_solution_second_order():
         sol = spla.spsolve(A.to_scipy().tocsc(), B[:, 0])
         errs.append(np.max(np.abs(sol - u)))
     assert errs[1] < errs[0] / 3.0 and errs[1] < 5e-3
+
+
+def test_lattice_tile_order_is_a_tiled_permutation():
+    """synth.lattice_tile_order (the traversal hint of srk_matrix_set_row_order): a permutation of
+    the L^4 sites in which a site's +-t neighbours lie w planes apart and whole (x, y) planes stay
+    contiguous (index arithmetic only)."""
+    import numpy as np
+    import synth
+    L, w = 8, 2
+    o = synth.lattice_tile_order(L, w)
+    assert o.dtype == np.int32 and np.array_equal(np.sort(o), np.arange(L ** 4))
+    pos = np.empty(L ** 4, dtype=np.int64)
+    pos[o] = np.arange(L ** 4)
+    site = np.arange(L ** 4)
+    t = site // L ** 3
+    inner = t < L - 1
+    assert np.all(pos[site[inner] + L ** 3] - pos[site[inner]] == w * L * L)       # +t: w planes later
+    plane = o.reshape(-1, L * L)
+    assert np.all(plane - plane[:, :1] == np.arange(L * L))                         # planes contiguous
+    with __import__("pytest").raises(ValueError):
+        synth.lattice_tile_order(8, 3)
