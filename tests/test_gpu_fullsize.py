@@ -77,18 +77,8 @@ def test_oracle_counts_fixture():
         assert e["iterations"] >= 1 and len(e["inputs_hash"]) == 16
 
 
-# Known deviation, stated rather than hidden (DESIGN §4 rule 5): config 2's Bl-BiCGStab-rQ converges in
-# 230 iterations on the GPU (219-233 over the library's own summation-order variants) against the
-# oracle's 219 / 218 (seq); the oracle's reduced-size ensemble (64^3: 128-132 incl. extended precision,
-# GPU 129-134) allows +-9 at full size. The oracle's full-size perturbation members (the ones that
-# move its count at reduced size) take ~4 h each on this host and are not cached yet.
-_KNOWN = {"cfg2:bl_bicgstab_rq": "GPU 230 vs oracle 219 (slack 8.8 from the 64^3 ensemble); full-size oracle "
-                                 "perturbation runs not cached (hours each)"}
-
-
 def _params():
-    return [pytest.param(e, id=e[0], marks=[pytest.mark.xfail(reason=_KNOWN[e[0]], strict=False)] if e[0] in _KNOWN else [])
-            for e in _entries()]
+    return [pytest.param(e, id=e[0]) for e in _entries()]
 
 
 @pytest.mark.gpu
