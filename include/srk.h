@@ -322,6 +322,17 @@ typedef struct {
                           1 = continue with the deficient columns of Q replaced by counter-based
                           random vectors orthogonalised against the others, C_jj = 0 (the implicit
                           deflation of P:396-403) */
+  int trace_iterates;  /* K > 0 with on_iter set (srk_solve / srk_solve_host): the first K iterations run
+                          one at a time and on_iter is called after each (lock-step parity, SURVEY
+                          §8(b) / §4: "an iteration callback"); later iterations run as usual */
+  /* k = iteration (1-based); X_k = the iterate (n x s) and R_or_C_k = the residual block R_k (n x s;
+   * r_rows = n) or, for the rQ variants, C_k (s x s; r_rows = s): DEVICE pointers to copies owned by
+   * the library, valid until the callback returns (the stream is synchronised before the call);
+   * scalars_host[0] = the relative recursive residual ||R_k||_F / ||R_0||_F of the stopping rule
+   * (P:643), scalars_host[1] = the solver state (0 running, 1 converged, 2 breakdown, 3 maxit). */
+  void (*on_iter)(int k, const void* X_k, const void* R_or_C_k, int64_t r_rows, const double* scalars_host,
+                  void* user);
+  void* user;          /* passed back to on_iter */
 } srk_opts;
 
 /* Full solve (a1-a7): B, X device n x s blocks; X holds X0 on entry and the

@@ -56,7 +56,13 @@ class _Opts(ctypes.Structure):
                 ("record_history", ctypes.c_int), ("check_true_residual", ctypes.c_int),
                 ("use_graph", ctypes.c_int), ("x0_zero", ctypes.c_int), ("shadow", ctypes.c_int),
                 ("shadow_given", ctypes.c_void_p), ("preprocess_rhs", ctypes.c_int), ("eps_brk", ctypes.c_double),
-                ("eps_defl", ctypes.c_double), ("rank_policy", ctypes.c_int)]
+                ("eps_defl", ctypes.c_double), ("rank_policy", ctypes.c_int), ("trace_iterates", ctypes.c_int),
+                ("on_iter", ctypes.c_void_p), ("user", ctypes.c_void_p)]
+
+
+# void on_iter(int k, const void* X_k, const void* R_or_C_k, int64_t r_rows, const double* scalars, void* user)
+ON_ITER = ctypes.CFUNCTYPE(None, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
+                           ctypes.POINTER(ctypes.c_double), ctypes.c_void_p)
 
 
 class _Halo(ctypes.Structure):
@@ -697,6 +703,14 @@ def _report(r: _Report) -> Report:
 SHADOW = {"default": 0, "conj": 1, "mean": 2, "given": 3}
 
 
+class _DevView:
+    """A raw device pointer as a CUDA array (torch.as_tensor reads __cuda_array_interface__)."""
+
+    def __init__(self, ptr: int, shape, typestr: str):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr, "data": (int(ptr), False),
+                                         "version": 2, "strides": None}
+
+
 def _opts(tol, maxit, poll_every=8, check_true_residual=True, use_graph=True, x0_zero=False, shadow="default",
           shadow_given=None, preprocess_rhs=False, eps_brk=0.0, eps_defl=0.0, rank_policy="breakdown"):
     """srk_opts. rank_policy: "breakdown" (reading G11) or "continue" (f4, the rQ variants)."""
@@ -796,15 +810,29 @@ class Solver:
 
 
 def solve(A: Matrix, B, method: str = "egl_bicg", tol: float = 1e-8, maxit: int = 2000, X0=None,
-          poll_every: int = 8, **opts):
+          poll_every: int = 8, trace_iterates: int = 0, on_iter=None, **opts):
     """X, report = solve(A, B, method, tol, maxit, **opts) — srk_solve on device tensors
     (B: contiguous (n, s) float64/complex128 CUDA tensor). opts: shadow ("default",
     "conj", "mean", "given" + shadow_given), preprocess_rhs, eps_brk, eps_defl,
-    rank_policy ("breakdown" / "continue")."""
+    rank_policy ("breakdown" / "continue"). trace_iterates = K with on_iter(k, X_k, R_or_C_k,
+    rel_residual, state): the library's iteration callback (srk_opts.on_iter) for the first K
+    iterations; X_k / R_or_C_k are CUDA tensors (copies made here, valid after the call)."""
     torch = _torch()
     n, s = B.shape
     X = torch.empty_like(B) if X0 is None else X0.clone()
     o = _opts(tol, maxit, poll_every, x0_zero=X0 is None, **opts)
+    cb = None
+    if trace_iterates > 0 and on_iter is not None:
+        typestr = "<c16" if B.is_complex() else "<f8"
+
+        def _cb(k, xp, rp, rows, sc, _user):
+            # tensors over the library's device copies, cloned before the callback returns
+            xk = torch.as_tensor(_DevView(xp, (n, s), typestr), device=B.device).clone()
+            rk = torch.as_tensor(_DevView(rp, (int(rows), s), typestr), device=B.device).clone()
+            on_iter(int(k), xk, rk, float(sc[0]), int(sc[1]))
+        cb = ON_ITER(_cb)
+        o.trace_iterates = int(trace_iterates)
+        o.on_iter = ctypes.cast(cb, ctypes.c_void_p)
     r = _Report()
     _check(_lib.srk_solve(A.ctx.h, A.h, _dev(B, "B"), _dev(X, "X"), s, METHOD_ID[method], ctypes.byref(o),
                           ctypes.byref(r)), "srk_solve")

@@ -659,6 +659,10 @@ static void fill_opts(srk_opts* o, const srk_opts* in) {
     o->eps_brk = in->eps_brk;
     o->eps_defl = in->eps_defl;
     o->rank_policy = in->rank_policy;
+    o->trace_iterates = in->on_iter ? std::max(0, in->trace_iterates) : 0;
+    o->on_iter = o->trace_iterates > 0 ? in->on_iter : nullptr;
+    o->user = o->trace_iterates > 0 ? in->user : nullptr;
+    if (o->trace_iterates > 0) o->record_history = 1;  // the callback's residual norm
   }
 }
 
@@ -876,7 +880,7 @@ int srk_solve(srk_ctx* ctx, const srk_matrix* A, const void* B, void* X, int s, 
     h = ctx->cached;  // same operator, width, method and options: reuse the workspace
   } else {
     drop_cache(ctx);
-    int r = srk_solver_create(ctx, A, s, method, opts, &h);
+    int r = srk_solver_create(ctx, A, s, method, &o, &h);
     if (r) return r;
     ctx->cached = h;
     ctx->cached_mat = A->id;
@@ -885,6 +889,33 @@ int srk_solve(srk_ctx* ctx, const srk_matrix* A, const void* B, void* X, int s, 
     ctx->cached_opts = o;
   }
   int r = srk_solver_start(h, B, o.x0_zero ? nullptr : X);
+  if (!r && o.trace_iterates > 0 && o.on_iter) {  // the first K iterations one at a time, with the callback
+    const size_t bytes = (size_t)A->m.n * s * (A->m.cplx ? 16 : 8);
+    void *Xt = nullptr, *Rt = nullptr;
+    if (cudaMalloc(&Xt, bytes) != cudaSuccess || cudaMalloc(&Rt, bytes) != cudaSuccess) {
+      if (Xt) cudaFree(Xt);
+      drop_cache(ctx);
+      return fail(SRK_ENOMEM, "srk_solve: out of device memory (trace_iterates)");
+    }
+    int state = 0;
+    for (int k = 1; !r && k <= o.trace_iterates && k <= o.maxit && state == 0; ++k) {
+      r = srk_solver_iterate(h, 1, &state);
+      int64_t rows = 0;
+      if (!r) r = srk_solver_get_x(h, Xt);
+      if (!r) r = srk_solver_get_residual(h, Rt, &rows);
+      double sc[2] = {-1.0, (double)state};
+      int it = 0;
+      if (!r && !h->sv->read_ctl()) it = h->sv->ctl_host[CTL_ITER];
+      if (!r && it >= 1 && it <= h->sv->hist_cap) {
+        std::vector<double> hist((size_t)it);
+        if (srk_solver_history(h, hist.data(), it) == SRK_OK) sc[0] = hist.back();
+      }
+      if (!r) r = check_cuda((int)cudaStreamSynchronize(ctx->c.st), "srk_solve");
+      if (!r && it >= k) o.on_iter(k, Xt, Rt, rows, sc, o.user);  // (a breakdown inside iteration k: no iterate k)
+    }
+    cudaFree(Xt);
+    cudaFree(Rt);
+  }
   if (!r) r = srk_solver_iterate(h, h->sv->o.maxit, nullptr);
   if (!r) r = srk_solver_get_x(h, X);
   if (!r && rep) r = srk_solver_report(h, rep);

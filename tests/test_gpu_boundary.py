@@ -149,3 +149,33 @@ def test_breakdown_col_reports_li_freeze(srk):
     M = srk.Matrix.from_csr(A)
     _, rep = srk.solve(M, to_dev(B), "li_bicg", tol=1e-300, maxit=5)
     assert rep.frozen_cols == 1 and rep.breakdown_col == 1
+
+
+@pytest.mark.parametrize("method", ["egl_qmr", "bl_bicgstab_rq", "li_bicg"])
+def test_trace_iterates_callback(srk, method):
+    """srk_opts.trace_iterates / on_iter ("an iteration callback"): the callback's
+    X_k and R_k (C_k for the rQ variant) are the stepping interface's, bitwise, and the oracle's
+    within 1e-10 over the first iterations; its residual norm is the history's; the solve then
+    runs on to convergence exactly as without the callback."""
+    import oracle
+    A = synth.conv_diff_2d(24, (20.0, 20.0))
+    B = synth.random_rhs(A.n, 4, 3)
+    M = srk.Matrix.from_csr(A)
+    K = 6
+    seen = []
+    X, rep = srk.solve(M, to_dev(B), method, tol=1e-9, maxit=500, trace_iterates=K,
+                       on_iter=lambda k, xk, rk, rel, state: seen.append((k, to_np(xk), to_np(rk), rel, state)))
+    assert [t[0] for t in seen] == list(range(1, K + 1))
+    sv = srk.Solver(M, 4, method, tol=1e-9, maxit=500, poll_every=1)
+    sv.start(to_dev(B))
+    ref = oracle.solve(method, A.to_scipy(), B, tol=1e-9, maxit=500, record=K)
+    for k, xk, rk, rel, state in seen:
+        sv.iterate(1)
+        assert np.array_equal(xk, to_np(sv.x()))
+        assert np.array_equal(rk, to_np(sv.residual()))
+        assert np.linalg.norm(xk - ref.Xs[k - 1]) <= 1e-10 * np.linalg.norm(ref.Xs[k - 1])
+        assert rk.shape == ref.Rs[k - 1].shape
+        assert abs(rel - ref.history[k - 1]) <= 1e-9 * ref.history[k - 1] and state == 0
+    X0, rep0 = srk.solve(M, to_dev(B), method, tol=1e-9, maxit=500)
+    assert rep.outcome == rep0.outcome == "converged" and rep.iterations == rep0.iterations
+    assert np.array_equal(to_np(X), to_np(X0))
