@@ -34,6 +34,10 @@ constexpr int BAND_FMAX = 3;  // far diagonals staged per tile
 constexpr int BAND_DMAX = 8;  // pipeline stages (runtime D <= DMAX)
 constexpr int BAND_NWMAX = 16;  // consumer warps: 16 (1 CTA / SM) or 8 (2 CTAs / SM)
 
+struct BandOffs {
+  long long d[8];
+};
+
 struct BandArgs {
   const void* dia;  // the K diagonals row-major: [npad][K] (zero-padded)
   long long npad;
@@ -993,9 +997,73 @@ static int launch_plane_t(const BandArgs& ba, const Mat::Band& b, int nsm, cudaS
   return (int)cudaGetLastError();
 }
 
+
+// ---------------------------------------------------------------------------
+// Banded vector product (s = 1, no fused reduction): the economic variants' one A^H-vector
+// product per iteration. One row per thread, RT rows per thread, every load of a
+// thread's rows issued before the first FMA: the K diagonal values of row i (contiguous, [n][K]
+// row-major; a warp's 32 rows are one contiguous 32 K-value span, so the K strided loads of a warp
+// touch the same sectors: L1 hits after the first) and p[i + d_k], coalesced across the warp for
+// every k, whose K readers run within neighbouring tiles (L1 / L2 hits): DRAM = K values + p + q per
+// row (72 B for the 7-point stencil against 104 B for the CSR arrays). Summation in ascending
+// offset (= CSR order), as in the other band kernels. (A first version staged a CTA tile's values
+// through shared memory with two barriers per tile: 0.74 ms on config 3 against the CSR kernel's
+// 0.385 ms — the staging and the p loads ran back to back instead of overlapping.)
+template <typename T, int KT>
+__global__ void __launch_bounds__(256) band_vec_kernel(const T* __restrict__ dia, const T* __restrict__ p, T* __restrict__ q,
+                                                       long long n, int Krt, BandOffs offs, const int* done) {
+  if (done && *done) return;
+  constexpr int RT = 2;
+  const int K = KT > 0 ? KT : Krt;
+  constexpr int KM = KT > 0 ? KT : BAND_KMAX;
+  const long long stride = (long long)gridDim.x * 256 * RT;
+  for (long long r0 = (long long)blockIdx.x * 256 * RT; r0 < n; r0 += stride) {
+    T dv[RT][KM], pv[RT][KM];
+#pragma unroll
+    for (int u = 0; u < RT; ++u) {
+      const long long i = r0 + u * 256 + threadIdx.x;
+#pragma unroll
+      for (int k = 0; k < KM; ++k) {
+        const long long jj = i + offs.d[k];
+        const bool in = k < K && i < n;
+        dv[u][k] = in ? __ldcs(dia + i * K + k) : Ar<T>::zero();
+        pv[u][k] = (in && jj >= 0 && jj < n) ? __ldg(p + jj) : Ar<T>::zero();
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < RT; ++u) {
+      const long long i = r0 + u * 256 + threadIdx.x;
+      T acc = Ar<T>::zero();
+#pragma unroll
+      for (int k = 0; k < KM; ++k)
+        if (k < K) acc = Ar<T>::fma(dv[u][k], pv[u][k], acc);
+      if (i < n) q[i] = acc;
+    }
+  }
+}
+
+template <typename T>
+static int launch_band_vec(const BandArgs& a, int nsm, cudaStream_t st, int* grid_out) {
+  const long long need = (a.n + 511) / 512;
+  const int grid = (int)std::max<long long>(1, std::min<long long>(need, (long long)nsm * 8));
+  if (grid_out) {
+    *grid_out = grid;
+    return 0;
+  }
+  BandOffs offs{};
+  for (int k = 0; k < a.K; ++k) offs.d[k] = a.off[k];
+  const T* dia = reinterpret_cast<const T*>(a.dia);
+  const T* p = reinterpret_cast<const T*>(a.P);
+  T* q = reinterpret_cast<T*>(a.Q);
+  if (a.K == 7) band_vec_kernel<T, 7><<<grid, 256, 0, st>>>(dia, p, q, a.n, a.K, offs, a.done);
+  else if (a.K == 5) band_vec_kernel<T, 5><<<grid, 256, 0, st>>>(dia, p, q, a.n, a.K, offs, a.done);
+  else band_vec_kernel<T, 0><<<grid, 256, 0, st>>>(dia, p, q, a.n, a.K, offs, a.done);
+  return (int)cudaGetLastError();
+}
+
 bool band_supported(bool cplx, int s) {
   if (cplx) return s == 1 || s == 4 || s == 8;
-  return s == 2 || s == 4 || s == 8 || s == 16;
+  return s == 1 || s == 2 || s == 4 || s == 8 || s == 16;  // (s = 1 real: band_vec_kernel, no fused reduction)
 }
 
 
@@ -1009,6 +1077,16 @@ int launch_band(bool cplx, int s, const Mat::Band& b, const void* P, void* Q, lo
   a.dia = b.val;
   a.npad = b.npad;
   a.K = b.K;
+  static const bool no_vec = getenv("SRK_NO_BAND_VEC") != nullptr;  // A/B switch
+  if (s == 1 && !cplx) {  // the economic variants' vector product
+    if (nred > 0 || no_vec) return (int)cudaErrorNotSupported;
+    for (int k = 0; k < b.K; ++k) a.off[k] = b.off[k];
+    a.P = P;
+    a.Q = Q;
+    a.n = n;
+    a.done = done;
+    return launch_band_vec<double>(a, nsm, st, grid_out);
+  }
   if (band_plane_pattern(b)) {  // the 7-point pattern: the plane-marching kernel
     BandArgs pa = a;
     pa.P = P;
