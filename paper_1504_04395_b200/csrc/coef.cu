@@ -458,6 +458,16 @@ __device__ void qmr_scalar(const CoefArgs& a, int mode) {
         xi[c] = mkT(mode == 2 ? sqrt((double)s) * xin : xin, 0.0, T());
         W<T>(a, SL_GAMP)[c] = mkT(ga, 0.0, T());
         W<T>(a, SL_THETAP)[c] = mkT(th, 0.0, T());
+        if (mode != 0) {
+          // next iteration's 1/rho and c1 = xi delta/eps for the fused tail (QMR::seg): the arithmetic
+          // of phases 1-2 on the values they will see (rho, xi just set; K1 and eps of this iteration),
+          // without their breakdown tests — those phases still run and raise the flag before anything
+          // reads a P built from a non-finite coefficient
+          const T ir = cdiv(one<T>(), rho[c]), ix = cdiv(one<T>(), xi[c]);
+          const T dn = Ar<T>::mul(Ar<T>::mul(W<T>(a, SL_K1)[c], ir), ix);
+          W<T>(a, SL_INVRHO_N)[c] = ir;
+          W<T>(a, SL_C1_N)[c] = cdiv(Ar<T>::mul(xi[c], dn), W<T>(a, SL_EPS)[c]);
+        }
       }
     } else if (a.phase == 5) {
       if (mode == 0) li_all_frozen(a);

@@ -2,6 +2,7 @@
 // operator-preparation kernels (CSR validation and the
 // explicit A^H = conj(A)^T copy used by the BiCG/QMR families).
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
 
@@ -509,6 +510,37 @@ int Eng::upd(int s, std::vector<const void*> in, std::vector<OutSpec> outs, std:
   if (prof) prof->end(c->st);
   if (err) return err;
   return err = finish_reds(*this, reds, poffs, s, grid, a.pstride);
+}
+
+int Eng::qmr_tail(int s, void* P, void* D, const void* Pt, void* S, void* X, void* R, const void* Vt, int off_eta,
+                  int off_f, int off_invrho, int off_c1, int woff_r2) {
+  if (err) return err;
+  if (!qmr_tail_ok(s)) return err = (int)cudaErrorInvalidValue;
+  const size_t esz = cplx ? 16 : 8;
+  QmrTailArgs a{};
+  a.P = P; a.D = D; a.S = S; a.X = X; a.R = R; a.Pt = Pt; a.Vt = Vt;
+  a.units = (long long)((size_t)n * s * esz / 16);
+  a.ws = ws;
+  a.off_eta = off_eta; a.off_f = off_f; a.off_invrho = off_invrho; a.off_c1 = off_c1;
+  a.pstride = 1;
+  a.poff = 0;
+  a.done = done;
+  static std::atomic<int> occ_c[2] = {{0}, {0}};
+  int occ = occ_c[cplx].load();
+  if (occ == 0) {
+    occ = std::max(1, launch_qmr_tail(cplx, a, -1, nullptr));
+    occ_c[cplx].store(occ);
+  }
+  const long long need = std::max<long long>(1, (a.units + 255) / 256);
+  const int grid = (int)std::min<long long>(need, (long long)c->nsm * occ);  // one wave
+  if ((err = c->ensure_partials((size_t)grid))) return err;
+  a.partials = c->partials;
+  nlaunch++;
+  if (prof) prof->begin(PT_UPD, c->st, 16 * 7 + 5, 12.0 * (double)n * s * esz);
+  err = launch_qmr_tail(cplx, a, grid, c->st);
+  if (prof) prof->end(c->st);
+  if (err) return err;
+  return err = finish_reds(*this, {RQ{RED_NORM2, SRC_OUT + 3, -1, nullptr, woff_r2}}, {0}, s, grid, 1);
 }
 
 // Block-sparse operator: the BSR product, then the requested reductions over Q as

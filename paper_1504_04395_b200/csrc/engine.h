@@ -19,6 +19,7 @@ int padded_width(int cap, bool cplx);
 int launch_spmm(bool cplx, int cap, bool full, const SpmmArgs& a, int grid, int block, size_t smem, cudaStream_t st);
 int launch_upd(bool cplx, int cap, bool full, const UpdArgs& a, int grid, int block, size_t smem, cudaStream_t st);
 int launch_fin(const FinArgs& a, cudaStream_t st);
+int launch_qmr_tail(bool cplx, const QmrTailArgs& a, int grid, cudaStream_t st);  // grid < 0: resident CTAs per SM
 int launch_gram_mma(const GramArgs& g, int grid, cudaStream_t st);
 int launch_bsr(const BsrArgs& a, int s, int grid, cudaStream_t st);  // grid < 0: resident WARPS per SM
 int bsr_warps_per_cta();
@@ -227,6 +228,11 @@ struct Eng {
   int spmm_split(bool adj, const void* P, void* Q, int s, const std::vector<RQ>& reds, const Mat::Sorted& in,
                  long long ni, const Mat::Sorted& bd, long long nbd);
   int upd(int s, std::vector<const void*> in, std::vector<OutSpec> outs, std::vector<RQ> reds);
+  // Gl / eGl-QMR: (D, S, X, R) of this iteration and P of the next in one pass (qmr_tail.cu);
+  // offsets into ws of eta, f, 1/rho', c1' and of ||R||^2. qmr_tail_ok: the blocks are whole 16-byte units
+  bool qmr_tail_ok(int s) const { return ((n * (long long)s * (cplx ? 16 : 8)) % 16) == 0; }
+  int qmr_tail(int s, void* P, void* D, const void* Pt, void* S, void* X, void* R, const void* Vt, int off_eta,
+               int off_f, int off_invrho, int off_c1, int woff_r2);
   // s x s Gram Y^H X on the FP64 tensor cores (gram_mma.cu), written to ws + woff
   int gram_full(const void* X, const void* Y, int s, int woff);
   int spmm_bsr(bool adj, const void* P, void* Q, int s, const std::vector<RQ>& reds);

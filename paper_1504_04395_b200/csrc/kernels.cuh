@@ -139,6 +139,19 @@ struct BsrArgs {
   int pstride;
 };
 
+// Gl / eGl-QMR fused tail (qmr_tail.cu): D, S, X, R of iteration k and P of iteration k+1
+// in one pass over flat blocks of `units` 16-byte units; ||R||^2 into partials[cta*pstride + poff].
+struct QmrTailArgs {
+  void *P, *D, *S, *X, *R;   // read and rewritten
+  const void *Pt, *Vt;       // read
+  long long units;
+  const double* ws;
+  int off_eta, off_f, off_invrho, off_c1;  // offsets (doubles) of eta, f, 1/rho', c1' in ws
+  double* partials;
+  int pstride, poff;
+  const int* done;
+};
+
 // Segments for the deterministic second-stage reduction of CTA partials.
 struct FinSeg {
   int poff, len, woff;

@@ -878,6 +878,11 @@ struct QMR : Solver {  // mode 0 Li, 1 Gl, 2 eGl
     return mode == 2 && !off_env && A && !A->bsr && !A->prec && A->ghost_rows() == 0 && A->has_adj && n <= SMALL_N_MAX &&
            !(c->comm && c->comm->nranks > 1);
   }
+  // Gl / eGl-QMR (scalar coefficients): the iteration's last update also forms the next P
+  bool fused_tail() const {
+    static const bool off_env = getenv("SRK_NO_QMR_FUSE") != nullptr;  // A/B switch
+    return mode != 0 && !off_env && e.qmr_tail_ok(s);
+  }
   bool ends_iter() const override { return small(); }
   int seg_multi(int k) override {
     if (!small() || k < 1 || e.err) return 0;
@@ -918,9 +923,14 @@ struct QMR : Solver {  // mode 0 Li, 1 Gl, 2 eGl
     coef(1);                   // 1/rho, 1/xi
     coef(2, host_iter == 0);   // delta = <Ṽ, W̃>/(rho xi); c1 = xi delta/eps, c2 = conj(rho delta/eps)
     // P = V - c1 P = Ṽ/rho - c1 P ;  Q = W - c2 Q = W̃/xi - c2 Q
+    // (fused tail: after the first iteration P was already formed by the previous iteration's last kernel)
+    const bool fuse = fused_tail();
+    const bool p_done = fuse && host_iter > 0;
     if (mode == 2) {
-      e.upd(s, {Vt, P}, {OutSpec{P, {{0, SC(off[SL_INVRHO])}, {1, SC(off[SL_C1], 1)}}}}, {});
+      if (!p_done) e.upd(s, {Vt, P}, {OutSpec{P, {{0, SC(off[SL_INVRHO])}, {1, SC(off[SL_C1], 1)}}}}, {});
       e.upd(1, {Wt, Qv}, {OutSpec{Qv, {{0, SC(off[SL_INVXI])}, {1, SC(off[SL_C2], 1)}}}}, {});
+    } else if (p_done) {
+      e.upd(s, {Wt, Qv}, {OutSpec{Qv, {{0, K(SL_INVXI)}, {1, K(SL_C2, 1)}}}}, {});
     } else {
       e.upd(s, {Vt, P, Wt, Qv},
             {OutSpec{P, {{0, K(SL_INVRHO)}, {1, K(SL_C1, 1)}}}, OutSpec{Qv, {{2, K(SL_INVXI)}, {3, K(SL_C2, 1)}}}}, {});
@@ -933,7 +943,14 @@ struct QMR : Solver {  // mode 0 Li, 1 Gl, 2 eGl
     // Ṽ = P~ - beta V = P~ - (beta/rho) Ṽ, with ||Ṽ||^2 and the next <Ṽ, W̃>
     if (mode == 2) e.upd(s, {Pt, Vt}, {OutSpec{Vt, {{0, C1()}, {1, K(SL_BR, 1)}}}}, vt_reds(O0, -1));
     else e.upd(s, {Pt, Vt, Wt}, {OutSpec{Vt, {{0, C1()}, {1, K(SL_BR, 1)}}}}, vt_reds(O0, 2));
-    coef(4);  // theta, gamma, eta, f
+    coef(4);  // theta, gamma, eta, f (and the next iteration's 1/rho, c1)
+    if (fuse) {
+      // (D, S, X, R) of this iteration and P = Ṽ/rho' - c1' P of the next in one pass (qmr_tail.cu):
+      // 12 block passes instead of 10 + 3
+      e.qmr_tail(s, P, D, Pt, S, X, R, Vt, off[SL_ETA], off[SL_F], off[SL_INVRHO_N], off[SL_C1_N], off[SL_R2]);
+      coef(5);
+      return;
+    }
     e.upd(s, {P, D, Pt, S, X, R},
           {OutSpec{D, {{0, K(SL_ETA)}, {1, K(SL_F)}}},
            OutSpec{S, {{2, K(SL_ETA)}, {3, K(SL_F)}}},
