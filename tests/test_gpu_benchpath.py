@@ -2,8 +2,8 @@
 s = 16, unpreconditioned, multi-kernel): the same operator family (3D 7-point
 convection-diffusion, c = (50, 30, 10)) at 48^3 (n = 110,592, above
 the single-CTA small-operator limit of 16,384 rows), the same kernels and launch
-configuration — the SpMM with the fused eGl vector-sum epilogue, the 6-input / 4-output
-block update — compared with the oracle over 20 iterations: X_k, R_k and the recursive
+configuration — the SpMM with the fused eGl vector-sum epilogue, the 7-input / 5-output
+fused tail (D, S, X, R of iteration k and P of iteration k+1, qmr_tail.cu) — compared with the oracle over 20 iterations: X_k, R_k and the recursive
 residual history under the §8c.5 envelope, then a full solve under the count rule
 (within max(2%, |it_O - it_O'| + 2) of the oracle's two reduction orders) and the
 oracle-recomputed true residual."""
@@ -56,12 +56,16 @@ def test_benchpath_lockstep(srk, problem, method):
     h = sv.history(n_it)
     ho = np.array(a.history[:n_it])
     assert np.all(np.abs(h - ho) / ho <= env[:n_it]), (h, ho)
-    # the timed kernels ran: the s = 16 SpMM and (eGl-QMR) the 6-input / 4-output update
+    # the timed kernels ran: the s = 16 SpMM and (eGl-QMR) the 7-input / 5-output fused tail
     launches = sv.profile_launches()
     sigs = {(t, g) for t, g, _, _ in launches}
     assert ("spmm", S) in sigs
     if method == "egl_qmr":
-        assert ("update", 16 * 6 + 4) in sigs, sorted(sigs)
+        assert ("update", 16 * 7 + 5) in sigs, sorted(sigs)
+        # P is formed standalone only in the first iteration (2 in / 1 out at width s appears once
+        # besides the Ṽ update of every iteration)
+        n_tail = sum(1 for t, g, _, _ in launches if (t, g) == ("update", 16 * 7 + 5))
+        assert n_tail == n_it
         assert ("spmm_adj", 1) in sigs  # the economic A^H vector product
     sv.close()
 
@@ -81,3 +85,49 @@ def test_benchpath_full_solve(srk, problem, method):
     true = np.linalg.norm(B - As @ X) / np.linalg.norm(B)
     assert true <= 1e-8
     assert abs(true - rep.final_true_rel_residual) <= 1e-12 + 1e-6 * true
+
+
+_FUSE_CODE = """
+import sys; sys.path.insert(0, {root!r})
+import numpy as np, torch, synth, paper_1504_04395_b200 as srk
+srk.load_library()
+A = synth.conv_diff_3d({m}, (50.0, 30.0, 10.0), {dt})
+B = synth.random_rhs(A.n, {s}, 2, {cplx})
+M = srk.Matrix.from_csr(A, need_adjoint=True)
+sv = srk.Solver(M, {s}, {method!r}, tol=1e-8, maxit=2000, poll_every={poll}, use_graph={graph})
+sv.start(torch.from_numpy(B).cuda())
+sv.iterate({k})
+np.save({out!r}, np.stack([sv.x().cpu().numpy(), sv.residual().cpu().numpy()]))
+X, rep = srk.solve(M, torch.from_numpy(B).cuda(), {method!r}, tol=1e-8, maxit=2000)
+print(rep.outcome, rep.iterations)
+"""
+
+
+@pytest.mark.parametrize("method", ["egl_qmr", "gl_qmr"])
+@pytest.mark.parametrize("cplx,s", [(False, 16), (True, 8), (False, 5), (True, 3)])
+def test_qmr_fused_tail_equals_separate_updates(srk, tmp_path, method, cplx, s):
+    """The fused tail (qmr_tail.cu: D, S, X, R of iteration k and P of iteration k+1 in one
+    pass, next iteration's 1/rho and c1 from coefficient phase 4) keeps the per-element FMA
+    order of the two separate updates: X_k and R_k after 12 iterations — stepped one by one
+    and inside a replayed CUDA graph — are bitwise those of the unfused plan
+    (SRK_NO_QMR_FUSE=1, a subprocess: the switch is read once), and the full solves agree in
+    outcome and count. Widths 5 / 3 give blocks whose flat length is still a whole number of
+    16-byte units (n even), with a ragged last CTA."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    m = 28  # n = 21,952 > the single-CTA limit
+    res = {}
+    for tag, env, poll in (("fused", {}, 1), ("graph", {}, 4), ("plain", {"SRK_NO_QMR_FUSE": "1"}, 1)):
+        out = str(tmp_path / f"{tag}.npy")
+        code = _FUSE_CODE.format(root=root, m=m, dt="np.complex128" if cplx else "np.float64", s=s, cplx=cplx,
+                                 method=method, poll=poll, graph=(tag == "graph"), k=12, out=out)
+        r = subprocess.run([sys.executable, "-c", code], env={**os.environ, **env}, capture_output=True, text=True,
+                           timeout=900)
+        assert r.returncode == 0, r.stderr[-800:]
+        res[tag] = (np.load(out), r.stdout.split()[-2:])
+    assert np.isfinite(res["plain"][0]).all()
+    assert np.array_equal(res["fused"][0], res["plain"][0])
+    assert np.array_equal(res["graph"][0], res["plain"][0])
+    assert res["fused"][1] == res["plain"][1] == res["graph"][1], (res["fused"][1], res["plain"][1])
