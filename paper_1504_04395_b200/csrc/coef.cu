@@ -467,6 +467,8 @@ __device__ void qmr_scalar(const CoefArgs& a, int mode) {
           const T dn = Ar<T>::mul(Ar<T>::mul(W<T>(a, SL_K1)[c], ir), ix);
           W<T>(a, SL_INVRHO_N)[c] = ir;
           W<T>(a, SL_C1_N)[c] = cdiv(Ar<T>::mul(xi[c], dn), W<T>(a, SL_EPS)[c]);
+          W<T>(a, SL_INVXI_N)[c] = ix;
+          W<T>(a, SL_C2_N)[c] = Ar<T>::conj(cdiv(Ar<T>::mul(rho[c], dn), W<T>(a, SL_EPS)[c]));
         }
       }
     } else if (a.phase == 5) {

@@ -35,7 +35,7 @@ enum Slot : int {
   // QMR
   SL_QRHO, SL_QXI, SL_INVRHO, SL_INVXI, SL_DELTA, SL_EPS, SL_C1, SL_C2, SL_GAMP, SL_ETA, SL_THETAP, SL_F,
   SL_RHON2, SL_XI2, SL_K1, SL_BR, SL_BX,
-  SL_INVRHO_N, SL_C1_N,  // next iteration's 1/rho and c1, known once Ṽ is formed (the fused tail, qmr_tail.cu)
+  SL_INVRHO_N, SL_C1_N, SL_INVXI_N, SL_C2_N,  // next iteration's 1/rho, c1 (and 1/xi, c2), known once Ṽ is formed (the fused tail, qmr_tail.cu)
   // Bl-QMR
   SL_OMP, SL_TAUT, SL_TAU, SL_TOP, SL_RII, SL_RIII, SL_TR, SL_GHAT, SL_RHOB, SL_XIB, SL_RHOBN, SL_XIBN,
   SL_PEND,

@@ -512,8 +512,50 @@ int Eng::upd(int s, std::vector<const void*> in, std::vector<OutSpec> outs, std:
   return err = finish_reds(*this, reds, poffs, s, grid, a.pstride);
 }
 
+static int log2_or_neg(int v) {
+  for (int k = 0; k < 31; ++k)
+    if ((1 << k) == v) return k;
+  return -1;
+}
+
+int Eng::qmr_vt(int s, const void* Pt, void* Vt, const void* AHQ, const void* Wt, int off_br, int off_bx, int woff_rho2,
+                int woff_k1, int woff_xi2) {
+  if (err) return err;
+  if (!qmr_vec_ok(s)) return err = (int)cudaErrorInvalidValue;
+  const size_t esz = cplx ? 16 : 8;
+  QmrVtArgs a{};
+  a.Pt = Pt; a.Vt = Vt; a.AHQ = AHQ; a.Wt = Wt;
+  a.upr = (int)((size_t)s * esz / 16);
+  a.sh = log2_or_neg(a.upr);
+  a.units = n * (long long)a.upr;
+  a.ws = ws;
+  a.off_br = off_br; a.off_bx = off_bx;
+  a.pstride = 2 + (cplx ? 2 : 1);
+  a.done = done;
+  static std::atomic<int> occ_c[2] = {{0}, {0}};
+  int occ = occ_c[cplx].load();
+  if (occ == 0) {
+    occ = std::max(1, launch_qmr_vt(cplx, a, -1, nullptr));
+    occ_c[cplx].store(occ);
+  }
+  const long long need = std::max<long long>(1, (a.units + 255) / 256);
+  const int grid = (int)std::min<long long>(need, (long long)c->nsm * occ);
+  if ((err = c->ensure_partials((size_t)grid * a.pstride))) return err;
+  a.partials = c->partials;
+  nlaunch++;
+  if (prof) prof->begin(PT_UPD, c->st, 16 * 2 + 1, 3.0 * (double)n * s * esz + 2.0 * (double)n * esz);
+  err = launch_qmr_vt(cplx, a, grid, c->st);
+  if (prof) prof->end(c->st);
+  if (err) return err;
+  const int nd = cplx ? 2 : 1;
+  return err = finish_reds(*this,
+                           {RQ{RED_NORM2, SRC_OUT, -1, nullptr, woff_rho2}, RQ{RED_SUMVEC, SRC_OUT, -1, Wt, woff_k1},
+                            RQ{RED_NORM2, SRC_OUT, -1, nullptr, woff_xi2}},
+                           {0, 1, 1 + nd}, s, grid, a.pstride);
+}
+
 int Eng::qmr_tail(int s, void* P, void* D, const void* Pt, void* S, void* X, void* R, const void* Vt, int off_eta,
-                  int off_f, int off_invrho, int off_c1, int woff_r2) {
+                  int off_f, int off_invrho, int off_c1, int woff_r2, const QmrVec* v) {
   if (err) return err;
   if (!qmr_tail_ok(s)) return err = (int)cudaErrorInvalidValue;
   const size_t esz = cplx ? 16 : 8;
@@ -525,6 +567,13 @@ int Eng::qmr_tail(int s, void* P, void* D, const void* Pt, void* S, void* X, voi
   a.pstride = 1;
   a.poff = 0;
   a.done = done;
+  if (v) {
+    if (!qmr_vec_ok(s)) return err = (int)cudaErrorInvalidValue;
+    a.Wt = v->Wt; a.Qv = v->Qv; a.AHQ = v->AHQ;
+    a.upr = (int)((size_t)s * esz / 16);
+    a.sh = log2_or_neg(a.upr);
+    a.off_bx = v->off_bx; a.off_invxi = v->off_invxi; a.off_c2 = v->off_c2;
+  }
   static std::atomic<int> occ_c[2] = {{0}, {0}};
   int occ = occ_c[cplx].load();
   if (occ == 0) {
@@ -536,7 +585,7 @@ int Eng::qmr_tail(int s, void* P, void* D, const void* Pt, void* S, void* X, voi
   if ((err = c->ensure_partials((size_t)grid))) return err;
   a.partials = c->partials;
   nlaunch++;
-  if (prof) prof->begin(PT_UPD, c->st, 16 * 7 + 5, 12.0 * (double)n * s * esz);
+  if (prof) prof->begin(PT_UPD, c->st, 16 * 7 + 5, 12.0 * (double)n * s * esz + (v ? 5.0 * (double)n * esz : 0.0));
   err = launch_qmr_tail(cplx, a, grid, c->st);
   if (prof) prof->end(c->st);
   if (err) return err;

@@ -20,6 +20,7 @@ int launch_spmm(bool cplx, int cap, bool full, const SpmmArgs& a, int grid, int 
 int launch_upd(bool cplx, int cap, bool full, const UpdArgs& a, int grid, int block, size_t smem, cudaStream_t st);
 int launch_fin(const FinArgs& a, cudaStream_t st);
 int launch_qmr_tail(bool cplx, const QmrTailArgs& a, int grid, cudaStream_t st);  // grid < 0: resident CTAs per SM
+int launch_qmr_vt(bool cplx, const QmrVtArgs& a, int grid, cudaStream_t st);
 int launch_gram_mma(const GramArgs& g, int grid, cudaStream_t st);
 int launch_bsr(const BsrArgs& a, int s, int grid, cudaStream_t st);  // grid < 0: resident WARPS per SM
 int bsr_warps_per_cta();
@@ -212,6 +213,12 @@ struct Prof {
   ~Prof();
 };
 
+struct QmrVec {  // eGl-QMR fused tail: the left Lanczos vectors and their coefficients' offsets in ws
+  void *Wt, *Qv;
+  const void* AHQ;
+  int off_bx, off_invxi, off_c2;
+};
+
 struct Eng {
   Prof* prof = nullptr;
   Ctx* c = nullptr;
@@ -232,7 +239,11 @@ struct Eng {
   // offsets into ws of eta, f, 1/rho', c1' and of ||R||^2. qmr_tail_ok: the blocks are whole 16-byte units
   bool qmr_tail_ok(int s) const { return ((n * (long long)s * (cplx ? 16 : 8)) % 16) == 0; }
   int qmr_tail(int s, void* P, void* D, const void* Pt, void* S, void* X, void* R, const void* Vt, int off_eta,
-               int off_f, int off_invrho, int off_c1, int woff_r2);
+               int off_f, int off_invrho, int off_c1, int woff_r2, const QmrVec* v = nullptr);
+  // eGl: the n-vector updates ride in the two block kernels (whole 16-byte units per block row)
+  bool qmr_vec_ok(int s) const { return ((long long)s * (cplx ? 16 : 8)) % 16 == 0; }
+  int qmr_vt(int s, const void* Pt, void* Vt, const void* AHQ, const void* Wt, int off_br, int off_bx, int woff_rho2,
+             int woff_k1, int woff_xi2);
   // s x s Gram Y^H X on the FP64 tensor cores (gram_mma.cu), written to ws + woff
   int gram_full(const void* X, const void* Y, int s, int woff);
   int spmm_bsr(bool adj, const void* P, void* Q, int s, const std::vector<RQ>& reds);

@@ -150,6 +150,26 @@ struct QmrTailArgs {
   double* partials;
   int pstride, poff;
   const int* done;
+  // eGl (upr > 0): the n-vectors w̃ (rewritten: A^H q - bx w̃) and q (rewritten: w̃/xi' - c2' q);
+  // upr = 16-byte units per block row, sh = log2(upr) or -1
+  void *Wt, *Qv;
+  const void* AHQ;
+  int upr, sh;
+  int off_bx, off_invxi, off_c2;
+};
+// eGl-QMR Ṽ update with the reductions of Ṽ and of the new w̃ (qmr_tail.cu); partials per CTA:
+// [||Ṽ||^2, sum(w̃^H Ṽ) (ND doubles), ||w̃||^2]
+struct QmrVtArgs {
+  const void* Pt;
+  void* Vt;
+  const void *AHQ, *Wt;
+  long long units;
+  int upr, sh;
+  const double* ws;
+  int off_br, off_bx;
+  double* partials;
+  int pstride;
+  const int* done;
 };
 
 // Segments for the deterministic second-stage reduction of CTA partials.

@@ -40,6 +40,12 @@ __global__ void __launch_bounds__(256, sizeof(T) == 16 ? 3 : 4) qmr_tail_kernel(
   const T f = Ar<T>::ld(a.ws + a.off_f);
   const T ir = Ar<T>::ld(a.ws + a.off_invrho);
   const T nc1 = Ar<T>::sub(zero, Ar<T>::ld(a.ws + a.off_c1));
+  T nbx = zero, ix = zero, nc2 = zero;
+  if (a.upr > 0) {
+    nbx = Ar<T>::sub(zero, Ar<T>::ld(a.ws + a.off_bx));
+    ix = Ar<T>::ld(a.ws + a.off_invxi);
+    nc2 = Ar<T>::sub(zero, Ar<T>::ld(a.ws + a.off_c2));
+  }
   RedAcc<T, W, false> acc;
   red_zero(acc);
   auto ld = [&](const void* base, long long u, T (&v)[E]) {
@@ -75,9 +81,81 @@ __global__ void __launch_bounds__(256, sizeof(T) == 16 ? 3 : 4) qmr_tail_kernel(
     st(a.R, u, rn);
     st(a.P, u, pn);
     red_acc<T, W, false>(acc, rn, rn);
+    // eGl: the left Lanczos vectors of the next iteration, by the thread that owns the first unit of
+    // a row (nobody else touches them): w̃ <- A^H q - (conj(beta)/xi) w̃ (deferred from qmr_vt_kernel,
+    // which only reduced it) and q <- w̃/xi' - c2' q
+    if (a.upr > 0) {
+      const long long row = a.sh >= 0 ? (u >> a.sh) : (u / a.upr);
+      if (u == (a.sh >= 0 ? (row << a.sh) : row * a.upr)) {
+        T* wt = reinterpret_cast<T*>(a.Wt) + row;
+        T* qv = reinterpret_cast<T*>(a.Qv) + row;
+        const T wn = Ar<T>::fma(*wt, nbx, Ar<T>::fma(reinterpret_cast<const T*>(a.AHQ)[row], one, zero));
+        *wt = wn;
+        *qv = Ar<T>::fma(*qv, nc2, Ar<T>::fma(wn, ix, zero));
+      }
+    }
   }
   __syncwarp();
   red_flush<T, W, RED_NORM2, false>(acc, a.partials, a.pstride, a.poff, W, rsm);
+}
+
+// eGl-QMR: Ṽ <- P~ - (beta/rho) Ṽ with ||Ṽ||^2 and sum(w̃^H Ṽ) for the NEW left vector
+// w̃ = A^H q - (conj(beta)/xi) w̃, formed per row in registers from its two operands and reduced
+// (||w̃||^2, by the first unit of each row) but not stored: the fused tail stores it (see above),
+// so no thread reads an entry another one rewrites. One launch and one finalisation instead of
+// the n-vector update, the block update and their two finalisations; flat 16-byte units as above.
+template <typename T>
+__global__ void __launch_bounds__(256, 4) qmr_vt_kernel(QmrVtArgs a) {
+  if (a.done && *a.done) return;
+  constexpr int W = 128 / (int)sizeof(T);
+  using L = Lay<T, W>;
+  constexpr int E = L::EPL;
+  __shared__ double rsm[16];
+  const T zero = Ar<T>::zero();
+  T one;
+  if constexpr (Ar<T>::cplx) one = mk(1.0, 0.0); else one = 1.0;
+  const T nbr = Ar<T>::sub(zero, Ar<T>::ld(a.ws + a.off_br));
+  const T nbx = Ar<T>::sub(zero, Ar<T>::ld(a.ws + a.off_bx));
+  RedAcc<T, W, false> arho, ak1, axi;
+  red_zero(arho);
+  red_zero(ak1);
+  red_zero(axi);
+  const long long stride = (long long)gridDim.x * 256;
+  for (long long u = (long long)blockIdx.x * 256 + threadIdx.x; u < a.units; u += stride) {
+    const long long row = a.sh >= 0 ? (u >> a.sh) : (u / a.upr);
+    const double2 tp = reinterpret_cast<const double2*>(a.Pt)[u];
+    const double2 tv = reinterpret_cast<const double2*>(a.Vt)[u];
+    const T ah = reinterpret_cast<const T*>(a.AHQ)[row];
+    const T wo = reinterpret_cast<const T*>(a.Wt)[row];
+    T pt[E], vt[E], vn[E];
+    if constexpr (E == 2) { pt[0] = tp.x; pt[1] = tp.y; vt[0] = tv.x; vt[1] = tv.y; } else { pt[0] = tp; vt[0] = tv; }
+    const T wn = Ar<T>::fma(wo, nbx, Ar<T>::fma(ah, one, zero));
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      vn[e] = Ar<T>::fma(vt[e], nbr, Ar<T>::fma(pt[e], one, zero));
+      arho.v[e] = Ar<T>::cfma(vn[e], vn[e], arho.v[e]);
+      ak1.v[e] = Ar<T>::cfma(wn, vn[e], ak1.v[e]);
+    }
+    if constexpr (E == 2) reinterpret_cast<double2*>(a.Vt)[u] = make_double2(vn[0], vn[1]);
+    else reinterpret_cast<double2*>(a.Vt)[u] = vn[0];
+    if (u == (a.sh >= 0 ? (row << a.sh) : row * a.upr)) axi.v[0] = Ar<T>::cfma(wn, wn, axi.v[0]);
+  }
+  __syncwarp();
+  red_flush<T, W, RED_NORM2, false>(arho, a.partials, a.pstride, 0, W, rsm);
+  red_flush<T, W, RED_SUMVEC, false>(ak1, a.partials, a.pstride, 1, W, rsm);
+  red_flush<T, W, RED_NORM2, false>(axi, a.partials, a.pstride, 1 + Ar<T>::ND, W, rsm);
+}
+
+int launch_qmr_vt(bool cplx, const QmrVtArgs& a, int grid, cudaStream_t st) {
+  if (grid < 0) {
+    int nb = 0;
+    if (cplx) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, qmr_vt_kernel<double2>, 256, 0);
+    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, qmr_vt_kernel<double>, 256, 0);
+    return nb;
+  }
+  if (cplx) qmr_vt_kernel<double2><<<grid, 256, 0, st>>>(a);
+  else qmr_vt_kernel<double><<<grid, 256, 0, st>>>(a);
+  return (int)cudaGetLastError();
 }
 
 // grid < 0: resident CTAs per SM of this instance

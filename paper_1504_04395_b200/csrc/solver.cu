@@ -883,6 +883,10 @@ struct QMR : Solver {  // mode 0 Li, 1 Gl, 2 eGl
     static const bool off_env = getenv("SRK_NO_QMR_FUSE") != nullptr;  // A/B switch
     return mode != 0 && !off_env && e.qmr_tail_ok(s);
   }
+  bool fused_vec() const {
+    static const bool off_env = getenv("SRK_NO_QMR_VEC_FUSE") != nullptr;  // A/B switch
+    return mode == 2 && !off_env && e.qmr_vec_ok(s);
+  }
   bool ends_iter() const override { return small(); }
   int seg_multi(int k) override {
     if (!small() || k < 1 || e.err) return 0;
@@ -925,10 +929,11 @@ struct QMR : Solver {  // mode 0 Li, 1 Gl, 2 eGl
     // P = V - c1 P = Ṽ/rho - c1 P ;  Q = W - c2 Q = W̃/xi - c2 Q
     // (fused tail: after the first iteration P was already formed by the previous iteration's last kernel)
     const bool fuse = fused_tail();
+    const bool vfuse = fuse && fused_vec();  // eGl: w̃ and q ride in the block kernels as well
     const bool p_done = fuse && host_iter > 0;
     if (mode == 2) {
       if (!p_done) e.upd(s, {Vt, P}, {OutSpec{P, {{0, SC(off[SL_INVRHO])}, {1, SC(off[SL_C1], 1)}}}}, {});
-      e.upd(1, {Wt, Qv}, {OutSpec{Qv, {{0, SC(off[SL_INVXI])}, {1, SC(off[SL_C2], 1)}}}}, {});
+      if (!(vfuse && p_done)) e.upd(1, {Wt, Qv}, {OutSpec{Qv, {{0, SC(off[SL_INVXI])}, {1, SC(off[SL_C2], 1)}}}}, {});
     } else if (p_done) {
       e.upd(s, {Wt, Qv}, {OutSpec{Qv, {{0, K(SL_INVXI)}, {1, K(SL_C2, 1)}}}}, {});
     } else {
@@ -938,16 +943,24 @@ struct QMR : Solver {  // mode 0 Li, 1 Gl, 2 eGl
     e.spmm(false, P, Pt, s, {RQ{dmode(), 0, -1, Qv, off[SL_EPS]}});  // P~ = A P ; eps = <P~, Q>
     e.spmm(true, Qv, AHQ, ws_(), {});                                // A^H Q
     coef(3);  // beta = eps/delta ; BR = beta/rho ; BX = conj(beta)/xi
-    // W̃ = A^H Q - conj(beta) W = A^H Q - (conj(beta)/xi) W̃   (first: Ṽ's kernel reads the new W̃)
-    e.upd(ws_(), {AHQ, Wt}, {OutSpec{Wt, {{0, C1()}, {1, K(SL_BX, 1)}}}}, {RQ{nrm(), O0, -1, nullptr, off[SL_XI2]}});
-    // Ṽ = P~ - beta V = P~ - (beta/rho) Ṽ, with ||Ṽ||^2 and the next <Ṽ, W̃>
-    if (mode == 2) e.upd(s, {Pt, Vt}, {OutSpec{Vt, {{0, C1()}, {1, K(SL_BR, 1)}}}}, vt_reds(O0, -1));
-    else e.upd(s, {Pt, Vt, Wt}, {OutSpec{Vt, {{0, C1()}, {1, K(SL_BR, 1)}}}}, vt_reds(O0, 2));
-    coef(4);  // theta, gamma, eta, f (and the next iteration's 1/rho, c1)
+    if (vfuse) {
+      // one kernel: Ṽ = P~ - (beta/rho) Ṽ with ||Ṽ||^2, <Ṽ, W̃> and ||W̃||^2 for the new
+      // W̃ = A^H Q - (conj(beta)/xi) W̃, formed per row in registers (stored by the tail below)
+      e.qmr_vt(s, Pt, Vt, AHQ, Wt, off[SL_BR], off[SL_BX], off[SL_RHON2], off[SL_K1], off[SL_XI2]);
+    } else {
+      // W̃ = A^H Q - conj(beta) W = A^H Q - (conj(beta)/xi) W̃   (first: Ṽ's kernel reads the new W̃)
+      e.upd(ws_(), {AHQ, Wt}, {OutSpec{Wt, {{0, C1()}, {1, K(SL_BX, 1)}}}}, {RQ{nrm(), O0, -1, nullptr, off[SL_XI2]}});
+      // Ṽ = P~ - beta V = P~ - (beta/rho) Ṽ, with ||Ṽ||^2 and the next <Ṽ, W̃>
+      if (mode == 2) e.upd(s, {Pt, Vt}, {OutSpec{Vt, {{0, C1()}, {1, K(SL_BR, 1)}}}}, vt_reds(O0, -1));
+      else e.upd(s, {Pt, Vt, Wt}, {OutSpec{Vt, {{0, C1()}, {1, K(SL_BR, 1)}}}}, vt_reds(O0, 2));
+    }
+    coef(4);  // theta, gamma, eta, f (and the next iteration's 1/rho, c1, 1/xi, c2)
     if (fuse) {
       // (D, S, X, R) of this iteration and P = Ṽ/rho' - c1' P of the next in one pass (qmr_tail.cu):
-      // 12 block passes instead of 10 + 3
-      e.qmr_tail(s, P, D, Pt, S, X, R, Vt, off[SL_ETA], off[SL_F], off[SL_INVRHO_N], off[SL_C1_N], off[SL_R2]);
+      // 12 block passes instead of 10 + 3; eGl: also W̃ (stored here) and q = W̃/xi' - c2' q
+      const QmrVec v{Wt, Qv, AHQ, off[SL_BX], off[SL_INVXI_N], off[SL_C2_N]};
+      e.qmr_tail(s, P, D, Pt, S, X, R, Vt, off[SL_ETA], off[SL_F], off[SL_INVRHO_N], off[SL_C1_N], off[SL_R2],
+                 vfuse ? &v : nullptr);
       coef(5);
       return;
     }

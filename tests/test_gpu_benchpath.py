@@ -91,7 +91,7 @@ _FUSE_CODE = """
 import sys; sys.path.insert(0, {root!r})
 import numpy as np, torch, synth, paper_1504_04395_b200 as srk
 srk.load_library()
-A = synth.conv_diff_3d({m}, (50.0, 30.0, 10.0), {dt})
+A = synth.conv_diff_3d({m}, (20.0, 10.0, 5.0), {dt})
 B = synth.random_rhs(A.n, {s}, 2, {cplx})
 M = srk.Matrix.from_csr(A, need_adjoint=True)
 sv = srk.Solver(M, {s}, {method!r}, tol=1e-8, maxit=2000, poll_every={poll}, use_graph={graph})
@@ -104,30 +104,46 @@ print(rep.outcome, rep.iterations)
 
 
 @pytest.mark.parametrize("method", ["egl_qmr", "gl_qmr"])
-@pytest.mark.parametrize("cplx,s", [(False, 16), (True, 8), (False, 5), (True, 3)])
+@pytest.mark.parametrize("cplx,s", [(False, 16), (True, 8), (False, 5), (False, 6), (True, 3)])
 def test_qmr_fused_tail_equals_separate_updates(srk, tmp_path, method, cplx, s):
     """The fused tail (qmr_tail.cu: D, S, X, R of iteration k and P of iteration k+1 in one
     pass, next iteration's 1/rho and c1 from coefficient phase 4) keeps the per-element FMA
     order of the two separate updates: X_k and R_k after 12 iterations — stepped one by one
     and inside a replayed CUDA graph — are bitwise those of the unfused plan
-    (SRK_NO_QMR_FUSE=1, a subprocess: the switch is read once), and the full solves agree in
-    outcome and count. Widths 5 / 3 give blocks whose flat length is still a whole number of
-    16-byte units (n even), with a ragged last CTA."""
+    (SRK_NO_QMR_FUSE=1, a subprocess: the switches are read once), and the full solves agree in
+    outcome and count. eGl-QMR at whole 16-byte units per row also carries its n-vectors in the
+    block kernels (qmr_vt_kernel and the tail's vector part), which changes the summation order
+    of ||Ṽ||^2, <Ṽ, W̃>, ||W̃||^2: bitwise with that switched off (SRK_NO_QMR_VEC_FUSE=1), within
+    1e-11 with it on (the operator is the 28^3 stencil with c = (20, 10, 5), on which the oracle's
+    own two summation orders differ by 4e-16 / 1e-14 in X / R at iteration 12 and its counts do not
+    move under 1e-15 perturbations of B; with c = (50, 30, 10) at this size a near-breakdown at
+    iteration 9 spreads the oracle itself by 4e-10 and its counts by 6%; the lock step against the
+    oracle is test_benchpath_lockstep). Widths 5 / 6 / 3
+    give ragged last CTAs, rows of 3 units (the division path) and the no-vector fallback."""
     import os
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     m = 28  # n = 21,952 > the single-CTA limit
     res = {}
-    for tag, env, poll in (("fused", {}, 1), ("graph", {}, 4), ("plain", {"SRK_NO_QMR_FUSE": "1"}, 1)):
+    novec = {"SRK_NO_QMR_VEC_FUSE": "1"}
+    for tag, env, poll in (("fused", novec, 1), ("graph", novec, 4), ("plain", {"SRK_NO_QMR_FUSE": "1"}, 1),
+                           ("vec", {}, 1), ("vecgraph", {}, 4)):
         out = str(tmp_path / f"{tag}.npy")
         code = _FUSE_CODE.format(root=root, m=m, dt="np.complex128" if cplx else "np.float64", s=s, cplx=cplx,
-                                 method=method, poll=poll, graph=(tag == "graph"), k=12, out=out)
+                                 method=method, poll=poll, graph=tag.endswith("graph"), k=12, out=out)
         r = subprocess.run([sys.executable, "-c", code], env={**os.environ, **env}, capture_output=True, text=True,
                            timeout=900)
         assert r.returncode == 0, r.stderr[-800:]
         res[tag] = (np.load(out), r.stdout.split()[-2:])
-    assert np.isfinite(res["plain"][0]).all()
-    assert np.array_equal(res["fused"][0], res["plain"][0])
-    assert np.array_equal(res["graph"][0], res["plain"][0])
+    ref = res["plain"][0]
+    assert np.isfinite(ref).all()
+    assert np.array_equal(res["fused"][0], ref)
+    assert np.array_equal(res["graph"][0], ref)
     assert res["fused"][1] == res["plain"][1] == res["graph"][1], (res["fused"][1], res["plain"][1])
+    assert np.array_equal(res["vec"][0], res["vecgraph"][0])
+    for j in range(2):
+        assert rel(res["vec"][0][j], ref[j]) <= 1e-11, (j, rel(res["vec"][0][j], ref[j]))
+    assert res["vec"][1][0] == res["plain"][1][0] == "converged"
+    it_v, it_p = int(res["vec"][1][1]), int(res["plain"][1][1])
+    assert abs(it_v - it_p) <= max(2, 0.02 * it_p), (it_v, it_p)
