@@ -518,6 +518,48 @@ static int log2_or_neg(int v) {
   return -1;
 }
 
+int Eng::flat(int plan, int s, std::vector<const void*> in, std::vector<void*> out, std::vector<int> coff,
+              std::vector<int> woff) {
+  if (err) return err;
+  const FlatPlanInfo pi = flat_plan_info(plan);
+  if (!qmr_tail_ok(s) || pi.ni == 0 || (int)in.size() != pi.ni || (int)out.size() != pi.no || (int)coff.size() != pi.nc ||
+      (int)woff.size() != pi.nr)
+    return err = (int)cudaErrorInvalidValue;
+  const size_t esz = cplx ? 16 : 8;
+  FlatArgs a{};
+  for (int i = 0; i < pi.ni; ++i) a.in[i] = in[i];
+  for (int i = 0; i < pi.no; ++i) a.out[i] = out[i];
+  for (int i = 0; i < pi.nc; ++i) a.coff[i] = coff[i];
+  a.units = (long long)((size_t)n * s * esz / 16);
+  a.ws = ws;
+  a.done = done;
+  std::vector<RQ> reds;
+  std::vector<int> poffs;
+  int pstride = 0;
+  for (int r = 0; r < pi.nr; ++r) {
+    reds.push_back(RQ{pi.rmode[r], 0, -1, nullptr, woff[r]});
+    poffs.push_back(pstride);
+    pstride += red_len(pi.rmode[r], s, cplx);  // NORM2: 1, TRACE: one value
+  }
+  a.pstride = std::max(pstride, 1);
+  static std::atomic<int> occ_c[8][2] = {};
+  int occ = occ_c[plan & 7][cplx].load();
+  if (occ == 0) {
+    occ = std::max(1, launch_flat(plan, cplx, a, -1, nullptr));
+    occ_c[plan & 7][cplx].store(occ);
+  }
+  const long long need = std::max<long long>(1, (a.units + 255) / 256);
+  const int grid = (int)std::min<long long>(need, (long long)c->nsm * occ);  // one wave
+  if ((err = c->ensure_partials((size_t)grid * a.pstride))) return err;
+  a.partials = c->partials;
+  nlaunch++;
+  if (prof) prof->begin(PT_UPD, c->st, 16 * pi.ni + pi.no, (double)(pi.ni + pi.no) * (double)n * s * esz);
+  err = launch_flat(plan, cplx, a, grid, c->st);
+  if (prof) prof->end(c->st);
+  if (err) return err;
+  return err = finish_reds(*this, reds, poffs, s, grid, a.pstride);
+}
+
 int Eng::qmr_vt(int s, const void* Pt, void* Vt, const void* AHQ, const void* Wt, int off_br, int off_bx, int woff_rho2,
                 int woff_k1, int woff_xi2) {
   if (err) return err;

@@ -21,6 +21,8 @@ int launch_upd(bool cplx, int cap, bool full, const UpdArgs& a, int grid, int bl
 int launch_fin(const FinArgs& a, cudaStream_t st);
 int launch_qmr_tail(bool cplx, const QmrTailArgs& a, int grid, cudaStream_t st);  // grid < 0: resident CTAs per SM
 int launch_qmr_vt(bool cplx, const QmrVtArgs& a, int grid, cudaStream_t st);
+FlatPlanInfo flat_plan_info(int plan);
+int launch_flat(int plan, bool cplx, const FlatArgs& a, int grid, cudaStream_t st);  // grid < 0: resident CTAs per SM
 int launch_gram_mma(const GramArgs& g, int grid, cudaStream_t st);
 int launch_bsr(const BsrArgs& a, int s, int grid, cudaStream_t st);  // grid < 0: resident WARPS per SM
 int bsr_warps_per_cta();
@@ -240,6 +242,10 @@ struct Eng {
   bool qmr_tail_ok(int s) const { return ((n * (long long)s * (cplx ? 16 : 8)) % 16) == 0; }
   int qmr_tail(int s, void* P, void* D, const void* Pt, void* S, void* X, void* R, const void* Vt, int off_eta,
                int off_f, int off_invrho, int off_c1, int woff_r2, const QmrVec* v = nullptr);
+  // a scalar-coefficient update as a flat plan (flat_upd.cu): inputs, outputs, coefficient offsets in ws
+  // and the workspace offsets of the plan's reductions, in the plan's order; needs qmr_tail_ok(s)
+  int flat(int plan, int s, std::vector<const void*> in, std::vector<void*> out, std::vector<int> coff,
+           std::vector<int> woff);
   // eGl: the n-vector updates ride in the two block kernels (whole 16-byte units per block row)
   bool qmr_vec_ok(int s) const { return ((long long)s * (cplx ? 16 : 8)) % 16 == 0; }
   int qmr_vt(int s, const void* Pt, void* Vt, const void* AHQ, const void* Wt, int off_br, int off_bx, int woff_rho2,

@@ -172,6 +172,23 @@ struct QmrVtArgs {
   const int* done;
 };
 
+// Flat scalar-coefficient updates as compile-time plans (flat_upd.cu)
+enum FlatPlan : int { FP_STAB_S = 0, FP_STAB_XR = 1, FP_STAB_P = 2 };
+struct FlatPlanInfo {
+  int ni, no, nc, nr;
+  int rmode[2];
+};
+struct FlatArgs {
+  const void* in[6];
+  void* out[3];       // may alias inputs (a unit is read and rewritten by the same thread)
+  long long units;    // 16-byte units per block
+  const double* ws;
+  int coff[4];        // offsets (doubles) of the plan's coefficients in ws
+  double* partials;   // per CTA: the plan's reductions back to back
+  int pstride;
+  const int* done;
+};
+
 // Segments for the deterministic second-stage reduction of CTA partials.
 struct FinSeg {
   int poff, len, woff;

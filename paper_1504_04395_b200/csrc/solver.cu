@@ -672,16 +672,29 @@ struct GlBiCGStab : Solver {  // Gl (scalar) and Li (diag)
     e.upd(s, {R, Rt}, {}, {RQ{rmode(), 0, 1, nullptr, off[SL_RHO]}});
     return coef(0);
   }
+  // Gl (scalar coefficients): the three updates as flat plans (flat_upd.cu)
+  bool flat() const {
+    static const bool off_env = getenv("SRK_NO_FLAT_UPDATE") != nullptr;  // A/B switch
+    return !li && !off_env && e.qmr_tail_ok(s);
+  }
   void seg(int q) override {
     if (q == 0) {
       e.spmm(false, P, V, s, {RQ{rmode(), 0, -1, Rt, off[SL_DEN]}});  // V = A P ; <v, r̃>
       coef(1);
-      e.upd(s, {R, V}, {OutSpec{S, {{0, C1()}, {1, K(SL_ALPHA, 1)}}}}, {RQ{RED_NORM2, O0, -1, nullptr, off[SL_S2]}});
+      if (flat()) e.flat(FP_STAB_S, s, {R, V}, {S}, {off[SL_ALPHA]}, {off[SL_S2]});
+      else e.upd(s, {R, V}, {OutSpec{S, {{0, C1()}, {1, K(SL_ALPHA, 1)}}}}, {RQ{RED_NORM2, O0, -1, nullptr, off[SL_S2]}});
       coef(2);  // half-step test on ||S||_F
     } else {
       e.spmm(false, S, T, s,
              {RQ{rmode(), 0, -1, S, off[SL_ST]}, RQ{li ? RED_COLNORM2 : RED_NORM2, 0, -1, nullptr, off[SL_TT]}});
       coef(3);
+      if (flat()) {
+        e.flat(FP_STAB_XR, s, {X, P, S, T, Rt}, {X, R}, {off[SL_ALPHA], off[SL_OMEGA], off[SL_OMEGA]},
+               {off[SL_RHON], off[SL_R2]});
+        coef(4);
+        e.flat(FP_STAB_P, s, {R, P, V}, {P}, {off[SL_BETA], off[SL_BW]}, {});
+        return;
+      }
       e.upd(s, {X, P, S, T, Rt},
             {OutSpec{X, {{0, C1()}, {1, K(SL_ALPHA)}, {2, K(SL_OMEGA)}}},
              OutSpec{R, {{2, C1()}, {3, K(SL_OMEGA, 1)}}}},
@@ -839,7 +852,8 @@ struct BlBiCGStabrQ : Solver {
 // W = W̃/ξ are never materialised: 1/ρ and 1/ξ are folded into the coefficients
 // of the kernels that read Ṽ and W̃, and δ = <V, W> = <Ṽ, W̃>/(ρ ξ) is fused into
 // the kernel that produces Ṽ — an iteration moves 18 n x s blocks
-// instead of 20. Same recurrences as oracle/solvers.py::_qmr_li_gl.
+// instead of 20, and 17 with the fused tail (Gl / eGl: the last update also forms the
+// next P, qmr_tail.cu). Same recurrences as oracle/solvers.py::_qmr_li_gl.
 struct QMR : Solver {  // mode 0 Li, 1 Gl, 2 eGl
   int mode = 1;
   void *Vt, *P, *Pt, *D, *S, *Wt, *Qv, *AHQ;

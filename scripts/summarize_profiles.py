@@ -6,7 +6,7 @@
 Captures: prof_spmm (config 3 SpMM), prof_upd (config 3's dominant 6-in / 4-out update),
 prof_bsr (config 4 BSR-12 product), prof_gram (s = 64 CTA-tiled DMMA Gram), prof_updmma
 (config 2 tensor-core block update), prof_gramwarp (config 2 per-warp Gram of a block with
-itself), prof_plane (config 3's plane-marching SpMM), prof_small (config 1's single-CTA eGl-BiCG iteration kernel; a launch covers the
+itself), prof_plane (config 3's plane-marching SpMM), prof_tail / prof_vt (config 3's fused eGl-QMR tail and V~ kernels, qmr_tail.cu), prof_small (config 1's single-CTA eGl-BiCG iteration kernel; a launch covers the
 iterations between two polls). Reads gpurun_out/launches.csv (ncu --metrics gpu__time_duration.sum launch list of
 `python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu`), gpurun_out/prof_*.ncu-rep
 (`ncu --set full`) and gpurun_out/bench.log, and writes
@@ -53,7 +53,7 @@ def main(tag, pre=""):
     os.makedirs(PROF, exist_ok=True)
     spath = os.path.join(PROF, f"{tag}_ncu_summary.json")
     summary = json.load(open(spath)) if os.path.exists(spath) else {}  # later captures of a round update the file
-    for name in ("spmm", "upd", "bsr", "gram", "updmma", "gramwarp", "small", "band", "plane"):
+    for name in ("spmm", "upd", "bsr", "gram", "updmma", "gramwarp", "small", "band", "plane", "tail", "vt"):
         rep = os.path.join(OUT, f"{pre}prof_{name}.ncu-rep")
         if not os.path.exists(rep):
             continue
@@ -71,7 +71,9 @@ def main(tag, pre=""):
         tj["cfg3_egl_qmr_spmm"] = summary["plane"]["dram_bytes_per_launch"]
     elif "spmm" in summary:
         tj["cfg3_egl_qmr_spmm"] = summary["spmm"]["dram_bytes_per_launch"]
-    if "upd" in summary:  # the 6-input / 4-output update: the dominant kernel of the eGl-QMR step
+    if "tail" in summary:  # the fused 7-input / 5-output tail (qmr_tail.cu): the dominant kernel of the eGl-QMR step
+        tj["cfg3_egl_qmr_dominant"] = summary["tail"]["dram_bytes_per_launch"]
+    elif "upd" in summary:  # before the fused tail: the 6-input / 4-output update
         tj["cfg3_egl_qmr_dominant"] = summary["upd"]["dram_bytes_per_launch"]
     if len(tj) > 1:
         json.dump(tj, open(os.path.join(PROF, "traffic.json"), "w"), indent=1)

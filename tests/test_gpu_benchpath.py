@@ -147,3 +147,34 @@ def test_qmr_fused_tail_equals_separate_updates(srk, tmp_path, method, cplx, s):
     assert res["vec"][1][0] == res["plain"][1][0] == "converged"
     it_v, it_p = int(res["vec"][1][1]), int(res["plain"][1][1])
     assert abs(it_v - it_p) <= max(2, 0.02 * it_p), (it_v, it_p)
+
+
+@pytest.mark.parametrize("cplx,s", [(False, 16), (True, 12), (False, 5), (True, 3)])
+def test_gl_bicgstab_flat_plans_equal_generic_updates(srk, tmp_path, cplx, s):
+    """Gl-BiCGStab's three updates as flat plans (flat_upd.cu: the FMA order of the generic
+    upd_kernel per element, another summation order in ||S||^2, <R, R~>, ||R||^2) against the
+    generic kernels (SRK_NO_FLAT_UPDATE=1, a subprocess: the switch is read once): X_k and R_k
+    after 12 iterations within 1e-11 (well-conditioned operator, see the QMR test above),
+    stepped and graph-replayed runs bitwise equal, full solves with the same outcome and counts
+    within 2. Width 12 complex is config 4's; 5 / 3 give ragged last CTAs."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for tag, env, poll in (("flat", {}, 1), ("flatgraph", {}, 4), ("plain", {"SRK_NO_FLAT_UPDATE": "1"}, 1)):
+        out = str(tmp_path / f"{tag}.npy")
+        code = _FUSE_CODE.format(root=root, m=28, dt="np.complex128" if cplx else "np.float64", s=s, cplx=cplx,
+                                 method="gl_bicgstab", poll=poll, graph=tag.endswith("graph"), k=12, out=out)
+        r = subprocess.run([sys.executable, "-c", code], env={**os.environ, **env}, capture_output=True, text=True,
+                           timeout=900)
+        assert r.returncode == 0, r.stderr[-800:]
+        res[tag] = (np.load(out), r.stdout.split()[-2:])
+    ref = res["plain"][0]
+    assert np.isfinite(ref).all()
+    assert np.array_equal(res["flat"][0], res["flatgraph"][0])
+    for j in range(2):
+        assert rel(res["flat"][0][j], ref[j]) <= 1e-11, (j, rel(res["flat"][0][j], ref[j]))
+    assert res["flat"][1][0] == res["plain"][1][0] == "converged"
+    it_f, it_p = int(res["flat"][1][1]), int(res["plain"][1][1])
+    assert abs(it_f - it_p) <= max(2, 0.02 * it_p), (it_f, it_p)
