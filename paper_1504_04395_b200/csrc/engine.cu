@@ -560,6 +560,41 @@ int Eng::flat(int plan, int s, std::vector<const void*> in, std::vector<void*> o
   return err = finish_reds(*this, reds, poffs, s, grid, a.pstride);
 }
 
+int Eng::egl_bicg_flat(int which, int s, void* X, void* R, void* P, const void* Q, void* rh, void* ph, const void* qh,
+                       int off_alpha, int off_beta, int woff_rhon, int woff_r2) {
+  if (err) return err;
+  if (!qmr_vec_ok(s)) return err = (int)cudaErrorInvalidValue;
+  const size_t esz = cplx ? 16 : 8;
+  EglFlatArgs a{};
+  a.X = X; a.R = R; a.P = P; a.Q = Q; a.rh = rh; a.ph = ph; a.qh = qh;
+  a.upr = (int)((size_t)s * esz / 16);
+  a.sh = log2_or_neg(a.upr);
+  a.units = n * (long long)a.upr;
+  a.ws = ws;
+  a.off_alpha = off_alpha; a.off_beta = off_beta;
+  const int nd = cplx ? 2 : 1;
+  a.pstride = nd + 1;
+  a.done = done;
+  static std::atomic<int> occ_c[2][2] = {};
+  int occ = occ_c[which & 1][cplx].load();
+  if (occ == 0) {
+    occ = std::max(1, launch_egl_flat(which, cplx, a, -1, nullptr));
+    occ_c[which & 1][cplx].store(occ);
+  }
+  const long long need = std::max<long long>(1, (a.units + 255) / 256);
+  const int grid = (int)std::min<long long>(need, (long long)c->nsm * occ);  // one wave
+  if (which == 0 && (err = c->ensure_partials((size_t)grid * a.pstride))) return err;
+  a.partials = c->partials;
+  nlaunch++;
+  const double B = (double)n * s * esz, v = (double)n * esz;
+  if (prof) prof->begin(PT_UPD, c->st, which == 0 ? 16 * 4 + 2 : 16 * 2 + 1, which == 0 ? 6.0 * B + 2.0 * v : 3.0 * B + 5.0 * v);
+  err = launch_egl_flat(which, cplx, a, grid, c->st);
+  if (prof) prof->end(c->st);
+  if (err || which != 0) return err;
+  return err = finish_reds(*this, {RQ{RED_SUMVEC, SRC_OUT + 1, -1, rh, woff_rhon}, RQ{RED_NORM2, SRC_OUT + 1, -1, nullptr, woff_r2}},
+                           {0, nd}, s, grid, a.pstride);
+}
+
 int Eng::qmr_vt(int s, const void* Pt, void* Vt, const void* AHQ, const void* Wt, int off_br, int off_bx, int woff_rho2,
                 int woff_k1, int woff_xi2) {
   if (err) return err;

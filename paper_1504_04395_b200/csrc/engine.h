@@ -22,6 +22,7 @@ int launch_fin(const FinArgs& a, cudaStream_t st);
 int launch_qmr_tail(bool cplx, const QmrTailArgs& a, int grid, cudaStream_t st);  // grid < 0: resident CTAs per SM
 int launch_qmr_vt(bool cplx, const QmrVtArgs& a, int grid, cudaStream_t st);
 FlatPlanInfo flat_plan_info(int plan);
+int launch_egl_flat(int which, bool cplx, const EglFlatArgs& a, int grid, cudaStream_t st);  // grid < 0: resident CTAs per SM
 int launch_flat(int plan, bool cplx, const FlatArgs& a, int grid, cudaStream_t st);  // grid < 0: resident CTAs per SM
 int launch_gram_mma(const GramArgs& g, int grid, cudaStream_t st);
 int launch_bsr(const BsrArgs& a, int s, int grid, cudaStream_t st);  // grid < 0: resident WARPS per SM
@@ -246,6 +247,11 @@ struct Eng {
   // and the workspace offsets of the plan's reductions, in the plan's order; needs qmr_tail_ok(s)
   int flat(int plan, int s, std::vector<const void*> in, std::vector<void*> out, std::vector<int> coff,
            std::vector<int> woff);
+  // eGl-BiCG (egl_flat.cu; needs qmr_vec_ok(s)): which = 0: X += alpha P, R -= alpha Q with sum(r̂^H R) and
+  // ||R||^2 for the new r̂ = r̂ - conj(alpha) q̂ (kept in registers); which = 1: P = R + beta P, r̂ stored,
+  // p̂ = r̂ + conj(beta) p̂
+  int egl_bicg_flat(int which, int s, void* X, void* R, void* P, const void* Q, void* rh, void* ph, const void* qh,
+                    int off_alpha, int off_beta, int woff_rhon, int woff_r2);
   // eGl: the n-vector updates ride in the two block kernels (whole 16-byte units per block row)
   bool qmr_vec_ok(int s) const { return ((long long)s * (cplx ? 16 : 8)) % 16 == 0; }
   int qmr_vt(int s, const void* Pt, void* Vt, const void* AHQ, const void* Wt, int off_br, int off_bx, int woff_rho2,

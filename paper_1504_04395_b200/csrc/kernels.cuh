@@ -189,6 +189,22 @@ struct FlatArgs {
   const int* done;
 };
 
+// eGl-BiCG lean kernels (egl_flat.cu): flat blocks of `units` 16-byte units, upr units per block row
+// (sh = log2(upr) or -1); n-vectors r̂, q̂, p̂; partials per CTA: [sum(r̂^H R) (ND doubles), ||R||^2]
+struct EglFlatArgs {
+  void *X, *R, *P;
+  const void* Q;
+  void *rh, *ph;
+  const void* qh;
+  long long units;
+  int upr, sh;
+  const double* ws;
+  int off_alpha, off_beta;
+  double* partials;
+  int pstride;
+  const int* done;
+};
+
 // Segments for the deterministic second-stage reduction of CTA partials.
 struct FinSeg {
   int poff, len, woff;

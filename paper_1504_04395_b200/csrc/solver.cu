@@ -554,6 +554,14 @@ struct EglBiCG : Solver {  // Alg. 4
     e.spmm(false, P, Q, s, {RQ{RED_SUMVEC, 0, -1, ph, off[SL_DEN]}});  // sum(p̂^H Q)
     e.spmm(true, ph, qh, 1, {});                                        // A^H p̂ (one vector)
     coef(1);
+    static const bool no_lean = getenv("SRK_NO_FLAT_UPDATE") != nullptr;  // A/B switch
+    if (!no_lean && e.qmr_vec_ok(s)) {
+      // the two block updates as lean flat kernels that carry r̂ and p̂ (egl_flat.cu)
+      e.egl_bicg_flat(0, s, X, R, P, Q, rh, ph, qh, off[SL_ALPHA], off[SL_BETA], off[SL_RHON], off[SL_R2]);
+      coef(2);
+      e.egl_bicg_flat(1, s, X, R, P, Q, rh, ph, qh, off[SL_ALPHA], off[SL_BETA], off[SL_RHON], off[SL_R2]);
+      return;
+    }
     e.upd(1, {rh, qh}, {OutSpec{rh, {{0, C1()}, {1, SC(off[SL_ALPHA], 1, 1)}}}}, {});
     e.upd(s, {X, P, R, Q},
           {OutSpec{X, {{0, C1()}, {1, SC(off[SL_ALPHA])}}}, OutSpec{R, {{2, C1()}, {3, SC(off[SL_ALPHA], 1)}}}},

@@ -149,9 +149,11 @@ def test_qmr_fused_tail_equals_separate_updates(srk, tmp_path, method, cplx, s):
     assert abs(it_v - it_p) <= max(2, 0.02 * it_p), (it_v, it_p)
 
 
-@pytest.mark.parametrize("cplx,s", [(False, 16), (True, 12), (False, 5), (True, 3)])
-def test_gl_bicgstab_flat_plans_equal_generic_updates(srk, tmp_path, cplx, s):
-    """Gl-BiCGStab's three updates as flat plans (flat_upd.cu: the FMA order of the generic
+@pytest.mark.parametrize("method", ["gl_bicgstab", "egl_bicg"])
+@pytest.mark.parametrize("cplx,s", [(False, 16), (True, 12), (False, 5), (False, 6), (True, 3)])
+def test_flat_plans_equal_generic_updates(srk, tmp_path, method, cplx, s):
+    """eGl-BiCG's two block updates as lean flat kernels that carry r̂ and p̂ (egl_flat.cu) and
+    Gl-BiCGStab's three updates as flat plans (flat_upd.cu: the FMA order of the generic
     upd_kernel per element, another summation order in ||S||^2, <R, R~>, ||R||^2) against the
     generic kernels (SRK_NO_FLAT_UPDATE=1, a subprocess: the switch is read once): X_k and R_k
     after 12 iterations within 1e-11 (well-conditioned operator, see the QMR test above),
@@ -165,7 +167,7 @@ def test_gl_bicgstab_flat_plans_equal_generic_updates(srk, tmp_path, cplx, s):
     for tag, env, poll in (("flat", {}, 1), ("flatgraph", {}, 4), ("plain", {"SRK_NO_FLAT_UPDATE": "1"}, 1)):
         out = str(tmp_path / f"{tag}.npy")
         code = _FUSE_CODE.format(root=root, m=28, dt="np.complex128" if cplx else "np.float64", s=s, cplx=cplx,
-                                 method="gl_bicgstab", poll=poll, graph=tag.endswith("graph"), k=12, out=out)
+                                 method=method, poll=poll, graph=tag.endswith("graph"), k=12, out=out)
         r = subprocess.run([sys.executable, "-c", code], env={**os.environ, **env}, capture_output=True, text=True,
                            timeout=900)
         assert r.returncode == 0, r.stderr[-800:]
