@@ -729,6 +729,13 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) band_plane_kernel(PlaneArgs 
   red_zero<T, S, false>(acc1);
   const int m0 = a.nred > 0 ? a.red[0].mode : RED_NONE;
   const int m1 = a.nred > 1 ? a.red[1].mode : RED_NONE;
+  // row operands (TRACE / DIAG: acc += conj(y_row) .* q_row): the product's own input row is the
+  // centre row already in registers (Gl-BiCGStab's <A S, S>); the rows of one external block
+  // (<A P, R~>) are requested at the top of each plane step, ahead of the window wait
+  int qext = -1;
+  if (m0 != RED_NONE && red_ykind(m0) == 2 && a.red[0].yext != a.P) qext = 0;
+  if (m1 != RED_NONE && red_ykind(m1) == 2 && a.red[1].yext != a.P) qext = 1;
+  const T* yext = qext >= 0 ? reinterpret_cast<const T*>(a.red[qext].yext) : nullptr;
   int st = 0;
   unsigned ph = 0;
   auto release = [&]() {
@@ -777,6 +784,17 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) band_plane_kernel(PlaneArgs 
         ns = 0;
         nph ^= 1u;
       }
+      T yr[RPL][L::EPL];
+#pragma unroll
+      for (int k = 0; k < RPL; ++k) {
+#pragma unroll
+        for (int e = 0; e < L::EPL; ++e) yr[k][e] = Ar<T>::zero();
+        if (yext && live[k]) {
+          const int rr = slot + k * SLOTS;
+          const long long i = z * F + (long long)(y0 + rr / PL_TX) * m + x0 + rr % PL_TX;
+          if (i < n) row_load_ex_rw<T, S>(yext + (size_t)i * S, g, yr[k]);
+        }
+      }
       bwait(full + ns, nph);  // window z + 1
       const T* wc = win + (size_t)cs * C::WR * S;
       const T* wn = win + (size_t)ns * C::WR * S;
@@ -821,7 +839,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) band_plane_kernel(PlaneArgs 
                 T yy[L::EPL];
                 const T yv = yk == 1 ? sy[((size_t)yslot[q] * PL_TY + yl) * C::YL + sh + xl] : Ar<T>::zero();
 #pragma unroll
-                for (int e = 0; e < L::EPL; ++e) yy[e] = yk == 0 ? x[e] : yv;
+                for (int e = 0; e < L::EPL; ++e) yy[e] = yk == 0 ? x[e] : (yk == 1 ? yv : (q == qext ? yr[k][e] : cur[k][e]));
                 if (q == 0) red_acc<T, S, false>(acc0, x, yy);
                 else red_acc<T, S, false>(acc1, x, yy);
               }
@@ -945,16 +963,16 @@ static int launch_plane_t(const BandArgs& ba, const Mat::Band& b, int nsm, cudaS
   a.ntx = (a.m + PL_TX - 1) / PL_TX;
   a.nty = (a.ny + PL_TY - 1) / PL_TY;
   a.nred = ba.nred;
-  int ny = 0;
+  int ny = 0, next = 0;
   for (int q = 0; q < a.nred; ++q) {
     a.red[q] = ba.red[q];
     const int md = a.red[q].mode;
     const int yk = (md == RED_NORM2 || md == RED_COLNORM2) ? 0 : (md == RED_SUMVEC ? 1 : 2);
-    if (yk == 2) return (int)cudaErrorNotSupported;  // row operands: the band / CSR kernels
-    if (yk == 1 && (!a.red[q].yext || ((uintptr_t)a.red[q].yext & 15) || a.red[q].ysrc >= 0))
+    if (yk && (!a.red[q].yext || ((uintptr_t)a.red[q].yext & 15) || a.red[q].ysrc >= 0))
       return (int)cudaErrorNotSupported;
-    a.ystage[q] = yk;
-    ny += yk;
+    if (yk == 2 && a.red[q].yext != a.P && ++next > 1) return (int)cudaErrorNotSupported;  // one external row operand
+    a.ystage[q] = yk == 1;  // SUMVEC vectors are staged per plane by the copy engine
+    ny += yk == 1;
   }
   a.partials = ba.partials;
   a.pstride = ba.pstride;

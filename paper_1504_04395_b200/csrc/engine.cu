@@ -217,7 +217,10 @@ int Eng::spmm(bool adj, const void* P, void* Q, int s, std::vector<RQ> reds) {
     yred |= (q.mode != RED_NORM2 && q.mode != RED_COLNORM2);
     yrow |= (q.mode != RED_NORM2 && q.mode != RED_COLNORM2 && q.mode != RED_SUMVEC);
   }
-  if (yred && !yrow && bd.K > 0 && band_plane_pattern(bd)) yred = false;  // staged by the plane kernel
+  // the plane-marching kernel takes vector operands (staged per plane) and row operands (the input's
+  // own rows from registers, one external block's rows by early loads)
+  static const bool plane_rows = getenv("SRK_NO_PLANE_ROWS") == nullptr;  // A/B switch
+  if (yred && (!yrow || plane_rows) && bd.K > 0 && band_plane_pattern(bd)) yred = false;
   if (bd.K > 0 && !full && (band_all || !yred) && A->ghost_rows() == 0 && band_supported(cplx, s) && reds.size() <= 2) {
     std::vector<Red> rr(reds.size());
     std::vector<int> poffs;
@@ -238,7 +241,7 @@ int Eng::spmm(bool adj, const void* P, void* Q, int s, std::vector<RQ> reds) {
         // algorithmic bytes of the banded form: the K diagonals once, P read once, Q written once
         double nb = (double)bd.K * n * esz + 2.0 * (double)n * s * esz;
         for (auto& q : reds)
-          if (q.yext && q.mode != RED_NORM2 && q.mode != RED_COLNORM2)
+          if (q.yext && q.yext != P && q.mode != RED_NORM2 && q.mode != RED_COLNORM2)
             nb += (double)n * (q.mode == RED_SUMVEC ? 1 : s) * esz;
         prof->begin(adj ? PT_SPMM_ADJ : PT_SPMM, c->st, s, nb);
       }

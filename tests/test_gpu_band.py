@@ -192,6 +192,19 @@ def test_plane_spmm_matches_oracle_product(srk, name, adj):
             # sum cancels, so a bound relative to the result alone would be order dependent)
             assert np.all(np.abs(to_np(gv).ravel() - np.asarray(ref).ravel()) <= 1e-13 * np.asarray(mag).ravel()), \
                 (name, adj, s, gram)
+        # row operands (Gl-BiCGStab's <A P, R~> and <A S, S>, Li's per-column forms): an external block
+        # (rows requested ahead of each plane step) and the product's own input (rows already in registers)
+        Yb = synth.random_rhs(n, s, s + 11, cplx)
+        Pd = to_dev(P)
+        for gram in ("trace", "diag"):
+            for Yh, Yd in ((Yb, to_dev(Yb)), (P, Pd)):
+                prod = Yh.conj() * R
+                ref = [prod.sum()] if gram == "trace" else prod.sum(axis=0)
+                mag = [np.abs(prod).sum()] if gram == "trace" else np.abs(prod).sum(axis=0)
+                Q2, gv = srk.spmm_block(M, Pd, adjoint=adj, gram=gram, Y=Yd)
+                assert rel(to_np(Q2), R) <= 1e-14, (name, gram)
+                assert np.all(np.abs(to_np(gv).ravel() - np.asarray(ref).ravel()) <= 1e-13 * np.asarray(mag).ravel()), \
+                    (name, adj, s, gram, Yh is P)
 
 
 _PLANE_VS_RING = r"""
