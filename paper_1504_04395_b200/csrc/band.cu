@@ -601,7 +601,10 @@ size_t plane_smem(int NB, int ny) {
   return 128 + (size_t)NB * (C::WIN + C::VAL + (size_t)ny * C::YV);
 }
 
-template <typename T, int S, int NW>
+// YROW: instance with row-operand reductions (TRACE / DIAG); the plain / NORM2 / SUMVEC instance
+// keeps its register budget (config 3's SpMM + eGl sum: 92 registers, 0.87 ms; with the row-operand
+// code compiled in: 96 registers, 0.90 ms)
+template <typename T, int S, int NW, bool YROW>
 __global__ void __launch_bounds__(32 * (NW + 1), 1) band_plane_kernel(PlaneArgs a) {
   if (a.done && *a.done) return;
   using L = Lay<T, S>;
@@ -733,8 +736,10 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) band_plane_kernel(PlaneArgs 
   // centre row already in registers (Gl-BiCGStab's <A S, S>); the rows of one external block
   // (<A P, R~>) are requested at the top of each plane step, ahead of the window wait
   int qext = -1;
-  if (m0 != RED_NONE && red_ykind(m0) == 2 && a.red[0].yext != a.P) qext = 0;
-  if (m1 != RED_NONE && red_ykind(m1) == 2 && a.red[1].yext != a.P) qext = 1;
+  if constexpr (YROW) {
+    if (m0 != RED_NONE && red_ykind(m0) == 2 && a.red[0].yext != a.P) qext = 0;
+    if (m1 != RED_NONE && red_ykind(m1) == 2 && a.red[1].yext != a.P) qext = 1;
+  }
   const T* yext = qext >= 0 ? reinterpret_cast<const T*>(a.red[qext].yext) : nullptr;
   int st = 0;
   unsigned ph = 0;
@@ -784,15 +789,17 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) band_plane_kernel(PlaneArgs 
         ns = 0;
         nph ^= 1u;
       }
-      T yr[RPL][L::EPL];
+      T yr[YROW ? RPL : 1][L::EPL];
+      if constexpr (YROW) {
 #pragma unroll
-      for (int k = 0; k < RPL; ++k) {
+        for (int k = 0; k < RPL; ++k) {
 #pragma unroll
-        for (int e = 0; e < L::EPL; ++e) yr[k][e] = Ar<T>::zero();
-        if (yext && live[k]) {
-          const int rr = slot + k * SLOTS;
-          const long long i = z * F + (long long)(y0 + rr / PL_TX) * m + x0 + rr % PL_TX;
-          if (i < n) row_load_ex_rw<T, S>(yext + (size_t)i * S, g, yr[k]);
+          for (int e = 0; e < L::EPL; ++e) yr[k][e] = Ar<T>::zero();
+          if (yext && live[k]) {
+            const int rr = slot + k * SLOTS;
+            const long long i = z * F + (long long)(y0 + rr / PL_TX) * m + x0 + rr % PL_TX;
+            if (i < n) row_load_ex_rw<T, S>(yext + (size_t)i * S, g, yr[k]);
+          }
         }
       }
       bwait(full + ns, nph);  // window z + 1
@@ -839,7 +846,10 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) band_plane_kernel(PlaneArgs 
                 T yy[L::EPL];
                 const T yv = yk == 1 ? sy[((size_t)yslot[q] * PL_TY + yl) * C::YL + sh + xl] : Ar<T>::zero();
 #pragma unroll
-                for (int e = 0; e < L::EPL; ++e) yy[e] = yk == 0 ? x[e] : (yk == 1 ? yv : (q == qext ? yr[k][e] : cur[k][e]));
+                for (int e = 0; e < L::EPL; ++e) {
+                  if constexpr (YROW) yy[e] = yk == 0 ? x[e] : (yk == 1 ? yv : (q == qext ? yr[k][e] : cur[k][e]));
+                  else yy[e] = yk == 0 ? x[e] : yv;
+                }
                 if (q == 0) red_acc<T, S, false>(acc0, x, yy);
                 else red_acc<T, S, false>(acc1, x, yy);
               }
@@ -963,7 +973,7 @@ static int launch_plane_t(const BandArgs& ba, const Mat::Band& b, int nsm, cudaS
   a.ntx = (a.m + PL_TX - 1) / PL_TX;
   a.nty = (a.ny + PL_TY - 1) / PL_TY;
   a.nred = ba.nred;
-  int ny = 0, next = 0;
+  int ny = 0, next = 0, nrow = 0;
   for (int q = 0; q < a.nred; ++q) {
     a.red[q] = ba.red[q];
     const int md = a.red[q].mode;
@@ -971,6 +981,7 @@ static int launch_plane_t(const BandArgs& ba, const Mat::Band& b, int nsm, cudaS
     if (yk && (!a.red[q].yext || ((uintptr_t)a.red[q].yext & 15) || a.red[q].ysrc >= 0))
       return (int)cudaErrorNotSupported;
     if (yk == 2 && a.red[q].yext != a.P && ++next > 1) return (int)cudaErrorNotSupported;  // one external row operand
+    nrow += yk == 2;
     a.ystage[q] = yk == 1;  // SUMVEC vectors are staged per plane by the copy engine
     ny += yk == 1;
   }
@@ -1009,9 +1020,12 @@ static int launch_plane_t(const BandArgs& ba, const Mat::Band& b, int nsm, cudaS
   }
   const size_t smem = plane_smem<T, S>(a.NB, ny);
   static std::atomic<unsigned long long> attr{0};
-  if (first_on_device(attr))
-    cudaFuncSetAttribute(band_plane_kernel<T, S, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-  band_plane_kernel<T, S, NW><<<grid, 32 * (NW + 1), smem, st>>>(a);
+  if (first_on_device(attr)) {
+    cudaFuncSetAttribute(band_plane_kernel<T, S, NW, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    cudaFuncSetAttribute(band_plane_kernel<T, S, NW, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+  }
+  if (nrow) band_plane_kernel<T, S, NW, true><<<grid, 32 * (NW + 1), smem, st>>>(a);
+  else band_plane_kernel<T, S, NW, false><<<grid, 32 * (NW + 1), smem, st>>>(a);
   return (int)cudaGetLastError();
 }
 

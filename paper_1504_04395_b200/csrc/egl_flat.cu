@@ -84,6 +84,16 @@ __global__ void __launch_bounds__(256, 4) egl_bicg_p_kernel(EglFlatArgs a) {
   const T ncal = Ar<T>::sub(zero, Ar<T>::conj(Ar<T>::ld(a.ws + a.off_alpha)));
   const long long stride = (long long)gridDim.x * 256;
   for (long long u = (long long)blockIdx.x * 256 + threadIdx.x; u < a.units; u += stride) {
+    // the row's n-vector entries are requested with the block loads (by the thread that owns the
+    // row's first unit)
+    const long long row = a.sh >= 0 ? (u >> a.sh) : (u / a.upr);
+    const bool lead = u == (a.sh >= 0 ? (row << a.sh) : row * a.upr);
+    T ro = zero, qo = zero, po = zero;
+    if (lead) {
+      ro = reinterpret_cast<const T*>(a.rh)[row];
+      qo = reinterpret_cast<const T*>(a.qh)[row];
+      po = reinterpret_cast<const T*>(a.ph)[row];
+    }
     const double2 tr = reinterpret_cast<const double2*>(a.R)[u];
     const double2 tp = reinterpret_cast<const double2*>(a.P)[u];
     if constexpr (E == 2) {
@@ -92,13 +102,10 @@ __global__ void __launch_bounds__(256, 4) egl_bicg_p_kernel(EglFlatArgs a) {
     } else {
       reinterpret_cast<double2*>(a.P)[u] = Ar<T>::fma(tp, be, Ar<T>::fma(tr, one, zero));
     }
-    const long long row = a.sh >= 0 ? (u >> a.sh) : (u / a.upr);
-    if (u == (a.sh >= 0 ? (row << a.sh) : row * a.upr)) {
-      T* rh = reinterpret_cast<T*>(a.rh) + row;
-      T* ph = reinterpret_cast<T*>(a.ph) + row;
-      const T rhn = Ar<T>::fma(reinterpret_cast<const T*>(a.qh)[row], ncal, Ar<T>::fma(*rh, one, zero));
-      *rh = rhn;
-      *ph = Ar<T>::fma(*ph, cbe, Ar<T>::fma(rhn, one, zero));
+    if (lead) {
+      const T rhn = Ar<T>::fma(qo, ncal, Ar<T>::fma(ro, one, zero));
+      reinterpret_cast<T*>(a.rh)[row] = rhn;
+      reinterpret_cast<T*>(a.ph)[row] = Ar<T>::fma(po, cbe, Ar<T>::fma(rhn, one, zero));
     }
   }
 }

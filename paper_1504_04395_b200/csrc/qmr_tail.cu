@@ -58,6 +58,20 @@ __global__ void __launch_bounds__(256, sizeof(T) == 16 ? 3 : 4) qmr_tail_kernel(
   };
   const long long stride = (long long)gridDim.x * 256;
   for (long long u = (long long)blockIdx.x * 256 + threadIdx.x; u < a.units; u += stride) {
+    // eGl: the thread that owns the first unit of a row also carries the row's n-vector entries;
+    // their loads are issued with the block loads
+    bool lead = false;
+    long long row = 0;
+    T wo = zero, ah = zero, qo = zero;
+    if (a.upr > 0) {
+      row = a.sh >= 0 ? (u >> a.sh) : (u / a.upr);
+      lead = u == (a.sh >= 0 ? (row << a.sh) : row * a.upr);
+      if (lead) {
+        wo = reinterpret_cast<const T*>(a.Wt)[row];
+        ah = reinterpret_cast<const T*>(a.AHQ)[row];
+        qo = reinterpret_cast<const T*>(a.Qv)[row];
+      }
+    }
     T p[E], d[E], pt[E], s[E], x[E], r[E], vt[E];
     ld(a.P, u, p);
     ld(a.D, u, d);
@@ -84,15 +98,10 @@ __global__ void __launch_bounds__(256, sizeof(T) == 16 ? 3 : 4) qmr_tail_kernel(
     // eGl: the left Lanczos vectors of the next iteration, by the thread that owns the first unit of
     // a row (nobody else touches them): w̃ <- A^H q - (conj(beta)/xi) w̃ (deferred from qmr_vt_kernel,
     // which only reduced it) and q <- w̃/xi' - c2' q
-    if (a.upr > 0) {
-      const long long row = a.sh >= 0 ? (u >> a.sh) : (u / a.upr);
-      if (u == (a.sh >= 0 ? (row << a.sh) : row * a.upr)) {
-        T* wt = reinterpret_cast<T*>(a.Wt) + row;
-        T* qv = reinterpret_cast<T*>(a.Qv) + row;
-        const T wn = Ar<T>::fma(*wt, nbx, Ar<T>::fma(reinterpret_cast<const T*>(a.AHQ)[row], one, zero));
-        *wt = wn;
-        *qv = Ar<T>::fma(*qv, nc2, Ar<T>::fma(wn, ix, zero));
-      }
+    if (lead) {
+      const T wn = Ar<T>::fma(wo, nbx, Ar<T>::fma(ah, one, zero));
+      reinterpret_cast<T*>(a.Wt)[row] = wn;
+      reinterpret_cast<T*>(a.Qv)[row] = Ar<T>::fma(qo, nc2, Ar<T>::fma(wn, ix, zero));
     }
   }
   __syncwarp();
