@@ -14,7 +14,8 @@
 //
 // Plans: Gl-BiCGStab (SURVEY App. A.4 with scalar coefficients; the method of config 4 and
 // config 3's second method): S = R - alpha V with ||S||^2; (X, R) = (X + alpha P + omega S,
-// S - omega T) with <R, R~> and ||R||^2; P = R + beta P - beta omega V.
+// S - omega T) with <R, R~> and ||R||^2; P = R + beta P - beta omega V. Gl-BiCG (Alg. 2): the (X, R, R^)
+// update with <R, R^> and ||R||^2, and the (P, P^) update.
 #include <cuda_runtime.h>
 
 #include "block_kernels.cuh"
@@ -31,6 +32,7 @@ __device__ __forceinline__ T one_of() {
 // S = R - alpha V ; ||S||^2                      in: R, V ; coef: alpha (negated)
 struct PlanStabS {
   static constexpr int NI = 2, NO = 1, NC = 1, NR = 1;
+  __host__ __device__ static constexpr bool cj(int) { return false; }
   __host__ __device__ static constexpr bool neg(int) { return true; }
   __host__ __device__ static constexpr int rmode(int) { return RED_NORM2; }
   template <typename T>
@@ -43,6 +45,7 @@ struct PlanStabS {
 // X = X + alpha P + omega S ; R = S - omega T ; <R, R~>, ||R||^2      in: X, P, S, T, R~ ; coef: alpha, omega, -omega
 struct PlanStabXR {
   static constexpr int NI = 5, NO = 2, NC = 3, NR = 2;
+  __host__ __device__ static constexpr bool cj(int) { return false; }
   __host__ __device__ static constexpr bool neg(int i) { return i == 2; }
   __host__ __device__ static constexpr int rmode(int r) { return r == 0 ? RED_TRACE : RED_NORM2; }
   template <typename T>
@@ -57,6 +60,7 @@ struct PlanStabXR {
 // P = R + beta P - (beta omega) V                in: R, P, V ; coef: beta, beta omega (negated)
 struct PlanStabP {
   static constexpr int NI = 3, NO = 1, NC = 2, NR = 0;
+  __host__ __device__ static constexpr bool cj(int) { return false; }
   __host__ __device__ static constexpr bool neg(int i) { return i == 1; }
   __host__ __device__ static constexpr int rmode(int) { return RED_NONE; }
   template <typename T>
@@ -66,8 +70,39 @@ struct PlanStabP {
   }
 };
 
+// Gl-BiCG (Alg. 2): X = X + alpha P ; R = R - alpha Q ; R^ = R^ - conj(alpha) Q^ ; <R, R^>, ||R||^2
+//                                in: X, P, R, Q, R^, Q^ ; coef: alpha, -alpha, -conj(alpha)
+struct PlanBicgXR {
+  static constexpr int NI = 6, NO = 3, NC = 3, NR = 2;
+  __host__ __device__ static constexpr bool cj(int i) { return i == 2; }
+  __host__ __device__ static constexpr bool neg(int i) { return i >= 1; }
+  __host__ __device__ static constexpr int rmode(int r) { return r == 0 ? RED_TRACE : RED_NORM2; }
+  template <typename T>
+  __device__ __forceinline__ static void elem(const T (&x)[NI], const T (&c)[NC], T (&y)[NO], T (&ra)[NR]) {
+    const T z = Ar<T>::zero();
+    y[0] = Ar<T>::fma(x[1], c[0], Ar<T>::fma(x[0], one_of<T>(), z));
+    y[1] = Ar<T>::fma(x[3], c[1], Ar<T>::fma(x[2], one_of<T>(), z));
+    y[2] = Ar<T>::fma(x[5], c[2], Ar<T>::fma(x[4], one_of<T>(), z));
+    ra[0] = Ar<T>::cfma(y[2], y[1], ra[0]);
+    ra[1] = Ar<T>::cfma(y[1], y[1], ra[1]);
+  }
+};
+// P = R + beta P ; P^ = R^ + conj(beta) P^        in: R, P, R^, P^ ; coef: beta, conj(beta)
+struct PlanBicgP {
+  static constexpr int NI = 4, NO = 2, NC = 2, NR = 0;
+  __host__ __device__ static constexpr bool cj(int i) { return i == 1; }
+  __host__ __device__ static constexpr bool neg(int) { return false; }
+  __host__ __device__ static constexpr int rmode(int) { return RED_NONE; }
+  template <typename T>
+  __device__ __forceinline__ static void elem(const T (&x)[NI], const T (&c)[NC], T (&y)[NO], T (&)[1]) {
+    const T z = Ar<T>::zero();
+    y[0] = Ar<T>::fma(x[1], c[0], Ar<T>::fma(x[0], one_of<T>(), z));
+    y[1] = Ar<T>::fma(x[3], c[1], Ar<T>::fma(x[2], one_of<T>(), z));
+  }
+};
+
 template <typename T, typename P>
-__global__ void __launch_bounds__(256, (sizeof(T) == 16 && P::NI > 3) ? 3 : 4) flat_kernel(FlatArgs a) {
+__global__ void __launch_bounds__(256, (sizeof(T) == 16 && P::NI > 3) ? (P::NI > 5 ? 2 : 3) : (P::NI > 5 ? 3 : 4)) flat_kernel(FlatArgs a) {
   if (a.done && *a.done) return;
   constexpr int W = 128 / (int)sizeof(T);
   using L = Lay<T, W>;
@@ -78,6 +113,7 @@ __global__ void __launch_bounds__(256, (sizeof(T) == 16 && P::NI > 3) ? 3 : 4) f
 #pragma unroll
   for (int i = 0; i < P::NC; ++i) {
     c[i] = Ar<T>::ld(a.ws + a.coff[i]);
+    if (P::cj(i)) c[i] = Ar<T>::conj(c[i]);
     if (P::neg(i)) c[i] = Ar<T>::sub(Ar<T>::zero(), c[i]);
   }
   RedAcc<T, W, false> acc[NRA];
@@ -150,6 +186,8 @@ FlatPlanInfo flat_plan_info(int plan) {
     case FP_STAB_S: return info_of<PlanStabS>();
     case FP_STAB_XR: return info_of<PlanStabXR>();
     case FP_STAB_P: return info_of<PlanStabP>();
+    case FP_BICG_XR: return info_of<PlanBicgXR>();
+    case FP_BICG_P: return info_of<PlanBicgP>();
     default: return FlatPlanInfo{};
   }
 }
@@ -160,6 +198,8 @@ int launch_flat(int plan, bool cplx, const FlatArgs& a, int grid, cudaStream_t s
     case FP_STAB_S: return launch_plan<PlanStabS>(cplx, a, grid, st);
     case FP_STAB_XR: return launch_plan<PlanStabXR>(cplx, a, grid, st);
     case FP_STAB_P: return launch_plan<PlanStabP>(cplx, a, grid, st);
+    case FP_BICG_XR: return launch_plan<PlanBicgXR>(cplx, a, grid, st);
+    case FP_BICG_P: return launch_plan<PlanBicgP>(cplx, a, grid, st);
     default: return grid < 0 ? 0 : (int)cudaErrorInvalidValue;
   }
 }

@@ -173,7 +173,7 @@ struct QmrVtArgs {
 };
 
 // Flat scalar-coefficient updates as compile-time plans (flat_upd.cu)
-enum FlatPlan : int { FP_STAB_S = 0, FP_STAB_XR = 1, FP_STAB_P = 2 };
+enum FlatPlan : int { FP_STAB_S = 0, FP_STAB_XR = 1, FP_STAB_P = 2, FP_BICG_XR = 3, FP_BICG_P = 4 };
 struct FlatPlanInfo {
   int ni, no, nc, nr;
   int rmode[2];

@@ -483,6 +483,14 @@ struct GlBiCG : Solver {  // Alg. 2 (Gl) and Alg. 1 (Li: diag coefficients)
     e.spmm(false, P, Q, s, {RQ{rmode(), 0, -1, Ph, off[SL_DEN]}});   // Q = A P ; <q, p̂>
     e.spmm(true, Ph, Qh, s, {});                                     // A^H P̂
     coef(1);
+    static const bool no_flat = getenv("SRK_NO_FLAT_UPDATE") != nullptr;  // A/B switch
+    if (!li && !no_flat && e.qmr_tail_ok(s)) {  // Gl (scalar coefficients): flat plans (flat_upd.cu)
+      e.flat(FP_BICG_XR, s, {X, P, R, Q, Rh, Qh}, {X, R, Rh}, {off[SL_ALPHA], off[SL_ALPHA], off[SL_ALPHA]},
+             {off[SL_RHON], off[SL_R2]});
+      coef(2);
+      e.flat(FP_BICG_P, s, {R, P, Rh, Ph}, {P, Ph}, {off[SL_BETA], off[SL_BETA]}, {});
+      return;
+    }
     e.upd(s, {X, P, R, Q, Rh, Qh},
           {OutSpec{X, {{0, C1()}, {1, K(SL_ALPHA)}}},
            OutSpec{R, {{2, C1()}, {3, K(SL_ALPHA, 1)}}},

@@ -87,25 +87,65 @@ def test_benchpath_full_solve(srk, problem, method):
     assert abs(true - rep.final_true_rel_residual) <= 1e-12 + 1e-6 * true
 
 
-_FUSE_CODE = """
+_DUMP_CODE = """
 import sys; sys.path.insert(0, {root!r})
 import numpy as np, torch, synth, paper_1504_04395_b200 as srk
 srk.load_library()
-A = synth.conv_diff_3d({m}, (20.0, 10.0, 5.0), {dt})
-B = synth.random_rhs(A.n, {s}, 2, {cplx})
-M = srk.Matrix.from_csr(A, need_adjoint=True)
-sv = srk.Solver(M, {s}, {method!r}, tol=1e-8, maxit=2000, poll_every={poll}, use_graph={graph})
-sv.start(torch.from_numpy(B).cuda())
-sv.iterate({k})
-np.save({out!r}, np.stack([sv.x().cpu().numpy(), sv.residual().cpu().numpy()]))
-X, rep = srk.solve(M, torch.from_numpy(B).cuda(), {method!r}, tol=1e-8, maxit=2000)
-print(rep.outcome, rep.iterations)
+out = {{}}
+for method, cplx, s in {cases!r}:
+    A = synth.conv_diff_3d(28, (20.0, 10.0, 5.0), np.complex128 if cplx else np.float64)  # n = 21,952 > the single-CTA limit
+    B = synth.random_rhs(A.n, s, 2, cplx)
+    M = srk.Matrix.from_csr(A, need_adjoint=True)
+    for tag, poll, graph in (("step", 1, False), ("graph", 4, True)):
+        sv = srk.Solver(M, s, method, tol=1e-8, maxit=2000, poll_every=poll, use_graph=graph)
+        sv.start(torch.from_numpy(B).cuda())
+        sv.iterate(12)
+        out[f"{{method}}_{{int(cplx)}}_{{s}}_{{tag}}"] = np.stack([sv.x().cpu().numpy(), sv.residual().cpu().numpy()])
+        sv.close()
+    X, rep = srk.solve(M, torch.from_numpy(B).cuda(), method, tol=1e-8, maxit=2000)
+    out[f"{{method}}_{{int(cplx)}}_{{s}}_count"] = np.array([rep.iterations if rep.outcome == "converged" else -1])
+np.savez({path!r}, **out)
+print("DUMP_OK")
 """
 
+QMR_CASES = [(m, c, s) for m in ("egl_qmr", "gl_qmr") for c, s in ((False, 16), (True, 8), (False, 5), (False, 6), (True, 3))]
+FLAT_CASES = [(m, c, s) for m in ("gl_bicgstab", "egl_bicg", "gl_bicg")
+              for c, s in ((False, 16), (True, 12), (False, 5), (False, 6), (True, 3))]
 
-@pytest.mark.parametrize("method", ["egl_qmr", "gl_qmr"])
-@pytest.mark.parametrize("cplx,s", [(False, 16), (True, 8), (False, 5), (False, 6), (True, 3)])
-def test_qmr_fused_tail_equals_separate_updates(srk, tmp_path, method, cplx, s):
+
+def _dump(tmp, name, cases, env):
+    """X_12, R_12 (stepped one by one, and with the last 8 iterations replayed as a CUDA graph) and
+    the full-solve count of every case, in ONE subprocess per switch setting (the A/B switches
+    are read once per process)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    path = str(tmp / f"{name}.npz")
+    code = _DUMP_CODE.format(root=root, cases=cases, path=path)
+    r = subprocess.run([sys.executable, "-c", code], env={**os.environ, **env}, capture_output=True, text=True,
+                       timeout=1800)
+    assert r.returncode == 0 and "DUMP_OK" in r.stdout, r.stderr[-800:]
+    return dict(np.load(path))
+
+
+@pytest.fixture(scope="module")
+def qmr_dumps(tmp_path_factory):
+    tmp = tmp_path_factory.mktemp("qmr_fuse")
+    return {"vec": _dump(tmp, "vec", QMR_CASES, {}),
+            "fused": _dump(tmp, "fused", QMR_CASES, {"SRK_NO_QMR_VEC_FUSE": "1"}),
+            "plain": _dump(tmp, "plain", QMR_CASES, {"SRK_NO_QMR_FUSE": "1"})}
+
+
+@pytest.fixture(scope="module")
+def flat_dumps(tmp_path_factory):
+    tmp = tmp_path_factory.mktemp("flat")
+    return {"flat": _dump(tmp, "flat", FLAT_CASES, {}),
+            "plain": _dump(tmp, "plain", FLAT_CASES, {"SRK_NO_FLAT_UPDATE": "1"})}
+
+
+@pytest.mark.parametrize("method,cplx,s", QMR_CASES)
+def test_qmr_fused_tail_equals_separate_updates(qmr_dumps, method, cplx, s):
     """The fused tail (qmr_tail.cu: D, S, X, R of iteration k and P of iteration k+1 in one
     pass, next iteration's 1/rho and c1 from coefficient phase 4) keeps the per-element FMA
     order of the two separate updates: X_k and R_k after 12 iterations — stepped one by one
@@ -118,65 +158,40 @@ def test_qmr_fused_tail_equals_separate_updates(srk, tmp_path, method, cplx, s):
     own two summation orders differ by 4e-16 / 1e-14 in X / R at iteration 12 and its counts do not
     move under 1e-15 perturbations of B; with c = (50, 30, 10) at this size a near-breakdown at
     iteration 9 spreads the oracle itself by 4e-10 and its counts by 6%; the lock step against the
-    oracle is test_benchpath_lockstep). Widths 5 / 6 / 3
-    give ragged last CTAs, rows of 3 units (the division path) and the no-vector fallback."""
-    import os
-    import subprocess
-    import sys
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    m = 28  # n = 21,952 > the single-CTA limit
-    res = {}
-    novec = {"SRK_NO_QMR_VEC_FUSE": "1"}
-    for tag, env, poll in (("fused", novec, 1), ("graph", novec, 4), ("plain", {"SRK_NO_QMR_FUSE": "1"}, 1),
-                           ("vec", {}, 1), ("vecgraph", {}, 4)):
-        out = str(tmp_path / f"{tag}.npy")
-        code = _FUSE_CODE.format(root=root, m=m, dt="np.complex128" if cplx else "np.float64", s=s, cplx=cplx,
-                                 method=method, poll=poll, graph=tag.endswith("graph"), k=12, out=out)
-        r = subprocess.run([sys.executable, "-c", code], env={**os.environ, **env}, capture_output=True, text=True,
-                           timeout=900)
-        assert r.returncode == 0, r.stderr[-800:]
-        res[tag] = (np.load(out), r.stdout.split()[-2:])
-    ref = res["plain"][0]
+    oracle is test_benchpath_lockstep). Widths 5 / 6 / 3 give ragged last CTAs, rows of 3 units
+    (the division path) and the no-vector fallback."""
+    key = f"{method}_{int(cplx)}_{s}_"
+    ref = qmr_dumps["plain"][key + "step"]
     assert np.isfinite(ref).all()
-    assert np.array_equal(res["fused"][0], ref)
-    assert np.array_equal(res["graph"][0], ref)
-    assert res["fused"][1] == res["plain"][1] == res["graph"][1], (res["fused"][1], res["plain"][1])
-    assert np.array_equal(res["vec"][0], res["vecgraph"][0])
+    assert np.array_equal(qmr_dumps["fused"][key + "step"], ref)
+    assert np.array_equal(qmr_dumps["fused"][key + "graph"], ref)
+    assert np.array_equal(qmr_dumps["plain"][key + "graph"], ref)
+    it_p = int(qmr_dumps["plain"][key + "count"][0])
+    assert it_p > 0 and int(qmr_dumps["fused"][key + "count"][0]) == it_p
+    vec = qmr_dumps["vec"][key + "step"]
+    assert np.array_equal(vec, qmr_dumps["vec"][key + "graph"])
     for j in range(2):
-        assert rel(res["vec"][0][j], ref[j]) <= 1e-11, (j, rel(res["vec"][0][j], ref[j]))
-    assert res["vec"][1][0] == res["plain"][1][0] == "converged"
-    it_v, it_p = int(res["vec"][1][1]), int(res["plain"][1][1])
-    assert abs(it_v - it_p) <= max(2, 0.02 * it_p), (it_v, it_p)
+        assert rel(vec[j], ref[j]) <= 1e-11, (j, rel(vec[j], ref[j]))
+    it_v = int(qmr_dumps["vec"][key + "count"][0])
+    assert it_v > 0 and abs(it_v - it_p) <= max(2, 0.02 * it_p), (it_v, it_p)
 
 
-@pytest.mark.parametrize("method", ["gl_bicgstab", "egl_bicg"])
-@pytest.mark.parametrize("cplx,s", [(False, 16), (True, 12), (False, 5), (False, 6), (True, 3)])
-def test_flat_plans_equal_generic_updates(srk, tmp_path, method, cplx, s):
+@pytest.mark.parametrize("method,cplx,s", FLAT_CASES)
+def test_flat_plans_equal_generic_updates(flat_dumps, method, cplx, s):
     """eGl-BiCG's two block updates as lean flat kernels that carry r̂ and p̂ (egl_flat.cu) and
-    Gl-BiCGStab's three updates as flat plans (flat_upd.cu: the FMA order of the generic
-    upd_kernel per element, another summation order in ||S||^2, <R, R~>, ||R||^2) against the
+    Gl-BiCGStab's three / Gl-BiCG's two updates as flat plans (flat_upd.cu: the FMA order of the
+    generic upd_kernel per element, another summation order in the fused reductions) against the
     generic kernels (SRK_NO_FLAT_UPDATE=1, a subprocess: the switch is read once): X_k and R_k
     after 12 iterations within 1e-11 (well-conditioned operator, see the QMR test above),
-    stepped and graph-replayed runs bitwise equal, full solves with the same outcome and counts
-    within 2. Width 12 complex is config 4's; 5 / 3 give ragged last CTAs."""
-    import os
-    import subprocess
-    import sys
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    res = {}
-    for tag, env, poll in (("flat", {}, 1), ("flatgraph", {}, 4), ("plain", {"SRK_NO_FLAT_UPDATE": "1"}, 1)):
-        out = str(tmp_path / f"{tag}.npy")
-        code = _FUSE_CODE.format(root=root, m=28, dt="np.complex128" if cplx else "np.float64", s=s, cplx=cplx,
-                                 method=method, poll=poll, graph=tag.endswith("graph"), k=12, out=out)
-        r = subprocess.run([sys.executable, "-c", code], env={**os.environ, **env}, capture_output=True, text=True,
-                           timeout=900)
-        assert r.returncode == 0, r.stderr[-800:]
-        res[tag] = (np.load(out), r.stdout.split()[-2:])
-    ref = res["plain"][0]
+    stepped and graph-replayed runs bitwise equal, full solves converged with counts
+    within 2. Width 12 complex is config 4's; 5 / 6 / 3 give ragged last CTAs, rows of 3 units
+    and (eGl-BiCG at odd real width) the generic fallback."""
+    key = f"{method}_{int(cplx)}_{s}_"
+    ref = flat_dumps["plain"][key + "step"]
+    flat = flat_dumps["flat"][key + "step"]
     assert np.isfinite(ref).all()
-    assert np.array_equal(res["flat"][0], res["flatgraph"][0])
+    assert np.array_equal(flat, flat_dumps["flat"][key + "graph"])
     for j in range(2):
-        assert rel(res["flat"][0][j], ref[j]) <= 1e-11, (j, rel(res["flat"][0][j], ref[j]))
-    assert res["flat"][1][0] == res["plain"][1][0] == "converged"
-    it_f, it_p = int(res["flat"][1][1]), int(res["plain"][1][1])
-    assert abs(it_f - it_p) <= max(2, 0.02 * it_p), (it_f, it_p)
+        assert rel(flat[j], ref[j]) <= 1e-11, (j, rel(flat[j], ref[j]))
+    it_f, it_p = int(flat_dumps["flat"][key + "count"][0]), int(flat_dumps["plain"][key + "count"][0])
+    assert it_f > 0 and it_p > 0 and abs(it_f - it_p) <= max(2, 0.02 * it_p), (it_f, it_p)
