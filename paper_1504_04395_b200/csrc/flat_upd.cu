@@ -15,7 +15,8 @@
 // Plans: Gl-BiCGStab (SURVEY App. A.4 with scalar coefficients; the method of config 4 and
 // config 3's second method): S = R - alpha V with ||S||^2; (X, R) = (X + alpha P + omega S,
 // S - omega T) with <R, R~> and ||R||^2; P = R + beta P - beta omega V. Gl-BiCG (Alg. 2): the (X, R, R^)
-// update with <R, R^> and ||R||^2, and the (P, P^) update.
+// update with <R, R^> and ||R||^2, and the (P, P^) update. Gl-QMR: the (V~, W~) update with its three
+// reductions.
 #include <cuda_runtime.h>
 
 #include "block_kernels.cuh"
@@ -101,6 +102,24 @@ struct PlanBicgP {
   }
 };
 
+// Gl-QMR: V~ = P~ - (beta/rho) V~ ; W~ = A^H Q - (conj(beta)/xi) W~ ; ||V~||^2, <V~, W~>, ||W~||^2
+//                            in: P~, V~, A^H Q, W~ ; coef: beta/rho (negated), conj(beta)/xi (negated)
+struct PlanQmrVW {
+  static constexpr int NI = 4, NO = 2, NC = 2, NR = 3;
+  __host__ __device__ static constexpr bool cj(int) { return false; }
+  __host__ __device__ static constexpr bool neg(int) { return true; }
+  __host__ __device__ static constexpr int rmode(int r) { return r == 1 ? RED_TRACE : RED_NORM2; }
+  template <typename T>
+  __device__ __forceinline__ static void elem(const T (&x)[NI], const T (&c)[NC], T (&y)[NO], T (&ra)[NR]) {
+    const T z = Ar<T>::zero();
+    y[0] = Ar<T>::fma(x[1], c[0], Ar<T>::fma(x[0], one_of<T>(), z));
+    y[1] = Ar<T>::fma(x[3], c[1], Ar<T>::fma(x[2], one_of<T>(), z));
+    ra[0] = Ar<T>::cfma(y[0], y[0], ra[0]);
+    ra[1] = Ar<T>::cfma(y[1], y[0], ra[1]);
+    ra[2] = Ar<T>::cfma(y[1], y[1], ra[2]);
+  }
+};
+
 template <typename T, typename P>
 __global__ void __launch_bounds__(256, (sizeof(T) == 16 && P::NI > 3) ? (P::NI > 5 ? 2 : 3) : (P::NI > 5 ? 3 : 4)) flat_kernel(FlatArgs a) {
   if (a.done && *a.done) return;
@@ -157,7 +176,11 @@ __global__ void __launch_bounds__(256, (sizeof(T) == 16 && P::NI > 3) ? (P::NI >
     red_flush<T, W, P::rmode(1), false>(acc[1], a.partials, a.pstride, poff, W, rsm);
     poff += red_len(P::rmode(1), W, Ar<T>::cplx);
   }
-  static_assert(P::NR <= 2, "two reductions per plan");
+  if constexpr (P::NR > 2) {
+    red_flush<T, W, P::rmode(2), false>(acc[2], a.partials, a.pstride, poff, W, rsm);
+    poff += red_len(P::rmode(2), W, Ar<T>::cplx);
+  }
+  static_assert(P::NR <= 3, "three reductions per plan");
 }
 
 template <typename P>
@@ -177,7 +200,7 @@ template <typename P>
 static FlatPlanInfo info_of() {
   FlatPlanInfo f{};
   f.ni = P::NI; f.no = P::NO; f.nc = P::NC; f.nr = P::NR;
-  for (int r = 0; r < P::NR && r < 2; ++r) f.rmode[r] = P::rmode(r);
+  for (int r = 0; r < P::NR && r < 3; ++r) f.rmode[r] = P::rmode(r);
   return f;
 }
 
@@ -188,6 +211,7 @@ FlatPlanInfo flat_plan_info(int plan) {
     case FP_STAB_P: return info_of<PlanStabP>();
     case FP_BICG_XR: return info_of<PlanBicgXR>();
     case FP_BICG_P: return info_of<PlanBicgP>();
+    case FP_QMR_VW: return info_of<PlanQmrVW>();
     default: return FlatPlanInfo{};
   }
 }
@@ -200,6 +224,7 @@ int launch_flat(int plan, bool cplx, const FlatArgs& a, int grid, cudaStream_t s
     case FP_STAB_P: return launch_plan<PlanStabP>(cplx, a, grid, st);
     case FP_BICG_XR: return launch_plan<PlanBicgXR>(cplx, a, grid, st);
     case FP_BICG_P: return launch_plan<PlanBicgP>(cplx, a, grid, st);
+    case FP_QMR_VW: return launch_plan<PlanQmrVW>(cplx, a, grid, st);
     default: return grid < 0 ? 0 : (int)cudaErrorInvalidValue;
   }
 }

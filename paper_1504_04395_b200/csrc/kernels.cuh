@@ -173,10 +173,10 @@ struct QmrVtArgs {
 };
 
 // Flat scalar-coefficient updates as compile-time plans (flat_upd.cu)
-enum FlatPlan : int { FP_STAB_S = 0, FP_STAB_XR = 1, FP_STAB_P = 2, FP_BICG_XR = 3, FP_BICG_P = 4 };
+enum FlatPlan : int { FP_STAB_S = 0, FP_STAB_XR = 1, FP_STAB_P = 2, FP_BICG_XR = 3, FP_BICG_P = 4, FP_QMR_VW = 5 };
 struct FlatPlanInfo {
   int ni, no, nc, nr;
-  int rmode[2];
+  int rmode[3];
 };
 struct FlatArgs {
   const void* in[6];

@@ -916,6 +916,10 @@ struct QMR : Solver {  // mode 0 Li, 1 Gl, 2 eGl
     static const bool off_env = getenv("SRK_NO_QMR_FUSE") != nullptr;  // A/B switch
     return mode != 0 && !off_env && e.qmr_tail_ok(s);
   }
+  bool flat_vw() const {
+    static const bool off_env = getenv("SRK_NO_FLAT_UPDATE") != nullptr;  // A/B switch
+    return !off_env && e.qmr_tail_ok(s);
+  }
   bool fused_vec() const {
     static const bool off_env = getenv("SRK_NO_QMR_VEC_FUSE") != nullptr;  // A/B switch
     return mode == 2 && !off_env && e.qmr_vec_ok(s);
@@ -980,6 +984,9 @@ struct QMR : Solver {  // mode 0 Li, 1 Gl, 2 eGl
       // one kernel: Ṽ = P~ - (beta/rho) Ṽ with ||Ṽ||^2, <Ṽ, W̃> and ||W̃||^2 for the new
       // W̃ = A^H Q - (conj(beta)/xi) W̃, formed per row in registers (stored by the tail below)
       e.qmr_vt(s, Pt, Vt, AHQ, Wt, off[SL_BR], off[SL_BX], off[SL_RHON2], off[SL_K1], off[SL_XI2]);
+    } else if (mode == 1 && flat_vw()) {
+      // Gl: both Lanczos blocks and their three reductions as one flat plan (flat_upd.cu)
+      e.flat(FP_QMR_VW, s, {Pt, Vt, AHQ, Wt}, {Vt, Wt}, {off[SL_BR], off[SL_BX]}, {off[SL_RHON2], off[SL_K1], off[SL_XI2]});
     } else {
       // W̃ = A^H Q - conj(beta) W = A^H Q - (conj(beta)/xi) W̃   (first: Ṽ's kernel reads the new W̃)
       e.upd(ws_(), {AHQ, Wt}, {OutSpec{Wt, {{0, C1()}, {1, K(SL_BX, 1)}}}}, {RQ{nrm(), O0, -1, nullptr, off[SL_XI2]}});

@@ -109,7 +109,7 @@ print("DUMP_OK")
 """
 
 QMR_CASES = [(m, c, s) for m in ("egl_qmr", "gl_qmr") for c, s in ((False, 16), (True, 8), (False, 5), (False, 6), (True, 3))]
-FLAT_CASES = [(m, c, s) for m in ("gl_bicgstab", "egl_bicg", "gl_bicg")
+FLAT_CASES = [(m, c, s) for m in ("gl_bicgstab", "egl_bicg", "gl_bicg", "gl_qmr")
               for c, s in ((False, 16), (True, 12), (False, 5), (False, 6), (True, 3))]
 
 
@@ -179,7 +179,7 @@ def test_qmr_fused_tail_equals_separate_updates(qmr_dumps, method, cplx, s):
 @pytest.mark.parametrize("method,cplx,s", FLAT_CASES)
 def test_flat_plans_equal_generic_updates(flat_dumps, method, cplx, s):
     """eGl-BiCG's two block updates as lean flat kernels that carry r̂ and p̂ (egl_flat.cu) and
-    Gl-BiCGStab's three / Gl-BiCG's two updates as flat plans (flat_upd.cu: the FMA order of the
+    Gl-BiCGStab's three updates, Gl-BiCG's (X, R, R̂) update and Gl-QMR's (Ṽ, W̃) update as flat plans (flat_upd.cu: the FMA order of the
     generic upd_kernel per element, another summation order in the fused reductions) against the
     generic kernels (SRK_NO_FLAT_UPDATE=1, a subprocess: the switch is read once): X_k and R_k
     after 12 iterations within 1e-11 (well-conditioned operator, see the QMR test above),
