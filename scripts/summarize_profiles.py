@@ -6,7 +6,7 @@
 Captures: prof_spmm (config 3 SpMM), prof_upd (config 3's dominant 6-in / 4-out update),
 prof_bsr (config 4 BSR-12 product), prof_gram (s = 64 CTA-tiled DMMA Gram), prof_updmma
 (config 2 tensor-core block update), prof_gramwarp (config 2 per-warp Gram of a block with
-itself), prof_plane (config 3's plane-marching SpMM), prof_tail / prof_vt (config 3's fused eGl-QMR tail and V~ kernels, qmr_tail.cu), prof_small (config 1's single-CTA eGl-BiCG iteration kernel; a launch covers the
+itself), prof_plane (config 3's plane-marching SpMM), prof_tail / prof_vt (config 3's fused eGl-QMR tail and V~ kernels, qmr_tail.cu), prof_flat (config 4's Gl-BiCGStab (X, R) flat plan, flat_upd.cu), prof_planerow (config 3's Gl-BiCGStab product with a row operand), prof_small (config 1's single-CTA eGl-BiCG iteration kernel; a launch covers the
 iterations between two polls). Reads gpurun_out/launches.csv (ncu --metrics gpu__time_duration.sum launch list of
 `python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu`), gpurun_out/prof_*.ncu-rep
 (`ncu --set full`) and gpurun_out/bench.log, and writes
@@ -53,7 +53,7 @@ def main(tag, pre=""):
     os.makedirs(PROF, exist_ok=True)
     spath = os.path.join(PROF, f"{tag}_ncu_summary.json")
     summary = json.load(open(spath)) if os.path.exists(spath) else {}  # later captures of a round update the file
-    for name in ("spmm", "upd", "bsr", "gram", "updmma", "gramwarp", "small", "band", "plane", "tail", "vt"):
+    for name in ("spmm", "upd", "bsr", "gram", "updmma", "gramwarp", "small", "band", "plane", "tail", "vt", "flat", "planerow"):
         rep = os.path.join(OUT, f"{pre}prof_{name}.ncu-rep")
         if not os.path.exists(rep):
             continue
